@@ -1,0 +1,143 @@
+/*
+ * acco.h — C-ABI of the B200-native ACCO library (libacco: _acco_b200.so).
+ *
+ * This is the drop-in boundary for the ACCO round of the reference simulator
+ * `accosim` (/root/reference/proj). Every entry point below names the
+ * reference interface it replaces (file:line). Conventions:
+ *   - plain pointers and sizes only; no C++ / torch types;
+ *   - device pointers are caller-owned unless a *_create/destroy pair owns them;
+ *   - `stream` is a cudaStream_t passed as void*; ops are asynchronous on it;
+ *   - every function returns a status code (below) and never throws; the
+ *     message of the last failure on the calling thread is acco_last_error().
+ *
+ * Status codes mirror the accosim CLI exit codes
+ * (/root/reference/proj/tools/accosim_main.cpp:30-33) plus two B200 codes.
+ */
+#ifndef ACCO_H_
+#define ACCO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACCO_ABI_VERSION 1
+
+#define ACCO_OK 0
+#define ACCO_VERIFY_FAIL 1  /* accosim exit 1 */
+#define ACCO_INVALID 2      /* std::invalid_argument, accosim exit 2 */
+#define ACCO_DIVERGED 3     /* RunTrace.diverged, accosim exit 3 */
+#define ACCO_CUDA_ERROR 4   /* CUDA / NCCL failure (B200 only) */
+#define ACCO_LOGIC_ERROR 5  /* std::logic_error (protocol invariants) */
+
+#define ACCO_DTYPE_F32 0
+#define ACCO_DTYPE_BF16 1
+
+const char* acco_last_error(void);
+int acco_version(void);
+
+/* ------------------------------------------------------------------ shards
+ * shard_partition (proj/include/accosim/shard.hpp:24-38): contiguous
+ * near-equal split, the first (dim mod n) ranges get one extra element. */
+int acco_shard_partition(uint64_t dim, int n, uint64_t* lo_out, uint64_t* hi_out);
+
+/* ------------------------------------------------------------------- rng
+ * rng::derive / Stream (proj/include/accosim/rng.hpp:13-56) and the
+ * micro-batch index draw of stochastic_grad (proj/src/problems.cpp:442-444).
+ * Exposed so callers can pin token indexing bit-exactly. */
+uint64_t acco_rng_derive(uint64_t master, uint64_t a, uint64_t b, uint64_t c, uint64_t d);
+int acco_sample_indices(uint64_t stream_seed, int batch, int n_samples, int32_t* out);
+
+/* -------------------------------------------------------------- optimizer
+ * OptimizerConfig (proj/include/accosim/optim.hpp:21-32). kind: 0 sgd,
+ * 1 adam, 2 adamw. scheduler: 0 constant, 1 cosine. */
+typedef struct acco_opt_cfg {
+    int kind;
+    double learning_rate;
+    double adam_beta1;
+    double adam_beta2;
+    double adam_eps;
+    double weight_decay;
+    int scheduler;
+    int n_warmup_steps;
+    long long total_steps;
+    double cosine_min_factor;
+} acco_opt_cfg;
+
+/* scheduled_lr (proj/src/optim.cpp:37-48). */
+double acco_scheduled_lr(const acco_opt_cfg* cfg, long long t);
+
+/* OptimizerState (proj/include/accosim/optim.hpp:35-43) for one shard
+ * [lo, hi), device resident: fp32 master params, first/second moments
+ * (v unused for sgd, m unused for sgd). `step` is host state. */
+typedef struct acco_shard_state {
+    long long step;
+    float* theta;
+    float* m;
+    float* v;
+    uint64_t lo;
+    uint64_t hi;
+} acco_shard_state;
+
+/* K6 — ACCO estimate branch (proj/src/protocols.cpp:647-658): the optimizer
+ * step of opt_step (proj/src/optim.cpp:50-92) on a *transient* copy of the
+ * shard state: theta_est = Opt(theta, gsum / total); m, v and step are NOT
+ * written. `total` is read from device memory (the counts all-reduce output).
+ * Output dtype is ACCO_DTYPE_F32 or ACCO_DTYPE_BF16 (the all-gather payload).
+ * `nonfinite_flag` (device int, nullable) is set to 1 if any input is
+ * non-finite — opt_step's std::invalid_argument (optim.cpp:56-57). */
+int acco_opt_estimate(const acco_opt_cfg* cfg, const acco_shard_state* st, const float* gsum,
+                      const int64_t* total_dev, void* theta_out, int out_dtype,
+                      int* nonfinite_flag, void* stream);
+
+/* K7 — ACCO commit branch (proj/src/protocols.cpp:659-707): persistent
+ * step on the shard: mean = (gsum + g_retained) / (total + retained_total),
+ * theta, m, v updated in place, step += 1 (host), theta also written to
+ * theta_out (all-gather payload, may be NULL). g_retained / retained_total_dev
+ * may be NULL (DDP / ZeRO-1: plain sharded_opt_step, optim.cpp:94-119). */
+int acco_opt_commit(const acco_opt_cfg* cfg, acco_shard_state* st, const float* gsum,
+                    const float* g_retained, const int64_t* total_dev,
+                    const int64_t* retained_total_dev, void* theta_out, int out_dtype,
+                    int* nonfinite_flag, void* stream);
+
+/* -------------------------------------------------------------- collectives
+ * Fabric (proj/include/accosim/collectives.hpp:31-49) over NCCL on
+ * NVLink 5 / NVSwitch: one rank per process (one GPU). */
+typedef struct acco_comm acco_comm;
+int acco_comm_unique_id(unsigned char id_out[128]);
+int acco_comm_init_rank(int nranks, int rank, const unsigned char id[128], int device,
+                        acco_comm** out);
+int acco_comm_destroy(acco_comm* comm);
+int acco_comm_size(const acco_comm* comm);
+int acco_comm_rank(const acco_comm* comm);
+/* Fabric::all_reduce (collectives.cpp:36-46), fp32 sum. */
+int acco_all_reduce_f32(acco_comm* comm, const float* send, float* recv, uint64_t count,
+                        void* stream);
+/* Fabric::all_reduce_counts (collectives.cpp:48-53), int64 sum. */
+int acco_all_reduce_i64(acco_comm* comm, const int64_t* send, int64_t* recv, uint64_t count,
+                        void* stream);
+/* Fabric::reduce_scatter (collectives.cpp:55-75): send holds nranks*count
+ * elements (owner-padded chunks), recv gets this rank's summed chunk. */
+int acco_reduce_scatter_f32(acco_comm* comm, const float* send, float* recv, uint64_t count,
+                            void* stream);
+/* Fabric::all_gather (collectives.cpp:77-91): recv holds nranks*count. */
+int acco_all_gather(acco_comm* comm, const void* send, void* recv, uint64_t count, int dtype,
+                    void* stream);
+
+/* ----------------------------------------------------------- raw GEMM (K1)
+ * C[m,n] (op)= sum_k A(m,k) B(n,k); operands K-major (ptr[row*ld+k]) or
+ * MN-major (ptr[k*ld+row]). dtype BF16 -> tcgen05/TMA kernel, F32 -> SIMT
+ * parity kernel. epi_mode: 0 store(+bias+residual), 1 gelu (aux=pre-act),
+ * 2 dgelu (C=acc*gelu'(aux)), 3 fp32 accumulate (C = beta*C + acc). */
+int acco_gemm(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t ldb,
+              int b_mn_major, int m, int n, int k, int dtype, int epi_mode, void* c, int64_t ldc,
+              const void* bias, const void* residual, int64_t ldr, void* aux, int64_t ld_aux,
+              int beta, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ACCO_H_ */

@@ -1,0 +1,56 @@
+// Shared device/host helpers for the ACCO B200 library (sm_100a only).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "paper_2406_02613_b200 targets sm_100a only"
+#endif
+
+namespace acco {
+
+// Thrown inside the library; the C-ABI layer converts it to a status code
+// (see include/acco.h) and stores the message for acco_last_error().
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+enum Status : int {
+    kOk = 0,
+    kVerifyFail = 1,     // accosim exit code 1
+    kInvalidArg = 2,     // accosim exit code 2 (std::invalid_argument)
+    kDiverged = 3,       // accosim exit code 3
+    kCudaError = 4,      // B200-only: CUDA / NCCL failure
+    kLogicError = 5,     // std::logic_error in the reference (invariants)
+};
+
+#define ACCO_CUDA(expr)                                                                 \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            throw ::acco::Error(::acco::kCudaError, std::string(#expr) + ": " +         \
+                                                        cudaGetErrorString(_e) + " @" + \
+                                                        __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+#define ACCO_CHECK_LAUNCH() ACCO_CUDA(cudaGetLastError())
+
+#define ACCO_REQUIRE(cond, msg)                                                  \
+    do {                                                                         \
+        if (!(cond)) throw ::acco::Error(::acco::kInvalidArg, std::string(msg)); \
+    } while (0)
+
+inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// Number of SMs on the current device (148 on B200); cached per process.
+int num_sms();
+
+}  // namespace acco

@@ -1,0 +1,49 @@
+// GEMM entry points used by the LM plugin (K1/K3 in SURVEY.md §2.3).
+//
+//   C[M,N] (op)= sum_k A(m,k) * B(n,k)
+//
+// Operand addressing (row-major storage, `ld` in elements):
+//   K-major : A(m,k) = A.ptr[m*ld + k]      (the usual X[M,K] / W[N,K] layout)
+//   MN-major: A(m,k) = A.ptr[k*ld + m]      (a transposed view, e.g. dY^T in wgrad)
+//
+// The bf16 path is the tcgen05/TMA/TMEM kernel (gemm_tcgen05.cu); the fp32
+// path is a SIMT kernel used only for the fp32-accurate parity mode
+// (SURVEY.md §7 "fp64 oracle vs fp32/bf16 GPU").
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace acco {
+
+struct GemmOperand {
+    const void* ptr = nullptr;
+    int64_t ld = 0;
+    bool mn_major = false;
+};
+
+enum EpiMode : int {
+    kEpiStore = 0,   // C = acc + bias + residual            (activation dtype)
+    kEpiGelu = 1,    // aux = acc + bias; C = gelu(aux)       (activation dtype)
+    kEpiDGelu = 2,   // C = (acc) * gelu'(aux)                (activation dtype)
+    kEpiAccF32 = 3,  // C_f32 = beta*C_f32 + acc              (fp32 gradient accumulator)
+};
+
+struct Epilogue {
+    int mode = kEpiStore;
+    void* C = nullptr;
+    int64_t ldc = 0;
+    const void* bias = nullptr;      // [N], activation dtype
+    const void* residual = nullptr;  // [M, ldr], activation dtype (may alias C)
+    int64_t ldr = 0;
+    void* aux = nullptr;             // [M, ld_aux] pre-activation (gelu modes)
+    int64_t ld_aux = 0;
+    int beta = 0;                    // kEpiAccF32: accumulate into C when 1
+};
+
+void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
+               const Epilogue& ep, cudaStream_t stream);
+void gemm_f32(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
+              const Epilogue& ep, cudaStream_t stream);
+
+}  // namespace acco

@@ -1,0 +1,274 @@
+// Fused sharded optimizer kernels — K6 (ACCO estimate) and K7 (ACCO commit)
+// of SURVEY.md §2.3, restating opt_step (/root/reference/proj/src/optim.cpp:50-92)
+// as one HBM-streaming pass over the shard:
+//
+//   estimate: reads g_sum, theta, m, v; writes theta_est (bf16/fp32 all-gather
+//             payload). Moments are read but never written: the reference runs
+//             the estimate on a *transient copy* of the shard state
+//             (protocols.cpp:654), so it is a pure function here.      18 B/elem (AdamW, bf16 out)
+//   commit  : reads g_sum, g_retained, theta, m, v; writes theta, m, v and the
+//             all-gather payload.                                       34 B/elem
+//
+// 1/total, 1/(total+retained), the learning-rate schedule and both bias
+// corrections are folded in; totals are read from device memory (the output of
+// the counts all-reduce), so the comm stream never synchronises with the host.
+#include "acco.h"
+#include "capi_util.h"
+#include "common.cuh"
+#include "optim.h"
+
+#include <cmath>
+
+namespace acco {
+
+double scheduled_lr(const OptConfig& cfg, long long t) {
+    // proj/src/optim.cpp:37-48
+    const double peak = cfg.learning_rate;
+    const long long warmup = cfg.n_warmup_steps;
+    if (t < warmup) return peak * static_cast<double>(t + 1) / static_cast<double>(warmup);
+    if (cfg.scheduler == 0) return peak;
+    const double floor = peak * cfg.cosine_min_factor;
+    const long long span = cfg.total_steps - 1 - warmup;
+    if (span <= 0) return peak;
+    double x = static_cast<double>(t - warmup) / static_cast<double>(span);
+    if (x > 1.0) x = 1.0;
+    return floor + (peak - floor) * 0.5 * (1.0 + std::cos(3.14159265358979323846 * x));
+}
+
+void validate(const OptConfig& cfg) {
+    ACCO_REQUIRE(cfg.kind >= 0 && cfg.kind <= 2, "optimizer: unknown kind");
+    ACCO_REQUIRE(cfg.learning_rate > 0.0, "optimizer: learning_rate > 0");
+    ACCO_REQUIRE(cfg.adam_beta1 >= 0.0 && cfg.adam_beta1 < 1.0 && cfg.adam_beta2 >= 0.0 &&
+                     cfg.adam_beta2 < 1.0,
+                 "optimizer: adam betas must lie in [0, 1)");
+    ACCO_REQUIRE(cfg.weight_decay >= 0.0, "optimizer: weight_decay >= 0");
+}
+
+namespace {
+
+struct KArgs {
+    const float* g;
+    const float* gret;
+    const int64_t* total;
+    const int64_t* rtotal;
+    float* theta;  // read; written by commit
+    float* m;
+    float* v;
+    void* out;     // may be null for commit
+    int64_t n;
+    float lr, b1, b2, omb1, omb2, c1, c2, eps, wd;
+    int* flag;
+};
+
+template <class OutT>
+__device__ __forceinline__ void store_out(void* out, int64_t i, float x) {
+    static_cast<OutT*>(out)[i] = from_f_opt<OutT>(x);
+}
+
+// One element of opt_step; returns the new theta and updates m/v in registers.
+template <int KIND>
+__device__ __forceinline__ float step_elem(const KArgs& a, float g, float th, float& m, float& v) {
+    if (KIND == 0) {  // sgd: theta -= lr * (g + wd*theta)
+        return th - a.lr * (g + a.wd * th);
+    }
+    if (KIND == 1) g += a.wd * th;  // adam: coupled decay
+    m = a.b1 * m + a.omb1 * g;
+    v = a.b2 * v + a.omb2 * g * g;
+    const float mh = m / a.c1;
+    const float vh = v / a.c2;
+    float u = mh / (sqrtf(vh) + a.eps);
+    if (KIND == 2) u += a.wd * th;  // adamw: decoupled decay
+    return th - a.lr * u;
+}
+
+template <int KIND, bool COMMIT, bool HAS_RET, class OutT, bool VEC>
+__global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
+    int64_t tot = *a.total;
+    if (HAS_RET && a.rtotal) tot += *a.rtotal;
+    const float inv = static_cast<float>(1.0 / static_cast<double>(tot));
+    bool bad = false;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (VEC) {
+        const int64_t n4 = a.n / 4;
+        for (int64_t q = tid; q < n4; q += stride) {
+            float4 g = __ldcs(reinterpret_cast<const float4*>(a.g) + q);
+            if (HAS_RET) {
+                float4 r = __ldcs(reinterpret_cast<const float4*>(a.gret) + q);
+                g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
+            }
+            g.x *= inv; g.y *= inv; g.z *= inv; g.w *= inv;
+            float4 th = reinterpret_cast<const float4*>(a.theta)[q];
+            float4 m = make_float4(0.f, 0.f, 0.f, 0.f), v = m;
+            if (KIND != 0) {
+                m = reinterpret_cast<const float4*>(a.m)[q];
+                v = reinterpret_cast<const float4*>(a.v)[q];
+            }
+            bad |= !(isfinite(g.x) && isfinite(g.y) && isfinite(g.z) && isfinite(g.w) &&
+                     isfinite(th.x) && isfinite(th.y) && isfinite(th.z) && isfinite(th.w));
+            float4 nt;
+            nt.x = step_elem<KIND>(a, g.x, th.x, m.x, v.x);
+            nt.y = step_elem<KIND>(a, g.y, th.y, m.y, v.y);
+            nt.z = step_elem<KIND>(a, g.z, th.z, m.z, v.z);
+            nt.w = step_elem<KIND>(a, g.w, th.w, m.w, v.w);
+            if (COMMIT) {
+                reinterpret_cast<float4*>(a.theta)[q] = nt;
+                if (KIND != 0) {
+                    reinterpret_cast<float4*>(a.m)[q] = m;
+                    reinterpret_cast<float4*>(a.v)[q] = v;
+                }
+            }
+            if (a.out) store4<OutT>(a.out, q, nt);
+        }
+        // tail (n % 4) handled by the scalar loop below
+        for (int64_t i = n4 * 4 + tid; i < a.n; i += stride) {
+            float g = a.g[i];
+            if (HAS_RET) g += a.gret[i];
+            g *= inv;
+            float th = a.theta[i];
+            float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
+            bad |= !(isfinite(g) && isfinite(th));
+            float nt = step_elem<KIND>(a, g, th, m, v);
+            if (COMMIT) {
+                a.theta[i] = nt;
+                if (KIND != 0) { a.m[i] = m; a.v[i] = v; }
+            }
+            if (a.out) store_out<OutT>(a.out, i, nt);
+        }
+    } else {
+        for (int64_t i = tid; i < a.n; i += stride) {
+            float g = a.g[i];
+            if (HAS_RET) g += a.gret[i];
+            g *= inv;
+            float th = a.theta[i];
+            float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
+            bad |= !(isfinite(g) && isfinite(th));
+            float nt = step_elem<KIND>(a, g, th, m, v);
+            if (COMMIT) {
+                a.theta[i] = nt;
+                if (KIND != 0) { a.m[i] = m; a.v[i] = v; }
+            }
+            if (a.out) store_out<OutT>(a.out, i, nt);
+        }
+    }
+    if (bad && a.flag) atomicOr(a.flag, 1);
+}
+
+template <int KIND, bool COMMIT, bool HAS_RET, class OutT>
+void launch_vec(const KArgs& a, bool vec, cudaStream_t s) {
+    const int threads = 256;
+    // persistent-style grid: a few waves of 148 SMs x 8 resident blocks
+    const int64_t work = vec ? (a.n + 3) / 4 : a.n;
+    int blocks = static_cast<int>(std::min<int64_t>((work + threads - 1) / threads,
+                                                    static_cast<int64_t>(num_sms()) * 8));
+    if (blocks < 1) blocks = 1;
+    if (vec)
+        opt_kernel<KIND, COMMIT, HAS_RET, OutT, true><<<blocks, threads, 0, s>>>(a);
+    else
+        opt_kernel<KIND, COMMIT, HAS_RET, OutT, false><<<blocks, threads, 0, s>>>(a);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <bool COMMIT, bool HAS_RET, class OutT>
+void launch_kind(int kind, const KArgs& a, bool vec, cudaStream_t s) {
+    if (kind == 0) launch_vec<0, COMMIT, HAS_RET, OutT>(a, vec, s);
+    else if (kind == 1) launch_vec<1, COMMIT, HAS_RET, OutT>(a, vec, s);
+    else launch_vec<2, COMMIT, HAS_RET, OutT>(a, vec, s);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* gsum,
+               const float* gret, const int64_t* total_dev, const int64_t* rtotal_dev, float* theta,
+               float* m, float* v, int64_t n, void* out, int out_dtype, int* flag,
+               cudaStream_t stream) {
+    if (n == 0) return;  // empty trailing shard: no-op (test_optim.cpp:168-181)
+    validate(cfg);
+    ACCO_REQUIRE(gsum && theta && total_dev, "optimizer: null shard pointer");
+    ACCO_REQUIRE(cfg.kind == 0 || (m && v), "optimizer: adam/adamw need m and v");
+    KArgs a{};
+    a.g = gsum;
+    a.gret = gret;
+    a.total = total_dev;
+    a.rtotal = rtotal_dev;
+    a.theta = theta;
+    a.m = m;
+    a.v = v;
+    a.out = out;
+    a.n = n;
+    a.flag = flag;
+    // lr(t) and bias correction with step t+1 (optim.cpp:59-74); the estimate
+    // and the commit of round t both use the same `step`.
+    const double lr = scheduled_lr(cfg, step);
+    const double st = static_cast<double>(step + 1);
+    a.lr = static_cast<float>(lr);
+    a.b1 = static_cast<float>(cfg.adam_beta1);
+    a.b2 = static_cast<float>(cfg.adam_beta2);
+    a.omb1 = static_cast<float>(1.0 - cfg.adam_beta1);
+    a.omb2 = static_cast<float>(1.0 - cfg.adam_beta2);
+    a.c1 = static_cast<float>(1.0 - std::pow(cfg.adam_beta1, st));
+    a.c2 = static_cast<float>(1.0 - std::pow(cfg.adam_beta2, st));
+    a.eps = static_cast<float>(cfg.adam_eps);
+    a.wd = static_cast<float>(cfg.weight_decay);
+    const bool vec = aligned16(gsum) && (!gret || aligned16(gret)) && aligned16(theta) &&
+                     (cfg.kind == 0 || (aligned16(m) && aligned16(v))) &&
+                     (!out || (reinterpret_cast<uintptr_t>(out) & (out_dtype == ACCO_DTYPE_BF16 ? 7 : 15)) == 0);
+    const bool has_ret = gret != nullptr;
+    ACCO_REQUIRE(out_dtype == ACCO_DTYPE_F32 || out_dtype == ACCO_DTYPE_BF16, "optimizer: bad out dtype");
+#define ACCO_OPT_DISPATCH(C)                                                                    \
+    if (out_dtype == ACCO_DTYPE_BF16) {                                                         \
+        if (has_ret) launch_kind<C, true, __nv_bfloat16>(cfg.kind, a, vec, stream);             \
+        else launch_kind<C, false, __nv_bfloat16>(cfg.kind, a, vec, stream);                    \
+    } else {                                                                                    \
+        if (has_ret) launch_kind<C, true, float>(cfg.kind, a, vec, stream);                     \
+        else launch_kind<C, false, float>(cfg.kind, a, vec, stream);                            \
+    }
+    if (commit) {
+        ACCO_OPT_DISPATCH(true)
+    } else {
+        ACCO_OPT_DISPATCH(false)
+    }
+#undef ACCO_OPT_DISPATCH
+}
+
+}  // namespace acco
+
+using namespace acco;
+
+extern "C" {
+
+double acco_scheduled_lr(const acco_opt_cfg* cfg, long long t) {
+    return scheduled_lr(from_c(*cfg), t);
+}
+
+int acco_opt_estimate(const acco_opt_cfg* cfg, const acco_shard_state* st, const float* gsum,
+                      const int64_t* total_dev, void* theta_out, int out_dtype, int* nonfinite_flag,
+                      void* stream) {
+    return guarded([&] {
+        ACCO_REQUIRE(cfg && st, "acco_opt_estimate: null argument");
+        ACCO_REQUIRE(st->hi >= st->lo, "acco_opt_estimate: bad shard range");
+        ACCO_REQUIRE(theta_out, "acco_opt_estimate: theta_out required");
+        opt_apply(from_c(*cfg), st->step, false, gsum, nullptr, total_dev, nullptr, st->theta, st->m,
+                  st->v, static_cast<int64_t>(st->hi - st->lo), theta_out, out_dtype, nonfinite_flag,
+                  static_cast<cudaStream_t>(stream));
+    });
+}
+
+int acco_opt_commit(const acco_opt_cfg* cfg, acco_shard_state* st, const float* gsum,
+                    const float* g_retained, const int64_t* total_dev,
+                    const int64_t* retained_total_dev, void* theta_out, int out_dtype,
+                    int* nonfinite_flag, void* stream) {
+    return guarded([&] {
+        ACCO_REQUIRE(cfg && st, "acco_opt_commit: null argument");
+        ACCO_REQUIRE(st->hi >= st->lo, "acco_opt_commit: bad shard range");
+        opt_apply(from_c(*cfg), st->step, true, gsum, g_retained, total_dev,
+                  g_retained ? retained_total_dev : nullptr, st->theta, st->m, st->v,
+                  static_cast<int64_t>(st->hi - st->lo), theta_out, out_dtype, nonfinite_flag,
+                  static_cast<cudaStream_t>(stream));
+        st->step += 1;
+    });
+}
+
+}  // extern "C"

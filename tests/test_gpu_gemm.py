@@ -1,0 +1,110 @@
+"""tcgen05 bf16 GEMM and SIMT fp32 GEMM vs a torch fp32 reference of the same op.
+
+Tolerances: bf16 inputs are exact in fp32, so the only differences are the
+fp32 accumulation order (<= 1e-5 rel) plus bf16 output rounding (2^-8 rel).
+"""
+import itertools
+
+import pytest
+import torch
+
+from paper_2406_02613_b200 import _lib
+from paper_2406_02613_b200.ops import gemm
+
+pytestmark = pytest.mark.gpu
+
+
+def _operand(rows, k, mn_major, dtype, dev, gen):
+    x = torch.randn(rows, k, generator=gen, device="cpu").to(dtype).to(dev)
+    if mn_major:
+        return x, x.t().contiguous()  # logical [rows,k]; stored [k,rows]
+    return x, x
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / b.float().norm().clamp_min(1e-30)).item()
+
+
+SHAPES = [(128, 128, 64), (256, 512, 128), (304, 200, 96), (512, 768, 768), (1024, 2304, 768),
+          (136, 264, 200), (2048, 4096, 1024)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", list(itertools.product([False, True], repeat=2)))
+@pytest.mark.parametrize("shape", SHAPES)
+def test_bf16_store(cuda, shape, a_mn, b_mn):
+    m, n, k = shape
+    g = torch.Generator().manual_seed(m * 7 + n + k)
+    a, a_st = _operand(m, k, a_mn, torch.bfloat16, cuda, g)
+    b, b_st = _operand(n, k, b_mn, torch.bfloat16, cuda, g)
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, c)
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float().t()
+    assert _rel(c, ref) < 6e-3
+
+
+@pytest.mark.parametrize("a_mn,b_mn", list(itertools.product([False, True], repeat=2)))
+def test_bf16_acc_f32(cuda, a_mn, b_mn):
+    m, n, k = 384, 640, 1024
+    g = torch.Generator().manual_seed(1)
+    a, a_st = _operand(m, k, a_mn, torch.bfloat16, cuda, g)
+    b, b_st = _operand(n, k, b_mn, torch.bfloat16, cuda, g)
+    c0 = torch.randn(m, n, generator=g).to(cuda)
+    c = c0.clone()
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, c, mode=3, beta=1)
+    torch.cuda.synchronize()
+    ref = c0 + a.float() @ b.float().t()
+    assert _rel(c, ref) < 2e-6
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, c, mode=3, beta=0)
+    torch.cuda.synchronize()
+    assert _rel(c, a.float() @ b.float().t()) < 2e-6
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_epilogues(cuda, dtype):
+    m, n, k = 256, 384, 192
+    g = torch.Generator().manual_seed(3)
+    tol = 8e-3 if dtype == torch.bfloat16 else 2e-6
+    a = torch.randn(m, k, generator=g).to(dtype).to(cuda)
+    b = torch.randn(n, k, generator=g).to(dtype).to(cuda)
+    bias = torch.randn(n, generator=g).to(dtype).to(cuda)
+    res = torch.randn(m, n, generator=g).to(dtype).to(cuda)
+    acc = a.float() @ b.float().t()
+    # store + bias + residual
+    c = torch.empty(m, n, dtype=dtype, device=cuda)
+    gemm(a, False, b, False, m, n, k, c, bias=bias, residual=res)
+    torch.cuda.synchronize()
+    assert _rel(c, acc + bias.float() + res.float()) < tol
+    # gelu
+    aux = torch.empty(m, n, dtype=dtype, device=cuda)
+    gemm(a, False, b, False, m, n, k, c, mode=1, bias=bias, aux=aux)
+    torch.cuda.synchronize()
+    pre = acc + bias.float()
+    assert _rel(aux, pre) < tol
+    assert _rel(c, torch.nn.functional.gelu(pre, approximate="tanh")) < tol
+    # dgelu
+    gemm(a, False, b, False, m, n, k, c, mode=2, aux=aux)
+    torch.cuda.synchronize()
+    x = aux.float().requires_grad_(True)
+    y = torch.nn.functional.gelu(x, approximate="tanh")
+    (gx,) = torch.autograd.grad(y, x, acc)
+    assert _rel(c, gx) < tol
+
+
+@pytest.mark.parametrize("a_mn,b_mn", list(itertools.product([False, True], repeat=2)))
+def test_f32_simt(cuda, a_mn, b_mn):
+    m, n, k = 200, 136, 72
+    g = torch.Generator().manual_seed(5)
+    a, a_st = _operand(m, k, a_mn, torch.float32, cuda, g)
+    b, b_st = _operand(n, k, b_mn, torch.float32, cuda, g)
+    c = torch.empty(m, n, device=cuda)
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, c)
+    torch.cuda.synchronize()
+    ref = (a.double() @ b.double().t())
+    assert _rel(c, ref) < 1e-6
+
+
+def test_bad_args_raise(cuda):
+    a = torch.zeros(8, 8, dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(_lib.InvalidArgument):
+        gemm(a, False, a, False, 0, 8, 8, torch.empty(8, 8, dtype=torch.bfloat16, device=cuda))
