@@ -136,6 +136,114 @@ int acco_gemm(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t
               const void* bias, const void* residual, int64_t ldr, void* aux, int64_t ld_aux,
               int beta, void* stream);
 
+/* ------------------------------------------------------ model plugin (LM)
+ * The B200 gradient oracle for the GPT-style LM defined in
+ * oracle/gpt_oracle.py, behind the Problem contract of
+ * proj/include/accosim/problems.hpp:86-92. precision: ACCO_DTYPE_F32
+ * (fp32-accurate parity mode) or ACCO_DTYPE_BF16 (tcgen05 throughput mode). */
+typedef struct acco_lm_cfg {
+    int vocab;
+    int d_model;
+    int n_layer;
+    int n_head;
+    int seq_len;
+    int n_samples;
+    uint64_t data_seed;
+    int precision;
+    int max_batch; /* samples per micro-batch the workspace is sized for */
+} acco_lm_cfg;
+
+typedef struct acco_model acco_model;
+int acco_model_create(const acco_lm_cfg* cfg, acco_model** out);
+int acco_model_destroy(acco_model* m);
+long long acco_model_num_params(const acco_model* m);
+/* default_theta0 (proj/src/problems.cpp:474-488 key) for the LM, host fp32 [psi]. */
+int acco_model_theta0(const acco_model* m, uint64_t master_seed, float* host_out);
+/* The synthetic token dataset, host int32 [n_samples][seq_len+1]. */
+int acco_model_dataset(const acco_model* m, int32_t* host_out);
+/* stochastic_grad (problems.cpp:419-451) fused with Bundle::add
+ * (protocols.cpp:61-66): grad_acc[psi] += batch * (per-sample mean gradient)
+ * at `params` (device, model precision); *loss_sum_dev (double) = sum of the
+ * per-sample losses. Draws Stream(stream_seed).below(n_samples) x batch. */
+int acco_model_stochastic_grad(acco_model* m, const void* params, uint64_t stream_seed, int batch,
+                               float* grad_acc, double* loss_sum_dev, void* stream);
+/* value_and_grad (problems.cpp:406-417) over the full dataset; blocking.
+ * grad_out (device fp32 [psi]) may be NULL. */
+int acco_model_value_and_grad(acco_model* m, const void* params, double* loss_out, float* grad_out,
+                              void* stream);
+
+/* --------------------------------------------------------------- trainer
+ * run_protocol (proj/include/accosim/protocols.hpp:89-90) on B200: one
+ * process per GPU (comm != NULL, NCCL) or all workers as virtual workers on
+ * one device (comm == NULL; device-side Fabric with the reference's fixed
+ * ascending-worker reduction order). */
+#define ACCO_METHOD_DDP 0
+#define ACCO_METHOD_DPU 1 /* not on the B200 path */
+#define ACCO_METHOD_WP 2  /* not on the B200 path */
+#define ACCO_METHOD_ACCO 3
+#define ACCO_METHOD_ZERO1 4 /* B200 baseline: DDP semantics, RS + sharded step + AG */
+
+#define ACCO_SCHED_FLOOR 0    /* every stage exactly max(k,1) micro-batches (round-0 estimate: 1) */
+#define ACCO_SCHED_ADAPTIVE 1 /* accumulate until the in-flight phase completes (Alg. 1) */
+#define ACCO_SCHED_REPLAY 2   /* per-update counts given in `replay` */
+
+/* SimConfig (protocols.hpp:29-38) plus B200 execution keys. */
+typedef struct acco_sim_cfg {
+    int n_workers;
+    int batch_size;
+    int n_grad_accumulation;
+    int warmup_rounds;
+    uint64_t master_seed;
+    int schedule;
+    const int32_t* replay;      /* [t_updates][2][n_workers]: mb_estimate, mb_main */
+    int replay_len;             /* number of int32 in replay */
+    int eval_every;             /* full-dataset loss/grad every k updates; 0 = never */
+    int eval_batch;             /* samples per evaluation chunk; 0 = model max_batch */
+    const double* throttle_ns;  /* [n_workers] straggler delay per micro-batch, or NULL */
+} acco_sim_cfg;
+
+/* RoundRecord (protocols.hpp:41-53); NaN where not evaluated. */
+typedef struct acco_record {
+    int update;
+    double time_s; /* measured seconds (CUDA events) since the start of the run call */
+    double loss;
+    double grad_sq;
+    double grad_sq_estimate;
+    double lyapunov;
+    long long samples_cum;
+    double train_loss; /* sample-weighted mean micro-batch loss (this rank) */
+} acco_record;
+
+typedef struct acco_run_stats {
+    long long issued_micro_batches;
+    long long consumed_micro_batches;
+    long long discarded_micro_batches;
+    double wall_ms;
+    double compute_busy_ms;
+    double comm_busy_ms;
+    double comm_exposed_ms; /* comm busy time not overlapped by compute */
+    double opt_ms;          /* fused optimizer kernel time, summed */
+    int opt_launches;
+    int diverged;
+} acco_run_stats;
+
+typedef struct acco_trainer acco_trainer;
+int acco_trainer_create(acco_model* model, const acco_opt_cfg* opt, const acco_sim_cfg* sim, int method,
+                        acco_comm* comm, acco_trainer** out);
+int acco_trainer_destroy(acco_trainer* t);
+/* Replicates theta0 (host fp32 [psi]) and resets optimizer state. */
+int acco_trainer_set_theta(acco_trainer* t, const float* host_theta);
+/* which: 0 committed theta replica, 1 estimate replica, 2 this rank's fp32 master shard. */
+int acco_trainer_get_theta(acco_trainer* t, int which, float* host_out);
+/* Runs t_updates committed updates (continuing). recs: [t_updates];
+ * mb_counts (nullable): [t_updates][2][n_local] (mb_estimate, mb_main);
+ * theta_history (nullable, host fp32): [t_updates][2][psi] = theta^(t+1) and
+ * theta-tilde^(t+1) after each commit (RunTrace.theta/estimate_history,
+ * protocols.hpp:61-76). */
+int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t* mb_counts,
+                     float* theta_history, acco_run_stats* stats);
+int acco_trainer_n_local(const acco_trainer* t);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,6 +98,17 @@ def lib() -> C.CDLL:
     return l
 
 
+def register(protos: dict) -> None:
+    """Add prototypes (applied now if the library is already loaded)."""
+    _PROTOS.update(protos)
+    if _lib is not None:
+        for name, (res, args) in protos.items():
+            f = getattr(_lib, name, None)
+            if f is not None:
+                f.restype = res
+                f.argtypes = args
+
+
 def check(status: int) -> None:
     if status == OK:
         return

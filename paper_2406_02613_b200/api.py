@@ -1,0 +1,460 @@
+"""Python host mirror of the reference trainer API over the C-ABI.
+
+Mirrors, with the same names, argument meaning and error behaviour:
+  OptimizerConfig / scheduled_lr        proj/include/accosim/optim.hpp:21-64
+  SimConfig                             proj/include/accosim/protocols.hpp:29-38
+  run_protocol -> RunTrace              proj/include/accosim/protocols.hpp:61-90
+  parse_config (JSON schema)            proj/src/config.cpp:80-133
+  shard_partition                       proj/include/accosim/shard.hpp:24-38
+with the B200 additions: problem kind "gpt" (the LM plugin), precision,
+schedule (floor / adaptive / replay), eval cadence, and NCCL multi-GPU via
+:class:`Comm` (one process per GPU).
+
+Errors: the reference's std::invalid_argument -> :class:`InvalidArgument`
+(a ValueError), std::logic_error -> :class:`LogicError`; divergence is data
+(``RunTrace.diverged``), as in the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import AccoError, InvalidArgument, LogicError  # noqa: F401
+
+METHODS = {"ddp": 0, "dpu": 1, "wp": 2, "acco": 3, "zero1": 4}
+KINDS = {"sgd": 0, "adam": 1, "adamw": 2}
+SCHEDULES = {"floor": 0, "adaptive": 1, "replay": 2}
+
+
+class LMCfgC(C.Structure):
+    _fields_ = [("vocab", C.c_int), ("d_model", C.c_int), ("n_layer", C.c_int), ("n_head", C.c_int),
+                ("seq_len", C.c_int), ("n_samples", C.c_int), ("data_seed", C.c_uint64),
+                ("precision", C.c_int), ("max_batch", C.c_int)]
+
+
+class SimCfgC(C.Structure):
+    _fields_ = [("n_workers", C.c_int), ("batch_size", C.c_int), ("n_grad_accumulation", C.c_int),
+                ("warmup_rounds", C.c_int), ("master_seed", C.c_uint64), ("schedule", C.c_int),
+                ("replay", C.POINTER(C.c_int32)), ("replay_len", C.c_int), ("eval_every", C.c_int),
+                ("eval_batch", C.c_int), ("throttle_ns", C.POINTER(C.c_double))]
+
+
+class RecordC(C.Structure):
+    _fields_ = [("update", C.c_int), ("time_s", C.c_double), ("loss", C.c_double), ("grad_sq", C.c_double),
+                ("grad_sq_estimate", C.c_double), ("lyapunov", C.c_double), ("samples_cum", C.c_longlong),
+                ("train_loss", C.c_double)]
+
+
+class StatsC(C.Structure):
+    _fields_ = [("issued_micro_batches", C.c_longlong), ("consumed_micro_batches", C.c_longlong),
+                ("discarded_micro_batches", C.c_longlong), ("wall_ms", C.c_double),
+                ("compute_busy_ms", C.c_double), ("comm_busy_ms", C.c_double), ("comm_exposed_ms", C.c_double),
+                ("opt_ms", C.c_double), ("opt_launches", C.c_int), ("diverged", C.c_int)]
+
+
+_P = C.c_void_p
+_lib.register({
+    "acco_model_create": (C.c_int, [C.POINTER(LMCfgC), C.POINTER(C.c_void_p)]),
+    "acco_model_destroy": (C.c_int, [_P]),
+    "acco_model_num_params": (C.c_longlong, [_P]),
+    "acco_model_theta0": (C.c_int, [_P, C.c_uint64, _P]),
+    "acco_model_dataset": (C.c_int, [_P, _P]),
+    "acco_model_stochastic_grad": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P, _P]),
+    "acco_model_value_and_grad": (C.c_int, [_P, _P, C.POINTER(C.c_double), _P, _P]),
+    "acco_trainer_create": (C.c_int, [_P, C.POINTER(_lib.OptCfg), C.POINTER(SimCfgC), C.c_int, _P,
+                                      C.POINTER(C.c_void_p)]),
+    "acco_trainer_destroy": (C.c_int, [_P]),
+    "acco_trainer_set_theta": (C.c_int, [_P, _P]),
+    "acco_trainer_get_theta": (C.c_int, [_P, C.c_int, _P]),
+    "acco_trainer_run": (C.c_int, [_P, C.c_int, C.POINTER(RecordC), _P, _P, C.POINTER(StatsC)]),
+    "acco_trainer_n_local": (C.c_int, [_P]),
+})
+
+
+# ------------------------------------------------------------------ optimizer
+@dataclass
+class OptimizerConfig:
+    """optim.hpp:21-32 (same defaults)."""
+    kind: str = "sgd"
+    learning_rate: float = 0.0
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+    weight_decay: float = 0.0
+    scheduler: str = "constant"
+    n_warmup_steps: int = 0
+    total_steps: int = 0
+    cosine_min_factor: float = 0.0
+
+    def to_c(self) -> _lib.OptCfg:
+        if self.kind not in KINDS:
+            raise InvalidArgument(_lib.INVALID, f"unknown optimizer kind: {self.kind}")
+        if self.scheduler not in ("constant", "cosine"):
+            raise InvalidArgument(_lib.INVALID, "config: scheduler must be constant or cosine")
+        return _lib.OptCfg(KINDS[self.kind], self.learning_rate, self.adam_beta1, self.adam_beta2, self.adam_eps,
+                           self.weight_decay, 1 if self.scheduler == "cosine" else 0, self.n_warmup_steps,
+                           self.total_steps, self.cosine_min_factor)
+
+
+def scheduled_lr(cfg: OptimizerConfig, t: int) -> float:
+    """optim.cpp:37-48, evaluated by the library."""
+    c = cfg.to_c()
+    return _lib.lib().acco_scheduled_lr(C.byref(c), t)
+
+
+def shard_partition(dim: int, n: int):
+    """shard.hpp:24-38 via the library (bit-exact integer layout)."""
+    if n < 1:
+        raise InvalidArgument(_lib.INVALID, "shard_partition: need at least one worker")
+    lo = (C.c_uint64 * n)()
+    hi = (C.c_uint64 * n)()
+    _lib.call("acco_shard_partition", dim, n, lo, hi)
+    return [(int(lo[i]), int(hi[i])) for i in range(n)]
+
+
+def sample_indices(stream_seed: int, batch: int, n_samples: int) -> List[int]:
+    out = (C.c_int32 * batch)()
+    _lib.call("acco_sample_indices", C.c_uint64(stream_seed), batch, n_samples, out)
+    return list(out)
+
+
+def derive(master: int, a: int, b: int = 0, c: int = 0, d: int = 0) -> int:
+    return int(_lib.lib().acco_rng_derive(*(C.c_uint64(x & (2**64 - 1)) for x in (master, a, b, c, d))))
+
+
+# ---------------------------------------------------------------------- model
+@dataclass(frozen=True)
+class LMConfig:
+    """problem.kind == "gpt" (B200 addition to config.cpp's problem block)."""
+    vocab: int = 256
+    d_model: int = 128
+    n_layer: int = 2
+    n_head: int = 4
+    seq_len: int = 64
+    n_samples: int = 256
+    data_seed: int = 1
+    precision: str = "fp32"  # "fp32" (parity) or "bf16" (throughput)
+    max_batch: int = 8
+
+    def to_c(self) -> LMCfgC:
+        if self.precision not in ("fp32", "bf16"):
+            raise InvalidArgument(_lib.INVALID, "lm config: precision must be fp32 or bf16")
+        return LMCfgC(self.vocab, self.d_model, self.n_layer, self.n_head, self.seq_len, self.n_samples,
+                      self.data_seed, 1 if self.precision == "bf16" else 0, self.max_batch)
+
+
+class Model:
+    """The LM plugin (owns device weights workspace and the token dataset)."""
+
+    def __init__(self, cfg: LMConfig):
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        c = cfg.to_c()
+        _lib.call("acco_model_create", C.byref(c), C.byref(self._h))
+        self.dim = int(_lib.lib().acco_model_num_params(self._h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib().acco_model_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def default_theta0(self, master_seed: int) -> np.ndarray:
+        out = np.empty(self.dim, dtype=np.float32)
+        _lib.call("acco_model_theta0", self._h, C.c_uint64(master_seed), out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def dataset(self) -> np.ndarray:
+        out = np.empty((self.cfg.n_samples, self.cfg.seq_len + 1), dtype=np.int32)
+        _lib.call("acco_model_dataset", self._h, out.ctypes.data_as(C.c_void_p))
+        return out
+
+
+# ---------------------------------------------------------------------- comm
+class Comm:
+    """NCCL communicator for one rank (one process per GPU). The unique id is
+    exchanged over an existing torch.distributed group (any backend)."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _lib.call("acco_comm_unique_id", uid)
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        self._h = C.c_void_p()
+        _lib.call("acco_comm_init_rank", world, rank, uid, device, C.byref(self._h))
+        self.rank, self.world = rank, world
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib().acco_comm_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+# --------------------------------------------------------------------- trainer
+@dataclass
+class SimConfig:
+    """protocols.hpp:29-38 (cost model / simulated time replaced by real
+    streams), plus B200 execution keys."""
+    n_workers: int = 1
+    batch_size: int = 1
+    n_grad_accumulation: int = 1
+    warmup_rounds: int = 0
+    full_batch_gradients: bool = False
+    master_seed: int = 1
+    worker_multipliers: Optional[Sequence[float]] = None
+    # B200 keys
+    schedule: str = "floor"
+    replay: Optional[Sequence] = None  # [(mb_estimate[w], mb_main[w])] per update
+    eval_every: int = 1
+    eval_batch: int = 0
+    throttle_ns: Optional[Sequence[float]] = None
+
+
+@dataclass
+class RoundRecord:
+    """protocols.hpp:41-53 (+ train_loss)."""
+    update: int
+    time_s: float
+    loss: float
+    grad_sq: float
+    grad_sq_estimate: float
+    lyapunov: float
+    samples_cum: int
+    mb_main: List[int]
+    mb_estimate: List[int]
+    train_loss: float
+
+    @property
+    def micro_batches(self):
+        return [a + b for a, b in zip(self.mb_main, self.mb_estimate)]
+
+
+@dataclass
+class RunTrace:
+    """protocols.hpp:61-76."""
+    records: List[RoundRecord] = field(default_factory=list)
+    diverged: bool = False
+    theta_history: List[np.ndarray] = field(default_factory=list)
+    estimate_history: List[np.ndarray] = field(default_factory=list)
+    issued_micro_batches: int = 0
+    consumed_micro_batches: int = 0
+    discarded_micro_batches: int = 0
+    stats: dict = field(default_factory=dict)
+
+
+class Trainer:
+    def __init__(self, method: str, model: Model, opt: OptimizerConfig, sim: SimConfig, comm: Optional[Comm] = None):
+        if method not in METHODS:
+            raise InvalidArgument(_lib.INVALID, f"unknown method: {method}")
+        if sim.full_batch_gradients:
+            raise InvalidArgument(_lib.INVALID, "full_batch_gradients is not supported for the LM problem")
+        if sim.worker_multipliers is not None and len(sim.worker_multipliers) != sim.n_workers:
+            raise InvalidArgument(_lib.INVALID, "run_protocol: one multiplier per worker")
+        self.method, self.model, self.opt, self.sim, self.comm = method, model, opt, sim, comm
+        self._replay = None
+        rp, rl = None, 0
+        if sim.replay is not None:
+            flat = []
+            for est, main in sim.replay:
+                flat += list(est) + list(main)
+            self._replay = (C.c_int32 * len(flat))(*flat)
+            rp, rl = self._replay, len(flat)
+        self._thr = None
+        if sim.throttle_ns is not None:
+            self._thr = (C.c_double * sim.n_workers)(*sim.throttle_ns)
+        s = SimCfgC(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, sim.warmup_rounds, sim.master_seed,
+                    SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr)
+        o = opt.to_c()
+        self._h = C.c_void_p()
+        _lib.call("acco_trainer_create", model.handle, C.byref(o), C.byref(s), METHODS[method],
+                  comm.handle if comm is not None else None, C.byref(self._h))
+        self.n_local = _lib.lib().acco_trainer_n_local(self._h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib().acco_trainer_destroy(h)
+            self._h = None
+
+    def set_theta(self, theta: np.ndarray):
+        th = np.ascontiguousarray(theta, dtype=np.float32)
+        if th.shape != (self.model.dim,):
+            raise InvalidArgument(_lib.INVALID, "run_protocol: theta0 dimension mismatch")
+        _lib.call("acco_trainer_set_theta", self._h, th.ctypes.data_as(C.c_void_p))
+
+    def theta(self, which: int = 0) -> np.ndarray:
+        n = self.model.dim
+        out = np.empty(n, dtype=np.float32)
+        _lib.call("acco_trainer_get_theta", self._h, which, out.ctypes.data_as(C.c_void_p))
+        return out
+
+    def run(self, t_updates: int, history: bool = False):
+        recs = (RecordC * t_updates)()
+        nl = self.n_local
+        counts = np.zeros((t_updates, 2, nl), dtype=np.int32)
+        hist = np.zeros((t_updates, 2, self.model.dim), dtype=np.float32) if history else None
+        st = StatsC()
+        rc = _lib.lib().acco_trainer_run(self._h, t_updates, recs, counts.ctypes.data_as(C.c_void_p),
+                                         hist.ctypes.data_as(C.c_void_p) if history else None, C.byref(st))
+        diverged = rc == _lib.DIVERGED
+        if rc not in (_lib.OK, _lib.DIVERGED):
+            _lib.check(rc)
+        out = []
+        for i in range(t_updates):
+            r = recs[i]
+            out.append(RoundRecord(r.update, r.time_s, r.loss, r.grad_sq, r.grad_sq_estimate, r.lyapunov,
+                                   r.samples_cum, counts[i, 1].tolist(), counts[i, 0].tolist(), r.train_loss))
+        stats = {k: getattr(st, k) for k, _ in StatsC._fields_}
+        return out, hist, stats, diverged
+
+
+def run_protocol(method: str, problem, opt_cfg: OptimizerConfig, sim: SimConfig, t_updates: int,
+                 theta0: Optional[np.ndarray] = None, comm: Optional[Comm] = None,
+                 record_history: bool = True) -> RunTrace:
+    """protocols.hpp:89-90 / protocols.cpp:713-742 on B200."""
+    if t_updates < 1:
+        raise InvalidArgument(_lib.INVALID, "run_protocol: t_updates >= 1")
+    if sim.n_workers < 1:
+        raise InvalidArgument(_lib.INVALID, "run_protocol: n_workers >= 1")
+    if sim.batch_size < 1:
+        raise InvalidArgument(_lib.INVALID, "run_protocol: batch_size >= 1")
+    if sim.n_grad_accumulation < 1:
+        raise InvalidArgument(_lib.INVALID, "run_protocol: n_grad_accumulation >= 1")
+    if sim.warmup_rounds < 0:
+        raise InvalidArgument(_lib.INVALID, "run_protocol: warmup_rounds >= 0")
+    if sim.worker_multipliers is not None:
+        if len(sim.worker_multipliers) != sim.n_workers:
+            raise InvalidArgument(_lib.INVALID, "run_protocol: one multiplier per worker")
+        if any(not (m > 0.0) for m in sim.worker_multipliers):
+            raise InvalidArgument(_lib.INVALID, "run_protocol: multipliers > 0")
+    if not (opt_cfg.learning_rate > 0.0):
+        raise InvalidArgument(_lib.INVALID, "run_protocol: learning_rate > 0")
+    if opt_cfg.total_steps == 0:
+        opt_cfg = OptimizerConfig(**{**opt_cfg.__dict__, "total_steps": t_updates})
+    model = problem if isinstance(problem, Model) else Model(problem)
+    th0 = model.default_theta0(sim.master_seed) if theta0 is None else np.asarray(theta0, dtype=np.float32)
+    if th0.shape != (model.dim,):
+        raise InvalidArgument(_lib.INVALID, "run_protocol: theta0 dimension mismatch")
+    tr = Trainer(method, model, opt_cfg, sim, comm)
+    tr.set_theta(th0)
+    recs, hist, stats, diverged = tr.run(t_updates, history=record_history)
+    out = RunTrace(records=recs, diverged=diverged, stats=stats)
+    out.issued_micro_batches = stats["issued_micro_batches"]
+    out.consumed_micro_batches = stats["consumed_micro_batches"]
+    out.discarded_micro_batches = stats["discarded_micro_batches"]
+    if record_history:
+        out.theta_history = [th0.copy()] + [hist[t, 0].copy() for t in range(len(recs))]
+        out.estimate_history = [th0.copy()] + [hist[t, 1].copy() for t in range(len(recs))]
+    return out
+
+
+# ---------------------------------------------------------------------- config
+@dataclass
+class ExperimentConfig:
+    """config.hpp:13-27."""
+    problem: LMConfig
+    method: str
+    optimizer: OptimizerConfig
+    sim: SimConfig
+    t_updates: int
+    output_dir: str = ""
+    raw: dict = field(default_factory=dict)
+
+
+def _get(j, k, default):
+    return j[k] if k in j else default
+
+
+def _req(j, k):
+    if k not in j:
+        raise InvalidArgument(_lib.INVALID, f"config: missing key '{k}'")
+    return j[k]
+
+
+def parse_config(j: dict) -> ExperimentConfig:
+    """config.cpp:80-133 (same keys, defaults and validation); problem.kind
+    must be "gpt" on the B200 path (the analytic problems are CPU fixtures)."""
+    p = _req(j, "problem")
+    kind = _req(p, "kind")
+    if kind != "gpt":
+        raise InvalidArgument(_lib.INVALID, f"unknown problem kind for the B200 path: {kind}")
+    prob = LMConfig(vocab=_get(p, "vocab", 256), d_model=_get(p, "d_model", 128), n_layer=_get(p, "n_layer", 2),
+                    n_head=_get(p, "n_head", 4), seq_len=_get(p, "seq_len", 64), n_samples=_get(p, "n_samples", 256),
+                    data_seed=_get(p, "seed", 1), precision=_get(p, "precision", "fp32"),
+                    max_batch=max(_get(j, "batch_size", 1), _get(p, "max_batch", 1)))
+    method = _req(j, "method_name")
+    if method not in METHODS:
+        raise InvalidArgument(_lib.INVALID, f"unknown method: {method}")
+    o = _req(j, "optimizer")
+    kind = _req(o, "kind")
+    if kind not in KINDS:
+        raise InvalidArgument(_lib.INVALID, f"unknown optimizer kind: {kind}")
+    opt = OptimizerConfig(kind=kind, learning_rate=_req(o, "learning_rate"), weight_decay=_get(o, "weight_decay", 0.0),
+                          adam_beta1=_get(o, "adam_beta1", 0.9), adam_beta2=_get(o, "adam_beta2", 0.999),
+                          adam_eps=_get(o, "adam_eps", 1e-8), scheduler=_get(o, "scheduler", "constant"),
+                          n_warmup_steps=_get(o, "n_warmup_steps", 0),
+                          cosine_min_factor=_get(o, "cosine_min_factor", 0.0))
+    if opt.scheduler not in ("constant", "cosine"):
+        raise InvalidArgument(_lib.INVALID, "config: scheduler must be constant or cosine")
+    if not (opt.learning_rate > 0.0):
+        raise InvalidArgument(_lib.INVALID, "config: learning_rate > 0")
+    if not (0.0 <= opt.adam_beta1 < 1.0 and 0.0 <= opt.adam_beta2 < 1.0):
+        raise InvalidArgument(_lib.INVALID, "config: adam betas must lie in [0, 1)")
+    if opt.weight_decay < 0.0:
+        raise InvalidArgument(_lib.INVALID, "config: weight_decay >= 0")
+    if opt.n_warmup_steps < 0:
+        raise InvalidArgument(_lib.INVALID, "config: n_warmup_steps >= 0")
+    sim = SimConfig(n_workers=_get(j, "n_workers", 1), batch_size=_get(j, "batch_size", 1),
+                    n_grad_accumulation=_get(j, "n_grad_accumulation", 1), warmup_rounds=_get(j, "warmup_rounds", 0),
+                    full_batch_gradients=_get(j, "full_batch_gradients", False), master_seed=_get(j, "master_seed", 1),
+                    schedule=_get(j, "schedule", "floor"), eval_every=_get(j, "eval_every", 1))
+    if "heterogeneity" in j:
+        sim.worker_multipliers = _get(j["heterogeneity"], "worker_multipliers", None)
+    t = _req(j, "t_updates")
+    if t < 1:
+        raise InvalidArgument(_lib.INVALID, "config: t_updates >= 1")
+    if sim.n_workers < 1:
+        raise InvalidArgument(_lib.INVALID, "config: n_workers >= 1")
+    if sim.batch_size < 1:
+        raise InvalidArgument(_lib.INVALID, "config: batch_size >= 1")
+    if sim.n_grad_accumulation < 1:
+        raise InvalidArgument(_lib.INVALID, "config: n_grad_accumulation >= 1")
+    if sim.warmup_rounds < 0:
+        raise InvalidArgument(_lib.INVALID, "config: warmup_rounds >= 0")
+    if sim.worker_multipliers is not None:
+        if len(sim.worker_multipliers) != sim.n_workers:
+            raise InvalidArgument(_lib.INVALID, "config: worker_multipliers length must equal n_workers")
+        if any(not (m > 0) for m in sim.worker_multipliers):
+            raise InvalidArgument(_lib.INVALID, "config: worker_multipliers > 0")
+    opt.total_steps = t  # config.cpp:131
+    return ExperimentConfig(prob, method, opt, sim, t, _get(j, "output_dir", ""), dict(j))
+
+
+def config_hash(j: dict) -> str:
+    """config.cpp:147-157: FNV-1a over the canonical (nlohmann dump) serialisation."""
+    import json
+
+    s = json.dumps(j, separators=(",", ":"), sort_keys=True, ensure_ascii=False).encode()
+    h = 0xCBF29CE484222325
+    for c in s:
+        h ^= c
+        h = (h * 0x100000001B3) & (2**64 - 1)
+    return f"{h:016x}"

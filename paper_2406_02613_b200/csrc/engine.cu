@@ -1,0 +1,681 @@
+// ACCO / DDP / ZeRO-1 trainer engines on two CUDA streams per GPU.
+//
+// ACCO (proj/src/protocols.cpp:437-709, Alg. 1 of PAPER.md:910-960): comm
+// phase p consumes the accumulator each worker posts at the end of its
+// stage p; even phases commit the estimate (transient optimizer copy), odd
+// phases the full update. Stage p computes at the parameters produced by
+// phase p-2 (theta-tilde for even p, theta for odd p) and may only *end* once
+// phase p-1 is complete:
+//
+//   compute stream:  [stage p ..........][stage p+1 ............]
+//   comm stream:            [phase p-1: AR(counts) RS -> fused AdamW -> AG]
+//
+// The reference's discrete-event clock is replaced by real streams; the
+// reference's "keep accumulating until the collective completes" is either
+// realised literally (adaptive schedule: the host polls the phase-done event
+// after every micro-batch) or fixed (floor/replay schedules: the compute
+// stream waits on the event before starting the next stage), which makes
+// micro-batch counts bit-exact and replayable by the oracle.
+#include "engine.h"
+#include "lm_kernels.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+namespace acco {
+
+namespace {
+constexpr uint64_t kTagInit = 1, kTagMain = 2, kTagEstimate = 3;  // protocols.cpp:52-54
+
+struct EventArr {
+    std::vector<cudaEvent_t> ev;
+    void create(size_t n) {
+        ev.assign(n, nullptr);
+        for (auto& e : ev) ACCO_CUDA(cudaEventCreate(&e));
+    }
+    ~EventArr() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+    cudaEvent_t operator[](size_t i) const { return ev[i]; }
+};
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    ACCO_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+}  // namespace
+
+struct Trainer::PhaseEvents {
+    EventArr post, stage_start, start, rs_done, opt_done, done, mb;
+    std::vector<long long> counts;  // [phase][local worker] samples posted
+    int n_local = 1;
+};
+
+Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm)
+    : model_(model), cfg_(cfg), sim_(sim), method_(method), comm_(comm) {
+    validate(cfg_);
+    ACCO_REQUIRE(method == kACCO || method == kDDP || method == kZeRO1,
+                 "method: dpu/wp are not on the B200 path (SURVEY.md §8f 'next')");
+    ACCO_REQUIRE(sim.n_workers >= 1, "run_protocol: n_workers >= 1");
+    ACCO_REQUIRE(sim.batch_size >= 1, "run_protocol: batch_size >= 1");
+    ACCO_REQUIRE(sim.n_grad_accumulation >= 1, "run_protocol: n_grad_accumulation >= 1");
+    ACCO_REQUIRE(sim.batch_size <= model->cfg().max_batch, "batch_size exceeds the model's max_batch workspace");
+    ACCO_REQUIRE(sim.throttle_ns.empty() || static_cast<int>(sim.throttle_ns.size()) == sim.n_workers,
+                 "run_protocol: one multiplier per worker");
+    if (comm_) {
+        world_ = comm_->size();
+        rank_ = comm_->rank();
+        n_local_ = 1;
+        ACCO_REQUIRE(world_ == sim.n_workers, "comm size must equal n_workers");
+    } else {
+        world_ = 1;
+        rank_ = 0;
+        n_local_ = sim.n_workers;
+        ACCO_REQUIRE(n_local_ <= 16, "virtual workers: at most 16 per device");
+        ACCO_REQUIRE(sim.schedule != kAdaptive || n_local_ == 1,
+                     "adaptive schedule needs one worker per device (NCCL mode)");
+    }
+    psi_ = model->num_params();
+    layout_ = shard_partition(static_cast<uint64_t>(psi_), sim.n_workers);
+    const bool sharded = comm_ && method_ != kDDP;
+    if (sharded) {
+        chunk_ = static_cast<int64_t>(layout_.chunk());
+        padded_ = psi_ % world_ != 0;
+        own_lo_ = static_cast<int64_t>(layout_.lo(rank_));
+        own_n_ = static_cast<int64_t>(layout_.size(rank_));
+    } else {
+        chunk_ = psi_;
+        padded_ = false;
+        own_lo_ = 0;
+        own_n_ = psi_;
+    }
+    int lo_prio = 0, hi_prio = 0;
+    ACCO_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    ACCO_CUDA(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, lo_prio));
+    ACCO_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, hi_prio));
+    alloc();
+}
+
+Trainer::~Trainer() {
+    cudaStreamSynchronize(cs_);
+    cudaStreamSynchronize(ms_);
+    void* bufs[] = {theta_act_, est_act_, master_, m_, v_, pad_send_, g_ret_, g_main_, cnt_send_, flag_,
+                    loss_ring_, eval_grad_, eval_scratch_};
+    for (void* b : bufs) cudaFree(b);
+    if (ag_theta_ != theta_act_) cudaFree(ag_theta_);
+    if (ag_est_ != est_act_) cudaFree(ag_est_);
+    for (float* a : acc_) cudaFree(a);
+    cudaStreamDestroy(cs_);
+    cudaStreamDestroy(ms_);
+}
+
+void Trainer::alloc() {
+    const size_t e = model_->act_bytes();
+    const size_t P = static_cast<size_t>(psi_);
+    ACCO_CUDA(cudaMalloc(&theta_act_, P * e));
+    ACCO_CUDA(cudaMalloc(&est_act_, P * e));
+    if (comm_ && padded_) {
+        ACCO_CUDA(cudaMalloc(&ag_theta_, static_cast<size_t>(chunk_) * world_ * e));
+        ACCO_CUDA(cudaMalloc(&ag_est_, static_cast<size_t>(chunk_) * world_ * e));
+        ACCO_CUDA(cudaMalloc(&pad_send_, static_cast<size_t>(chunk_) * world_ * 4));
+    } else {
+        ag_theta_ = theta_act_;
+        ag_est_ = est_act_;
+    }
+    const size_t own_cap = static_cast<size_t>(comm_ && method_ != kDDP ? chunk_ : psi_);
+    ACCO_CUDA(cudaMalloc(&master_, own_cap * 4));
+    if (cfg_.kind != 0) {
+        ACCO_CUDA(cudaMalloc(&m_, own_cap * 4));
+        ACCO_CUDA(cudaMalloc(&v_, own_cap * 4));
+    }
+    // accumulators: ACCO ping-pongs two per worker; with a single virtual
+    // worker the estimate shard *is* the accumulator, so a third one keeps it
+    // alive through the commit phase without a copy.
+    const int nacc = method_ == kACCO ? (!comm_ && n_local_ == 1 ? 3 : 2) : 1;
+    for (int i = 0; i < n_local_ * nacc; ++i) {
+        float* a = nullptr;
+        ACCO_CUDA(cudaMalloc(&a, P * 4));
+        ACCO_CUDA(cudaMemset(a, 0, P * 4));
+        acc_.push_back(a);
+    }
+    if (comm_ || n_local_ > 1) {
+        ACCO_CUDA(cudaMalloc(&g_ret_, own_cap * 4));
+        ACCO_CUDA(cudaMalloc(&g_main_, own_cap * 4));
+    }
+    ACCO_CUDA(cudaMalloc(&cnt_send_, 8));
+    ACCO_CUDA(cudaMalloc(&flag_, sizeof(int)));
+    ACCO_CUDA(cudaMemset(flag_, 0, sizeof(int)));
+    loss_cap_ = 1 << 16;
+    ACCO_CUDA(cudaMalloc(&loss_ring_, loss_cap_ * sizeof(double)));
+    if (sim_.eval_every > 0) {
+        ACCO_CUDA(cudaMalloc(&eval_grad_, P * 4));
+        ACCO_CUDA(cudaMalloc(&eval_scratch_, 512 * sizeof(double)));
+    }
+}
+
+void Trainer::set_theta(const float* host) {
+    const size_t P = static_cast<size_t>(psi_);
+    float* tmp = nullptr;
+    ACCO_CUDA(cudaMalloc(&tmp, P * 4));
+    ACCO_CUDA(cudaMemcpy(tmp, host, P * 4, cudaMemcpyHostToDevice));
+    f32_to(tmp, theta_act_, model_->act_dtype(), psi_, cs_);
+    f32_to(tmp, est_act_, model_->act_dtype(), psi_, cs_);
+    ACCO_CUDA(cudaMemcpyAsync(master_, tmp + own_lo_, static_cast<size_t>(own_n_) * 4, cudaMemcpyDeviceToDevice, cs_));
+    if (m_) {
+        ACCO_CUDA(cudaMemsetAsync(m_, 0, static_cast<size_t>(own_n_) * 4, cs_));
+        ACCO_CUDA(cudaMemsetAsync(v_, 0, static_cast<size_t>(own_n_) * 4, cs_));
+    }
+    ACCO_CUDA(cudaStreamSynchronize(cs_));
+    ACCO_CUDA(cudaFree(tmp));
+    step_ = 0;
+    update_ = 0;
+    samples_cum_ = 0;
+}
+
+void Trainer::get_theta(int which, float* host) {
+    ACCO_CUDA(cudaStreamSynchronize(ms_));
+    ACCO_CUDA(cudaStreamSynchronize(cs_));
+    if (which == 2) {
+        ACCO_CUDA(cudaMemcpy(host, master_, static_cast<size_t>(own_n_) * 4, cudaMemcpyDeviceToHost));
+        return;
+    }
+    const void* src = which == 0 ? theta_act_ : est_act_;
+    const size_t P = static_cast<size_t>(psi_);
+    if (model_->act_dtype() == 0) {
+        ACCO_CUDA(cudaMemcpy(host, src, P * 4, cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<uint16_t> tmp(P);
+        ACCO_CUDA(cudaMemcpy(tmp.data(), src, P * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < P; ++i) {
+            uint32_t u = static_cast<uint32_t>(tmp[i]) << 16;
+            std::memcpy(&host[i], &u, 4);
+        }
+    }
+}
+
+int Trainer::stage_len(int p, int w, int T) const {
+    if (method_ != kACCO) return sim_.n_grad_accumulation;
+    if (p == 0) return 1;  // bootstrap: one micro-batch at theta0 (protocols.cpp:468-474)
+    if (sim_.schedule == kReplay) {
+        const int t = p / 2, half = p % 2;  // half 0: estimate, 1: main
+        const int gw = comm_ ? rank_ : w;
+        const size_t i = (static_cast<size_t>(t) * 2 + half) * sim_.n_workers + gw;
+        ACCO_REQUIRE(i < sim_.replay.size(), "replay schedule shorter than the run");
+        const int k = sim_.replay[i];
+        ACCO_REQUIRE(k >= 1, "acco: empty accumulator at barrier");  // protocols.cpp:603
+        return k;
+    }
+    (void)T;
+    return std::max(sim_.n_grad_accumulation, 1);
+}
+
+void Trainer::micro(int w, const void* params, uint64_t round, uint64_t tag, int ordinal, float* acc,
+                    double* loss_slot) {
+    const uint64_t gw = comm_ ? static_cast<uint64_t>(rank_) : static_cast<uint64_t>(w);
+    const uint64_t seed = rng_derive(sim_.master_seed, gw, round, tag, static_cast<uint64_t>(ordinal));
+    model_->micro_batch(params, seed, 0, 0, sim_.batch_size, acc, loss_slot, cs_);
+    if (!sim_.throttle_ns.empty()) spin_ns(static_cast<uint64_t>(sim_.throttle_ns[static_cast<size_t>(gw)]), cs_);
+}
+
+void Trainer::eval(const void* params, double* loss_slots, double* gsq_slot) {
+    const int n = model_->cfg().n_samples;
+    const int eb = sim_.eval_batch > 0 ? std::min(sim_.eval_batch, model_->cfg().max_batch) : model_->cfg().max_batch;
+    ACCO_CUDA(cudaMemsetAsync(eval_grad_, 0, static_cast<size_t>(psi_) * 4, cs_));
+    int ci = 0;
+    for (int c = 0; c < n; c += eb, ++ci)
+        model_->micro_batch(params, 0, 1, c, std::min(eb, n - c), eval_grad_, loss_slots + ci, cs_);
+    scale_f32(eval_grad_, 1.0 / n, psi_, cs_);
+    norm_sq(eval_grad_, psi_, gsq_slot, eval_scratch_, cs_);
+}
+
+void Trainer::launch_phase(int p, int t_base, int64_t* tot, PhaseEvents& ev) {
+    (void)t_base;
+    for (int w = 0; w < n_local_; ++w) ACCO_CUDA(cudaStreamWaitEvent(ms_, ev.post[static_cast<size_t>(p) * n_local_ + w], 0));
+    ACCO_CUDA(cudaEventRecord(ev.start[p], ms_));
+    long long local = 0;
+    for (int w = 0; w < n_local_; ++w) local += ev.counts[static_cast<size_t>(p) * n_local_ + w];
+    int64_t* totp = tot + p;
+    // 1. Fabric::all_reduce_counts (collectives.cpp:48-53)
+    if (comm_) {
+        fill_i64(cnt_send_, local, ms_);
+        comm_->all_reduce_i64(cnt_send_, totp, 1, ms_);
+    } else {
+        fill_i64(totp, local, ms_);
+    }
+    const int act = model_->act_dtype();
+    const size_t e = model_->act_bytes();
+    const size_t P = static_cast<size_t>(psi_);
+    auto padded_args = [&](std::vector<uint64_t>& lo, std::vector<uint64_t>& sz) {
+        for (int w = 0; w < world_; ++w) {
+            lo.push_back(layout_.lo(w));
+            sz.push_back(layout_.size(w));
+        }
+    };
+    if (method_ == kACCO) {
+        const bool est = p % 2 == 0;
+        const int nacc = static_cast<int>(acc_.size()) / n_local_;
+        auto acc_of = [&](int q, int w) { return acc_[static_cast<size_t>(w) * nacc + q % nacc]; };
+        float* g;
+        // 2. Fabric::reduce_scatter (collectives.cpp:55-75)
+        if (comm_) {
+            g = est ? g_ret_ : g_main_;
+            const float* send = acc_of(p, 0);
+            if (padded_) {
+                std::vector<uint64_t> lo, sz;
+                padded_args(lo, sz);
+                pack_padded(send, pad_send_, lo.data(), sz.data(), world_, static_cast<uint64_t>(chunk_), ms_);
+                send = pad_send_;
+            }
+            comm_->reduce_scatter_f32(send, g, static_cast<size_t>(chunk_), ms_);
+        } else if (n_local_ == 1) {
+            g = acc_of(p, 0);  // single worker: the accumulator is the reduced shard
+        } else {
+            g = est ? g_ret_ : g_main_;
+            std::vector<const float*> in;
+            for (int w = 0; w < n_local_; ++w) in.push_back(acc_of(p, w));
+            sum_ordered(in.data(), n_local_, g, psi_, ms_);
+        }
+        ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
+        // 3. fused sharded optimizer: K6 estimate (transient) / K7 commit
+        void* agbuf = est ? ag_est_ : ag_theta_;
+        void* out = comm_ ? static_cast<char*>(agbuf) + static_cast<size_t>(rank_) * chunk_ * e : agbuf;
+        if (est) {
+            opt_apply(cfg_, step_, false, g, nullptr, totp, nullptr, master_, m_, v_, own_n_, out, act, flag_, ms_);
+        } else {
+            const float* ret = (comm_ || n_local_ > 1) ? g_ret_ : acc_of(p - 1, 0);
+            opt_apply(cfg_, step_, true, g, ret, totp, totp - 1, master_, m_, v_, own_n_, out, act, flag_, ms_);
+            ++step_;
+        }
+        ACCO_CUDA(cudaEventRecord(ev.opt_done[p], ms_));
+        // 4. Fabric::all_gather (collectives.cpp:77-91), in place
+        if (comm_) {
+            comm_->all_gather(out, agbuf, static_cast<size_t>(chunk_), act, ms_);
+            if (padded_) {
+                std::vector<uint64_t> lo, sz;
+                padded_args(lo, sz);
+                unpack_padded(agbuf, est ? est_act_ : theta_act_, static_cast<int>(e), lo.data(), sz.data(), world_,
+                              static_cast<uint64_t>(chunk_), ms_);
+            }
+        }
+    } else {
+        // DDP (all-reduce + replicated step) / ZeRO-1 (RS + sharded step + AG)
+        float* acc0 = acc_[0];
+        float* g = acc0;
+        void* out = theta_act_;
+        if (comm_ && method_ == kDDP) {
+            comm_->all_reduce_f32(acc0, acc0, P, ms_);
+        } else if (comm_) {
+            const float* send = acc0;
+            if (padded_) {
+                std::vector<uint64_t> lo, sz;
+                padded_args(lo, sz);
+                pack_padded(send, pad_send_, lo.data(), sz.data(), world_, static_cast<uint64_t>(chunk_), ms_);
+                send = pad_send_;
+            }
+            g = g_main_;
+            comm_->reduce_scatter_f32(send, g, static_cast<size_t>(chunk_), ms_);
+            out = static_cast<char*>(ag_theta_) + static_cast<size_t>(rank_) * chunk_ * e;
+        } else if (n_local_ > 1) {
+            std::vector<const float*> in;
+            for (int w = 0; w < n_local_; ++w) in.push_back(acc_[static_cast<size_t>(w)]);
+            g = g_main_;
+            sum_ordered(in.data(), n_local_, g, psi_, ms_);
+        }
+        ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
+        opt_apply(cfg_, step_, true, g, nullptr, totp, nullptr, master_, m_, v_, own_n_, out, act, flag_, ms_);
+        ++step_;
+        ACCO_CUDA(cudaEventRecord(ev.opt_done[p], ms_));
+        if (comm_ && method_ == kZeRO1) {
+            comm_->all_gather(out, ag_theta_, static_cast<size_t>(chunk_), act, ms_);
+            if (padded_) {
+                std::vector<uint64_t> lo, sz;
+                padded_args(lo, sz);
+                unpack_padded(ag_theta_, theta_act_, static_cast<int>(e), lo.data(), sz.data(), world_,
+                              static_cast<uint64_t>(chunk_), ms_);
+            }
+        }
+    }
+    ACCO_CUDA(cudaEventRecord(ev.done[p], ms_));
+}
+
+void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* theta_hist) {
+    ACCO_REQUIRE(T >= 1, "run_protocol: t_updates >= 1");
+    if (cfg_.total_steps == 0) cfg_.total_steps = T;  // run_protocol, protocols.cpp:729
+    recs.clear();
+    st = RunStats{};
+    if (theta_hist) ACCO_CUDA(cudaMalloc(&hist_dev_, static_cast<size_t>(T) * 2 * psi_ * model_->act_bytes()));
+    try {
+        if (method_ == kACCO)
+            run_acco(T, recs, st);
+        else
+            run_sync(T, recs, st);
+        if (theta_hist) fetch_history(T, theta_hist);
+    } catch (...) {
+        if (hist_dev_) cudaFree(hist_dev_);
+        hist_dev_ = nullptr;
+        throw;
+    }
+    if (hist_dev_) cudaFree(hist_dev_);
+    hist_dev_ = nullptr;
+}
+
+// after the commit of update t (comm stream): copy theta^(t+1), theta-tilde^(t+1)
+void Trainer::snapshot(int t) {
+    if (!hist_dev_) return;
+    const size_t bytes = static_cast<size_t>(psi_) * model_->act_bytes();
+    char* dst = hist_dev_ + static_cast<size_t>(t) * 2 * bytes;
+    ACCO_CUDA(cudaMemcpyAsync(dst, theta_act_, bytes, cudaMemcpyDeviceToDevice, ms_));
+    ACCO_CUDA(cudaMemcpyAsync(dst + bytes, method_ == kACCO ? est_act_ : theta_act_, bytes,
+                              cudaMemcpyDeviceToDevice, ms_));
+}
+
+void Trainer::fetch_history(int T, float* host) {
+    const size_t n = static_cast<size_t>(T) * 2 * psi_;
+    if (model_->act_dtype() == 0) {
+        ACCO_CUDA(cudaMemcpy(host, hist_dev_, n * 4, cudaMemcpyDeviceToHost));
+        return;
+    }
+    std::vector<uint16_t> tmp(n);
+    ACCO_CUDA(cudaMemcpy(tmp.data(), hist_dev_, n * 2, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t u = static_cast<uint32_t>(tmp[i]) << 16;
+        std::memcpy(&host[i], &u, 4);
+    }
+}
+
+namespace {
+
+// comm busy time not covered by compute busy time (SURVEY.md §8d "exposed comm")
+double exposed(const std::vector<std::pair<double, double>>& comm, std::vector<std::pair<double, double>> comp,
+               double* comm_busy, double* comp_busy) {
+    std::sort(comp.begin(), comp.end());
+    std::vector<std::pair<double, double>> u;
+    for (auto& iv : comp) {
+        if (!u.empty() && iv.first <= u.back().second)
+            u.back().second = std::max(u.back().second, iv.second);
+        else
+            u.push_back(iv);
+    }
+    double cb = 0, xb = 0, ex = 0;
+    for (auto& iv : u) xb += iv.second - iv.first;
+    for (auto& c : comm) {
+        const double len = c.second - c.first;
+        cb += len;
+        double cov = 0;
+        for (auto& iv : u) cov += std::max(0.0, std::min(c.second, iv.second) - std::max(c.first, iv.first));
+        ex += std::max(0.0, len - cov);
+    }
+    *comm_busy = cb;
+    *comp_busy = xb;
+    return ex;
+}
+
+}  // namespace
+
+void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
+    const int NP = 2 * T;
+    const int nl = n_local_;
+    const int B = sim_.batch_size;
+    const int nacc = static_cast<int>(acc_.size()) / nl;
+    PhaseEvents ev;
+    ev.n_local = nl;
+    ev.post.create(static_cast<size_t>(NP) * nl);
+    ev.stage_start.create(static_cast<size_t>(NP) * nl);
+    ev.start.create(NP);
+    ev.rs_done.create(NP);
+    ev.opt_done.create(NP);
+    ev.done.create(NP);
+    ev.mb.create(4);
+    ev.counts.assign(static_cast<size_t>(NP) * nl, 0);
+    int64_t* tot = nullptr;
+    ACCO_CUDA(cudaMalloc(&tot, NP * sizeof(int64_t)));
+    const bool do_eval = sim_.eval_every > 0;
+    const int n_eval_chunks = do_eval ? ceil_div(model_->cfg().n_samples,
+                                                  sim_.eval_batch > 0 ? std::min(sim_.eval_batch, model_->cfg().max_batch)
+                                                                      : model_->cfg().max_batch)
+                                      : 0;
+    double* eval_buf = nullptr;  // [T][2 (theta, est)][n_chunks + 1 (gsq)]
+    if (do_eval) ACCO_CUDA(cudaMalloc(&eval_buf, static_cast<size_t>(T) * 2 * (n_eval_chunks + 1) * sizeof(double)));
+    std::vector<int> mb_phase;  // phase of each micro-batch's loss slot
+    std::vector<int> stage_len_rec(static_cast<size_t>(NP) * nl, 0);
+    const long long mb0 = mb_counter_;
+    cudaEvent_t base;
+    ACCO_CUDA(cudaEventCreate(&base));
+    ACCO_CUDA(cudaEventRecord(base, cs_));
+    ACCO_CUDA(cudaStreamWaitEvent(ms_, base, 0));
+    const uint64_t r0 = static_cast<uint64_t>(update_);
+    for (int p = 0; p < NP; ++p) {
+        for (int w = 0; w < nl; ++w) {
+            // stage p computes at the parameters of phase p-2 and reuses its accumulator
+            if (p >= 2) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[p - 2], 0));
+            ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(p) * nl + w], cs_));
+            float* acc = acc_[static_cast<size_t>(w) * nacc + p % nacc];
+            ACCO_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(psi_) * 4, cs_));
+            const void* params;
+            uint64_t round, tag;
+            if (p == 0) {
+                params = theta_act_, round = r0, tag = kTagInit;
+            } else if (p % 2 == 1) {
+                params = theta_act_, round = r0 + static_cast<uint64_t>((p - 1) / 2), tag = kTagMain;
+            } else {
+                params = est_act_, round = r0 + static_cast<uint64_t>(p / 2), tag = kTagEstimate;
+            }
+            int k = 0;
+            const bool adaptive = sim_.schedule == kAdaptive && p >= 1;
+            const int target = stage_len(p, w, T);
+            while (true) {
+                if (!adaptive && k >= target) break;
+                if (adaptive && k >= target) {
+                    // floor met: hand off as soon as phase p-1 has completed
+                    // (protocols.cpp:566-573); bounded lookahead of 2 micro-batches
+                    ACCO_CUDA(cudaEventSynchronize(ev.mb[(k + 2) % 4]));
+                    if (cudaEventQuery(ev.done[p - 1]) == cudaSuccess) break;
+                }
+                const int slot = static_cast<int>(mb_counter_ % loss_cap_);
+                micro(w, params, round, tag, k, acc, loss_ring_ + slot);
+                ACCO_CUDA(cudaEventRecord(ev.mb[k % 4], cs_));
+                mb_phase.push_back(p);
+                ++mb_counter_;
+                ++k;
+            }
+            stage_len_rec[static_cast<size_t>(p) * nl + w] = k;
+            ev.counts[static_cast<size_t>(p) * nl + w] = static_cast<long long>(k) * B;
+            ACCO_CUDA(cudaEventRecord(ev.post[static_cast<size_t>(p) * nl + w], cs_));
+        }
+        launch_phase(p, 0, tot, ev);
+        if (p % 2 == 1) snapshot((p - 1) / 2);
+        if (do_eval && p % 2 == 1) {
+            const int t = (p - 1) / 2;
+            if ((static_cast<long long>(update_) + t + 1) % sim_.eval_every == 0) {
+                ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[p], 0));
+                double* e0 = eval_buf + static_cast<size_t>(t) * 2 * (n_eval_chunks + 1);
+                eval(theta_act_, e0, e0 + n_eval_chunks);
+                eval(est_act_, e0 + n_eval_chunks + 1, e0 + 2 * n_eval_chunks + 1);
+            }
+        }
+    }
+    ACCO_CUDA(cudaStreamSynchronize(ms_));
+    ACCO_CUDA(cudaStreamSynchronize(cs_));
+
+    // ---- gather results
+    std::vector<int64_t> tot_h(NP);
+    ACCO_CUDA(cudaMemcpy(tot_h.data(), tot, NP * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    const long long nmb = mb_counter_ - mb0;
+    ACCO_REQUIRE(nmb <= loss_cap_, "loss ring overflow: run fewer updates per call");
+    std::vector<double> ring(static_cast<size_t>(loss_cap_));
+    ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double> phase_loss(NP, 0.0);
+    for (long long i = 0; i < nmb; ++i)
+        phase_loss[static_cast<size_t>(mb_phase[static_cast<size_t>(i)])] += ring[static_cast<size_t>((mb0 + i) % loss_cap_)];
+    std::vector<double> evh;
+    if (do_eval) {
+        evh.resize(static_cast<size_t>(T) * 2 * (n_eval_chunks + 1));
+        ACCO_CUDA(cudaMemcpy(evh.data(), eval_buf, evh.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    int flag = 0;
+    ACCO_CUDA(cudaMemcpy(&flag, flag_, sizeof(int), cudaMemcpyDeviceToHost));
+    st.diverged = flag;
+    const int n = model_->cfg().n_samples;
+    for (int t = 0; t < T; ++t) {
+        UpdateRecord r;
+        r.update = static_cast<int>(update_) + t;
+        r.time_s = elapsed(base, ev.done[2 * t + 1]) * 1e-3;
+        const long long comb = tot_h[2 * t] + tot_h[2 * t + 1];
+        samples_cum_ += comb;
+        r.samples_cum = samples_cum_;
+        long long local = 0;
+        for (int w = 0; w < nl; ++w) {
+            r.mb_estimate.push_back(stage_len_rec[static_cast<size_t>(2 * t) * nl + w]);
+            r.mb_main.push_back(stage_len_rec[static_cast<size_t>(2 * t + 1) * nl + w]);
+            local += ev.counts[static_cast<size_t>(2 * t) * nl + w] + ev.counts[static_cast<size_t>(2 * t + 1) * nl + w];
+        }
+        r.train_loss = (phase_loss[2 * t] + phase_loss[2 * t + 1]) / static_cast<double>(local);
+        if (do_eval && (update_ + t + 1) % sim_.eval_every == 0) {
+            const double* e0 = evh.data() + static_cast<size_t>(t) * 2 * (n_eval_chunks + 1);
+            double l0 = 0, l1 = 0;
+            for (int c = 0; c < n_eval_chunks; ++c) {
+                l0 += e0[c];
+                l1 += e0[n_eval_chunks + 1 + c];
+            }
+            r.loss = l0 / n;
+            r.grad_sq = e0[n_eval_chunks];
+            r.grad_sq_estimate = e0[2 * n_eval_chunks + 1];
+        }
+        st.consumed += comb / B;
+        recs.push_back(r);
+    }
+    st.issued = nmb;
+    // timeline: comm phases vs compute stages
+    std::vector<std::pair<double, double>> comm_iv, comp_iv;
+    for (int p = 0; p < NP; ++p) {
+        comm_iv.emplace_back(elapsed(base, ev.start[p]), elapsed(base, ev.done[p]));
+        st.opt_ms += elapsed(ev.rs_done[p], ev.opt_done[p]);
+        for (int w = 0; w < nl; ++w)
+            comp_iv.emplace_back(elapsed(base, ev.stage_start[static_cast<size_t>(p) * nl + w]),
+                                 elapsed(base, ev.post[static_cast<size_t>(p) * nl + w]));
+    }
+    st.opt_launches = NP;
+    st.comm_exposed_ms = exposed(comm_iv, comp_iv, &st.comm_busy_ms, &st.compute_busy_ms);
+    st.wall_ms = elapsed(base, ev.done[NP - 1]);
+    update_ += T;
+    cudaEventDestroy(base);
+    cudaFree(tot);
+    if (eval_buf) cudaFree(eval_buf);
+}
+
+void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
+    const int nl = n_local_;
+    const int B = sim_.batch_size;
+    const int k = sim_.n_grad_accumulation;
+    PhaseEvents ev;
+    ev.n_local = nl;
+    ev.post.create(static_cast<size_t>(T) * nl);
+    ev.stage_start.create(static_cast<size_t>(T) * nl);
+    ev.start.create(T);
+    ev.rs_done.create(T);
+    ev.opt_done.create(T);
+    ev.done.create(T);
+    ev.counts.assign(static_cast<size_t>(T) * nl, 0);
+    int64_t* tot = nullptr;
+    ACCO_CUDA(cudaMalloc(&tot, T * sizeof(int64_t)));
+    const bool do_eval = sim_.eval_every > 0;
+    const int n_eval_chunks = do_eval ? ceil_div(model_->cfg().n_samples,
+                                                  sim_.eval_batch > 0 ? std::min(sim_.eval_batch, model_->cfg().max_batch)
+                                                                      : model_->cfg().max_batch)
+                                      : 0;
+    double* eval_buf = nullptr;
+    if (do_eval) ACCO_CUDA(cudaMalloc(&eval_buf, static_cast<size_t>(T) * (n_eval_chunks + 1) * sizeof(double)));
+    std::vector<int> mb_round;
+    const long long mb0 = mb_counter_;
+    cudaEvent_t base;
+    ACCO_CUDA(cudaEventCreate(&base));
+    ACCO_CUDA(cudaEventRecord(base, cs_));
+    ACCO_CUDA(cudaStreamWaitEvent(ms_, base, 0));
+    for (int r = 0; r < T; ++r) {
+        const uint64_t round = static_cast<uint64_t>(update_ + r);
+        for (int w = 0; w < nl; ++w) {
+            if (r >= 1) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r - 1], 0));
+            ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(r) * nl + w], cs_));
+            float* acc = acc_[static_cast<size_t>(w)];
+            ACCO_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(psi_) * 4, cs_));
+            for (int j = 0; j < k; ++j) {
+                const int slot = static_cast<int>(mb_counter_ % loss_cap_);
+                micro(w, theta_act_, round, kTagMain, j, acc, loss_ring_ + slot);
+                mb_round.push_back(r);
+                ++mb_counter_;
+            }
+            ev.counts[static_cast<size_t>(r) * nl + w] = static_cast<long long>(k) * B;
+            ACCO_CUDA(cudaEventRecord(ev.post[static_cast<size_t>(r) * nl + w], cs_));
+        }
+        launch_phase(r, 0, tot, ev);
+        snapshot(r);
+        if (do_eval && (update_ + r + 1) % sim_.eval_every == 0) {
+            ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r], 0));
+            double* e0 = eval_buf + static_cast<size_t>(r) * (n_eval_chunks + 1);
+            eval(theta_act_, e0, e0 + n_eval_chunks);
+        }
+    }
+    ACCO_CUDA(cudaStreamSynchronize(ms_));
+    ACCO_CUDA(cudaStreamSynchronize(cs_));
+    std::vector<int64_t> tot_h(T);
+    ACCO_CUDA(cudaMemcpy(tot_h.data(), tot, T * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    const long long nmb = mb_counter_ - mb0;
+    ACCO_REQUIRE(nmb <= loss_cap_, "loss ring overflow: run fewer updates per call");
+    std::vector<double> ring(static_cast<size_t>(loss_cap_));
+    ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    std::vector<double> rl(T, 0.0);
+    for (long long i = 0; i < nmb; ++i)
+        rl[static_cast<size_t>(mb_round[static_cast<size_t>(i)])] += ring[static_cast<size_t>((mb0 + i) % loss_cap_)];
+    std::vector<double> evh;
+    if (do_eval) {
+        evh.resize(static_cast<size_t>(T) * (n_eval_chunks + 1));
+        ACCO_CUDA(cudaMemcpy(evh.data(), eval_buf, evh.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    int flag = 0;
+    ACCO_CUDA(cudaMemcpy(&flag, flag_, sizeof(int), cudaMemcpyDeviceToHost));
+    st.diverged = flag;
+    const int n = model_->cfg().n_samples;
+    for (int r = 0; r < T; ++r) {
+        UpdateRecord rec;
+        rec.update = static_cast<int>(update_) + r;
+        rec.time_s = elapsed(base, ev.done[r]) * 1e-3;
+        samples_cum_ += tot_h[r];
+        rec.samples_cum = samples_cum_;
+        rec.train_loss = rl[r] / static_cast<double>(static_cast<long long>(nl) * k * B);
+        for (int w = 0; w < nl; ++w) {
+            rec.mb_main.push_back(k);
+            rec.mb_estimate.push_back(0);
+        }
+        if (do_eval && (update_ + r + 1) % sim_.eval_every == 0) {
+            const double* e0 = evh.data() + static_cast<size_t>(r) * (n_eval_chunks + 1);
+            double l0 = 0;
+            for (int c = 0; c < n_eval_chunks; ++c) l0 += e0[c];
+            rec.loss = l0 / n;
+            rec.grad_sq = e0[n_eval_chunks];
+            rec.grad_sq_estimate = rec.grad_sq;
+        }
+        st.consumed += tot_h[r] / B;
+        recs.push_back(rec);
+    }
+    st.issued = nmb;
+    std::vector<std::pair<double, double>> comm_iv, comp_iv;
+    for (int r = 0; r < T; ++r) {
+        comm_iv.emplace_back(elapsed(base, ev.start[r]), elapsed(base, ev.done[r]));
+        st.opt_ms += elapsed(ev.rs_done[r], ev.opt_done[r]);
+        for (int w = 0; w < nl; ++w)
+            comp_iv.emplace_back(elapsed(base, ev.stage_start[static_cast<size_t>(r) * nl + w]),
+                                 elapsed(base, ev.post[static_cast<size_t>(r) * nl + w]));
+    }
+    st.opt_launches = T;
+    st.comm_exposed_ms = exposed(comm_iv, comp_iv, &st.comm_busy_ms, &st.compute_busy_ms);
+    st.wall_ms = elapsed(base, ev.done[T - 1]);
+    update_ += T;
+    cudaEventDestroy(base);
+    cudaFree(tot);
+    if (eval_buf) cudaFree(eval_buf);
+}
+
+}  // namespace acco

@@ -1,0 +1,110 @@
+// Trainer engines: ACCO (proj/src/protocols.cpp:437-709) and the DDP
+// (:191-338) / ZeRO-1 baselines, on real CUDA streams instead of the
+// reference's discrete-event clock.
+#pragma once
+
+#include <vector>
+
+#include "comm.h"
+#include "host_util.h"
+#include "model.h"
+#include "optim.h"
+
+namespace acco {
+
+enum Method : int { kDDP = 0, kDPU = 1, kWP = 2, kACCO = 3, kZeRO1 = 4 };
+enum Schedule : int { kFloor = 0, kAdaptive = 1, kReplay = 2 };
+
+struct SimCfg {
+    int n_workers = 1;
+    int batch_size = 1;
+    int n_grad_accumulation = 1;
+    int warmup_rounds = 0;
+    uint64_t master_seed = 1;
+    int schedule = kFloor;
+    std::vector<int32_t> replay;     // [T][2][n_workers] (mb_estimate, mb_main)
+    int eval_every = 0;              // 0: no full-dataset evaluation
+    std::vector<double> throttle_ns; // per worker, extra ns after every micro-batch
+    int eval_batch = 0;              // samples per evaluation chunk (0 = model max)
+};
+
+struct UpdateRecord {
+    int update = 0;
+    double time_s = 0;
+    double loss = NAN, grad_sq = NAN, grad_sq_estimate = NAN, lyapunov = NAN;
+    long long samples_cum = 0;
+    double train_loss = NAN;
+    std::vector<int> mb_main, mb_estimate;  // local workers
+};
+
+struct RunStats {
+    long long issued = 0, consumed = 0, discarded = 0;
+    double wall_ms = 0, compute_busy_ms = 0, comm_busy_ms = 0, comm_exposed_ms = 0;
+    double opt_ms = 0;  // optimizer-kernel time summed over phases (device events)
+    int opt_launches = 0;
+    int diverged = 0;
+};
+
+class Trainer {
+public:
+    Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm);
+    ~Trainer();
+    Trainer(const Trainer&) = delete;
+    Trainer& operator=(const Trainer&) = delete;
+
+    void set_theta(const float* host_theta);
+    void get_theta(int which, float* host_out);
+    // Runs t_updates committed updates, continuing from the current state.
+    // theta_hist (host, nullable): [t_updates][2][psi] fp32 — theta^(t+1) and
+    // theta-tilde^(t+1) after each commit (RunTrace.theta/estimate_history).
+    void run(int t_updates, std::vector<UpdateRecord>& recs, RunStats& st, float* theta_hist = nullptr);
+    int n_local() const { return n_local_; }
+    cudaStream_t compute_stream() const { return cs_; }
+
+private:
+    struct PhaseEvents;
+    void alloc();
+    void launch_phase(int p, int t_base, int64_t* tot, PhaseEvents& ev);
+    void run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st);
+    void run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st);
+    void snapshot(int t);
+    void fetch_history(int T, float* host);
+    char* hist_dev_ = nullptr;
+    int stage_len(int p, int w, int T) const;
+    void micro(int w, const void* params, uint64_t round, uint64_t tag, int ordinal, float* acc, double* loss_slot);
+    void eval(const void* params, double* loss_slots, double* gsq_slot);
+    void* theta_params() const { return theta_act_; }
+    void* est_params() const { return est_act_; }
+
+    GPTModel* model_;
+    OptConfig cfg_;
+    SimCfg sim_;
+    int method_;
+    Comm* comm_;
+    int n_local_ = 1, world_ = 1, rank_ = 0;
+    ShardLayout layout_;
+    int64_t psi_ = 0, chunk_ = 0, own_n_ = 0, own_lo_ = 0;
+    bool padded_ = false;
+    cudaStream_t cs_ = nullptr, ms_ = nullptr;  // compute, comm
+    // device state
+    void* theta_act_ = nullptr;  // flat replica of theta (activation dtype)
+    void* est_act_ = nullptr;    // flat replica of theta-tilde
+    void* ag_theta_ = nullptr;   // padded all-gather buffers (== flat when not padded)
+    void* ag_est_ = nullptr;
+    float *master_ = nullptr, *m_ = nullptr, *v_ = nullptr;
+    std::vector<float*> acc_;  // [n_local][2]
+    float* pad_send_ = nullptr;
+    float *g_ret_ = nullptr, *g_main_ = nullptr, *full_red_ = nullptr;
+    int64_t* cnt_send_ = nullptr;
+    int* flag_ = nullptr;
+    double* loss_ring_ = nullptr;
+    int loss_cap_ = 0;
+    float* eval_grad_ = nullptr;
+    double* eval_scratch_ = nullptr;
+    long long step_ = 0;   // optimizer step (OptimizerState::step), shared by all shards
+    long long update_ = 0; // committed updates so far (continues across run() calls)
+    long long samples_cum_ = 0;
+    long long mb_counter_ = 0;
+};
+
+}  // namespace acco

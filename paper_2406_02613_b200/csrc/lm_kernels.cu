@@ -1,0 +1,537 @@
+// LM element-wise / normalisation / loss kernels and engine utilities.
+// See lm_kernels.h. The LM definition is oracle/gpt_oracle.py's.
+#include "epilogue.cuh"
+#include "host_util.h"
+#include "lm_kernels.h"
+
+#include <vector>
+
+namespace acco {
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ----------------------------------------------------------------- tokens
+__global__ void gather_tokens_kernel(const int32_t* __restrict__ data, int seq, int n_samples,
+                                     uint64_t seed, int mode, int start, int32_t* tok_in,
+                                     int32_t* tok_out, int32_t* idx_out) {
+    const int b = blockIdx.x;
+    int idx;
+    if (mode == 0)
+        idx = static_cast<int>(stream_draw(seed, static_cast<uint64_t>(b)) % static_cast<uint64_t>(n_samples));
+    else
+        idx = start + b;
+    if (threadIdx.x == 0 && idx_out) idx_out[b] = idx;
+    const int32_t* row = data + static_cast<int64_t>(idx) * (seq + 1);
+    for (int t = threadIdx.x; t < seq; t += blockDim.x) {
+        tok_in[b * seq + t] = row[t];
+        tok_out[b * seq + t] = row[t + 1];
+    }
+}
+
+// ----------------------------------------------------------------- embedding
+template <class T>
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ wte,
+                                 const T* __restrict__ wpe, T* __restrict__ x, int seq, int d) {
+    const int m = blockIdx.x;
+    const int t = m % seq;
+    const T* e = wte + static_cast<int64_t>(tok[m]) * d;
+    const T* p = wpe + static_cast<int64_t>(t) * d;
+    T* o = x + static_cast<int64_t>(m) * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = from_f<T>(to_f(e[c]) + to_f(p[c]));
+}
+
+// ----------------------------------------------------------------- layernorm
+constexpr float kLnEps = 1e-5f;
+
+template <class T>
+__global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+                              T* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd,
+                              int M, int d) {
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const T* xr = x + static_cast<int64_t>(row) * d;
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s += to_f(xr[c]);
+    const float mu = warp_sum(s) / d;
+    float v = 0.f;
+    for (int c = lane; c < d; c += 32) {
+        float t = to_f(xr[c]) - mu;
+        v += t * t;
+    }
+    const float rs = rsqrtf(warp_sum(v) / d + kLnEps);
+    T* yr = y + static_cast<int64_t>(row) * d;
+    for (int c = lane; c < d; c += 32)
+        yr[c] = from_f<T>((to_f(xr[c]) - mu) * rs * to_f(g[c]) + to_f(b[c]));
+    if (lane == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+    }
+}
+
+template <class T>
+__global__ void ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ g,
+                              const float* __restrict__ mean, const float* __restrict__ rstd,
+                              T* __restrict__ dx, int accumulate, int M, int d) {
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const int64_t o = static_cast<int64_t>(row) * d;
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane; c < d; c += 32) {
+        float xh = (to_f(x[o + c]) - mu) * rs;
+        float dxh = to_f(dy[o + c]) * to_f(g[c]);
+        s1 += dxh;
+        s2 += dxh * xh;
+    }
+    s1 = warp_sum(s1) / d;
+    s2 = warp_sum(s2) / d;
+    for (int c = lane; c < d; c += 32) {
+        float xh = (to_f(x[o + c]) - mu) * rs;
+        float dxh = to_f(dy[o + c]) * to_f(g[c]);
+        float v = rs * (dxh - s1 - xh * s2);
+        if (accumulate) v += to_f(dx[o + c]);
+        dx[o + c] = from_f<T>(v);
+    }
+}
+
+// ------------------------------------------------ deterministic column reduce
+// partial[chunk][col] = sum over rows of the chunk (fixed order), then
+// out[col] += sum_chunk partial[chunk][col] (fixed order).
+constexpr int kColRows = 8;  // row lanes per block
+constexpr int kColChunk = 256;
+
+// F(row, col) -> float (two outputs for LN: dy*xhat and dy)
+template <class T, int KIND>
+__global__ void colreduce_partial(const T* __restrict__ y, int64_t ld, const T* __restrict__ x,
+                                  const float* __restrict__ mean, const float* __restrict__ rstd,
+                                  int M, int N, float* __restrict__ part0, float* __restrict__ part1) {
+    __shared__ float s0[kColRows][33], s1[kColRows][33];
+    const int col = blockIdx.x * 32 + threadIdx.x;
+    const int chunk = blockIdx.y;
+    const int r0 = chunk * kColChunk;
+    const int r1 = min(M, r0 + kColChunk);
+    float a0 = 0.f, a1 = 0.f;
+    if (col < N) {
+        for (int r = r0 + threadIdx.y; r < r1; r += kColRows) {
+            float dy = to_f(y[static_cast<int64_t>(r) * ld + col]);
+            if (KIND == 0) {
+                a0 += dy;
+            } else {
+                float xh = (to_f(x[static_cast<int64_t>(r) * N + col]) - mean[r]) * rstd[r];
+                a0 += dy * xh;
+                a1 += dy;
+            }
+        }
+    }
+    s0[threadIdx.y][threadIdx.x] = a0;
+    s1[threadIdx.y][threadIdx.x] = a1;
+    __syncthreads();
+    if (threadIdx.y == 0 && col < N) {
+        float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kColRows; ++i) {
+            t0 += s0[i][threadIdx.x];
+            t1 += s1[i][threadIdx.x];
+        }
+        part0[static_cast<int64_t>(chunk) * N + col] = t0;
+        if (KIND == 1) part1[static_cast<int64_t>(chunk) * N + col] = t1;
+    }
+}
+
+__global__ void colreduce_final(const float* __restrict__ part, int nchunk, int N, float* __restrict__ out) {
+    const int col = blockIdx.x * blockDim.x + threadIdx.x;
+    if (col >= N) return;
+    float t = 0.f;
+    for (int c = 0; c < nchunk; ++c) t += part[static_cast<int64_t>(c) * N + col];
+    out[col] += t;
+}
+
+// ------------------------------------------------------------- cross entropy
+template <class T>
+__global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, int64_t ld,
+                                                 const int32_t* __restrict__ target, int V, float inv_seq,
+                                                 float* __restrict__ row_loss) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    T* L = logits + static_cast<int64_t>(row) * ld;
+    // pass 1: online max / sum-exp per thread
+    float m = -INFINITY, s = 0.f;
+    for (int c = threadIdx.x; c < V; c += blockDim.x) {
+        float v = to_f(L[c]);
+        if (v > m) {
+            s = s * expf(m - v) + 1.f;
+            m = v;
+        } else {
+            s += expf(v - m);
+        }
+    }
+    // block reduce (max, then rescaled sums)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    float wm = warp_max(m);
+    if (lane == 0) red[wid] = wm;
+    __syncthreads();
+    float gm = -INFINITY;
+    for (int i = 0; i < nw; ++i) gm = fmaxf(gm, red[i]);
+    __syncthreads();
+    float ls = (m == -INFINITY) ? 0.f : s * expf(m - gm);
+    ls = warp_sum(ls);
+    if (lane == 0) red[wid] = ls;
+    __syncthreads();
+    float tot = 0.f;
+    for (int i = 0; i < nw; ++i) tot += red[i];
+    const float lse = gm + logf(tot);
+    const int tgt = target[row];
+    if (threadIdx.x == 0) row_loss[row] = lse - to_f(L[tgt]);
+    __syncthreads();
+    // pass 2: dlogits
+    for (int c = threadIdx.x; c < V; c += blockDim.x) {
+        float p = expf(to_f(L[c]) - lse);
+        if (c == tgt) p -= 1.f;
+        L[c] = from_f<T>(p * inv_seq);
+    }
+}
+
+__global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int M, int seq, double* out) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < M; i += blockDim.x) s += row_loss[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = red[0] / seq;
+}
+
+// --------------------------------------------------------- embedding backward
+// single-CTA bitonic sort of keys (tok * M + m): stable grouping by token with
+// ascending positions inside each group.
+__global__ void sort_keys_kernel(const int32_t* __restrict__ tok, int M, int P, uint32_t* out) {
+    extern __shared__ uint32_t keys[];
+    for (int i = threadIdx.x; i < P; i += blockDim.x)
+        keys[i] = i < M ? static_cast<uint32_t>(tok[i]) * static_cast<uint32_t>(M) + i : 0xffffffffu;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    uint32_t a = keys[i], b = keys[ixj];
+                    bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < M; i += blockDim.x) out[i] = keys[i];
+}
+
+template <class T>
+__global__ void embed_bwd_wte_kernel(const uint32_t* __restrict__ sorted, int M, const T* __restrict__ dx,
+                                     int d, float* __restrict__ grad_wte) {
+    const int i = blockIdx.x;
+    const uint32_t tok = sorted[i] / static_cast<uint32_t>(M);
+    if (i > 0 && sorted[i - 1] / static_cast<uint32_t>(M) == tok) return;  // not a segment start
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float acc = 0.f;
+        for (int j = i; j < M && sorted[j] / static_cast<uint32_t>(M) == tok; ++j) {
+            const int m = static_cast<int>(sorted[j] % static_cast<uint32_t>(M));
+            acc += to_f(dx[static_cast<int64_t>(m) * d + c]);
+        }
+        grad_wte[static_cast<int64_t>(tok) * d + c] += acc;
+    }
+}
+
+template <class T>
+__global__ void embed_bwd_wpe_kernel(const T* __restrict__ dx, int B, int seq, int d, float* __restrict__ grad_wpe) {
+    const int t = blockIdx.x;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float acc = 0.f;
+        for (int b = 0; b < B; ++b) acc += to_f(dx[(static_cast<int64_t>(b) * seq + t) * d + c]);
+        grad_wpe[static_cast<int64_t>(t) * d + c] += acc;
+    }
+}
+
+// ------------------------------------------------------------------ utilities
+__global__ void fill_i64_kernel(int64_t* p, int64_t v) { *p = v; }
+__global__ void add_i64_kernel(int64_t* dst, const int64_t* a, const int64_t* b) { *dst = *a + *b; }
+
+struct PtrList {
+    const float* p[16];
+};
+
+__global__ void sum_ordered_kernel(PtrList in, int nin, float* __restrict__ out, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        float s = in.p[0][i];
+        for (int w = 1; w < nin; ++w) s += in.p[w][i];
+        out[i] = s;
+    }
+}
+
+template <class T>
+__global__ void f32_to_kernel(const float* __restrict__ src, T* __restrict__ dst, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = from_f<T>(src[i]);
+}
+
+__global__ void scale_kernel(float* x, float a, int64_t n) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) x[i] *= a;
+}
+
+__global__ void norm_sq_partial(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+    __shared__ double red[256];
+    double s = 0.0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double v = x[i];
+        s += v * v;
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void norm_sq_final(const double* __restrict__ part, int nb, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < nb; ++i) s += part[i];
+        *out = s;
+    }
+}
+
+struct Ranges {
+    uint64_t lo[64];
+    uint64_t sz[64];
+};
+
+__global__ void pack_kernel(const float* __restrict__ flat, float* __restrict__ padded, Ranges r, int n,
+                            uint64_t chunk) {
+    const uint64_t total = chunk * n;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int w = static_cast<int>(i / chunk);
+        const uint64_t j = i % chunk;
+        padded[i] = j < r.sz[w] ? flat[r.lo[w] + j] : 0.f;
+    }
+}
+
+template <class E>
+__global__ void unpack_kernel(const E* __restrict__ padded, E* __restrict__ flat, Ranges r, int n,
+                              uint64_t chunk) {
+    const uint64_t total = chunk * n;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int w = static_cast<int>(i / chunk);
+        const uint64_t j = i % chunk;
+        if (j < r.sz[w]) flat[r.lo[w] + j] = padded[i];
+    }
+}
+
+__global__ void spin_kernel(uint64_t ns) {
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint64_t t = t0;
+    while (t - t0 < ns) {
+        __nanosleep(1000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    }
+}
+
+int grid_for(int64_t n, int threads = 256) {
+    int64_t b = (n + threads - 1) / threads;
+    int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+    return static_cast<int>(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+// =================================================================== launchers
+void gather_tokens(const int32_t* data, int seq, int n_samples, uint64_t seed, int mode, int start, int B,
+                   int32_t* tok_in, int32_t* tok_out, int32_t* idx_out, cudaStream_t s) {
+    gather_tokens_kernel<<<B, 128, 0, s>>>(data, seq, n_samples, seed, mode, start, tok_in, tok_out, idx_out);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int seq, int d, cudaStream_t s) {
+    embed_fwd_kernel<T><<<M, 128, 0, s>>>(tok, wte, wpe, x, seq, d);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
+                   cudaStream_t s) {
+    ln_fwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(x, g, b, y, mean, rstd, M, d);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
+                   bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d, cudaStream_t s) {
+    // parameter gradients first (they read dy only), then dx
+    const int nchunk = ceil_div(M, kColChunk);
+    float* p0 = scratch;
+    float* p1 = scratch + static_cast<int64_t>(nchunk) * d;
+    colreduce_partial<T, 1><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd, M,
+                                                                                         d, p0, p1);
+    ACCO_CHECK_LAUNCH();
+    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p0, nchunk, d, gdst);
+    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst);
+    ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, cudaStream_t s) {
+    const int nchunk = ceil_div(M, kColChunk);
+    colreduce_partial<T, 0><<<dim3(ceil_div(N, 32), nchunk), dim3(32, kColRows), 0, s>>>(
+        y, ld, nullptr, nullptr, nullptr, M, N, scratch, nullptr);
+    ACCO_CHECK_LAUNCH();
+    colreduce_final<<<ceil_div(N, 256), 256, 0, s>>>(scratch, nchunk, N, out);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, int seq, float* row_loss,
+                   cudaStream_t s) {
+    ce_kernel<T><<<M, 512, 0, s>>>(logits, ld, target, V, 1.0f / seq, row_loss);
+    ACCO_CHECK_LAUNCH();
+}
+
+void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s) {
+    loss_reduce_kernel<<<1, 256, 0, s>>>(row_loss, M, seq, out);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
+               uint32_t* sort_scratch, cudaStream_t s) {
+    ACCO_REQUIRE(static_cast<uint64_t>(V) * static_cast<uint64_t>(M) < 0xffffffffull,
+                 "embed_bwd: vocab * tokens exceeds the 32-bit sort key");
+    int P = 1;
+    while (P < M) P <<= 1;
+    ACCO_REQUIRE(P * 4 <= 200 * 1024, "embed_bwd: micro-batch too large for the single-CTA sort");
+    static bool configured = false;
+    if (!configured) {
+        ACCO_CUDA(cudaFuncSetAttribute(sort_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        configured = true;
+    }
+    sort_keys_kernel<<<1, 1024, P * 4, s>>>(tok, M, P, sort_scratch);
+    ACCO_CHECK_LAUNCH();
+    embed_bwd_wte_kernel<T><<<M, 128, 0, s>>>(sort_scratch, M, dx, d, grad_wte);
+    ACCO_CHECK_LAUNCH();
+    embed_bwd_wpe_kernel<T><<<seq, 128, 0, s>>>(dx, M / seq, seq, d, grad_wpe);
+    ACCO_CHECK_LAUNCH();
+}
+
+void fill_i64(int64_t* p, int64_t v, cudaStream_t s) {
+    fill_i64_kernel<<<1, 1, 0, s>>>(p, v);
+    ACCO_CHECK_LAUNCH();
+}
+
+void add_i64(int64_t* dst, const int64_t* a, const int64_t* b, cudaStream_t s) {
+    add_i64_kernel<<<1, 1, 0, s>>>(dst, a, b);
+    ACCO_CHECK_LAUNCH();
+}
+
+void sum_ordered(const float* const* in, int nin, float* out, int64_t n, cudaStream_t s) {
+    ACCO_REQUIRE(nin >= 1 && nin <= 16, "sum_ordered: 1..16 inputs");
+    PtrList l{};
+    for (int i = 0; i < nin; ++i) l.p[i] = in[i];
+    sum_ordered_kernel<<<grid_for(n), 256, 0, s>>>(l, nin, out, n);
+    ACCO_CHECK_LAUNCH();
+}
+
+void f32_to(const float* src, void* dst, int dtype, int64_t n, cudaStream_t s) {
+    if (dtype == 1)
+        f32_to_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+    else
+        f32_to_kernel<float><<<grid_for(n), 256, 0, s>>>(src, static_cast<float*>(dst), n);
+    ACCO_CHECK_LAUNCH();
+}
+
+void scale_f32(float* x, double alpha, int64_t n, cudaStream_t s) {
+    scale_kernel<<<grid_for(n), 256, 0, s>>>(x, static_cast<float>(alpha), n);
+    ACCO_CHECK_LAUNCH();
+}
+
+void norm_sq(const float* x, int64_t n, double* out, double* scratch, cudaStream_t s) {
+    const int nb = 256;
+    norm_sq_partial<<<nb, 256, 0, s>>>(x, n, scratch);
+    norm_sq_final<<<1, 32, 0, s>>>(scratch, nb, out);
+    ACCO_CHECK_LAUNCH();
+}
+
+static Ranges make_ranges(const uint64_t* lo, const uint64_t* sz, int n) {
+    ACCO_REQUIRE(n >= 1 && n <= 64, "padded layout: 1..64 workers");
+    Ranges r{};
+    for (int i = 0; i < n; ++i) {
+        r.lo[i] = lo[i];
+        r.sz[i] = sz[i];
+    }
+    return r;
+}
+
+void pack_padded(const float* flat, float* padded, const uint64_t* lo, const uint64_t* sz, int n, uint64_t chunk,
+                 cudaStream_t s) {
+    pack_kernel<<<grid_for(static_cast<int64_t>(chunk * n)), 256, 0, s>>>(flat, padded, make_ranges(lo, sz, n), n,
+                                                                          chunk);
+    ACCO_CHECK_LAUNCH();
+}
+
+void unpack_padded(const void* padded, void* flat, int elem_bytes, const uint64_t* lo, const uint64_t* sz, int n,
+                   uint64_t chunk, cudaStream_t s) {
+    Ranges r = make_ranges(lo, sz, n);
+    const int g = grid_for(static_cast<int64_t>(chunk * n));
+    if (elem_bytes == 4)
+        unpack_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(padded), static_cast<float*>(flat), r, n, chunk);
+    else
+        unpack_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(padded),
+                                                        static_cast<__nv_bfloat16*>(flat), r, n, chunk);
+    ACCO_CHECK_LAUNCH();
+}
+
+void spin_ns(uint64_t ns, cudaStream_t s) {
+    if (ns == 0) return;
+    spin_kernel<<<1, 1, 0, s>>>(ns);
+    ACCO_CHECK_LAUNCH();
+}
+
+#define ACCO_INST(T)                                                                                          \
+    template void embed_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);          \
+    template void layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, cudaStream_t); \
+    template void layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, float*, \
+                                   float*, float*, int, int, cudaStream_t);                                   \
+    template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, cudaStream_t);                   \
+    template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
+    template void embed_bwd<T>(const int32_t*, const T*, int, int, int, int, float*, float*, uint32_t*,      \
+                               cudaStream_t);
+ACCO_INST(float)
+ACCO_INST(__nv_bfloat16)
+#undef ACCO_INST
+
+}  // namespace acco

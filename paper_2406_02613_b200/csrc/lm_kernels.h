@@ -1,0 +1,73 @@
+// Non-GEMM kernels of the LM plugin (K2 of SURVEY.md §2.3) and the small
+// device utilities of the engine. Activation dtype T is float (parity mode)
+// or __nv_bfloat16 (throughput mode); all arithmetic is fp32; every reduction
+// is order-fixed (no float atomics) so runs are bitwise deterministic, like
+// the reference's fixed-order folds (proj/src/problems.cpp:92-131).
+#pragma once
+
+#include "common.cuh"
+
+namespace acco {
+
+// tokens of a micro-batch: mode 0 = B indices Stream(seed).below(n_samples)
+// (problems.cpp:442-444); mode 1 = contiguous samples [start, start+B).
+void gather_tokens(const int32_t* data, int seq, int n_samples, uint64_t seed, int mode, int start,
+                   int B, int32_t* tok_in, int32_t* tok_out, int32_t* idx_out, cudaStream_t s);
+
+template <class T>
+void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int seq, int d,
+               cudaStream_t s);
+
+template <class T>
+void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
+                   cudaStream_t s);
+
+// dx (+)= LN backward of dy; dg/db gradients added into fp32 gdst/bdst.
+template <class T>
+void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd,
+                   T* dx, bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d,
+                   cudaStream_t s);
+
+// out[c] += sum_r y[r*ld + c] (deterministic two-level), fp32 out.
+template <class T>
+void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, cudaStream_t s);
+
+// In place: logits[M, ld] -> dlogits = (softmax - onehot(target)) / seq;
+// row_loss[m] = logsumexp - logit[target].
+template <class T>
+void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, int seq,
+                   float* row_loss, cudaStream_t s);
+
+// out[slot] = sum over rows of row_loss / seq (fixed order) = sum of sample losses.
+void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s);
+
+// Embedding backward: grad_wte[tok[m]] += dx[m] (sorted segments, ascending m),
+// grad_wpe[t] += sum_b dx[b*seq + t].
+template <class T>
+void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte,
+               float* grad_wpe, uint32_t* sort_scratch, cudaStream_t s);
+
+template <class T>
+void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd, cudaStream_t s);
+template <class T>
+void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, float* dsum,
+                   int B, int seq, int H, int hd, cudaStream_t s);
+
+// ---- engine utilities
+void fill_i64(int64_t* p, int64_t v, cudaStream_t s);
+void add_i64(int64_t* dst, const int64_t* a, const int64_t* b, cudaStream_t s);
+// out = sum_w in[w] in ascending w (the Fabric's fixed order), n floats each.
+void sum_ordered(const float* const* in, int nin, float* out, int64_t n, cudaStream_t s);
+void f32_to(const float* src, void* dst, int dtype, int64_t n, cudaStream_t s);
+void scale_f32(float* x, double alpha, int64_t n, cudaStream_t s);
+// out = sum x^2 in a fixed order (double accumulation).
+void norm_sq(const float* x, int64_t n, double* out, double* scratch, cudaStream_t s);
+// owner-padded layout: padded[w*chunk + j] <-> flat[lo_w + j]
+void pack_padded(const float* flat, float* padded, const uint64_t* lo, const uint64_t* sz, int n,
+                 uint64_t chunk, cudaStream_t s);
+void unpack_padded(const void* padded, void* flat, int elem_bytes, const uint64_t* lo,
+                   const uint64_t* sz, int n, uint64_t chunk, cudaStream_t s);
+// straggler throttle (HeterogeneityProfile, protocols.hpp:19-27): spin ns on the stream
+void spin_ns(uint64_t ns, cudaStream_t s);
+
+}  // namespace acco

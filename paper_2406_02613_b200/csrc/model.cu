@@ -1,0 +1,299 @@
+// GPT-style LM plugin (see model.h). Forward + backward of one micro-batch,
+// accumulating the summed per-sample gradients straight into the fp32
+// gradient-accumulation buffer through the wgrad GEMM epilogues (K3: the
+// reference's Bundle::add, proj/src/protocols.cpp:61-66, has no separate pass).
+#include "gemm.h"
+#include "host_util.h"
+#include "lm_kernels.h"
+#include "model.h"
+
+#include <cmath>
+
+namespace acco {
+
+// ------------------------------------------------------------ host definitions
+std::vector<ParamSpec> lm_param_layout(const LMConfig& c) {
+    const int64_t d = c.d_model;
+    std::vector<ParamSpec> v;
+    auto add = [&](const std::string& n, int64_t r, int64_t cc, int kind) {
+        int64_t off = v.empty() ? 0 : v.back().off + v.back().numel();
+        v.push_back({n, r, cc, kind, off});
+    };
+    add("wte", c.vocab, d, 0);
+    add("wpe", c.seq_len, d, 0);
+    for (int l = 0; l < c.n_layer; ++l) {
+        const std::string p = "h." + std::to_string(l) + ".";
+        add(p + "ln_1.weight", d, 1, 2);
+        add(p + "ln_1.bias", d, 1, 3);
+        add(p + "attn.c_attn.weight", 3 * d, d, 0);
+        add(p + "attn.c_attn.bias", 3 * d, 1, 3);
+        add(p + "attn.c_proj.weight", d, d, 1);
+        add(p + "attn.c_proj.bias", d, 1, 3);
+        add(p + "ln_2.weight", d, 1, 2);
+        add(p + "ln_2.bias", d, 1, 3);
+        add(p + "mlp.c_fc.weight", 4 * d, d, 0);
+        add(p + "mlp.c_fc.bias", 4 * d, 1, 3);
+        add(p + "mlp.c_proj.weight", d, 4 * d, 1);
+        add(p + "mlp.c_proj.bias", d, 1, 3);
+    }
+    add("ln_f.weight", d, 1, 2);
+    add("ln_f.bias", d, 1, 3);
+    return v;
+}
+
+std::vector<int32_t> lm_dataset(const LMConfig& c) {
+    // oracle/gpt_oracle.py dataset(): integer-only Markov chain
+    const uint64_t V = static_cast<uint64_t>(c.vocab);
+    std::vector<int32_t> succ(static_cast<size_t>(V));
+    Stream ss(rng_derive(c.data_seed, 0x5eed, V));
+    for (uint64_t v = 0; v < V; ++v) succ[v] = static_cast<int32_t>(ss.below(V));
+    const int T1 = c.seq_len + 1;
+    std::vector<int32_t> tok(static_cast<size_t>(c.n_samples) * T1);
+    for (int s = 0; s < c.n_samples; ++s) {
+        Stream st(rng_derive(c.data_seed, 0xda7a, static_cast<uint64_t>(s)));
+        uint64_t x = st.below(V);
+        int32_t* row = tok.data() + static_cast<size_t>(s) * T1;
+        row[0] = static_cast<int32_t>(x);
+        for (int t = 1; t < T1; ++t) {
+            uint64_t r = st.next_u64();
+            x = (r & 3) ? static_cast<uint64_t>(succ[x]) : (r >> 2) % V;
+            row[t] = static_cast<int32_t>(x);
+        }
+    }
+    return tok;
+}
+
+void lm_default_theta0(const LMConfig& c, uint64_t master_seed, float* out) {
+    // oracle/gpt_oracle.py default_theta0(): exact arithmetic in fp64
+    const double kSqrt3 = 1.7320508075688772;
+    Stream st(rng_derive(master_seed, 0x7e7a0));
+    for (const ParamSpec& p : lm_param_layout(c)) {
+        float* o = out + p.off;
+        const int64_t n = p.numel();
+        if (p.kind == 2) {
+            for (int64_t i = 0; i < n; ++i) o[i] = 1.0f;
+        } else if (p.kind == 3) {
+            for (int64_t i = 0; i < n; ++i) o[i] = 0.0f;
+        } else {
+            const double stdv = p.kind == 0 ? 0.02 : 0.02 / std::sqrt(2.0 * c.n_layer);
+            const double a = stdv * kSqrt3;
+            for (int64_t i = 0; i < n; ++i) o[i] = static_cast<float>(a * (2.0 * st.uniform01() - 1.0));
+        }
+    }
+}
+
+// ------------------------------------------------------------------- model
+namespace {
+enum Slot { sX, sH1, sQKV, sY, sXM, sH2, sA, sU, kPerLayer };
+}
+
+GPTModel::GPTModel(const LMConfig& c) : c_(c) {
+    ACCO_REQUIRE(c.vocab >= 2 && c.d_model >= 8 && c.n_layer >= 1 && c.n_head >= 1 && c.seq_len >= 1,
+                 "lm config: positive sizes required");
+    ACCO_REQUIRE(c.d_model % c.n_head == 0, "lm config: d_model must be divisible by n_head");
+    ACCO_REQUIRE(c.d_model % 8 == 0, "lm config: d_model must be a multiple of 8 (TMA alignment)");
+    ACCO_REQUIRE(c.n_samples >= 1 && c.max_batch >= 1, "lm config: n_samples, max_batch >= 1");
+    ACCO_REQUIRE(c.precision == 0 || c.precision == 1, "lm config: precision must be fp32 or bf16");
+    layout_ = lm_param_layout(c);
+    psi_ = layout_.back().off + layout_.back().numel();
+    vpad_ = (c.vocab + 63) / 64 * 64;
+    const int64_t M = static_cast<int64_t>(c.max_batch) * c.seq_len;
+    const int64_t d = c.d_model, L = c.n_layer, H = c.n_head;
+    const size_t e = act_bytes();
+    auto sz = [&](int slot) -> int64_t {
+        switch (slot) {
+            case sQKV: return 3 * d;
+            case sA: case sU: return 4 * d;
+            default: return d;
+        }
+    };
+    // arena: L layers x kPerLayer slots, then x[L], hf, logits, dx, dt, dqkv, da
+    std::vector<int64_t> cols;
+    for (int l = 0; l < L; ++l)
+        for (int s = 0; s < kPerLayer; ++s) cols.push_back(sz(s));
+    cols.push_back(d);          // x[L]
+    cols.push_back(d);          // hf
+    cols.push_back(vpad_);      // logits
+    cols.push_back(d);          // dx
+    cols.push_back(d);          // dt
+    cols.push_back(3 * d);      // dqkv
+    cols.push_back(4 * d);      // da
+    size_t total = 0;
+    std::vector<size_t> offs;
+    for (int64_t cc : cols) {
+        offs.push_back(total);
+        total += (static_cast<size_t>(M * cc) * e + 255) / 256 * 256;
+    }
+    arena_bytes_ = total;
+    ACCO_CUDA(cudaMalloc(&arena_, arena_bytes_));
+    for (size_t o : offs) act_.push_back(static_cast<char*>(arena_) + o);
+
+    std::vector<int32_t> data = lm_dataset(c);
+    ACCO_CUDA(cudaMalloc(&data_, data.size() * sizeof(int32_t)));
+    ACCO_CUDA(cudaMemcpy(data_, data.data(), data.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    ACCO_CUDA(cudaMalloc(&tok_in_, M * sizeof(int32_t)));
+    ACCO_CUDA(cudaMalloc(&tok_out_, M * sizeof(int32_t)));
+    ACCO_CUDA(cudaMalloc(&idx_, c.max_batch * sizeof(int32_t)));
+    ACCO_CUDA(cudaMalloc(&sort_, M * sizeof(uint32_t)));
+    ACCO_CUDA(cudaMalloc(&row_loss_, M * sizeof(float)));
+    ACCO_CUDA(cudaMalloc(&stats_, (4 * L + 2) * M * sizeof(float)));
+    ACCO_CUDA(cudaMalloc(&lse_, L * H * M * sizeof(float)));
+    ACCO_CUDA(cudaMalloc(&dsum_, H * M * sizeof(float)));
+    const int64_t nchunk = (M + 255) / 256;
+    ACCO_CUDA(cudaMalloc(&scratch_, nchunk * 4 * d * 2 * sizeof(float)));
+}
+
+GPTModel::~GPTModel() {
+    cudaFree(arena_);
+    cudaFree(data_);
+    cudaFree(tok_in_);
+    cudaFree(tok_out_);
+    cudaFree(idx_);
+    cudaFree(sort_);
+    cudaFree(row_loss_);
+    cudaFree(stats_);
+    cudaFree(lse_);
+    cudaFree(dsum_);
+    cudaFree(scratch_);
+}
+
+namespace {
+
+template <class T>
+void mm(const T* a, int64_t lda, bool amn, const T* b, int64_t ldb, bool bmn, int m, int n, int k,
+        const Epilogue& ep, cudaStream_t s) {
+    GemmOperand A{a, lda, amn}, B{b, ldb, bmn};
+    if constexpr (sizeof(T) == 2)
+        gemm_bf16(A, B, m, n, k, ep, s);
+    else
+        gemm_f32(A, B, m, n, k, ep, s);
+}
+
+Epilogue ep_store(void* c, int64_t ldc, const void* bias = nullptr, const void* res = nullptr, int64_t ldr = 0) {
+    Epilogue e;
+    e.mode = kEpiStore;
+    e.C = c;
+    e.ldc = ldc;
+    e.bias = bias;
+    e.residual = res;
+    e.ldr = ldr;
+    return e;
+}
+Epilogue ep_gelu(void* c, int64_t ldc, const void* bias, void* aux) {
+    Epilogue e = ep_store(c, ldc, bias);
+    e.mode = kEpiGelu;
+    e.aux = aux;
+    e.ld_aux = ldc;
+    return e;
+}
+Epilogue ep_dgelu(void* c, int64_t ldc, void* aux) {
+    Epilogue e = ep_store(c, ldc);
+    e.mode = kEpiDGelu;
+    e.aux = aux;
+    e.ld_aux = ldc;
+    return e;
+}
+Epilogue ep_acc(float* c, int64_t ldc) {
+    Epilogue e;
+    e.mode = kEpiAccF32;
+    e.C = c;
+    e.ldc = ldc;
+    e.beta = 1;
+    return e;
+}
+
+}  // namespace
+
+template <class T>
+void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss, bool backward,
+                   cudaStream_t s) {
+    const int Tq = c_.seq_len, d = c_.d_model, H = c_.n_head, hd = d / H, V = c_.vocab, L = c_.n_layer;
+    ACCO_REQUIRE(B >= 1 && B <= c_.max_batch, "micro_batch: batch size exceeds the model workspace");
+    if (mode == 1) ACCO_REQUIRE(start >= 0 && start + B <= c_.n_samples, "micro_batch: sample range out of bounds");
+    const int M = B * Tq;
+    const int64_t Mmax = static_cast<int64_t>(c_.max_batch) * Tq;
+    auto slot = [&](int l, int sl) { return reinterpret_cast<T*>(act_[static_cast<size_t>(l * kPerLayer + sl)]); };
+    const int tail = L * kPerLayer;
+    T* XL = reinterpret_cast<T*>(act_[tail + 0]);
+    T* HF = reinterpret_cast<T*>(act_[tail + 1]);
+    T* LOG = reinterpret_cast<T*>(act_[tail + 2]);
+    T* DX = reinterpret_cast<T*>(act_[tail + 3]);
+    T* DT = reinterpret_cast<T*>(act_[tail + 4]);
+    T* DQKV = reinterpret_cast<T*>(act_[tail + 5]);
+    T* DA = reinterpret_cast<T*>(act_[tail + 6]);
+    auto X = [&](int l) { return l == L ? XL : slot(l, sX); };
+    auto stat = [&](int i) { return stats_ + static_cast<int64_t>(i) * Mmax; };
+    // parameter pointers: index into layout_ (oracle order)
+    auto W = [&](int i) { return P + layout_[static_cast<size_t>(i)].off; };
+    auto Gp = [&](int i) { return G + layout_[static_cast<size_t>(i)].off; };
+    const int kWte = 0, kWpe = 1, kLnf = 2 + 12 * L;
+    auto li = [&](int l, int j) { return 2 + 12 * l + j; };  // j: 0 ln1w 1 ln1b 2 Wqkv 3 bqkv 4 Wproj 5 bproj
+                                                            //    6 ln2w 7 ln2b 8 Wfc 9 bfc 10 Wfc2 11 bfc2
+
+    gather_tokens(data_, Tq, c_.n_samples, seed, mode, start, B, tok_in_, tok_out_, idx_, s);
+    embed_fwd<T>(tok_in_, W(kWte), W(kWpe), X(0), M, Tq, d, s);
+    for (int l = 0; l < L; ++l) {
+        T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
+          *A = slot(l, sA), *U = slot(l, sU);
+        layernorm_fwd<T>(X(l), W(li(l, 0)), W(li(l, 1)), H1, stat(4 * l), stat(4 * l + 1), M, d, s);
+        mm<T>(H1, d, false, W(li(l, 2)), d, false, M, 3 * d, d, ep_store(QKV, 3 * d, W(li(l, 3))), s);
+        attention_fwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, B, Tq, H, hd, s);
+        mm<T>(Y, d, false, W(li(l, 4)), d, false, M, d, d, ep_store(XM, d, W(li(l, 5)), X(l), d), s);
+        layernorm_fwd<T>(XM, W(li(l, 6)), W(li(l, 7)), H2, stat(4 * l + 2), stat(4 * l + 3), M, d, s);
+        mm<T>(H2, d, false, W(li(l, 8)), d, false, M, 4 * d, d, ep_gelu(U, 4 * d, W(li(l, 9)), A), s);
+        mm<T>(U, 4 * d, false, W(li(l, 10)), 4 * d, false, M, d, 4 * d, ep_store(X(l + 1), d, W(li(l, 11)), XM, d), s);
+    }
+    layernorm_fwd<T>(X(L), W(kLnf), W(kLnf + 1), HF, stat(4 * L), stat(4 * L + 1), M, d, s);
+    mm<T>(HF, d, false, W(kWte), d, false, M, V, d, ep_store(LOG, vpad_), s);
+    cross_entropy<T>(LOG, vpad_, tok_out_, V, M, Tq, row_loss_, s);
+    loss_reduce(row_loss_, M, Tq, loss, s);
+    if (!backward) return;
+
+    // LM head (tied to wte): dwte += dlogits^T hf ; dhf = dlogits wte
+    mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d), s);
+    mm<T>(LOG, vpad_, false, W(kWte), d, true, M, d, V, ep_store(DT, d), s);
+    layernorm_bwd<T>(DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), DX, false, Gp(kLnf), Gp(kLnf + 1), scratch_,
+                     M, d, s);
+    for (int l = L - 1; l >= 0; --l) {
+        T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
+          *A = slot(l, sA), *U = slot(l, sU);
+        // MLP
+        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d), s);
+        colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, s);
+        mm<T>(DX, d, false, W(li(l, 10)), 4 * d, true, M, 4 * d, d, ep_dgelu(DA, 4 * d, A), s);
+        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d), s);
+        colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, s);
+        mm<T>(DA, 4 * d, false, W(li(l, 8)), d, true, M, d, 4 * d, ep_store(DT, d), s);
+        layernorm_bwd<T>(DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), DX, true, Gp(li(l, 6)), Gp(li(l, 7)),
+                         scratch_, M, d, s);
+        // attention
+        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d), s);
+        colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, s);
+        mm<T>(DX, d, false, W(li(l, 4)), d, true, M, d, d, ep_store(DT, d), s);
+        attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, hd, s);
+        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d), s);
+        colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, s);
+        mm<T>(DQKV, 3 * d, false, W(li(l, 2)), d, true, M, d, 3 * d, ep_store(DT, d), s);
+        layernorm_bwd<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, Gp(li(l, 0)), Gp(li(l, 1)),
+                         scratch_, M, d, s);
+    }
+    embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), sort_, s);
+}
+
+void GPTModel::micro_batch(const void* params, uint64_t seed, int mode, int start, int B, float* grad_acc,
+                           double* loss_sum, cudaStream_t s) {
+    if (c_.precision == 1)
+        run<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(params), seed, mode, start, B, grad_acc, loss_sum, true, s);
+    else
+        run<float>(static_cast<const float*>(params), seed, mode, start, B, grad_acc, loss_sum, true, s);
+}
+
+void GPTModel::forward_loss(const void* params, uint64_t seed, int mode, int start, int B, double* loss_sum,
+                            cudaStream_t s) {
+    if (c_.precision == 1)
+        run<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(params), seed, mode, start, B, nullptr, loss_sum, false, s);
+    else
+        run<float>(static_cast<const float*>(params), seed, mode, start, B, nullptr, loss_sum, false, s);
+}
+
+}  // namespace acco

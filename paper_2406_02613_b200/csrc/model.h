@@ -1,0 +1,90 @@
+// GPT-style LM plugin: the B200 implementation of the reference's gradient
+// oracle contract `stochastic_grad(Problem, theta, MicroBatch)`
+// (/root/reference/proj/include/accosim/problems.hpp:86-92,
+// proj/src/problems.cpp:419-451) for the LM defined in oracle/gpt_oracle.py.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace acco {
+
+struct LMConfig {
+    int vocab = 256;
+    int d_model = 128;
+    int n_layer = 2;
+    int n_head = 4;
+    int seq_len = 64;
+    int n_samples = 256;
+    uint64_t data_seed = 1;
+    int precision = 0;  // 0 = fp32 (parity), 1 = bf16 (tcgen05 throughput)
+    int max_batch = 8;  // samples per micro-batch (workspace sizing)
+};
+
+struct ParamSpec {
+    std::string name;
+    int64_t rows, cols;  // cols == 1 for vectors
+    int kind;            // 0 w(.02) 1 wp(.02/sqrt(2L)) 2 one 3 zero
+    int64_t off;
+    int64_t numel() const { return rows * cols; }
+};
+
+std::vector<ParamSpec> lm_param_layout(const LMConfig& c);
+// Markov dataset [n_samples, seq_len+1] (int32), host.
+std::vector<int32_t> lm_dataset(const LMConfig& c);
+// theta0 (fp64 on host -> float), the oracle's default_theta0.
+void lm_default_theta0(const LMConfig& c, uint64_t master_seed, float* out);
+
+class GPTModel {
+public:
+    explicit GPTModel(const LMConfig& c);
+    ~GPTModel();
+    GPTModel(const GPTModel&) = delete;
+    GPTModel& operator=(const GPTModel&) = delete;
+
+    const LMConfig& cfg() const { return c_; }
+    int64_t num_params() const { return psi_; }
+    int act_dtype() const { return c_.precision; }  // ACCO_DTYPE_*
+    size_t act_bytes() const { return c_.precision ? 2 : 4; }
+    const std::vector<ParamSpec>& layout() const { return layout_; }
+
+    // One micro-batch fwd+bwd at `params` (activation dtype, flat layout):
+    // grad_acc[psi] (fp32) += sum over the B samples of their gradients
+    // (= Bundle::add of N * per-sample-mean, protocols.cpp:61-66), and
+    // *loss_sum (device double) = sum over samples of the per-sample loss.
+    // mode 0: indices Stream(stream_seed).below(n_samples); mode 1: [start, start+B).
+    void micro_batch(const void* params, uint64_t stream_seed, int mode, int start, int B, float* grad_acc,
+                     double* loss_sum, cudaStream_t s);
+    // Token indices drawn by the last micro_batch (device int32 [B]).
+    const int32_t* last_indices() const { return idx_; }
+    // Forward only (loss), used by evaluation when no gradient is needed.
+    void forward_loss(const void* params, uint64_t stream_seed, int mode, int start, int B, double* loss_sum,
+                      cudaStream_t s);
+
+private:
+    template <class T>
+    void run(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss, bool backward,
+             cudaStream_t s);
+
+    LMConfig c_;
+    std::vector<ParamSpec> layout_;
+    int64_t psi_ = 0;
+    int vpad_ = 0;
+    // device buffers
+    int32_t* data_ = nullptr;
+    int32_t *tok_in_ = nullptr, *tok_out_ = nullptr, *idx_ = nullptr;
+    uint32_t* sort_ = nullptr;
+    void* arena_ = nullptr;
+    size_t arena_bytes_ = 0;
+    float* row_loss_ = nullptr;
+    float* stats_ = nullptr;    // per-layer LN mean/rstd
+    float* lse_ = nullptr;      // per-layer attention lse
+    float* dsum_ = nullptr;
+    float* scratch_ = nullptr;  // column-reduce partials
+    std::vector<char*> act_;    // activation slots (see model.cu)
+};
+
+}  // namespace acco

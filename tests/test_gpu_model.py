@@ -1,0 +1,124 @@
+"""LM plugin (stochastic_grad contract, problems.cpp:419-451) vs the fp64 oracle.
+
+fp32 mode: gradient rel <= 1e-5 (norm-wise) and loss rel <= 1e-6.
+bf16 mode (tcgen05 GEMMs, bf16 activations): rel <= 3e-2 on the gradient,
+1e-2 on the loss — bf16 rounding of activations/weights, not a precision claim.
+Dataset, theta0 and token indexing are bit-exact."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import accosim_oracle as O
+from oracle import gpt_oracle as G
+from paper_2406_02613_b200 import _lib, api
+
+pytestmark = pytest.mark.gpu
+
+CFGS = {
+    "tiny": dict(vocab=64, d_model=32, n_layer=2, n_head=2, seq_len=16, n_samples=32, data_seed=3),
+    "c1": dict(vocab=256, d_model=128, n_layer=2, n_head=4, seq_len=64, n_samples=64, data_seed=1),
+    "ragged": dict(vocab=100, d_model=64, n_layer=1, n_head=1, seq_len=24, n_samples=16, data_seed=9),
+}
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def _grad(model, params_t, seed, B, dev):
+    g = torch.zeros(model.dim, device=dev)
+    loss = torch.zeros(1, dtype=torch.float64, device=dev)
+    _lib.call("acco_model_stochastic_grad", model.handle, C.c_void_p(params_t.data_ptr()), C.c_uint64(seed), B,
+              C.c_void_p(g.data_ptr()), C.c_void_p(loss.data_ptr()),
+              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    return g.double().cpu().numpy(), loss.item()
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+def test_dataset_theta0_bitexact(cuda, name):
+    c = CFGS[name]
+    m = api.Model(api.LMConfig(**c, precision="fp32", max_batch=4))
+    gc = G.GPTConfig(**c)
+    assert m.dim == G.param_count(gc)
+    assert np.array_equal(m.dataset(), G.dataset(gc))
+    assert np.array_equal(m.default_theta0(11), G.default_theta0(gc, 11).astype(np.float32))
+
+
+@pytest.mark.parametrize("name", list(CFGS))
+def test_fp32_gradient_matches_oracle(cuda, name):
+    c = CFGS[name]
+    B = 4
+    m = api.Model(api.LMConfig(**c, precision="fp32", max_batch=B))
+    gc = G.GPTConfig(**c)
+    prob = G.LMProblem(gc)
+    rng = np.random.default_rng(0)
+    th = (G.default_theta0(gc, 5) + 0.02 * rng.standard_normal(m.dim)).astype(np.float32)
+    seed = O.derive(5, 1, 2, 2, 0)
+    g, loss_sum = _grad(m, torch.tensor(th, device=cuda), seed, B, cuda)
+    og, n, ol = prob.stochastic_grad(th.astype(np.float64), seed, B)
+    assert n == B
+    assert abs(loss_sum / B - ol) <= 1e-6 * abs(ol)
+    assert _rel(g, og * B) <= 1e-5  # accumulator holds N * mean (Bundle::add)
+
+
+def test_accumulates_across_micro_batches(cuda):
+    c = CFGS["tiny"]
+    m = api.Model(api.LMConfig(**c, precision="fp32", max_batch=3))
+    gc = G.GPTConfig(**c)
+    prob = G.LMProblem(gc)
+    th = G.default_theta0(gc, 1).astype(np.float32)
+    pt = torch.tensor(th, device=cuda)
+    acc = torch.zeros(m.dim, device=cuda)
+    loss = torch.zeros(2, dtype=torch.float64, device=cuda)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    seeds = [O.derive(1, 0, 0, 2, j) for j in range(2)]
+    for j, sd in enumerate(seeds):
+        _lib.call("acco_model_stochastic_grad", m.handle, C.c_void_p(pt.data_ptr()), C.c_uint64(sd), 3,
+                  C.c_void_p(acc.data_ptr()), C.c_void_p(loss[j:].data_ptr()), s)
+    torch.cuda.synchronize()
+    ref = sum(prob.stochastic_grad(th.astype(np.float64), sd, 3)[0] * 3 for sd in seeds)
+    assert _rel(acc.cpu().numpy(), ref) <= 1e-5
+
+
+def test_value_and_grad_full_dataset(cuda):
+    c = CFGS["tiny"]
+    m = api.Model(api.LMConfig(**c, precision="fp32", max_batch=8))
+    gc = G.GPTConfig(**c)
+    th = G.default_theta0(gc, 2).astype(np.float32)
+    pt = torch.tensor(th, device=cuda)
+    g = torch.zeros(m.dim, device=cuda)
+    loss = C.c_double()
+    _lib.call("acco_model_value_and_grad", m.handle, C.c_void_p(pt.data_ptr()), C.byref(loss),
+              C.c_void_p(g.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    of, og = G.LMProblem(gc).value_and_grad(th.astype(np.float64))
+    assert abs(loss.value - of) <= 1e-6 * abs(of)
+    assert _rel(g.cpu().numpy(), og) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["tiny", "c1"])
+def test_bf16_gradient_close_to_oracle(cuda, name):
+    c = CFGS[name]
+    B = 4
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=B))
+    gc = G.GPTConfig(**c)
+    rng = np.random.default_rng(1)
+    th = (G.default_theta0(gc, 5) + 0.05 * rng.standard_normal(m.dim)).astype(np.float32)
+    th_bf = torch.tensor(th).to(torch.bfloat16)
+    seed = O.derive(9, 0, 1, 2, 0)
+    g, loss_sum = _grad(m, th_bf.to(cuda), seed, B, cuda)
+    og, _, ol = G.LMProblem(gc).stochastic_grad(th_bf.float().double().numpy(), seed, B)
+    assert abs(loss_sum / B - ol) <= 1e-2 * abs(ol)
+    assert _rel(g, og * B) <= 3e-2
+
+
+def test_micro_batch_bounds(cuda):
+    m = api.Model(api.LMConfig(**CFGS["tiny"], precision="fp32", max_batch=2))
+    pt = torch.zeros(m.dim, device=cuda)
+    with pytest.raises(_lib.InvalidArgument):
+        _grad(m, pt, 1, 3, cuda)
+    with pytest.raises(_lib.InvalidArgument):
+        api.Model(api.LMConfig(vocab=64, d_model=30, n_layer=1, n_head=3, seq_len=8, n_samples=4))
