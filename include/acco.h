@@ -38,6 +38,15 @@ extern "C" {
 const char* acco_last_error(void);
 int acco_version(void);
 
+/* Instrumentation (B200 only): number of this library's kernel launches so
+ * far, and optional CUDA-event timing per kernel class on the launching
+ * stream — class 0 GEMM (work = algorithmic flops), 1 attention (flops),
+ * 2 fused optimizer (algorithmic bytes), 3 other. */
+long long acco_launch_count(void);
+void acco_prof_enable(int on);
+int acco_prof_reset(void);
+int acco_prof_read(double ms[4], double work[4], long long launches[4]);
+
 /* ------------------------------------------------------------------ shards
  * shard_partition (proj/include/accosim/shard.hpp:24-38): contiguous
  * near-equal split, the first (dim mod n) ranges get one extra element. */
@@ -151,6 +160,9 @@ typedef struct acco_lm_cfg {
     uint64_t data_seed;
     int precision;
     int max_batch; /* samples per micro-batch the workspace is sized for */
+    int host_data; /* 1: dataset stays in pinned host memory; every micro-batch's
+                      token rows are copied host->device (data-loader path), and
+                      every micro-batch loss is read back device->host */
 } acco_lm_cfg;
 
 typedef struct acco_model acco_model;
@@ -225,6 +237,8 @@ typedef struct acco_run_stats {
     double opt_ms;          /* fused optimizer kernel time, summed */
     int opt_launches;
     int diverged;
+    long long h2d_bytes; /* host-data path: token rows shipped host->device */
+    long long d2h_bytes; /* host-data path: per-micro-batch losses read back */
 } acco_run_stats;
 
 typedef struct acco_trainer acco_trainer;

@@ -51,6 +51,10 @@ class ShardState(C.Structure):
 _P = C.c_void_p
 _PROTOS = {
     "acco_last_error": (C.c_char_p, []),
+    "acco_launch_count": (C.c_longlong, []),
+    "acco_prof_enable": (None, [C.c_int]),
+    "acco_prof_reset": (C.c_int, []),
+    "acco_prof_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "acco_version": (C.c_int, []),
     "acco_shard_partition": (C.c_int, [C.c_uint64, C.c_int, _P, _P]),
     "acco_rng_derive": (C.c_uint64, [C.c_uint64] * 5),

@@ -34,7 +34,7 @@ SCHEDULES = {"floor": 0, "adaptive": 1, "replay": 2}
 class LMCfgC(C.Structure):
     _fields_ = [("vocab", C.c_int), ("d_model", C.c_int), ("n_layer", C.c_int), ("n_head", C.c_int),
                 ("seq_len", C.c_int), ("n_samples", C.c_int), ("data_seed", C.c_uint64),
-                ("precision", C.c_int), ("max_batch", C.c_int)]
+                ("precision", C.c_int), ("max_batch", C.c_int), ("host_data", C.c_int)]
 
 
 class SimCfgC(C.Structure):
@@ -54,7 +54,8 @@ class StatsC(C.Structure):
     _fields_ = [("issued_micro_batches", C.c_longlong), ("consumed_micro_batches", C.c_longlong),
                 ("discarded_micro_batches", C.c_longlong), ("wall_ms", C.c_double),
                 ("compute_busy_ms", C.c_double), ("comm_busy_ms", C.c_double), ("comm_exposed_ms", C.c_double),
-                ("opt_ms", C.c_double), ("opt_launches", C.c_int), ("diverged", C.c_int)]
+                ("opt_ms", C.c_double), ("opt_launches", C.c_int), ("diverged", C.c_int),
+                ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
 
 
 _P = C.c_void_p
@@ -127,6 +128,30 @@ def derive(master: int, a: int, b: int = 0, c: int = 0, d: int = 0) -> int:
     return int(_lib.lib().acco_rng_derive(*(C.c_uint64(x & (2**64 - 1)) for x in (master, a, b, c, d))))
 
 
+def launch_count() -> int:
+    """Kernel launches issued by this library so far (process-wide)."""
+    return int(_lib.lib().acco_launch_count())
+
+
+PROF_CLASSES = ("gemm", "attention", "optimizer", "other")
+
+
+def prof_enable(on: bool = True):
+    _lib.lib().acco_prof_enable(int(on))
+    if on:
+        _lib.call("acco_prof_reset")
+
+
+def prof_read() -> dict:
+    """Per-class kernel time (CUDA events on the launching stream), work
+    (algorithmic flops for gemm/attention, bytes for the optimizer), launches."""
+    ms = (C.c_double * 4)()
+    work = (C.c_double * 4)()
+    n = (C.c_longlong * 4)()
+    _lib.call("acco_prof_read", ms, work, n)
+    return {c: {"ms": ms[i], "work": work[i], "launches": int(n[i])} for i, c in enumerate(PROF_CLASSES)}
+
+
 # ---------------------------------------------------------------------- model
 @dataclass(frozen=True)
 class LMConfig:
@@ -140,12 +165,13 @@ class LMConfig:
     data_seed: int = 1
     precision: str = "fp32"  # "fp32" (parity) or "bf16" (throughput)
     max_batch: int = 8
+    host_data: bool = False  # data-loader path: per-micro-batch H2D of token rows
 
     def to_c(self) -> LMCfgC:
         if self.precision not in ("fp32", "bf16"):
             raise InvalidArgument(_lib.INVALID, "lm config: precision must be fp32 or bf16")
         return LMCfgC(self.vocab, self.d_model, self.n_layer, self.n_head, self.seq_len, self.n_samples,
-                      self.data_seed, 1 if self.precision == "bf16" else 0, self.max_batch)
+                      self.data_seed, 1 if self.precision == "bf16" else 0, self.max_batch, int(self.host_data))
 
 
 class Model:

@@ -258,8 +258,14 @@ bool attention_bwd_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const f
                        const __nv_bfloat16* dy, __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int hd,
                        cudaStream_t s);
 
+// algorithmic causal-attention flops: QK^T and PV over the lower triangle
+static double attn_flops(int B, int seq, int H, int hd) {
+    return 2.0 * 2.0 * B * H * (static_cast<double>(seq) * (seq + 1) / 2) * hd;
+}
+
 template <class T>
 void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd, cudaStream_t s) {
+    ProfScope prof(kProfAttn, attn_flops(B, seq, H, hd), s);
     if constexpr (sizeof(T) == 2) {
         if (attention_fwd_mma(qkv, y, lse, B, seq, H, hd, s)) return;
     }
@@ -273,6 +279,7 @@ void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd
 template <class T>
 void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, float* dsum, int B, int seq,
                    int H, int hd, cudaStream_t s) {
+    ProfScope prof(kProfAttn, 2.5 * attn_flops(B, seq, H, hd), s);
     if constexpr (sizeof(T) == 2) {
         if (attention_bwd_mma(qkv, y, lse, dy, dqkv, dsum, B, seq, H, hd, s)) return;
     }

@@ -4,8 +4,11 @@
 #include "capi_util.h"
 #include "gemm.h"
 
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 namespace acco {
 
@@ -23,11 +26,75 @@ int num_sms() {
     return n;
 }
 
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+struct ProfEntry {
+    int cls;
+    double work;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::atomic<bool> g_prof_on{false};
+std::vector<ProfEntry> g_prof;
+std::vector<cudaEvent_t> g_prof_pool;
+size_t g_prof_next = 0;
+}  // namespace
+
+bool prof_on() { return g_prof_on.load(std::memory_order_relaxed); }
+
+cudaEvent_t prof_event() {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (g_prof_next == g_prof_pool.size()) {
+        cudaEvent_t e;
+        ACCO_CUDA(cudaEventCreate(&e));
+        g_prof_pool.push_back(e);
+    }
+    return g_prof_pool[g_prof_next++];
+}
+
+void prof_record(int cls, double work, cudaEvent_t a, cudaEvent_t b) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back({cls, work, a, b});
+}
+
 }  // namespace acco
 
 using namespace acco;
 
 extern "C" {
+
+long long acco_launch_count(void) { return g_launches.load(); }
+
+void acco_prof_enable(int on) { g_prof_on.store(on != 0); }
+
+int acco_prof_reset(void) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof.clear();
+        g_prof_next = 0;
+    });
+}
+
+int acco_prof_read(double* ms, double* work, long long* launches) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        for (int c = 0; c < kProfClasses; ++c) {
+            ms[c] = 0;
+            work[c] = 0;
+            launches[c] = 0;
+        }
+        for (const ProfEntry& e : g_prof) {
+            ACCO_CUDA(cudaEventSynchronize(e.b));
+            float t = 0.f;
+            ACCO_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
+            ms[e.cls] += t;
+            work[e.cls] += e.work;
+            launches[e.cls] += 1;
+        }
+    });
+}
 
 const char* acco_last_error(void) { return g_last_error.c_str(); }
 

@@ -30,6 +30,7 @@ LMConfig to_lm(const acco_lm_cfg& c) {
     l.data_seed = c.data_seed;
     l.precision = c.precision;
     l.max_batch = c.max_batch;
+    l.host_data = c.host_data;
     return l;
 }
 }  // namespace
@@ -168,6 +169,8 @@ int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t*
             stats->opt_ms = st.opt_ms;
             stats->opt_launches = st.opt_launches;
             stats->diverged = st.diverged || diverged;
+            stats->h2d_bytes = st.h2d_bytes;
+            stats->d2h_bytes = st.d2h_bytes;
         }
         if (st.diverged) diverged = 1;
     });

@@ -41,7 +41,11 @@ enum Status : int {
                                                         __FILE__ + ":" + std::to_string(__LINE__)); \
     } while (0)
 
-#define ACCO_CHECK_LAUNCH() ACCO_CUDA(cudaGetLastError())
+#define ACCO_CHECK_LAUNCH()              \
+    do {                                 \
+        ACCO_CUDA(cudaGetLastError());   \
+        ::acco::count_launch();          \
+    } while (0)
 
 #define ACCO_REQUIRE(cond, msg)                                                  \
     do {                                                                         \
@@ -52,5 +56,35 @@ inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b -
 
 // Number of SMs on the current device (148 on B200); cached per process.
 int num_sms();
+
+// Every kernel launch of this library increments a process-wide counter
+// (acco_launch_count), so benches can report how many of *our* kernels ran.
+void count_launch();
+
+// Optional per-class kernel timing with CUDA events on the launching stream
+// (acco_prof_*): used by bench.py for the live roofline numbers.
+enum ProfClass : int { kProfGemm = 0, kProfAttn = 1, kProfOpt = 2, kProfOther = 3, kProfClasses = 4 };
+bool prof_on();
+void prof_record(int cls, double work, cudaEvent_t a, cudaEvent_t b);
+cudaEvent_t prof_event();
+struct ProfScope {
+    int cls;
+    double work;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    ProfScope(int c, double w, cudaStream_t st) : cls(c), work(w), s(st) {
+        if (prof_on()) {
+            a = prof_event();
+            cudaEventRecord(a, s);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEvent_t b = prof_event();
+            cudaEventRecord(b, s);
+            prof_record(cls, work, a, b);
+        }
+    }
+};
 
 }  // namespace acco

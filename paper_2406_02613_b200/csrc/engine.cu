@@ -108,6 +108,7 @@ Trainer::~Trainer() {
     if (ag_theta_ != theta_act_) cudaFree(ag_theta_);
     if (ag_est_ != est_act_) cudaFree(ag_est_);
     for (float* a : acc_) cudaFree(a);
+    if (loss_host_) cudaFreeHost(loss_host_);
     cudaStreamDestroy(cs_);
     cudaStreamDestroy(ms_);
 }
@@ -150,6 +151,7 @@ void Trainer::alloc() {
     ACCO_CUDA(cudaMemset(flag_, 0, sizeof(int)));
     loss_cap_ = 1 << 16;
     ACCO_CUDA(cudaMalloc(&loss_ring_, loss_cap_ * sizeof(double)));
+    if (model_->host_data()) ACCO_CUDA(cudaHostAlloc(&loss_host_, loss_cap_ * sizeof(double), cudaHostAllocDefault));
     if (sim_.eval_every > 0) {
         ACCO_CUDA(cudaMalloc(&eval_grad_, P * 4));
         ACCO_CUDA(cudaMalloc(&eval_scratch_, 512 * sizeof(double)));
@@ -217,6 +219,11 @@ void Trainer::micro(int w, const void* params, uint64_t round, uint64_t tag, int
     const uint64_t gw = comm_ ? static_cast<uint64_t>(rank_) : static_cast<uint64_t>(w);
     const uint64_t seed = rng_derive(sim_.master_seed, gw, round, tag, static_cast<uint64_t>(ordinal));
     model_->micro_batch(params, seed, 0, 0, sim_.batch_size, acc, loss_slot, cs_);
+    if (loss_host_) {  // host-data path: every micro-batch loss is read back as it completes
+        const ptrdiff_t slot = loss_slot - loss_ring_;
+        ACCO_CUDA(cudaMemcpyAsync(loss_host_ + slot, loss_slot, sizeof(double), cudaMemcpyDeviceToHost, cs_));
+        d2h_bytes_ += sizeof(double);
+    }
     if (!sim_.throttle_ns.empty()) spin_ns(static_cast<uint64_t>(sim_.throttle_ns[static_cast<size_t>(gw)]), cs_);
 }
 
@@ -347,11 +354,14 @@ void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* t
     recs.clear();
     st = RunStats{};
     if (theta_hist) ACCO_CUDA(cudaMalloc(&hist_dev_, static_cast<size_t>(T) * 2 * psi_ * model_->act_bytes()));
+    const long long h2d0 = model_->h2d_bytes(), d2h0 = d2h_bytes_;
     try {
         if (method_ == kACCO)
             run_acco(T, recs, st);
         else
             run_sync(T, recs, st);
+        st.h2d_bytes = model_->h2d_bytes() - h2d0;
+        st.d2h_bytes = d2h_bytes_ - d2h0;
         if (theta_hist) fetch_history(T, theta_hist);
     } catch (...) {
         if (hist_dev_) cudaFree(hist_dev_);
@@ -469,9 +479,10 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             while (true) {
                 if (!adaptive && k >= target) break;
                 if (adaptive && k >= target) {
-                    // floor met: hand off as soon as phase p-1 has completed
-                    // (protocols.cpp:566-573); bounded lookahead of 2 micro-batches
-                    ACCO_CUDA(cudaEventSynchronize(ev.mb[(k + 2) % 4]));
+                    // floor met: the decision is taken when micro-batch k-1
+                    // completes, as in on_mb_done (protocols.cpp:566-573) — hand
+                    // off iff phase p-1 has completed, else accumulate another.
+                    ACCO_CUDA(cudaEventSynchronize(ev.mb[(k - 1) % 4]));
                     if (cudaEventQuery(ev.done[p - 1]) == cudaSuccess) break;
                 }
                 const int slot = static_cast<int>(mb_counter_ % loss_cap_);
@@ -506,7 +517,10 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     const long long nmb = mb_counter_ - mb0;
     ACCO_REQUIRE(nmb <= loss_cap_, "loss ring overflow: run fewer updates per call");
     std::vector<double> ring(static_cast<size_t>(loss_cap_));
-    ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (loss_host_)
+        std::memcpy(ring.data(), loss_host_, ring.size() * sizeof(double));
+    else
+        ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
     std::vector<double> phase_loss(NP, 0.0);
     for (long long i = 0; i < nmb; ++i)
         phase_loss[static_cast<size_t>(mb_phase[static_cast<size_t>(i)])] += ring[static_cast<size_t>((mb0 + i) % loss_cap_)];
@@ -625,7 +639,10 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     const long long nmb = mb_counter_ - mb0;
     ACCO_REQUIRE(nmb <= loss_cap_, "loss ring overflow: run fewer updates per call");
     std::vector<double> ring(static_cast<size_t>(loss_cap_));
-    ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    if (loss_host_)
+        std::memcpy(ring.data(), loss_host_, ring.size() * sizeof(double));
+    else
+        ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
     std::vector<double> rl(T, 0.0);
     for (long long i = 0; i < nmb; ++i)
         rl[static_cast<size_t>(mb_round[static_cast<size_t>(i)])] += ring[static_cast<size_t>((mb0 + i) % loss_cap_)];

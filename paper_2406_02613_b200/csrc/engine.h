@@ -43,6 +43,7 @@ struct RunStats {
     double opt_ms = 0;  // optimizer-kernel time summed over phases (device events)
     int opt_launches = 0;
     int diverged = 0;
+    long long h2d_bytes = 0, d2h_bytes = 0;  // host-data path traffic during the run
 };
 
 class Trainer {
@@ -98,6 +99,8 @@ private:
     int64_t* cnt_send_ = nullptr;
     int* flag_ = nullptr;
     double* loss_ring_ = nullptr;
+    double* loss_host_ = nullptr;  // pinned mirror of loss_ring_ (host-data path)
+    long long d2h_bytes_ = 0;
     int loss_cap_ = 0;
     float* eval_grad_ = nullptr;
     double* eval_scratch_ = nullptr;

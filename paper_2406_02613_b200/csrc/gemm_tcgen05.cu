@@ -313,6 +313,7 @@ void dispatch_major(const GemmOperand& A, const GemmOperand& B, int M, int N, in
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
                cudaStream_t stream) {
     ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_bf16: empty problem");
+    ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
     // Wide tiles amortise the A re-reads; narrow N (e.g. attn-proj, N=768) keeps
     // enough CTAs in flight to fill 148 SMs.
     const long long tiles256 = static_cast<long long>(ceil_div(N, 256)) * ceil_div(M, kBM);

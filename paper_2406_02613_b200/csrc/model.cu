@@ -8,6 +8,7 @@
 #include "model.h"
 
 #include <cmath>
+#include <cstring>
 
 namespace acco {
 
@@ -85,6 +86,7 @@ void lm_default_theta0(const LMConfig& c, uint64_t master_seed, float* out) {
 // ------------------------------------------------------------------- model
 namespace {
 enum Slot { sX, sH1, sQKV, sY, sXM, sH2, sA, sU, kPerLayer };
+constexpr int kStages = 4;  // host-data staging slots in flight
 }
 
 GPTModel::GPTModel(const LMConfig& c) : c_(c) {
@@ -131,6 +133,15 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     std::vector<int32_t> data = lm_dataset(c);
     ACCO_CUDA(cudaMalloc(&data_, data.size() * sizeof(int32_t)));
     ACCO_CUDA(cudaMemcpy(data_, data.data(), data.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (c.host_data) {
+        const size_t row = static_cast<size_t>(c.seq_len) + 1;
+        ACCO_CUDA(cudaHostAlloc(&pinned_data_, data.size() * sizeof(int32_t), cudaHostAllocDefault));
+        std::memcpy(pinned_data_, data.data(), data.size() * sizeof(int32_t));
+        ACCO_CUDA(cudaHostAlloc(&stage_host_, kStages * c.max_batch * row * sizeof(int32_t), cudaHostAllocDefault));
+        ACCO_CUDA(cudaMalloc(&stage_dev_, kStages * c.max_batch * row * sizeof(int32_t)));
+        stage_ev_.resize(kStages);
+        for (auto& e : stage_ev_) ACCO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     ACCO_CUDA(cudaMalloc(&tok_in_, M * sizeof(int32_t)));
     ACCO_CUDA(cudaMalloc(&tok_out_, M * sizeof(int32_t)));
     ACCO_CUDA(cudaMalloc(&idx_, c.max_batch * sizeof(int32_t)));
@@ -155,6 +166,31 @@ GPTModel::~GPTModel() {
     cudaFree(lse_);
     cudaFree(dsum_);
     cudaFree(scratch_);
+    if (pinned_data_) cudaFreeHost(pinned_data_);
+    if (stage_host_) cudaFreeHost(stage_host_);
+    if (stage_dev_) cudaFree(stage_dev_);
+    for (auto& e : stage_ev_) cudaEventDestroy(e);
+}
+
+// Host data-loader path: draw the B sample indices on the host
+// (Stream(seed).below(n), problems.cpp:442-444), copy those token rows into a
+// pinned staging slot and ship them H2D on the compute stream.
+const int32_t* GPTModel::stage_tokens(uint64_t seed, int B, cudaStream_t s) {
+    const size_t row = static_cast<size_t>(c_.seq_len) + 1;
+    const int slot = stage_next_;
+    stage_next_ = (stage_next_ + 1) % kStages;
+    ACCO_CUDA(cudaEventSynchronize(stage_ev_[static_cast<size_t>(slot)]));  // slot's previous H2D done
+    int32_t* h = stage_host_ + static_cast<size_t>(slot) * c_.max_batch * row;
+    int32_t* d = stage_dev_ + static_cast<size_t>(slot) * c_.max_batch * row;
+    Stream st(seed);
+    for (int b = 0; b < B; ++b) {
+        const uint64_t idx = st.below(static_cast<uint64_t>(c_.n_samples));
+        std::memcpy(h + b * row, pinned_data_ + idx * row, row * sizeof(int32_t));
+    }
+    ACCO_CUDA(cudaMemcpyAsync(d, h, B * row * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    ACCO_CUDA(cudaEventRecord(stage_ev_[static_cast<size_t>(slot)], s));
+    h2d_bytes_ += static_cast<long long>(B * row * sizeof(int32_t));
+    return d;
 }
 
 namespace {
@@ -230,7 +266,10 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     auto li = [&](int l, int j) { return 2 + 12 * l + j; };  // j: 0 ln1w 1 ln1b 2 Wqkv 3 bqkv 4 Wproj 5 bproj
                                                             //    6 ln2w 7 ln2b 8 Wfc 9 bfc 10 Wfc2 11 bfc2
 
-    gather_tokens(data_, Tq, c_.n_samples, seed, mode, start, B, tok_in_, tok_out_, idx_, s);
+    if (host_data() && mode == 0)
+        gather_tokens(stage_tokens(seed, B, s), Tq, B, 0, 1, 0, B, tok_in_, tok_out_, idx_, s);
+    else
+        gather_tokens(data_, Tq, c_.n_samples, seed, mode, start, B, tok_in_, tok_out_, idx_, s);
     embed_fwd<T>(tok_in_, W(kWte), W(kWpe), X(0), M, Tq, d, s);
     for (int l = 0; l < L; ++l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),

@@ -22,6 +22,7 @@ struct LMConfig {
     uint64_t data_seed = 1;
     int precision = 0;  // 0 = fp32 (parity), 1 = bf16 (tcgen05 throughput)
     int max_batch = 8;  // samples per micro-batch (workspace sizing)
+    int host_data = 0;  // 1: per-micro-batch H2D of the token rows from pinned host memory
 };
 
 struct ParamSpec {
@@ -63,6 +64,8 @@ public:
     // Forward only (loss), used by evaluation when no gradient is needed.
     void forward_loss(const void* params, uint64_t stream_seed, int mode, int start, int B, double* loss_sum,
                       cudaStream_t s);
+    bool host_data() const { return c_.host_data != 0; }
+    long long h2d_bytes() const { return h2d_bytes_; }
 
 private:
     template <class T>
@@ -85,6 +88,14 @@ private:
     float* dsum_ = nullptr;
     float* scratch_ = nullptr;  // column-reduce partials
     std::vector<char*> act_;    // activation slots (see model.cu)
+    // host-data path
+    int32_t* pinned_data_ = nullptr;
+    int32_t* stage_host_ = nullptr;  // [kStages][max_batch*(seq+1)] pinned
+    int32_t* stage_dev_ = nullptr;
+    std::vector<cudaEvent_t> stage_ev_;
+    int stage_next_ = 0;
+    long long h2d_bytes_ = 0;
+    const int32_t* stage_tokens(uint64_t seed, int B, cudaStream_t s);
 };
 
 }  // namespace acco

@@ -217,6 +217,12 @@ void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* g
                      (!out || (reinterpret_cast<uintptr_t>(out) & (out_dtype == ACCO_DTYPE_BF16 ? 7 : 15)) == 0);
     const bool has_ret = gret != nullptr;
     ACCO_REQUIRE(out_dtype == ACCO_DTYPE_F32 || out_dtype == ACCO_DTYPE_BF16, "optimizer: bad out dtype");
+    // algorithmic bytes per element: reads g (+ retained),
+    // theta (+ m, v); commit writes theta (+ m, v); payload 2 (bf16) / 4 B.
+    const int mv = cfg.kind != 0 ? 8 : 0;
+    const double per_elem = 4.0 + (has_ret ? 4 : 0) + 4 + mv + (commit ? 4 + mv : 0) +
+                            (out ? (out_dtype == ACCO_DTYPE_BF16 ? 2 : 4) : 0);
+    ProfScope prof(kProfOpt, per_elem * static_cast<double>(n), stream);
 #define ACCO_OPT_DISPATCH(C)                                                                    \
     if (out_dtype == ACCO_DTYPE_BF16) {                                                         \
         if (has_ret) launch_kind<C, true, __nv_bfloat16>(cfg.kind, a, vec, stream);             \
