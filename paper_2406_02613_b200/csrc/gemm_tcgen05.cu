@@ -1,22 +1,31 @@
-// bf16 GEMM on the 5th-generation tensor cores (sm_100a).
+// bf16 GEMM on the 5th-generation tensor cores (sm_100a), persistent.
 //
-// One CTA computes a 128 x BN output tile:
-//   warp 0  : TMA producer (one elected lane) — K-major or MN-major operand
-//             tiles, 128B-swizzled, into a STAGES-deep smem ring
-//   warp 1  : MMA issuer (one lane) — tcgen05.mma.cta_group::1.kind::f16,
-//             fp32 accumulator in TMEM, tcgen05.commit frees smem slots
-//   warp 2  : TMEM allocator
-//   warps 4-7: epilogue — tcgen05.ld TMEM -> registers -> fused epilogue
-//             (bias / GELU / dGELU / residual / fp32 gradient accumulate)
+// One CTA per SM loops over 128 x BN output tiles (grouped raster for L2 reuse):
+//   warp 0   : TMA producer (one lane) — K-major or MN-major 128B-swizzled
+//              operand tiles into a STAGES-deep smem ring (mbarrier full/empty)
+//   warp 1   : MMA issuer (one lane) — tcgen05.mma.cta_group::1.kind::f16,
+//              fp32 accumulators in TMEM, TWO accumulator buffers (2 x BN
+//              columns) so the epilogue of tile i overlaps the MMAs of tile i+1
+//   warp 2   : TMEM allocator
+//   warps 4-7: epilogue — per 32x32 chunk: tcgen05.ld -> fused math (bias /
+//              GELU / dGELU / residual) -> swizzled smem -> TMA bulk-tensor
+//              store (bf16), or TMA bulk *reduce-add* into the fp32 gradient
+//              accumulator (beta = 1); residual / GELU-aux inputs arrive by TMA
+//              one chunk ahead. No per-element address math or uncoalesced
+//              stores on the SM: the TMA engine does the global traffic.
+// Split-K (work unit = tile x k-split) for the weight-gradient GEMMs whose tile
+// count cannot fill 148 SMs: each split TMA-stores an fp32 slab, a fixed-order
+// reduce adds the slabs into C — deterministic, no atomics.
 //
-// This is the K1/K3 kernel of SURVEY.md §2.3: forward (both operands K-major),
-// dgrad (B MN-major) and wgrad (both MN-major, fp32 beta=1 epilogue into the
-// gradient-accumulation buffer, i.e. Bundle::add of
-// /root/reference/proj/src/protocols.cpp:61-66 fused into the GEMM).
+// This is K1/K3 of SURVEY.md §2.3: forward (both operands K-major), dgrad (B
+// MN-major) and wgrad (both MN-major, fp32 accumulate epilogue into the
+// gradient-accumulation buffer: the reference's Bundle::add,
+// /root/reference/proj/src/protocols.cpp:61-66, fused into the GEMM).
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "gemm.h"
 
+#include <cstring>
 #include <mutex>
 
 namespace acco {
@@ -25,6 +34,9 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one SW128 row
 constexpr int kThreads = 256;
+constexpr int kGroupM = 8;
+constexpr int kEpiWarpBytes = 8192;  // per epilogue warp: 2 x (out + in/aux) bf16 chunks, or 2 x fp32 chunks
+constexpr int kEpiBytes = 4 * kEpiWarpBytes;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -34,9 +46,11 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
@@ -50,26 +64,46 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t a = smem_u32(bar);
+    const uint32_t a = smem_u32(bar);
     while (!mbar_try_wait(a, parity)) {
     }
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
 }
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accum) {
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
@@ -77,22 +111,19 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(bar))
-        : "memory");
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
         "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-          "=r"(v[31])
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -117,14 +148,92 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + (2 * STAGES + 1) * 8 + 16;
+    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + kEpiBytes + (2 * STAGES + 4 + 8) * 8 + 16;
 }
+
+struct Sched {
+    int tiles_m, tiles_n, splits, kb_total, kb_per_split;
+    __host__ __device__ int units() const { return tiles_m * tiles_n * splits; }
+};
+
+// unit -> (m block, n block, split); grouped raster over M for L2 reuse of B
+__device__ __forceinline__ void decode(const Sched& s, int u, int& mb, int& nb, int& sp) {
+    const int tiles = s.tiles_m * s.tiles_n;
+    sp = u / tiles;
+    const int t = u % tiles;
+    const int per_group = kGroupM * s.tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * kGroupM;
+    const int gsize = min(s.tiles_m - first_m, kGroupM);
+    const int r = t % per_group;
+    mb = first_m + r % gsize;
+    nb = r / gsize;
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// bf16-path GELU (tanh form) on the MUFU tanh; error << bf16 rounding
+__device__ __forceinline__ float gelu_fast(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.0f + tanh_fast(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float dgelu_fast(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float t = tanh_fast(k0 * (x + k1 * x * x * x));
+    return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x * x);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// One 32 x 32 bf16 chunk in smem as TMA SWIZZLE_64B lays it out: row r at
+// r*64, 16B unit c at (c ^ ((r >> 1) & 3)).
+__device__ __forceinline__ void st_row_bf16(uint8_t* buf, int r, const float* v) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint4 u = make_uint4(pack_bf16(v[8 * c + 0], v[8 * c + 1]), pack_bf16(v[8 * c + 2], v[8 * c + 3]),
+                             pack_bf16(v[8 * c + 4], v[8 * c + 5]), pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+        *reinterpret_cast<uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4)) = u;
+    }
+}
+__device__ __forceinline__ void ld_row_bf16(const uint8_t* buf, int r, float* v) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint4 u = *reinterpret_cast<const uint4*>(buf + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
+            v[8 * c + 2 * k] = __bfloat162float(h.x);
+            v[8 * c + 2 * k + 1] = __bfloat162float(h.y);
+        }
+    }
+}
+// One 32 x 32 fp32 chunk as TMA SWIZZLE_128B lays it out: row r at r*128,
+// 16B unit c at (c ^ (r & 7)).
+__device__ __forceinline__ void st_row_f32(uint8_t* buf, int r, const float* v) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<float4*>(buf + r * 128 + ((c ^ (r & 7)) << 4)) =
+            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+}
+
+struct EpiMaps {
+    CUtensorMap out;  // bf16 2D {N, M} box 32x32 SW64, or fp32 3D {N, M, slabs} box 32x32x1 SW128
+    CUtensorMap aux;  // bf16 2D: GELU pre-activation (written in kEpiGelu, read in kEpiDGelu)
+    CUtensorMap res;  // bf16 2D: residual input
+};
 
 // --------------------------------------------------------------------- kernel
 template <int BN, int STAGES, int A_MN, int B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, Epilogue ep) {
+                   const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int split_slabs) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -132,116 +241,248 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int B_BYTES = BN * kBK * 2;
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint8_t* sEpi = sB + STAGES * B_BYTES;  // 1024-aligned
+    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + kEpiBytes);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint64_t* inbar = tempty + 2;      // [4 warps][2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * kBM;
-    const int n0 = blockIdx.x * BN;
-    const int num_kb = (K + kBK - 1) / kBK;
+    const int nunits = sc.units();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+        }
+        for (int i = 0; i < 8; ++i) mbar_init(&inbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(BN));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(2 * BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_d = *tmem_slot;
+    const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                uint8_t* a_dst = sA + s * A_BYTES;
-                uint8_t* b_dst = sB + s * B_BYTES;
-                if (A_MN) {
+            int it = 0;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                int mb, nb, sp;
+                decode(sc, u, mb, nb, sp);
+                const int m0 = mb * kBM, n0 = nb * BN;
+                const int kb0 = sp * sc.kb_per_split;
+                const int kb1 = min(sc.kb_total, kb0 + sc.kb_per_split);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                    uint8_t* a_dst = sA + s * A_BYTES;
+                    uint8_t* b_dst = sB + s * B_BYTES;
+                    if (A_MN) {
 #pragma unroll
-                    for (int j = 0; j < kBM / 64; ++j)
-                        tma_load_2d(a_dst + j * 64 * kBK * 2, &tmA, &full[s], m0 + j * 64, kb * kBK);
-                } else {
-                    tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m0);
-                }
-                if (B_MN) {
+                        for (int j = 0; j < kBM / 64; ++j)
+                            tma_load_2d(a_dst + j * 64 * kBK * 2, &tmA, &full[s], m0 + j * 64, kb * kBK);
+                    } else {
+                        tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m0);
+                    }
+                    if (B_MN) {
 #pragma unroll
-                    for (int j = 0; j < BN / 64; ++j)
-                        tma_load_2d(b_dst + j * 64 * kBK * 2, &tmB, &full[s], n0 + j * 64, kb * kBK);
-                } else {
-                    tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0);
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_2d(b_dst + j * 64 * kBK * 2, &tmB, &full[s], n0 + j * 64, kb * kBK);
+                    } else {
+                        tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16(kBM, BN, A_MN, B_MN);
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&full[s], ph);
+            int it = 0, lt = 0;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
+                int mb, nb, sp;
+                decode(sc, u, mb, nb, sp);
+                const int kb0 = sp * sc.kb_per_split;
+                const int kb1 = min(sc.kb_total, kb0 + sc.kb_per_split);
+                const int acc = lt & 1;
+                mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
                 tc_fence_after();
-                const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-                const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+                    const uint32_t b_base = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-                for (int kk = 0; kk < kBK / 16; ++kk) {
-                    // K-major: advance 16 elements (32 B) inside the 128B swizzle row.
-                    // MN-major: advance 16 K-rows = two 8-row atoms (2048 B).
-                    uint64_t ad = A_MN ? sdesc(a_base + kk * 2048, 64 * kBK * 2, 1024)
-                                       : sdesc(a_base + kk * 32, 16, 1024);
-                    uint64_t bd = B_MN ? sdesc(b_base + kk * 2048, 64 * kBK * 2, 1024)
-                                       : sdesc(b_base + kk * 32, 16, 1024);
-                    umma_bf16(tmem_d, ad, bd, idesc, (kb | kk) != 0);
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        // K-major: advance 16 elements (32 B) inside the 128B swizzle row.
+                        // MN-major: advance 16 K-rows = two 8-row atoms (2048 B).
+                        const uint64_t ad = A_MN ? sdesc(a_base + kk * 2048, 64 * kBK * 2, 1024)
+                                                 : sdesc(a_base + kk * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? sdesc(b_base + kk * 2048, 64 * kBK * 2, 1024)
+                                                 : sdesc(b_base + kk * 32, 16, 1024);
+                        umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
                 }
-                umma_commit(&empty[s]);
+                umma_commit(&tfull[acc]);
             }
-            umma_commit(tmem_full);
         }
     } else if (warp >= 4) {
         const int wq = warp - 4;
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-        const int row = m0 + wq * 32 + lane;
-        for (int c = 0; c < BN; c += 32) {
-            uint32_t v[32];
-            tmem_ld32(tmem_d + (static_cast<uint32_t>(wq * 32) << 16) + c, v);
-            const int col = n0 + c;
-            if (row < M && col < N) {
-                float x[32];
+        uint8_t* wbuf = sEpi + wq * kEpiWarpBytes;
+        uint64_t* ib = inbar + 2 * wq;
+        const bool f32 = ep.mode == kEpiAccF32;
+        const bool has_in = !f32 && (ep.mode == kEpiDGelu || ep.residual != nullptr);
+        const CUtensorMap* in_map = ep.mode == kEpiDGelu ? &em.aux : &em.res;
+        const __nv_bfloat16* bias = static_cast<const __nv_bfloat16*>(ep.bias);
+        uint32_t in_phase = 0;  // bit b: parity of the next wait on input buffer b
+        constexpr int kChunks = BN / 32;
+        int lt = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
+            int mb, nb, sp;
+            decode(sc, u, mb, nb, sp);
+            const int acc = lt & 1;
+            const int row0 = mb * kBM + wq * 32;
+            const int n0 = nb * BN;
+            if (has_in && lane == 0) {  // input chunk 0 of this tile
+                mbar_expect_tx(&ib[0], 2048);
+                tma_load_2d(wbuf + 4096, in_map, &ib[0], n0, row0);
+            }
+            mbar_wait(&tfull[acc], (lt >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < kChunks; ++c) {
+                const int b = c & 1;
+                const int col0 = n0 + c * 32;
+                if (has_in && lane == 0 && c + 1 < kChunks) {  // next input chunk, one ahead
+                    mbar_expect_tx(&ib[b ^ 1], 2048);
+                    tma_load_2d(wbuf + 4096 + (b ^ 1) * 2048, in_map, &ib[b ^ 1], col0 + 32, row0);
+                }
+                uint32_t raw[32];
+                tmem_ld32(tbase + c * 32, raw);
+                if (c == kChunks - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                }
+                float v[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) x[i] = __uint_as_float(v[i]);
-                epilogue_row<__nv_bfloat16, 32>(ep, row, col, min(32, N - col), x);
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(raw[i]);
+                if (bias) {
+                    if (col0 + 32 <= N) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint4 u4 = *reinterpret_cast<const uint4*>(bias + col0 + 8 * q);
+                            const uint32_t w[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
+                                v[8 * q + 2 * k] += __bfloat162float(h.x);
+                                v[8 * q + 2 * k + 1] += __bfloat162float(h.y);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (col0 + i < N) v[i] += __bfloat162float(bias[col0 + i]);
+                    }
+                }
+                if (has_in) {
+                    mbar_wait(&ib[b], (in_phase >> b) & 1);
+                    in_phase ^= 1u << b;
+                    float iv[32];
+                    ld_row_bf16(wbuf + 4096 + b * 2048, lane, iv);
+                    if (ep.mode == kEpiDGelu) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(iv[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] += iv[i];
+                    }
+                }
+                // the TMA store that last used these staging buffers (chunk c-2)
+                // must have finished reading them
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                if (f32) {
+                    uint8_t* ob = wbuf + b * 4096;
+                    st_row_f32(ob, lane, v);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (split_slabs > 1)
+                            tma_store_3d(&em.out, ob, col0, row0, sp);
+                        else if (ep.beta)
+                            tma_reduce_add_3d(&em.out, ob, col0, row0, 0);
+                        else
+                            tma_store_3d(&em.out, ob, col0, row0, 0);
+                        bulk_commit();
+                    }
+                } else {
+                    uint8_t* ob = wbuf + b * 2048;
+                    if (ep.mode == kEpiGelu) {
+                        st_row_bf16(wbuf + 4096 + b * 2048, lane, v);  // pre-activation (aux)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
+                    }
+                    st_row_bf16(ob, lane, v);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&em.out, ob, col0, row0);
+                        if (ep.mode == kEpiGelu) tma_store_2d(&em.aux, wbuf + 4096 + b * 2048, col0, row0);
+                        bulk_commit();
+                    }
+                }
             }
         }
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+    }
+}
+
+// C = beta*C + sum_s slab[s] (fixed order)
+__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C,
+                              int64_t ldc, int beta) {
+    const int64_t total = static_cast<int64_t>(M) * N;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        float s = 0.f;
+        for (int k = 0; k < splits; ++k) s += ws[static_cast<int64_t>(k) * total + i];
+        const int64_t r = i / N, c = i % N;
+        float* o = C + r * ldc + c;
+        *o = beta ? *o + s : s;
     }
 }
 
 // ----------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
-                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                              CUtensorMapFloatOOBfill);
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeFn encode_fn() {
     static EncodeFn fn = nullptr;
@@ -250,62 +491,124 @@ EncodeFn encode_fn() {
         void* p = nullptr;
         cudaDriverEntryPointQueryResult q;
         ACCO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        if (q != cudaDriverEntryPointSuccess || !p)
-            throw Error(kCudaError, "cuTensorMapEncodeTiled unavailable");
+        if (q != cudaDriverEntryPointSuccess || !p) throw Error(kCudaError, "cuTensorMapEncodeTiled unavailable");
         fn = reinterpret_cast<EncodeFn>(p);
     });
     return fn;
 }
 
-// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows.
-CUtensorMap make_map(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                     uint32_t box_inner, uint32_t box_outer) {
+CUtensorMap encode(CUtensorMapDataType dt, int rank, const void* ptr, const cuuint64_t* dims,
+                   const cuuint64_t* strides, const cuuint32_t* box, CUtensorMapSwizzle sw) {
     ACCO_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "gemm: operand not 16B aligned");
-    ACCO_REQUIRE((ld_elems * 2) % 16 == 0, "gemm: leading dimension must be a multiple of 8");
+    for (int i = 0; i < rank - 1; ++i) ACCO_REQUIRE(strides[i] % 16 == 0, "gemm: row stride must be a multiple of 16 bytes");
     CUtensorMap m;
-    cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {ld_elems * 2};
-    cuuint32_t box[2] = {box_inner, box_outer};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
-                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, dt, rank, const_cast<void*>(ptr), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(kCudaError, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
 }
 
+// 2-D bf16 tensor map: `inner` contiguous elements per row, `outer` rows.
+CUtensorMap make_map(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems, uint32_t box_inner,
+                     uint32_t box_outer, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {ld_elems * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    return encode(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, sw);
+}
+
+// 3-D fp32 map {N, M, slabs} for the accumulate / split-K epilogue.
+CUtensorMap make_map_f32(const void* ptr, uint64_t n, uint64_t m, uint64_t slabs, uint64_t ld_elems) {
+    cuuint64_t dims[3] = {n, m, slabs};
+    cuuint64_t strides[2] = {ld_elems * 4, ld_elems * 4 * m};
+    cuuint32_t box[3] = {32, 32, 1};
+    return encode(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 // Tensor map for an operand with `rows` (M or N) and reduction extent K.
 CUtensorMap operand_map(const GemmOperand& op, int rows, int K, int tile_rows) {
-    if (op.mn_major)  // stored [K][rows]: inner = rows
-        return make_map(op.ptr, rows, K, op.ld, 64, kBK);
-    return make_map(op.ptr, K, rows, op.ld, kBK, tile_rows);  // stored [rows][K]
+    if (op.mn_major) return make_map(op.ptr, rows, K, op.ld, 64, kBK);  // stored [K][rows]
+    return make_map(op.ptr, K, rows, op.ld, kBK, tile_rows);             // stored [rows][K]
+}
+
+float* split_workspace(size_t floats) {
+    static float* ws = nullptr;
+    static size_t cap = 0;
+    if (floats > cap) {
+        if (ws) ACCO_CUDA(cudaFree(ws));
+        ACCO_CUDA(cudaMalloc(&ws, floats * sizeof(float)));
+        cap = floats;
+    }
+    return ws;
 }
 
 template <int BN, int STAGES, int A_MN, int B_MN>
-void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
+void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep, int splits,
             cudaStream_t stream) {
     auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN>;
     constexpr int smem = smem_bytes<BN, STAGES>();
+    static_assert(smem <= 232448, "shared memory budget");
     static bool configured = false;  // per instantiation
     if (!configured) {
         ACCO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         configured = true;
     }
+    Sched sc;
+    sc.tiles_m = ceil_div(M, kBM);
+    sc.tiles_n = ceil_div(N, BN);
+    sc.kb_total = ceil_div(K, kBK);
+    sc.splits = splits;
+    sc.kb_per_split = ceil_div(sc.kb_total, splits);
+    sc.splits = ceil_div(sc.kb_total, sc.kb_per_split);  // no empty splits
+    EpiMaps em;
+    std::memset(&em, 0, sizeof(em));
+    float* ws = nullptr;
+    if (ep.mode == kEpiAccF32) {
+        if (sc.splits > 1) {
+            ws = split_workspace(static_cast<size_t>(sc.splits) * M * N);
+            em.out = make_map_f32(ws, N, M, sc.splits, N);
+        } else {
+            em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
+        }
+    } else {
+        em.out = make_map(ep.C, N, M, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (ep.aux) em.aux = make_map(ep.aux, N, M, ep.ld_aux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        if (ep.residual) em.res = make_map(ep.residual, N, M, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
     CUtensorMap ta = operand_map(A, M, K, kBM);
     CUtensorMap tb = operand_map(B, N, K, BN);
-    dim3 grid(ceil_div(N, BN), ceil_div(M, kBM));
-    kern<<<grid, kThreads, smem, stream>>>(ta, tb, M, N, K, ep);
+    const int grid = std::min(sc.units(), num_sms());
+    kern<<<grid, kThreads, smem, stream>>>(ta, tb, em, M, N, sc, ep, sc.splits);
     ACCO_CHECK_LAUNCH();
+    if (ws) {
+        const int64_t total = static_cast<int64_t>(M) * N;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, num_sms() * 8));
+        splitk_reduce<<<blocks, 256, 0, stream>>>(ws, sc.splits, M, N, static_cast<float*>(ep.C), ep.ldc, ep.beta);
+        ACCO_CHECK_LAUNCH();
+    }
 }
 
 template <int BN, int STAGES>
-void dispatch_major(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
-                    const Epilogue& ep, cudaStream_t s) {
-    if (!A.mn_major && !B.mn_major) launch<BN, STAGES, 0, 0>(A, B, M, N, K, ep, s);
-    else if (!A.mn_major && B.mn_major) launch<BN, STAGES, 0, 1>(A, B, M, N, K, ep, s);
-    else if (A.mn_major && !B.mn_major) launch<BN, STAGES, 1, 0>(A, B, M, N, K, ep, s);
-    else launch<BN, STAGES, 1, 1>(A, B, M, N, K, ep, s);
+void dispatch_major(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep, int splits,
+                    cudaStream_t s) {
+    if (!A.mn_major && !B.mn_major) launch<BN, STAGES, 0, 0>(A, B, M, N, K, ep, splits, s);
+    else if (!A.mn_major && B.mn_major) launch<BN, STAGES, 0, 1>(A, B, M, N, K, ep, splits, s);
+    else if (A.mn_major && !B.mn_major) launch<BN, STAGES, 1, 0>(A, B, M, N, K, ep, splits, s);
+    else launch<BN, STAGES, 1, 1>(A, B, M, N, K, ep, splits, s);
+}
+
+// Relative cost model for tile-shape / split-K selection: waves of work units
+// times per-unit work, with narrower tiles paying for their lower operand reuse.
+double plan_cost(int M, int N, int K, int bn, int splits, int sms) {
+    const int units = ceil_div(M, kBM) * ceil_div(N, bn) * splits;
+    const double waves = std::ceil(static_cast<double>(units) / sms);
+    const double kb = std::ceil(static_cast<double>(ceil_div(K, kBK)) / splits);
+    const double eff = bn == 256 ? 1.0 : 1.25;
+    double c = waves * bn * kb * eff;
+    if (splits > 1) c += 0.02 * static_cast<double>(M) * N * (splits + 1) / (128.0 * 64.0);  // reduce pass
+    return c;
 }
 
 }  // namespace
@@ -313,14 +616,28 @@ void dispatch_major(const GemmOperand& A, const GemmOperand& B, int M, int N, in
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
                cudaStream_t stream) {
     ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_bf16: empty problem");
+    ACCO_REQUIRE(!(ep.residual && (ep.mode == kEpiGelu || ep.mode == kEpiDGelu)),
+                 "gemm_bf16: residual add is not combined with the GELU epilogues");
+    ACCO_REQUIRE(ep.mode == kEpiStore || ep.mode == kEpiAccF32 || ep.aux, "gemm_bf16: GELU epilogues need aux");
     ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
-    // Wide tiles amortise the A re-reads; narrow N (e.g. attn-proj, N=768) keeps
-    // enough CTAs in flight to fill 148 SMs.
-    const long long tiles256 = static_cast<long long>(ceil_div(N, 256)) * ceil_div(M, kBM);
-    if (N >= 256 && tiles256 >= 148)
-        dispatch_major<256, 4>(A, B, M, N, K, ep, stream);
+    const int sms = num_sms();
+    int best_bn = 256, best_sp = 1;
+    double best = 1e300;
+    for (int bn : {256, 128}) {
+        for (int sp : {1, 2, 3, 4, 6, 8}) {
+            if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp)) continue;
+            const double c = plan_cost(M, N, K, bn, sp, sms);
+            if (c < best * 0.97) {
+                best = c;
+                best_bn = bn;
+                best_sp = sp;
+            }
+        }
+    }
+    if (best_bn == 256)
+        dispatch_major<256, 4>(A, B, M, N, K, ep, best_sp, stream);
     else
-        dispatch_major<128, 6>(A, B, M, N, K, ep, stream);
+        dispatch_major<128, 6>(A, B, M, N, K, ep, best_sp, stream);
 }
 
 }  // namespace acco

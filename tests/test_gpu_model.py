@@ -115,6 +115,30 @@ def test_bf16_gradient_close_to_oracle(cuda, name):
     assert _rel(g, og * B) <= 3e-2
 
 
+@pytest.mark.parametrize("seq", [128, 100, 256])
+def test_bf16_tensor_core_attention_per_tensor(cuda, seq):
+    """head size 64 routes attention to the mma.sync flash kernels; check every
+    weight tensor's gradient separately so an attention-backward error cannot
+    hide under the (large) embedding gradient."""
+    c = dict(vocab=128, d_model=128, n_layer=2, n_head=2, seq_len=seq, n_samples=16, data_seed=4)
+    B = 3
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=B))
+    gc = G.GPTConfig(**c)
+    rng = np.random.default_rng(2)
+    th = (G.default_theta0(gc, 3) + 0.05 * rng.standard_normal(m.dim)).astype(np.float32)
+    th_bf = torch.tensor(th).to(torch.bfloat16)
+    seed = O.derive(4, 1, 0, 2, 0)
+    g, loss_sum = _grad(m, th_bf.to(cuda), seed, B, cuda)
+    og, _, ol = G.LMProblem(gc).stochastic_grad(th_bf.float().double().numpy(), seed, B)
+    og = og * B
+    assert abs(loss_sum / B - ol) <= 1e-2 * abs(ol)
+    for name, shape, _, off in G.param_layout(gc):
+        n = int(np.prod(shape))
+        if n < 1024:
+            continue
+        assert _rel(g[off:off + n], og[off:off + n]) <= 5e-2, name
+
+
 def test_micro_batch_bounds(cuda):
     m = api.Model(api.LMConfig(**CFGS["tiny"], precision="fp32", max_batch=2))
     pt = torch.zeros(m.dim, device=cuda)
