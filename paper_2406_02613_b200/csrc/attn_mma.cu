@@ -47,6 +47,11 @@ __device__ __forceinline__ void mma(float* c, const uint32_t* a, uint32_t b0, ui
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2; ex2(-inf) = 0
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ uint32_t pack(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -141,16 +146,23 @@ __global__ void __launch_bounds__(kThreads) fa_fwd(const __nv_bfloat16* __restri
         if (j == 0) load_a(qa, sQ, warp * 16);
         float s[8][4] = {};
         mma_abt(s, qa, sK[j & 1]);
-        // scale (log2 domain) + causal / length mask
-        const int qr = q0 + warp * 16 + (t >> 2);
+        // scale (log2 domain); causal / length mask only on the diagonal tile
+        if (j == qt) {
+            const int qr = q0 + warp * 16 + (t >> 2);
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt)
+            for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int key = j * BR + nt * 8 + (t & 3) * 2 + (e & 1);
-                const int q = qr + (e >> 1) * 8;
-                s[nt][e] = (key > q || key >= T) ? -INFINITY : s[nt][e] * sl;
-            }
+                for (int e = 0; e < 4; ++e) {
+                    const int key = j * BR + nt * 8 + (t & 3) * 2 + (e & 1);
+                    const int q = qr + (e >> 1) * 8;
+                    s[nt][e] = (key > q || key >= T) ? -INFINITY : s[nt][e] * sl;
+                }
+        } else {
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) s[nt][e] *= sl;
+        }
 #pragma unroll
         for (int hr = 0; hr < 2; ++hr) {
             float mx = m[hr];
@@ -158,13 +170,14 @@ __global__ void __launch_bounds__(kThreads) fa_fwd(const __nv_bfloat16* __restri
             for (int nt = 0; nt < 8; ++nt) mx = fmaxf(mx, fmaxf(s[nt][2 * hr], s[nt][2 * hr + 1]));
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float alpha = (m[hr] == -INFINITY) ? 0.f : exp2f(m[hr] - mx);
+            // key 0 is always visible, so mx is finite after the first tile
+            const float alpha = ex2(m[hr] - mx);
             m[hr] = mx;
             float rs = 0.f;
 #pragma unroll
             for (int nt = 0; nt < 8; ++nt) {
-                const float p0 = (mx == -INFINITY) ? 0.f : exp2f(s[nt][2 * hr] - mx);
-                const float p1 = (mx == -INFINITY) ? 0.f : exp2f(s[nt][2 * hr + 1] - mx);
+                const float p0 = ex2(s[nt][2 * hr] - mx);
+                const float p1 = ex2(s[nt][2 * hr + 1] - mx);
                 s[nt][2 * hr] = p0;
                 s[nt][2 * hr + 1] = p1;
                 rs += p0 + p1;
@@ -250,14 +263,18 @@ __global__ void __launch_bounds__(kThreads) fa_bwd_dkv(const __nv_bfloat16* __re
         float dp[8][4] = {};
         mma_abt(dp, va, sO[buf]);  // dP^T = V dO^T
         const int kr = k0 + warp * 16 + (t >> 2);
+        const bool edge = it == kt || it == nkt - 1;  // diagonal or ragged tail
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const int qi = nt * 8 + (t & 3) * 2 + (e & 1);
-                const int q = it * BR + qi;
-                const int key = kr + (e >> 1) * 8;
-                const float p = (q < key || q >= T || key >= T) ? 0.f : exp2f(s[nt][e] * sl - sL[buf][qi]);
+                float p = ex2(s[nt][e] * sl - sL[buf][qi]);
+                if (edge) {
+                    const int q = it * BR + qi;
+                    const int key = kr + (e >> 1) * 8;
+                    if (q < key || q >= T || key >= T) p = 0.f;
+                }
                 s[nt][e] = p;                                   // P^T
                 dp[nt][e] = p * (dp[nt][e] - sD[buf][qi]);      // dS^T
             }
@@ -336,9 +353,12 @@ __global__ void __launch_bounds__(kThreads) fa_bwd_dq(const __nv_bfloat16* __res
         for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const int key = j * BR + nt * 8 + (t & 3) * 2 + (e & 1);
-                const int q = qr + (e >> 1) * 8;
-                const float p = (key > q || key >= T) ? 0.f : exp2f(s[nt][e] * sl - L[e >> 1]);
+                float p = ex2(s[nt][e] * sl - L[e >> 1]);
+                if (j == qt) {
+                    const int key = j * BR + nt * 8 + (t & 3) * 2 + (e & 1);
+                    const int q = qr + (e >> 1) * 8;
+                    if (key > q || key >= T) p = 0.f;
+                }
                 s[nt][e] = p * (dp[nt][e] - Dv[e >> 1]);  // dS
             }
         mma_pb(dq, s, sK[j & 1]);  // dQ += dS K

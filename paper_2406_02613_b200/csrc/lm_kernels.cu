@@ -4,6 +4,7 @@
 #include "host_util.h"
 #include "lm_kernels.h"
 
+#include <algorithm>
 #include <vector>
 
 namespace acco {
@@ -150,6 +151,101 @@ __global__ void colreduce_partial(const T* __restrict__ y, int64_t ld, const T* 
     }
 }
 
+// Vectorised column reduction: a block owns a 64-column slab x one row chunk;
+// threads = 8 column groups (8 contiguous columns, 16B bf16 loads) x 32 row
+// lanes. Partial sums per chunk go to `part`; the last block of a slab (atomic
+// ticket) folds the chunks in ascending order and adds into out (+ out1) —
+// deterministic, one launch. KIND 0: sum y; KIND 1 (LayerNorm params):
+// out += sum dy*xhat, out1 += sum dy.
+constexpr int kVecRows = 32;
+
+template <class T>
+__device__ __forceinline__ void load8(const T* p, float* v);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* v) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float* v) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+template <class T, int KIND>
+__global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y, int64_t ld, const T* __restrict__ x,
+                                                         const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                         int M, int N, int rows_per_chunk, float* __restrict__ part,
+                                                         unsigned* __restrict__ tickets, float* __restrict__ out,
+                                                         float* __restrict__ out1) {
+    __shared__ float s0[kVecRows][65], s1[kVecRows][65];
+    __shared__ bool last;
+    const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
+    const int c0 = blockIdx.x * 64 + cg * 8;
+    const int chunk = blockIdx.y, nchunk = gridDim.y;
+    const int r0 = chunk * rows_per_chunk, r1 = min(M, r0 + rows_per_chunk);
+    float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (c0 < N) {
+        for (int r = r0 + rl; r < r1; r += kVecRows) {
+            float dy[8];
+            load8<T>(y + static_cast<int64_t>(r) * ld + c0, dy);
+            if (KIND == 0) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) a0[k] += dy[k];
+            } else {
+                float xv[8];
+                load8<T>(x + static_cast<int64_t>(r) * N + c0, xv);
+                const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    a0[k] += dy[k] * ((xv[k] - mu) * rs);
+                    a1[k] += dy[k];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        s0[rl][cg * 8 + k] = a0[k];
+        s1[rl][cg * 8 + k] = a1[k];
+    }
+    __syncthreads();
+    const int ci = threadIdx.x;  // column within slab (first 64 threads)
+    const int col = blockIdx.x * 64 + ci;
+    if (ci < 64 && col < N) {
+        float t0 = 0.f, t1 = 0.f;
+        for (int i = 0; i < kVecRows; ++i) {
+            t0 += s0[i][ci];
+            t1 += s1[i][ci];
+        }
+        part[(static_cast<int64_t>(chunk) * 2 + 0) * N + col] = t0;
+        if (KIND == 1) part[(static_cast<int64_t>(chunk) * 2 + 1) * N + col] = t1;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == static_cast<unsigned>(nchunk - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (ci < 64 && col < N) {
+        float t0 = 0.f, t1 = 0.f;
+        for (int c = 0; c < nchunk; ++c) {
+            t0 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 0) * N + col]);
+            if (KIND == 1) t1 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 1) * N + col]);
+        }
+        out[col] += t0;
+        if (KIND == 1) out1[col] += t1;
+    }
+    if (threadIdx.x == 0) tickets[blockIdx.x] = 0;  // ready for the next launch (stream-ordered)
+}
+
 __global__ void colreduce_final(const float* __restrict__ part, int nchunk, int N, float* __restrict__ out) {
     const int col = blockIdx.x * blockDim.x + threadIdx.x;
     if (col >= N) return;
@@ -200,6 +296,82 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, int64_t
         float p = expf(to_f(L[c]) - lse);
         if (c == tgt) p -= 1.f;
         L[c] = from_f<T>(p * inv_seq);
+    }
+}
+
+// bf16 single-pass variant: the whole row (V <= 512 threads x 8 x NV) lives in
+// registers, so logits are read once and dlogits written once (HBM floor).
+template <int NV>
+__global__ void __launch_bounds__(512) ce_bf16_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
+                                                      const int32_t* __restrict__ target, int V, float inv_seq,
+                                                      float* __restrict__ row_loss) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    uint4* L = reinterpret_cast<uint4*>(logits + static_cast<int64_t>(row) * ld);
+    const int nvec = (V + 7) / 8;
+    uint4 r[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int idx = threadIdx.x + i * 512;
+        r[i] = idx < nvec ? L[idx] : make_uint4(0, 0, 0, 0);
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int base = (threadIdx.x + i * 512) * 8;
+        const uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float v = __uint_as_float((k & 1) ? (w[k >> 1] & 0xffff0000u) : (w[k >> 1] << 16));
+            if (base + k < V) m = fmaxf(m, v);
+        }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    m = warp_max(m);
+    if (lane == 0) red[wid] = m;
+    __syncthreads();
+    float gm = red[0];
+    for (int i = 1; i < nw; ++i) gm = fmaxf(gm, red[i]);
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int base = (threadIdx.x + i * 512) * 8;
+        const uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float v = __uint_as_float((k & 1) ? (w[k >> 1] & 0xffff0000u) : (w[k >> 1] << 16));
+            if (base + k < V) s += __expf(v - gm);
+        }
+    }
+    s = warp_sum(s);
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    float tot = 0.f;
+    for (int i = 0; i < nw; ++i) tot += red[i];
+    const float lse = gm + __logf(tot);
+    const int tgt = target[row];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const int idx = threadIdx.x + i * 512;
+        if (idx >= nvec) continue;
+        const int base = idx * 8;
+        uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
+        float p[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float v = __uint_as_float((k & 1) ? (w[k >> 1] & 0xffff0000u) : (w[k >> 1] << 16));
+            if (base + k == tgt) row_loss[row] = lse - v;
+            float q = base + k < V ? __expf(v - lse) : 0.f;
+            if (base + k == tgt) q -= 1.f;
+            p[k] = q * inv_seq;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(p[2 * k], p[2 * k + 1]);
+            w[k] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        L[idx] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -389,9 +561,42 @@ void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float*
     ACCO_CHECK_LAUNCH();
 }
 
+static unsigned* tickets() {
+    static unsigned* t = nullptr;
+    if (!t) {
+        ACCO_CUDA(cudaMalloc(&t, 8192 * sizeof(unsigned)));
+        ACCO_CUDA(cudaMemset(t, 0, 8192 * sizeof(unsigned)));
+    }
+    return t;
+}
+
+template <class T>
+static bool vec_ok(const void* p, int64_t ld, int N) {
+    return N % 8 == 0 && ld % 8 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ceil_div(N, 64) <= 8192;
+}
+
+// grid: slabs x chunks with ~2 waves of 148 SMs
+template <class T, int KIND>
+static void colsum_vec(const T* y, int64_t ld, const T* x, const float* mean, const float* rstd, int M, int N,
+                       float* out, float* out1, float* scratch, cudaStream_t s) {
+    const int slabs = ceil_div(N, 64);
+    int nchunk = std::max(1, std::min(ceil_div(2 * num_sms(), slabs), ceil_div(M, kVecRows)));
+    const int rpc = ceil_div(ceil_div(M, nchunk), kVecRows) * kVecRows;
+    nchunk = ceil_div(M, rpc);
+    colsum_vec_kernel<T, KIND><<<dim3(slabs, nchunk), 256, 0, s>>>(y, ld, x, mean, rstd, M, N, rpc, scratch,
+                                                                    tickets(), out, out1);
+    ACCO_CHECK_LAUNCH();
+}
+
 template <class T>
 void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
                    bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d, cudaStream_t s) {
+    if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d)) {
+        colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, s);
+        ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+        ACCO_CHECK_LAUNCH();
+        return;
+    }
     // parameter gradients first (they read dy only), then dx
     const int nchunk = ceil_div(M, kColChunk);
     float* p0 = scratch;
@@ -407,6 +612,10 @@ void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const
 
 template <class T>
 void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, cudaStream_t s) {
+    if (vec_ok<T>(y, ld, N)) {
+        colsum_vec<T, 0>(y, ld, nullptr, nullptr, nullptr, M, N, out, nullptr, scratch, s);
+        return;
+    }
     const int nchunk = ceil_div(M, kColChunk);
     colreduce_partial<T, 0><<<dim3(ceil_div(N, 32), nchunk), dim3(32, kColRows), 0, s>>>(
         y, ld, nullptr, nullptr, nullptr, M, N, scratch, nullptr);
@@ -418,6 +627,22 @@ void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch
 template <class T>
 void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, int seq, float* row_loss,
                    cudaStream_t s) {
+    if constexpr (sizeof(T) == 2) {
+        const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 8 == 0;
+        const int nvec = (V + 7) / 8;
+        if (aligned && nvec <= 512 * 16) {
+            auto* L = reinterpret_cast<__nv_bfloat16*>(logits);
+            const float inv = 1.0f / seq;
+            if (nvec <= 512 * 4)
+                ce_bf16_kernel<4><<<M, 512, 0, s>>>(L, ld, target, V, inv, row_loss);
+            else if (nvec <= 512 * 8)
+                ce_bf16_kernel<8><<<M, 512, 0, s>>>(L, ld, target, V, inv, row_loss);
+            else
+                ce_bf16_kernel<16><<<M, 512, 0, s>>>(L, ld, target, V, inv, row_loss);
+            ACCO_CHECK_LAUNCH();
+            return;
+        }
+    }
     ce_kernel<T><<<M, 512, 0, s>>>(logits, ld, target, V, 1.0f / seq, row_loss);
     ACCO_CHECK_LAUNCH();
 }

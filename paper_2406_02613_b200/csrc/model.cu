@@ -7,6 +7,7 @@
 #include "lm_kernels.h"
 #include "model.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -150,7 +151,9 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_CUDA(cudaMalloc(&stats_, (4 * L + 2) * M * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&lse_, L * H * M * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&dsum_, H * M * sizeof(float)));
-    const int64_t nchunk = (M + 255) / 256;
+    // column-reduction partials: [chunks][2][N] with N <= 4d; chunks <= max(M/256,
+    // 2 x SMs) (see colsum_vec / colreduce in lm_kernels.cu)
+    const int64_t nchunk = std::max<int64_t>((M + 255) / 256, 2 * num_sms());
     ACCO_CUDA(cudaMalloc(&scratch_, nchunk * 4 * d * 2 * sizeof(float)));
 }
 
