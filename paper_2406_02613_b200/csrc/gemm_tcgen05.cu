@@ -14,8 +14,9 @@
 //              one chunk ahead. No per-element address math or uncoalesced
 //              stores on the SM: the TMA engine does the global traffic.
 // Split-K (work unit = tile x k-split) for the weight-gradient GEMMs whose tile
-// count cannot fill 148 SMs: each split TMA-stores an fp32 slab, a fixed-order
-// reduce adds the slabs into C — deterministic, no atomics.
+// count cannot fill 148 SMs: splits of a tile TMA-reduce-add into C *in split
+// order* (a per-(tile, quadrant) semaphore hands the rows from split s to s+1),
+// so the fp32 sums are deterministic, with no workspace and no extra pass.
 //
 // This is K1/K3 of SURVEY.md §2.3: forward (both operands K-major), dgrad (B
 // MN-major) and wgrad (both MN-major, fp32 accumulate epilogue into the
@@ -25,6 +26,8 @@
 #include "epilogue.cuh"
 #include "gemm.h"
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -93,6 +96,15 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const 
                  "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -233,7 +245,7 @@ struct EpiMaps {
 template <int BN, int STAGES, int A_MN, int B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int split_slabs) {
+                   const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -365,6 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_expect_tx(&ib[0], 2048);
                 tma_load_2d(wbuf + 4096, in_map, &ib[0], n0, row0);
             }
+            // ordered split-K: this quadrant's rows are added in split order
+            int* sem = split_sem ? split_sem + ((mb * sc.tiles_n + nb) * 4 + wq) * 32 : nullptr;  // own 128B line
+            if (sem && lane == 0) {
+                while (ld_acquire(sem) != sp) __nanosleep(64);
+                fence_async_global();
+            }
+            __syncwarp();
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
@@ -428,9 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        if (split_slabs > 1)
-                            tma_store_3d(&em.out, ob, col0, row0, sp);
-                        else if (ep.beta)
+                        if (sp > 0 || ep.beta)
                             tma_reduce_add_3d(&em.out, ob, col0, row0, 0);
                         else
                             tma_store_3d(&em.out, ob, col0, row0, 0);
@@ -453,6 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (sem && lane == 0) {  // this split's adds are complete: hand over to split sp+1
+                bulk_wait_all();
+                fence_async_global();
+                st_release(sem, sp + 1 == sc.splits ? 0 : sp + 1);
+            }
+            __syncwarp();
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
@@ -462,20 +485,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
-    }
-}
-
-// C = beta*C + sum_s slab[s] (fixed order)
-__global__ void splitk_reduce(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C,
-                              int64_t ldc, int beta) {
-    const int64_t total = static_cast<int64_t>(M) * N;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-        float s = 0.f;
-        for (int k = 0; k < splits; ++k) s += ws[static_cast<int64_t>(k) * total + i];
-        const int64_t r = i / N, c = i % N;
-        float* o = C + r * ldc + c;
-        *o = beta ? *o + s : s;
     }
 }
 
@@ -533,15 +542,15 @@ CUtensorMap operand_map(const GemmOperand& op, int rows, int K, int tile_rows) {
     return make_map(op.ptr, K, rows, op.ld, kBK, tile_rows);             // stored [rows][K]
 }
 
-float* split_workspace(size_t floats) {
-    static float* ws = nullptr;
-    static size_t cap = 0;
-    if (floats > cap) {
-        if (ws) ACCO_CUDA(cudaFree(ws));
-        ACCO_CUDA(cudaMalloc(&ws, floats * sizeof(float)));
-        cap = floats;
+constexpr int kSemSlots = 1 << 18;  // (tile, quadrant) semaphores for ordered split-K
+
+int* split_semaphores() {
+    static int* sem = nullptr;
+    if (!sem) {
+        ACCO_CUDA(cudaMalloc(&sem, kSemSlots * sizeof(int)));
+        ACCO_CUDA(cudaMemset(sem, 0, kSemSlots * sizeof(int)));
     }
-    return ws;
+    return sem;
 }
 
 template <int BN, int STAGES, int A_MN, int B_MN>
@@ -564,13 +573,12 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     sc.splits = ceil_div(sc.kb_total, sc.kb_per_split);  // no empty splits
     EpiMaps em;
     std::memset(&em, 0, sizeof(em));
-    float* ws = nullptr;
+    int* sem = nullptr;
     if (ep.mode == kEpiAccF32) {
+        em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
         if (sc.splits > 1) {
-            ws = split_workspace(static_cast<size_t>(sc.splits) * M * N);
-            em.out = make_map_f32(ws, N, M, sc.splits, N);
-        } else {
-            em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
+            ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 4 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
+            sem = split_semaphores();
         }
     } else {
         em.out = make_map(ep.C, N, M, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -580,14 +588,8 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     CUtensorMap ta = operand_map(A, M, K, kBM);
     CUtensorMap tb = operand_map(B, N, K, BN);
     const int grid = std::min(sc.units(), num_sms());
-    kern<<<grid, kThreads, smem, stream>>>(ta, tb, em, M, N, sc, ep, sc.splits);
+    kern<<<grid, kThreads, smem, stream>>>(ta, tb, em, M, N, sc, ep, sem);
     ACCO_CHECK_LAUNCH();
-    if (ws) {
-        const int64_t total = static_cast<int64_t>(M) * N;
-        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, num_sms() * 8));
-        splitk_reduce<<<blocks, 256, 0, stream>>>(ws, sc.splits, M, N, static_cast<float*>(ep.C), ep.ldc, ep.beta);
-        ACCO_CHECK_LAUNCH();
-    }
 }
 
 template <int BN, int STAGES>
@@ -607,7 +609,9 @@ double plan_cost(int M, int N, int K, int bn, int splits, int sms) {
     const double kb = std::ceil(static_cast<double>(ceil_div(K, kBK)) / splits);
     const double eff = bn == 256 ? 1.0 : 1.25;
     double c = waves * bn * kb * eff;
-    if (splits > 1) c += 0.02 * static_cast<double>(M) * N * (splits + 1) / (128.0 * 64.0);  // reduce pass
+    // ordered split-K: each extra split adds one epilogue hand-off (~2-3 us,
+    // measured) to the critical path; 1 cost unit ~ one 64-deep k-block column
+    if (splits > 1) c += 2500.0 * (splits - 1);
     return c;
 }
 
@@ -625,13 +629,22 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     double best = 1e300;
     for (int bn : {256, 128}) {
         for (int sp : {1, 2, 3, 4, 6, 8}) {
-            if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp)) continue;
+            if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp ||
+                           ceil_div(M, kBM) * ceil_div(N, bn) * 4 * 32 > kSemSlots))
+                continue;
             const double c = plan_cost(M, N, K, bn, sp, sms);
             if (c < best * 0.97) {
                 best = c;
                 best_bn = bn;
                 best_sp = sp;
             }
+        }
+    }
+    if (const char* f = std::getenv("ACCO_GEMM_FORCE")) {  // tuning knob: "<bn>,<splits>"
+        int fb = 0, fs = 0;
+        if (std::sscanf(f, "%d,%d", &fb, &fs) == 2 && (fb == 128 || fb == 256) && fs >= 1) {
+            best_bn = fb;
+            best_sp = ep.mode == kEpiAccF32 ? fs : 1;
         }
     }
     if (best_bn == 256)
