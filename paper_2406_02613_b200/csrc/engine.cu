@@ -218,7 +218,8 @@ void Trainer::micro(int w, const void* params, uint64_t round, uint64_t tag, int
                     double* loss_slot) {
     const uint64_t gw = comm_ ? static_cast<uint64_t>(rank_) : static_cast<uint64_t>(w);
     const uint64_t seed = rng_derive(sim_.master_seed, gw, round, tag, static_cast<uint64_t>(ordinal));
-    model_->micro_batch(params, seed, 0, 0, sim_.batch_size, acc, loss_slot, cs_);
+    // the stage's first micro-batch overwrites the accumulator (Bundle::reset + add)
+    model_->micro_batch(params, seed, 0, 0, sim_.batch_size, acc, loss_slot, cs_, ordinal > 0);
     if (loss_host_) {  // host-data path: every micro-batch loss is read back as it completes
         const ptrdiff_t slot = loss_slot - loss_ring_;
         ACCO_CUDA(cudaMemcpyAsync(loss_host_ + slot, loss_slot, sizeof(double), cudaMemcpyDeviceToHost, cs_));
@@ -463,7 +464,6 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             if (p >= 2) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[p - 2], 0));
             ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(p) * nl + w], cs_));
             float* acc = acc_[static_cast<size_t>(w) * nacc + p % nacc];
-            ACCO_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(psi_) * 4, cs_));
             const void* params;
             uint64_t round, tag;
             if (p == 0) {
@@ -614,7 +614,6 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             if (r >= 1) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r - 1], 0));
             ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(r) * nl + w], cs_));
             float* acc = acc_[static_cast<size_t>(w)];
-            ACCO_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(psi_) * 4, cs_));
             for (int j = 0; j < k; ++j) {
                 const int slot = static_cast<int>(mb_counter_ % loss_cap_);
                 micro(w, theta_act_, round, kTagMain, j, acc, loss_ring_ + slot);

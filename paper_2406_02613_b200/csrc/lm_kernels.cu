@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
                                                          const float* __restrict__ mean, const float* __restrict__ rstd,
                                                          int M, int N, int rows_per_chunk, float* __restrict__ part,
                                                          unsigned* __restrict__ tickets, float* __restrict__ out,
-                                                         float* __restrict__ out1) {
+                                                         float* __restrict__ out1, int acc) {
     __shared__ float s0[kVecRows][65], s1[kVecRows][65];
     __shared__ bool last;
     const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
@@ -240,18 +240,19 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
             t0 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 0) * N + col]);
             if (KIND == 1) t1 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 1) * N + col]);
         }
-        out[col] += t0;
-        if (KIND == 1) out1[col] += t1;
+        out[col] = (acc ? out[col] : 0.f) + t0;
+        if (KIND == 1) out1[col] = (acc ? out1[col] : 0.f) + t1;
     }
     if (threadIdx.x == 0) tickets[blockIdx.x] = 0;  // ready for the next launch (stream-ordered)
 }
 
-__global__ void colreduce_final(const float* __restrict__ part, int nchunk, int N, float* __restrict__ out) {
+__global__ void colreduce_final(const float* __restrict__ part, int nchunk, int N, float* __restrict__ out,
+                                int acc) {
     const int col = blockIdx.x * blockDim.x + threadIdx.x;
     if (col >= N) return;
     float t = 0.f;
     for (int c = 0; c < nchunk; ++c) t += part[static_cast<int64_t>(c) * N + col];
-    out[col] += t;
+    out[col] = (acc ? out[col] : 0.f) + t;
 }
 
 // ------------------------------------------------------------- cross entropy
@@ -432,12 +433,14 @@ __global__ void embed_bwd_wte_kernel(const uint32_t* __restrict__ sorted, int M,
 }
 
 template <class T>
-__global__ void embed_bwd_wpe_kernel(const T* __restrict__ dx, int B, int seq, int d, float* __restrict__ grad_wpe) {
+__global__ void embed_bwd_wpe_kernel(const T* __restrict__ dx, int B, int seq, int d, float* __restrict__ grad_wpe,
+                                     int accumulate) {
     const int t = blockIdx.x;
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
         float acc = 0.f;
         for (int b = 0; b < B; ++b) acc += to_f(dx[(static_cast<int64_t>(b) * seq + t) * d + c]);
-        grad_wpe[static_cast<int64_t>(t) * d + c] += acc;
+        float* g = grad_wpe + static_cast<int64_t>(t) * d + c;
+        *g = (accumulate ? *g : 0.f) + acc;
     }
 }
 
@@ -578,21 +581,22 @@ static bool vec_ok(const void* p, int64_t ld, int N) {
 // grid: slabs x chunks with ~2 waves of 148 SMs
 template <class T, int KIND>
 static void colsum_vec(const T* y, int64_t ld, const T* x, const float* mean, const float* rstd, int M, int N,
-                       float* out, float* out1, float* scratch, cudaStream_t s) {
+                       float* out, float* out1, float* scratch, bool acc, cudaStream_t s) {
     const int slabs = ceil_div(N, 64);
     int nchunk = std::max(1, std::min(ceil_div(2 * num_sms(), slabs), ceil_div(M, kVecRows)));
     const int rpc = ceil_div(ceil_div(M, nchunk), kVecRows) * kVecRows;
     nchunk = ceil_div(M, rpc);
     colsum_vec_kernel<T, KIND><<<dim3(slabs, nchunk), 256, 0, s>>>(y, ld, x, mean, rstd, M, N, rpc, scratch,
-                                                                    tickets(), out, out1);
+                                                                    tickets(), out, out1, acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
 void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
-                   bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d, cudaStream_t s) {
+                   bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d, bool acc,
+                   cudaStream_t s) {
     if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d)) {
-        colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, s);
+        colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, acc, s);
         ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
         ACCO_CHECK_LAUNCH();
         return;
@@ -604,23 +608,23 @@ void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const
     colreduce_partial<T, 1><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd, M,
                                                                                          d, p0, p1);
     ACCO_CHECK_LAUNCH();
-    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p0, nchunk, d, gdst);
-    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst);
+    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p0, nchunk, d, gdst, acc ? 1 : 0);
+    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst, acc ? 1 : 0);
     ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
-void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, cudaStream_t s) {
+void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, bool acc, cudaStream_t s) {
     if (vec_ok<T>(y, ld, N)) {
-        colsum_vec<T, 0>(y, ld, nullptr, nullptr, nullptr, M, N, out, nullptr, scratch, s);
+        colsum_vec<T, 0>(y, ld, nullptr, nullptr, nullptr, M, N, out, nullptr, scratch, acc, s);
         return;
     }
     const int nchunk = ceil_div(M, kColChunk);
     colreduce_partial<T, 0><<<dim3(ceil_div(N, 32), nchunk), dim3(32, kColRows), 0, s>>>(
         y, ld, nullptr, nullptr, nullptr, M, N, scratch, nullptr);
     ACCO_CHECK_LAUNCH();
-    colreduce_final<<<ceil_div(N, 256), 256, 0, s>>>(scratch, nchunk, N, out);
+    colreduce_final<<<ceil_div(N, 256), 256, 0, s>>>(scratch, nchunk, N, out, acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -654,7 +658,7 @@ void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_
 
 template <class T>
 void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
-               uint32_t* sort_scratch, cudaStream_t s) {
+               uint32_t* sort_scratch, bool acc_wpe, cudaStream_t s) {
     ACCO_REQUIRE(static_cast<uint64_t>(V) * static_cast<uint64_t>(M) < 0xffffffffull,
                  "embed_bwd: vocab * tokens exceeds the 32-bit sort key");
     int P = 1;
@@ -669,7 +673,7 @@ void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, fl
     ACCO_CHECK_LAUNCH();
     embed_bwd_wte_kernel<T><<<M, 128, 0, s>>>(sort_scratch, M, dx, d, grad_wte);
     ACCO_CHECK_LAUNCH();
-    embed_bwd_wpe_kernel<T><<<seq, 128, 0, s>>>(dx, M / seq, seq, d, grad_wpe);
+    embed_bwd_wpe_kernel<T><<<seq, 128, 0, s>>>(dx, M / seq, seq, d, grad_wpe, acc_wpe ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -750,11 +754,11 @@ void spin_ns(uint64_t ns, cudaStream_t s) {
     template void embed_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);          \
     template void layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, cudaStream_t); \
     template void layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, float*, \
-                                   float*, float*, int, int, cudaStream_t);                                   \
-    template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, cudaStream_t);                   \
+                                   float*, float*, int, int, bool, cudaStream_t);                             \
+    template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);             \
     template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
     template void embed_bwd<T>(const int32_t*, const T*, int, int, int, int, float*, float*, uint32_t*,      \
-                               cudaStream_t);
+                               bool, cudaStream_t);
 ACCO_INST(float)
 ACCO_INST(__nv_bfloat16)
 #undef ACCO_INST

@@ -26,11 +26,12 @@ void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float*
 template <class T>
 void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd,
                    T* dx, bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d,
-                   cudaStream_t s);
+                   bool accumulate_params, cudaStream_t s);
 
 // out[c] += sum_r y[r*ld + c] (deterministic two-level), fp32 out.
 template <class T>
-void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, cudaStream_t s);
+void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, bool accumulate,
+                cudaStream_t s);
 
 // In place: logits[M, ld] -> dlogits = (softmax - onehot(target)) / seq;
 // row_loss[m] = logsumexp - logit[target].
@@ -45,7 +46,7 @@ void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_
 // grad_wpe[t] += sum_b dx[b*seq + t].
 template <class T>
 void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte,
-               float* grad_wpe, uint32_t* sort_scratch, cudaStream_t s);
+               float* grad_wpe, uint32_t* sort_scratch, bool accumulate_wpe, cudaStream_t s);
 
 template <class T>
 void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd, cudaStream_t s);

@@ -232,12 +232,12 @@ Epilogue ep_dgelu(void* c, int64_t ldc, void* aux) {
     e.ld_aux = ldc;
     return e;
 }
-Epilogue ep_acc(float* c, int64_t ldc) {
+Epilogue ep_acc(float* c, int64_t ldc, int beta) {
     Epilogue e;
     e.mode = kEpiAccF32;
     e.C = c;
     e.ldc = ldc;
-    e.beta = 1;
+    e.beta = beta;
     return e;
 }
 
@@ -291,39 +291,46 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     loss_reduce(row_loss_, M, Tq, loss, s);
     if (!backward) return;
 
-    // LM head (tied to wte): dwte += dlogits^T hf ; dhf = dlogits wte
-    mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d), s);
+    // Every gradient element is written by exactly one kernel first in this
+    // order, so with acc == false the first write *stores* and the caller's
+    // per-stage memset of the accumulator is unnecessary.
+    const bool acc = accumulate_;
+    const int beta = acc ? 1 : 0;
+    // LM head (tied to wte): dwte (+)= dlogits^T hf ; dhf = dlogits wte
+    mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d, beta), s);
     mm<T>(LOG, vpad_, false, W(kWte), d, true, M, d, V, ep_store(DT, d), s);
     layernorm_bwd<T>(DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), DX, false, Gp(kLnf), Gp(kLnf + 1), scratch_,
-                     M, d, s);
+                     M, d, acc, s);
     for (int l = L - 1; l >= 0; --l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
           *A = slot(l, sA), *U = slot(l, sU);
         // MLP
-        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d), s);
-        colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, s);
+        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d, beta), s);
+        colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, acc, s);
         mm<T>(DX, d, false, W(li(l, 10)), 4 * d, true, M, 4 * d, d, ep_dgelu(DA, 4 * d, A), s);
-        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d), s);
-        colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, s);
+        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d, beta), s);
+        colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, acc, s);
         mm<T>(DA, 4 * d, false, W(li(l, 8)), d, true, M, d, 4 * d, ep_store(DT, d), s);
         layernorm_bwd<T>(DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), DX, true, Gp(li(l, 6)), Gp(li(l, 7)),
-                         scratch_, M, d, s);
+                         scratch_, M, d, acc, s);
         // attention
-        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d), s);
-        colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, s);
+        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
+        colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, acc, s);
         mm<T>(DX, d, false, W(li(l, 4)), d, true, M, d, d, ep_store(DT, d), s);
         attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, hd, s);
-        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d), s);
-        colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, s);
+        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d, beta), s);
+        colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, s);
         mm<T>(DQKV, 3 * d, false, W(li(l, 2)), d, true, M, d, 3 * d, ep_store(DT, d), s);
         layernorm_bwd<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, Gp(li(l, 0)), Gp(li(l, 1)),
-                         scratch_, M, d, s);
+                         scratch_, M, d, acc, s);
     }
-    embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), sort_, s);
+    // wte rows: the head wgrad above stored/added every row; the embedding adds
+    embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), sort_, acc, s);
 }
 
 void GPTModel::micro_batch(const void* params, uint64_t seed, int mode, int start, int B, float* grad_acc,
-                           double* loss_sum, cudaStream_t s) {
+                           double* loss_sum, cudaStream_t s, bool accumulate) {
+    accumulate_ = accumulate;
     if (c_.precision == 1)
         run<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(params), seed, mode, start, B, grad_acc, loss_sum, true, s);
     else

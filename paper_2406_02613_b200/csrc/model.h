@@ -57,8 +57,10 @@ public:
     // (= Bundle::add of N * per-sample-mean, protocols.cpp:61-66), and
     // *loss_sum (device double) = sum over samples of the per-sample loss.
     // mode 0: indices Stream(stream_seed).below(n_samples); mode 1: [start, start+B).
+    // accumulate=false: the gradient of this micro-batch *overwrites* grad_acc
+    // (first micro-batch of a stage; no memset needed).
     void micro_batch(const void* params, uint64_t stream_seed, int mode, int start, int B, float* grad_acc,
-                     double* loss_sum, cudaStream_t s);
+                     double* loss_sum, cudaStream_t s, bool accumulate = true);
     // Token indices drawn by the last micro_batch (device int32 [B]).
     const int32_t* last_indices() const { return idx_; }
     // Forward only (loss), used by evaluation when no gradient is needed.
@@ -95,6 +97,7 @@ private:
     std::vector<cudaEvent_t> stage_ev_;
     int stage_next_ = 0;
     long long h2d_bytes_ = 0;
+    bool accumulate_ = true;
     const int32_t* stage_tokens(uint64_t seed, int B, cudaStream_t s);
 };
 

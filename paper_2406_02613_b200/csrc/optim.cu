@@ -17,7 +17,9 @@
 #include "common.cuh"
 #include "optim.h"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace acco {
 
@@ -159,8 +161,9 @@ void launch_vec(const KArgs& a, bool vec, cudaStream_t s) {
     const int threads = 256;
     // persistent-style grid: a few waves of 148 SMs x 8 resident blocks
     const int64_t work = vec ? (a.n + 3) / 4 : a.n;
-    int blocks = static_cast<int>(std::min<int64_t>((work + threads - 1) / threads,
-                                                    static_cast<int64_t>(num_sms()) * 8));
+    int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+    if (const char* e = std::getenv("ACCO_OPT_BLOCKS")) cap = std::max<int64_t>(1, std::atoll(e));  // tuning knob
+    int blocks = static_cast<int>(std::min<int64_t>((work + threads - 1) / threads, cap));
     if (blocks < 1) blocks = 1;
     if (vec)
         opt_kernel<KIND, COMMIT, HAS_RET, OutT, true><<<blocks, threads, 0, s>>>(a);
