@@ -251,9 +251,14 @@ void bwd_impl(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, 
 
 }  // namespace
 
-// Tensor-core path for bf16 (attn_mma.cu); returns false if not applicable.
+// Tensor-core paths for bf16: tcgen05 (attn_tc.cu), then mma.sync
+// (attn_mma.cu); each returns false if not applicable.
+bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int seq, int H, int hd,
+                      cudaStream_t s);
 bool attention_fwd_mma(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int seq, int H, int hd,
                        cudaStream_t s);
+bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse, const __nv_bfloat16* dy,
+                      __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int hd, cudaStream_t s);
 bool attention_bwd_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse,
                        const __nv_bfloat16* dy, __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int hd,
                        cudaStream_t s);
@@ -267,6 +272,7 @@ template <class T>
 void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd, cudaStream_t s) {
     ProfScope prof(kProfAttn, attn_flops(B, seq, H, hd), s);
     if constexpr (sizeof(T) == 2) {
+        if (attention_fwd_tc(qkv, y, lse, B, seq, H, hd, s)) return;
         if (attention_fwd_mma(qkv, y, lse, B, seq, H, hd, s)) return;
     }
     if (hd == 32) fwd_impl<T, 32>(qkv, y, lse, B, seq, H, s);
@@ -281,6 +287,7 @@ void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* d
                    int H, int hd, cudaStream_t s) {
     ProfScope prof(kProfAttn, 2.5 * attn_flops(B, seq, H, hd), s);
     if constexpr (sizeof(T) == 2) {
+        if (attention_bwd_tc(qkv, y, lse, dy, dqkv, dsum, B, seq, H, hd, s)) return;
         if (attention_bwd_mma(qkv, y, lse, dy, dqkv, dsum, B, seq, H, hd, s)) return;
     }
     if (hd == 32) bwd_impl<T, 32>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, s);

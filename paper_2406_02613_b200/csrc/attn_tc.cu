@@ -1,0 +1,849 @@
+// Causal flash-attention forward on the 5th-generation tensor cores (sm_100a),
+// head size 64, bf16 in / fp32 accumulate.
+//
+// One CTA per (batch*head, 128-query tile), heavy (late) tiles first:
+//   warp 0   : TMA producer — Q once, then K_j / V_j 128-key tiles into a
+//              2-stage ring (both as [keys][64] rows, 128B-swizzled)
+//   warp 1   : MMA issuer — S = Q K_j^T (UMMA 128x128x64, K-major x K-major)
+//              into TMEM, then O += P_j V_j (UMMA 128x64x128: P from smem
+//              K-major, V as an MN-major B operand) into a TMEM accumulator
+//   warp 2   : TMEM allocator (256 columns: S 128 + O 64)
+//   warps 4-7: softmax — thread = query row = TMEM lane: tcgen05.ld of the S
+//              row, online softmax entirely thread-local (no shuffles), P
+//              (bf16) to swizzled smem for the PV MMA. The O rescale is lazy:
+//              the running max is only raised when it grows by > 2^8, so O
+//              (in TMEM) is rarely touched; final O / l and lse from TMEM.
+// S of tile j+1 is issued while the softmax of tile j runs.
+#include "common.cuh"
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+namespace acco {
+namespace {
+
+constexpr int HD = 64;
+constexpr int BQ = 128;  // queries per CTA (UMMA M)
+constexpr int BKV = 128; // keys per tile (UMMA N of QK^T, K of PV)
+constexpr int kStages = 2;
+constexpr int kThreads = 384;  // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: softmax (2 per TMEM quadrant)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThresh = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
+
+constexpr int Q_BYTES = BQ * HD * 2;          // 16 KB
+constexpr int KV_BYTES = BKV * HD * 2;        // 16 KB per K or V tile
+constexpr int P_BYTES = BQ * BKV * 2;         // 32 KB (two 64-key chunks)
+constexpr int SMEM = 1024 + Q_BYTES + kStages * 2 * KV_BYTES + P_BYTES + 256 + 4096;  // + row-max/sum exchange
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+          "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+    return d;
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
+           (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
+              int T, int H, float scale) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = sQ + Q_BYTES;                       // [stage] K tiles
+    uint8_t* sV = sK + kStages * KV_BYTES;            // [stage] V tiles
+    uint8_t* sP = sV + kStages * KV_BYTES;            // two 64-key chunks of [128][64] bf16
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = bars + 1;            // [kStages]
+    uint64_t* kv_empty = kv_full + kStages;  // [kStages]
+    uint64_t* s_full = kv_empty + kStages;
+    uint64_t* s_free = s_full + 1;
+    uint64_t* p_full = s_free + 1;
+    uint64_t* o_done = p_full + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+    const int nqt = (T + BQ - 1) / BQ;
+    const int qt = nqt - 1 - blockIdx.x;
+    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    const int d = H * HD;
+    const int q0 = qt * BQ;
+    const int nkt = (min(T, q0 + BQ) + BKV - 1) / BKV;  // causal: key tiles up to the diagonal
+    const int row_base = b * T;                          // qkv row of (b, t=0)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_free, 256);
+        mbar_init(p_full, 256);
+        mbar_init(o_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tS = tmem, tO = tmem + 128;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(q_full, Q_BYTES);
+            tma_load_2d(sQ, &tmQKV, q_full, h * HD, row_base + q0);
+            for (int j = 0; j < nkt; ++j) {
+                const int s = j % kStages;
+                mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
+                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], d + h * HD, row_base + j * BKV);
+                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], 2 * d + h * HD, row_base + j * BKV);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
+            constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P K-major, V MN-major
+            const uint32_t q_base = smem_u32(sQ), p_base = smem_u32(sP);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int j) {
+                const int s = j % kStages;
+                mbar_wait(&kv_full[s], (j / kStages) & 1);
+                tc_after();
+                const uint32_t k_base = smem_u32(sK + s * KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk)
+                    umma(tS, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024), id_s, kk > 0);
+                umma_commit(s_full);
+            };
+            issue_s(0);
+            for (int j = 0; j < nkt; ++j) {
+                const int s = j % kStages;
+                if (j + 1 < nkt) {
+                    mbar_wait(s_free, j & 1);  // softmax has S_j in registers
+                    tc_after();
+                    issue_s(j + 1);
+                }
+                mbar_wait(p_full, j & 1);  // P_j in smem (and O rescaled if needed)
+                tc_after();
+                const uint32_t v_base = smem_u32(sV + s * KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    const uint64_t ad = sdesc(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024);
+                    const uint64_t bd = sdesc(v_base + kk * 2048, 64 * 128, 1024);
+                    umma(tO, ad, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&kv_empty[s]);
+                umma_commit(o_done);
+            }
+        }
+    } else if (warp >= 4) {
+        // 8 softmax warps: quadrant wq (TMEM lanes) x half (64 of the 128 keys,
+        // 32 of the 64 O columns); the row max is combined with the partner warp
+        const int wq = warp & 3, half = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;  // query row within the tile = TMEM lane
+        const int q = q0 + r;
+        const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+        const float sl = scale * kLog2e;
+        float* red = reinterpret_cast<float*>(tslot + 4);  // [2 parity][2 half][128] row maxima
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nkt; ++j) {
+            mbar_wait(s_full, j & 1);
+            tc_after();
+            uint32_t sr[64];  // this half of the S row, scaled in place (log2 domain)
+            tmem_ld32(tS + lane_off + half * 64, sr);
+            tmem_ld32(tS + lane_off + half * 64 + 32, sr + 32);
+            tmem_wait_ld();
+            tc_before();
+            mbar_arrive(s_free);  // S TMEM may be overwritten by the next QK^T
+            const bool diag = (j + 1) * BKV > q0;  // tile touching the causal edge (or T tail)
+            float mx = m;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                float x = __uint_as_float(sr[i]) * sl;
+                if (diag) {
+                    const int key = j * BKV + half * 64 + i;
+                    if (key > q || key >= T) x = -INFINITY;
+                }
+                sr[i] = __float_as_uint(x);
+                mx = fmaxf(mx, x);
+            }
+            float* rb = red + (j & 1) * 256;
+            rb[half * 128 + r] = mx;
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + wq) : "memory");  // the quadrant's two warps
+            mx = fmaxf(mx, rb[(1 - half) * 128 + r]);
+            // lazy rescale: raise the running max only when it grows by > 2^8
+            const bool need = mx > m + kRescaleThresh;
+            const float alpha = need ? ex2(m - mx) : 1.f;
+            if (need) m = mx;
+            l *= alpha;
+            if (j > 0) {
+                mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} finished: O stable, P buffer free
+                tc_after();
+            }
+            // P = 2^(s - m) -> bf16, swizzled K-major into this half's 64-key chunk
+            float rs = 0.f;
+#pragma unroll
+            for (int unit = 0; unit < 8; ++unit) {
+                float p[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    p[k] = ex2(__uint_as_float(sr[unit * 8 + k]) - m);
+                    rs += p[k];
+                }
+                uint4 u;
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(p[0], p[1]), h1 = __floats2bfloat162_rn(p[2], p[3]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(p[4], p[5]), h3 = __floats2bfloat162_rn(p[6], p[7]);
+                u.x = *reinterpret_cast<uint32_t*>(&h0);
+                u.y = *reinterpret_cast<uint32_t*>(&h1);
+                u.z = *reinterpret_cast<uint32_t*>(&h2);
+                u.w = *reinterpret_cast<uint32_t*>(&h3);
+                *reinterpret_cast<uint4*>(sP + half * (BQ * 128) + r * 128 + ((unit ^ (r & 7)) << 4)) = u;
+            }
+            l += rs;
+            // O *= alpha for rows whose max moved (warp-collective TMEM access, 32 of 64 columns)
+            if (j > 0 && __any_sync(0xffffffffu, need)) {
+                uint32_t o[32];
+                tmem_ld32(tO + lane_off + half * 32, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                tmem_st32(tO + lane_off + half * 32, o);
+                tmem_wait_st();
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_before();
+            mbar_arrive(p_full);
+        }
+        // epilogue: O / l (l = both halves' partial sums), lse
+        float* lb = red + 512;
+        lb[half * 128 + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + wq) : "memory");
+        l += lb[(1 - half) * 128 + r];
+        mbar_wait(o_done, (nkt - 1) & 1);
+        tc_after();
+        uint32_t o[32];
+        tmem_ld32(tO + lane_off + half * 32, o);
+        tmem_wait_ld();
+        if (q < T) {
+            const float inv = 1.f / l;
+            __nv_bfloat16* yr = y + (static_cast<int64_t>(b) * T + q) * d + h * HD + half * 32;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint4 u;
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv);
+                __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv);
+                u.x = *reinterpret_cast<uint32_t*>(&h0);
+                u.y = *reinterpret_cast<uint32_t*>(&h1);
+                u.z = *reinterpret_cast<uint32_t*>(&h2);
+                u.w = *reinterpret_cast<uint32_t*>(&h3);
+                reinterpret_cast<uint4*>(yr)[c] = u;
+            }
+            if (half == 0) lse[static_cast<int64_t>(bh) * T + q] = (m + log2f(l)) / kLog2e;
+        }
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    }
+}
+
+// ----------------------------------------------------------------- backward
+// A [128 rows][128] bf16 tile written by threads (thread = row) as a K-major
+// UMMA A operand = two 64-column chunks of [128][128B], SW128.
+// One 64-column chunk (8 x 16B units) of such a tile: row r of chunk `chunk`.
+__device__ __forceinline__ void st_row64_chunk(uint8_t* buf, int chunk, int r, const float* v) {
+#pragma unroll
+    for (int unit = 0; unit < 8; ++unit) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * unit + 0], v[8 * unit + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * unit + 2], v[8 * unit + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * unit + 4], v[8 * unit + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * unit + 6], v[8 * unit + 7]);
+        uint4 u;
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        u.z = *reinterpret_cast<uint32_t*>(&h2);
+        u.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(buf + chunk * (128 * 128) + r * 128 + ((unit ^ (r & 7)) << 4)) = u;
+    }
+}
+// K-major A descriptor for k-step kk (16 columns) of such a tile
+__device__ __forceinline__ uint64_t a128_desc(uint32_t base, int kk) {
+    return sdesc(base + (kk >> 2) * (128 * 128) + (kk & 3) * 32, 16, 1024);
+}
+// Store 32 floats of a thread's row (scaled) as bf16 to global (64 B contiguous)
+__device__ __forceinline__ void st_row32_global(__nv_bfloat16* dst, const uint32_t* o, float scale) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 0]) * scale, __uint_as_float(o[8 * c + 1]) * scale);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2]) * scale, __uint_as_float(o[8 * c + 3]) * scale);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 4]) * scale, __uint_as_float(o[8 * c + 5]) * scale);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 6]) * scale, __uint_as_float(o[8 * c + 7]) * scale);
+        uint4 u;
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        u.z = *reinterpret_cast<uint32_t*>(&h2);
+        u.w = *reinterpret_cast<uint32_t*>(&h3);
+        reinterpret_cast<uint4*>(dst)[c] = u;
+    }
+}
+
+constexpr int BW_T = 128;                          // tile rows (keys or queries)
+constexpr int BW_TILE = BW_T * HD * 2;             // 16 KB [128][64] bf16
+constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P / dS operand)
+// dKV smem: K, V (once) + 2 stages x (Q, dO) + lse/D (2 stages) + P^T + dS^T
+constexpr int DKV_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 2 * BW_SQ + 256;
+
+// dK/dV: one CTA per (batch*head, 128-key tile); loops over the query tiles
+// at and after the diagonal. Per query tile:
+//   S^T = K Q^T, dP^T = V dO^T          (TMEM, 128 x 128 each)
+//   softmax-bwd warps (thread = key row): P^T = 2^(S^T sl - lse2[q]),
+//   dS^T = P^T (dP^T - D[q])  -> bf16 smem operands
+//   dV += P^T dO, dK += dS^T Q          (TMEM, 128 x 64 each; Q/dO MN-major B)
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
+                  int T, int H, float scale) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sK = smem;
+    uint8_t* sV = sK + BW_TILE;
+    uint8_t* sQ = sV + BW_TILE;            // [2 stages]
+    uint8_t* sO = sQ + 2 * BW_TILE;        // dO [2 stages]
+    uint8_t* sPT = sO + 2 * BW_TILE;       // P^T operand
+    uint8_t* sDS = sPT + BW_SQ;            // dS^T operand
+    float* sL = reinterpret_cast<float*>(sDS + BW_SQ);  // [2][128] lse (log2 domain)
+    float* sD = sL + 2 * BW_T;                           // [2][128] D
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BW_T);
+    uint64_t* kv_full = bars;
+    uint64_t* q_full = bars + 1;       // [2]
+    uint64_t* q_empty = q_full + 2;    // [2]
+    uint64_t* s_full = q_empty + 2;    // S^T and dP^T ready
+    uint64_t* s_free = s_full + 1;     // softmax has them in registers
+    uint64_t* p_full = s_free + 1;     // P^T, dS^T in smem
+    uint64_t* g_done = p_full + 1;     // dV/dK MMAs of this tile done (operands free)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 1);
+
+    const int nt = (T + BW_T - 1) / BW_T;
+    const int kt = blockIdx.x;
+    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    const int d = H * HD;
+    const int k0 = kt * BW_T;
+    const int row_base = b * T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nq = nt - kt;  // query tiles kt .. nt-1
+
+    if (threadIdx.x == 0) {
+        mbar_init(kv_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_free, 256);
+        mbar_init(p_full, 256);
+        mbar_init(g_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(kv_full, 2 * BW_TILE);
+            tma_load_2d(sK, &tmQKV, kv_full, d + h * HD, row_base + k0);
+            tma_load_2d(sV, &tmQKV, kv_full, 2 * d + h * HD, row_base + k0);
+            for (int i = 0; i < nq; ++i) {
+                const int s = i & 1;
+                const int q0 = (kt + i) * BW_T;
+                mbar_wait(&q_empty[s], ((i >> 1) & 1) ^ 1);
+                mbar_expect_tx(&q_full[s], 2 * BW_TILE);
+                tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
+                tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);  // K Q^T / V dO^T
+            constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);    // P^T dO / dS^T Q (B MN-major)
+            const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+            const uint32_t pt_base = smem_u32(sPT), ds_base = smem_u32(sDS);
+            mbar_wait(kv_full, 0);
+            auto issue_s = [&](int i) {  // S^T = K Q_i^T, dP^T = V dO_i^T
+                const int s = i & 1;
+                mbar_wait(&q_full[s], (i >> 1) & 1);
+                tc_after();
+                const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    umma(tS, sdesc(k_base + kk * 32, 16, 1024), sdesc(q_base + kk * 32, 16, 1024), id_s, kk > 0);
+                    umma(tP, sdesc(v_base + kk * 32, 16, 1024), sdesc(o_base + kk * 32, 16, 1024), id_s, kk > 0);
+                }
+                umma_commit(s_full);
+            };
+            issue_s(0);
+            for (int i = 0; i < nq; ++i) {
+                const int s = i & 1;
+                const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
+                if (i + 1 < nq) {  // next tile's S^T/dP^T overlap this tile's softmax
+                    mbar_wait(s_free, i & 1);
+                    issue_s(i + 1);
+                }
+                mbar_wait(p_full, i & 1);  // P^T / dS^T written
+                tc_after();
+#pragma unroll
+                for (int kk = 0; kk < BW_T / 16; ++kk) {
+                    umma(tDV, a128_desc(pt_base, kk), sdesc(o_base + kk * 2048, 64 * 128, 1024), id_g,
+                         (i > 0 || kk > 0) ? 1u : 0u);
+                    umma(tDK, a128_desc(ds_base, kk), sdesc(q_base + kk * 2048, 64 * 128, 1024), id_g,
+                         (i > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&q_empty[s]);
+                umma_commit(g_done);
+            }
+        }
+    } else if (warp >= 4) {
+        // 8 warps: quadrant wq (key rows = TMEM lanes) x half (64 of 128 queries)
+        const int wq = warp & 3, hf = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;  // key row = TMEM lane
+        const int key = k0 + r;
+        const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+        const float sl = scale * kLog2e;
+        for (int i = 0; i < nq; ++i) {
+            const int s = i & 1;
+            const int q0 = (kt + i) * BW_T;
+            // lse (log2) and D for this query tile -> smem (one per half-0 thread)
+            if (hf == 0) {
+                const int q = q0 + r;
+                sL[s * BW_T + r] = q < T ? lse[static_cast<int64_t>(bh) * T + q] * kLog2e : 0.f;
+                sD[s * BW_T + r] = q < T ? dsum[static_cast<int64_t>(bh) * T + q] : 0.f;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // softmax warps only
+            mbar_wait(s_full, i & 1);
+            tc_after();
+            if (i > 0) {
+                mbar_wait(g_done, (i - 1) & 1);  // previous dV/dK MMAs have read the operands
+                tc_after();
+            }
+            const bool edge = i == 0 || i == nq - 1;  // diagonal / ragged tail
+            {
+                uint32_t st[64];
+                float p[64];
+                tmem_ld32(tS + lane_off + hf * 64, st);
+                tmem_ld32(tS + lane_off + hf * 64 + 32, st + 32);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const int qi = hf * 64 + c;
+                    float x = ex2(__uint_as_float(st[c]) * sl - sL[s * BW_T + qi]);
+                    if (edge) {
+                        const int q = q0 + qi;
+                        if (q < key || q >= T || key >= T) x = 0.f;
+                    }
+                    p[c] = x;
+                }
+                tmem_ld32(tP + lane_off + hf * 64, st);
+                tmem_ld32(tP + lane_off + hf * 64 + 32, st + 32);
+                tmem_wait_ld();
+                tc_before();
+                mbar_arrive(s_free);  // S^T / dP^T TMEM may be overwritten
+                st_row64_chunk(sPT, hf, r, p);
+#pragma unroll
+                for (int c = 0; c < 64; ++c) p[c] = p[c] * (__uint_as_float(st[c]) - sD[s * BW_T + hf * 64 + c]);
+                st_row64_chunk(sDS, hf, r, p);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_before();
+            mbar_arrive(p_full);
+        }
+        mbar_wait(g_done, (nq - 1) & 1);
+        tc_after();
+        uint32_t o[32];  // this warp's 32 of the 64 output columns
+        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * T + key) * (3 * d) + h * HD + hf * 32;
+        tmem_ld32(tDV + lane_off + hf * 32, o);
+        tmem_wait_ld();
+        if (key < T) st_row32_global(dst + 2 * d, o, 1.f);
+        tmem_ld32(tDK + lane_off + hf * 32, o);
+        tmem_wait_ld();
+        if (key < T) st_row32_global(dst + d, o, scale);
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// dQ: one CTA per (batch*head, 128-query tile), loops over key tiles up to the
+// diagonal: S = Q K^T, dP = dO V^T (TMEM); thread = query row: P, dS -> smem;
+// dQ += dS K (K as MN-major B). Heavy tiles first.
+constexpr int DQ_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + BW_SQ + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
+                 const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
+                 int T, int H, float scale) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sO = sQ + BW_TILE;           // dO
+    uint8_t* sK = sO + BW_TILE;           // [2 stages]
+    uint8_t* sV = sK + 2 * BW_TILE;       // [2 stages]
+    uint8_t* sDS = sV + 2 * BW_TILE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + BW_SQ);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = bars + 1;     // [2]
+    uint64_t* kv_empty = kv_full + 2; // [2]
+    uint64_t* s_full = kv_empty + 2;
+    uint64_t* s_free = s_full + 1;
+    uint64_t* p_full = s_free + 1;
+    uint64_t* g_done = p_full + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 1);
+
+    const int nt = (T + BW_T - 1) / BW_T;
+    const int qt = nt - 1 - blockIdx.x;
+    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    const int d = H * HD;
+    const int q0 = qt * BW_T;
+    const int row_base = b * T;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nk = qt + 1;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
+        mbar_init(s_full, 1);
+        mbar_init(s_free, 256);
+        mbar_init(p_full, 256);
+        mbar_init(g_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(q_full, 2 * BW_TILE);
+            tma_load_2d(sQ, &tmQKV, q_full, h * HD, row_base + q0);
+            tma_load_2d(sO, &tmDO, q_full, h * HD, row_base + q0);
+            for (int j = 0; j < nk; ++j) {
+                const int s = j & 1;
+                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
+                tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], d + h * HD, row_base + j * BW_T);
+                tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], 2 * d + h * HD, row_base + j * BW_T);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);
+            constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);
+            const uint32_t q_base = smem_u32(sQ), o_base = smem_u32(sO), ds_base = smem_u32(sDS);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int j) {  // S = Q K_j^T, dP = dO V_j^T
+                const int s = j & 1;
+                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                tc_after();
+                const uint32_t k_base = smem_u32(sK + s * BW_TILE), v_base = smem_u32(sV + s * BW_TILE);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    umma(tS, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024), id_s, kk > 0);
+                    umma(tP, sdesc(o_base + kk * 32, 16, 1024), sdesc(v_base + kk * 32, 16, 1024), id_s, kk > 0);
+                }
+                umma_commit(s_full);
+            };
+            issue_s(0);
+            for (int j = 0; j < nk; ++j) {
+                const int s = j & 1;
+                const uint32_t k_base = smem_u32(sK + s * BW_TILE);
+                if (j + 1 < nk) {
+                    mbar_wait(s_free, j & 1);
+                    issue_s(j + 1);
+                }
+                mbar_wait(p_full, j & 1);
+                tc_after();
+#pragma unroll
+                for (int kk = 0; kk < BW_T / 16; ++kk)
+                    umma(tDQ, a128_desc(ds_base, kk), sdesc(k_base + kk * 2048, 64 * 128, 1024), id_g,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(&kv_empty[s]);
+                umma_commit(g_done);
+            }
+        }
+    } else if (warp >= 4) {
+        // 8 warps: quadrant wq (query rows = TMEM lanes) x half (64 of 128 keys)
+        const int wq = warp & 3, hf = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;
+        const int q = q0 + r;
+        const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+        const float sl = scale * kLog2e;
+        const float L = q < T ? lse[static_cast<int64_t>(bh) * T + q] * kLog2e : 0.f;
+        const float Dq = q < T ? dsum[static_cast<int64_t>(bh) * T + q] : 0.f;
+        for (int j = 0; j < nk; ++j) {
+            mbar_wait(s_full, j & 1);
+            tc_after();
+            if (j > 0) {
+                mbar_wait(g_done, (j - 1) & 1);  // previous dQ MMA has read dS
+                tc_after();
+            }
+            const bool diag = j == nk - 1;
+            {
+                uint32_t st[64];
+                float p[64];
+                tmem_ld32(tS + lane_off + hf * 64, st);
+                tmem_ld32(tS + lane_off + hf * 64 + 32, st + 32);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    float x = ex2(__uint_as_float(st[c]) * sl - L);
+                    if (diag) {
+                        const int key = j * BW_T + hf * 64 + c;
+                        if (key > q || key >= T) x = 0.f;
+                    }
+                    p[c] = x;
+                }
+                tmem_ld32(tP + lane_off + hf * 64, st);
+                tmem_ld32(tP + lane_off + hf * 64 + 32, st + 32);
+                tmem_wait_ld();
+                tc_before();
+                mbar_arrive(s_free);
+#pragma unroll
+                for (int c = 0; c < 64; ++c) p[c] = p[c] * (__uint_as_float(st[c]) - Dq);
+                st_row64_chunk(sDS, hf, r, p);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tc_before();
+            mbar_arrive(p_full);
+        }
+        mbar_wait(g_done, (nk - 1) & 1);
+        tc_after();
+        uint32_t o[32];
+        tmem_ld32(tDQ + lane_off + hf * 32, o);
+        tmem_wait_ld();
+        if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(b) * T + q) * (3 * d) + h * HD + hf * 32, o, scale);
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ACCO_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) throw Error(kCudaError, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// [rows][cols] bf16 matrix (row stride ld), box 64 x 128, SW128
+CUtensorMap rows_map(const void* p, int64_t cols, int64_t rows, int64_t ld) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    cuuint32_t box[2] = {64, 128};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(kCudaError, "attention tensor map: " + std::to_string(r));
+    return m;
+}
+
+// D[bh, t] = sum_c dO[t, c] O[t, c] (one warp per row of 64)
+__global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dy,
+                               float* __restrict__ dsum, int B, int T, int H) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= static_cast<int64_t>(B) * H * T) return;
+    const int t = static_cast<int>(row % T);
+    const int bh = static_cast<int>(row / T);
+    const int b = bh / H, h = bh % H;
+    const int64_t o = (static_cast<int64_t>(b) * T + t) * (H * HD) + h * HD + lane * 2;
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(y + o);
+    const __nv_bfloat162 g = *reinterpret_cast<const __nv_bfloat162*>(dy + o);
+    float s = __bfloat162float(a.x) * __bfloat162float(g.x) + __bfloat162float(a.y) * __bfloat162float(g.y);
+#pragma unroll
+    for (int w = 16; w > 0; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
+    if (lane == 0) dsum[row] = s;
+}
+
+bool tc_applicable(const void* a, const void* b, int hd) {
+    return hd == HD && !(reinterpret_cast<uintptr_t>(a) & 15) && !(reinterpret_cast<uintptr_t>(b) & 15) &&
+           !std::getenv("ACCO_ATTN_LEGACY");
+}
+
+}  // namespace
+
+bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse, const __nv_bfloat16* dy,
+                      __nv_bfloat16* dqkv, float* dsum, int B, int T, int H, int hd, cudaStream_t s) {
+    if (!tc_applicable(qkv, dy, hd) || !tc_applicable(y, dqkv, hd)) return false;
+    const int d = H * HD;
+    const int64_t rows = static_cast<int64_t>(B) * T;
+    const int64_t nrow = rows * H;
+    dsum_tc_kernel<<<static_cast<int>((nrow + 7) / 8), 256, 0, s>>>(y, dy, dsum, B, T, H);
+    ACCO_CHECK_LAUNCH();
+    CUtensorMap mq = rows_map(qkv, 3 * d, rows, 3 * d);
+    CUtensorMap mo = rows_map(dy, d, rows, d);
+    static bool cfg = false;
+    if (!cfg) {
+        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, DKV_SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ_SMEM));
+        cfg = true;
+    }
+    const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+    dim3 grid((T + BW_T - 1) / BW_T, B * H);
+    fa_bwd_dkv_tc<<<grid, kThreads, DKV_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, scale);
+    ACCO_CHECK_LAUNCH();
+    fa_bwd_dq_tc<<<grid, kThreads, DQ_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, scale);
+    ACCO_CHECK_LAUNCH();
+    return true;
+}
+
+// qkv: [B*T, 3*d] bf16 (q | k | v, head h at columns h*64); returns false if
+// the tensor-core path does not apply (head size, alignment).
+bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int T, int H, int hd,
+                      cudaStream_t s) {
+    if (!tc_applicable(qkv, y, hd)) return false;
+    const int d = H * HD;
+    CUtensorMap m = rows_map(qkv, 3 * d, static_cast<int64_t>(B) * T, 3 * d);
+    static bool cfg = false;
+    if (!cfg) {
+        ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        cfg = true;
+    }
+    dim3 grid((T + BQ - 1) / BQ, B * H);
+    fa_fwd_tc<<<grid, kThreads, SMEM, s>>>(m, y, lse, T, H, 1.0f / sqrtf(static_cast<float>(hd)));
+    ACCO_CHECK_LAUNCH();
+    return true;
+}
+
+}  // namespace acco

@@ -139,6 +139,22 @@ def test_bf16_tensor_core_attention_per_tensor(cuda, seq):
         assert _rel(g[off:off + n], og[off:off + n]) <= 5e-2, name
 
 
+@pytest.mark.parametrize("seq", [128, 200, 384, 1024])
+def test_tcgen05_attention_matches_mma_path(cuda, seq, monkeypatch):
+    """Same bf16 model gradient with the tcgen05 flash forward vs the mma.sync
+    one (ACCO_ATTN_LEGACY): both bf16, so agreement is at bf16 rounding."""
+    c = dict(vocab=128, d_model=128, n_layer=1, n_head=2, seq_len=seq, n_samples=8, data_seed=6)
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=2))
+    gc = G.GPTConfig(**c)
+    th = torch.tensor(G.default_theta0(gc, 3) * 10).to(torch.bfloat16).to(cuda)
+    seed = O.derive(6, 0, 0, 2, 0)
+    g_tc, l_tc = _grad(m, th, seed, 2, cuda)
+    monkeypatch.setenv("ACCO_ATTN_LEGACY", "1")
+    g_mma, l_mma = _grad(m, th, seed, 2, cuda)
+    assert abs(l_tc - l_mma) <= 2e-3 * abs(l_mma)
+    assert _rel(g_tc, g_mma) <= 2e-2
+
+
 def test_micro_batch_bounds(cuda):
     m = api.Model(api.LMConfig(**CFGS["tiny"], precision="fp32", max_batch=2))
     pt = torch.zeros(m.dim, device=cuda)
