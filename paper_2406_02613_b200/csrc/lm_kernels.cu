@@ -107,6 +107,109 @@ __global__ void ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
     }
 }
 
+// bf16 LayerNorm with 16B vector loads, row held in registers: lane owns
+// chunks c = lane + 32*i (8 elements each), d = 256 * CH.
+__device__ __forceinline__ void unpack8b(const uint4& u, float* v) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ uint4 pack8b(const float* v) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+        w[k] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int CH>
+__global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
+                           const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
+                           float* __restrict__ rstd, int M) {
+    constexpr int d = 256 * CH;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * d);
+    float v[CH * 8];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) unpack8b(xr[lane + 32 * i], v + 8 * i);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < CH * 8; ++i) s += v[i];
+    const float mu = warp_sum(s) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < CH * 8; ++i) q += (v[i] - mu) * (v[i] - mu);
+    const float rs = rsqrtf(warp_sum(q) / d + kLnEps);
+    uint4* yr = reinterpret_cast<uint4*>(y + static_cast<int64_t>(row) * d);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+        float gv[8], bv[8], o[8];
+        unpack8b(reinterpret_cast<const uint4*>(g)[lane + 32 * i], gv);
+        unpack8b(reinterpret_cast<const uint4*>(b)[lane + 32 * i], bv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = (v[8 * i + k] - mu) * rs * gv[k] + bv[k];
+        yr[lane + 32 * i] = pack8b(o);
+    }
+    if (lane == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+    }
+}
+
+template <int CH>
+__global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                           const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+                           const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx, int accumulate, int M) {
+    constexpr int d = 256 * CH;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const int64_t o = static_cast<int64_t>(row) * d;
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + o);
+    const uint4* xr = reinterpret_cast<const uint4*>(x + o);
+    const float mu = mean[row], rs = rstd[row];
+    float xh[CH * 8], dxh[CH * 8];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+        float dv[8], gv[8];
+        unpack8b(xr[lane + 32 * i], xh + 8 * i);
+        unpack8b(dyr[lane + 32 * i], dv);
+        unpack8b(reinterpret_cast<const uint4*>(g)[lane + 32 * i], gv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            xh[8 * i + k] = (xh[8 * i + k] - mu) * rs;
+            dxh[8 * i + k] = dv[k] * gv[k];
+        }
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < CH * 8; ++i) {
+        s1 += dxh[i];
+        s2 += dxh[i] * xh[i];
+    }
+    s1 = warp_sum(s1) / d;
+    s2 = warp_sum(s2) / d;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + o);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+        float r[8], prev[8];
+        if (accumulate) unpack8b(dxr[lane + 32 * i], prev);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            r[k] = rs * (dxh[8 * i + k] - s1 - xh[8 * i + k] * s2);
+            if (accumulate) r[k] += prev[k];
+        }
+        dxr[lane + 32 * i] = pack8b(r);
+    }
+}
+
 // ------------------------------------------------ deterministic column reduce
 // partial[chunk][col] = sum over rows of the chunk (fixed order), then
 // out[col] += sum_chunk partial[chunk][col] (fixed order).
@@ -193,6 +296,7 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
     const int r0 = chunk * rows_per_chunk, r1 = min(M, r0 + rows_per_chunk);
     float a0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, a1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (c0 < N) {
+#pragma unroll 4
         for (int r = r0 + rl; r < r1; r += kVecRows) {
             float dy[8];
             load8<T>(y + static_cast<int64_t>(r) * ld + c0, dy);
@@ -300,79 +404,82 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, int64_t
     }
 }
 
-// bf16 single-pass variant: the whole row (V <= 512 threads x 8 x NV) lives in
-// registers, so logits are read once and dlogits written once (HBM floor).
-template <int NV>
-__global__ void __launch_bounds__(512) ce_bf16_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
-                                                      const int32_t* __restrict__ target, int V, float inv_seq,
-                                                      float* __restrict__ row_loss) {
-    __shared__ float red[32];
+// bf16 two-pass variant with 16B vector loads: pass 1 streams the row from HBM
+// (online max / sum-exp per 8-element vector), pass 2 re-reads it while it is
+// still in L2 (148 SMs x a few 100 KB rows << 126 MB) and writes dlogits, so
+// HBM sees one read + one write per logit. Small blocks -> several rows per SM.
+__device__ __forceinline__ void unpack8(const uint4& u, float* v) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+}
+
+__global__ void __launch_bounds__(256) ce_vec_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
+                                                     const int32_t* __restrict__ target, int V, float inv_seq,
+                                                     float* __restrict__ row_loss) {
+    __shared__ float red_m[8], red_s[8];
     const int row = blockIdx.x;
     uint4* L = reinterpret_cast<uint4*>(logits + static_cast<int64_t>(row) * ld);
     const int nvec = (V + 7) / 8;
-    uint4 r[NV];
+    const int nfull = V / 8;  // vectors with 8 valid elements
+    float m = -INFINITY, s = 0.f;
+    for (int i = threadIdx.x; i < nvec; i += 256) {
+        float v[8];
+        unpack8(L[i], v);
+        if (i >= nfull)
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int idx = threadIdx.x + i * 512;
-        r[i] = idx < nvec ? L[idx] : make_uint4(0, 0, 0, 0);
-    }
-    float m = -INFINITY;
+            for (int k = 0; k < 8; ++k)
+                if (i * 8 + k >= V) v[k] = -INFINITY;
+        float lm = v[0];
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int base = (threadIdx.x + i * 512) * 8;
-        const uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float v = __uint_as_float((k & 1) ? (w[k >> 1] & 0xffff0000u) : (w[k >> 1] << 16));
-            if (base + k < V) m = fmaxf(m, v);
+        for (int k = 1; k < 8; ++k) lm = fmaxf(lm, v[k]);
+        if (lm > m) {
+            s *= __expf(m - lm);
+            m = lm;
         }
-    }
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    m = warp_max(m);
-    if (lane == 0) red[wid] = m;
-    __syncthreads();
-    float gm = red[0];
-    for (int i = 1; i < nw; ++i) gm = fmaxf(gm, red[i]);
-    __syncthreads();
-    float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int base = (threadIdx.x + i * 512) * 8;
-        const uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float v = __uint_as_float((k & 1) ? (w[k >> 1] & 0xffff0000u) : (w[k >> 1] << 16));
-            if (base + k < V) s += __expf(v - gm);
-        }
+        for (int k = 0; k < 8; ++k) s += __expf(v[k] - m);
     }
-    s = warp_sum(s);
-    if (lane == 0) red[wid] = s;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    float wm = warp_max(m);
+    float ws = (m == -INFINITY) ? 0.f : s * __expf(m - wm);
+    ws = warp_sum(ws);
+    if (lane == 0) {
+        red_m[wid] = wm;
+        red_s[wid] = ws;
+    }
     __syncthreads();
+    float gm = red_m[0];
+    for (int i = 1; i < 8; ++i) gm = fmaxf(gm, red_m[i]);
     float tot = 0.f;
-    for (int i = 0; i < nw; ++i) tot += red[i];
+    for (int i = 0; i < 8; ++i) tot += red_m[i] == -INFINITY ? 0.f : red_s[i] * __expf(red_m[i] - gm);
     const float lse = gm + __logf(tot);
     const int tgt = target[row];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-        const int idx = threadIdx.x + i * 512;
-        if (idx >= nvec) continue;
-        const int base = idx * 8;
-        uint32_t w[4] = {r[i].x, r[i].y, r[i].z, r[i].w};
-        float p[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const float v = __uint_as_float((k & 1) ? (w[k >> 1] & 0xffff0000u) : (w[k >> 1] << 16));
-            if (base + k == tgt) row_loss[row] = lse - v;
-            float q = base + k < V ? __expf(v - lse) : 0.f;
-            if (base + k == tgt) q -= 1.f;
-            p[k] = q * inv_seq;
-        }
+    for (int i = threadIdx.x; i < nvec; i += 256) {
+        float v[8];
+        unpack8(L[i], v);
+        uint32_t w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(p[2 * k], p[2 * k + 1]);
+            float p0 = __expf(v[2 * k] - lse), p1 = __expf(v[2 * k + 1] - lse);
+            const int e0 = i * 8 + 2 * k;
+            if (e0 >= V) p0 = 0.f;
+            if (e0 + 1 >= V) p1 = 0.f;
+            if (e0 == tgt) {
+                row_loss[row] = lse - v[2 * k];
+                p0 -= 1.f;
+            }
+            if (e0 + 1 == tgt) {
+                row_loss[row] = lse - v[2 * k + 1];
+                p1 -= 1.f;
+            }
+            __nv_bfloat162 h = __floats2bfloat162_rn(p0 * inv_seq, p1 * inv_seq);
             w[k] = *reinterpret_cast<uint32_t*>(&h);
         }
-        L[idx] = make_uint4(w[0], w[1], w[2], w[3]);
+        L[i] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -557,11 +664,47 @@ void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int 
     ACCO_CHECK_LAUNCH();
 }
 
+static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
 template <class T>
 void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
                    cudaStream_t s) {
+    if constexpr (sizeof(T) == 2) {
+        if (a16(x) && a16(g) && a16(b) && a16(y) && d % 256 == 0) {
+            const int grid = ceil_div(M, 8);
+            switch (d / 256) {
+                case 1: ln_fwd_vec<1><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 2: ln_fwd_vec<2><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 3: ln_fwd_vec<3><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 4: ln_fwd_vec<4><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 8: ln_fwd_vec<8><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                default: break;
+            }
+        }
+    }
     ln_fwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(x, g, b, y, mean, rstd, M, d);
     ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+static bool ln_bwd_dx_vec(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
+                          bool accumulate_dx, int M, int d, cudaStream_t s) {
+    if constexpr (sizeof(T) == 2) {
+        if (a16(dy) && a16(x) && a16(g) && a16(dx) && d % 256 == 0) {
+            const int grid = ceil_div(M, 8), acc = accumulate_dx ? 1 : 0;
+            switch (d / 256) {
+                case 1: ln_bwd_vec<1><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 2: ln_bwd_vec<2><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 3: ln_bwd_vec<3><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 4: ln_bwd_vec<4><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 8: ln_bwd_vec<8><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                default: return false;
+            }
+            ACCO_CHECK_LAUNCH();
+            return true;
+        }
+    }
+    return false;
 }
 
 static unsigned* tickets() {
@@ -597,8 +740,10 @@ void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const
                    cudaStream_t s) {
     if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d)) {
         colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, acc, s);
-        ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
-        ACCO_CHECK_LAUNCH();
+        if (!ln_bwd_dx_vec<T>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) {
+            ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+            ACCO_CHECK_LAUNCH();
+        }
         return;
     }
     // parameter gradients first (they read dy only), then dx
@@ -633,16 +778,9 @@ void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, i
                    cudaStream_t s) {
     if constexpr (sizeof(T) == 2) {
         const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 8 == 0;
-        const int nvec = (V + 7) / 8;
-        if (aligned && nvec <= 512 * 16) {
-            auto* L = reinterpret_cast<__nv_bfloat16*>(logits);
-            const float inv = 1.0f / seq;
-            if (nvec <= 512 * 4)
-                ce_bf16_kernel<4><<<M, 512, 0, s>>>(L, ld, target, V, inv, row_loss);
-            else if (nvec <= 512 * 8)
-                ce_bf16_kernel<8><<<M, 512, 0, s>>>(L, ld, target, V, inv, row_loss);
-            else
-                ce_bf16_kernel<16><<<M, 512, 0, s>>>(L, ld, target, V, inv, row_loss);
+        if (aligned) {
+            ce_vec_kernel<<<M, 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(logits), ld, target, V, 1.0f / seq,
+                                            row_loss);
             ACCO_CHECK_LAUNCH();
             return;
         }
