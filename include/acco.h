@@ -134,6 +134,12 @@ int acco_reduce_scatter_f32(acco_comm* comm, const float* send, float* recv, uin
 /* Fabric::all_gather (collectives.cpp:77-91): recv holds nranks*count. */
 int acco_all_gather(acco_comm* comm, const void* send, void* recv, uint64_t count, int dtype,
                     void* stream);
+/* Owner-padded layout for NCCL's equal-count RS/AG when dim mod n != 0:
+ * chunk = ceil(dim/n); padded[w*chunk + j] <-> flat[lo_w + j] for
+ * j < hi_w - lo_w (shard_partition ranges), zero padding otherwise.
+ * pack: fp32 flat -> padded; unpack: padded -> flat (dtype F32 or BF16). */
+int acco_pack_padded(const float* flat, float* padded, uint64_t dim, int n, void* stream);
+int acco_unpack_padded(const void* padded, void* flat, uint64_t dim, int n, int dtype, void* stream);
 
 /* ----------------------------------------------------------- raw GEMM (K1)
  * C[m,n] (op)= sum_k A(m,k) B(n,k); operands K-major (ptr[row*ld+k]) or

@@ -72,6 +72,8 @@ _PROTOS = {
     "acco_all_reduce_i64": (C.c_int, [_P, _P, _P, C.c_uint64, _P]),
     "acco_reduce_scatter_f32": (C.c_int, [_P, _P, _P, C.c_uint64, _P]),
     "acco_all_gather": (C.c_int, [_P, _P, _P, C.c_uint64, C.c_int, _P]),
+    "acco_pack_padded": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P]),
+    "acco_unpack_padded": (C.c_int, [_P, _P, C.c_uint64, C.c_int, C.c_int, _P]),
     "acco_gemm": (C.c_int, [_P, C.c_int64, C.c_int, _P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
                             C.c_int, C.c_int, _P, C.c_int64, _P, _P, C.c_int64, _P, C.c_int64,
                             C.c_int, _P]),

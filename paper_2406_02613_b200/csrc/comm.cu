@@ -4,8 +4,11 @@
 #include "acco.h"
 #include "capi_util.h"
 #include "comm.h"
+#include "host_util.h"
+#include "lm_kernels.h"
 
 #include <cstring>
+#include <vector>
 
 namespace acco {
 
@@ -87,6 +90,32 @@ int acco_all_reduce_i64(acco_comm* c, const int64_t* send, int64_t* recv, uint64
 int acco_reduce_scatter_f32(acco_comm* c, const float* send, float* recv, uint64_t count, void* stream) {
     return guarded([&] { c->impl->reduce_scatter_f32(send, recv, count, static_cast<cudaStream_t>(stream)); });
 }
+int acco_pack_padded(const float* flat, float* padded, uint64_t dim, int n, void* stream) {
+    return guarded([&] {
+        ShardLayout l = shard_partition(dim, n);
+        std::vector<uint64_t> lo, sz;
+        for (int w = 0; w < n; ++w) {
+            lo.push_back(l.lo(w));
+            sz.push_back(l.size(w));
+        }
+        pack_padded(flat, padded, lo.data(), sz.data(), n, l.chunk(), static_cast<cudaStream_t>(stream));
+    });
+}
+
+int acco_unpack_padded(const void* padded, void* flat, uint64_t dim, int n, int dtype, void* stream) {
+    return guarded([&] {
+        ACCO_REQUIRE(dtype == ACCO_DTYPE_F32 || dtype == ACCO_DTYPE_BF16, "unpack_padded: bad dtype");
+        ShardLayout l = shard_partition(dim, n);
+        std::vector<uint64_t> lo, sz;
+        for (int w = 0; w < n; ++w) {
+            lo.push_back(l.lo(w));
+            sz.push_back(l.size(w));
+        }
+        unpack_padded(padded, flat, dtype == ACCO_DTYPE_F32 ? 4 : 2, lo.data(), sz.data(), n, l.chunk(),
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
 int acco_all_gather(acco_comm* c, const void* send, void* recv, uint64_t count, int dtype, void* stream) {
     return guarded([&] {
         ACCO_REQUIRE(dtype == ACCO_DTYPE_F32 || dtype == ACCO_DTYPE_BF16, "all_gather: bad dtype");
