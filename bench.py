@@ -293,6 +293,12 @@ def main():
     attn = {"ms": a["ms"], "tflops": a["work"] / (a["ms"] / 1e3) / 1e12 if a["ms"] > 0 else 0.0,
             "share_of_step": a["ms"] / p["wall_ms"]}
 
+    # per-class device time of the profiled pass (CUDA events on the launching
+    # streams; the optimizer class runs on the comm stream, concurrently)
+    breakdown = {c: {"ms_per_step": v["ms"] / args.steps, "share_of_step": v["ms"] / p["wall_ms"],
+                     "launches_per_step": v["launches"] / args.steps}
+                 for c, v in p.items() if isinstance(v, dict) and v.get("launches")}
+
     cpu = None
     if not args.no_cpu_baseline and world == 1 and not args.profile:
         from oracle import cpu_bench
@@ -320,7 +326,7 @@ def main():
                           "exposed_comm_pct": 100.0 * v["stats"]["comm_exposed_ms"] / v["stats"]["comm_busy_ms"]
                           if v["stats"]["comm_busy_ms"] else 0.0} for k, v in base.items()},
         "acco_vs_zero1_speedup": acco["tokens_per_s"] / base["zero1"]["tokens_per_s"] if "zero1" in base else None,
-        "roofline": roof, "roofline_optimizer": roof_opt, "attention": attn,
+        "roofline": roof, "roofline_optimizer": roof_opt, "attention": attn, "breakdown": breakdown,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": acco["clocks"], "gpu_launches": acco["launches"],
         "stage_counts_first_updates": acco["mb"],
     }

@@ -41,11 +41,15 @@ int acco_version(void);
 /* Instrumentation (B200 only): number of this library's kernel launches so
  * far, and optional CUDA-event timing per kernel class on the launching
  * stream — class 0 GEMM (work = algorithmic flops), 1 attention (flops),
- * 2 fused optimizer (algorithmic bytes), 3 other. */
+ * 2 fused optimizer (algorithmic bytes), 3 bias / LN-parameter column
+ * reductions (bytes), 4 LayerNorm fwd/bwd (bytes), 5 cross-entropy (bytes),
+ * 6 token gather / embedding (bytes), 7 other. */
+#define ACCO_PROF_CLASSES 8
 long long acco_launch_count(void);
 void acco_prof_enable(int on);
 int acco_prof_reset(void);
-int acco_prof_read(double ms[4], double work[4], long long launches[4]);
+int acco_prof_read(double ms[ACCO_PROF_CLASSES], double work[ACCO_PROF_CLASSES],
+                   long long launches[ACCO_PROF_CLASSES]);
 
 /* ------------------------------------------------------------------ shards
  * shard_partition (proj/include/accosim/shard.hpp:24-38): contiguous
@@ -196,8 +200,8 @@ int acco_model_value_and_grad(acco_model* m, const void* params, double* loss_ou
  * one device (comm == NULL; device-side Fabric with the reference's fixed
  * ascending-worker reduction order). */
 #define ACCO_METHOD_DDP 0
-#define ACCO_METHOD_DPU 1 /* not on the B200 path */
-#define ACCO_METHOD_WP 2  /* not on the B200 path */
+#define ACCO_METHOD_DPU 1 /* one-step-delayed update (protocols.cpp:357-379), warmup_rounds as DDP */
+#define ACCO_METHOD_WP 2  /* weight prediction (protocols.cpp:383-424): commit + transient prediction step */
 #define ACCO_METHOD_ACCO 3
 #define ACCO_METHOD_ZERO1 4 /* B200 baseline: DDP semantics, RS + sharded step + AG */
 
@@ -263,6 +267,29 @@ int acco_trainer_get_theta(acco_trainer* t, int which, float* host_out);
 int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t* mb_counts,
                      float* theta_history, acco_run_stats* stats);
 int acco_trainer_n_local(const acco_trainer* t);
+
+/* timeline.csv rows of the last acco_trainer_run (Timeline/Interval,
+ * proj/include/accosim/simclock.hpp; written by csvio.cpp:48-66), measured
+ * with CUDA events on the compute / comm streams, seconds since the run start.
+ * kind: ACCO_IV_* below (event_kind strings "init_grad", "microbatch",
+ * "all_reduce", "reduce_scatter", "optimizer", "all_gather"). */
+#define ACCO_IV_INIT_GRAD 0
+#define ACCO_IV_MICROBATCH 1
+#define ACCO_IV_ALL_REDUCE 2
+#define ACCO_IV_REDUCE_SCATTER 3
+#define ACCO_IV_OPTIMIZER 4
+#define ACCO_IV_ALL_GATHER 5
+typedef struct acco_interval {
+    int worker_id;
+    int stream; /* 0 compute, 1 comm */
+    int kind;
+    int micro_batches;
+    double t_start;
+    double t_end;
+    long long bytes;
+} acco_interval;
+/* Copies up to cap rows into out (nullable); *n_out = total row count. */
+int acco_trainer_timeline(const acco_trainer* t, acco_interval* out, int cap, int* n_out);
 
 #ifdef __cplusplus
 }

@@ -385,6 +385,7 @@ class SimConfig:
     n_grad_accumulation: int = 1
     full_batch_gradients: bool = False
     master_seed: int = 1
+    warmup_rounds: int = 0  # dpu: leading rounds with ddp semantics (protocols.hpp:33)
 
 
 def make_batch_stream(sim: SimConfig, rnd: int, tag: int, worker: int, ordinal: int) -> int:
@@ -432,6 +433,7 @@ class Trace:
     estimate_history: List[np.ndarray] = field(default_factory=list)
     consumed_mean_grad: List[np.ndarray] = field(default_factory=list)
     issued_micro_batches: int = 0
+    discarded_micro_batches: int = 0
     diverged: bool = False
 
 
@@ -585,6 +587,98 @@ def run_ddp(grad_fn: GradFn, theta0: np.ndarray, cfg: OptimizerConfig, sim: SimC
                       loss_sum / total):
             break
     return trace
+
+
+def _reduce_mean(bundles):
+    """reduce_mean (protocols.cpp:191-206): AR of the sums, AR of the counts, x 1/total."""
+    s = all_reduce([b.grad_sum for b in bundles])
+    total = all_reduce_counts([b.samples for b in bundles])
+    if total <= 0:
+        raise RuntimeError("protocol: zero consumed samples")
+    return s * (1.0 / float(total)), total
+
+
+def _run_delayed(method: str, grad_fn: GradFn, theta0: np.ndarray, cfg: OptimizerConfig, sim: SimConfig,
+                 t_updates: int, eval_fn: Optional[EvalFn] = None, smoothness=None, optimum=None,
+                 eval_every: int = 1) -> Trace:
+    """SyncEngine::dpu_round / wp_round (protocols.cpp:340-425), DPU's leading
+    `warmup_rounds` as ddp_round (:235-238). One pending bundle per worker
+    (computed in the previous round, or the Init-tag seed of :340-351) is
+    consumed by each update; the last round's fresh bundles are discarded."""
+    if cfg.total_steps == 0:
+        cfg = replace(cfg, total_steps=t_updates)
+    n = sim.n_workers
+    dim = theta0.shape[0]
+    state = OptimizerState.for_range(cfg, 0, dim)
+    theta = np.array(theta0, dtype=np.float64, copy=True)
+    estimate = theta.copy()
+    trace = Trace()
+    trace.theta_history.append(theta.copy())
+    trace.estimate_history.append(estimate.copy())
+    commit = _Commit(eval_fn, cfg, smoothness, optimum, eval_every)
+    k = sim.n_grad_accumulation
+    pending = None  # [(bundle, loss_sum)] per worker
+    for r in range(t_updates):
+        if method == "dpu" and r < sim.warmup_rounds:  # ddp_round
+            fresh = [_stage(grad_fn, sim, theta, w, r, TAG_MAIN, k, trace) for w in range(n)]
+            mean, total = _reduce_mean([b for b, _ in fresh])
+            if not np.all(np.isfinite(mean)):
+                trace.diverged = True
+                break
+            state, theta = opt_step(state, theta, mean, cfg)
+            estimate = theta
+            ok = commit(trace, r, theta, estimate, total, [b.micro for b, _ in fresh], [0] * n, mean,
+                        sum(l for _, l in fresh) / total)
+            if not ok:
+                break
+            continue
+        if method == "dpu":
+            if pending is None:  # seed_pending at the committed params
+                pending = [_stage(grad_fn, sim, theta, w, r, TAG_INIT, 1, trace) for w in range(n)]
+            params_for_compute = theta
+            fresh = [_stage(grad_fn, sim, params_for_compute, w, r, TAG_MAIN, k, trace) for w in range(n)]
+            consumed, pending = pending, fresh
+            mean, total = _reduce_mean([b for b, _ in consumed])
+            if not np.all(np.isfinite(mean)):
+                trace.diverged = True
+                break
+            state, theta = opt_step(state, theta, mean, cfg)
+            estimate = params_for_compute  # the applied gradients' params
+        else:  # wp
+            if pending is None:  # seed at the current prediction
+                pending = [_stage(grad_fn, sim, estimate, w, r, TAG_INIT, 1, trace) for w in range(n)]
+            consumed = pending
+            mean, total = _reduce_mean([b for b, _ in consumed])
+            if not np.all(np.isfinite(mean)):
+                trace.diverged = True
+                break
+            state, theta = opt_step(state, theta, mean, cfg)
+            _, estimate = opt_step(state.copy(), theta, mean, cfg)  # prediction on a throwaway copy
+            pending = [_stage(grad_fn, sim, estimate, w, r, TAG_MAIN, k, trace) for w in range(n)]
+        if not commit(trace, r, theta, estimate, total, [b.micro for b, _ in consumed], [0] * n, mean,
+                      sum(l for _, l in consumed) / total):
+            break
+    trace.discarded_micro_batches = sum(b.micro for b, _ in pending) if pending else 0
+    return trace
+
+
+def run_dpu(grad_fn, theta0, cfg, sim, t_updates, **kw) -> Trace:
+    return _run_delayed("dpu", grad_fn, theta0, cfg, sim, t_updates, **kw)
+
+
+def run_wp(grad_fn, theta0, cfg, sim, t_updates, **kw) -> Trace:
+    return _run_delayed("wp", grad_fn, theta0, cfg, sim, t_updates, **kw)
+
+
+def run_method(method: str, grad_fn, theta0, cfg, sim, t_updates, schedule=None, **kw) -> Trace:
+    """run_protocol's dispatch (protocols.cpp:734-741)."""
+    if method == "acco":
+        return run_acco(grad_fn, theta0, cfg, sim, t_updates, schedule=schedule, **kw)
+    if method in ("ddp", "zero1"):
+        return run_ddp(grad_fn, theta0, cfg, sim, t_updates, **kw)
+    if method in ("dpu", "wp"):
+        return _run_delayed(method, grad_fn, theta0, cfg, sim, t_updates, **kw)
+    raise ValueError(f"unknown method {method}")
 
 
 def schedule_from_records(records) -> list:

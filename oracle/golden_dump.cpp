@@ -6,8 +6,13 @@
 //   lr.json        scheduled_lr                    (proj/src/optim.cpp:37-48)
 //   optim.json     opt_step / sharded_opt_step     (proj/src/optim.cpp:50-119)
 //   fabric.json    Fabric RS / AG / AR / counts    (proj/src/collectives.cpp:36-91)
-//   protocols.json run_protocol ACCO + DDP traces  (proj/src/protocols.cpp:191-742)
+//   protocols.json run_protocol ACCO/DDP/DPU/WP traces (proj/src/protocols.cpp:191-742)
+//   io/            write_run_outputs of one run + the trace it was written from
+//                  (proj/src/csvio.cpp:12-102, config.cpp:147-157)
+//   memory.json    memory_model_bytes / memory_reported_gb (proj/src/convergence.cpp:182-205)
+#include <cmath>
 #include <cstdio>
+#include <limits>
 #include <fstream>
 #include <string>
 #include <vector>
@@ -15,6 +20,9 @@
 #include <json.hpp>
 
 #include "accosim/collectives.hpp"
+#include "accosim/config.hpp"
+#include "accosim/convergence.hpp"
+#include "accosim/csvio.hpp"
 #include "accosim/optim.hpp"
 #include "accosim/problems.hpp"
 #include "accosim/protocols.hpp"
@@ -233,6 +241,7 @@ static json run_case(const std::string& name, Method m, const Problem& p, Optimi
     j["sim"] = {{"n_workers", sim.n_workers},
                 {"batch_size", sim.batch_size},
                 {"n_grad_accumulation", sim.n_grad_accumulation},
+                {"warmup_rounds", sim.warmup_rounds},
                 {"full_batch_gradients", sim.full_batch_gradients},
                 {"master_seed", sim.master_seed},
                 {"alpha_s", sim.cost.alpha_s},
@@ -369,7 +378,107 @@ static json protocols_fixture() {
         cases.push_back(run_case("ddp_mlp_adamw", Method::ddp, make_mlp(2024, 4, 8, 64, 0.1),
                                  adamw(0.0075, 0.0, false), sim, 10));
     }
+    // one-step-delay baselines (protocols.cpp:340-425)
+    {
+        SimConfig sim;
+        sim.n_workers = 3;
+        sim.batch_size = 2;
+        sim.master_seed = 99;
+        cases.push_back(run_case("dpu_quadratic", Method::dpu, make_quadratic(55, 6, 0.2, 1.0, 0.7),
+                                 sgd(0.15), sim, 10));
+    }
+    {
+        SimConfig sim;
+        sim.n_workers = 2;
+        sim.batch_size = 4;
+        sim.n_grad_accumulation = 2;
+        sim.warmup_rounds = 3;
+        sim.master_seed = 17;
+        cases.push_back(run_case("dpu_logistic_adamw_warmup3", Method::dpu, make_logistic(11, 64, 8),
+                                 adamw(0.05, 0.01, true), sim, 10));
+    }
+    {
+        SimConfig sim;
+        sim.n_workers = 3;
+        sim.batch_size = 2;
+        sim.master_seed = 99;
+        cases.push_back(run_case("wp_quadratic", Method::wp, make_quadratic(55, 6, 0.2, 1.0, 0.7),
+                                 sgd(0.15), sim, 10));
+    }
+    {
+        SimConfig sim;
+        sim.n_workers = 2;
+        sim.batch_size = 8;
+        sim.n_grad_accumulation = 2;
+        sim.master_seed = 5;
+        cases.push_back(run_case("wp_mlp_adamw", Method::wp, make_mlp(2024, 4, 8, 64, 0.1),
+                                 adamw(0.0075, 0.1, true), sim, 10));
+    }
     return cases;
+}
+
+static json io_fixture(const std::string& dir) {
+    // the config of proj/tests/test_io.cpp:17-37
+    json cfgj = {
+        {"problem", {{"kind", "quadratic"}, {"dimension", 4}, {"l_smooth", 1.0},
+                     {"mu", 0.2}, {"noise_sigma", 0.1}, {"seed", 5}}},
+        {"method_name", "acco"},
+        {"optimizer",
+         {{"kind", "adamw"}, {"learning_rate", 0.01}, {"weight_decay", 0.1},
+          {"adam_beta1", 0.9}, {"adam_beta2", 0.95}, {"scheduler", "cosine"},
+          {"n_warmup_steps", 2}}},
+        {"n_workers", 2},
+        {"batch_size", 3},
+        {"n_grad_accumulation", 1},
+        {"warmup_rounds", 0},
+        {"t_updates", 5},
+        {"cost_model", {{"alpha_s", 0.1}, {"beta_s_per_byte", 1e-9}}},
+        {"heterogeneity",
+         {{"compute_s_per_microbatch", 1.0}, {"worker_multipliers", {1.0, 2.0}}}},
+        {"master_seed", 11},
+    };
+    ExperimentConfig cfg = parse_config(cfgj);
+    RunTrace tr = run_protocol(cfg.method, cfg.problem, cfg.optimizer, cfg.sim, cfg.t_updates);
+    write_run_outputs(dir + "/io", cfg.raw, tr, cfg.sim.n_workers);
+    json j;
+    j["config"] = cfg.raw;
+    j["config_hash"] = config_hash(cfg.raw);
+    j["n_workers"] = cfg.sim.n_workers;
+    j["diverged"] = tr.diverged;
+    json recs = json::array();
+    for (const RoundRecord& r : tr.records)
+        recs.push_back({{"update", r.update}, {"time_s", r.time_s}, {"samples_cum", r.samples_cum},
+                        {"loss", r.loss}, {"grad_sq", r.grad_sq},
+                        {"lyapunov", std::isnan(r.lyapunov) ? json(nullptr) : json(r.lyapunov)},
+                        {"idle_frac", r.idle_frac}});
+    j["records"] = recs;
+    json ivs = json::array();
+    for (const Interval& iv : tr.timeline.intervals)
+        ivs.push_back({iv.worker, to_string(iv.stream), iv.kind, iv.t_start, iv.t_end, iv.micro_batches, iv.bytes});
+    j["intervals"] = ivs;
+    // format_g17 samples (csvio.cpp:12-16) incl. the values the LM path emits
+    json g17 = json::array();
+    for (double v : {0.0, -0.0, 1.0, 0.1, 1e-300, 123456789.125, 3.0e22, -2.5e-7, 1.0 / 3.0, 6.02214076e23})
+        g17.push_back({v, format_g17(v)});
+    j["g17"] = g17;
+    j["g17_nan"] = format_g17(std::numeric_limits<double>::quiet_NaN());
+    j["g17_inf"] = format_g17(std::numeric_limits<double>::infinity());
+    j["metrics_header_1"] = metrics_header(1);
+    j["metrics_header_3"] = metrics_header(3);
+    return j;
+}
+
+static json memory_fixture() {
+    json rows = json::array();
+    for (const char* m : {"ddp", "zero1", "zero2", "zero3", "slowmo", "diloco", "co2", "dpu", "wp", "acco"})
+        for (double k : {12.0, 16.0})
+            for (double n : {1.0, 8.0, 64.0})
+                for (double psi : {124439808.0, 7.5e9}) {
+                    double b = memory_model_bytes(memory_method_from(m), k, n, psi);
+                    rows.push_back({{"method", m}, {"k", k}, {"n", n}, {"psi", psi}, {"bytes", b},
+                                    {"gb", memory_reported_gb(b)}});
+                }
+    return rows;
 }
 
 int main(int argc, char** argv) {
@@ -380,5 +489,7 @@ int main(int argc, char** argv) {
     write(dir, "optim.json", optim_fixture());
     write(dir, "fabric.json", fabric_fixture());
     write(dir, "protocols.json", protocols_fixture());
+    write(dir, "io_trace.json", io_fixture(dir));
+    write(dir, "memory.json", memory_fixture());
     return 0;
 }

@@ -58,8 +58,16 @@ class StatsC(C.Structure):
                 ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
 
 
+class IntervalC(C.Structure):
+    _fields_ = [("worker_id", C.c_int), ("stream", C.c_int), ("kind", C.c_int), ("micro_batches", C.c_int),
+                ("t_start", C.c_double), ("t_end", C.c_double), ("bytes", C.c_longlong)]
+
+
+IV_KINDS = ("init_grad", "microbatch", "all_reduce", "reduce_scatter", "optimizer", "all_gather")
+
 _P = C.c_void_p
 _lib.register({
+    "acco_trainer_timeline": (C.c_int, [_P, C.POINTER(IntervalC), C.c_int, C.POINTER(C.c_int)]),
     "acco_model_create": (C.c_int, [C.POINTER(LMCfgC), C.POINTER(C.c_void_p)]),
     "acco_model_destroy": (C.c_int, [_P]),
     "acco_model_num_params": (C.c_longlong, [_P]),
@@ -133,7 +141,7 @@ def launch_count() -> int:
     return int(_lib.lib().acco_launch_count())
 
 
-PROF_CLASSES = ("gemm", "attention", "optimizer", "other")
+PROF_CLASSES = ("gemm", "attention", "optimizer", "column_reduce", "layernorm", "cross_entropy", "embedding", "other")
 
 
 def prof_enable(on: bool = True):
@@ -145,9 +153,10 @@ def prof_enable(on: bool = True):
 def prof_read() -> dict:
     """Per-class kernel time (CUDA events on the launching stream), work
     (algorithmic flops for gemm/attention, bytes for the optimizer), launches."""
-    ms = (C.c_double * 4)()
-    work = (C.c_double * 4)()
-    n = (C.c_longlong * 4)()
+    k = len(PROF_CLASSES)
+    ms = (C.c_double * k)()
+    work = (C.c_double * k)()
+    n = (C.c_longlong * k)()
     _lib.call("acco_prof_read", ms, work, n)
     return {c: {"ms": ms[i], "work": work[i], "launches": int(n[i])} for i, c in enumerate(PROF_CLASSES)}
 
@@ -267,6 +276,7 @@ class RoundRecord:
     mb_main: List[int]
     mb_estimate: List[int]
     train_loss: float
+    idle_frac: List[float] = field(default_factory=list)  # compute-stream idle per worker this window
 
     @property
     def micro_batches(self):
@@ -284,6 +294,7 @@ class RunTrace:
     consumed_micro_batches: int = 0
     discarded_micro_batches: int = 0
     stats: dict = field(default_factory=dict)
+    timeline: list = field(default_factory=list)  # csvio.Interval rows, CUDA-event times
 
 
 class Trainer:
@@ -351,6 +362,17 @@ class Trainer:
         stats = {k: getattr(st, k) for k, _ in StatsC._fields_}
         return out, hist, stats, diverged
 
+    def timeline(self):
+        """timeline.csv rows of the last run() (CUDA-event times, seconds)."""
+        from .csvio import Interval
+
+        n = C.c_int(0)
+        _lib.call("acco_trainer_timeline", self._h, None, 0, C.byref(n))
+        buf = (IntervalC * max(n.value, 1))()
+        _lib.call("acco_trainer_timeline", self._h, buf, n.value, C.byref(n))
+        return [Interval(b.worker_id, "comm" if b.stream else "compute", IV_KINDS[b.kind], b.t_start, b.t_end,
+                         b.micro_batches, b.bytes) for b in buf[:n.value]]
+
 
 def run_protocol(method: str, problem, opt_cfg: OptimizerConfig, sim: SimConfig, t_updates: int,
                  theta0: Optional[np.ndarray] = None, comm: Optional[Comm] = None,
@@ -382,7 +404,8 @@ def run_protocol(method: str, problem, opt_cfg: OptimizerConfig, sim: SimConfig,
     tr = Trainer(method, model, opt_cfg, sim, comm)
     tr.set_theta(th0)
     recs, hist, stats, diverged = tr.run(t_updates, history=record_history)
-    out = RunTrace(records=recs, diverged=diverged, stats=stats)
+    out = RunTrace(records=recs, diverged=diverged, stats=stats, timeline=tr.timeline())
+    _fill_idle(out, sim, comm)
     out.issued_micro_batches = stats["issued_micro_batches"]
     out.consumed_micro_batches = stats["consumed_micro_batches"]
     out.discarded_micro_batches = stats["discarded_micro_batches"]
@@ -390,6 +413,23 @@ def run_protocol(method: str, problem, opt_cfg: OptimizerConfig, sim: SimConfig,
         out.theta_history = [th0.copy()] + [hist[t, 0].copy() for t in range(len(recs))]
         out.estimate_history = [th0.copy()] + [hist[t, 1].copy() for t in range(len(recs))]
     return out
+
+
+def _fill_idle(trace: RunTrace, sim: SimConfig, comm) -> None:
+    """RoundRecord.idle_frac for every worker (NCCL mode: gathered from the ranks)."""
+    from .csvio import idle_fractions
+
+    if comm is None:
+        rows = idle_fractions(trace.records, trace.timeline, range(sim.n_workers))
+    else:
+        import torch.distributed as dist
+
+        mine = idle_fractions(trace.records, trace.timeline, [comm.rank])
+        allr = [None] * comm.world
+        dist.all_gather_object(allr, [r[0] for r in mine])
+        rows = [[allr[w][t] for w in range(comm.world)] for t in range(len(trace.records))]
+    for r, row in zip(trace.records, rows):
+        r.idle_frac = row
 
 
 # ---------------------------------------------------------------------- config
@@ -484,3 +524,27 @@ def config_hash(j: dict) -> str:
         h ^= c
         h = (h * 0x100000001B3) & (2**64 - 1)
     return f"{h:016x}"
+
+
+# ---------------------------------------------------------------- memory model
+MEMORY_METHODS = ("ddp", "zero1", "zero2", "zero3", "slowmo", "diloco", "co2", "dpu", "wp", "acco")
+
+
+def memory_model_bytes(method: str, k: float, n: float, psi: float) -> float:
+    """Per-replica bytes (convergence.cpp:182-201; the paper's Table 1): bf16
+    params + grads (2 + 2 B), optimizer K B/param (sharded by N where the
+    method shards it); ACCO / DPU / WP add one bf16 communication buffer."""
+    if not (k > 0.0) or not (n >= 1.0) or not (psi >= 1.0):
+        raise InvalidArgument(_lib.INVALID, "memory_model: K > 0, N >= 1, psi >= 1 required")
+    table = {"ddp": (2 + 2 + k), "zero1": (2 + 2 + k / n), "zero2": (2 + (2 + k) / n), "zero3": ((2 + 2 + k) / n),
+             "slowmo": (2 + 2 + 2 * 2 + k), "diloco": (2 + 2 + 2 * 2 + k), "co2": (2 + 2 + 4 * 2 + k)}
+    if method in ("dpu", "wp", "acco"):
+        return (2 + 2 + 2 + k / n) * psi
+    if method not in table:
+        raise InvalidArgument(_lib.INVALID, f"memory_model: unknown method {method}")
+    return table[method] * psi
+
+
+def memory_reported_gb(b: float) -> int:
+    """convergence.cpp:203-205."""
+    return int(math.floor(b / 1e9 + 0.25))

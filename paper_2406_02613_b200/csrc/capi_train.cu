@@ -132,6 +132,18 @@ int acco_trainer_get_theta(acco_trainer* t, int which, float* host_out) {
 
 int acco_trainer_n_local(const acco_trainer* t) { return t ? t->impl->n_local() : 0; }
 
+int acco_trainer_timeline(const acco_trainer* t, acco_interval* out, int cap, int* n_out) {
+    return guarded([&] {
+        ACCO_REQUIRE(t && n_out, "acco_trainer_timeline: null argument");
+        const auto& tl = t->impl->timeline();
+        *n_out = static_cast<int>(tl.size());
+        for (int i = 0; out && i < cap && i < static_cast<int>(tl.size()); ++i) {
+            const auto& iv = tl[static_cast<size_t>(i)];
+            out[i] = acco_interval{iv.worker, iv.stream, iv.kind, iv.micro_batches, iv.t_start, iv.t_end, iv.bytes};
+        }
+    });
+}
+
 int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t* mb_counts, float* theta_history,
                      acco_run_stats* stats) {
     int diverged = 0;

@@ -63,7 +63,17 @@ void count_launch();
 
 // Optional per-class kernel timing with CUDA events on the launching stream
 // (acco_prof_*): used by bench.py for the live roofline numbers.
-enum ProfClass : int { kProfGemm = 0, kProfAttn = 1, kProfOpt = 2, kProfOther = 3, kProfClasses = 4 };
+enum ProfClass : int {
+    kProfGemm = 0,    // work = algorithmic flops
+    kProfAttn = 1,    // flops
+    kProfOpt = 2,     // algorithmic bytes
+    kProfReduce = 3,  // bias / LN-parameter column reductions: bytes
+    kProfNorm = 4,    // LayerNorm fwd/bwd: bytes
+    kProfCE = 5,      // cross-entropy fwd+bwd: bytes
+    kProfEmbed = 6,   // token gather, embedding fwd/bwd: bytes
+    kProfOther = 7,
+    kProfClasses = 8
+};
 bool prof_on();
 void prof_record(int cls, double work, cudaEvent_t a, cudaEvent_t b);
 cudaEvent_t prof_event();

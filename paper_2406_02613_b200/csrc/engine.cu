@@ -49,7 +49,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 }  // namespace
 
 struct Trainer::PhaseEvents {
-    EventArr post, stage_start, start, rs_done, opt_done, done, mb;
+    EventArr post, stage_start, start, cnt_done, rs_done, opt_done, done, mb;
     std::vector<long long> counts;  // [phase][local worker] samples posted
     int n_local = 1;
 };
@@ -57,8 +57,9 @@ struct Trainer::PhaseEvents {
 Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm)
     : model_(model), cfg_(cfg), sim_(sim), method_(method), comm_(comm) {
     validate(cfg_);
-    ACCO_REQUIRE(method == kACCO || method == kDDP || method == kZeRO1,
-                 "method: dpu/wp are not on the B200 path (SURVEY.md §8f 'next')");
+    ACCO_REQUIRE(method == kACCO || method == kDDP || method == kZeRO1 || method == kDPU || method == kWP,
+                 "method: unknown protocol");
+    ACCO_REQUIRE(sim.warmup_rounds >= 0, "run_protocol: warmup_rounds >= 0");
     ACCO_REQUIRE(sim.n_workers >= 1, "run_protocol: n_workers >= 1");
     ACCO_REQUIRE(sim.batch_size >= 1, "run_protocol: batch_size >= 1");
     ACCO_REQUIRE(sim.n_grad_accumulation >= 1, "run_protocol: n_grad_accumulation >= 1");
@@ -135,7 +136,7 @@ void Trainer::alloc() {
     // accumulators: ACCO ping-pongs two per worker; with a single virtual
     // worker the estimate shard *is* the accumulator, so a third one keeps it
     // alive through the commit phase without a copy.
-    const int nacc = method_ == kACCO ? (!comm_ && n_local_ == 1 ? 3 : 2) : 1;
+    const int nacc = method_ == kACCO ? (!comm_ && n_local_ == 1 ? 3 : 2) : (method_ == kDPU || method_ == kWP ? 2 : 1);
     for (int i = 0; i < n_local_ * nacc; ++i) {
         float* a = nullptr;
         ACCO_CUDA(cudaMalloc(&a, P * 4));
@@ -175,6 +176,7 @@ void Trainer::set_theta(const float* host) {
     step_ = 0;
     update_ = 0;
     samples_cum_ = 0;
+    pending_valid_ = false;
 }
 
 void Trainer::get_theta(int which, float* host) {
@@ -198,11 +200,12 @@ void Trainer::get_theta(int which, float* host) {
     }
 }
 
-int Trainer::stage_len(int p, int w, int T) const {
+int Trainer::stage_len(int p, int w, bool boot) const {
     if (method_ != kACCO) return sim_.n_grad_accumulation;
-    if (p == 0) return 1;  // bootstrap: one micro-batch at theta0 (protocols.cpp:468-474)
+    if (p == 0 && boot) return 1;  // bootstrap: one micro-batch at theta0 (protocols.cpp:468-474)
     if (sim_.schedule == kReplay) {
-        const int t = p / 2, half = p % 2;  // half 0: estimate, 1: main
+        const long long t = update_ + p / 2;
+        const int half = p % 2;  // half 0: estimate, 1: main
         const int gw = comm_ ? rank_ : w;
         const size_t i = (static_cast<size_t>(t) * 2 + half) * sim_.n_workers + gw;
         ACCO_REQUIRE(i < sim_.replay.size(), "replay schedule shorter than the run");
@@ -210,7 +213,6 @@ int Trainer::stage_len(int p, int w, int T) const {
         ACCO_REQUIRE(k >= 1, "acco: empty accumulator at barrier");  // protocols.cpp:603
         return k;
     }
-    (void)T;
     return std::max(sim_.n_grad_accumulation, 1);
 }
 
@@ -239,8 +241,66 @@ void Trainer::eval(const void* params, double* loss_slots, double* gsq_slot) {
     norm_sq(eval_grad_, psi_, gsq_slot, eval_scratch_, cs_);
 }
 
-void Trainer::launch_phase(int p, int t_base, int64_t* tot, PhaseEvents& ev) {
-    (void)t_base;
+// Fabric::reduce_scatter (collectives.cpp:55-75) of the accumulators with
+// parity acc_q: into this rank's shard `dst` (NCCL), the fixed-order sum of
+// the virtual workers, or the accumulator itself for one worker. DDP over NCCL
+// all-reduces in place (SyncEngine's reduce_mean, protocols.cpp:191-206).
+float* Trainer::reduce_grads(int acc_q, float* dst) {
+    const int nacc = static_cast<int>(acc_.size()) / n_local_;
+    auto acc_of = [&](int w) { return acc_[static_cast<size_t>(w) * nacc + acc_q % nacc]; };
+    if (comm_ && method_ == kDDP) {
+        comm_->all_reduce_f32(acc_of(0), acc_of(0), static_cast<size_t>(psi_), ms_);
+        return acc_of(0);
+    }
+    if (comm_) {
+        const float* send = acc_of(0);
+        if (padded_) {
+            std::vector<uint64_t> lo, sz;
+            for (int w = 0; w < world_; ++w) {
+                lo.push_back(layout_.lo(w));
+                sz.push_back(layout_.size(w));
+            }
+            pack_padded(send, pad_send_, lo.data(), sz.data(), world_, static_cast<uint64_t>(chunk_), ms_);
+            send = pad_send_;
+        }
+        comm_->reduce_scatter_f32(send, dst, static_cast<size_t>(chunk_), ms_);
+        return dst;
+    }
+    if (n_local_ == 1) return acc_of(0);
+    std::vector<const float*> in;
+    for (int w = 0; w < n_local_; ++w) in.push_back(acc_of(w));
+    sum_ordered(in.data(), n_local_, dst, psi_, ms_);
+    return dst;
+}
+
+// Fused sharded optimizer step on this rank's shard (K6 transient estimate when
+// !commit, K7 commit otherwise; optim.cpp:50-119), then Fabric::all_gather
+// (collectives.cpp:77-91) of the activation-dtype parameters into act_dst.
+void Trainer::opt_gather(bool commit, const float* g, const float* ret, const int64_t* tot, const int64_t* ret_tot,
+                         void* act_dst, void* ag_dst, cudaEvent_t after_opt) {
+    const bool sharded = comm_ && method_ != kDDP;
+    const int act = model_->act_dtype();
+    const size_t e = model_->act_bytes();
+    void* out = sharded ? static_cast<char*>(ag_dst) + static_cast<size_t>(rank_) * chunk_ * e : act_dst;
+    opt_apply(cfg_, step_, commit, g, ret, tot, ret_tot, master_, m_, v_, own_n_, out, act, flag_, ms_);
+    if (after_opt) ACCO_CUDA(cudaEventRecord(after_opt, ms_));
+    if (!sharded) return;
+    comm_->all_gather(out, ag_dst, static_cast<size_t>(chunk_), act, ms_);
+    if (padded_) {
+        std::vector<uint64_t> lo, sz;
+        for (int w = 0; w < world_; ++w) {
+            lo.push_back(layout_.lo(w));
+            sz.push_back(layout_.size(w));
+        }
+        unpack_padded(ag_dst, act_dst, static_cast<int>(e), lo.data(), sz.data(), world_,
+                      static_cast<uint64_t>(chunk_), ms_);
+    }
+}
+
+// Comm phase p on the comm stream: AR(counts) -> reduce -> optimizer -> AG
+// (protocols.cpp:613-631 for ACCO; apply_and_commit / wp_round for the
+// synchronous family). acc_q: parity of the accumulators consumed.
+void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool warm) {
     for (int w = 0; w < n_local_; ++w) ACCO_CUDA(cudaStreamWaitEvent(ms_, ev.post[static_cast<size_t>(p) * n_local_ + w], 0));
     ACCO_CUDA(cudaEventRecord(ev.start[p], ms_));
     long long local = 0;
@@ -253,97 +313,34 @@ void Trainer::launch_phase(int p, int t_base, int64_t* tot, PhaseEvents& ev) {
     } else {
         fill_i64(totp, local, ms_);
     }
-    const int act = model_->act_dtype();
-    const size_t e = model_->act_bytes();
-    const size_t P = static_cast<size_t>(psi_);
-    auto padded_args = [&](std::vector<uint64_t>& lo, std::vector<uint64_t>& sz) {
-        for (int w = 0; w < world_; ++w) {
-            lo.push_back(layout_.lo(w));
-            sz.push_back(layout_.size(w));
-        }
-    };
+    ACCO_CUDA(cudaEventRecord(ev.cnt_done[p], ms_));
     if (method_ == kACCO) {
         const bool est = p % 2 == 0;
-        const int nacc = static_cast<int>(acc_.size()) / n_local_;
-        auto acc_of = [&](int q, int w) { return acc_[static_cast<size_t>(w) * nacc + q % nacc]; };
-        float* g;
-        // 2. Fabric::reduce_scatter (collectives.cpp:55-75)
-        if (comm_) {
-            g = est ? g_ret_ : g_main_;
-            const float* send = acc_of(p, 0);
-            if (padded_) {
-                std::vector<uint64_t> lo, sz;
-                padded_args(lo, sz);
-                pack_padded(send, pad_send_, lo.data(), sz.data(), world_, static_cast<uint64_t>(chunk_), ms_);
-                send = pad_send_;
-            }
-            comm_->reduce_scatter_f32(send, g, static_cast<size_t>(chunk_), ms_);
-        } else if (n_local_ == 1) {
-            g = acc_of(p, 0);  // single worker: the accumulator is the reduced shard
-        } else {
-            g = est ? g_ret_ : g_main_;
-            std::vector<const float*> in;
-            for (int w = 0; w < n_local_; ++w) in.push_back(acc_of(p, w));
-            sum_ordered(in.data(), n_local_, g, psi_, ms_);
-        }
+        float* g = reduce_grads(acc_q, est ? g_ret_ : g_main_);
         ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
-        // 3. fused sharded optimizer: K6 estimate (transient) / K7 commit
-        void* agbuf = est ? ag_est_ : ag_theta_;
-        void* out = comm_ ? static_cast<char*>(agbuf) + static_cast<size_t>(rank_) * chunk_ * e : agbuf;
-        if (est) {
-            opt_apply(cfg_, step_, false, g, nullptr, totp, nullptr, master_, m_, v_, own_n_, out, act, flag_, ms_);
-        } else {
-            const float* ret = (comm_ || n_local_ > 1) ? g_ret_ : acc_of(p - 1, 0);
-            opt_apply(cfg_, step_, true, g, ret, totp, totp - 1, master_, m_, v_, own_n_, out, act, flag_, ms_);
+        if (est) {  // estimate on a transient copy of the shard state (protocols.cpp:652-658)
+            opt_gather(false, g, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
+        } else {    // commit with the retained estimate shard (protocols.cpp:661-670)
+            const int nacc = static_cast<int>(acc_.size()) / n_local_;
+            const float* ret = (comm_ || n_local_ > 1) ? g_ret_ : acc_[static_cast<size_t>((acc_q + nacc - 1) % nacc)];
+            opt_gather(true, g, ret, totp, totp - 1, theta_act_, ag_theta_, ev.opt_done[p]);
             ++step_;
         }
-        ACCO_CUDA(cudaEventRecord(ev.opt_done[p], ms_));
-        // 4. Fabric::all_gather (collectives.cpp:77-91), in place
-        if (comm_) {
-            comm_->all_gather(out, agbuf, static_cast<size_t>(chunk_), act, ms_);
-            if (padded_) {
-                std::vector<uint64_t> lo, sz;
-                padded_args(lo, sz);
-                unpack_padded(agbuf, est ? est_act_ : theta_act_, static_cast<int>(e), lo.data(), sz.data(), world_,
-                              static_cast<uint64_t>(chunk_), ms_);
-            }
-        }
     } else {
-        // DDP (all-reduce + replicated step) / ZeRO-1 (RS + sharded step + AG)
-        float* acc0 = acc_[0];
-        float* g = acc0;
-        void* out = theta_act_;
-        if (comm_ && method_ == kDDP) {
-            comm_->all_reduce_f32(acc0, acc0, P, ms_);
-        } else if (comm_) {
-            const float* send = acc0;
-            if (padded_) {
-                std::vector<uint64_t> lo, sz;
-                padded_args(lo, sz);
-                pack_padded(send, pad_send_, lo.data(), sz.data(), world_, static_cast<uint64_t>(chunk_), ms_);
-                send = pad_send_;
-            }
-            g = g_main_;
-            comm_->reduce_scatter_f32(send, g, static_cast<size_t>(chunk_), ms_);
-            out = static_cast<char*>(ag_theta_) + static_cast<size_t>(rank_) * chunk_ * e;
-        } else if (n_local_ > 1) {
-            std::vector<const float*> in;
-            for (int w = 0; w < n_local_; ++w) in.push_back(acc_[static_cast<size_t>(w)]);
-            g = g_main_;
-            sum_ordered(in.data(), n_local_, g, psi_, ms_);
-        }
+        float* g = reduce_grads(acc_q, g_main_);
         ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
-        opt_apply(cfg_, step_, true, g, nullptr, totp, nullptr, master_, m_, v_, own_n_, out, act, flag_, ms_);
-        ++step_;
-        ACCO_CUDA(cudaEventRecord(ev.opt_done[p], ms_));
-        if (comm_ && method_ == kZeRO1) {
-            comm_->all_gather(out, ag_theta_, static_cast<size_t>(chunk_), act, ms_);
-            if (padded_) {
-                std::vector<uint64_t> lo, sz;
-                padded_args(lo, sz);
-                unpack_padded(ag_theta_, theta_act_, static_cast<int>(e), lo.data(), sz.data(), world_,
-                              static_cast<uint64_t>(chunk_), ms_);
-            }
+        if (method_ == kDPU && !warm) {
+            // theta^(r+1) goes to the other replica: stage r still reads theta^(r),
+            // which becomes the record's estimate (protocols.cpp:361-378)
+            opt_gather(true, g, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
+            ++step_;
+            std::swap(theta_act_, est_act_);
+            std::swap(ag_theta_, ag_est_);
+        } else {
+            opt_gather(true, g, nullptr, totp, nullptr, theta_act_, ag_theta_, ev.opt_done[p]);
+            ++step_;
+            // WP: prediction step from the updated state on a throwaway copy (protocols.cpp:398-403)
+            if (method_ == kWP) opt_gather(false, g, nullptr, totp, nullptr, est_act_, ag_est_, nullptr);
         }
     }
     ACCO_CUDA(cudaEventRecord(ev.done[p], ms_));
@@ -374,12 +371,12 @@ void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* t
 }
 
 // after the commit of update t (comm stream): copy theta^(t+1), theta-tilde^(t+1)
-void Trainer::snapshot(int t) {
+void Trainer::snapshot(int t, bool est_is_theta) {
     if (!hist_dev_) return;
     const size_t bytes = static_cast<size_t>(psi_) * model_->act_bytes();
     char* dst = hist_dev_ + static_cast<size_t>(t) * 2 * bytes;
     ACCO_CUDA(cudaMemcpyAsync(dst, theta_act_, bytes, cudaMemcpyDeviceToDevice, ms_));
-    ACCO_CUDA(cudaMemcpyAsync(dst + bytes, method_ == kACCO ? est_act_ : theta_act_, bytes,
+    ACCO_CUDA(cudaMemcpyAsync(dst + bytes, est_is_theta ? theta_act_ : est_act_, bytes,
                               cudaMemcpyDeviceToDevice, ms_));
 }
 
@@ -426,6 +423,47 @@ double exposed(const std::vector<std::pair<double, double>>& comm, std::vector<s
 
 }  // namespace
 
+// timeline.csv rows of the last run() (csvio.cpp:48-66; the reference's
+// simulated intervals, protocols.cpp:278-289 and :536-537, :620-627, here from
+// the CUDA events of the two streams). One compute interval per stage and
+// worker; per comm phase: counts all-reduce, reduce(-scatter), optimizer,
+// all-gather (sync_kind: DDP's single all-reduce).
+void Trainer::build_timeline(int n_phases, const PhaseEvents& ev, cudaEvent_t base, bool sync_kind,
+                             const std::vector<int>& stage_k, const std::vector<char>& stage_init,
+                             const std::vector<char>& slot_used) {
+    timeline_.clear();
+    const int nl = n_local_;
+    const size_t n_slots = slot_used.size();  // stage_k: [slot][local worker]
+    auto wid = [&](int w) { return comm_ ? rank_ : w; };
+    for (size_t q = 0; q < n_slots; ++q) {
+        if (!slot_used[q]) continue;
+        for (int w = 0; w < nl; ++w) {
+            Interval iv;
+            iv.worker = wid(w);
+            iv.stream = 0;
+            iv.kind = stage_init[q] ? kIvInitGrad : kIvMicrobatch;
+            iv.t_start = elapsed(base, ev.stage_start[q * nl + w]) * 1e-3;
+            iv.t_end = elapsed(base, ev.post[q * nl + w]) * 1e-3;
+            iv.micro_batches = stage_k[q * nl + w];
+            timeline_.push_back(iv);
+        }
+    }
+    const long long psi = psi_;
+    const long long grad_bytes = psi * 4, param_bytes = psi * static_cast<long long>(model_->act_bytes());
+    const bool all_reduce = sync_kind && method_ == kDDP;
+    for (int p = 0; p < n_phases; ++p) {
+        const double t0 = elapsed(base, ev.start[p]) * 1e-3, t1 = elapsed(base, ev.cnt_done[p]) * 1e-3,
+                     t2 = elapsed(base, ev.rs_done[p]) * 1e-3, t3 = elapsed(base, ev.opt_done[p]) * 1e-3,
+                     t4 = elapsed(base, ev.done[p]) * 1e-3;
+        for (int w = 0; w < nl; ++w) {
+            timeline_.push_back({wid(w), 1, kIvAllReduce, t0, t1, 0, 8});
+            timeline_.push_back({wid(w), 1, all_reduce ? kIvAllReduce : kIvReduceScatter, t1, t2, 0, grad_bytes});
+            timeline_.push_back({wid(w), 1, kIvOptimizer, t2, t3, 0, 0});
+            if (!all_reduce) timeline_.push_back({wid(w), 1, kIvAllGather, t3, t4, 0, param_bytes});
+        }
+    }
+}
+
 void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     const int NP = 2 * T;
     const int nl = n_local_;
@@ -436,6 +474,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     ev.post.create(static_cast<size_t>(NP) * nl);
     ev.stage_start.create(static_cast<size_t>(NP) * nl);
     ev.start.create(NP);
+    ev.cnt_done.create(NP);
     ev.rs_done.create(NP);
     ev.opt_done.create(NP);
     ev.done.create(NP);
@@ -458,6 +497,10 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     ACCO_CUDA(cudaEventRecord(base, cs_));
     ACCO_CUDA(cudaStreamWaitEvent(ms_, base, 0));
     const uint64_t r0 = static_cast<uint64_t>(update_);
+    // a continuing run() resumes with the estimate stage of round r0 (the
+    // pipeline of the previous call drained at its last commit); a fresh run
+    // bootstraps with one Init micro-batch at theta0
+    const bool boot = update_ == 0;
     for (int p = 0; p < NP; ++p) {
         for (int w = 0; w < nl; ++w) {
             // stage p computes at the parameters of phase p-2 and reuses its accumulator
@@ -466,7 +509,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             float* acc = acc_[static_cast<size_t>(w) * nacc + p % nacc];
             const void* params;
             uint64_t round, tag;
-            if (p == 0) {
+            if (p == 0 && boot) {
                 params = theta_act_, round = r0, tag = kTagInit;
             } else if (p % 2 == 1) {
                 params = theta_act_, round = r0 + static_cast<uint64_t>((p - 1) / 2), tag = kTagMain;
@@ -475,7 +518,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             }
             int k = 0;
             const bool adaptive = sim_.schedule == kAdaptive && p >= 1;
-            const int target = stage_len(p, w, T);
+            const int target = stage_len(p, w, boot);
             while (true) {
                 if (!adaptive && k >= target) break;
                 if (adaptive && k >= target) {
@@ -496,8 +539,8 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             ev.counts[static_cast<size_t>(p) * nl + w] = static_cast<long long>(k) * B;
             ACCO_CUDA(cudaEventRecord(ev.post[static_cast<size_t>(p) * nl + w], cs_));
         }
-        launch_phase(p, 0, tot, ev);
-        if (p % 2 == 1) snapshot((p - 1) / 2);
+        launch_phase(p, p, tot, ev);
+        if (p % 2 == 1) snapshot((p - 1) / 2, false);
         if (do_eval && p % 2 == 1) {
             const int t = (p - 1) / 2;
             if ((static_cast<long long>(update_) + t + 1) % sim_.eval_every == 0) {
@@ -573,6 +616,11 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     }
     st.opt_launches = NP;
     st.comm_exposed_ms = exposed(comm_iv, comp_iv, &st.comm_busy_ms, &st.compute_busy_ms);
+    {
+        std::vector<char> init(static_cast<size_t>(NP), 0), used(static_cast<size_t>(NP), 1);
+        init[0] = boot;
+        build_timeline(NP, ev, base, false, stage_len_rec, init, used);
+    }
     st.wall_ms = elapsed(base, ev.done[NP - 1]);
     update_ += T;
     cudaEventDestroy(base);
@@ -580,19 +628,31 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     if (eval_buf) cudaFree(eval_buf);
 }
 
+// Synchronous family (SyncEngine, protocols.cpp:218-425). DDP / ZeRO-1: the
+// round's bundles are computed at theta and applied at once. DPU: the bundle
+// computed in round r-1 at theta^(r-1) is applied while round r's bundle is
+// computed at theta^(r) (one-step delay; leading warmup_rounds as DDP). WP: the
+// pending bundle is applied, a prediction step on a throwaway state copy gives
+// theta-tilde, and round r's bundle is computed there. "slot q" = the bundle
+// consumed by phase q; slot T holds the DPU/WP bundle left pending at the end.
 void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     const int nl = n_local_;
     const int B = sim_.batch_size;
     const int k = sim_.n_grad_accumulation;
+    const bool delayed_method = method_ == kDPU || method_ == kWP;
+    const int NS = T + 1;  // slots
     PhaseEvents ev;
     ev.n_local = nl;
-    ev.post.create(static_cast<size_t>(T) * nl);
-    ev.stage_start.create(static_cast<size_t>(T) * nl);
+    ev.post.create(static_cast<size_t>(NS) * nl);
+    ev.stage_start.create(static_cast<size_t>(NS) * nl);
     ev.start.create(T);
+    ev.cnt_done.create(T);
     ev.rs_done.create(T);
     ev.opt_done.create(T);
     ev.done.create(T);
-    ev.counts.assign(static_cast<size_t>(T) * nl, 0);
+    ev.counts.assign(static_cast<size_t>(NS) * nl, 0);
+    std::vector<int> slot_k(static_cast<size_t>(NS), 0);
+    std::vector<char> slot_used(static_cast<size_t>(NS), 0), slot_init(static_cast<size_t>(NS), 0);
     int64_t* tot = nullptr;
     ACCO_CUDA(cudaMalloc(&tot, T * sizeof(int64_t)));
     const bool do_eval = sim_.eval_every > 0;
@@ -600,35 +660,87 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
                                                   sim_.eval_batch > 0 ? std::min(sim_.eval_batch, model_->cfg().max_batch)
                                                                       : model_->cfg().max_batch)
                                       : 0;
-    double* eval_buf = nullptr;
-    if (do_eval) ACCO_CUDA(cudaMalloc(&eval_buf, static_cast<size_t>(T) * (n_eval_chunks + 1) * sizeof(double)));
-    std::vector<int> mb_round;
+    double* eval_buf = nullptr;  // [T][2 (theta, est)][n_chunks + 1 (gsq)]
+    if (do_eval) ACCO_CUDA(cudaMalloc(&eval_buf, static_cast<size_t>(T) * 2 * (n_eval_chunks + 1) * sizeof(double)));
+    std::vector<char> est_is_theta(static_cast<size_t>(T), 1);
+    std::vector<int> mb_slot;
     const long long mb0 = mb_counter_;
     cudaEvent_t base;
     ACCO_CUDA(cudaEventCreate(&base));
     ACCO_CUDA(cudaEventRecord(base, cs_));
     ACCO_CUDA(cudaStreamWaitEvent(ms_, base, 0));
-    for (int r = 0; r < T; ++r) {
-        const uint64_t round = static_cast<uint64_t>(update_ + r);
+    const double carried_loss = pending_valid_ ? pending_loss_ : 0.0;
+    EventArr eval_ev;
+    eval_ev.create(1);
+    cudaEvent_t eval_done = eval_ev[0];
+    if (pending_valid_) {  // bundle left pending by the previous run() call: already resident
         for (int w = 0; w < nl; ++w) {
-            if (r >= 1) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r - 1], 0));
-            ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(r) * nl + w], cs_));
-            float* acc = acc_[static_cast<size_t>(w)];
-            for (int j = 0; j < k; ++j) {
-                const int slot = static_cast<int>(mb_counter_ % loss_cap_);
-                micro(w, theta_act_, round, kTagMain, j, acc, loss_ring_ + slot);
-                mb_round.push_back(r);
+            ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(w)], cs_));
+            ACCO_CUDA(cudaEventRecord(ev.post[static_cast<size_t>(w)], cs_));
+            ev.counts[static_cast<size_t>(w)] = static_cast<long long>(pending_k_) * B;
+        }
+        slot_k[0] = pending_k_;
+        slot_used[0] = 1;
+    }
+    // one stage per local worker: n micro-batches at params into accumulator parity q, bundle slot `slot`
+    auto stage = [&](int slot, int q, const void* params, uint64_t round, uint64_t tag, int n) {
+        const int nacc = static_cast<int>(acc_.size()) / nl;
+        for (int w = 0; w < nl; ++w) {
+            ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(slot) * nl + w], cs_));
+            float* acc = acc_[static_cast<size_t>(w) * nacc + q % nacc];
+            for (int j = 0; j < n; ++j) {
+                const int ls = static_cast<int>(mb_counter_ % loss_cap_);
+                micro(w, params, round, tag, j, acc, loss_ring_ + ls);
+                mb_slot.push_back(slot);
                 ++mb_counter_;
             }
-            ev.counts[static_cast<size_t>(r) * nl + w] = static_cast<long long>(k) * B;
-            ACCO_CUDA(cudaEventRecord(ev.post[static_cast<size_t>(r) * nl + w], cs_));
+            ev.counts[static_cast<size_t>(slot) * nl + w] = static_cast<long long>(n) * B;
+            ACCO_CUDA(cudaEventRecord(ev.post[static_cast<size_t>(slot) * nl + w], cs_));
         }
-        launch_phase(r, 0, tot, ev);
-        snapshot(r);
+        slot_k[static_cast<size_t>(slot)] = n;
+        slot_used[static_cast<size_t>(slot)] = 1;
+        slot_init[static_cast<size_t>(slot)] = tag == kTagInit;
+    };
+    for (int r = 0; r < T; ++r) {
+        const uint64_t R = static_cast<uint64_t>(update_ + r);
+        const bool warm = !delayed_method || (method_ == kDPU && static_cast<long long>(R) < sim_.warmup_rounds);
+        if (r >= 1) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r - 1], 0));
+        if (warm) {  // ddp_round (protocols.cpp:321-338)
+            ACCO_REQUIRE(!pending_valid_, "dpu: warm-up round after the delayed rounds started");
+            stage(r, 0, theta_act_, R, kTagMain, k);
+            launch_phase(r, 0, tot, ev, true);
+        } else if (method_ == kDPU) {  // dpu_round (protocols.cpp:357-379)
+            if (!pending_valid_) {
+                stage(r, 0, theta_act_, R, kTagInit, 1);  // seed_pending (:340-351)
+                pending_slot_ = 0;
+                pending_valid_ = true;
+            }
+            stage(r + 1, pending_slot_ ^ 1, theta_act_, R, kTagMain, k);
+            launch_phase(r, pending_slot_, tot, ev, false);
+            pending_slot_ ^= 1;
+            est_is_theta[static_cast<size_t>(r)] = 0;
+        } else {  // wp_round (protocols.cpp:383-424)
+            if (!pending_valid_) {
+                stage(r, 0, est_act_, R, kTagInit, 1);
+                pending_slot_ = 0;
+                pending_valid_ = true;
+            }
+            launch_phase(r, pending_slot_, tot, ev, false);
+            ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r], 0));
+            stage(r + 1, pending_slot_ ^ 1, est_act_, R, kTagMain, k);
+            pending_slot_ ^= 1;
+            est_is_theta[static_cast<size_t>(r)] = 0;
+        }
+        snapshot(r, est_is_theta[static_cast<size_t>(r)]);
         if (do_eval && (update_ + r + 1) % sim_.eval_every == 0) {
             ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r], 0));
-            double* e0 = eval_buf + static_cast<size_t>(r) * (n_eval_chunks + 1);
+            double* e0 = eval_buf + static_cast<size_t>(r) * 2 * (n_eval_chunks + 1);
             eval(theta_act_, e0, e0 + n_eval_chunks);
+            if (!est_is_theta[static_cast<size_t>(r)]) eval(est_act_, e0 + n_eval_chunks + 1, e0 + 2 * n_eval_chunks + 1);
+            // DPU's next phase overwrites est_act_ and only waits for the
+            // (already posted) fresh stage: order it after the evaluation too
+            ACCO_CUDA(cudaEventRecord(eval_done, cs_));
+            ACCO_CUDA(cudaStreamWaitEvent(ms_, eval_done, 0));
         }
     }
     ACCO_CUDA(cudaStreamSynchronize(ms_));
@@ -642,12 +754,13 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
         std::memcpy(ring.data(), loss_host_, ring.size() * sizeof(double));
     else
         ACCO_CUDA(cudaMemcpy(ring.data(), loss_ring_, ring.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    std::vector<double> rl(T, 0.0);
+    std::vector<double> sl(static_cast<size_t>(NS), 0.0);
+    sl[0] = carried_loss;
     for (long long i = 0; i < nmb; ++i)
-        rl[static_cast<size_t>(mb_round[static_cast<size_t>(i)])] += ring[static_cast<size_t>((mb0 + i) % loss_cap_)];
+        sl[static_cast<size_t>(mb_slot[static_cast<size_t>(i)])] += ring[static_cast<size_t>((mb0 + i) % loss_cap_)];
     std::vector<double> evh;
     if (do_eval) {
-        evh.resize(static_cast<size_t>(T) * (n_eval_chunks + 1));
+        evh.resize(static_cast<size_t>(T) * 2 * (n_eval_chunks + 1));
         ACCO_CUDA(cudaMemcpy(evh.data(), eval_buf, evh.size() * sizeof(double), cudaMemcpyDeviceToHost));
     }
     int flag = 0;
@@ -660,33 +773,48 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
         rec.time_s = elapsed(base, ev.done[r]) * 1e-3;
         samples_cum_ += tot_h[r];
         rec.samples_cum = samples_cum_;
-        rec.train_loss = rl[r] / static_cast<double>(static_cast<long long>(nl) * k * B);
+        const int kc = slot_k[static_cast<size_t>(r)];
+        rec.train_loss = sl[static_cast<size_t>(r)] / static_cast<double>(static_cast<long long>(nl) * kc * B);
         for (int w = 0; w < nl; ++w) {
-            rec.mb_main.push_back(k);
+            rec.mb_main.push_back(kc);
             rec.mb_estimate.push_back(0);
         }
         if (do_eval && (update_ + r + 1) % sim_.eval_every == 0) {
-            const double* e0 = evh.data() + static_cast<size_t>(r) * (n_eval_chunks + 1);
+            const double* e0 = evh.data() + static_cast<size_t>(r) * 2 * (n_eval_chunks + 1);
             double l0 = 0;
             for (int c = 0; c < n_eval_chunks; ++c) l0 += e0[c];
             rec.loss = l0 / n;
             rec.grad_sq = e0[n_eval_chunks];
-            rec.grad_sq_estimate = rec.grad_sq;
+            rec.grad_sq_estimate = est_is_theta[static_cast<size_t>(r)] ? rec.grad_sq : e0[2 * n_eval_chunks + 1];
         }
         st.consumed += tot_h[r] / B;
         recs.push_back(rec);
     }
     st.issued = nmb;
+    if (delayed_method && pending_valid_) {
+        pending_k_ = slot_k[static_cast<size_t>(T)];
+        pending_loss_ = sl[static_cast<size_t>(T)];
+        st.discarded = static_cast<long long>(pending_k_) * nl;  // if the run ended here (protocols.cpp:246)
+    }
     std::vector<std::pair<double, double>> comm_iv, comp_iv;
     for (int r = 0; r < T; ++r) {
         comm_iv.emplace_back(elapsed(base, ev.start[r]), elapsed(base, ev.done[r]));
         st.opt_ms += elapsed(ev.rs_done[r], ev.opt_done[r]);
-        for (int w = 0; w < nl; ++w)
-            comp_iv.emplace_back(elapsed(base, ev.stage_start[static_cast<size_t>(r) * nl + w]),
-                                 elapsed(base, ev.post[static_cast<size_t>(r) * nl + w]));
     }
-    st.opt_launches = T;
+    for (int q = 0; q < NS; ++q) {
+        if (!slot_used[static_cast<size_t>(q)]) continue;
+        for (int w = 0; w < nl; ++w)
+            comp_iv.emplace_back(elapsed(base, ev.stage_start[static_cast<size_t>(q) * nl + w]),
+                                 elapsed(base, ev.post[static_cast<size_t>(q) * nl + w]));
+    }
+    st.opt_launches = T * (method_ == kWP ? 2 : 1);
     st.comm_exposed_ms = exposed(comm_iv, comp_iv, &st.comm_busy_ms, &st.compute_busy_ms);
+    {
+        std::vector<int> k_sw;
+        for (int q = 0; q < NS; ++q)
+            for (int w = 0; w < nl; ++w) k_sw.push_back(slot_k[static_cast<size_t>(q)]);
+        build_timeline(T, ev, base, true, k_sw, slot_init, slot_used);
+    }
     st.wall_ms = elapsed(base, ev.done[T - 1]);
     update_ += T;
     cudaEventDestroy(base);

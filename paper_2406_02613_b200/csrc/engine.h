@@ -46,6 +46,19 @@ struct RunStats {
     long long h2d_bytes = 0, d2h_bytes = 0;  // host-data path traffic during the run
 };
 
+// One timeline.csv row (simclock.hpp Interval; csvio.cpp:48-66), from CUDA
+// events, seconds since the start of the run() call.
+enum IntervalKind : int { kIvInitGrad = 0, kIvMicrobatch = 1, kIvAllReduce = 2, kIvReduceScatter = 3,
+                          kIvOptimizer = 4, kIvAllGather = 5 };
+struct Interval {
+    int worker = 0;
+    int stream = 0;  // 0 compute, 1 comm
+    int kind = 0;
+    double t_start = 0, t_end = 0;
+    int micro_batches = 0;
+    long long bytes = 0;
+};
+
 class Trainer {
 public:
     Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm);
@@ -60,18 +73,26 @@ public:
     // theta-tilde^(t+1) after each commit (RunTrace.theta/estimate_history).
     void run(int t_updates, std::vector<UpdateRecord>& recs, RunStats& st, float* theta_hist = nullptr);
     int n_local() const { return n_local_; }
+    const std::vector<Interval>& timeline() const { return timeline_; }
     cudaStream_t compute_stream() const { return cs_; }
 
 private:
     struct PhaseEvents;
     void alloc();
-    void launch_phase(int p, int t_base, int64_t* tot, PhaseEvents& ev);
+    void launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool warm = false);
+    float* reduce_grads(int acc_q, float* dst);
+    void opt_gather(bool commit, const float* g, const float* ret, const int64_t* tot, const int64_t* ret_tot,
+                    void* act_dst, void* ag_dst, cudaEvent_t after_opt);
     void run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st);
     void run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st);
-    void snapshot(int t);
+    void snapshot(int t, bool est_is_theta);
     void fetch_history(int T, float* host);
     char* hist_dev_ = nullptr;
-    int stage_len(int p, int w, int T) const;
+    int stage_len(int p, int w, bool boot) const;
+    void build_timeline(int n_phases, const PhaseEvents& ev, cudaEvent_t base, bool sync_kind,
+                        const std::vector<int>& stage_k, const std::vector<char>& stage_init,
+                        const std::vector<char>& slot_used);
+    std::vector<Interval> timeline_;
     void micro(int w, const void* params, uint64_t round, uint64_t tag, int ordinal, float* acc, double* loss_slot);
     void eval(const void* params, double* loss_slots, double* gsq_slot);
     void* theta_params() const { return theta_act_; }
@@ -108,6 +129,12 @@ private:
     long long update_ = 0; // committed updates so far (continues across run() calls)
     long long samples_cum_ = 0;
     long long mb_counter_ = 0;
+    // DPU / WP: the bundle computed in the last round awaits its optimizer
+    // step (SyncEngine::pending_, protocols.cpp:268); it survives run() calls
+    bool pending_valid_ = false;
+    int pending_slot_ = 0;       // accumulator parity holding it
+    int pending_k_ = 0;          // its micro-batches per worker
+    double pending_loss_ = 0.0;  // its summed micro-batch losses (local workers)
 };
 
 }  // namespace acco

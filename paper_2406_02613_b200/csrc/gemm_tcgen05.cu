@@ -278,9 +278,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 accumulators
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(2 * BN));
+                     "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
     }
 }
 
@@ -607,7 +608,7 @@ double plan_cost(int M, int N, int K, int bn, int splits, int sms) {
     const int units = ceil_div(M, kBM) * ceil_div(N, bn) * splits;
     const double waves = std::ceil(static_cast<double>(units) / sms);
     const double kb = std::ceil(static_cast<double>(ceil_div(K, kBK)) / splits);
-    const double eff = bn == 256 ? 1.0 : 1.25;
+    const double eff = bn == 256 ? 1.0 : bn == 192 ? 1.08 : 1.25;
     double c = waves * bn * kb * eff;
     // ordered split-K: each extra split adds one epilogue hand-off (~2-3 us,
     // measured) to the critical path; 1 cost unit ~ one 64-deep k-block column
@@ -627,7 +628,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     const int sms = num_sms();
     int best_bn = 256, best_sp = 1;
     double best = 1e300;
-    for (int bn : {256, 128}) {
+    for (int bn : {256, 192, 128}) {
         for (int sp : {1, 2, 3, 4, 6, 8}) {
             if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp ||
                            ceil_div(M, kBM) * ceil_div(N, bn) * 4 * 32 > kSemSlots))
@@ -642,13 +643,15 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     }
     if (const char* f = std::getenv("ACCO_GEMM_FORCE")) {  // tuning knob: "<bn>,<splits>"
         int fb = 0, fs = 0;
-        if (std::sscanf(f, "%d,%d", &fb, &fs) == 2 && (fb == 128 || fb == 256) && fs >= 1) {
+        if (std::sscanf(f, "%d,%d", &fb, &fs) == 2 && (fb == 128 || fb == 192 || fb == 256) && fs >= 1) {
             best_bn = fb;
             best_sp = ep.mode == kEpiAccF32 ? fs : 1;
         }
     }
     if (best_bn == 256)
         dispatch_major<256, 4>(A, B, M, N, K, ep, best_sp, stream);
+    else if (best_bn == 192)
+        dispatch_major<192, 4>(A, B, M, N, K, ep, best_sp, stream);
     else
         dispatch_major<128, 6>(A, B, M, N, K, ep, best_sp, stream);
 }

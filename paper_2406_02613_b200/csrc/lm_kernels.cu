@@ -654,12 +654,14 @@ int grid_for(int64_t n, int threads = 256) {
 // =================================================================== launchers
 void gather_tokens(const int32_t* data, int seq, int n_samples, uint64_t seed, int mode, int start, int B,
                    int32_t* tok_in, int32_t* tok_out, int32_t* idx_out, cudaStream_t s) {
+    ProfScope prof(kProfEmbed, 8.0 * B * seq, s);
     gather_tokens_kernel<<<B, 128, 0, s>>>(data, seq, n_samples, seed, mode, start, tok_in, tok_out, idx_out);
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
 void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int seq, int d, cudaStream_t s) {
+    ProfScope prof(kProfEmbed, 3.0 * M * d * sizeof(T), s);
     embed_fwd_kernel<T><<<M, 128, 0, s>>>(tok, wte, wpe, x, seq, d);
     ACCO_CHECK_LAUNCH();
 }
@@ -669,6 +671,7 @@ static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) ==
 template <class T>
 void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
                    cudaStream_t s) {
+    ProfScope prof(kProfNorm, 2.0 * M * d * sizeof(T) + 8.0 * M, s);
     if constexpr (sizeof(T) == 2) {
         if (a16(x) && a16(g) && a16(b) && a16(y) && d % 256 == 0) {
             const int grid = ceil_div(M, 8);
@@ -738,6 +741,7 @@ template <class T>
 void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
                    bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d, bool acc,
                    cudaStream_t s) {
+    ProfScope prof(kProfNorm, 3.0 * M * d * sizeof(T) + 8.0 * M, s);
     if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d)) {
         colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, acc, s);
         if (!ln_bwd_dx_vec<T>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) {
@@ -761,6 +765,7 @@ void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const
 
 template <class T>
 void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, bool acc, cudaStream_t s) {
+    ProfScope prof(kProfReduce, 1.0 * M * N * sizeof(T), s);
     if (vec_ok<T>(y, ld, N)) {
         colsum_vec<T, 0>(y, ld, nullptr, nullptr, nullptr, M, N, out, nullptr, scratch, acc, s);
         return;
@@ -776,6 +781,7 @@ void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch
 template <class T>
 void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, int seq, float* row_loss,
                    cudaStream_t s) {
+    ProfScope prof(kProfCE, 2.0 * M * V * sizeof(T), s);
     if constexpr (sizeof(T) == 2) {
         const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 8 == 0;
         if (aligned) {
@@ -797,6 +803,7 @@ void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_
 template <class T>
 void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
                uint32_t* sort_scratch, bool acc_wpe, cudaStream_t s) {
+    ProfScope prof(kProfEmbed, 1.0 * M * d * sizeof(T), s);
     ACCO_REQUIRE(static_cast<uint64_t>(V) * static_cast<uint64_t>(M) < 0xffffffffull,
                  "embed_bwd: vocab * tokens exceeds the 32-bit sort key");
     int P = 1;

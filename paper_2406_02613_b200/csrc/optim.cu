@@ -68,19 +68,26 @@ __device__ __forceinline__ void store_out(void* out, int64_t i, float x) {
 }
 
 // One element of opt_step; returns the new theta and updates m/v in registers.
+// Every rounding is pinned with _rn intrinsics (no compiler-chosen FMA
+// contraction), so the float4 path, the scalar path and any shard split give
+// bitwise-identical results — sharded == unsharded (verify.cpp:274-324).
 template <int KIND>
 __device__ __forceinline__ float step_elem(const KArgs& a, float g, float th, float& m, float& v) {
     if (KIND == 0) {  // sgd: theta -= lr * (g + wd*theta)
-        return th - a.lr * (g + a.wd * th);
+        return __fmaf_rn(-a.lr, __fmaf_rn(a.wd, th, g), th);
     }
-    if (KIND == 1) g += a.wd * th;  // adam: coupled decay
-    m = a.b1 * m + a.omb1 * g;
-    v = a.b2 * v + a.omb2 * g * g;
-    const float mh = m / a.c1;
-    const float vh = v / a.c2;
-    float u = mh / (sqrtf(vh) + a.eps);
-    if (KIND == 2) u += a.wd * th;  // adamw: decoupled decay
-    return th - a.lr * u;
+    if (KIND == 1) g = __fmaf_rn(a.wd, th, g);  // adam: coupled decay
+    m = __fmaf_rn(a.b1, m, __fmul_rn(a.omb1, g));
+    v = __fmaf_rn(a.b2, v, __fmul_rn(__fmul_rn(a.omb2, g), g));
+    const float mh = __fdiv_rn(m, a.c1);
+    const float vh = __fdiv_rn(v, a.c2);
+    float u = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.eps));
+    if (KIND == 2) u = __fmaf_rn(a.wd, th, u);  // adamw: decoupled decay
+    return __fmaf_rn(-a.lr, u, th);
+}
+
+__device__ __forceinline__ float scale_grad(float g, float r, float inv, bool has_ret) {
+    return __fmul_rn(has_ret ? __fadd_rn(g, r) : g, inv);
 }
 
 template <int KIND, bool COMMIT, bool HAS_RET, class OutT, bool VEC>
@@ -95,11 +102,12 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
         const int64_t n4 = a.n / 4;
         for (int64_t q = tid; q < n4; q += stride) {
             float4 g = __ldcs(reinterpret_cast<const float4*>(a.g) + q);
-            if (HAS_RET) {
-                float4 r = __ldcs(reinterpret_cast<const float4*>(a.gret) + q);
-                g.x += r.x; g.y += r.y; g.z += r.z; g.w += r.w;
-            }
-            g.x *= inv; g.y *= inv; g.z *= inv; g.w *= inv;
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (HAS_RET) r = __ldcs(reinterpret_cast<const float4*>(a.gret) + q);
+            g.x = scale_grad(g.x, r.x, inv, HAS_RET);
+            g.y = scale_grad(g.y, r.y, inv, HAS_RET);
+            g.z = scale_grad(g.z, r.z, inv, HAS_RET);
+            g.w = scale_grad(g.w, r.w, inv, HAS_RET);
             float4 th = reinterpret_cast<const float4*>(a.theta)[q];
             float4 m = make_float4(0.f, 0.f, 0.f, 0.f), v = m;
             if (KIND != 0) {
@@ -124,9 +132,7 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
         }
         // tail (n % 4) handled by the scalar loop below
         for (int64_t i = n4 * 4 + tid; i < a.n; i += stride) {
-            float g = a.g[i];
-            if (HAS_RET) g += a.gret[i];
-            g *= inv;
+            const float g = scale_grad(a.g[i], HAS_RET ? a.gret[i] : 0.f, inv, HAS_RET);
             float th = a.theta[i];
             float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
             bad |= !(isfinite(g) && isfinite(th));
@@ -139,9 +145,7 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
         }
     } else {
         for (int64_t i = tid; i < a.n; i += stride) {
-            float g = a.g[i];
-            if (HAS_RET) g += a.gret[i];
-            g *= inv;
+            const float g = scale_grad(a.g[i], HAS_RET ? a.gret[i] : 0.f, inv, HAS_RET);
             float th = a.theta[i];
             float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
             bad |= !(isfinite(g) && isfinite(th));

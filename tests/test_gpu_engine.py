@@ -28,14 +28,13 @@ def _oracle(method, cfg, opt, sim, T, schedule=None, theta0=None):
     prob = G.LMProblem(gc)
     th0 = G.default_theta0(gc, sim.master_seed).astype(np.float32).astype(np.float64) if theta0 is None else theta0
     ocfg = O.OptimizerConfig(**{k: getattr(opt, k) for k in O.OptimizerConfig.__dataclass_fields__})
-    osim = O.SimConfig(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, False, sim.master_seed)
+    osim = O.SimConfig(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, False, sim.master_seed,
+                       sim.warmup_rounds)
 
     def grad_fn(theta, stream):
         return prob.stochastic_grad(theta, stream, sim.batch_size)
 
-    if method == "acco":
-        return O.run_acco(grad_fn, th0, ocfg, osim, T, schedule=schedule, eval_fn=prob.value_and_grad)
-    return O.run_ddp(grad_fn, th0, ocfg, osim, T, eval_fn=prob.value_and_grad)
+    return O.run_method(method, grad_fn, th0, ocfg, osim, T, schedule=schedule, eval_fn=prob.value_and_grad)
 
 
 def _compare(tr, ref, tol=1e-5):
@@ -118,8 +117,49 @@ def test_engine_validation(cuda):
     with pytest.raises(api.InvalidArgument):
         api.run_protocol("acco", m, ADAMW, api.SimConfig(batch_size=8), 2)  # exceeds workspace
     with pytest.raises(api.InvalidArgument):
-        api.run_protocol("dpu", m, ADAMW, api.SimConfig(), 2)
+        api.run_protocol("dpu", m, ADAMW, api.SimConfig(warmup_rounds=-1), 2)
+    with pytest.raises(api.InvalidArgument):
+        api.run_protocol("pipeline", m, ADAMW, api.SimConfig(), 2)
     with pytest.raises(api.InvalidArgument):
         api.run_protocol("acco", m, ADAMW, api.SimConfig(), 0)
     with pytest.raises(api.InvalidArgument):
         api.run_protocol("acco", m, ADAMW, api.SimConfig(n_workers=2, schedule="adaptive"), 2)
+
+
+@pytest.mark.parametrize("method,n_workers,k,warmup", [("dpu", 1, 1, 0), ("dpu", 2, 2, 0), ("dpu", 2, 1, 2),
+                                                       ("wp", 1, 1, 0), ("wp", 3, 2, 0)])
+@pytest.mark.parametrize("opt", [ADAMW, SGD], ids=["adamw", "sgd"])
+def test_delayed_baselines_match_oracle(cuda, method, n_workers, k, warmup, opt):
+    """DPU / WP (protocols.cpp:340-425) on the same kernels: one pending bundle
+    per worker consumed per update, seeds, warm-up rounds, discarded tail."""
+    sim = api.SimConfig(n_workers=n_workers, batch_size=4, n_grad_accumulation=k, master_seed=13,
+                        warmup_rounds=warmup, eval_every=1)
+    tr = api.run_protocol(method, api.LMConfig(**MINI, precision="fp32", max_batch=8), opt, sim, 6)
+    ref = _oracle(method, MINI, opt, sim, 6)
+    assert not tr.diverged
+    _compare(tr, ref)
+    assert tr.issued_micro_batches == ref.issued_micro_batches
+    assert tr.discarded_micro_batches == ref.discarded_micro_batches == k * n_workers
+    for r, o in zip(tr.records, ref.records):
+        assert abs(r.grad_sq_estimate - o.grad_sq_estimate) <= 1e-4 * abs(o.grad_sq_estimate)
+
+
+@pytest.mark.parametrize("method", ["dpu", "wp", "acco", "zero1"])
+def test_run_continues_across_calls(cuda, method):
+    """Trainer.run(3) + run(3) == one 6-update run: the optimizer step, round
+    numbering (seeds) and the DPU/WP pending bundle carry over."""
+    opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
+                              scheduler="cosine", total_steps=6)
+    sim = api.SimConfig(n_workers=2, batch_size=4, n_grad_accumulation=1, master_seed=21)
+    model = api.Model(api.LMConfig(**MINI, precision="fp32", max_batch=8))
+    th0 = model.default_theta0(sim.master_seed)
+    t = api.Trainer(method, model, opt, sim)
+    t.set_theta(th0)
+    r1, h1, _, _ = t.run(3, history=True)
+    r2, h2, _, _ = t.run(3, history=True)
+    ref = _oracle(method, MINI, opt, sim, 6, theta0=th0.astype(np.float64))
+    hist = np.concatenate([h1, h2])
+    for i in range(6):
+        assert _rel(hist[i, 0], ref.theta_history[i + 1]) <= 1e-5, i
+        assert _rel(hist[i, 1], ref.estimate_history[i + 1]) <= 1e-5, i
+    assert [r.samples_cum for r in r1 + r2] == [o.samples_cum for o in ref.records]

@@ -108,3 +108,28 @@ def test_bad_args_raise(cuda):
     a = torch.zeros(8, 8, dtype=torch.bfloat16, device=cuda)
     with pytest.raises(_lib.InvalidArgument):
         gemm(a, False, a, False, 0, 8, 8, torch.empty(8, 8, dtype=torch.bfloat16, device=cuda))
+
+
+@pytest.mark.parametrize("force", ["128,1", "192,1", "256,1", "192,3", "128,4"])
+@pytest.mark.parametrize("a_mn,b_mn", list(itertools.product([False, True], repeat=2)))
+def test_every_tile_config(cuda, monkeypatch, force, a_mn, b_mn):
+    """Each tile width (BN 128/192/256) and ordered split-K, forced past the
+    cost model, on a ragged shape with several waves of tiles."""
+    monkeypatch.setenv("ACCO_GEMM_FORCE", force)
+    m, n, k = 1000, 776, 520
+    g = torch.Generator().manual_seed(11)
+    a, a_st = _operand(m, k, a_mn, torch.bfloat16, cuda, g)
+    b, b_st = _operand(n, k, b_mn, torch.bfloat16, cuda, g)
+    ref = a.float() @ b.float().t()
+    c = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, c)
+    c32 = torch.randn(m, n, generator=g).to(cuda)
+    c0 = c32.clone()
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, c32, mode=3, beta=1)
+    aux = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    cg = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    gemm(a_st, a_mn, b_st, b_mn, m, n, k, cg, mode=1, aux=aux)
+    torch.cuda.synchronize()
+    assert _rel(c, ref) < 6e-3
+    assert _rel(c32, c0 + ref) < 2e-6
+    assert _rel(cg, torch.nn.functional.gelu(ref, approximate="tanh")) < 8e-3

@@ -90,7 +90,7 @@ def _run_golden_case(c):
     cfg = O.OptimizerConfig.from_dict(c["optimizer"])
     s = c["sim"]
     sim = O.SimConfig(s["n_workers"], s["batch_size"], s["n_grad_accumulation"], s["full_batch_gradients"],
-                      s["master_seed"])
+                      s["master_seed"], s.get("warmup_rounds", 0))
     theta0 = np.array(c["theta_history"][0])
     bs, fb = sim.batch_size, sim.full_batch_gradients
 
@@ -101,8 +101,8 @@ def _run_golden_case(c):
         sched = O.schedule_from_records(c["records"])
         return O.run_acco(grad_fn, theta0, cfg, sim, c["t_updates"], schedule=sched,
                           eval_fn=p.value_and_grad, smoothness=p.smoothness, optimum=p.optimum)
-    return O.run_ddp(grad_fn, theta0, cfg, sim, c["t_updates"], eval_fn=p.value_and_grad,
-                     smoothness=p.smoothness, optimum=p.optimum)
+    return O.run_method(c["method"], grad_fn, theta0, cfg, sim, c["t_updates"], eval_fn=p.value_and_grad,
+                        smoothness=p.smoothness, optimum=p.optimum)
 
 
 @pytest.mark.parametrize("name", [c["name"] for c in load("protocols.json")])
@@ -125,6 +125,12 @@ def test_protocol_trajectories_bitwise(name):
         assert a.tolist() == b
     assert sum(sum(r.mb_main) + sum(r.mb_estimate) for r in tr.records) == c["consumed"]
     assert c["issued"] == c["consumed"] + c["discarded"]
+    if c["method"] != "acco":  # (acco replays the consumed schedule; its discards are not replayed)
+        assert tr.issued_micro_batches == c["issued"]
+    if c["method"] in ("dpu", "wp"):
+        assert tr.discarded_micro_batches == c["discarded"]
+        for r, g in zip(tr.records, c["records"]):
+            assert r.mb_main == g["mb_main"] and r.mb_estimate == g["mb_estimate"]
 
 
 @pytest.mark.parametrize("name", ["acco_logistic_adamw_k2", "acco_mlp_adam_warmup_k3", "acco_single_worker"])
