@@ -49,17 +49,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// A waiting thread is suspended in try_wait (up to this many ns) instead of
+// spinning, so waiting warps do not steal issue slots from the softmax warps.
+constexpr uint32_t kSuspendNs = 20000;
+// Watchdog for mbarrier spins: a pipeline bug becomes a launch error (trap)
+// after ~4 s instead of a hung GPU.
+__device__ __forceinline__ void watchdog(uint64_t& t0) {
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t0 == 0) t0 = now;
+    else if (now - t0 > 4000000000ull) __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     uint32_t ok = 0;
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
     while (!ok) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}\n"
             : "=r"(ok)
-            : "r"(a), "r"(parity)
+            : "r"(a), "r"(parity), "r"(kSuspendNs)
             : "memory");
+        if (!ok && (++spins & 255u) == 0) watchdog(t0);
     }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -343,6 +357,294 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ------------------------------------------------- forward, two-tile ping-pong
+// One CTA per (batch*head, pair of adjacent 128-query tiles 2p, 2p+1), heavy
+// pairs first. Both tiles share every K/V tile they both need (keys up to
+// tile 2p), loaded once. Two softmax groups (warps 4-7: tile 2p, warps 8-11:
+// tile 2p+1), thread = query row = TMEM lane, own the S/P and O of their tile
+// in TMEM. P never leaves TMEM: it is written (bf16 pairs) over the consumed
+// S columns and fed to O += P V as the A operand from tensor memory. The MMA
+// warp interleaves the tiles, so the tensor core runs one tile's PV / next QK^T
+// while the other tile's softmax runs:
+//     S0(0) S1(0) | [P0] PV0(0) S0(1) | [P1] PV1(0) S1(1) | [P0] PV0(1) S0(2) ...
+// The row sums l = sum_k P are computed by the tensor core too (P x ones,
+// N = 16, next to O), so they are exactly the sums of the bf16 P that PV used
+// and the softmax threads only do max / exp / pack.
+__device__ __forceinline__ void st_row32_global_fwd(__nv_bfloat16* dst, const uint32_t* o, float scale) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint4 u;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 0]) * scale, __uint_as_float(o[8 * c + 1]) * scale);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2]) * scale, __uint_as_float(o[8 * c + 3]) * scale);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 4]) * scale, __uint_as_float(o[8 * c + 5]) * scale);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 6]) * scale, __uint_as_float(o[8 * c + 7]) * scale);
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        u.z = *reinterpret_cast<uint32_t*>(&h2);
+        u.w = *reinterpret_cast<uint32_t*>(&h3);
+        reinterpret_cast<uint4*>(dst)[c] = u;
+    }
+}
+
+constexpr int F2_STAGES = 3;
+constexpr int F2_ONES = 2048;  // [16][128] bf16 ones: B operand of the row-sum MMA
+constexpr int F2_SMEM = 1024 + 2 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + F2_ONES + 256;
+
+__device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
+               int T, int H, float scale) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                         // [2 tiles]
+    uint8_t* sK = sQ + 2 * Q_BYTES;             // [stage]
+    uint8_t* sV = sK + F2_STAGES * KV_BYTES;    // [stage]
+    uint8_t* sOnes = sV + F2_STAGES * KV_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + F2_ONES);
+    uint64_t* q_full = bars;
+    uint64_t* kv_full = q_full + 1;              // [F2_STAGES]
+    uint64_t* kv_empty = kv_full + F2_STAGES;    // [F2_STAGES]
+    uint64_t* s_full = kv_empty + F2_STAGES;     // [2 tiles]
+    uint64_t* p_full = s_full + 2;               // [2 tiles]
+    uint64_t* o_done = p_full + 2;               // [2 tiles]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+    const int nqt = (T + BQ - 1) / BQ;
+    const int npair = (nqt + 1) / 2;
+    const int pr = npair - 1 - blockIdx.x;     // heavy pairs first
+    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    const int d = H * HD;
+    const int row_base = b * T;
+    const int nt[2] = {2 * pr + 1, 2 * pr + 2 <= nqt ? 2 * pr + 2 : 0};  // kv tiles per query tile (0: absent)
+    const int nkv = nt[1] ? nt[1] : nt[0];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        for (int s = 0; s < F2_STAGES; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
+        for (int x = 0; x < 2; ++x) {
+            mbar_init(&s_full[x], 1);
+            mbar_init(&p_full[x], 128);
+            mbar_init(&o_done[x], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 3) {  // bf16 ones for the row-sum MMA (read through the async proxy)
+        for (int i = lane; i < F2_ONES / 16; i += 32)
+            reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tslot;
+    // columns: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320), O tile 1 [320,384),
+    // row sums l (16 equal columns) tile 0 [384,400), tile 1 [400,416)
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(q_full, (nt[1] ? 2 : 1) * Q_BYTES);
+            tma_load_2d(sQ, &tmQKV, q_full, h * HD, row_base + 2 * pr * BQ);
+            if (nt[1]) tma_load_2d(sQ + Q_BYTES, &tmQKV, q_full, h * HD, row_base + (2 * pr + 1) * BQ);
+            for (int j = 0; j < nkv; ++j) {
+                const int s = j % F2_STAGES;
+                mbar_wait(&kv_empty[s], ((j / F2_STAGES) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
+                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], d + h * HD, row_base + j * BKV);
+                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], 2 * d + h * HD, row_base + j * BKV);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
+            constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
+            constexpr uint32_t id_l = idesc_bf16(BQ, 16, 0, 0);   // l += P 1: the row sums on the tensor core
+            const uint64_t ones = sdesc(smem_u32(sOnes), 16, 1024);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int x, int j) {
+                const int s = j % F2_STAGES;
+                if (x == 0 || !nt[0] || j >= nt[0]) {  // first user of K_j waits for it
+                    mbar_wait(&kv_full[s], (j / F2_STAGES) & 1);
+                    tc_after();
+                }
+                const uint32_t q_base = smem_u32(sQ + x * Q_BYTES), k_base = smem_u32(sK + s * KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk)
+                    umma(tmem + x * 128, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024), id_s,
+                         kk > 0);
+                umma_commit(&s_full[x]);
+            };
+            auto issue_pv = [&](int x, int j) {
+                const int s = j % F2_STAGES;
+                mbar_wait(&p_full[x], j & 1);
+                tc_after();
+                const uint32_t v_base = smem_u32(sV + s * KV_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8, sdesc(v_base + kk * 2048, 64 * 128, 1024),
+                            id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_ts(tmem + 384 + x * 16, tmem + x * 128 + kk * 8, ones, id_l, (j > 0 || kk > 0) ? 1u : 0u);
+                }
+            };
+            issue_s(0, 0);
+            if (nt[1]) issue_s(1, 0);
+            for (int j = 0; j < nkv; ++j) {
+                for (int x = 0; x < 2; ++x) {
+                    if (j >= nt[x]) continue;
+                    issue_pv(x, j);
+                    if (j + 1 < nt[x]) issue_s(x, j + 1);
+                    else umma_commit(&o_done[x]);
+                }
+                umma_commit(&kv_empty[j % F2_STAGES]);  // both tiles' PV_j issued: stage free on completion
+            }
+        }
+    } else if (warp >= 4) {
+        const int x = (warp - 4) >> 2;  // tile of this softmax group
+        const int wq = warp & 3;
+        const int n = nt[x];
+        if (n > 0) {
+            const int r = wq * 32 + lane;
+            const int q = (2 * pr + x) * BQ + r;
+            const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+            const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
+            const uint32_t tL = tmem + 384 + x * 16 + lane_off;
+            const float sl = scale * kLog2e;
+            float m = -INFINITY;
+            for (int j = 0; j < n; ++j) {
+                mbar_wait(&s_full[x], j & 1);
+                tc_after();
+                const bool diag = j == n - 1;  // the causal edge (and any ragged tail) sits in the last tile
+                const int kbase = j * BKV;
+                // pass 1: row max, S streamed from TMEM 64 columns (two loads) per wait.
+                // Valid keys of this row in the diagonal tile: [kbase, min(q + 1, T)).
+                const int lim = min(q + 1, T) - kbase;
+                float mx = -INFINITY;
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    uint32_t sv[64];
+                    tmem_ld32(tS + h2 * 64, sv);
+                    tmem_ld32(tS + h2 * 64 + 32, sv + 32);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) {
+                        float xv = __uint_as_float(sv[i]);
+                        if (diag) xv = h2 * 64 + i < lim ? xv : -INFINITY;
+                        mx = fmaxf(mx, xv);
+                    }
+                }
+                mx *= sl;
+                // lazy rescale: move the reference max only when it grows by > 2^8;
+                // O is stable here (s_full(j) is committed after PV(j-1))
+                if (j == 0) {
+                    m = mx;
+                } else {
+                    const bool need = mx > m + kRescaleThresh;
+                    const float alpha = need ? ex2(m - mx) : 1.f;
+                    if (need) m = mx;
+                    if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
+                        uint32_t o[32];
+#pragma unroll
+                        for (int c = 0; c < 2; ++c) {
+                            tmem_ld32(tO + c * 32, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                            tmem_st32(tO + c * 32, o);
+                        }
+                        uint32_t lv[16];  // the row sums live next to O
+                        tmem_ld16(tL, lv);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) lv[i] = __float_as_uint(__uint_as_float(lv[i]) * alpha);
+                        tmem_st16(tL, lv);
+                        tmem_wait_st();
+                    }
+                }
+                // pass 2: P = 2^(s - m) -> bf16 pairs over the consumed S columns; S
+                // re-read 64 columns per wait (P chunk h2 lands on columns already read)
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    uint32_t sv[64];
+                    tmem_ld32(tS + h2 * 64, sv);
+                    tmem_ld32(tS + h2 * 64 + 32, sv + 32);
+                    tmem_wait_ld();
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        float p0 = ex2(fmaf(__uint_as_float(sv[2 * i]), sl, -m));
+                        float p1 = ex2(fmaf(__uint_as_float(sv[2 * i + 1]), sl, -m));
+                        if (diag) {
+                            p0 = h2 * 64 + 2 * i < lim ? p0 : 0.f;
+                            p1 = h2 * 64 + 2 * i + 1 < lim ? p1 : 0.f;
+                        }
+                        __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
+                        pk[i] = *reinterpret_cast<uint32_t*>(&hb);
+                    }
+                    tmem_st16(tS + h2 * 32, pk);
+                    tmem_st16(tS + h2 * 32 + 16, pk + 16);
+                }
+                tmem_wait_st();
+                tc_before();
+                mbar_arrive(&p_full[x]);
+            }
+            mbar_wait(&o_done[x], 0);
+            tc_after();
+            uint32_t lv[16];
+            tmem_ld16(tL, lv);
+            tmem_wait_ld();
+            const float l = __uint_as_float(lv[0]);  // sum of the bf16 P the PV MMA used
+            const float inv = 1.f / l;
+            __nv_bfloat16* yr = y + (static_cast<int64_t>(b) * T + q) * d + h * HD;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + c * 32, o);  // warp-collective: every lane loads
+                tmem_wait_ld();
+                if (q < T) st_row32_global_fwd(yr + c * 32, o, inv);
+            }
+            if (q < T) lse[static_cast<int64_t>(bh) * T + q] = (m + log2f(l)) / kLog2e;
+        }
+    }
+    tc_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 // ----------------------------------------------------------------- backward
 // A [128 rows][128] bf16 tile written by threads (thread = row) as a K-major
 // UMMA A operand = two 64-column chunks of [128][128B], SW128.
@@ -354,6 +656,23 @@ __device__ __forceinline__ void st_row64_chunk(uint8_t* buf, int chunk, int r, c
         __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * unit + 2], v[8 * unit + 3]);
         __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * unit + 4], v[8 * unit + 5]);
         __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * unit + 6], v[8 * unit + 7]);
+        uint4 u;
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        u.z = *reinterpret_cast<uint32_t*>(&h2);
+        u.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(buf + chunk * (128 * 128) + r * 128 + ((unit ^ (r & 7)) << 4)) = u;
+    }
+}
+// Half of such a 64-column chunk: units 4*part .. 4*part+3 (32 columns)
+__device__ __forceinline__ void st_row32_part(uint8_t* buf, int chunk, int r, int part, const float* v) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int unit = 4 * part + k;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * k + 0], v[8 * k + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * k + 2], v[8 * k + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * k + 4], v[8 * k + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * k + 6], v[8 * k + 7]);
         uint4 u;
         u.x = *reinterpret_cast<uint32_t*>(&h0);
         u.y = *reinterpret_cast<uint32_t*>(&h1);
@@ -513,48 +832,80 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int key = k0 + r;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
+        // lse (log2) and D of query tile i, loaded one tile ahead (registers)
+        // by the half-0 threads and published through a double-buffered smem row
+        auto fetch = [&](int i, float& lv, float& dv) {
+            const int q = (kt + i) * BW_T + r;
+            const bool ok = i < nq && q < T;
+            lv = ok ? __ldg(lse + static_cast<int64_t>(bh) * T + q) * kLog2e : 0.f;
+            dv = ok ? __ldg(dsum + static_cast<int64_t>(bh) * T + q) : 0.f;
+        };
+        float nl = 0.f, nd = 0.f;
+        if (hf == 0) fetch(0, nl, nd);
         for (int i = 0; i < nq; ++i) {
             const int s = i & 1;
             const int q0 = (kt + i) * BW_T;
-            // lse (log2) and D for this query tile -> smem (one per half-0 thread)
             if (hf == 0) {
-                const int q = q0 + r;
-                sL[s * BW_T + r] = q < T ? lse[static_cast<int64_t>(bh) * T + q] * kLog2e : 0.f;
-                sD[s * BW_T + r] = q < T ? dsum[static_cast<int64_t>(bh) * T + q] : 0.f;
+                sL[s * BW_T + r] = nl;
+                sD[s * BW_T + r] = nd;
             }
             asm volatile("bar.sync 1, 256;" ::: "memory");  // softmax warps only
+            if (hf == 0) fetch(i + 1, nl, nd);  // latency hidden behind this tile
             mbar_wait(s_full, i & 1);
             tc_after();
-            if (i > 0) {
-                mbar_wait(g_done, (i - 1) & 1);  // previous dV/dK MMAs have read the operands
-                tc_after();
-            }
-            const bool edge = i == 0 || i == nq - 1;  // diagonal / ragged tail
+            // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
+            // rows past T belong to the next sequence)
+            const bool edge = i == 0 || q0 + BW_T > T;
+            const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + hf * 64);
+            const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + hf * 64);
             {
-                uint32_t st[64];
                 float p[64];
-                tmem_ld32(tS + lane_off + hf * 64, st);
-                tmem_ld32(tS + lane_off + hf * 64 + 32, st + 32);
-                tmem_wait_ld();
 #pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    const int qi = hf * 64 + c;
-                    float x = ex2(__uint_as_float(st[c]) * sl - sL[s * BW_T + qi]);
-                    if (edge) {
-                        const int q = q0 + qi;
-                        if (q < key || q >= T || key >= T) x = 0.f;
+                for (int hh = 0; hh < 2; ++hh) {  // S^T streamed 32 columns at a time
+                    uint32_t st[32];
+                    tmem_ld32(tS + lane_off + hf * 64 + hh * 32, st);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 l4 = L4[hh * 8 + c4];
+                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int c = hh * 32 + c4 * 4 + e;
+                            float x = ex2(fmaf(__uint_as_float(st[c4 * 4 + e]), sl, -lv[e]));
+                            if (edge) {
+                                const int q = q0 + hf * 64 + c;
+                                x = (q >= key && q < T) ? x : 0.f;
+                            }
+                            p[c] = x;
+                        }
                     }
-                    p[c] = x;
                 }
-                tmem_ld32(tP + lane_off + hf * 64, st);
-                tmem_ld32(tP + lane_off + hf * 64 + 32, st + 32);
-                tmem_wait_ld();
-                tc_before();
-                mbar_arrive(s_free);  // S^T / dP^T TMEM may be overwritten
+                if (i > 0) {  // the previous dV/dK MMAs have read the smem operands
+                    mbar_wait(g_done, (i - 1) & 1);
+                    tc_after();
+                }
                 st_row64_chunk(sPT, hf, r, p);
 #pragma unroll
-                for (int c = 0; c < 64; ++c) p[c] = p[c] * (__uint_as_float(st[c]) - sD[s * BW_T + hf * 64 + c]);
-                st_row64_chunk(sDS, hf, r, p);
+                for (int hh = 0; hh < 2; ++hh) {  // dS^T = P^T (dP^T - D), 32 columns at a time
+                    uint32_t st[32];
+                    tmem_ld32(tP + lane_off + hf * 64 + hh * 32, st);
+                    tmem_wait_ld();
+                    if (hh == 1) {
+                        tc_before();
+                        mbar_arrive(s_free);  // S^T / dP^T TMEM may be overwritten
+                    }
+                    float ds[32];
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 d4 = D4[hh * 8 + c4];
+                        ds[4 * c4 + 0] = p[hh * 32 + 4 * c4 + 0] * (__uint_as_float(st[4 * c4 + 0]) - d4.x);
+                        ds[4 * c4 + 1] = p[hh * 32 + 4 * c4 + 1] * (__uint_as_float(st[4 * c4 + 1]) - d4.y);
+                        ds[4 * c4 + 2] = p[hh * 32 + 4 * c4 + 2] * (__uint_as_float(st[4 * c4 + 2]) - d4.z);
+                        ds[4 * c4 + 3] = p[hh * 32 + 4 * c4 + 3] * (__uint_as_float(st[4 * c4 + 3]) - d4.w);
+                    }
+                    st_row32_part(sDS, hf, r, hh, ds);
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc_before();
@@ -699,10 +1050,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < nk; ++j) {
             mbar_wait(s_full, j & 1);
             tc_after();
-            if (j > 0) {
-                mbar_wait(g_done, (j - 1) & 1);  // previous dQ MMA has read dS
-                tc_after();
-            }
             const bool diag = j == nk - 1;
             {
                 uint32_t st[64];
@@ -712,10 +1059,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait_ld();
 #pragma unroll
                 for (int c = 0; c < 64; ++c) {
-                    float x = ex2(__uint_as_float(st[c]) * sl - L);
+                    float x = ex2(fmaf(__uint_as_float(st[c]), sl, -L));
                     if (diag) {
                         const int key = j * BW_T + hf * 64 + c;
-                        if (key > q || key >= T) x = 0.f;
+                        x = (key <= q && key < T) ? x : 0.f;
                     }
                     p[c] = x;
                 }
@@ -726,6 +1073,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(s_free);
 #pragma unroll
                 for (int c = 0; c < 64; ++c) p[c] = p[c] * (__uint_as_float(st[c]) - Dq);
+                if (j > 0) {  // the previous dQ MMA has read dS
+                    mbar_wait(g_done, (j - 1) & 1);
+                    tc_after();
+                }
                 st_row64_chunk(sDS, hf, r, p);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -838,10 +1189,16 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
     static bool cfg = false;
     if (!cfg) {
         ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM));
         cfg = true;
     }
-    dim3 grid((T + BQ - 1) / BQ, B * H);
-    fa_fwd_tc<<<grid, kThreads, SMEM, s>>>(m, y, lse, T, H, 1.0f / sqrtf(static_cast<float>(hd)));
+    const float scale = 1.0f / sqrtf(static_cast<float>(hd));
+    const int nqt = (T + BQ - 1) / BQ;
+    if (std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
+        fa_fwd_tc<<<dim3(nqt, B * H), kThreads, SMEM, s>>>(m, y, lse, T, H, scale);
+    } else {
+        fa_fwd_tc2<<<dim3((nqt + 1) / 2, B * H), kThreads, F2_SMEM, s>>>(m, y, lse, T, H, scale);
+    }
     ACCO_CHECK_LAUNCH();
     return true;
 }

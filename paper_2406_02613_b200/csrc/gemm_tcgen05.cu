@@ -59,16 +59,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(ok)
-        : "r"(addr), "r"(parity)
+        : "r"(addr), "r"(parity), "r"(20000u)  // suspend hint (ns): waiting warps sleep, not spin
         : "memory");
     return ok != 0;
 }
+// Watchdog for mbarrier spins: a pipeline bug becomes a launch error (trap)
+// after ~4 s instead of a hung GPU.
+__device__ __forceinline__ void watchdog(uint64_t& t0) {
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (t0 == 0) t0 = now;
+    else if (now - t0 > 4000000000ull) __trap();
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
     while (!mbar_try_wait(a, parity)) {
+        if ((++spins & 255u) == 0) watchdog(t0);
     }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {

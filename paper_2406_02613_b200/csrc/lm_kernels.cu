@@ -338,14 +338,31 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (ci < 64 && col < N) {
+    // the slab's last block folds the nchunk partials: 4 threads per column,
+    // each a fixed strided subset (independent loads in flight), then the four
+    // sub-sums in a fixed order — deterministic
+    {
+        const int cc = threadIdx.x & 63, sub = threadIdx.x >> 6;
+        const int colc = blockIdx.x * 64 + cc;
         float t0 = 0.f, t1 = 0.f;
-        for (int c = 0; c < nchunk; ++c) {
-            t0 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 0) * N + col]);
-            if (KIND == 1) t1 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 1) * N + col]);
+        if (colc < N) {
+#pragma unroll 4
+            for (int c = sub; c < nchunk; c += 4) {
+                t0 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 0) * N + colc]);
+                if (KIND == 1) t1 += __ldcg(&part[(static_cast<int64_t>(c) * 2 + 1) * N + colc]);
+            }
         }
-        out[col] = (acc ? out[col] : 0.f) + t0;
-        if (KIND == 1) out1[col] = (acc ? out1[col] : 0.f) + t1;
+        s0[sub][cc] = t0;
+        s1[sub][cc] = t1;
+        __syncthreads();
+        if (sub == 0 && colc < N) {
+            const float r0 = ((s0[0][cc] + s0[1][cc]) + s0[2][cc]) + s0[3][cc];
+            out[colc] = (acc ? out[colc] : 0.f) + r0;
+            if (KIND == 1) {
+                const float r1 = ((s1[0][cc] + s1[1][cc]) + s1[2][cc]) + s1[3][cc];
+                out1[colc] = (acc ? out1[colc] : 0.f) + r1;
+            }
+        }
     }
     if (threadIdx.x == 0) tickets[blockIdx.x] = 0;  // ready for the next launch (stream-ordered)
 }
@@ -729,7 +746,9 @@ template <class T, int KIND>
 static void colsum_vec(const T* y, int64_t ld, const T* x, const float* mean, const float* rstd, int M, int N,
                        float* out, float* out1, float* scratch, bool acc, cudaStream_t s) {
     const int slabs = ceil_div(N, 64);
-    int nchunk = std::max(1, std::min(ceil_div(2 * num_sms(), slabs), ceil_div(M, kVecRows)));
+    // ~8 blocks per SM: enough 16B loads in flight to stream the (L2-resident)
+    // operand at bandwidth; partials are reduced by each slab's last block
+    int nchunk = std::max(1, std::min(ceil_div(8 * num_sms(), slabs), ceil_div(M, kVecRows)));
     const int rpc = ceil_div(ceil_div(M, nchunk), kVecRows) * kVecRows;
     nchunk = ceil_div(M, rpc);
     colsum_vec_kernel<T, KIND><<<dim3(slabs, nchunk), 256, 0, s>>>(y, ld, x, mean, rstd, M, N, rpc, scratch,
@@ -738,19 +757,13 @@ static void colsum_vec(const T* y, int64_t ld, const T* x, const float* mean, co
 }
 
 template <class T>
-void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
-                   bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d, bool acc,
-                   cudaStream_t s) {
-    ProfScope prof(kProfNorm, 3.0 * M * d * sizeof(T) + 8.0 * M, s);
+void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* gdst, float* bdst,
+                          float* scratch, int M, int d, bool acc, cudaStream_t s) {
+    ProfScope prof(kProfReduce, 2.0 * M * d * sizeof(T) + 8.0 * M, s);
     if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d)) {
         colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, acc, s);
-        if (!ln_bwd_dx_vec<T>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) {
-            ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
-            ACCO_CHECK_LAUNCH();
-        }
         return;
     }
-    // parameter gradients first (they read dy only), then dx
     const int nchunk = ceil_div(M, kColChunk);
     float* p0 = scratch;
     float* p1 = scratch + static_cast<int64_t>(nchunk) * d;
@@ -759,6 +772,15 @@ void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const
     ACCO_CHECK_LAUNCH();
     colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p0, nchunk, d, gdst, acc ? 1 : 0);
     colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst, acc ? 1 : 0);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
+                      bool accumulate_dx, int M, int d, cudaStream_t s) {
+    ProfScope prof(kProfNorm, 3.0 * M * d * sizeof(T) + 8.0 * M, s);
+    if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d) && ln_bwd_dx_vec<T>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s))
+        return;
     ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
     ACCO_CHECK_LAUNCH();
 }
@@ -898,8 +920,10 @@ void spin_ns(uint64_t ns, cudaStream_t s) {
 #define ACCO_INST(T)                                                                                          \
     template void embed_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);          \
     template void layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, cudaStream_t); \
-    template void layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, float*, \
-                                   float*, float*, int, int, bool, cudaStream_t);                             \
+    template void layernorm_bwd_params<T>(const T*, const T*, const float*, const float*, float*, float*,      \
+                                          float*, int, int, bool, cudaStream_t);                              \
+    template void layernorm_bwd_dx<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, int, \
+                                      int, cudaStream_t);                                                     \
     template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);             \
     template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
     template void embed_bwd<T>(const int32_t*, const T*, int, int, int, int, float*, float*, uint32_t*,      \

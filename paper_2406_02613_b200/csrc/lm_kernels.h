@@ -22,11 +22,15 @@ template <class T>
 void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
                    cudaStream_t s);
 
-// dx (+)= LN backward of dy; dg/db gradients added into fp32 gdst/bdst.
+// LN backward, split so the parameter reductions can run on a side stream:
+// dg/db (+)= sum_rows dy * xhat, dy into fp32 gdst/bdst (uses `scratch`) ...
 template <class T>
-void layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd,
-                   T* dx, bool accumulate_dx, float* gdst, float* bdst, float* scratch, int M, int d,
-                   bool accumulate_params, cudaStream_t s);
+void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* gdst,
+                          float* bdst, float* scratch, int M, int d, bool accumulate_params, cudaStream_t s);
+// ... and dx (+)= the input gradient.
+template <class T>
+void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
+                      bool accumulate_dx, int M, int d, cudaStream_t s);
 
 // out[c] += sum_r y[r*ld + c] (deterministic two-level), fp32 out.
 template <class T>

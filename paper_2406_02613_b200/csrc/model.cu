@@ -152,9 +152,12 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_CUDA(cudaMalloc(&lse_, L * H * M * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&dsum_, H * M * sizeof(float)));
     // column-reduction partials: [chunks][2][N] with N <= 4d; chunks <= max(M/256,
-    // 2 x SMs) (see colsum_vec / colreduce in lm_kernels.cu)
-    const int64_t nchunk = std::max<int64_t>((M + 255) / 256, 2 * num_sms());
+    // 8 x SMs) (see colsum_vec / colreduce in lm_kernels.cu)
+    const int64_t nchunk = std::max<int64_t>((M + 255) / 256, 8 * num_sms());
     ACCO_CUDA(cudaMalloc(&scratch_, nchunk * 4 * d * 2 * sizeof(float)));
+    ACCO_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+    ACCO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    ACCO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
 }
 
 GPTModel::~GPTModel() {
@@ -168,6 +171,12 @@ GPTModel::~GPTModel() {
     cudaFree(stats_);
     cudaFree(lse_);
     cudaFree(dsum_);
+    if (aux_) {
+        cudaStreamSynchronize(aux_);
+        cudaStreamDestroy(aux_);
+        cudaEventDestroy(ev_fork_);
+        cudaEventDestroy(ev_join_);
+    }
     cudaFree(scratch_);
     if (pinned_data_) cudaFreeHost(pinned_data_);
     if (stage_host_) cudaFreeHost(stage_host_);
@@ -296,36 +305,62 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     // per-stage memset of the accumulator is unnecessary.
     const bool acc = accumulate_;
     const int beta = acc ? 1 : 0;
+    // Column reductions (bias and LN-parameter gradients) go to the side
+    // stream aux_ right after their input is produced and overlap the next
+    // GEMMs; `join` is placed before the next kernel that overwrites a buffer
+    // an outstanding reduction still reads (DX, DA, DT, DQKV). They share one
+    // scratch area, so they are serialised on aux_ (FIFO) — same kernels and
+    // summation order as inline, so results are bitwise unchanged.
+    auto fork = [&] {
+        ACCO_CUDA(cudaEventRecord(ev_fork_, s));
+        ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    };
+    auto join = [&] {
+        ACCO_CUDA(cudaEventRecord(ev_join_, aux_));
+        ACCO_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    };
     // LM head (tied to wte): dwte (+)= dlogits^T hf ; dhf = dlogits wte
     mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d, beta), s);
     mm<T>(LOG, vpad_, false, W(kWte), d, true, M, d, V, ep_store(DT, d), s);
-    layernorm_bwd<T>(DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), DX, false, Gp(kLnf), Gp(kLnf + 1), scratch_,
-                     M, d, acc, s);
+    fork();
+    layernorm_bwd_params<T>(DT, X(L), stat(4 * L), stat(4 * L + 1), Gp(kLnf), Gp(kLnf + 1), scratch_, M, d, acc, aux_);
+    layernorm_bwd_dx<T>(DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), DX, false, M, d, s);
     for (int l = L - 1; l >= 0; --l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
           *A = slot(l, sA), *U = slot(l, sU);
         // MLP
+        fork();
+        colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, acc, aux_);
         mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d, beta), s);
-        colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, acc, s);
+        join();  // DA (and DT, DX) free of outstanding readers
         mm<T>(DX, d, false, W(li(l, 10)), 4 * d, true, M, 4 * d, d, ep_dgelu(DA, 4 * d, A), s);
+        fork();
+        colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, acc, aux_);
         mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d, beta), s);
-        colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, acc, s);
         mm<T>(DA, 4 * d, false, W(li(l, 8)), d, true, M, d, 4 * d, ep_store(DT, d), s);
-        layernorm_bwd<T>(DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), DX, true, Gp(li(l, 6)), Gp(li(l, 7)),
-                         scratch_, M, d, acc, s);
+        fork();
+        layernorm_bwd_params<T>(DT, XM, stat(4 * l + 2), stat(4 * l + 3), Gp(li(l, 6)), Gp(li(l, 7)), scratch_, M, d,
+                                acc, aux_);
+        layernorm_bwd_dx<T>(DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), DX, true, M, d, s);
         // attention
+        fork();
+        colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, acc, aux_);
         mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
-        colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, acc, s);
+        join();  // DT (read by the LN2 parameter reduction) is overwritten next
         mm<T>(DX, d, false, W(li(l, 4)), d, true, M, d, d, ep_store(DT, d), s);
         attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, hd, s);
+        fork();
+        colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, aux_);
         mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d, beta), s);
-        colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, s);
         mm<T>(DQKV, 3 * d, false, W(li(l, 2)), d, true, M, d, 3 * d, ep_store(DT, d), s);
-        layernorm_bwd<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, Gp(li(l, 0)), Gp(li(l, 1)),
-                         scratch_, M, d, acc, s);
+        fork();
+        layernorm_bwd_params<T>(DT, X(l), stat(4 * l), stat(4 * l + 1), Gp(li(l, 0)), Gp(li(l, 1)), scratch_, M, d,
+                                acc, aux_);
+        layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s);
     }
     // wte rows: the head wgrad above stored/added every row; the embedding adds
     embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), sort_, acc, s);
+    join();  // the accumulator is complete when the compute stream passes this point
 }
 
 void GPTModel::micro_batch(const void* params, uint64_t seed, int mode, int start, int B, float* grad_acc,

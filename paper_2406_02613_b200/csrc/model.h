@@ -89,6 +89,10 @@ private:
     float* lse_ = nullptr;      // per-layer attention lse
     float* dsum_ = nullptr;
     float* scratch_ = nullptr;  // column-reduce partials
+    // side stream for the bias / LN-parameter column reductions: they only feed
+    // the gradient accumulator, so they run beside the GEMMs (fork/join events)
+    cudaStream_t aux_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     std::vector<char*> act_;    // activation slots (see model.cu)
     // host-data path
     int32_t* pinned_data_ = nullptr;

@@ -72,7 +72,7 @@ def test_nccl_collectives_world1(cuda, nccl_comm):
     assert _lib.lib().acco_comm_size(h) == 1 and _lib.lib().acco_comm_rank(h) == 0
 
 
-@pytest.mark.parametrize("method", ["acco", "zero1", "ddp"])
+@pytest.mark.parametrize("method", ["acco", "zero1", "ddp", "dpu", "wp"])
 def test_engine_nccl_mode_matches_oracle(cuda, nccl_comm, method):
     opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
                               scheduler="cosine")
@@ -85,7 +85,7 @@ def test_engine_nccl_mode_matches_oracle(cuda, nccl_comm, method):
     ocfg = O.OptimizerConfig(**{k: getattr(opt, k) for k in O.OptimizerConfig.__dataclass_fields__})
     osim = O.SimConfig(1, 4, 2, False, 7)
     fn = (lambda th, s: prob.stochastic_grad(th, s, 4))
-    ref = (O.run_acco if method == "acco" else O.run_ddp)(fn, th0, ocfg, osim, 4, eval_fn=prob.value_and_grad)
+    ref = O.run_method(method, fn, th0, ocfg, osim, 4, eval_fn=prob.value_and_grad)
     for t in range(4):
         a, b = tr.theta_history[t + 1], ref.theta_history[t + 1]
         assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
