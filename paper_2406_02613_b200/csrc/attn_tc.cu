@@ -367,9 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // warp interleaves the tiles, so the tensor core runs one tile's PV / next QK^T
 // while the other tile's softmax runs:
 //     S0(0) S1(0) | [P0] PV0(0) S0(1) | [P1] PV1(0) S1(1) | [P0] PV0(1) S0(2) ...
-// The row sums l = sum_k P are computed by the tensor core too (P x ones,
-// N = 16, next to O), so they are exactly the sums of the bf16 P that PV used
-// and the softmax threads only do max / exp / pack.
+// Row sums accumulate in fp32 with packed f32x2 adds (sm_100), so lse stays
+// consistent with the fp32 P the backward recomputes.
 __device__ __forceinline__ void st_row32_global_fwd(__nv_bfloat16* dst, const uint32_t* o, float scale) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -387,8 +386,7 @@ __device__ __forceinline__ void st_row32_global_fwd(__nv_bfloat16* dst, const ui
 }
 
 constexpr int F2_STAGES = 3;
-constexpr int F2_ONES = 2048;  // [16][128] bf16 ones: B operand of the row-sum MMA
-constexpr int F2_SMEM = 1024 + 2 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + F2_ONES + 256;
+constexpr int F2_SMEM = 1024 + 2 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + 256;
 
 __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -406,13 +404,68 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
         : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
+__device__ __forceinline__ float2 fma_f32x2(float2 a, float2 b, float2 c) {
+    uint64_t r;
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+        "mov.b64 ra, {%1, %2};\n\t"
+        "mov.b64 rb, {%3, %4};\n\t"
+        "mov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 %0, ra, rb, rc;\n\t}\n"
+        : "=l"(r)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
+    uint64_t r;
+    asm("{\n\t.reg .b64 ra, rb;\n\t"
+        "mov.b64 ra, {%1, %2};\n\t"
+        "mov.b64 rb, {%3, %4};\n\t"
+        "add.rn.f32x2 %0, ra, rb;\n\t}\n"
+        : "=l"(r)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    float2 o;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
+    return o;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+    return r;
+}
+// Max of 64 S values (columns base..base+63 of the tile); MASK: columns >= lim
+// are outside the causal window / sequence.
+template <bool MASK>
+__device__ __forceinline__ float row_max64(const uint32_t* sv, int base, int lim, float mx) {
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+        float x0 = __uint_as_float(sv[i]), x1 = __uint_as_float(sv[i + 1]);
+        if (MASK) {
+            x0 = base + i < lim ? x0 : -INFINITY;
+            x1 = base + i + 1 < lim ? x1 : -INFINITY;
+        }
+        mx = max3(mx, x0, x1);
+    }
+    return mx;
+}
+// P = 2^(s * sl - m) for 64 S values -> 32 packed bf16 pairs; row sum in l2.
+template <bool MASK>
+__device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m, int base, int lim, float2& l2,
+                                           uint32_t* pk) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const float2 xs = fma_f32x2(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])),
+                                    make_float2(sl, sl), make_float2(-m, -m));
+        float p0 = ex2(xs.x), p1 = ex2(xs.y);
+        if (MASK) {
+            p0 = base + 2 * i < lim ? p0 : 0.f;
+            p1 = base + 2 * i + 1 < lim ? p1 : 0.f;
+        }
+        l2 = add_f32x2(l2, make_float2(p0, p1));
+        __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
+        pk[i] = *reinterpret_cast<uint32_t*>(&hb);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -423,8 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sQ = smem;                         // [2 tiles]
     uint8_t* sK = sQ + 2 * Q_BYTES;             // [stage]
     uint8_t* sV = sK + F2_STAGES * KV_BYTES;    // [stage]
-    uint8_t* sOnes = sV + F2_STAGES * KV_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sOnes + F2_ONES);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + F2_STAGES * KV_BYTES);
     uint64_t* q_full = bars;
     uint64_t* kv_full = q_full + 1;              // [F2_STAGES]
     uint64_t* kv_empty = kv_full + F2_STAGES;    // [F2_STAGES]
@@ -456,11 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 3) {  // bf16 ones for the row-sum MMA (read through the async proxy)
-        for (int i = lane; i < F2_ONES / 16; i += 32)
-            reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
                      "r"(512));
@@ -470,8 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_after();
     const uint32_t tmem = *tslot;
-    // columns: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320), O tile 1 [320,384),
-    // row sums l (16 equal columns) tile 0 [384,400), tile 1 [400,416)
+    // columns: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320), O tile 1 [320,384)
 
     if (warp == 0) {
         if (lane == 0) {
@@ -490,8 +537,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
             constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
-            constexpr uint32_t id_l = idesc_bf16(BQ, 16, 0, 0);   // l += P 1: the row sums on the tensor core
-            const uint64_t ones = sdesc(smem_u32(sOnes), 16, 1024);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int x, int j) {
                 const int s = j % F2_STAGES;
@@ -515,7 +560,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < BKV / 16; ++kk) {
                     umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8, sdesc(v_base + kk * 2048, 64 * 128, 1024),
                             id_o, (j > 0 || kk > 0) ? 1u : 0u);
-                    umma_ts(tmem + 384 + x * 16, tmem + x * 128 + kk * 8, ones, id_l, (j > 0 || kk > 0) ? 1u : 0u);
                 }
             };
             issue_s(0, 0);
@@ -539,9 +583,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int q = (2 * pr + x) * BQ + r;
             const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
             const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
-            const uint32_t tL = tmem + 384 + x * 16 + lane_off;
             const float sl = scale * kLog2e;
             float m = -INFINITY;
+            float2 l2 = make_float2(0.f, 0.f);  // fp32 row sum (even / odd keys), packed adds
             for (int j = 0; j < n; ++j) {
                 mbar_wait(&s_full[x], j & 1);
                 tc_after();
@@ -557,12 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld32(tS + h2 * 64, sv);
                     tmem_ld32(tS + h2 * 64 + 32, sv + 32);
                     tmem_wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 64; ++i) {
-                        float xv = __uint_as_float(sv[i]);
-                        if (diag) xv = h2 * 64 + i < lim ? xv : -INFINITY;
-                        mx = fmaxf(mx, xv);
-                    }
+                    mx = diag ? row_max64<true>(sv, h2 * 64, lim, mx) : row_max64<false>(sv, h2 * 64, lim, mx);
                 }
                 mx *= sl;
                 // lazy rescale: move the reference max only when it grows by > 2^8;
@@ -573,6 +612,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const bool need = mx > m + kRescaleThresh;
                     const float alpha = need ? ex2(m - mx) : 1.f;
                     if (need) m = mx;
+                    l2.x *= alpha;
+                    l2.y *= alpha;
                     if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
                         uint32_t o[32];
 #pragma unroll
@@ -583,12 +624,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
                             tmem_st32(tO + c * 32, o);
                         }
-                        uint32_t lv[16];  // the row sums live next to O
-                        tmem_ld16(tL, lv);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) lv[i] = __float_as_uint(__uint_as_float(lv[i]) * alpha);
-                        tmem_st16(tL, lv);
                         tmem_wait_st();
                     }
                 }
@@ -601,17 +636,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tmem_ld32(tS + h2 * 64 + 32, sv + 32);
                     tmem_wait_ld();
                     uint32_t pk[32];
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        float p0 = ex2(fmaf(__uint_as_float(sv[2 * i]), sl, -m));
-                        float p1 = ex2(fmaf(__uint_as_float(sv[2 * i + 1]), sl, -m));
-                        if (diag) {
-                            p0 = h2 * 64 + 2 * i < lim ? p0 : 0.f;
-                            p1 = h2 * 64 + 2 * i + 1 < lim ? p1 : 0.f;
-                        }
-                        __nv_bfloat162 hb = __floats2bfloat162_rn(p0, p1);
-                        pk[i] = *reinterpret_cast<uint32_t*>(&hb);
-                    }
+                    if (diag)
+                        exp_pack64<true>(sv, sl, m, h2 * 64, lim, l2, pk);
+                    else
+                        exp_pack64<false>(sv, sl, m, h2 * 64, lim, l2, pk);
                     tmem_st16(tS + h2 * 32, pk);
                     tmem_st16(tS + h2 * 32 + 16, pk + 16);
                 }
@@ -621,10 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mbar_wait(&o_done[x], 0);
             tc_after();
-            uint32_t lv[16];
-            tmem_ld16(tL, lv);
-            tmem_wait_ld();
-            const float l = __uint_as_float(lv[0]);  // sum of the bf16 P the PV MMA used
+            const float l = l2.x + l2.y;  // fp32 sum: lse stays consistent with the fp32 P of the backward
             const float inv = 1.f / l;
             __nv_bfloat16* yr = y + (static_cast<int64_t>(b) * T + q) * d + h * HD;
 #pragma unroll
@@ -642,6 +667,57 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         tc_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ---- backward softmax helpers (masking hoisted out of the unrolled loops)
+// p[c] = 2^(s_c * sl - lse2[c]) for 32 columns; MASK: columns outside
+// [lo, hi) -> 0 (dK/dV: thread = key, columns = queries)
+template <bool MASK>
+__device__ __forceinline__ void exp_cols32(const uint32_t* st, const float4* L4, float sl, int base, int lo, int hi,
+                                           float* p) {
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 l4 = L4[c4];
+        const float2 a = fma_f32x2(make_float2(__uint_as_float(st[4 * c4]), __uint_as_float(st[4 * c4 + 1])),
+                                   make_float2(sl, sl), make_float2(-l4.x, -l4.y));
+        const float2 b = fma_f32x2(make_float2(__uint_as_float(st[4 * c4 + 2]), __uint_as_float(st[4 * c4 + 3])),
+                                   make_float2(sl, sl), make_float2(-l4.z, -l4.w));
+        float v[4] = {ex2(a.x), ex2(a.y), ex2(b.x), ex2(b.y)};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = base + 4 * c4 + e;
+            if (MASK) v[e] = (c >= lo && c < hi) ? v[e] : 0.f;
+            p[4 * c4 + e] = v[e];
+        }
+    }
+}
+// p[c] = 2^(s_c * sl - L) for 64 columns (dQ: thread = query, columns = keys);
+// MASK: columns >= lim -> 0
+template <bool MASK>
+__device__ __forceinline__ void exp_row64(const uint32_t* st, float sl, float L, int lim, float* p) {
+#pragma unroll
+    for (int c = 0; c < 64; c += 2) {
+        const float2 a = fma_f32x2(make_float2(__uint_as_float(st[c]), __uint_as_float(st[c + 1])),
+                                   make_float2(sl, sl), make_float2(-L, -L));
+        float p0 = ex2(a.x), p1 = ex2(a.y);
+        if (MASK) {
+            p0 = c < lim ? p0 : 0.f;
+            p1 = c + 1 < lim ? p1 : 0.f;
+        }
+        p[c] = p0;
+        p[c + 1] = p1;
+    }
+}
+// ds[c] = p[c] * (dp[c] - D[c]) with packed f32x2 math
+__device__ __forceinline__ void ds_pairs(const float* p, const uint32_t* dp, const float* D, int n, float* ds) {
+#pragma unroll
+    for (int c = 0; c < n; c += 2) {
+        const float2 t = fma_f32x2(make_float2(__uint_as_float(dp[c]), __uint_as_float(dp[c + 1])), make_float2(1.f, 1.f),
+                                   make_float2(-D[c], -D[c + 1]));
+        const float2 r = fma_f32x2(make_float2(p[c], p[c + 1]), t, make_float2(0.f, 0.f));
+        ds[c] = r.x;
+        ds[c + 1] = r.y;
     }
 }
 
@@ -860,26 +936,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + hf * 64);
             {
                 float p[64];
+                // valid query columns c of this half: q0 + hf*64 + c in [key, T)
+                const int lo = key - (q0 + hf * 64), hi = T - (q0 + hf * 64);
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {  // S^T streamed 32 columns at a time
                     uint32_t st[32];
                     tmem_ld32(tS + lane_off + hf * 64 + hh * 32, st);
                     tmem_wait_ld();
-#pragma unroll
-                    for (int c4 = 0; c4 < 8; ++c4) {
-                        const float4 l4 = L4[hh * 8 + c4];
-                        const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int c = hh * 32 + c4 * 4 + e;
-                            float x = ex2(fmaf(__uint_as_float(st[c4 * 4 + e]), sl, -lv[e]));
-                            if (edge) {
-                                const int q = q0 + hf * 64 + c;
-                                x = (q >= key && q < T) ? x : 0.f;
-                            }
-                            p[c] = x;
-                        }
-                    }
+                    if (edge)
+                        exp_cols32<true>(st, L4 + hh * 8, sl, hh * 32, lo, hi, p + hh * 32);
+                    else
+                        exp_cols32<false>(st, L4 + hh * 8, sl, hh * 32, lo, hi, p + hh * 32);
                 }
                 if (i > 0) {  // the previous dV/dK MMAs have read the smem operands
                     mbar_wait(g_done, (i - 1) & 1);
@@ -896,14 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_arrive(s_free);  // S^T / dP^T TMEM may be overwritten
                     }
                     float ds[32];
-#pragma unroll
-                    for (int c4 = 0; c4 < 8; ++c4) {
-                        const float4 d4 = D4[hh * 8 + c4];
-                        ds[4 * c4 + 0] = p[hh * 32 + 4 * c4 + 0] * (__uint_as_float(st[4 * c4 + 0]) - d4.x);
-                        ds[4 * c4 + 1] = p[hh * 32 + 4 * c4 + 1] * (__uint_as_float(st[4 * c4 + 1]) - d4.y);
-                        ds[4 * c4 + 2] = p[hh * 32 + 4 * c4 + 2] * (__uint_as_float(st[4 * c4 + 2]) - d4.z);
-                        ds[4 * c4 + 3] = p[hh * 32 + 4 * c4 + 3] * (__uint_as_float(st[4 * c4 + 3]) - d4.w);
-                    }
+                    ds_pairs(p + hh * 32, st, reinterpret_cast<const float*>(D4 + hh * 8), 32, ds);
                     st_row32_part(sDS, hf, r, hh, ds);
                 }
             }
@@ -1057,22 +1117,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld32(tS + lane_off + hf * 64, st);
                 tmem_ld32(tS + lane_off + hf * 64 + 32, st + 32);
                 tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 64; ++c) {
-                    float x = ex2(fmaf(__uint_as_float(st[c]), sl, -L));
-                    if (diag) {
-                        const int key = j * BW_T + hf * 64 + c;
-                        x = (key <= q && key < T) ? x : 0.f;
-                    }
-                    p[c] = x;
-                }
+                // valid key columns c: j*128 + hf*64 + c <= q and < T
+                const int lim = min(q + 1, T) - (j * BW_T + hf * 64);
+                if (diag)
+                    exp_row64<true>(st, sl, L, lim, p);
+                else
+                    exp_row64<false>(st, sl, L, lim, p);
                 tmem_ld32(tP + lane_off + hf * 64, st);
                 tmem_ld32(tP + lane_off + hf * 64 + 32, st + 32);
                 tmem_wait_ld();
                 tc_before();
                 mbar_arrive(s_free);
+                {
+                    float dv[64];
 #pragma unroll
-                for (int c = 0; c < 64; ++c) p[c] = p[c] * (__uint_as_float(st[c]) - Dq);
+                    for (int c = 0; c < 64; ++c) dv[c] = Dq;
+                    ds_pairs(p, st, dv, 64, p);
+                }
                 if (j > 0) {  // the previous dQ MMA has read dS
                     mbar_wait(g_done, (j - 1) & 1);
                     tc_after();
