@@ -161,6 +161,8 @@ def main():
     ap.add_argument("--model", default="gpt2-small", choices=list(MODELS))
     ap.add_argument("--batch", type=int, default=8, help="sequences per micro-batch per GPU")
     ap.add_argument("--schedule", default="adaptive", choices=["adaptive", "floor"])
+    ap.add_argument("--fabric", default="nccl", choices=["nccl", "peer"],
+                    help="comm phase: NCCL RS/AG around the fused optimizer, or the fused peer-memory fold kernel")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--profile", action="store_true", help="ncu-friendly: short run, no baselines")
@@ -181,7 +183,15 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2406_02613_b200 import api
 
-    comm = api.Comm(rank, world, local) if world > 1 else None
+    nccl = api.Comm(rank, world, local) if world > 1 else None
+
+    def make_comm(method):
+        # the peer fabric registers one trainer's buffers, so each trainer gets its own
+        if args.fabric == "peer" and method != "ddp":
+            return api.PeerComm(rank, world, local)
+        return nccl
+
+    comm = nccl
     B, T = args.batch, cfgd["seq_len"]
     n_samples = 4096
     lm = api.LMConfig(**cfgd, n_samples=n_samples, data_seed=1, precision="bf16", max_batch=B)
@@ -206,7 +216,7 @@ def main():
     def timed(method, k, schedule, profile=False, clocks=False):
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=k, master_seed=1,
                             schedule=schedule, eval_every=0)
-        tr = api.Trainer(method, model, opt, sim, comm)
+        tr = api.Trainer(method, model, opt, sim, make_comm(method))
         tr.set_theta(model.default_theta0(1))
         tr.run(args.warmup)
         barrier()
@@ -252,7 +262,7 @@ def main():
         model_h = api.Model(lm_h)
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=1, master_seed=1,
                             schedule=args.schedule, eval_every=0)
-        tr = api.Trainer("acco", model_h, opt, sim, comm)
+        tr = api.Trainer("acco", model_h, opt, sim, make_comm("acco"))
         tr.set_theta(model_h.default_theta0(1))
         tr.run(args.warmup)
         barrier()
@@ -317,7 +327,9 @@ def main():
         "config": {"workload": f"{args.model} ACCO ({args.schedule} schedule, k=1), B={B}x{T} tokens per "
                                f"micro-batch per GPU, 2 micro-batches + 2 comm phases per update",
                    "model": args.model, "global_batch": int(acco["tokens"] / args.steps), "seq_len": T,
-                   "parallelism": f"dp{world} ACCO (ZeRO-1-sharded fp32 AdamW states, NCCL RS/AG)",
+                   "parallelism": f"dp{world} ACCO (ZeRO-1-sharded fp32 AdamW states, " +
+                                  ("NCCL RS/AG)" if args.fabric == "nccl" else
+                                   "fused peer-memory fold+AdamW+replica-store kernel over NVLink)"),
                    "l2": "inputs larger than L2 (bf16 params 249 MB + activations per step)"},
         "exposed_comm_pct": 100.0 * st["comm_exposed_ms"] / st["comm_busy_ms"] if st["comm_busy_ms"] else 0.0,
         "comm_busy_ms_per_step": st["comm_busy_ms"] / args.steps,

@@ -268,6 +268,25 @@ int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t*
                      float* theta_history, acco_run_stats* stats);
 int acco_trainer_n_local(const acco_trainer* t);
 
+/* ------------------------------------------------------------- peer fabric
+ * B200-native alternative to NCCL for the comm phase: ONE fused kernel per
+ * phase reads every rank's accumulator shard over NVLink peer memory (CUDA
+ * IPC), folds them in ascending rank order (the reference Fabric's reduce
+ * order, collectives.cpp:55-75), applies the optimizer step and stores the
+ * new parameters into every rank's replica (all-gather fused in); the counts
+ * all-reduce and the phase barriers are device flags. One process per GPU of
+ * one box. Setup: create the fabric, create the trainer on it, export this
+ * rank's blob, all-gather the blobs out of band (any host transport), connect. */
+typedef struct acco_peer acco_peer;
+int acco_peer_create(int nranks, int rank, int device, acco_peer** out);
+int acco_peer_destroy(acco_peer* p);
+int acco_trainer_create_peer(acco_model* model, const acco_opt_cfg* opt, const acco_sim_cfg* sim, int method,
+                             acco_peer* peer, acco_trainer** out);
+long long acco_trainer_peer_blob_bytes(const acco_trainer* t);
+int acco_trainer_peer_export(const acco_trainer* t, void* blob);
+/* blobs: [nranks][blob_bytes], rank order */
+int acco_trainer_peer_connect(acco_trainer* t, const void* blobs);
+
 /* timeline.csv rows of the last acco_trainer_run (Timeline/Interval,
  * proj/include/accosim/simclock.hpp; written by csvio.cpp:48-66), measured
  * with CUDA events on the compute / comm streams, seconds since the run start.

@@ -58,15 +58,20 @@ def cmd_run(config_path: str, out_dir: str) -> int:
     cfg = _load(config_path)
     rank, world, local = _dist()
     comm = None
-    if world > 1:
-        if cfg.sim.n_workers != world:
-            raise api.InvalidArgument(2, f"run: n_workers ({cfg.sim.n_workers}) must equal the world size ({world})")
+    fabric = cfg.raw.get("fabric", "nccl")  # B200 key: "nccl" or "peer" (fused NVLink fold kernel)
+    if fabric not in ("nccl", "peer"):
+        raise api.InvalidArgument(2, f"config: unknown fabric {fabric}")
+    if world > 1 and cfg.sim.n_workers != world:
+        raise api.InvalidArgument(2, f"run: n_workers ({cfg.sim.n_workers}) must equal the world size ({world})")
+    if fabric == "peer" and (world > 1 or cfg.sim.n_workers == 1):
+        comm = api.PeerComm(rank, world, local)
+    elif world > 1:
         comm = api.Comm(rank, world, local)
     if not out_dir:
         out_dir = cfg.output_dir or os.path.join(_default_out_root(), "run_" + api.config_hash(cfg.raw))
     tr = api.run_protocol(cfg.method, cfg.problem, cfg.optimizer, cfg.sim, cfg.t_updates, comm=comm,
                           record_history=False)
-    if comm is not None:  # merge the ranks' timelines (each rank owns its worker's rows)
+    if world > 1:  # merge the ranks' timelines (each rank owns its worker's rows)
         import torch.distributed as dist
 
         parts = [None] * world

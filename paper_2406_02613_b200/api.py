@@ -68,6 +68,11 @@ IV_KINDS = ("init_grad", "microbatch", "all_reduce", "reduce_scatter", "optimize
 _P = C.c_void_p
 _lib.register({
     "acco_trainer_timeline": (C.c_int, [_P, C.POINTER(IntervalC), C.c_int, C.POINTER(C.c_int)]),
+    "acco_peer_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "acco_peer_destroy": (C.c_int, [_P]),
+    "acco_trainer_peer_blob_bytes": (C.c_longlong, [_P]),
+    "acco_trainer_peer_export": (C.c_int, [_P, _P]),
+    "acco_trainer_peer_connect": (C.c_int, [_P, _P]),
     "acco_model_create": (C.c_int, [C.POINTER(LMCfgC), C.POINTER(C.c_void_p)]),
     "acco_model_destroy": (C.c_int, [_P]),
     "acco_model_num_params": (C.c_longlong, [_P]),
@@ -77,6 +82,8 @@ _lib.register({
     "acco_model_value_and_grad": (C.c_int, [_P, _P, C.POINTER(C.c_double), _P, _P]),
     "acco_trainer_create": (C.c_int, [_P, C.POINTER(_lib.OptCfg), C.POINTER(SimCfgC), C.c_int, _P,
                                       C.POINTER(C.c_void_p)]),
+    "acco_trainer_create_peer": (C.c_int, [_P, C.POINTER(_lib.OptCfg), C.POINTER(SimCfgC), C.c_int, _P,
+                                           C.POINTER(C.c_void_p)]),
     "acco_trainer_destroy": (C.c_int, [_P]),
     "acco_trainer_set_theta": (C.c_int, [_P, _P]),
     "acco_trainer_get_theta": (C.c_int, [_P, C.c_int, _P]),
@@ -243,6 +250,45 @@ class Comm:
         return self._h
 
 
+class PeerComm:
+    """Peer fabric for one rank (one process per GPU of one box): the comm
+    phase as one fused kernel over NVLink peer memory (include/acco.h,
+    csrc/peer.h) instead of NCCL. The IPC handles of every rank's buffers are
+    all-gathered over an existing torch.distributed group when a Trainer is
+    created on it."""
+
+    kind = "peer"
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        self._h = C.c_void_p()
+        _lib.call("acco_peer_create", world, rank, device, C.byref(self._h))
+        self.rank, self.world, self.group = rank, world, group
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.lib().acco_peer_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def connect(self, trainer_handle) -> None:
+        n = _lib.lib().acco_trainer_peer_blob_bytes(trainer_handle)
+        blob = (C.c_ubyte * n)()
+        _lib.call("acco_trainer_peer_export", trainer_handle, blob)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            parts = [None] * self.world
+            dist.all_gather_object(parts, bytes(blob), group=self.group)
+        else:
+            parts = [bytes(blob)]
+        allb = (C.c_ubyte * (n * self.world)).from_buffer_copy(b"".join(parts))
+        _lib.call("acco_trainer_peer_connect", trainer_handle, allb)
+
+
 # --------------------------------------------------------------------- trainer
 @dataclass
 class SimConfig:
@@ -321,8 +367,13 @@ class Trainer:
                     SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr)
         o = opt.to_c()
         self._h = C.c_void_p()
-        _lib.call("acco_trainer_create", model.handle, C.byref(o), C.byref(s), METHODS[method],
-                  comm.handle if comm is not None else None, C.byref(self._h))
+        if isinstance(comm, PeerComm):
+            _lib.call("acco_trainer_create_peer", model.handle, C.byref(o), C.byref(s), METHODS[method],
+                      comm.handle, C.byref(self._h))
+            comm.connect(self._h)
+        else:
+            _lib.call("acco_trainer_create", model.handle, C.byref(o), C.byref(s), METHODS[method],
+                      comm.handle if comm is not None else None, C.byref(self._h))
         self.n_local = _lib.lib().acco_trainer_n_local(self._h)
 
     def __del__(self):
@@ -421,6 +472,8 @@ def _fill_idle(trace: RunTrace, sim: SimConfig, comm) -> None:
 
     if comm is None:
         rows = idle_fractions(trace.records, trace.timeline, range(sim.n_workers))
+    elif comm.world == 1:
+        rows = idle_fractions(trace.records, trace.timeline, [comm.rank])
     else:
         import torch.distributed as dist
 

@@ -18,6 +18,10 @@ struct acco_trainer {
     std::unique_ptr<Trainer> impl;
 };
 
+struct acco_peer {
+    std::unique_ptr<PeerFabric> impl;
+};
+
 namespace {
 LMConfig to_lm(const acco_lm_cfg& c) {
     LMConfig l;
@@ -32,6 +36,22 @@ LMConfig to_lm(const acco_lm_cfg& c) {
     l.max_batch = c.max_batch;
     l.host_data = c.host_data;
     return l;
+}
+SimCfg to_sim(const acco_sim_cfg* sim) {
+    SimCfg s;
+    s.n_workers = sim->n_workers;
+    s.batch_size = sim->batch_size;
+    s.n_grad_accumulation = sim->n_grad_accumulation;
+    s.warmup_rounds = sim->warmup_rounds;
+    s.master_seed = sim->master_seed;
+    s.schedule = sim->schedule;
+    ACCO_REQUIRE(s.schedule >= kFloor && s.schedule <= kReplay, "sim: unknown schedule");
+    if (sim->replay && sim->replay_len > 0) s.replay.assign(sim->replay, sim->replay + sim->replay_len);
+    ACCO_REQUIRE(s.schedule != kReplay || !s.replay.empty(), "sim: replay schedule requires counts");
+    s.eval_every = sim->eval_every;
+    s.eval_batch = sim->eval_batch;
+    if (sim->throttle_ns) s.throttle_ns.assign(sim->throttle_ns, sim->throttle_ns + sim->n_workers);
+    return s;
 }
 }  // namespace
 
@@ -94,24 +114,51 @@ int acco_model_value_and_grad(acco_model* m, const void* params, double* loss_ou
     });
 }
 
+
 int acco_trainer_create(acco_model* model, const acco_opt_cfg* opt, const acco_sim_cfg* sim, int method,
                         acco_comm* comm, acco_trainer** out) {
     return guarded([&] {
         ACCO_REQUIRE(model && opt && sim && out, "acco_trainer_create: null argument");
-        SimCfg s;
-        s.n_workers = sim->n_workers;
-        s.batch_size = sim->batch_size;
-        s.n_grad_accumulation = sim->n_grad_accumulation;
-        s.warmup_rounds = sim->warmup_rounds;
-        s.master_seed = sim->master_seed;
-        s.schedule = sim->schedule;
-        ACCO_REQUIRE(s.schedule >= kFloor && s.schedule <= kReplay, "sim: unknown schedule");
-        if (sim->replay && sim->replay_len > 0) s.replay.assign(sim->replay, sim->replay + sim->replay_len);
-        ACCO_REQUIRE(s.schedule != kReplay || !s.replay.empty(), "sim: replay schedule requires counts");
-        s.eval_every = sim->eval_every;
-        s.eval_batch = sim->eval_batch;
-        if (sim->throttle_ns) s.throttle_ns.assign(sim->throttle_ns, sim->throttle_ns + sim->n_workers);
-        *out = new acco_trainer{std::make_unique<Trainer>(model->impl.get(), from_c(*opt), s, method, comm_impl(comm))};
+        *out = new acco_trainer{
+            std::make_unique<Trainer>(model->impl.get(), from_c(*opt), to_sim(sim), method, comm_impl(comm))};
+    });
+}
+
+int acco_peer_create(int nranks, int rank, int device, acco_peer** out) {
+    return guarded([&] {
+        ACCO_REQUIRE(out, "acco_peer_create: null argument");
+        *out = new acco_peer{std::make_unique<PeerFabric>(nranks, rank, device)};
+    });
+}
+
+int acco_peer_destroy(acco_peer* p) {
+    return guarded([&] { delete p; });
+}
+
+int acco_trainer_create_peer(acco_model* model, const acco_opt_cfg* opt, const acco_sim_cfg* sim, int method,
+                             acco_peer* peer, acco_trainer** out) {
+    return guarded([&] {
+        ACCO_REQUIRE(model && opt && sim && peer && out, "acco_trainer_create_peer: null argument");
+        *out = new acco_trainer{std::make_unique<Trainer>(model->impl.get(), from_c(*opt), to_sim(sim), method,
+                                                          nullptr, peer->impl.get())};
+    });
+}
+
+long long acco_trainer_peer_blob_bytes(const acco_trainer* t) {
+    return t && t->impl->peer() ? static_cast<long long>(t->impl->peer()->blob_bytes()) : -1;
+}
+
+int acco_trainer_peer_export(const acco_trainer* t, void* blob) {
+    return guarded([&] {
+        ACCO_REQUIRE(t && t->impl->peer() && blob, "acco_trainer_peer_export: not a peer-fabric trainer");
+        t->impl->peer()->export_blob(blob);
+    });
+}
+
+int acco_trainer_peer_connect(acco_trainer* t, const void* blobs) {
+    return guarded([&] {
+        ACCO_REQUIRE(t && t->impl->peer() && blobs, "acco_trainer_peer_connect: not a peer-fabric trainer");
+        t->impl->peer()->connect(blobs);
     });
 }
 

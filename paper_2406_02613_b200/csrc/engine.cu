@@ -54,8 +54,9 @@ struct Trainer::PhaseEvents {
     int n_local = 1;
 };
 
-Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm)
-    : model_(model), cfg_(cfg), sim_(sim), method_(method), comm_(comm) {
+Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm,
+                 PeerFabric* peer)
+    : model_(model), cfg_(cfg), sim_(sim), method_(method), comm_(comm), peer_(peer) {
     validate(cfg_);
     ACCO_REQUIRE(method == kACCO || method == kDDP || method == kZeRO1 || method == kDPU || method == kWP,
                  "method: unknown protocol");
@@ -66,7 +67,14 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
     ACCO_REQUIRE(sim.batch_size <= model->cfg().max_batch, "batch_size exceeds the model's max_batch workspace");
     ACCO_REQUIRE(sim.throttle_ns.empty() || static_cast<int>(sim.throttle_ns.size()) == sim.n_workers,
                  "run_protocol: one multiplier per worker");
-    if (comm_) {
+    ACCO_REQUIRE(!(comm_ && peer_), "trainer: NCCL communicator or peer fabric, not both");
+    if (peer_) {
+        world_ = peer_->size();
+        rank_ = peer_->rank();
+        n_local_ = 1;
+        ACCO_REQUIRE(world_ == sim.n_workers, "peer fabric size must equal n_workers");
+        ACCO_REQUIRE(method != kDDP, "peer fabric: sharded methods only (acco, zero1, dpu, wp)");
+    } else if (comm_) {
         world_ = comm_->size();
         rank_ = comm_->rank();
         n_local_ = 1;
@@ -81,10 +89,10 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
     }
     psi_ = model->num_params();
     layout_ = shard_partition(static_cast<uint64_t>(psi_), sim.n_workers);
-    const bool sharded = comm_ && method_ != kDDP;
+    const bool sharded = (comm_ || peer_) && method_ != kDDP;
     if (sharded) {
         chunk_ = static_cast<int64_t>(layout_.chunk());
-        padded_ = psi_ % world_ != 0;
+        padded_ = comm_ && psi_ % world_ != 0;  // NCCL's equal counts; the peer fold addresses [lo, hi) directly
         own_lo_ = static_cast<int64_t>(layout_.lo(rank_));
         own_n_ = static_cast<int64_t>(layout_.size(rank_));
     } else {
@@ -98,6 +106,14 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
     ACCO_CUDA(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, lo_prio));
     ACCO_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, hi_prio));
     alloc();
+    if (peer_) {  // exported to the peers: accumulators, then the two replicas
+        rep_[0] = theta_act_;
+        rep_[1] = est_act_;
+        std::vector<void*> bufs(acc_.begin(), acc_.end());
+        bufs.push_back(rep_[0]);
+        bufs.push_back(rep_[1]);
+        peer_->register_buffers(bufs);
+    }
 }
 
 Trainer::~Trainer() {
@@ -127,7 +143,7 @@ void Trainer::alloc() {
         ag_theta_ = theta_act_;
         ag_est_ = est_act_;
     }
-    const size_t own_cap = static_cast<size_t>(comm_ && method_ != kDDP ? chunk_ : psi_);
+    const size_t own_cap = static_cast<size_t>((comm_ || peer_) && method_ != kDDP ? chunk_ : psi_);
     ACCO_CUDA(cudaMalloc(&master_, own_cap * 4));
     if (cfg_.kind != 0) {
         ACCO_CUDA(cudaMalloc(&m_, own_cap * 4));
@@ -143,10 +159,8 @@ void Trainer::alloc() {
         ACCO_CUDA(cudaMemset(a, 0, P * 4));
         acc_.push_back(a);
     }
-    if (comm_ || n_local_ > 1) {
-        ACCO_CUDA(cudaMalloc(&g_ret_, own_cap * 4));
-        ACCO_CUDA(cudaMalloc(&g_main_, own_cap * 4));
-    }
+    if (comm_ || peer_ || n_local_ > 1) ACCO_CUDA(cudaMalloc(&g_ret_, own_cap * 4));  // retained estimate shard
+    if (comm_) ACCO_CUDA(cudaMalloc(&g_main_, own_cap * 4));                  // reduce-scatter target
     ACCO_CUDA(cudaMalloc(&cnt_send_, 8));
     ACCO_CUDA(cudaMalloc(&flag_, sizeof(int)));
     ACCO_CUDA(cudaMemset(flag_, 0, sizeof(int)));
@@ -241,16 +255,27 @@ void Trainer::eval(const void* params, double* loss_slots, double* gsq_slot) {
     norm_sq(eval_grad_, psi_, gsq_slot, eval_scratch_, cs_);
 }
 
-// Fabric::reduce_scatter (collectives.cpp:55-75) of the accumulators with
-// parity acc_q: into this rank's shard `dst` (NCCL), the fixed-order sum of
-// the virtual workers, or the accumulator itself for one worker. DDP over NCCL
-// all-reduces in place (SyncEngine's reduce_mean, protocols.cpp:191-206).
-float* Trainer::reduce_grads(int acc_q, float* dst) {
+// Gradient sources of one comm phase (accumulators with parity acc_q).
+// NCCL: Fabric::reduce_scatter (collectives.cpp:55-75) into this rank's shard
+// `dst` (DDP all-reduces in place, SyncEngine's reduce_mean,
+// protocols.cpp:191-206) and the fold has that one source. Virtual workers:
+// the fold reads every local accumulator itself, in ascending worker order
+// (the reference's reduce order) — no separate reduction pass.
+FoldIO Trainer::fold_sources(int acc_q, float* dst) {
     const int nacc = static_cast<int>(acc_.size()) / n_local_;
     auto acc_of = [&](int w) { return acc_[static_cast<size_t>(w) * nacc + acc_q % nacc]; };
+    FoldIO io;
+    if (peer_) {  // every rank's accumulator, this rank's shard, ascending rank order, over NVLink
+        for (int r = 0; r < world_; ++r)
+            io.src[r] = static_cast<const float*>(peer_->peer_buffer(r, acc_q % nacc)) + own_lo_;
+        io.nsrc = world_;
+        return io;
+    }
     if (comm_ && method_ == kDDP) {
         comm_->all_reduce_f32(acc_of(0), acc_of(0), static_cast<size_t>(psi_), ms_);
-        return acc_of(0);
+        io.src[0] = acc_of(0);
+        io.nsrc = 1;
+        return io;
     }
     if (comm_) {
         const float* send = acc_of(0);
@@ -264,25 +289,38 @@ float* Trainer::reduce_grads(int acc_q, float* dst) {
             send = pad_send_;
         }
         comm_->reduce_scatter_f32(send, dst, static_cast<size_t>(chunk_), ms_);
-        return dst;
+        io.src[0] = dst;
+        io.nsrc = 1;
+        return io;
     }
-    if (n_local_ == 1) return acc_of(0);
-    std::vector<const float*> in;
-    for (int w = 0; w < n_local_; ++w) in.push_back(acc_of(w));
-    sum_ordered(in.data(), n_local_, dst, psi_, ms_);
-    return dst;
+    for (int w = 0; w < n_local_; ++w) io.src[w] = acc_of(w);
+    io.nsrc = n_local_;
+    return io;
 }
 
 // Fused sharded optimizer step on this rank's shard (K6 transient estimate when
-// !commit, K7 commit otherwise; optim.cpp:50-119), then Fabric::all_gather
-// (collectives.cpp:77-91) of the activation-dtype parameters into act_dst.
-void Trainer::opt_gather(bool commit, const float* g, const float* ret, const int64_t* tot, const int64_t* ret_tot,
+// !commit, K7 commit otherwise; optim.cpp:50-119) over the folded sources,
+// then Fabric::all_gather (collectives.cpp:77-91) of the activation-dtype
+// parameters into act_dst (NCCL) — or written straight into act_dst.
+void Trainer::opt_gather(bool commit, FoldIO io, const float* ret, const int64_t* tot, const int64_t* ret_tot,
                          void* act_dst, void* ag_dst, cudaEvent_t after_opt) {
-    const bool sharded = comm_ && method_ != kDDP;
     const int act = model_->act_dtype();
     const size_t e = model_->act_bytes();
+    if (peer_) {  // the new shard goes straight into every rank's replica (all-gather fused in)
+        const int ri = act_dst == rep_[0] ? 0 : 1;
+        for (int r = 0; r < world_; ++r)
+            io.dst[r] = static_cast<char*>(peer_->peer_buffer(r, static_cast<int>(acc_.size()) + ri)) +
+                        static_cast<size_t>(own_lo_) * e;
+        io.ndst = world_;
+        opt_fold(cfg_, step_, commit, io, ret, tot, ret_tot, master_, m_, v_, own_n_, act, flag_, ms_);
+        if (after_opt) ACCO_CUDA(cudaEventRecord(after_opt, ms_));
+        return;
+    }
+    const bool sharded = comm_ && method_ != kDDP;
     void* out = sharded ? static_cast<char*>(ag_dst) + static_cast<size_t>(rank_) * chunk_ * e : act_dst;
-    opt_apply(cfg_, step_, commit, g, ret, tot, ret_tot, master_, m_, v_, own_n_, out, act, flag_, ms_);
+    io.dst[0] = out;
+    io.ndst = 1;
+    opt_fold(cfg_, step_, commit, io, ret, tot, ret_tot, master_, m_, v_, own_n_, act, flag_, ms_);
     if (after_opt) ACCO_CUDA(cudaEventRecord(after_opt, ms_));
     if (!sharded) return;
     comm_->all_gather(out, ag_dst, static_cast<size_t>(chunk_), act, ms_);
@@ -307,7 +345,11 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
     for (int w = 0; w < n_local_; ++w) local += ev.counts[static_cast<size_t>(p) * n_local_ + w];
     int64_t* totp = tot + p;
     // 1. Fabric::all_reduce_counts (collectives.cpp:48-53)
-    if (comm_) {
+    const unsigned long long seq = ++phase_seq_;
+    if (peer_) {  // post + wait for every rank's post; counts folded in rank order
+        peer_->signal_post(seq, static_cast<int>(seq & 1), local, ms_);
+        peer_->wait_posts(seq, static_cast<int>(seq & 1), totp, ms_);
+    } else if (comm_) {
         fill_i64(cnt_send_, local, ms_);
         comm_->all_reduce_i64(cnt_send_, totp, 1, ms_);
     } else {
@@ -316,38 +358,42 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
     ACCO_CUDA(cudaEventRecord(ev.cnt_done[p], ms_));
     if (method_ == kACCO) {
         const bool est = p % 2 == 0;
-        float* g = reduce_grads(acc_q, est ? g_ret_ : g_main_);
+        FoldIO io = fold_sources(acc_q, est ? g_ret_ : g_main_);
         ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
         if (est) {  // estimate on a transient copy of the shard state (protocols.cpp:652-658)
-            opt_gather(false, g, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
+            if (!comm_ && n_local_ > 1) io.ret_out = g_ret_;  // retain the folded shard for the commit
+            opt_gather(false, io, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
         } else {    // commit with the retained estimate shard (protocols.cpp:661-670)
             const int nacc = static_cast<int>(acc_.size()) / n_local_;
             const float* ret = (comm_ || n_local_ > 1) ? g_ret_ : acc_[static_cast<size_t>((acc_q + nacc - 1) % nacc)];
-            opt_gather(true, g, ret, totp, totp - 1, theta_act_, ag_theta_, ev.opt_done[p]);
+            opt_gather(true, io, ret, totp, totp - 1, theta_act_, ag_theta_, ev.opt_done[p]);
             ++step_;
         }
     } else {
-        float* g = reduce_grads(acc_q, g_main_);
+        const FoldIO io = fold_sources(acc_q, g_main_);
         ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
         if (method_ == kDPU && !warm) {
             // theta^(r+1) goes to the other replica: stage r still reads theta^(r),
             // which becomes the record's estimate (protocols.cpp:361-378)
-            opt_gather(true, g, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
+            opt_gather(true, io, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
             ++step_;
             std::swap(theta_act_, est_act_);
             std::swap(ag_theta_, ag_est_);
         } else {
-            opt_gather(true, g, nullptr, totp, nullptr, theta_act_, ag_theta_, ev.opt_done[p]);
+            opt_gather(true, io, nullptr, totp, nullptr, theta_act_, ag_theta_, ev.opt_done[p]);
             ++step_;
             // WP: prediction step from the updated state on a throwaway copy (protocols.cpp:398-403)
-            if (method_ == kWP) opt_gather(false, g, nullptr, totp, nullptr, est_act_, ag_est_, nullptr);
+            if (method_ == kWP) opt_gather(false, io, nullptr, totp, nullptr, est_act_, ag_est_, nullptr);
         }
     }
+    if (peer_) peer_->signal_done(seq, ms_);  // this rank's shard is in every replica
     ACCO_CUDA(cudaEventRecord(ev.done[p], ms_));
 }
 
 void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* theta_hist) {
     ACCO_REQUIRE(T >= 1, "run_protocol: t_updates >= 1");
+    ACCO_REQUIRE(!peer_ || peer_->connected(), "peer fabric: connect the ranks before run()");
+    if (peer_ && phase_seq_ > 0) peer_->wait_done(phase_seq_, cs_);  // peers finished writing our replicas
     if (cfg_.total_steps == 0) cfg_.total_steps = T;  // run_protocol, protocols.cpp:729
     recs.clear();
     st = RunStats{};
@@ -358,6 +404,10 @@ void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* t
             run_acco(T, recs, st);
         else
             run_sync(T, recs, st);
+        if (peer_) {  // the replicas are final only when every rank's last phase is done
+            peer_->wait_done(phase_seq_, cs_);
+            ACCO_CUDA(cudaStreamSynchronize(cs_));
+        }
         st.h2d_bytes = model_->h2d_bytes() - h2d0;
         st.d2h_bytes = d2h_bytes_ - d2h0;
         if (theta_hist) fetch_history(T, theta_hist);
@@ -373,6 +423,7 @@ void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* t
 // after the commit of update t (comm stream): copy theta^(t+1), theta-tilde^(t+1)
 void Trainer::snapshot(int t, bool est_is_theta) {
     if (!hist_dev_) return;
+    if (peer_) peer_->wait_done(phase_seq_, ms_);  // every rank's shard of this phase has landed
     const size_t bytes = static_cast<size_t>(psi_) * model_->act_bytes();
     char* dst = hist_dev_ + static_cast<size_t>(t) * 2 * bytes;
     ACCO_CUDA(cudaMemcpyAsync(dst, theta_act_, bytes, cudaMemcpyDeviceToDevice, ms_));
@@ -497,6 +548,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     ACCO_CUDA(cudaEventRecord(base, cs_));
     ACCO_CUDA(cudaStreamWaitEvent(ms_, base, 0));
     const uint64_t r0 = static_cast<uint64_t>(update_);
+    const unsigned long long seq0 = phase_seq_;  // phase p carries peer sequence seq0 + p + 1
     // a continuing run() resumes with the estimate stage of round r0 (the
     // pipeline of the previous call drained at its last commit); a fresh run
     // bootstraps with one Init micro-batch at theta0
@@ -504,7 +556,10 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     for (int p = 0; p < NP; ++p) {
         for (int w = 0; w < nl; ++w) {
             // stage p computes at the parameters of phase p-2 and reuses its accumulator
-            if (p >= 2) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[p - 2], 0));
+            if (p >= 2) {
+                ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[p - 2], 0));
+                if (peer_) peer_->wait_done(seq0 + static_cast<unsigned long long>(p - 1), cs_);  // every rank's phase p-2
+            }
             ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(p) * nl + w], cs_));
             float* acc = acc_[static_cast<size_t>(w) * nacc + p % nacc];
             const void* params;
@@ -545,6 +600,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             const int t = (p - 1) / 2;
             if ((static_cast<long long>(update_) + t + 1) % sim_.eval_every == 0) {
                 ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[p], 0));
+                if (peer_) peer_->wait_done(seq0 + static_cast<unsigned long long>(p + 1), cs_);
                 double* e0 = eval_buf + static_cast<size_t>(t) * 2 * (n_eval_chunks + 1);
                 eval(theta_act_, e0, e0 + n_eval_chunks);
                 eval(est_act_, e0 + n_eval_chunks + 1, e0 + 2 * n_eval_chunks + 1);
@@ -670,6 +726,7 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     ACCO_CUDA(cudaEventRecord(base, cs_));
     ACCO_CUDA(cudaStreamWaitEvent(ms_, base, 0));
     const double carried_loss = pending_valid_ ? pending_loss_ : 0.0;
+    const unsigned long long seq0 = phase_seq_;  // round r's phase carries peer sequence seq0 + r + 1
     EventArr eval_ev;
     eval_ev.create(1);
     cudaEvent_t eval_done = eval_ev[0];
@@ -704,7 +761,10 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     for (int r = 0; r < T; ++r) {
         const uint64_t R = static_cast<uint64_t>(update_ + r);
         const bool warm = !delayed_method || (method_ == kDPU && static_cast<long long>(R) < sim_.warmup_rounds);
-        if (r >= 1) ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r - 1], 0));
+        if (r >= 1) {
+            ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r - 1], 0));
+            if (peer_) peer_->wait_done(seq0 + static_cast<unsigned long long>(r), cs_);
+        }
         if (warm) {  // ddp_round (protocols.cpp:321-338)
             ACCO_REQUIRE(!pending_valid_, "dpu: warm-up round after the delayed rounds started");
             stage(r, 0, theta_act_, R, kTagMain, k);
@@ -727,6 +787,7 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             }
             launch_phase(r, pending_slot_, tot, ev, false);
             ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r], 0));
+            if (peer_) peer_->wait_done(seq0 + static_cast<unsigned long long>(r + 1), cs_);
             stage(r + 1, pending_slot_ ^ 1, est_act_, R, kTagMain, k);
             pending_slot_ ^= 1;
             est_is_theta[static_cast<size_t>(r)] = 0;
@@ -734,6 +795,7 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
         snapshot(r, est_is_theta[static_cast<size_t>(r)]);
         if (do_eval && (update_ + r + 1) % sim_.eval_every == 0) {
             ACCO_CUDA(cudaStreamWaitEvent(cs_, ev.done[r], 0));
+            if (peer_) peer_->wait_done(seq0 + static_cast<unsigned long long>(r + 1), cs_);
             double* e0 = eval_buf + static_cast<size_t>(r) * 2 * (n_eval_chunks + 1);
             eval(theta_act_, e0, e0 + n_eval_chunks);
             if (!est_is_theta[static_cast<size_t>(r)]) eval(est_act_, e0 + n_eval_chunks + 1, e0 + 2 * n_eval_chunks + 1);

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "comm.h"
+#include "peer.h"
 #include "host_util.h"
 #include "model.h"
 #include "optim.h"
@@ -61,7 +62,8 @@ struct Interval {
 
 class Trainer {
 public:
-    Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm);
+    Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int method, Comm* comm,
+            PeerFabric* peer = nullptr);
     ~Trainer();
     Trainer(const Trainer&) = delete;
     Trainer& operator=(const Trainer&) = delete;
@@ -73,6 +75,7 @@ public:
     // theta-tilde^(t+1) after each commit (RunTrace.theta/estimate_history).
     void run(int t_updates, std::vector<UpdateRecord>& recs, RunStats& st, float* theta_hist = nullptr);
     int n_local() const { return n_local_; }
+    PeerFabric* peer() const { return peer_; }
     const std::vector<Interval>& timeline() const { return timeline_; }
     cudaStream_t compute_stream() const { return cs_; }
 
@@ -80,8 +83,8 @@ private:
     struct PhaseEvents;
     void alloc();
     void launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool warm = false);
-    float* reduce_grads(int acc_q, float* dst);
-    void opt_gather(bool commit, const float* g, const float* ret, const int64_t* tot, const int64_t* ret_tot,
+    FoldIO fold_sources(int acc_q, float* dst);
+    void opt_gather(bool commit, FoldIO io, const float* ret, const int64_t* tot, const int64_t* ret_tot,
                     void* act_dst, void* ag_dst, cudaEvent_t after_opt);
     void run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st);
     void run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st);
@@ -103,6 +106,9 @@ private:
     SimCfg sim_;
     int method_;
     Comm* comm_;
+    PeerFabric* peer_ = nullptr;     // fused fold over NVLink peer memory instead of NCCL
+    unsigned long long phase_seq_ = 0;  // comm phases issued so far (peer protocol sequence)
+    void* rep_[2] = {nullptr, nullptr}; // registered replicas (DPU swaps theta_act_/est_act_ between them)
     int n_local_ = 1, world_ = 1, rank_ = 0;
     ShardLayout layout_;
     int64_t psi_ = 0, chunk_ = 0, own_n_ = 0, own_lo_ = 0;

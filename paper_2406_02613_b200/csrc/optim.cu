@@ -49,14 +49,17 @@ void validate(const OptConfig& cfg) {
 namespace {
 
 struct KArgs {
-    const float* g;
+    const float* src[kMaxFold];  // gradient sums folded in this order (reference: ascending worker)
+    int nsrc;
+    void* dst[kMaxFold];         // every destination receives the new parameters (activation dtype)
+    int ndst;
+    float* ret_out;              // estimate: keep the raw folded sum (the retained shard)
     const float* gret;
     const int64_t* total;
     const int64_t* rtotal;
     float* theta;  // read; written by commit
     float* m;
     float* v;
-    void* out;     // may be null for commit
     int64_t n;
     float lr, b1, b2, omb1, omb2, c1, c2, eps, wd;
     int* flag;
@@ -98,10 +101,20 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
     bool bad = false;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t n4 = VEC ? a.n / 4 : 0;
     if (VEC) {
-        const int64_t n4 = a.n / 4;
         for (int64_t q = tid; q < n4; q += stride) {
-            float4 g = __ldcs(reinterpret_cast<const float4*>(a.g) + q);
+            // Fabric fold (collectives.cpp:55-75): copy of the first input, then
+            // += the others in order
+            float4 g = __ldcs(reinterpret_cast<const float4*>(a.src[0]) + q);
+            for (int k = 1; k < a.nsrc; ++k) {
+                const float4 h = __ldcs(reinterpret_cast<const float4*>(a.src[k]) + q);
+                g.x = __fadd_rn(g.x, h.x);
+                g.y = __fadd_rn(g.y, h.y);
+                g.z = __fadd_rn(g.z, h.z);
+                g.w = __fadd_rn(g.w, h.w);
+            }
+            if (!COMMIT && a.ret_out) reinterpret_cast<float4*>(a.ret_out)[q] = g;
             float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
             if (HAS_RET) r = __ldcs(reinterpret_cast<const float4*>(a.gret) + q);
             g.x = scale_grad(g.x, r.x, inv, HAS_RET);
@@ -128,34 +141,24 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
                     reinterpret_cast<float4*>(a.v)[q] = v;
                 }
             }
-            if (a.out) store4<OutT>(a.out, q, nt);
+            for (int k = 0; k < a.ndst; ++k) store4<OutT>(a.dst[k], q, nt);
         }
-        // tail (n % 4) handled by the scalar loop below
-        for (int64_t i = n4 * 4 + tid; i < a.n; i += stride) {
-            const float g = scale_grad(a.g[i], HAS_RET ? a.gret[i] : 0.f, inv, HAS_RET);
-            float th = a.theta[i];
-            float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
-            bad |= !(isfinite(g) && isfinite(th));
-            float nt = step_elem<KIND>(a, g, th, m, v);
-            if (COMMIT) {
-                a.theta[i] = nt;
-                if (KIND != 0) { a.m[i] = m; a.v[i] = v; }
-            }
-            if (a.out) store_out<OutT>(a.out, i, nt);
+    }
+    // scalar path (unaligned shards) and the n % 4 tail of the vector path
+    for (int64_t i = n4 * 4 + tid; i < a.n; i += stride) {
+        float g = a.src[0][i];
+        for (int k = 1; k < a.nsrc; ++k) g = __fadd_rn(g, a.src[k][i]);
+        if (!COMMIT && a.ret_out) a.ret_out[i] = g;
+        g = scale_grad(g, HAS_RET ? a.gret[i] : 0.f, inv, HAS_RET);
+        float th = a.theta[i];
+        float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
+        bad |= !(isfinite(g) && isfinite(th));
+        float nt = step_elem<KIND>(a, g, th, m, v);
+        if (COMMIT) {
+            a.theta[i] = nt;
+            if (KIND != 0) { a.m[i] = m; a.v[i] = v; }
         }
-    } else {
-        for (int64_t i = tid; i < a.n; i += stride) {
-            const float g = scale_grad(a.g[i], HAS_RET ? a.gret[i] : 0.f, inv, HAS_RET);
-            float th = a.theta[i];
-            float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
-            bad |= !(isfinite(g) && isfinite(th));
-            float nt = step_elem<KIND>(a, g, th, m, v);
-            if (COMMIT) {
-                a.theta[i] = nt;
-                if (KIND != 0) { a.m[i] = m; a.v[i] = v; }
-            }
-            if (a.out) store_out<OutT>(a.out, i, nt);
-        }
+        for (int k = 0; k < a.ndst; ++k) store_out<OutT>(a.dst[k], i, nt);
     }
     if (bad && a.flag) atomicOr(a.flag, 1);
 }
@@ -187,23 +190,37 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 }  // namespace
 
-void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* gsum,
-               const float* gret, const int64_t* total_dev, const int64_t* rtotal_dev, float* theta,
-               float* m, float* v, int64_t n, void* out, int out_dtype, int* flag,
-               cudaStream_t stream) {
+void opt_fold(const OptConfig& cfg, long long step, bool commit, const FoldIO& io, const float* gret,
+              const int64_t* total_dev, const int64_t* rtotal_dev, float* theta, float* m, float* v, int64_t n,
+              int out_dtype, int* flag, cudaStream_t stream) {
     if (n == 0) return;  // empty trailing shard: no-op (test_optim.cpp:168-181)
     validate(cfg);
-    ACCO_REQUIRE(gsum && theta && total_dev, "optimizer: null shard pointer");
+    ACCO_REQUIRE(io.nsrc >= 1 && io.nsrc <= kMaxFold && io.ndst >= 0 && io.ndst <= kMaxFold,
+                 "optimizer: 1..16 sources, 0..16 destinations");
+    ACCO_REQUIRE(theta && total_dev, "optimizer: null shard pointer");
     ACCO_REQUIRE(cfg.kind == 0 || (m && v), "optimizer: adam/adamw need m and v");
+    ACCO_REQUIRE(out_dtype == ACCO_DTYPE_F32 || out_dtype == ACCO_DTYPE_BF16, "optimizer: bad out dtype");
     KArgs a{};
-    a.g = gsum;
+    bool vec = aligned16(theta) && (cfg.kind == 0 || (aligned16(m) && aligned16(v))) && (!gret || aligned16(gret)) &&
+               (!io.ret_out || aligned16(io.ret_out));
+    for (int k = 0; k < io.nsrc; ++k) {
+        ACCO_REQUIRE(io.src[k], "optimizer: null gradient source");
+        a.src[k] = io.src[k];
+        vec = vec && aligned16(io.src[k]);
+    }
+    for (int k = 0; k < io.ndst; ++k) {
+        a.dst[k] = io.dst[k];
+        vec = vec && (reinterpret_cast<uintptr_t>(io.dst[k]) & (out_dtype == ACCO_DTYPE_BF16 ? 7 : 15)) == 0;
+    }
+    a.nsrc = io.nsrc;
+    a.ndst = io.ndst;
+    a.ret_out = io.ret_out;
     a.gret = gret;
     a.total = total_dev;
     a.rtotal = rtotal_dev;
     a.theta = theta;
     a.m = m;
     a.v = v;
-    a.out = out;
     a.n = n;
     a.flag = flag;
     // lr(t) and bias correction with step t+1 (optim.cpp:59-74); the estimate
@@ -219,16 +236,13 @@ void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* g
     a.c2 = static_cast<float>(1.0 - std::pow(cfg.adam_beta2, st));
     a.eps = static_cast<float>(cfg.adam_eps);
     a.wd = static_cast<float>(cfg.weight_decay);
-    const bool vec = aligned16(gsum) && (!gret || aligned16(gret)) && aligned16(theta) &&
-                     (cfg.kind == 0 || (aligned16(m) && aligned16(v))) &&
-                     (!out || (reinterpret_cast<uintptr_t>(out) & (out_dtype == ACCO_DTYPE_BF16 ? 7 : 15)) == 0);
     const bool has_ret = gret != nullptr;
-    ACCO_REQUIRE(out_dtype == ACCO_DTYPE_F32 || out_dtype == ACCO_DTYPE_BF16, "optimizer: bad out dtype");
-    // algorithmic bytes per element: reads g (+ retained),
-    // theta (+ m, v); commit writes theta (+ m, v); payload 2 (bf16) / 4 B.
+    // algorithmic bytes per element: reads the folded sums
+    // (+ retained), theta (+ m, v); commit writes theta (+ m, v); estimate may
+    // keep the retained sum; payload 2 (bf16) / 4 B per destination.
     const int mv = cfg.kind != 0 ? 8 : 0;
-    const double per_elem = 4.0 + (has_ret ? 4 : 0) + 4 + mv + (commit ? 4 + mv : 0) +
-                            (out ? (out_dtype == ACCO_DTYPE_BF16 ? 2 : 4) : 0);
+    const double per_elem = 4.0 * io.nsrc + (has_ret ? 4 : 0) + 4 + mv + (commit ? 4 + mv : 0) +
+                            (io.ret_out ? 4 : 0) + io.ndst * (out_dtype == ACCO_DTYPE_BF16 ? 2 : 4);
     ProfScope prof(kProfOpt, per_elem * static_cast<double>(n), stream);
 #define ACCO_OPT_DISPATCH(C)                                                                    \
     if (out_dtype == ACCO_DTYPE_BF16) {                                                         \
@@ -244,6 +258,19 @@ void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* g
         ACCO_OPT_DISPATCH(false)
     }
 #undef ACCO_OPT_DISPATCH
+}
+
+void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* gsum, const float* gret,
+               const int64_t* total_dev, const int64_t* rtotal_dev, float* theta, float* m, float* v, int64_t n,
+               void* out, int out_dtype, int* flag, cudaStream_t stream) {
+    FoldIO io;
+    io.src[0] = gsum;
+    io.nsrc = 1;
+    if (out) {
+        io.dst[0] = out;
+        io.ndst = 1;
+    }
+    opt_fold(cfg, step, commit, io, gret, total_dev, rtotal_dev, theta, m, v, n, out_dtype, flag, stream);
 }
 
 }  // namespace acco

@@ -37,7 +37,24 @@ inline OptConfig from_c(const acco_opt_cfg& c) {
 double scheduled_lr(const OptConfig& cfg, long long t);
 void validate(const OptConfig& cfg);
 
-// One fused optimizer pass over a shard of n elements (see optim.cu).
+// One fused pass per comm phase over a shard of n elements: fold the gradient
+// sums src[0..nsrc) in order (the reference Fabric's reduce order — local
+// virtual workers, or peers' accumulators over NVLink), optionally keep the
+// folded sum (estimate's retained shard), apply the optimizer step, and write
+// the new parameters to every destination replica (local and/or peers').
+constexpr int kMaxFold = 16;
+struct FoldIO {
+    const float* src[kMaxFold] = {};
+    int nsrc = 0;
+    void* dst[kMaxFold] = {};
+    int ndst = 0;
+    float* ret_out = nullptr;
+};
+void opt_fold(const OptConfig& cfg, long long step, bool commit, const FoldIO& io, const float* gret,
+              const int64_t* total_dev, const int64_t* rtotal_dev, float* theta, float* m, float* v, int64_t n,
+              int out_dtype, int* flag, cudaStream_t stream);
+
+// Single-source form (see optim.cu).
 // commit=false: estimate (pure); commit=true: persistent update of theta/m/v.
 void opt_apply(const OptConfig& cfg, long long step, bool commit, const float* gsum,
                const float* gret, const int64_t* total_dev, const int64_t* rtotal_dev,

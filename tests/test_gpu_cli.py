@@ -74,3 +74,12 @@ def test_gpu_verify_suites_pass(cuda, tmp_path, suite):
     assert main(["verify", "--suite", suite, "--out", str(out)]) == 0
     rep = json.loads(out.read_text())
     assert rep["pass"] and rep["suite"] == suite
+
+
+def test_run_peer_fabric_config(cuda, tmp_path):
+    cfg = dict(CFG, n_workers=1, fabric="peer")
+    path = tmp_path / "cfg.json"
+    path.write_text(json.dumps(cfg))
+    assert main(["run", "--config", str(path), "--out", str(tmp_path / "o")]) == 0
+    _, rows = _metrics(tmp_path / "o" / "metrics.csv")
+    assert len(rows) == 5

@@ -91,3 +91,39 @@ def test_engine_nccl_mode_matches_oracle(cuda, nccl_comm, method):
         assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
         assert tr.records[t].samples_cum == ref.records[t].samples_cum
         assert abs(tr.records[t].loss - ref.records[t].loss) <= 1e-5 * abs(ref.records[t].loss)
+
+
+@pytest.mark.parametrize("method", ["acco", "zero1", "dpu", "wp"])
+def test_engine_peer_fabric_matches_oracle(cuda, method):
+    """Peer fabric (one fused fold + optimizer + replica-store kernel per comm
+    phase, device flags for counts and phase barriers) at world size 1: the
+    same protocol code path as N GPUs on NVLink, with this rank as its own peer."""
+    peer = api.PeerComm(rank=0, world=1, device=0)
+    opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
+                              scheduler="cosine")
+    sim = api.SimConfig(n_workers=1, batch_size=4, n_grad_accumulation=2, master_seed=7, eval_every=1)
+    tr = api.run_protocol(method, api.LMConfig(**MINI, precision="fp32", max_batch=4), opt, sim, 4, comm=peer)
+    gc = G.GPTConfig(**MINI)
+    prob = G.LMProblem(gc)
+    th0 = G.default_theta0(gc, 7).astype(np.float32).astype(np.float64)
+    ocfg = O.OptimizerConfig(**{k: getattr(opt, k) for k in O.OptimizerConfig.__dataclass_fields__})
+    osim = O.SimConfig(1, 4, 2, False, 7)
+    ref = O.run_method(method, (lambda th, s: prob.stochastic_grad(th, s, 4)), th0, ocfg, osim, 4,
+                       eval_fn=prob.value_and_grad)
+    for t in range(4):
+        a, b = tr.theta_history[t + 1], ref.theta_history[t + 1]
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5
+        e, f = tr.estimate_history[t + 1], ref.estimate_history[t + 1]
+        assert np.linalg.norm(e - f) / np.linalg.norm(f) <= 1e-5
+        assert tr.records[t].samples_cum == ref.records[t].samples_cum
+        assert abs(tr.records[t].loss - ref.records[t].loss) <= 1e-5 * abs(ref.records[t].loss)
+    kinds = {iv.kind for iv in tr.timeline if iv.stream == "comm"}
+    assert "optimizer" in kinds
+
+
+def test_peer_fabric_rejects_ddp(cuda):
+    peer = api.PeerComm(rank=0, world=1, device=0)
+    with pytest.raises(api.InvalidArgument):
+        api.Trainer("ddp", api.Model(api.LMConfig(**MINI, precision="fp32", max_batch=4)),
+                    api.OptimizerConfig(kind="sgd", learning_rate=0.1), api.SimConfig(n_workers=1, batch_size=4),
+                    peer)
