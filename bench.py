@@ -30,6 +30,9 @@ MODELS = {
     "gpt2-small": dict(vocab=50257, d_model=768, n_layer=12, n_head=12, seq_len=1024),
     "gpt2-medium": dict(vocab=50257, d_model=1024, n_layer=24, n_head=16, seq_len=1024),
     "c1": dict(vocab=256, d_model=128, n_layer=2, n_head=4, seq_len=64),
+    # C4: Llama-style 1.1B (TinyLlama-1.1B shape: GQA 32/4 heads of 64, SwiGLU 5632, untied head)
+    "llama-1b": dict(vocab=32000, d_model=2048, n_layer=22, n_head=32, seq_len=2048, arch="llama", n_kv_head=4,
+                     d_ff=5632),
 }
 
 
@@ -310,7 +313,9 @@ def main():
                  for c, v in p.items() if isinstance(v, dict) and v.get("launches")}
 
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and not args.profile:
+    if not args.no_cpu_baseline and world == 1 and not args.profile and cfgd.get("arch", "gpt2") == "gpt2":
+        # (the fp64 port of the 1.1B Llama would need ~40 GB host RAM and minutes
+        # per sample: its CPU baseline is not taken)
         from oracle import cpu_bench
         from oracle import gpt_oracle as G
 

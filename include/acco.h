@@ -173,6 +173,13 @@ typedef struct acco_lm_cfg {
     int host_data; /* 1: dataset stays in pinned host memory; every micro-batch's
                       token rows are copied host->device (data-loader path), and
                       every micro-batch loss is read back device->host */
+    /* model family (BASELINE.json C4): 0 = GPT-2 block (configs C1-C3),
+     * 1 = Llama block (RMSNorm, RoPE, grouped-query attention, SwiGLU, untied
+     * head; oracle/gpt_oracle.py arch="llama") */
+    int arch;
+    int n_kv_head;    /* llama: KV heads (0 -> n_head) */
+    int d_ff;         /* llama: SwiGLU hidden size (0 -> 4 * d_model) */
+    double rope_base; /* llama: rotary base (0 -> 10000) */
 } acco_lm_cfg;
 
 typedef struct acco_model acco_model;

@@ -34,7 +34,8 @@ SCHEDULES = {"floor": 0, "adaptive": 1, "replay": 2}
 class LMCfgC(C.Structure):
     _fields_ = [("vocab", C.c_int), ("d_model", C.c_int), ("n_layer", C.c_int), ("n_head", C.c_int),
                 ("seq_len", C.c_int), ("n_samples", C.c_int), ("data_seed", C.c_uint64),
-                ("precision", C.c_int), ("max_batch", C.c_int), ("host_data", C.c_int)]
+                ("precision", C.c_int), ("max_batch", C.c_int), ("host_data", C.c_int), ("arch", C.c_int),
+                ("n_kv_head", C.c_int), ("d_ff", C.c_int), ("rope_base", C.c_double)]
 
 
 class SimCfgC(C.Structure):
@@ -182,12 +183,19 @@ class LMConfig:
     precision: str = "fp32"  # "fp32" (parity) or "bf16" (throughput)
     max_batch: int = 8
     host_data: bool = False  # data-loader path: per-micro-batch H2D of token rows
+    arch: str = "gpt2"       # "gpt2" | "llama" (RMSNorm, RoPE, GQA, SwiGLU, untied head)
+    n_kv_head: int = 0       # llama: KV heads (0 -> n_head)
+    d_ff: int = 0            # llama: SwiGLU hidden (0 -> 4 * d_model)
+    rope_base: float = 10000.0
 
     def to_c(self) -> LMCfgC:
         if self.precision not in ("fp32", "bf16"):
             raise InvalidArgument(_lib.INVALID, "lm config: precision must be fp32 or bf16")
+        if self.arch not in ("gpt2", "llama"):
+            raise InvalidArgument(_lib.INVALID, "lm config: arch must be gpt2 or llama")
         return LMCfgC(self.vocab, self.d_model, self.n_layer, self.n_head, self.seq_len, self.n_samples,
-                      self.data_seed, 1 if self.precision == "bf16" else 0, self.max_batch, int(self.host_data))
+                      self.data_seed, 1 if self.precision == "bf16" else 0, self.max_batch, int(self.host_data),
+                      1 if self.arch == "llama" else 0, self.n_kv_head, self.d_ff, float(self.rope_base))
 
 
 class Model:
@@ -510,15 +518,18 @@ def _req(j, k):
 
 def parse_config(j: dict) -> ExperimentConfig:
     """config.cpp:80-133 (same keys, defaults and validation); problem.kind
-    must be "gpt" on the B200 path (the analytic problems are CPU fixtures)."""
+    must be "gpt" or "llama" on the B200 path (the analytic problems are CPU
+    fixtures); "llama" adds n_kv_head, d_ff, rope_base."""
     p = _req(j, "problem")
     kind = _req(p, "kind")
-    if kind != "gpt":
+    if kind not in ("gpt", "llama"):
         raise InvalidArgument(_lib.INVALID, f"unknown problem kind for the B200 path: {kind}")
     prob = LMConfig(vocab=_get(p, "vocab", 256), d_model=_get(p, "d_model", 128), n_layer=_get(p, "n_layer", 2),
                     n_head=_get(p, "n_head", 4), seq_len=_get(p, "seq_len", 64), n_samples=_get(p, "n_samples", 256),
                     data_seed=_get(p, "seed", 1), precision=_get(p, "precision", "fp32"),
-                    max_batch=max(_get(j, "batch_size", 1), _get(p, "max_batch", 1)))
+                    max_batch=max(_get(j, "batch_size", 1), _get(p, "max_batch", 1)),
+                    arch="llama" if kind == "llama" else "gpt2", n_kv_head=_get(p, "n_kv_head", 0),
+                    d_ff=_get(p, "d_ff", 0), rope_base=_get(p, "rope_base", 10000.0))
     method = _req(j, "method_name")
     if method not in METHODS:
         raise InvalidArgument(_lib.INVALID, f"unknown method: {method}")

@@ -14,13 +14,15 @@ constexpr int kTile = 64;
 
 template <class T, int HD>
 __global__ void __launch_bounds__(kTile) attn_fwd_kernel(const T* __restrict__ qkv, T* __restrict__ y,
-                                                         float* __restrict__ lse, int seq, int H, float scale) {
+                                                         float* __restrict__ lse, int seq, int H, int Hkv,
+                                                         float scale) {
     extern __shared__ float sm[];
     float(*Ks)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm);
     float(*Vs)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + kTile * (HD + 1));
     const int bh = blockIdx.x, b = bh / H, h = bh % H;
     const int d = H * HD;
-    const int64_t ld = 3 * d;
+    const int64_t ld = static_cast<int64_t>(H + 2 * Hkv) * HD;
+    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;  // this head's K / V columns
     const int t = blockIdx.y * kTile + threadIdx.x;
     const int64_t base = static_cast<int64_t>(b) * seq * ld;
     float q[HD], o[HD];
@@ -37,8 +39,8 @@ __global__ void __launch_bounds__(kTile) attn_fwd_kernel(const T* __restrict__ q
         for (int i = threadIdx.x; i < kTile * HD; i += kTile) {
             const int r = i / HD, c = i % HD;
             const int j = j0 + r;
-            Ks[r][c] = j < seq ? to_f(qkv[base + j * ld + d + h * HD + c]) : 0.f;
-            Vs[r][c] = j < seq ? to_f(qkv[base + j * ld + 2 * d + h * HD + c]) : 0.f;
+            Ks[r][c] = j < seq ? to_f(qkv[base + j * ld + kc + c]) : 0.f;
+            Vs[r][c] = j < seq ? to_f(qkv[base + j * ld + vc + c]) : 0.f;
         }
         __syncthreads();
         if (t < seq) {
@@ -89,13 +91,15 @@ __global__ void attn_dsum_kernel(const T* __restrict__ y, const T* __restrict__ 
 template <class T, int HD>
 __global__ void __launch_bounds__(kTile) attn_dq_kernel(const T* __restrict__ qkv, const float* __restrict__ lse,
                                                         const float* __restrict__ dsum, const T* __restrict__ dy,
-                                                        T* __restrict__ dqkv, int seq, int H, float scale) {
+                                                        T* __restrict__ dqkv, int seq, int H, int Hkv,
+                                                        float scale) {
     extern __shared__ float sm[];
     float(*Ks)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm);
     float(*Vs)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + kTile * (HD + 1));
     const int bh = blockIdx.x, b = bh / H, h = bh % H;
     const int d = H * HD;
-    const int64_t ld = 3 * d;
+    const int64_t ld = static_cast<int64_t>(H + 2 * Hkv) * HD;
+    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;
     const int t = blockIdx.y * kTile + threadIdx.x;
     const int64_t base = static_cast<int64_t>(b) * seq * ld;
     float q[HD], dO[HD], dq[HD];
@@ -117,8 +121,8 @@ __global__ void __launch_bounds__(kTile) attn_dq_kernel(const T* __restrict__ qk
         for (int i = threadIdx.x; i < kTile * HD; i += kTile) {
             const int r = i / HD, c = i % HD;
             const int j = j0 + r;
-            Ks[r][c] = j < seq ? to_f(qkv[base + j * ld + d + h * HD + c]) : 0.f;
-            Vs[r][c] = j < seq ? to_f(qkv[base + j * ld + 2 * d + h * HD + c]) : 0.f;
+            Ks[r][c] = j < seq ? to_f(qkv[base + j * ld + kc + c]) : 0.f;
+            Vs[r][c] = j < seq ? to_f(qkv[base + j * ld + vc + c]) : 0.f;
         }
         __syncthreads();
         if (t < seq) {
@@ -144,10 +148,13 @@ __global__ void __launch_bounds__(kTile) attn_dq_kernel(const T* __restrict__ qk
     }
 }
 
+// dK/dV: one block per (batch * KV head, key tile); the query heads of the
+// group (H / Hkv of them) are folded in ascending order (GQA), each over the
+// query rows at and after the key.
 template <class T, int HD>
 __global__ void __launch_bounds__(kTile) attn_dkv_kernel(const T* __restrict__ qkv, const float* __restrict__ lse,
                                                          const float* __restrict__ dsum, const T* __restrict__ dy,
-                                                         T* __restrict__ dqkv, int seq, int H, float scale) {
+                                                         T* __restrict__ dqkv, int seq, int H, int Hkv, float scale) {
     extern __shared__ float sm[];
     float(*Ko)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm);
     float(*Vo)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + 1 * kTile * (HD + 1));
@@ -155,81 +162,87 @@ __global__ void __launch_bounds__(kTile) attn_dkv_kernel(const T* __restrict__ q
     float(*dOs)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + 3 * kTile * (HD + 1));
     float* Ls = sm + 4 * kTile * (HD + 1);
     float* Ds = Ls + kTile;
-    const int bh = blockIdx.x, b = bh / H, h = bh % H;
+    const int bk = blockIdx.x, b = bk / Hkv, hk = bk % Hkv;
+    const int G = H / Hkv;
     const int d = H * HD;
-    const int64_t ld = 3 * d;
+    const int64_t ld = static_cast<int64_t>(H + 2 * Hkv) * HD;
+    const int kc = d + hk * HD, vc = kc + Hkv * HD;
     const int j0b = blockIdx.y * kTile;
     const int j = j0b + threadIdx.x;
     const int64_t base = static_cast<int64_t>(b) * seq * ld;
     for (int i = threadIdx.x; i < kTile * HD; i += kTile) {
         const int r = i / HD, c = i % HD;
         const int jj = j0b + r;
-        Ko[r][c] = jj < seq ? to_f(qkv[base + jj * ld + d + h * HD + c]) : 0.f;
-        Vo[r][c] = jj < seq ? to_f(qkv[base + jj * ld + 2 * d + h * HD + c]) : 0.f;
+        Ko[r][c] = jj < seq ? to_f(qkv[base + jj * ld + kc + c]) : 0.f;
+        Vo[r][c] = jj < seq ? to_f(qkv[base + jj * ld + vc + c]) : 0.f;
     }
     float dk[HD], dv[HD];
 #pragma unroll
     for (int c = 0; c < HD; ++c) dk[c] = dv[c] = 0.f;
-    for (int i0 = j0b; i0 < seq; i0 += kTile) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < kTile * HD; i += kTile) {
-            const int r = i / HD, c = i % HD;
-            const int ii = i0 + r;
-            Qs[r][c] = ii < seq ? to_f(qkv[base + ii * ld + h * HD + c]) : 0.f;
-            dOs[r][c] = ii < seq ? to_f(dy[(static_cast<int64_t>(b) * seq + ii) * d + h * HD + c]) : 0.f;
-        }
-        if (threadIdx.x < kTile) {
-            const int ii = i0 + threadIdx.x;
-            Ls[threadIdx.x] = ii < seq ? lse[static_cast<int64_t>(bh) * seq + ii] : 0.f;
-            Ds[threadIdx.x] = ii < seq ? dsum[static_cast<int64_t>(bh) * seq + ii] : 0.f;
-        }
-        __syncthreads();
-        if (j < seq) {
-            const int istart = max(0, j - i0);
-            const int iend = min(kTile, seq - i0);
-            for (int r = istart; r < iend; ++r) {
-                float s = 0.f, dp = 0.f;
+    for (int g = 0; g < G; ++g) {
+        const int h = hk * G + g;
+        const int64_t bh = static_cast<int64_t>(b) * H + h;
+        for (int i0 = j0b; i0 < seq; i0 += kTile) {
+            __syncthreads();
+            for (int i = threadIdx.x; i < kTile * HD; i += kTile) {
+                const int r = i / HD, c = i % HD;
+                const int ii = i0 + r;
+                Qs[r][c] = ii < seq ? to_f(qkv[base + ii * ld + h * HD + c]) : 0.f;
+                dOs[r][c] = ii < seq ? to_f(dy[(static_cast<int64_t>(b) * seq + ii) * d + h * HD + c]) : 0.f;
+            }
+            if (threadIdx.x < kTile) {
+                const int ii = i0 + threadIdx.x;
+                Ls[threadIdx.x] = ii < seq ? lse[bh * seq + ii] : 0.f;
+                Ds[threadIdx.x] = ii < seq ? dsum[bh * seq + ii] : 0.f;
+            }
+            __syncthreads();
+            if (j < seq) {
+                const int istart = max(0, j - i0);
+                const int iend = min(kTile, seq - i0);
+                for (int r = istart; r < iend; ++r) {
+                    float s = 0.f, dp = 0.f;
 #pragma unroll
-                for (int c = 0; c < HD; ++c) {
-                    s = fmaf(Qs[r][c], Ko[threadIdx.x][c], s);
-                    dp = fmaf(dOs[r][c], Vo[threadIdx.x][c], dp);
-                }
-                const float p = expf(s * scale - Ls[r]);
-                const float ds = p * (dp - Ds[r]);
+                    for (int c = 0; c < HD; ++c) {
+                        s = fmaf(Qs[r][c], Ko[threadIdx.x][c], s);
+                        dp = fmaf(dOs[r][c], Vo[threadIdx.x][c], dp);
+                    }
+                    const float p = expf(s * scale - Ls[r]);
+                    const float ds = p * (dp - Ds[r]);
 #pragma unroll
-                for (int c = 0; c < HD; ++c) {
-                    dv[c] = fmaf(p, dOs[r][c], dv[c]);
-                    dk[c] = fmaf(ds, Qs[r][c], dk[c]);
+                    for (int c = 0; c < HD; ++c) {
+                        dv[c] = fmaf(p, dOs[r][c], dv[c]);
+                        dk[c] = fmaf(ds, Qs[r][c], dk[c]);
+                    }
                 }
             }
         }
     }
     if (j < seq) {
-        T* o = dqkv + (static_cast<int64_t>(b) * seq + j) * ld + h * HD;
+        T* o = dqkv + (static_cast<int64_t>(b) * seq + j) * ld;
 #pragma unroll
         for (int c = 0; c < HD; ++c) {
-            o[d + c] = from_f<T>(dk[c] * scale);
-            o[2 * d + c] = from_f<T>(dv[c]);
+            o[kc + c] = from_f<T>(dk[c] * scale);
+            o[vc + c] = from_f<T>(dv[c]);
         }
     }
 }
 
 template <class T, int HD>
-void fwd_impl(const T* qkv, T* y, float* lse, int B, int seq, int H, cudaStream_t s) {
+void fwd_impl(const T* qkv, T* y, float* lse, int B, int seq, int H, int Hkv, cudaStream_t s) {
     const int smem = 2 * kTile * (HD + 1) * 4;
     static bool cfg = false;
     if (!cfg) {
         ACCO_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
-    attn_fwd_kernel<T, HD><<<dim3(B * H, ceil_div(seq, kTile)), kTile, smem, s>>>(qkv, y, lse, seq, H,
-                                                                                  1.0f / sqrtf(static_cast<float>(HD)));
+    attn_fwd_kernel<T, HD><<<dim3(B * H, ceil_div(seq, kTile)), kTile, smem, s>>>(
+        qkv, y, lse, seq, H, Hkv, 1.0f / sqrtf(static_cast<float>(HD)));
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T, int HD>
 void bwd_impl(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, float* dsum, int B, int seq, int H,
-              cudaStream_t s) {
+              int Hkv, cudaStream_t s) {
     const float scale = 1.0f / sqrtf(static_cast<float>(HD));
     const int64_t rows = static_cast<int64_t>(B) * H * seq;
     attn_dsum_kernel<T, HD><<<static_cast<int>((rows + 255) / 256), 256, 0, s>>>(y, dy, dsum, B, seq, H);
@@ -242,10 +255,11 @@ void bwd_impl(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, 
         ACCO_CUDA(cudaFuncSetAttribute(attn_dkv_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
         cfg = true;
     }
-    dim3 grid(B * H, ceil_div(seq, kTile));
-    attn_dq_kernel<T, HD><<<grid, kTile, smem_q, s>>>(qkv, lse, dsum, dy, dqkv, seq, H, scale);
+    attn_dq_kernel<T, HD><<<dim3(B * H, ceil_div(seq, kTile)), kTile, smem_q, s>>>(qkv, lse, dsum, dy, dqkv, seq, H,
+                                                                                  Hkv, scale);
     ACCO_CHECK_LAUNCH();
-    attn_dkv_kernel<T, HD><<<grid, kTile, smem_kv, s>>>(qkv, lse, dsum, dy, dqkv, seq, H, scale);
+    attn_dkv_kernel<T, HD><<<dim3(B * Hkv, ceil_div(seq, kTile)), kTile, smem_kv, s>>>(qkv, lse, dsum, dy, dqkv, seq,
+                                                                                     H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -253,12 +267,12 @@ void bwd_impl(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, 
 
 // Tensor-core paths for bf16: tcgen05 (attn_tc.cu), then mma.sync
 // (attn_mma.cu); each returns false if not applicable.
-bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int seq, int H, int hd,
-                      cudaStream_t s);
+bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int seq, int H, int Hkv,
+                      int hd, cudaStream_t s);
 bool attention_fwd_mma(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int seq, int H, int hd,
                        cudaStream_t s);
 bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse, const __nv_bfloat16* dy,
-                      __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int hd, cudaStream_t s);
+                      __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int Hkv, int hd, cudaStream_t s);
 bool attention_bwd_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse,
                        const __nv_bfloat16* dy, __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int hd,
                        cudaStream_t s);
@@ -269,41 +283,43 @@ static double attn_flops(int B, int seq, int H, int hd) {
 }
 
 template <class T>
-void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd, cudaStream_t s) {
+void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int Hkv, int hd, cudaStream_t s) {
     ProfScope prof(kProfAttn, attn_flops(B, seq, H, hd), s);
+    ACCO_REQUIRE(Hkv >= 1 && H % Hkv == 0, "attention: n_head must be a multiple of n_kv_head");
     if constexpr (sizeof(T) == 2) {
-        if (attention_fwd_tc(qkv, y, lse, B, seq, H, hd, s)) return;
-        if (attention_fwd_mma(qkv, y, lse, B, seq, H, hd, s)) return;
+        if (attention_fwd_tc(qkv, y, lse, B, seq, H, Hkv, hd, s)) return;
+        if (Hkv == H && attention_fwd_mma(qkv, y, lse, B, seq, H, hd, s)) return;
     }
-    if (hd == 32) fwd_impl<T, 32>(qkv, y, lse, B, seq, H, s);
-    else if (hd == 64) fwd_impl<T, 64>(qkv, y, lse, B, seq, H, s);
-    else if (hd == 16) fwd_impl<T, 16>(qkv, y, lse, B, seq, H, s);
-    else if (hd == 8) fwd_impl<T, 8>(qkv, y, lse, B, seq, H, s);
+    if (hd == 32) fwd_impl<T, 32>(qkv, y, lse, B, seq, H, Hkv, s);
+    else if (hd == 64) fwd_impl<T, 64>(qkv, y, lse, B, seq, H, Hkv, s);
+    else if (hd == 16) fwd_impl<T, 16>(qkv, y, lse, B, seq, H, Hkv, s);
+    else if (hd == 8) fwd_impl<T, 8>(qkv, y, lse, B, seq, H, Hkv, s);
     else throw Error(kInvalidArg, "attention: head size must be 8, 16, 32 or 64");
 }
 
 template <class T>
 void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, float* dsum, int B, int seq,
-                   int H, int hd, cudaStream_t s) {
+                   int H, int Hkv, int hd, cudaStream_t s) {
     ProfScope prof(kProfAttn, 2.5 * attn_flops(B, seq, H, hd), s);
+    ACCO_REQUIRE(Hkv >= 1 && H % Hkv == 0, "attention: n_head must be a multiple of n_kv_head");
     if constexpr (sizeof(T) == 2) {
-        if (attention_bwd_tc(qkv, y, lse, dy, dqkv, dsum, B, seq, H, hd, s)) return;
-        if (attention_bwd_mma(qkv, y, lse, dy, dqkv, dsum, B, seq, H, hd, s)) return;
+        if (attention_bwd_tc(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, hd, s)) return;
+        if (Hkv == H && attention_bwd_mma(qkv, y, lse, dy, dqkv, dsum, B, seq, H, hd, s)) return;
     }
-    if (hd == 32) bwd_impl<T, 32>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, s);
-    else if (hd == 64) bwd_impl<T, 64>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, s);
-    else if (hd == 16) bwd_impl<T, 16>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, s);
-    else if (hd == 8) bwd_impl<T, 8>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, s);
+    if (hd == 32) bwd_impl<T, 32>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
+    else if (hd == 64) bwd_impl<T, 64>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
+    else if (hd == 16) bwd_impl<T, 16>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
+    else if (hd == 8) bwd_impl<T, 8>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
     else throw Error(kInvalidArg, "attention: head size must be 8, 16, 32 or 64");
 }
 
-template void attention_fwd<float>(const float*, float*, float*, int, int, int, int, cudaStream_t);
-template void attention_fwd<__nv_bfloat16>(const __nv_bfloat16*, __nv_bfloat16*, float*, int, int, int, int,
+template void attention_fwd<float>(const float*, float*, float*, int, int, int, int, int, cudaStream_t);
+template void attention_fwd<__nv_bfloat16>(const __nv_bfloat16*, __nv_bfloat16*, float*, int, int, int, int, int,
                                            cudaStream_t);
 template void attention_bwd<float>(const float*, const float*, const float*, const float*, float*, float*, int,
-                                   int, int, int, cudaStream_t);
+                                   int, int, int, int, cudaStream_t);
 template void attention_bwd<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, const float*,
-                                           const __nv_bfloat16*, __nv_bfloat16*, float*, int, int, int, int,
+                                           const __nv_bfloat16*, __nv_bfloat16*, float*, int, int, int, int, int,
                                            cudaStream_t);
 
 }  // namespace acco

@@ -143,7 +143,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
 
 __global__ void __launch_bounds__(kThreads, 1)
     fa_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
-              int T, int H, float scale) {
+              int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qt = nqt - 1 - blockIdx.x;
     const int bh = blockIdx.y, b = bh / H, h = bh % H;
     const int d = H * HD;
+    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;  // this head's K / V columns
     const int q0 = qt * BQ;
     const int nkt = (min(T, q0 + BQ) + BKV - 1) / BKV;  // causal: key tiles up to the diagonal
     const int row_base = b * T;                          // qkv row of (b, t=0)
@@ -201,8 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = j % kStages;
                 mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
-                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], d + h * HD, row_base + j * BKV);
-                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], 2 * d + h * HD, row_base + j * BKV);
+                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], kc, row_base + j * BKV);
+                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], vc, row_base + j * BKV);
             }
         }
     } else if (warp == 1) {
@@ -470,7 +472,7 @@ __device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m
 
 __global__ void __launch_bounds__(kThreads, 1)
     fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
-               int T, int H, float scale) {
+               int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                         // [2 tiles]
@@ -490,6 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int pr = npair - 1 - blockIdx.x;     // heavy pairs first
     const int bh = blockIdx.y, b = bh / H, h = bh % H;
     const int d = H * HD;
+    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;  // this head's K / V columns
     const int row_base = b * T;
     const int nt[2] = {2 * pr + 1, 2 * pr + 2 <= nqt ? 2 * pr + 2 : 0};  // kv tiles per query tile (0: absent)
     const int nkv = nt[1] ? nt[1] : nt[0];
@@ -529,8 +533,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = j % F2_STAGES;
                 mbar_wait(&kv_empty[s], ((j / F2_STAGES) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
-                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], d + h * HD, row_base + j * BKV);
-                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], 2 * d + h * HD, row_base + j * BKV);
+                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], kc, row_base + j * BKV);
+                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], vc, row_base + j * BKV);
             }
         }
     } else if (warp == 1) {
@@ -793,7 +797,7 @@ constexpr int DKV_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + 2 * 2 * BW_T * 4
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                   const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                  int T, int H, float scale) {
+                  int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;
@@ -816,12 +820,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int nt = (T + BW_T - 1) / BW_T;
     const int kt = blockIdx.x;
-    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    // one CTA per (batch * KV head, key tile): the G = H / Hkv query heads of
+    // the group are folded in ascending order (GQA; G = 1 for MHA), iteration
+    // it = g * nq + (query tile - kt)
+    const int bk = blockIdx.y, b = bk / Hkv, hk = bk % Hkv;
+    const int G = H / Hkv;
     const int d = H * HD;
+    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    const int kc = d + hk * HD, vc = kc + Hkv * HD;
     const int k0 = kt * BW_T;
     const int row_base = b * T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nq = nt - kt;  // query tiles kt .. nt-1
+    const int nq = nt - kt;  // query tiles kt .. nt-1 per query head
+    const int niter = G * nq;
 
     if (threadIdx.x == 0) {
         mbar_init(kv_full, 1);
@@ -850,11 +861,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             mbar_expect_tx(kv_full, 2 * BW_TILE);
-            tma_load_2d(sK, &tmQKV, kv_full, d + h * HD, row_base + k0);
-            tma_load_2d(sV, &tmQKV, kv_full, 2 * d + h * HD, row_base + k0);
-            for (int i = 0; i < nq; ++i) {
+            tma_load_2d(sK, &tmQKV, kv_full, kc, row_base + k0);
+            tma_load_2d(sV, &tmQKV, kv_full, vc, row_base + k0);
+            for (int i = 0; i < niter; ++i) {
                 const int s = i & 1;
-                const int q0 = (kt + i) * BW_T;
+                const int h = hk * G + i / nq;
+                const int q0 = (kt + i % nq) * BW_T;
                 mbar_wait(&q_empty[s], ((i >> 1) & 1) ^ 1);
                 mbar_expect_tx(&q_full[s], 2 * BW_TILE);
                 tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
@@ -881,10 +893,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit(s_full);
             };
             issue_s(0);
-            for (int i = 0; i < nq; ++i) {
+            for (int i = 0; i < niter; ++i) {
                 const int s = i & 1;
                 const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
-                if (i + 1 < nq) {  // next tile's S^T/dP^T overlap this tile's softmax
+                if (i + 1 < niter) {  // next tile's S^T/dP^T overlap this tile's softmax
                     mbar_wait(s_free, i & 1);
                     issue_s(i + 1);
                 }
@@ -911,16 +923,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         // lse (log2) and D of query tile i, loaded one tile ahead (registers)
         // by the half-0 threads and published through a double-buffered smem row
         auto fetch = [&](int i, float& lv, float& dv) {
-            const int q = (kt + i) * BW_T + r;
-            const bool ok = i < nq && q < T;
-            lv = ok ? __ldg(lse + static_cast<int64_t>(bh) * T + q) * kLog2e : 0.f;
-            dv = ok ? __ldg(dsum + static_cast<int64_t>(bh) * T + q) : 0.f;
+            const int q = (kt + i % nq) * BW_T + r;
+            const bool ok = i < niter && q < T;
+            const int64_t bh = static_cast<int64_t>(b) * H + hk * G + i / nq;
+            lv = ok ? __ldg(lse + bh * T + q) * kLog2e : 0.f;
+            dv = ok ? __ldg(dsum + bh * T + q) : 0.f;
         };
         float nl = 0.f, nd = 0.f;
         if (hf == 0) fetch(0, nl, nd);
-        for (int i = 0; i < nq; ++i) {
+        for (int i = 0; i < niter; ++i) {
             const int s = i & 1;
-            const int q0 = (kt + i) * BW_T;
+            const int qi = i % nq;
+            const int q0 = (kt + qi) * BW_T;
             if (hf == 0) {
                 sL[s * BW_T + r] = nl;
                 sD[s * BW_T + r] = nd;
@@ -931,7 +945,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_after();
             // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
             // rows past T belong to the next sequence)
-            const bool edge = i == 0 || q0 + BW_T > T;
+            const bool edge = qi == 0 || q0 + BW_T > T;
             const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + hf * 64);
             const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + hf * 64);
             {
@@ -971,16 +985,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_before();
             mbar_arrive(p_full);
         }
-        mbar_wait(g_done, (nq - 1) & 1);
+        mbar_wait(g_done, (niter - 1) & 1);
         tc_after();
         uint32_t o[32];  // this warp's 32 of the 64 output columns
-        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * T + key) * (3 * d) + h * HD + hf * 32;
+        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * T + key) * ldq + hf * 32;
         tmem_ld32(tDV + lane_off + hf * 32, o);
         tmem_wait_ld();
-        if (key < T) st_row32_global(dst + 2 * d, o, 1.f);
+        if (key < T) st_row32_global(dst + vc, o, 1.f);
         tmem_ld32(tDK + lane_off + hf * 32, o);
         tmem_wait_ld();
-        if (key < T) st_row32_global(dst + d, o, scale);
+        if (key < T) st_row32_global(dst + kc, o, scale);
     }
     tc_before();
     __syncthreads();
@@ -998,7 +1012,7 @@ constexpr int DQ_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + BW_SQ + 256;
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                 int T, int H, float scale) {
+                 int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
@@ -1020,6 +1034,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int qt = nt - 1 - blockIdx.x;
     const int bh = blockIdx.y, b = bh / H, h = bh % H;
     const int d = H * HD;
+    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;  // this head's K / V columns
     const int q0 = qt * BW_T;
     const int row_base = b * T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1058,8 +1074,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = j & 1;
                 mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
-                tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], d + h * HD, row_base + j * BW_T);
-                tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], 2 * d + h * HD, row_base + j * BW_T);
+                tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], kc, row_base + j * BW_T);
+                tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], vc, row_base + j * BW_T);
             }
         }
     } else if (warp == 1) {
@@ -1149,7 +1165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t o[32];
         tmem_ld32(tDQ + lane_off + hf * 32, o);
         tmem_wait_ld();
-        if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(b) * T + q) * (3 * d) + h * HD + hf * 32, o, scale);
+        if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(b) * T + q) * ldq + h * HD + hf * 32, o, scale);
     }
     tc_before();
     __syncthreads();
@@ -1190,22 +1206,34 @@ CUtensorMap rows_map(const void* p, int64_t cols, int64_t rows, int64_t ld) {
     return m;
 }
 
-// D[bh, t] = sum_c dO[t, c] O[t, c] (one warp per row of 64)
+// D[bh, t] = sum_c dO[t, c] O[t, c]. y / dy are read as one flat stream of
+// 64-element head rows in memory order (token-major, head-minor): 8 threads
+// per row, 16 B each, 3-step shuffle reduction.
 __global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dy,
                                float* __restrict__ dsum, int B, int T, int H) {
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (row >= static_cast<int64_t>(B) * H * T) return;
-    const int t = static_cast<int>(row % T);
-    const int bh = static_cast<int>(row / T);
-    const int b = bh / H, h = bh % H;
-    const int64_t o = (static_cast<int64_t>(b) * T + t) * (H * HD) + h * HD + lane * 2;
-    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(y + o);
-    const __nv_bfloat162 g = *reinterpret_cast<const __nv_bfloat162*>(dy + o);
-    float s = __bfloat162float(a.x) * __bfloat162float(g.x) + __bfloat162float(a.y) * __bfloat162float(g.y);
+    const int64_t nrow = static_cast<int64_t>(B) * T * H;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t row = i >> 3;  // (b*T + t)*H + h
+    float s = 0.f;
+    if (row < nrow) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(y) + i);
+        const uint4 g = __ldg(reinterpret_cast<const uint4*>(dy) + i);
+        const uint32_t wa[4] = {a.x, a.y, a.z, a.w}, wg[4] = {g.x, g.y, g.z, g.w};
 #pragma unroll
-    for (int w = 16; w > 0; w >>= 1) s += __shfl_xor_sync(0xffffffffu, s, w);
-    if (lane == 0) dsum[row] = s;
+        for (int k = 0; k < 4; ++k) {
+            s = fmaf(__uint_as_float(wa[k] << 16), __uint_as_float(wg[k] << 16), s);
+            s = fmaf(__uint_as_float(wa[k] & 0xffff0000u), __uint_as_float(wg[k] & 0xffff0000u), s);
+        }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (row < nrow && (threadIdx.x & 7) == 0) {
+        const int h = static_cast<int>(row % H);
+        const int64_t bt = row / H;
+        const int t = static_cast<int>(bt % T), b = static_cast<int>(bt / T);
+        dsum[(static_cast<int64_t>(b) * H + h) * T + t] = s;
+    }
 }
 
 bool tc_applicable(const void* a, const void* b, int hd) {
@@ -1216,14 +1244,15 @@ bool tc_applicable(const void* a, const void* b, int hd) {
 }  // namespace
 
 bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse, const __nv_bfloat16* dy,
-                      __nv_bfloat16* dqkv, float* dsum, int B, int T, int H, int hd, cudaStream_t s) {
+                      __nv_bfloat16* dqkv, float* dsum, int B, int T, int H, int Hkv, int hd, cudaStream_t s) {
     if (!tc_applicable(qkv, dy, hd) || !tc_applicable(y, dqkv, hd)) return false;
     const int d = H * HD;
+    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     const int64_t rows = static_cast<int64_t>(B) * T;
     const int64_t nrow = rows * H;
-    dsum_tc_kernel<<<static_cast<int>((nrow + 7) / 8), 256, 0, s>>>(y, dy, dsum, B, T, H);
+    dsum_tc_kernel<<<static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s>>>(y, dy, dsum, B, T, H);
     ACCO_CHECK_LAUNCH();
-    CUtensorMap mq = rows_map(qkv, 3 * d, rows, 3 * d);
+    CUtensorMap mq = rows_map(qkv, ldq, rows, ldq);
     CUtensorMap mo = rows_map(dy, d, rows, d);
     static bool cfg = false;
     if (!cfg) {
@@ -1232,21 +1261,22 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
         cfg = true;
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
-    dim3 grid((T + BW_T - 1) / BW_T, B * H);
-    fa_bwd_dkv_tc<<<grid, kThreads, DKV_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, scale);
+    const int nt = (T + BW_T - 1) / BW_T;
+    fa_bwd_dkv_tc<<<dim3(nt, B * Hkv), kThreads, DKV_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
-    fa_bwd_dq_tc<<<grid, kThreads, DQ_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, scale);
+    fa_bwd_dq_tc<<<dim3(nt, B * H), kThreads, DQ_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
     return true;
 }
 
-// qkv: [B*T, 3*d] bf16 (q | k | v, head h at columns h*64); returns false if
-// the tensor-core path does not apply (head size, alignment).
-bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int T, int H, int hd,
+// qkv: [B*T, (H + 2*Hkv)*64] bf16 (H q heads | Hkv k heads | Hkv v heads);
+// returns false if the tensor-core path does not apply (head size, alignment).
+bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int T, int H, int Hkv, int hd,
                       cudaStream_t s) {
     if (!tc_applicable(qkv, y, hd)) return false;
     const int d = H * HD;
-    CUtensorMap m = rows_map(qkv, 3 * d, static_cast<int64_t>(B) * T, 3 * d);
+    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    CUtensorMap m = rows_map(qkv, ldq, static_cast<int64_t>(B) * T, ldq);
     static bool cfg = false;
     if (!cfg) {
         ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
@@ -1256,9 +1286,9 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nqt = (T + BQ - 1) / BQ;
     if (std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
-        fa_fwd_tc<<<dim3(nqt, B * H), kThreads, SMEM, s>>>(m, y, lse, T, H, scale);
+        fa_fwd_tc<<<dim3(nqt, B * H), kThreads, SMEM, s>>>(m, y, lse, T, H, Hkv, scale);
     } else {
-        fa_fwd_tc2<<<dim3((nqt + 1) / 2, B * H), kThreads, F2_SMEM, s>>>(m, y, lse, T, H, scale);
+        fa_fwd_tc2<<<dim3((nqt + 1) / 2, B * H), kThreads, F2_SMEM, s>>>(m, y, lse, T, H, Hkv, scale);
     }
     ACCO_CHECK_LAUNCH();
     return true;

@@ -35,6 +35,10 @@ LMConfig to_lm(const acco_lm_cfg& c) {
     l.precision = c.precision;
     l.max_batch = c.max_batch;
     l.host_data = c.host_data;
+    l.arch = c.arch;
+    l.n_kv_head = c.n_kv_head;
+    l.d_ff = c.d_ff;
+    l.rope_base = c.rope_base;
     return l;
 }
 SimCfg to_sim(const acco_sim_cfg* sim) {

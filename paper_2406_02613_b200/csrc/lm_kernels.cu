@@ -46,15 +46,21 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const T* __res
     const int m = blockIdx.x;
     const int t = m % seq;
     const T* e = wte + static_cast<int64_t>(tok[m]) * d;
-    const T* p = wpe + static_cast<int64_t>(t) * d;
     T* o = x + static_cast<int64_t>(m) * d;
+    if (wpe == nullptr) {  // Llama: no learned positions (RoPE in attention)
+        for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = e[c];
+        return;
+    }
+    const T* p = wpe + static_cast<int64_t>(t) * d;
     for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = from_f<T>(to_f(e[c]) + to_f(p[c]));
 }
 
 // ----------------------------------------------------------------- layernorm
 constexpr float kLnEps = 1e-5f;
 
-template <class T>
+// RMS = true: RMSNorm (Llama): mean fixed at 0 (stored as 0, so the LN
+// parameter-gradient kernels compute xhat = x * rstd unchanged), no bias.
+template <class T, bool RMS>
 __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
                               T* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd,
                               int M, int d) {
@@ -63,8 +69,9 @@ __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, 
     if (row >= M) return;
     const T* xr = x + static_cast<int64_t>(row) * d;
     float s = 0.f;
-    for (int c = lane; c < d; c += 32) s += to_f(xr[c]);
-    const float mu = warp_sum(s) / d;
+    if (!RMS)
+        for (int c = lane; c < d; c += 32) s += to_f(xr[c]);
+    const float mu = RMS ? 0.f : warp_sum(s) / d;
     float v = 0.f;
     for (int c = lane; c < d; c += 32) {
         float t = to_f(xr[c]) - mu;
@@ -73,14 +80,14 @@ __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, 
     const float rs = rsqrtf(warp_sum(v) / d + kLnEps);
     T* yr = y + static_cast<int64_t>(row) * d;
     for (int c = lane; c < d; c += 32)
-        yr[c] = from_f<T>((to_f(xr[c]) - mu) * rs * to_f(g[c]) + to_f(b[c]));
+        yr[c] = from_f<T>((to_f(xr[c]) - mu) * rs * to_f(g[c]) + (RMS ? 0.f : to_f(b[c])));
     if (lane == 0) {
         mean[row] = mu;
         rstd[row] = rs;
     }
 }
 
-template <class T>
+template <class T, bool RMS>
 __global__ void ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ g,
                               const float* __restrict__ mean, const float* __restrict__ rstd,
                               T* __restrict__ dx, int accumulate, int M, int d) {
@@ -96,7 +103,7 @@ __global__ void ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
         s1 += dxh;
         s2 += dxh * xh;
     }
-    s1 = warp_sum(s1) / d;
+    s1 = RMS ? 0.f : warp_sum(s1) / d;
     s2 = warp_sum(s2) / d;
     for (int c = lane; c < d; c += 32) {
         float xh = (to_f(x[o + c]) - mu) * rs;
@@ -127,7 +134,7 @@ __device__ __forceinline__ uint4 pack8b(const float* v) {
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int CH>
+template <int CH, bool RMS>
 __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                            const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
                            float* __restrict__ rstd, int M) {
@@ -140,9 +147,11 @@ __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloa
 #pragma unroll
     for (int i = 0; i < CH; ++i) unpack8b(xr[lane + 32 * i], v + 8 * i);
     float s = 0.f;
+    if (!RMS) {
 #pragma unroll
-    for (int i = 0; i < CH * 8; ++i) s += v[i];
-    const float mu = warp_sum(s) / d;
+        for (int i = 0; i < CH * 8; ++i) s += v[i];
+    }
+    const float mu = RMS ? 0.f : warp_sum(s) / d;
     float q = 0.f;
 #pragma unroll
     for (int i = 0; i < CH * 8; ++i) q += (v[i] - mu) * (v[i] - mu);
@@ -150,9 +159,9 @@ __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloa
     uint4* yr = reinterpret_cast<uint4*>(y + static_cast<int64_t>(row) * d);
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
-        float gv[8], bv[8], o[8];
+        float gv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
         unpack8b(reinterpret_cast<const uint4*>(g)[lane + 32 * i], gv);
-        unpack8b(reinterpret_cast<const uint4*>(b)[lane + 32 * i], bv);
+        if (!RMS) unpack8b(reinterpret_cast<const uint4*>(b)[lane + 32 * i], bv);
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = (v[8 * i + k] - mu) * rs * gv[k] + bv[k];
         yr[lane + 32 * i] = pack8b(o);
@@ -163,7 +172,7 @@ __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloa
     }
 }
 
-template <int CH>
+template <int CH, bool RMS>
 __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                            const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
                            const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx, int accumulate, int M) {
@@ -194,7 +203,7 @@ __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bflo
         s1 += dxh[i];
         s2 += dxh[i] * xh[i];
     }
-    s1 = warp_sum(s1) / d;
+    s1 = RMS ? 0.f : warp_sum(s1) / d;
     s2 = warp_sum(s2) / d;
     uint4* dxr = reinterpret_cast<uint4*>(dx + o);
 #pragma unroll
@@ -235,7 +244,7 @@ __global__ void colreduce_partial(const T* __restrict__ y, int64_t ld, const T* 
             } else {
                 float xh = (to_f(x[static_cast<int64_t>(r) * N + col]) - mean[r]) * rstd[r];
                 a0 += dy * xh;
-                a1 += dy;
+                if (KIND == 1) a1 += dy;
             }
         }
     }
@@ -259,7 +268,7 @@ __global__ void colreduce_partial(const T* __restrict__ y, int64_t ld, const T* 
 // lanes. Partial sums per chunk go to `part`; the last block of a slab (atomic
 // ticket) folds the chunks in ascending order and adds into out (+ out1) —
 // deterministic, one launch. KIND 0: sum y; KIND 1 (LayerNorm params):
-// out += sum dy*xhat, out1 += sum dy.
+// out += sum dy*xhat, out1 += sum dy; KIND 2 (RMSNorm weight): out += sum dy*xhat.
 constexpr int kVecRows = 32;
 
 template <class T>
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     a0[k] += dy[k] * ((xv[k] - mu) * rs);
-                    a1[k] += dy[k];
+                    if (KIND == 1) a1[k] += dy[k];
                 }
             }
         }
@@ -660,6 +669,130 @@ __global__ void spin_kernel(uint64_t ns) {
     }
 }
 
+// ------------------------------------------------------ rotary / SwiGLU (Llama)
+// In place on the q|k columns of qkv [M, ld]: nh = n_head + n_kv_head heads
+// of hd columns from column 0. Pair (i, i + hd/2), angle table cs[t][i] =
+// (cos, sin) (host fp64, rounded to fp32). dir = +1 rotates (forward);
+// dir = -1 applies the transpose (backward of the rotation on dq, dk).
+template <class T>
+__global__ void rope_kernel(T* __restrict__ qkv, int64_t ld, const float2* __restrict__ cs, int M, int seq, int nh,
+                            int hd, float dir) {
+    const int h2 = hd / 2;
+    const int64_t n = static_cast<int64_t>(M) * nh * h2;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(i % h2);
+        const int64_t mh = i / h2;
+        const int head = static_cast<int>(mh % nh);
+        const int m = static_cast<int>(mh / nh);
+        const float2 c = cs[static_cast<int64_t>(m % seq) * h2 + j];
+        const float sn = dir * c.y;
+        T* p = qkv + static_cast<int64_t>(m) * ld + head * hd + j;
+        const float x1 = to_f(p[0]), x2 = to_f(p[h2]);
+        p[0] = from_f<T>(x1 * c.x - x2 * sn);
+        p[h2] = from_f<T>(x2 * c.x + x1 * sn);
+    }
+}
+
+// bf16, 8 pairs per thread (16 B loads of each half)
+__global__ void rope_vec_kernel(__nv_bfloat16* __restrict__ qkv, int64_t ld, const float2* __restrict__ cs, int M,
+                                int seq, int nh, int hd, float dir) {
+    const int h2 = hd / 2, nv = h2 / 8;
+    const int64_t n = static_cast<int64_t>(M) * nh * nv;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int j0 = static_cast<int>(i % nv) * 8;
+        const int64_t mh = i / nv;
+        const int head = static_cast<int>(mh % nh);
+        const int m = static_cast<int>(mh / nh);
+        const float2* c = cs + static_cast<int64_t>(m % seq) * h2 + j0;
+        __nv_bfloat16* p = qkv + static_cast<int64_t>(m) * ld + head * hd + j0;
+        float a[8], b[8], ya[8], yb[8];
+        unpack8b(*reinterpret_cast<const uint4*>(p), a);
+        unpack8b(*reinterpret_cast<const uint4*>(p + h2), b);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float2 t = c[k];
+            const float sn = dir * t.y;
+            ya[k] = a[k] * t.x - b[k] * sn;
+            yb[k] = b[k] * t.x + a[k] * sn;
+        }
+        *reinterpret_cast<uint4*>(p) = pack8b(ya);
+        *reinterpret_cast<uint4*>(p + h2) = pack8b(yb);
+    }
+}
+
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+// a[m, j] = silu(gu[m, j]) * gu[m, F + j]
+template <class T>
+__global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ a, int M, int F) {
+    const int64_t n = static_cast<int64_t>(M) * F;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t m = i / F;
+        const int j = static_cast<int>(i % F);
+        const float g = to_f(gu[m * 2 * F + j]), u = to_f(gu[m * 2 * F + F + j]);
+        a[i] = from_f<T>(g * sigmoid_f(g) * u);
+    }
+}
+
+// dgu[m, j] = da * u * s * (1 + g (1 - s)),  dgu[m, F + j] = da * g * s
+template <class T>
+__global__ void swiglu_bwd_kernel(const T* __restrict__ da, const T* __restrict__ gu, T* __restrict__ dgu, int M,
+                                  int F) {
+    const int64_t n = static_cast<int64_t>(M) * F;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t m = i / F;
+        const int j = static_cast<int>(i % F);
+        const float g = to_f(gu[m * 2 * F + j]), u = to_f(gu[m * 2 * F + F + j]), d = to_f(da[i]);
+        const float sg = sigmoid_f(g);
+        dgu[m * 2 * F + j] = from_f<T>(d * u * sg * (1.0f + g * (1.0f - sg)));
+        dgu[m * 2 * F + F + j] = from_f<T>(d * g * sg);
+    }
+}
+
+// bf16, 8 columns per thread (F % 8 == 0)
+__global__ void swiglu_fwd_vec(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ a, int M, int F) {
+    const int fv = F / 8;
+    const int64_t n = static_cast<int64_t>(M) * fv;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t m = i / fv;
+        const int j = static_cast<int>(i % fv) * 8;
+        float g[8], u[8], o[8];
+        unpack8b(*reinterpret_cast<const uint4*>(gu + m * 2 * F + j), g);
+        unpack8b(*reinterpret_cast<const uint4*>(gu + m * 2 * F + F + j), u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = g[k] * sigmoid_f(g[k]) * u[k];
+        *reinterpret_cast<uint4*>(a + m * F + j) = pack8b(o);
+    }
+}
+
+__global__ void swiglu_bwd_vec(const __nv_bfloat16* __restrict__ da, const __nv_bfloat16* __restrict__ gu,
+                               __nv_bfloat16* __restrict__ dgu, int M, int F) {
+    const int fv = F / 8;
+    const int64_t n = static_cast<int64_t>(M) * fv;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t m = i / fv;
+        const int j = static_cast<int>(i % fv) * 8;
+        float g[8], u[8], d[8], dg[8], du[8];
+        unpack8b(*reinterpret_cast<const uint4*>(gu + m * 2 * F + j), g);
+        unpack8b(*reinterpret_cast<const uint4*>(gu + m * 2 * F + F + j), u);
+        unpack8b(*reinterpret_cast<const uint4*>(da + m * F + j), d);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float sg = sigmoid_f(g[k]);
+            dg[k] = d[k] * u[k] * sg * (1.0f + g[k] * (1.0f - sg));
+            du[k] = d[k] * g[k] * sg;
+        }
+        *reinterpret_cast<uint4*>(dgu + m * 2 * F + j) = pack8b(dg);
+        *reinterpret_cast<uint4*>(dgu + m * 2 * F + F + j) = pack8b(du);
+    }
+}
+
 int grid_for(int64_t n, int threads = 256) {
     int64_t b = (n + threads - 1) / threads;
     int64_t cap = static_cast<int64_t>(num_sms()) * 8;
@@ -685,39 +818,48 @@ void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int 
 
 static bool a16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-template <class T>
-void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
-                   cudaStream_t s) {
-    ProfScope prof(kProfNorm, 2.0 * M * d * sizeof(T) + 8.0 * M, s);
+template <bool RMS, class T>
+static void layernorm_fwd_impl(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
+                               cudaStream_t s) {
     if constexpr (sizeof(T) == 2) {
         if (a16(x) && a16(g) && a16(b) && a16(y) && d % 256 == 0) {
             const int grid = ceil_div(M, 8);
             switch (d / 256) {
-                case 1: ln_fwd_vec<1><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 2: ln_fwd_vec<2><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 3: ln_fwd_vec<3><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 4: ln_fwd_vec<4><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 8: ln_fwd_vec<8><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 1: ln_fwd_vec<1, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 2: ln_fwd_vec<2, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 3: ln_fwd_vec<3, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 4: ln_fwd_vec<4, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 8: ln_fwd_vec<8, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
                 default: break;
             }
         }
     }
-    ln_fwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(x, g, b, y, mean, rstd, M, d);
+    ln_fwd_kernel<T, RMS><<<ceil_div(M, 8), 256, 0, s>>>(x, g, b, y, mean, rstd, M, d);
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
+void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
+                   cudaStream_t s, bool rms) {
+    ProfScope prof(kProfNorm, 2.0 * M * d * sizeof(T) + 8.0 * M, s);
+    if (rms)
+        layernorm_fwd_impl<true>(x, g, static_cast<const T*>(nullptr), y, mean, rstd, M, d, s);
+    else
+        layernorm_fwd_impl<false>(x, g, b, y, mean, rstd, M, d, s);
+}
+
+template <bool RMS, class T>
 static bool ln_bwd_dx_vec(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
                           bool accumulate_dx, int M, int d, cudaStream_t s) {
     if constexpr (sizeof(T) == 2) {
         if (a16(dy) && a16(x) && a16(g) && a16(dx) && d % 256 == 0) {
             const int grid = ceil_div(M, 8), acc = accumulate_dx ? 1 : 0;
             switch (d / 256) {
-                case 1: ln_bwd_vec<1><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 2: ln_bwd_vec<2><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 3: ln_bwd_vec<3><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 4: ln_bwd_vec<4><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 8: ln_bwd_vec<8><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 1: ln_bwd_vec<1, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 2: ln_bwd_vec<2, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 3: ln_bwd_vec<3, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 4: ln_bwd_vec<4, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 8: ln_bwd_vec<8, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
                 default: return false;
             }
             ACCO_CHECK_LAUNCH();
@@ -760,28 +902,41 @@ template <class T>
 void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* gdst, float* bdst,
                           float* scratch, int M, int d, bool acc, cudaStream_t s) {
     ProfScope prof(kProfReduce, 2.0 * M * d * sizeof(T) + 8.0 * M, s);
+    // bdst == nullptr: RMSNorm (weight only)
     if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d)) {
-        colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, acc, s);
+        if (bdst)
+            colsum_vec<T, 1>(dy, d, x, mean, rstd, M, d, gdst, bdst, scratch, acc, s);
+        else
+            colsum_vec<T, 2>(dy, d, x, mean, rstd, M, d, gdst, nullptr, scratch, acc, s);
         return;
     }
     const int nchunk = ceil_div(M, kColChunk);
     float* p0 = scratch;
     float* p1 = scratch + static_cast<int64_t>(nchunk) * d;
-    colreduce_partial<T, 1><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd, M,
-                                                                                         d, p0, p1);
+    if (bdst)
+        colreduce_partial<T, 1><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd,
+                                                                                             M, d, p0, p1);
+    else
+        colreduce_partial<T, 2><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd,
+                                                                                             M, d, p0, p1);
     ACCO_CHECK_LAUNCH();
     colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p0, nchunk, d, gdst, acc ? 1 : 0);
-    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst, acc ? 1 : 0);
+    if (bdst) colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst, acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
 void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
-                      bool accumulate_dx, int M, int d, cudaStream_t s) {
+                      bool accumulate_dx, int M, int d, cudaStream_t s, bool rms) {
     ProfScope prof(kProfNorm, 3.0 * M * d * sizeof(T) + 8.0 * M, s);
-    if (vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d) && ln_bwd_dx_vec<T>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s))
-        return;
-    ln_bwd_kernel<T><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+    const bool v = vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d);
+    if (rms) {
+        if (v && ln_bwd_dx_vec<true>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) return;
+        ln_bwd_kernel<T, true><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+    } else {
+        if (v && ln_bwd_dx_vec<false>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) return;
+        ln_bwd_kernel<T, false><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+    }
     ACCO_CHECK_LAUNCH();
 }
 
@@ -824,7 +979,7 @@ void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_
 
 template <class T>
 void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
-               uint32_t* sort_scratch, bool acc_wpe, cudaStream_t s) {
+               uint32_t* sort_scratch, bool acc_wpe, cudaStream_t s, bool zero_wte) {
     ProfScope prof(kProfEmbed, 1.0 * M * d * sizeof(T), s);
     ACCO_REQUIRE(static_cast<uint64_t>(V) * static_cast<uint64_t>(M) < 0xffffffffull,
                  "embed_bwd: vocab * tokens exceeds the 32-bit sort key");
@@ -838,9 +993,59 @@ void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, fl
     }
     sort_keys_kernel<<<1, 1024, P * 4, s>>>(tok, M, P, sort_scratch);
     ACCO_CHECK_LAUNCH();
+    // untied embedding (Llama) on the stage's first micro-batch: no earlier
+    // kernel wrote grad_wte, so the rows no token touches must be zeroed
+    if (zero_wte) ACCO_CUDA(cudaMemsetAsync(grad_wte, 0, static_cast<size_t>(V) * d * sizeof(float), s));
     embed_bwd_wte_kernel<T><<<M, 128, 0, s>>>(sort_scratch, M, dx, d, grad_wte);
     ACCO_CHECK_LAUNCH();
-    embed_bwd_wpe_kernel<T><<<seq, 128, 0, s>>>(dx, M / seq, seq, d, grad_wpe, acc_wpe ? 1 : 0);
+    if (grad_wpe) {
+        embed_bwd_wpe_kernel<T><<<seq, 128, 0, s>>>(dx, M / seq, seq, d, grad_wpe, acc_wpe ? 1 : 0);
+        ACCO_CHECK_LAUNCH();
+    }
+}
+
+template <class T>
+void rope_apply(T* qkv, int64_t ld, const float2* cs, int M, int seq, int nh, int hd, bool inverse, cudaStream_t s) {
+    ProfScope prof(kProfOther, 4.0 * M * nh * hd * sizeof(T), s);
+    ACCO_REQUIRE(hd % 2 == 0, "rope: head size must be even");
+    const float dir = inverse ? -1.0f : 1.0f;
+    if constexpr (sizeof(T) == 2) {
+        if ((hd / 2) % 8 == 0 && ld % 8 == 0 && a16(qkv)) {
+            const int64_t n = static_cast<int64_t>(M) * nh * (hd / 16);
+            rope_vec_kernel<<<grid_for(n), 256, 0, s>>>(qkv, ld, cs, M, seq, nh, hd, dir);
+            ACCO_CHECK_LAUNCH();
+            return;
+        }
+    }
+    rope_kernel<T><<<grid_for(static_cast<int64_t>(M) * nh * (hd / 2)), 256, 0, s>>>(qkv, ld, cs, M, seq, nh, hd, dir);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void swiglu_fwd(const T* gu, T* a, int M, int F, cudaStream_t s) {
+    ProfScope prof(kProfOther, 3.0 * M * F * sizeof(T), s);
+    if constexpr (sizeof(T) == 2) {
+        if (F % 8 == 0 && a16(gu) && a16(a)) {
+            swiglu_fwd_vec<<<grid_for(static_cast<int64_t>(M) * F / 8), 256, 0, s>>>(gu, a, M, F);
+            ACCO_CHECK_LAUNCH();
+            return;
+        }
+    }
+    swiglu_fwd_kernel<T><<<grid_for(static_cast<int64_t>(M) * F), 256, 0, s>>>(gu, a, M, F);
+    ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void swiglu_bwd(const T* da, const T* gu, T* dgu, int M, int F, cudaStream_t s) {
+    ProfScope prof(kProfOther, 5.0 * M * F * sizeof(T), s);
+    if constexpr (sizeof(T) == 2) {
+        if (F % 8 == 0 && a16(gu) && a16(da) && a16(dgu)) {
+            swiglu_bwd_vec<<<grid_for(static_cast<int64_t>(M) * F / 8), 256, 0, s>>>(da, gu, dgu, M, F);
+            ACCO_CHECK_LAUNCH();
+            return;
+        }
+    }
+    swiglu_bwd_kernel<T><<<grid_for(static_cast<int64_t>(M) * F), 256, 0, s>>>(da, gu, dgu, M, F);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -919,15 +1124,19 @@ void spin_ns(uint64_t ns, cudaStream_t s) {
 
 #define ACCO_INST(T)                                                                                          \
     template void embed_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);          \
-    template void layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, cudaStream_t); \
+    template void layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, cudaStream_t,  \
+                                   bool);                                                                     \
     template void layernorm_bwd_params<T>(const T*, const T*, const float*, const float*, float*, float*,      \
                                           float*, int, int, bool, cudaStream_t);                              \
     template void layernorm_bwd_dx<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, int, \
-                                      int, cudaStream_t);                                                     \
+                                      int, cudaStream_t, bool);                                               \
     template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);             \
     template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
     template void embed_bwd<T>(const int32_t*, const T*, int, int, int, int, float*, float*, uint32_t*,      \
-                               bool, cudaStream_t);
+                               bool, cudaStream_t, bool);                                                     \
+    template void rope_apply<T>(T*, int64_t, const float2*, int, int, int, int, bool, cudaStream_t);          \
+    template void swiglu_fwd<T>(const T*, T*, int, int, cudaStream_t);                                        \
+    template void swiglu_bwd<T>(const T*, const T*, T*, int, int, cudaStream_t);
 ACCO_INST(float)
 ACCO_INST(__nv_bfloat16)
 #undef ACCO_INST

@@ -18,19 +18,22 @@ template <class T>
 void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int seq, int d,
                cudaStream_t s);
 
+// rms = true: RMSNorm (Llama; b unused, mean stored as 0 so the parameter
+// reduction below computes xhat = x * rstd unchanged).
 template <class T>
 void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int M, int d,
-                   cudaStream_t s);
+                   cudaStream_t s, bool rms = false);
 
 // LN backward, split so the parameter reductions can run on a side stream:
-// dg/db (+)= sum_rows dy * xhat, dy into fp32 gdst/bdst (uses `scratch`) ...
+// dg/db (+)= sum_rows dy * xhat, dy into fp32 gdst/bdst (uses `scratch`;
+// bdst == nullptr: RMSNorm, weight only) ...
 template <class T>
 void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* gdst,
                           float* bdst, float* scratch, int M, int d, bool accumulate_params, cudaStream_t s);
 // ... and dx (+)= the input gradient.
 template <class T>
 void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
-                      bool accumulate_dx, int M, int d, cudaStream_t s);
+                      bool accumulate_dx, int M, int d, cudaStream_t s, bool rms = false);
 
 // out[c] += sum_r y[r*ld + c] (deterministic two-level), fp32 out.
 template <class T>
@@ -47,16 +50,32 @@ void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, i
 void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s);
 
 // Embedding backward: grad_wte[tok[m]] += dx[m] (sorted segments, ascending m),
-// grad_wpe[t] += sum_b dx[b*seq + t].
+// grad_wpe[t] += sum_b dx[b*seq + t] (skipped when grad_wpe == nullptr);
+// zero_wte: grad_wte is zeroed first (untied embedding, first micro-batch).
 template <class T>
 void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte,
-               float* grad_wpe, uint32_t* sort_scratch, bool accumulate_wpe, cudaStream_t s);
+               float* grad_wpe, uint32_t* sort_scratch, bool accumulate_wpe, cudaStream_t s,
+               bool zero_wte = false);
 
+// Rotary embedding in place on the first nh heads (q then k) of qkv [M, ld]:
+// pairs (i, i + hd/2), cs[t][i] = (cos, sin); inverse = the transpose (bwd).
 template <class T>
-void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int hd, cudaStream_t s);
+void rope_apply(T* qkv, int64_t ld, const float2* cs, int M, int seq, int nh, int hd, bool inverse,
+                cudaStream_t s);
+// SwiGLU: a[M, F] = silu(gu[:, :F]) * gu[:, F:]; backward dgu[M, 2F] from da.
+template <class T>
+void swiglu_fwd(const T* gu, T* a, int M, int F, cudaStream_t s);
+template <class T>
+void swiglu_bwd(const T* da, const T* gu, T* dgu, int M, int F, cudaStream_t s);
+
+// Causal attention over qkv [B*seq, (H + 2*Hkv)*hd] (q heads, then Hkv k
+// heads, then Hkv v heads; query head h reads KV head h / (H / Hkv)), y and
+// dy [B*seq, H*hd]; dqkv has qkv's layout. Hkv == H: plain MHA (GPT-2).
+template <class T>
+void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int Hkv, int hd, cudaStream_t s);
 template <class T>
 void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, float* dsum,
-                   int B, int seq, int H, int hd, cudaStream_t s);
+                   int B, int seq, int H, int Hkv, int hd, cudaStream_t s);
 
 // ---- engine utilities
 void fill_i64(int64_t* p, int64_t v, cudaStream_t s);

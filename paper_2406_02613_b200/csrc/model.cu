@@ -22,6 +22,21 @@ std::vector<ParamSpec> lm_param_layout(const LMConfig& c) {
         v.push_back({n, r, cc, kind, off});
     };
     add("wte", c.vocab, d, 0);
+    if (c.arch == 1) {  // oracle/gpt_oracle.py param_layout, arch="llama"
+        const int64_t hd = d / c.n_head, nqkv = (c.n_head + 2 * c.kv_heads()) * hd, F = c.ffn();
+        for (int l = 0; l < c.n_layer; ++l) {
+            const std::string p = "layers." + std::to_string(l) + ".";
+            add(p + "attention_norm.weight", d, 1, 2);
+            add(p + "attention.wqkv", nqkv, d, 0);
+            add(p + "attention.wo", d, c.n_head * hd, 1);
+            add(p + "ffn_norm.weight", d, 1, 2);
+            add(p + "feed_forward.w_gate_up", 2 * F, d, 0);
+            add(p + "feed_forward.w_down", d, F, 1);
+        }
+        add("norm.weight", d, 1, 2);
+        add("output.weight", c.vocab, d, 0);
+        return v;
+    }
     add("wpe", c.seq_len, d, 0);
     for (int l = 0; l < c.n_layer; ++l) {
         const std::string p = "h." + std::to_string(l) + ".";
@@ -97,16 +112,29 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_REQUIRE(c.d_model % 8 == 0, "lm config: d_model must be a multiple of 8 (TMA alignment)");
     ACCO_REQUIRE(c.n_samples >= 1 && c.max_batch >= 1, "lm config: n_samples, max_batch >= 1");
     ACCO_REQUIRE(c.precision == 0 || c.precision == 1, "lm config: precision must be fp32 or bf16");
+    ACCO_REQUIRE(c.arch == 0 || c.arch == 1, "lm config: arch must be 0 (gpt2) or 1 (llama)");
+    if (c.arch == 1) {
+        ACCO_REQUIRE(c.kv_heads() >= 1 && c.n_head % c.kv_heads() == 0,
+                     "lm config: n_head must be a multiple of n_kv_head");
+        ACCO_REQUIRE((c.d_model / c.n_head) % 2 == 0, "lm config: rotary embeddings need an even head size");
+        ACCO_REQUIRE(c.ffn() % 8 == 0, "lm config: d_ff must be a multiple of 8 (TMA alignment)");
+    } else {
+        ACCO_REQUIRE(c.n_kv_head == 0 || c.n_kv_head == c.n_head, "lm config: gpt2 has no grouped-query attention");
+    }
     layout_ = lm_param_layout(c);
     psi_ = layout_.back().off + layout_.back().numel();
     vpad_ = (c.vocab + 63) / 64 * 64;
     const int64_t M = static_cast<int64_t>(c.max_batch) * c.seq_len;
     const int64_t d = c.d_model, L = c.n_layer, H = c.n_head;
     const size_t e = act_bytes();
+    const bool llama = c.arch == 1;
+    const int64_t nqkv = llama ? (H + 2 * c.kv_heads()) * (d / H) : 3 * d;
+    const int64_t F = c.ffn();
     auto sz = [&](int slot) -> int64_t {
         switch (slot) {
-            case sQKV: return 3 * d;
-            case sA: case sU: return 4 * d;
+            case sQKV: return nqkv;
+            case sA: return llama ? 2 * F : 4 * d;  // llama: gate|up pre-activation
+            case sU: return llama ? F : 4 * d;      // MLP activation (gelu / swiglu output)
             default: return d;
         }
     };
@@ -119,8 +147,9 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     cols.push_back(vpad_);      // logits
     cols.push_back(d);          // dx
     cols.push_back(d);          // dt
-    cols.push_back(3 * d);      // dqkv
-    cols.push_back(4 * d);      // da
+    cols.push_back(nqkv);       // dqkv
+    cols.push_back(llama ? 2 * F : 4 * d);  // da (llama: d(gate|up))
+    cols.push_back(llama ? F : 0);          // llama: d(swiglu output)
     size_t total = 0;
     std::vector<size_t> offs;
     for (int64_t cc : cols) {
@@ -155,6 +184,19 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     // 8 x SMs) (see colsum_vec / colreduce in lm_kernels.cu)
     const int64_t nchunk = std::max<int64_t>((M + 255) / 256, 8 * num_sms());
     ACCO_CUDA(cudaMalloc(&scratch_, nchunk * 4 * d * 2 * sizeof(float)));
+    if (llama) {  // rotary table, fp64 angles rounded to fp32 (oracle rope_table)
+        const int hd = c.d_model / c.n_head, h2 = hd / 2;
+        std::vector<float2> tab(static_cast<size_t>(c.seq_len) * h2);
+        for (int t = 0; t < c.seq_len; ++t)
+            for (int i = 0; i < h2; ++i) {
+                const double inv = std::pow(c.rope(), -2.0 * i / hd);
+                const double a = static_cast<double>(t) * inv;
+                tab[static_cast<size_t>(t) * h2 + i] = make_float2(static_cast<float>(std::cos(a)),
+                                                                   static_cast<float>(std::sin(a)));
+            }
+        ACCO_CUDA(cudaMalloc(&rope_, tab.size() * sizeof(float2)));
+        ACCO_CUDA(cudaMemcpy(rope_, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    }
     ACCO_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
@@ -178,6 +220,7 @@ GPTModel::~GPTModel() {
         cudaEventDestroy(ev_join_);
     }
     cudaFree(scratch_);
+    if (rope_) cudaFree(rope_);
     if (pinned_data_) cudaFreeHost(pinned_data_);
     if (stage_host_) cudaFreeHost(stage_host_);
     if (stage_dev_) cudaFree(stage_dev_);
@@ -252,9 +295,18 @@ Epilogue ep_acc(float* c, int64_t ldc, int beta) {
 
 }  // namespace
 
+void GPTModel::stage_input(uint64_t seed, int mode, int start, int B, cudaStream_t s) {
+    const int Tq = c_.seq_len;
+    if (host_data() && mode == 0)
+        gather_tokens(stage_tokens(seed, B, s), Tq, B, 0, 1, 0, B, tok_in_, tok_out_, idx_, s);
+    else
+        gather_tokens(data_, Tq, c_.n_samples, seed, mode, start, B, tok_in_, tok_out_, idx_, s);
+}
+
 template <class T>
 void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss, bool backward,
                    cudaStream_t s) {
+    if (c_.arch == 1) return run_llama<T>(P, seed, mode, start, B, G, loss, backward, s);
     const int Tq = c_.seq_len, d = c_.d_model, H = c_.n_head, hd = d / H, V = c_.vocab, L = c_.n_layer;
     ACCO_REQUIRE(B >= 1 && B <= c_.max_batch, "micro_batch: batch size exceeds the model workspace");
     if (mode == 1) ACCO_REQUIRE(start >= 0 && start + B <= c_.n_samples, "micro_batch: sample range out of bounds");
@@ -278,17 +330,14 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     auto li = [&](int l, int j) { return 2 + 12 * l + j; };  // j: 0 ln1w 1 ln1b 2 Wqkv 3 bqkv 4 Wproj 5 bproj
                                                             //    6 ln2w 7 ln2b 8 Wfc 9 bfc 10 Wfc2 11 bfc2
 
-    if (host_data() && mode == 0)
-        gather_tokens(stage_tokens(seed, B, s), Tq, B, 0, 1, 0, B, tok_in_, tok_out_, idx_, s);
-    else
-        gather_tokens(data_, Tq, c_.n_samples, seed, mode, start, B, tok_in_, tok_out_, idx_, s);
+    stage_input(seed, mode, start, B, s);
     embed_fwd<T>(tok_in_, W(kWte), W(kWpe), X(0), M, Tq, d, s);
     for (int l = 0; l < L; ++l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
           *A = slot(l, sA), *U = slot(l, sU);
         layernorm_fwd<T>(X(l), W(li(l, 0)), W(li(l, 1)), H1, stat(4 * l), stat(4 * l + 1), M, d, s);
         mm<T>(H1, d, false, W(li(l, 2)), d, false, M, 3 * d, d, ep_store(QKV, 3 * d, W(li(l, 3))), s);
-        attention_fwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, B, Tq, H, hd, s);
+        attention_fwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, B, Tq, H, H, hd, s);
         mm<T>(Y, d, false, W(li(l, 4)), d, false, M, d, d, ep_store(XM, d, W(li(l, 5)), X(l), d), s);
         layernorm_fwd<T>(XM, W(li(l, 6)), W(li(l, 7)), H2, stat(4 * l + 2), stat(4 * l + 3), M, d, s);
         mm<T>(H2, d, false, W(li(l, 8)), d, false, M, 4 * d, d, ep_gelu(U, 4 * d, W(li(l, 9)), A), s);
@@ -348,7 +397,7 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
         mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
         join();  // DT (read by the LN2 parameter reduction) is overwritten next
         mm<T>(DX, d, false, W(li(l, 4)), d, true, M, d, d, ep_store(DT, d), s);
-        attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, hd, s);
+        attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, H, hd, s);
         fork();
         colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, aux_);
         mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d, beta), s);
@@ -361,6 +410,105 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     // wte rows: the head wgrad above stored/added every row; the embedding adds
     embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), sort_, acc, s);
     join();  // the accumulator is complete when the compute stream passes this point
+}
+
+// Llama block (oracle/gpt_oracle.py _llama_loss_and_grad). Parameter indices
+// in layout_: 0 wte; per layer 1 + 6l + {0 attention_norm, 1 wqkv, 2 wo,
+// 3 ffn_norm, 4 w_gate_up, 5 w_down}; then norm, output.
+template <class T>
+void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss,
+                         bool backward, cudaStream_t s) {
+    const int Tq = c_.seq_len, d = c_.d_model, H = c_.n_head, Hk = c_.kv_heads(), hd = d / H, V = c_.vocab,
+              L = c_.n_layer, F = c_.ffn();
+    const int nqkv = (H + 2 * Hk) * hd;
+    ACCO_REQUIRE(B >= 1 && B <= c_.max_batch, "micro_batch: batch size exceeds the model workspace");
+    if (mode == 1) ACCO_REQUIRE(start >= 0 && start + B <= c_.n_samples, "micro_batch: sample range out of bounds");
+    const int M = B * Tq;
+    const int64_t Mmax = static_cast<int64_t>(c_.max_batch) * Tq;
+    auto slot = [&](int l, int sl) { return reinterpret_cast<T*>(act_[static_cast<size_t>(l * kPerLayer + sl)]); };
+    const int tail = L * kPerLayer;
+    T* XL = reinterpret_cast<T*>(act_[tail + 0]);
+    T* HF = reinterpret_cast<T*>(act_[tail + 1]);
+    T* LOG = reinterpret_cast<T*>(act_[tail + 2]);
+    T* DX = reinterpret_cast<T*>(act_[tail + 3]);
+    T* DT = reinterpret_cast<T*>(act_[tail + 4]);
+    T* DQKV = reinterpret_cast<T*>(act_[tail + 5]);
+    T* DGU = reinterpret_cast<T*>(act_[tail + 6]);
+    T* DU = reinterpret_cast<T*>(act_[tail + 7]);
+    auto X = [&](int l) { return l == L ? XL : slot(l, sX); };
+    auto stat = [&](int i) { return stats_ + static_cast<int64_t>(i) * Mmax; };
+    auto W = [&](int i) { return P + layout_[static_cast<size_t>(i)].off; };
+    auto Gp = [&](int i) { return G + layout_[static_cast<size_t>(i)].off; };
+    const int kWte = 0, kNorm = 1 + 6 * L, kOut = 2 + 6 * L;
+    auto li = [&](int l, int j) { return 1 + 6 * l + j; };
+    auto lse_l = [&](int l) { return lse_ + static_cast<int64_t>(l) * H * Mmax; };
+
+    stage_input(seed, mode, start, B, s);
+    embed_fwd<T>(tok_in_, W(kWte), nullptr, X(0), M, Tq, d, s);
+    for (int l = 0; l < L; ++l) {
+        T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
+          *GU = slot(l, sA), *A = slot(l, sU);
+        layernorm_fwd<T>(X(l), W(li(l, 0)), nullptr, H1, stat(4 * l), stat(4 * l + 1), M, d, s, true);
+        mm<T>(H1, d, false, W(li(l, 1)), d, false, M, nqkv, d, ep_store(QKV, nqkv), s);
+        rope_apply<T>(QKV, nqkv, rope_, M, Tq, H + Hk, hd, false, s);
+        attention_fwd<T>(QKV, Y, lse_l(l), B, Tq, H, Hk, hd, s);
+        mm<T>(Y, d, false, W(li(l, 2)), d, false, M, d, d, ep_store(XM, d, nullptr, X(l), d), s);
+        layernorm_fwd<T>(XM, W(li(l, 3)), nullptr, H2, stat(4 * l + 2), stat(4 * l + 3), M, d, s, true);
+        mm<T>(H2, d, false, W(li(l, 4)), d, false, M, 2 * F, d, ep_store(GU, 2 * F), s);
+        swiglu_fwd<T>(GU, A, M, F, s);
+        mm<T>(A, F, false, W(li(l, 5)), F, false, M, d, F, ep_store(X(l + 1), d, nullptr, XM, d), s);
+    }
+    layernorm_fwd<T>(X(L), W(kNorm), nullptr, HF, stat(4 * L), stat(4 * L + 1), M, d, s, true);
+    mm<T>(HF, d, false, W(kOut), d, false, M, V, d, ep_store(LOG, vpad_), s);
+    cross_entropy<T>(LOG, vpad_, tok_out_, V, M, Tq, row_loss_, s);
+    loss_reduce(row_loss_, M, Tq, loss, s);
+    if (!backward) return;
+
+    const bool acc = accumulate_;
+    const int beta = acc ? 1 : 0;
+    auto fork = [&] {
+        ACCO_CUDA(cudaEventRecord(ev_fork_, s));
+        ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    };
+    auto join = [&] {
+        ACCO_CUDA(cudaEventRecord(ev_join_, aux_));
+        ACCO_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    };
+    // LM head (untied): doutput (+)= dlogits^T hf ; dhf = dlogits output
+    mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kOut), d, beta), s);
+    mm<T>(LOG, vpad_, false, W(kOut), d, true, M, d, V, ep_store(DT, d), s);
+    fork();
+    layernorm_bwd_params<T>(DT, X(L), stat(4 * L), stat(4 * L + 1), Gp(kNorm), nullptr, scratch_, M, d, acc, aux_);
+    layernorm_bwd_dx<T>(DT, X(L), W(kNorm), stat(4 * L), stat(4 * L + 1), DX, false, M, d, s, true);
+    for (int l = L - 1; l >= 0; --l) {
+        T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
+          *GU = slot(l, sA), *A = slot(l, sU);
+        // MLP
+        mm<T>(DX, d, true, A, F, true, d, F, M, ep_acc(Gp(li(l, 5)), F, beta), s);
+        mm<T>(DX, d, false, W(li(l, 5)), F, true, M, F, d, ep_store(DU, F), s);
+        swiglu_bwd<T>(DU, GU, DGU, M, F, s);
+        mm<T>(DGU, 2 * F, true, H2, d, true, 2 * F, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
+        join();  // DT (read by the previous norm-weight reduction) is overwritten next
+        mm<T>(DGU, 2 * F, false, W(li(l, 4)), d, true, M, d, 2 * F, ep_store(DT, d), s);
+        fork();
+        layernorm_bwd_params<T>(DT, XM, stat(4 * l + 2), stat(4 * l + 3), Gp(li(l, 3)), nullptr, scratch_, M, d, acc,
+                                aux_);
+        layernorm_bwd_dx<T>(DT, XM, W(li(l, 3)), stat(4 * l + 2), stat(4 * l + 3), DX, true, M, d, s, true);
+        // attention
+        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 2)), d, beta), s);
+        join();
+        mm<T>(DX, d, false, W(li(l, 2)), d, true, M, d, d, ep_store(DT, d), s);
+        attention_bwd<T>(QKV, Y, lse_l(l), DT, DQKV, dsum_, B, Tq, H, Hk, hd, s);
+        rope_apply<T>(DQKV, nqkv, rope_, M, Tq, H + Hk, hd, true, s);
+        mm<T>(DQKV, nqkv, true, H1, d, true, nqkv, d, M, ep_acc(Gp(li(l, 1)), d, beta), s);
+        mm<T>(DQKV, nqkv, false, W(li(l, 1)), d, true, M, d, nqkv, ep_store(DT, d), s);
+        fork();
+        layernorm_bwd_params<T>(DT, X(l), stat(4 * l), stat(4 * l + 1), Gp(li(l, 0)), nullptr, scratch_, M, d, acc,
+                                aux_);
+        layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s, true);
+    }
+    embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), nullptr, sort_, acc, s, !acc);
+    join();
 }
 
 void GPTModel::micro_batch(const void* params, uint64_t seed, int mode, int start, int B, float* grad_acc,

@@ -23,6 +23,13 @@ struct LMConfig {
     int precision = 0;  // 0 = fp32 (parity), 1 = bf16 (tcgen05 throughput)
     int max_batch = 8;  // samples per micro-batch (workspace sizing)
     int host_data = 0;  // 1: per-micro-batch H2D of the token rows from pinned host memory
+    int arch = 0;       // 0 GPT-2 block, 1 Llama block (RMSNorm, RoPE, GQA, SwiGLU, untied head)
+    int n_kv_head = 0;  // llama: 0 -> n_head
+    int d_ff = 0;       // llama: 0 -> 4 * d_model
+    double rope_base = 0.0;  // llama: 0 -> 10000
+    int kv_heads() const { return n_kv_head > 0 ? n_kv_head : n_head; }
+    int ffn() const { return d_ff > 0 ? d_ff : 4 * d_model; }
+    double rope() const { return rope_base > 0.0 ? rope_base : 10000.0; }
 };
 
 struct ParamSpec {
@@ -73,6 +80,10 @@ private:
     template <class T>
     void run(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss, bool backward,
              cudaStream_t s);
+    template <class T>
+    void run_llama(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss, bool backward,
+                   cudaStream_t s);
+    void stage_input(uint64_t seed, int mode, int start, int B, cudaStream_t s);
 
     LMConfig c_;
     std::vector<ParamSpec> layout_;
@@ -89,6 +100,7 @@ private:
     float* lse_ = nullptr;      // per-layer attention lse
     float* dsum_ = nullptr;
     float* scratch_ = nullptr;  // column-reduce partials
+    float2* rope_ = nullptr;    // llama: (cos, sin) [seq][hd/2]
     // side stream for the bias / LN-parameter column reductions: they only feed
     // the gradient accumulator, so they run beside the GEMMs (fork/join events)
     cudaStream_t aux_ = nullptr;

@@ -102,3 +102,76 @@ def test_lm_problem_contract():
     assert n == 4 and loss == l2 and np.array_equal(g, g2)
     f, gf = p.value_and_grad(th)
     assert abs(f - math.log(32)) < 0.05  # near-uniform predictions at init
+
+
+# ---------------------------------------------------------------- Llama family (C4)
+LLAMA = G.GPTConfig(vocab=48, d_model=32, n_layer=2, n_head=4, seq_len=12, n_samples=8, data_seed=4,
+                    arch="llama", n_kv_head=2, d_ff=40)
+
+
+def _torch_llama_loss(cfg, theta, tok):
+    lay = G.param_layout(cfg)
+    P = {n: t.reshape(s) for (n, s, _, _), t in zip(lay, torch.split(theta, [int(np.prod(s)) for _, s, _, _ in lay]))}
+    B, T, d, H, Hk, F = tok.shape[0], cfg.seq_len, cfg.d_model, cfg.n_head, cfg.kv_heads, cfg.ffn
+    hd = d // H
+    cos, sin = (torch.tensor(a) for a in G.rope_table(cfg))
+
+    def rms(x, w):
+        return x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-5) * w
+
+    def rope(x):  # [B, h, T, hd]
+        x1, x2 = x[..., :hd // 2], x[..., hd // 2:]
+        return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], -1)
+
+    xi, yt = tok[:, :T], tok[:, 1:]
+    x = P["wte"][xi]
+    for l in range(cfg.n_layer):
+        p = f"layers.{l}."
+        qkv = rms(x, P[p + "attention_norm.weight"]) @ P[p + "attention.wqkv"].T
+        q, k, v = qkv.split([H * hd, Hk * hd, Hk * hd], -1)
+        q = rope(q.reshape(B, T, H, hd).transpose(1, 2))
+        k = rope(k.reshape(B, T, Hk, hd).transpose(1, 2))
+        v = v.reshape(B, T, Hk, hd).transpose(1, 2)
+        y = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True, enable_gqa=True)
+        x = x + y.transpose(1, 2).reshape(B, T, H * hd) @ P[p + "attention.wo"].T
+        g, u = (rms(x, P[p + "ffn_norm.weight"]) @ P[p + "feed_forward.w_gate_up"].T).split(F, -1)
+        x = x + (torch.nn.functional.silu(g) * u) @ P[p + "feed_forward.w_down"].T
+    logits = rms(x, P["norm.weight"]) @ P["output.weight"].T
+    nll = torch.nn.functional.cross_entropy(logits.reshape(-1, cfg.vocab), yt.reshape(-1), reduction="none")
+    return nll.reshape(B, T).mean(1).mean()
+
+
+def test_llama_param_count_c4():
+    # TinyLlama-1.1B shape (Llama-style ~1.1B, GQA, SwiGLU)
+    c4 = G.GPTConfig(vocab=32000, d_model=2048, n_layer=22, n_head=32, seq_len=2048, arch="llama",
+                     n_kv_head=4, d_ff=5632)
+    assert G.param_count(c4) == 1_100_048_384
+    names = [n for n, *_ in G.param_layout(LLAMA)]
+    assert names[:4] == ["wte", "layers.0.attention_norm.weight", "layers.0.attention.wqkv", "layers.0.attention.wo"]
+    assert names[-2:] == ["norm.weight", "output.weight"]
+
+
+def test_llama_matches_torch_float64_autograd():
+    th = G.default_theta0(LLAMA, 2) * 5.0
+    tok = G.dataset(LLAMA)
+    f, g = G.loss_and_grad(LLAMA, th, tok)
+    t = torch.tensor(th, dtype=torch.float64, requires_grad=True)
+    ft = _torch_llama_loss(LLAMA, t, torch.tensor(tok))
+    (gt,) = torch.autograd.grad(ft, t)
+    assert abs(f - ft.item()) <= 1e-12 * abs(f)
+    assert np.linalg.norm(g - gt.numpy()) <= 1e-10 * np.linalg.norm(g)
+
+
+def test_llama_finite_differences():
+    rng = np.random.default_rng(1)
+    th = G.default_theta0(LLAMA, 1) + 0.05 * rng.standard_normal(G.param_count(LLAMA))
+    tok = G.dataset(LLAMA)[:3]
+    f, g = G.loss_and_grad(LLAMA, th, tok)
+    eps = 1e-6
+    worst = 0.0
+    for j in rng.choice(th.size, 150, replace=False):
+        p = th.copy(); p[j] += eps
+        m = th.copy(); m[j] -= eps
+        num = (G.loss_and_grad(LLAMA, p, tok, False)[0] - G.loss_and_grad(LLAMA, m, tok, False)[0]) / (2 * eps)
+        worst = max(worst, abs(num - g[j]) / max(1.0, abs(num), abs(g[j])))
+    assert worst <= 1e-4
