@@ -112,6 +112,7 @@ __device__ __forceinline__ void mma_pb(float (*acc)[4], const float (*p)[4], con
 __global__ void __launch_bounds__(kThreads) fa_fwd(const __nv_bfloat16* __restrict__ qkv,
                                                    __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
                                                    int T, int H, float scale) {
+    ACCO_PDL_PROLOGUE();
     __shared__ __align__(128) uint8_t sQ[BR * 128];
     __shared__ __align__(128) uint8_t sK[2][BR * 128];
     __shared__ __align__(128) uint8_t sV[2][BR * 128];
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(kThreads) fa_bwd_dkv(const __nv_bfloat16* __re
                                                        const __nv_bfloat16* __restrict__ dy,
                                                        const float* __restrict__ lse, const float* __restrict__ dsum,
                                                        __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale) {
+    ACCO_PDL_PROLOGUE();
     extern __shared__ __align__(128) uint8_t dsm[];  // 49 KB: dynamic
     uint8_t* sK = dsm;
     uint8_t* sV = dsm + BR * 128;
@@ -302,6 +304,7 @@ __global__ void __launch_bounds__(kThreads) fa_bwd_dq(const __nv_bfloat16* __res
                                                       const __nv_bfloat16* __restrict__ dy,
                                                       const float* __restrict__ lse, const float* __restrict__ dsum,
                                                       __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale) {
+    ACCO_PDL_PROLOGUE();
     __shared__ __align__(128) uint8_t sQ[BR * 128];
     __shared__ __align__(128) uint8_t sO[BR * 128];
     __shared__ __align__(128) uint8_t sK[2][BR * 128];
@@ -379,6 +382,7 @@ __global__ void __launch_bounds__(kThreads) fa_bwd_dq(const __nv_bfloat16* __res
 
 __global__ void dsum_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dy,
                             float* __restrict__ dsum, int B, int T, int H) {
+    ACCO_PDL_PROLOGUE();
     // one warp per (b, h, t) row of 64: D = sum dO * O
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -405,7 +409,7 @@ bool attention_fwd_mma(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, i
                        cudaStream_t s) {
     if (!applicable(qkv, y, hd)) return false;
     dim3 grid((seq + BR - 1) / BR, B * H);
-    fa_fwd<<<grid, kThreads, 0, s>>>(qkv, y, lse, seq, H, 1.0f / sqrtf(static_cast<float>(hd)));
+    launch_pdl(fa_fwd, grid, kThreads, 0, s, qkv, y, lse, seq, H, 1.0f / sqrtf(static_cast<float>(hd)));
     ACCO_CHECK_LAUNCH();
     return true;
 }
@@ -414,7 +418,7 @@ bool attention_bwd_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const f
                        __nv_bfloat16* dqkv, float* dsum, int B, int seq, int H, int hd, cudaStream_t s) {
     if (!applicable(qkv, dy, hd) || !applicable(y, dqkv, hd)) return false;
     const int64_t rows = static_cast<int64_t>(B) * H * seq;
-    dsum_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, s>>>(y, dy, dsum, B, seq, H);
+    launch_pdl(dsum_kernel, static_cast<int>((rows + 7) / 8), 256, 0, s, y, dy, dsum, B, seq, H);
     ACCO_CHECK_LAUNCH();
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     dim3 grid((seq + BR - 1) / BR, B * H);
@@ -424,9 +428,9 @@ bool attention_bwd_mma(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const f
         ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dkv, cudaFuncAttributeMaxDynamicSharedMemorySize, kDkvSmem));
         cfg = true;
     }
-    fa_bwd_dkv<<<grid, kThreads, kDkvSmem, s>>>(qkv, dy, lse, dsum, dqkv, seq, H, scale);
+    launch_pdl(fa_bwd_dkv, grid, kThreads, kDkvSmem, s, qkv, dy, lse, dsum, dqkv, seq, H, scale);
     ACCO_CHECK_LAUNCH();
-    fa_bwd_dq<<<grid, kThreads, 0, s>>>(qkv, dy, lse, dsum, dqkv, seq, H, scale);
+    launch_pdl(fa_bwd_dq, grid, kThreads, 0, s, qkv, dy, lse, dsum, dqkv, seq, H, scale);
     ACCO_CHECK_LAUNCH();
     return true;
 }

@@ -16,6 +16,7 @@ template <class T, int HD>
 __global__ void __launch_bounds__(kTile) attn_fwd_kernel(const T* __restrict__ qkv, T* __restrict__ y,
                                                          float* __restrict__ lse, int seq, int H, int Hkv,
                                                          float scale) {
+    ACCO_PDL_PROLOGUE();
     extern __shared__ float sm[];
     float(*Ks)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm);
     float(*Vs)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + kTile * (HD + 1));
@@ -76,6 +77,7 @@ __global__ void __launch_bounds__(kTile) attn_fwd_kernel(const T* __restrict__ q
 template <class T, int HD>
 __global__ void attn_dsum_kernel(const T* __restrict__ y, const T* __restrict__ dy, float* __restrict__ dsum,
                                  int B, int seq, int H) {
+    ACCO_PDL_PROLOGUE();
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= static_cast<int64_t>(B) * H * seq) return;
     const int t = static_cast<int>(idx % seq);
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(kTile) attn_dq_kernel(const T* __restrict__ qk
                                                         const float* __restrict__ dsum, const T* __restrict__ dy,
                                                         T* __restrict__ dqkv, int seq, int H, int Hkv,
                                                         float scale) {
+    ACCO_PDL_PROLOGUE();
     extern __shared__ float sm[];
     float(*Ks)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm);
     float(*Vs)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + kTile * (HD + 1));
@@ -155,6 +158,7 @@ template <class T, int HD>
 __global__ void __launch_bounds__(kTile) attn_dkv_kernel(const T* __restrict__ qkv, const float* __restrict__ lse,
                                                          const float* __restrict__ dsum, const T* __restrict__ dy,
                                                          T* __restrict__ dqkv, int seq, int H, int Hkv, float scale) {
+    ACCO_PDL_PROLOGUE();
     extern __shared__ float sm[];
     float(*Ko)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm);
     float(*Vo)[HD + 1] = reinterpret_cast<float(*)[HD + 1]>(sm + 1 * kTile * (HD + 1));
@@ -235,7 +239,7 @@ void fwd_impl(const T* qkv, T* y, float* lse, int B, int seq, int H, int Hkv, cu
         ACCO_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cfg = true;
     }
-    attn_fwd_kernel<T, HD><<<dim3(B * H, ceil_div(seq, kTile)), kTile, smem, s>>>(
+    launch_pdl(attn_fwd_kernel<T, HD>, dim3(B * H, ceil_div(seq, kTile)), kTile, smem, s,
         qkv, y, lse, seq, H, Hkv, 1.0f / sqrtf(static_cast<float>(HD)));
     ACCO_CHECK_LAUNCH();
 }
@@ -245,7 +249,7 @@ void bwd_impl(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, 
               int Hkv, cudaStream_t s) {
     const float scale = 1.0f / sqrtf(static_cast<float>(HD));
     const int64_t rows = static_cast<int64_t>(B) * H * seq;
-    attn_dsum_kernel<T, HD><<<static_cast<int>((rows + 255) / 256), 256, 0, s>>>(y, dy, dsum, B, seq, H);
+    launch_pdl(attn_dsum_kernel<T, HD>, static_cast<int>((rows + 255) / 256), 256, 0, s, y, dy, dsum, B, seq, H);
     ACCO_CHECK_LAUNCH();
     const int smem_q = 2 * kTile * (HD + 1) * 4;
     const int smem_kv = (4 * kTile * (HD + 1) + 2 * kTile) * 4;
@@ -255,10 +259,10 @@ void bwd_impl(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, 
         ACCO_CUDA(cudaFuncSetAttribute(attn_dkv_kernel<T, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv));
         cfg = true;
     }
-    attn_dq_kernel<T, HD><<<dim3(B * H, ceil_div(seq, kTile)), kTile, smem_q, s>>>(qkv, lse, dsum, dy, dqkv, seq, H,
+    launch_pdl(attn_dq_kernel<T, HD>, dim3(B * H, ceil_div(seq, kTile)), kTile, smem_q, s, qkv, lse, dsum, dy, dqkv, seq, H,
                                                                                   Hkv, scale);
     ACCO_CHECK_LAUNCH();
-    attn_dkv_kernel<T, HD><<<dim3(B * Hkv, ceil_div(seq, kTile)), kTile, smem_kv, s>>>(qkv, lse, dsum, dy, dqkv, seq,
+    launch_pdl(attn_dkv_kernel<T, HD>, dim3(B * Hkv, ceil_div(seq, kTile)), kTile, smem_kv, s, qkv, lse, dsum, dy, dqkv, seq,
                                                                                      H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
 }

@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_after();
     const uint32_t tmem = *tslot;
+    pdl_trigger();
+    pdl_wait();
     const uint32_t tS = tmem, tO = tmem + 128;
 
     if (warp == 0) {
@@ -522,6 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_after();
     const uint32_t tmem = *tslot;
+    pdl_trigger();
+    pdl_wait();
     // columns: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320), O tile 1 [320,384)
 
     if (warp == 0) {
@@ -698,10 +702,10 @@ __device__ __forceinline__ void exp_cols32(const uint32_t* st, const float4* L4,
 }
 // p[c] = 2^(s_c * sl - L) for 64 columns (dQ: thread = query, columns = keys);
 // MASK: columns >= lim -> 0
-template <bool MASK>
+template <bool MASK, int N = 64>
 __device__ __forceinline__ void exp_row64(const uint32_t* st, float sl, float L, int lim, float* p) {
 #pragma unroll
-    for (int c = 0; c < 64; c += 2) {
+    for (int c = 0; c < N; c += 2) {
         const float2 a = fma_f32x2(make_float2(__uint_as_float(st[c]), __uint_as_float(st[c + 1])),
                                    make_float2(sl, sl), make_float2(-L, -L));
         float p0 = ex2(a.x), p1 = ex2(a.y);
@@ -783,10 +787,17 @@ __device__ __forceinline__ void st_row32_global(__nv_bfloat16* dst, const uint32
 }
 
 constexpr int BW_T = 128;                          // tile rows (keys or queries)
+// backward kernels: warps 0-3 (TMA, MMA, TMEM alloc, idle) + 16 softmax warps
+// (4 per TMEM lane quadrant, 32 columns each): the per-element chain
+// (TMEM load -> ex2 -> dS -> bf16 smem) is latency-bound at 2 warps per
+// scheduler, so 4 per scheduler keep the issue slots busy
+constexpr int BW_THREADS = 640;
+constexpr int BW_SOFTMAX = 512;
 constexpr int BW_TILE = BW_T * HD * 2;             // 16 KB [128][64] bf16
 constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P / dS operand)
 // dKV smem: K, V (once) + 2 stages x (Q, dO) + lse/D (2 stages) + P^T + dS^T
-constexpr int DKV_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 2 * BW_SQ + 256;
+constexpr int DKV_ST = 3;  // Q/dO ring depth (hides the L2 latency of the next query tile's loads)
+constexpr int DKV_SMEM = 1024 + 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 2 * BW_SQ + 256;
 
 // dK/dV: one CTA per (batch*head, 128-key tile); loops over the query tiles
 // at and after the diagonal. Per query tile:
@@ -794,7 +805,7 @@ constexpr int DKV_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + 2 * 2 * BW_T * 4
 //   softmax-bwd warps (thread = key row): P^T = 2^(S^T sl - lse2[q]),
 //   dS^T = P^T (dP^T - D[q])  -> bf16 smem operands
 //   dV += P^T dO, dK += dS^T Q          (TMEM, 128 x 64 each; Q/dO MN-major B)
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                   const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
                   int T, int H, int Hkv, float scale) {
@@ -802,17 +813,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;
     uint8_t* sV = sK + BW_TILE;
-    uint8_t* sQ = sV + BW_TILE;            // [2 stages]
-    uint8_t* sO = sQ + 2 * BW_TILE;        // dO [2 stages]
-    uint8_t* sPT = sO + 2 * BW_TILE;       // P^T operand
+    uint8_t* sQ = sV + BW_TILE;            // [DKV_ST stages]
+    uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
+    uint8_t* sPT = sO + DKV_ST * BW_TILE;  // P^T operand
     uint8_t* sDS = sPT + BW_SQ;            // dS^T operand
     float* sL = reinterpret_cast<float*>(sDS + BW_SQ);  // [2][128] lse (log2 domain)
     float* sD = sL + 2 * BW_T;                           // [2][128] D
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BW_T);
     uint64_t* kv_full = bars;
-    uint64_t* q_full = bars + 1;       // [2]
-    uint64_t* q_empty = q_full + 2;    // [2]
-    uint64_t* s_full = q_empty + 2;    // S^T and dP^T ready
+    uint64_t* q_full = bars + 1;            // [DKV_ST]
+    uint64_t* q_empty = q_full + DKV_ST;    // [DKV_ST]
+    uint64_t* s_full = q_empty + DKV_ST;    // S^T and dP^T ready
     uint64_t* s_free = s_full + 1;     // softmax has them in registers
     uint64_t* p_full = s_free + 1;     // P^T, dS^T in smem
     uint64_t* g_done = p_full + 1;     // dV/dK MMAs of this tile done (operands free)
@@ -836,13 +847,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(kv_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < DKV_ST; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
         }
         mbar_init(s_full, 1);
-        mbar_init(s_free, 256);
-        mbar_init(p_full, 256);
+        mbar_init(s_free, BW_SOFTMAX);
+        mbar_init(p_full, BW_SOFTMAX);
         mbar_init(g_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -856,6 +867,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_after();
     const uint32_t tmem = *tslot;
+    pdl_trigger();
+    pdl_wait();
     const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320;
 
     if (warp == 0) {
@@ -864,10 +877,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sK, &tmQKV, kv_full, kc, row_base + k0);
             tma_load_2d(sV, &tmQKV, kv_full, vc, row_base + k0);
             for (int i = 0; i < niter; ++i) {
-                const int s = i & 1;
+                const int s = i % DKV_ST;
                 const int h = hk * G + i / nq;
                 const int q0 = (kt + i % nq) * BW_T;
-                mbar_wait(&q_empty[s], ((i >> 1) & 1) ^ 1);
+                mbar_wait(&q_empty[s], ((i / DKV_ST) & 1) ^ 1);
                 mbar_expect_tx(&q_full[s], 2 * BW_TILE);
                 tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
                 tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
@@ -881,8 +894,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t pt_base = smem_u32(sPT), ds_base = smem_u32(sDS);
             mbar_wait(kv_full, 0);
             auto issue_s = [&](int i) {  // S^T = K Q_i^T, dP^T = V dO_i^T
-                const int s = i & 1;
-                mbar_wait(&q_full[s], (i >> 1) & 1);
+                const int s = i % DKV_ST;
+                mbar_wait(&q_full[s], (i / DKV_ST) & 1);
                 tc_after();
                 const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
 #pragma unroll
@@ -894,7 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             issue_s(0);
             for (int i = 0; i < niter; ++i) {
-                const int s = i & 1;
+                const int s = i % DKV_ST;
                 const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
                 if (i + 1 < niter) {  // next tile's S^T/dP^T overlap this tile's softmax
                     mbar_wait(s_free, i & 1);
@@ -914,14 +927,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // 8 warps: quadrant wq (key rows = TMEM lanes) x half (64 of 128 queries)
-        const int wq = warp & 3, hf = (warp - 4) >> 2;
+        // 16 warps: quadrant wq (key rows = TMEM lanes) x quarter qq (32 of 128 queries)
+        const int wq = warp & 3, qq = (warp - 4) >> 2;
         const int r = wq * 32 + lane;  // key row = TMEM lane
         const int key = k0 + r;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
         // lse (log2) and D of query tile i, loaded one tile ahead (registers)
-        // by the half-0 threads and published through a double-buffered smem row
+        // by the quarter-0 threads and published through a double-buffered smem row
         auto fetch = [&](int i, float& lv, float& dv) {
             const int q = (kt + i % nq) * BW_T + r;
             const bool ok = i < niter && q < T;
@@ -930,56 +943,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             dv = ok ? __ldg(dsum + bh * T + q) : 0.f;
         };
         float nl = 0.f, nd = 0.f;
-        if (hf == 0) fetch(0, nl, nd);
+        if (qq == 0) fetch(0, nl, nd);
         for (int i = 0; i < niter; ++i) {
             const int s = i & 1;
             const int qi = i % nq;
             const int q0 = (kt + qi) * BW_T;
-            if (hf == 0) {
+            if (qq == 0) {
                 sL[s * BW_T + r] = nl;
                 sD[s * BW_T + r] = nd;
             }
-            asm volatile("bar.sync 1, 256;" ::: "memory");  // softmax warps only
-            if (hf == 0) fetch(i + 1, nl, nd);  // latency hidden behind this tile
+            asm volatile("bar.sync 1, 512;" ::: "memory");  // softmax warps only
+            if (qq == 0) fetch(i + 1, nl, nd);  // latency hidden behind this tile
             mbar_wait(s_full, i & 1);
             tc_after();
             // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
             // rows past T belong to the next sequence)
             const bool edge = qi == 0 || q0 + BW_T > T;
-            const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + hf * 64);
-            const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + hf * 64);
+            const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + qq * 32);
+            const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + qq * 32);
             {
-                float p[64];
-                // valid query columns c of this half: q0 + hf*64 + c in [key, T)
-                const int lo = key - (q0 + hf * 64), hi = T - (q0 + hf * 64);
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {  // S^T streamed 32 columns at a time
-                    uint32_t st[32];
-                    tmem_ld32(tS + lane_off + hf * 64 + hh * 32, st);
-                    tmem_wait_ld();
-                    if (edge)
-                        exp_cols32<true>(st, L4 + hh * 8, sl, hh * 32, lo, hi, p + hh * 32);
-                    else
-                        exp_cols32<false>(st, L4 + hh * 8, sl, hh * 32, lo, hi, p + hh * 32);
-                }
+                // S^T and dP^T (this warp's 32 columns each) go to registers first
+                // and their TMEM is released at once, so the MMA warp computes the
+                // next tile's S^T / dP^T under this tile's exp / dS math
+                uint32_t st[32], dp[32];
+                tmem_ld32(tS + lane_off + qq * 32, st);
+                tmem_ld32(tP + lane_off + qq * 32, dp);
+                tmem_wait_ld();
+                tc_before();
+                mbar_arrive(s_free);
+                float* p = reinterpret_cast<float*>(st);  // in place
+                // valid query columns c of this quarter: q0 + qq*32 + c in [key, T)
+                const int lo = key - (q0 + qq * 32), hi = T - (q0 + qq * 32);
+                if (edge)
+                    exp_cols32<true>(st, L4, sl, 0, lo, hi, p);
+                else
+                    exp_cols32<false>(st, L4, sl, 0, lo, hi, p);
+                float* ds = reinterpret_cast<float*>(dp);  // dS^T = P^T (dP^T - D), in place
+                ds_pairs(p, dp, reinterpret_cast<const float*>(D4), 32, ds);
                 if (i > 0) {  // the previous dV/dK MMAs have read the smem operands
                     mbar_wait(g_done, (i - 1) & 1);
                     tc_after();
                 }
-                st_row64_chunk(sPT, hf, r, p);
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {  // dS^T = P^T (dP^T - D), 32 columns at a time
-                    uint32_t st[32];
-                    tmem_ld32(tP + lane_off + hf * 64 + hh * 32, st);
-                    tmem_wait_ld();
-                    if (hh == 1) {
-                        tc_before();
-                        mbar_arrive(s_free);  // S^T / dP^T TMEM may be overwritten
-                    }
-                    float ds[32];
-                    ds_pairs(p + hh * 32, st, reinterpret_cast<const float*>(D4 + hh * 8), 32, ds);
-                    st_row32_part(sDS, hf, r, hh, ds);
-                }
+                st_row32_part(sPT, qq >> 1, r, qq & 1, p);
+                st_row32_part(sDS, qq >> 1, r, qq & 1, ds);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc_before();
@@ -987,14 +993,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(g_done, (niter - 1) & 1);
         tc_after();
-        uint32_t o[32];  // this warp's 32 of the 64 output columns
-        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * T + key) * ldq + hf * 32;
-        tmem_ld32(tDV + lane_off + hf * 32, o);
+        uint32_t o[32];  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
+        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * T + key) * ldq + (qq & 1) * 32;
+        tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
         tmem_wait_ld();
-        if (key < T) st_row32_global(dst + vc, o, 1.f);
-        tmem_ld32(tDK + lane_off + hf * 32, o);
-        tmem_wait_ld();
-        if (key < T) st_row32_global(dst + kc, o, scale);
+        if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
     }
     tc_before();
     __syncthreads();
@@ -1007,9 +1010,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // dQ: one CTA per (batch*head, 128-query tile), loops over key tiles up to the
 // diagonal: S = Q K^T, dP = dO V^T (TMEM); thread = query row: P, dS -> smem;
 // dQ += dS K (K as MN-major B). Heavy tiles first.
-constexpr int DQ_SMEM = 1024 + 2 * BW_TILE + 2 * 2 * BW_TILE + BW_SQ + 256;
+// K/V ring depth: a K/V tile is released only when dQ of the previous use has
+// been issued, so 2 stages exposed the L2 latency of every load
+constexpr int DQ_ST = 4;
+constexpr int DQ_SMEM = 1024 + 2 * BW_TILE + DQ_ST * 2 * BW_TILE + BW_SQ + 256;
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
                  int T, int H, int Hkv, float scale) {
@@ -1017,14 +1023,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;
     uint8_t* sO = sQ + BW_TILE;           // dO
-    uint8_t* sK = sO + BW_TILE;           // [2 stages]
-    uint8_t* sV = sK + 2 * BW_TILE;       // [2 stages]
-    uint8_t* sDS = sV + 2 * BW_TILE;
+    uint8_t* sK = sO + BW_TILE;           // [DQ_ST stages]
+    uint8_t* sV = sK + DQ_ST * BW_TILE;   // [DQ_ST stages]
+    uint8_t* sDS = sV + DQ_ST * BW_TILE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + BW_SQ);
     uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;     // [2]
-    uint64_t* kv_empty = kv_full + 2; // [2]
-    uint64_t* s_full = kv_empty + 2;
+    uint64_t* kv_full = bars + 1;          // [DQ_ST]
+    uint64_t* kv_empty = kv_full + DQ_ST;  // [DQ_ST]
+    uint64_t* s_full = kv_empty + DQ_ST;
     uint64_t* s_free = s_full + 1;
     uint64_t* p_full = s_free + 1;
     uint64_t* g_done = p_full + 1;
@@ -1043,13 +1049,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < DQ_ST; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
         }
         mbar_init(s_full, 1);
-        mbar_init(s_free, 256);
-        mbar_init(p_full, 256);
+        mbar_init(s_free, BW_SOFTMAX);
+        mbar_init(p_full, BW_SOFTMAX);
         mbar_init(g_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1063,6 +1069,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_after();
     const uint32_t tmem = *tslot;
+    pdl_trigger();
+    pdl_wait();
     const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
 
     if (warp == 0) {
@@ -1071,8 +1079,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(sQ, &tmQKV, q_full, h * HD, row_base + q0);
             tma_load_2d(sO, &tmDO, q_full, h * HD, row_base + q0);
             for (int j = 0; j < nk; ++j) {
-                const int s = j & 1;
-                mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+                const int s = j % DQ_ST;
+                mbar_wait(&kv_empty[s], ((j / DQ_ST) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
                 tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], kc, row_base + j * BW_T);
                 tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], vc, row_base + j * BW_T);
@@ -1085,8 +1093,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t q_base = smem_u32(sQ), o_base = smem_u32(sO), ds_base = smem_u32(sDS);
             mbar_wait(q_full, 0);
             auto issue_s = [&](int j) {  // S = Q K_j^T, dP = dO V_j^T
-                const int s = j & 1;
-                mbar_wait(&kv_full[s], (j >> 1) & 1);
+                const int s = j % DQ_ST;
+                mbar_wait(&kv_full[s], (j / DQ_ST) & 1);
                 tc_after();
                 const uint32_t k_base = smem_u32(sK + s * BW_TILE), v_base = smem_u32(sV + s * BW_TILE);
 #pragma unroll
@@ -1098,7 +1106,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             issue_s(0);
             for (int j = 0; j < nk; ++j) {
-                const int s = j & 1;
+                const int s = j % DQ_ST;
                 const uint32_t k_base = smem_u32(sK + s * BW_TILE);
                 if (j + 1 < nk) {
                     mbar_wait(s_free, j & 1);
@@ -1115,8 +1123,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // 8 warps: quadrant wq (query rows = TMEM lanes) x half (64 of 128 keys)
-        const int wq = warp & 3, hf = (warp - 4) >> 2;
+        // 16 warps: quadrant wq (query rows = TMEM lanes) x quarter qq (32 of 128 keys)
+        const int wq = warp & 3, qq = (warp - 4) >> 2;
         const int r = wq * 32 + lane;
         const int q = q0 + r;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
@@ -1128,33 +1136,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_after();
             const bool diag = j == nk - 1;
             {
-                uint32_t st[64];
-                float p[64];
-                tmem_ld32(tS + lane_off + hf * 64, st);
-                tmem_ld32(tS + lane_off + hf * 64 + 32, st + 32);
-                tmem_wait_ld();
-                // valid key columns c: j*128 + hf*64 + c <= q and < T
-                const int lim = min(q + 1, T) - (j * BW_T + hf * 64);
-                if (diag)
-                    exp_row64<true>(st, sl, L, lim, p);
-                else
-                    exp_row64<false>(st, sl, L, lim, p);
-                tmem_ld32(tP + lane_off + hf * 64, st);
-                tmem_ld32(tP + lane_off + hf * 64 + 32, st + 32);
+                // S and dP to registers first, TMEM released at once: the next
+                // tile's S / dP MMAs run under this tile's exp / dS math
+                uint32_t st[32], dp[32];
+                tmem_ld32(tS + lane_off + qq * 32, st);
+                tmem_ld32(tP + lane_off + qq * 32, dp);
                 tmem_wait_ld();
                 tc_before();
                 mbar_arrive(s_free);
+                float* p = reinterpret_cast<float*>(st);  // in place
+                // valid key columns c: j*128 + qq*32 + c <= q and < T
+                const int lim = min(q + 1, T) - (j * BW_T + qq * 32);
+                if (diag)
+                    exp_row64<true, 32>(st, sl, L, lim, p);
+                else
+                    exp_row64<false, 32>(st, sl, L, lim, p);
                 {
-                    float dv[64];
+                    float dv[32];
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) dv[c] = Dq;
-                    ds_pairs(p, st, dv, 64, p);
+                    for (int c = 0; c < 32; ++c) dv[c] = Dq;
+                    ds_pairs(p, dp, dv, 32, p);
                 }
                 if (j > 0) {  // the previous dQ MMA has read dS
                     mbar_wait(g_done, (j - 1) & 1);
                     tc_after();
                 }
-                st_row64_chunk(sDS, hf, r, p);
+                st_row32_part(sDS, qq >> 1, r, qq & 1, p);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tc_before();
@@ -1162,10 +1169,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(g_done, (nk - 1) & 1);
         tc_after();
-        uint32_t o[32];
-        tmem_ld32(tDQ + lane_off + hf * 32, o);
-        tmem_wait_ld();
-        if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(b) * T + q) * ldq + h * HD + hf * 32, o, scale);
+        if (qq < 2) {
+            uint32_t o[32];
+            tmem_ld32(tDQ + lane_off + qq * 32, o);
+            tmem_wait_ld();
+            if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(b) * T + q) * ldq + h * HD + qq * 32, o, scale);
+        }
     }
     tc_before();
     __syncthreads();
@@ -1211,6 +1220,7 @@ CUtensorMap rows_map(const void* p, int64_t cols, int64_t rows, int64_t ld) {
 // per row, 16 B each, 3-step shuffle reduction.
 __global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dy,
                                float* __restrict__ dsum, int B, int T, int H) {
+    ACCO_PDL_PROLOGUE();
     const int64_t nrow = static_cast<int64_t>(B) * T * H;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t row = i >> 3;  // (b*T + t)*H + h
@@ -1250,7 +1260,7 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     const int64_t rows = static_cast<int64_t>(B) * T;
     const int64_t nrow = rows * H;
-    dsum_tc_kernel<<<static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s>>>(y, dy, dsum, B, T, H);
+    launch_pdl(dsum_tc_kernel, static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
     ACCO_CHECK_LAUNCH();
     CUtensorMap mq = rows_map(qkv, ldq, rows, ldq);
     CUtensorMap mo = rows_map(dy, d, rows, d);
@@ -1262,9 +1272,9 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nt = (T + BW_T - 1) / BW_T;
-    fa_bwd_dkv_tc<<<dim3(nt, B * Hkv), kThreads, DKV_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
+    launch_pdl(fa_bwd_dkv_tc, dim3(nt, B * Hkv), BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
-    fa_bwd_dq_tc<<<dim3(nt, B * H), kThreads, DQ_SMEM, s>>>(mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
+    launch_pdl(fa_bwd_dq_tc, dim3(nt, B * H), BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
     return true;
 }
@@ -1286,9 +1296,9 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nqt = (T + BQ - 1) / BQ;
     if (std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
-        fa_fwd_tc<<<dim3(nqt, B * H), kThreads, SMEM, s>>>(m, y, lse, T, H, Hkv, scale);
+        launch_pdl(fa_fwd_tc, dim3(nqt, B * H), kThreads, SMEM, s, m, y, lse, T, H, Hkv, scale);
     } else {
-        fa_fwd_tc2<<<dim3((nqt + 1) / 2, B * H), kThreads, F2_SMEM, s>>>(m, y, lse, T, H, Hkv, scale);
+        launch_pdl(fa_fwd_tc2, dim3((nqt + 1) / 2, B * H), kThreads, F2_SMEM, s, m, y, lse, T, H, Hkv, scale);
     }
     ACCO_CHECK_LAUNCH();
     return true;

@@ -5,6 +5,7 @@
 #include "gemm.h"
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -24,6 +25,11 @@ int num_sms() {
         ACCO_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
     }
     return n;
+}
+
+bool pdl_enabled() {
+    static const bool on = std::getenv("ACCO_NO_PDL") == nullptr;
+    return on;
 }
 
 static std::atomic<long long> g_launches{0};

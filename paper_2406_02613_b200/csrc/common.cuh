@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "paper_2406_02613_b200 targets sm_100a only"
@@ -53,6 +54,41 @@ enum Status : int {
     } while (0)
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// ------------------------------------------------ programmatic dependent launch
+// Every kernel of the training step starts with ACCO_PDL_PROLOGUE (or calls
+// pdl_trigger / pdl_wait itself after a prologue that touches no global
+// data): it lets the next kernel in the stream launch as soon as all of this
+// grid's CTAs are running, and blocks until the previous grid has completed
+// and its memory is visible. Launched through launch_pdl, a kernel's launch
+// latency and prologue (barrier init, TMEM alloc, descriptor prefetch) then
+// overlap the previous kernel's tail. ACCO_NO_PDL=1 disables the attribute
+// (the device instructions are no-ops without it).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define ACCO_PDL_PROLOGUE() \
+    do {                    \
+        ::acco::pdl_trigger(); \
+        ::acco::pdl_wait();    \
+    } while (0)
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) throw Error(kCudaError, std::string("launch_pdl: ") + cudaGetErrorString(e));
+}
 
 // Number of SMs on the current device (148 on B200); cached per process.
 int num_sms();

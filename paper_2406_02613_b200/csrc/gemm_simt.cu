@@ -17,6 +17,7 @@ template <int A_MN, int B_MN>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict__ A, int64_t lda,
                                                         const float* __restrict__ B, int64_t ldb,
                                                         int M, int N, int K, Epilogue ep) {
+    ACCO_PDL_PROLOGUE();
     __shared__ float As[kTK][kT + 4];
     __shared__ float Bs[kTK][kT + 4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -71,13 +72,13 @@ void gemm_f32(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, c
     const float* a = static_cast<const float*>(A.ptr);
     const float* b = static_cast<const float*>(B.ptr);
     if (!A.mn_major && !B.mn_major)
-        gemm_simt_kernel<0, 0><<<grid, 256, 0, stream>>>(a, A.ld, b, B.ld, M, N, K, ep);
+        launch_pdl(gemm_simt_kernel<0, 0>, grid, 256, 0, stream, a, A.ld, b, B.ld, M, N, K, ep);
     else if (!A.mn_major && B.mn_major)
-        gemm_simt_kernel<0, 1><<<grid, 256, 0, stream>>>(a, A.ld, b, B.ld, M, N, K, ep);
+        launch_pdl(gemm_simt_kernel<0, 1>, grid, 256, 0, stream, a, A.ld, b, B.ld, M, N, K, ep);
     else if (A.mn_major && !B.mn_major)
-        gemm_simt_kernel<1, 0><<<grid, 256, 0, stream>>>(a, A.ld, b, B.ld, M, N, K, ep);
+        launch_pdl(gemm_simt_kernel<1, 0>, grid, 256, 0, stream, a, A.ld, b, B.ld, M, N, K, ep);
     else
-        gemm_simt_kernel<1, 1><<<grid, 256, 0, stream>>>(a, A.ld, b, B.ld, M, N, K, ep);
+        launch_pdl(gemm_simt_kernel<1, 1>, grid, 256, 0, stream, a, A.ld, b, B.ld, M, N, K, ep);
     ACCO_CHECK_LAUNCH();
 }
 

@@ -299,6 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // prologue done (barriers, TMEM): let the next kernel launch, then wait for
+    // the previous one's results before the first TMA load / global write
+    pdl_trigger();
+    pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -600,7 +604,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     CUtensorMap ta = operand_map(A, M, K, kBM);
     CUtensorMap tb = operand_map(B, N, K, BN);
     const int grid = std::min(sc.units(), num_sms());
-    kern<<<grid, kThreads, smem, stream>>>(ta, tb, em, M, N, sc, ep, sem);
+    launch_pdl(kern, grid, kThreads, smem, stream, ta, tb, em, M, N, sc, ep, sem);
     ACCO_CHECK_LAUNCH();
 }
 

@@ -25,6 +25,7 @@ __device__ __forceinline__ float warp_max(float v) {
 __global__ void gather_tokens_kernel(const int32_t* __restrict__ data, int seq, int n_samples,
                                      uint64_t seed, int mode, int start, int32_t* tok_in,
                                      int32_t* tok_out, int32_t* idx_out) {
+    ACCO_PDL_PROLOGUE();
     const int b = blockIdx.x;
     int idx;
     if (mode == 0)
@@ -43,6 +44,7 @@ __global__ void gather_tokens_kernel(const int32_t* __restrict__ data, int seq, 
 template <class T>
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ wte,
                                  const T* __restrict__ wpe, T* __restrict__ x, int seq, int d) {
+    ACCO_PDL_PROLOGUE();
     const int m = blockIdx.x;
     const int t = m % seq;
     const T* e = wte + static_cast<int64_t>(tok[m]) * d;
@@ -64,6 +66,7 @@ template <class T, bool RMS>
 __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
                               T* __restrict__ y, float* __restrict__ mean, float* __restrict__ rstd,
                               int M, int d) {
+    ACCO_PDL_PROLOGUE();
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= M) return;
@@ -91,6 +94,7 @@ template <class T, bool RMS>
 __global__ void ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ g,
                               const float* __restrict__ mean, const float* __restrict__ rstd,
                               T* __restrict__ dx, int accumulate, int M, int d) {
+    ACCO_PDL_PROLOGUE();
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (row >= M) return;
@@ -138,6 +142,7 @@ template <int CH, bool RMS>
 __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                            const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
                            float* __restrict__ rstd, int M) {
+    ACCO_PDL_PROLOGUE();
     constexpr int d = 256 * CH;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -176,6 +181,7 @@ template <int CH, bool RMS>
 __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                            const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
                            const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx, int accumulate, int M) {
+    ACCO_PDL_PROLOGUE();
     constexpr int d = 256 * CH;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
@@ -230,6 +236,7 @@ template <class T, int KIND>
 __global__ void colreduce_partial(const T* __restrict__ y, int64_t ld, const T* __restrict__ x,
                                   const float* __restrict__ mean, const float* __restrict__ rstd,
                                   int M, int N, float* __restrict__ part0, float* __restrict__ part1) {
+    ACCO_PDL_PROLOGUE();
     __shared__ float s0[kColRows][33], s1[kColRows][33];
     const int col = blockIdx.x * 32 + threadIdx.x;
     const int chunk = blockIdx.y;
@@ -297,6 +304,7 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
                                                          int M, int N, int rows_per_chunk, float* __restrict__ part,
                                                          unsigned* __restrict__ tickets, float* __restrict__ out,
                                                          float* __restrict__ out1, int acc) {
+    ACCO_PDL_PROLOGUE();
     __shared__ float s0[kVecRows][65], s1[kVecRows][65];
     __shared__ bool last;
     const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;
@@ -378,6 +386,7 @@ __global__ void __launch_bounds__(256) colsum_vec_kernel(const T* __restrict__ y
 
 __global__ void colreduce_final(const float* __restrict__ part, int nchunk, int N, float* __restrict__ out,
                                 int acc) {
+    ACCO_PDL_PROLOGUE();
     const int col = blockIdx.x * blockDim.x + threadIdx.x;
     if (col >= N) return;
     float t = 0.f;
@@ -390,6 +399,7 @@ template <class T>
 __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, int64_t ld,
                                                  const int32_t* __restrict__ target, int V, float inv_seq,
                                                  float* __restrict__ row_loss) {
+    ACCO_PDL_PROLOGUE();
     __shared__ float red[32];
     const int row = blockIdx.x;
     T* L = logits + static_cast<int64_t>(row) * ld;
@@ -446,6 +456,7 @@ __device__ __forceinline__ void unpack8(const uint4& u, float* v) {
 __global__ void __launch_bounds__(256) ce_vec_kernel(__nv_bfloat16* __restrict__ logits, int64_t ld,
                                                      const int32_t* __restrict__ target, int V, float inv_seq,
                                                      float* __restrict__ row_loss) {
+    ACCO_PDL_PROLOGUE();
     __shared__ float red_m[8], red_s[8];
     const int row = blockIdx.x;
     uint4* L = reinterpret_cast<uint4*>(logits + static_cast<int64_t>(row) * ld);
@@ -510,6 +521,7 @@ __global__ void __launch_bounds__(256) ce_vec_kernel(__nv_bfloat16* __restrict__
 }
 
 __global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int M, int seq, double* out) {
+    ACCO_PDL_PROLOGUE();
     __shared__ double red[256];
     double s = 0.0;
     for (int i = threadIdx.x; i < M; i += blockDim.x) s += row_loss[i];
@@ -526,6 +538,7 @@ __global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int M, in
 // single-CTA bitonic sort of keys (tok * M + m): stable grouping by token with
 // ascending positions inside each group.
 __global__ void sort_keys_kernel(const int32_t* __restrict__ tok, int M, int P, uint32_t* out) {
+    ACCO_PDL_PROLOGUE();
     extern __shared__ uint32_t keys[];
     for (int i = threadIdx.x; i < P; i += blockDim.x)
         keys[i] = i < M ? static_cast<uint32_t>(tok[i]) * static_cast<uint32_t>(M) + i : 0xffffffffu;
@@ -552,6 +565,7 @@ __global__ void sort_keys_kernel(const int32_t* __restrict__ tok, int M, int P, 
 template <class T>
 __global__ void embed_bwd_wte_kernel(const uint32_t* __restrict__ sorted, int M, const T* __restrict__ dx,
                                      int d, float* __restrict__ grad_wte) {
+    ACCO_PDL_PROLOGUE();
     const int i = blockIdx.x;
     const uint32_t tok = sorted[i] / static_cast<uint32_t>(M);
     if (i > 0 && sorted[i - 1] / static_cast<uint32_t>(M) == tok) return;  // not a segment start
@@ -565,9 +579,82 @@ __global__ void embed_bwd_wte_kernel(const uint32_t* __restrict__ sorted, int M,
     }
 }
 
+// Parallel deterministic segment sums for the token-embedding gradient (the
+// Markov data makes a few tokens very hot, so a per-segment serial loop is
+// latency-bound). The sorted (token, position) list is cut into fixed chunks
+// of kEmbChunk entries; pass 1 sums each run (maximal same-token stretch) of
+// a chunk into run_sum[chunk * kEmbChunk + run]; pass 2, per token segment,
+// folds its runs in ascending chunk order into grad_wte. Fixed order
+// throughout: bitwise reproducible.
+constexpr int kEmbChunk = 32;
+
+template <class T>
+__global__ void embed_runs_kernel(const uint32_t* __restrict__ sorted, int M, const T* __restrict__ dx, int d,
+                                  float* __restrict__ run_sum) {
+    ACCO_PDL_PROLOGUE();
+    const int p0 = blockIdx.x * kEmbChunk, p1 = min(M, p0 + kEmbChunk);
+    const uint32_t uM = static_cast<uint32_t>(M);
+    for (int cg = threadIdx.x; cg < d / 8; cg += blockDim.x) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t prev = sorted[p0] / uM;
+        int r = 0;
+        for (int p = p0; p < p1; ++p) {
+            const uint32_t key = sorted[p];
+            const uint32_t tok = key / uM;
+            if (tok != prev) {
+                float4* o = reinterpret_cast<float4*>(run_sum + static_cast<int64_t>(p0 + r) * d + cg * 8);
+                o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+                ++r;
+                prev = tok;
+            }
+            float v[8];
+            load8<T>(dx + static_cast<int64_t>(key % uM) * d + cg * 8, v);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc[k] += v[k];
+        }
+        float4* o = reinterpret_cast<float4*>(run_sum + static_cast<int64_t>(p0 + r) * d + cg * 8);
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+    }
+}
+
+__global__ void embed_fold_kernel(const uint32_t* __restrict__ sorted, int M, const float* __restrict__ run_sum,
+                                  int d, float* __restrict__ grad_wte) {
+    ACCO_PDL_PROLOGUE();
+    const int i = blockIdx.x;
+    const uint32_t uM = static_cast<uint32_t>(M);
+    const uint32_t tok = sorted[i] / uM;
+    if (i > 0 && sorted[i - 1] / uM == tok) return;  // not a segment start
+    const int c = i / kEmbChunk;
+    int r0 = 0;  // run index of this segment inside its first chunk
+    for (int p = c * kEmbChunk + 1; p <= i; ++p) r0 += (sorted[p] / uM != sorted[p - 1] / uM) ? 1 : 0;
+    for (int cg = threadIdx.x; cg < d / 8; cg += blockDim.x) {
+        const float4* a = reinterpret_cast<const float4*>(run_sum + static_cast<int64_t>(c * kEmbChunk + r0) * d +
+                                                          cg * 8);
+        float4 s0 = a[0], s1 = a[1];
+        for (int cc = c + 1; cc * kEmbChunk < M && sorted[cc * kEmbChunk] / uM == tok; ++cc) {
+            const float4* b = reinterpret_cast<const float4*>(run_sum + static_cast<int64_t>(cc) * kEmbChunk * d +
+                                                              cg * 8);
+            const float4 t0 = b[0], t1 = b[1];
+            s0.x += t0.x; s0.y += t0.y; s0.z += t0.z; s0.w += t0.w;
+            s1.x += t1.x; s1.y += t1.y; s1.z += t1.z; s1.w += t1.w;
+        }
+        float4* g = reinterpret_cast<float4*>(grad_wte + static_cast<int64_t>(tok) * d + cg * 8);
+        float4 g0 = g[0], g1 = g[1];
+        g0.x += s0.x; g0.y += s0.y; g0.z += s0.z; g0.w += s0.w;
+        g1.x += s1.x; g1.y += s1.y; g1.z += s1.z; g1.w += s1.w;
+        g[0] = g0;
+        g[1] = g1;
+    }
+}
+
 template <class T>
 __global__ void embed_bwd_wpe_kernel(const T* __restrict__ dx, int B, int seq, int d, float* __restrict__ grad_wpe,
                                      int accumulate) {
+    ACCO_PDL_PROLOGUE();
     const int t = blockIdx.x;
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
         float acc = 0.f;
@@ -578,14 +665,17 @@ __global__ void embed_bwd_wpe_kernel(const T* __restrict__ dx, int B, int seq, i
 }
 
 // ------------------------------------------------------------------ utilities
-__global__ void fill_i64_kernel(int64_t* p, int64_t v) { *p = v; }
-__global__ void add_i64_kernel(int64_t* dst, const int64_t* a, const int64_t* b) { *dst = *a + *b; }
+__global__ void fill_i64_kernel(int64_t* p, int64_t v) {
+    ACCO_PDL_PROLOGUE(); *p = v; }
+__global__ void add_i64_kernel(int64_t* dst, const int64_t* a, const int64_t* b) {
+    ACCO_PDL_PROLOGUE(); *dst = *a + *b; }
 
 struct PtrList {
     const float* p[16];
 };
 
 __global__ void sum_ordered_kernel(PtrList in, int nin, float* __restrict__ out, int64_t n) {
+    ACCO_PDL_PROLOGUE();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
         float s = in.p[0][i];
@@ -596,17 +686,20 @@ __global__ void sum_ordered_kernel(PtrList in, int nin, float* __restrict__ out,
 
 template <class T>
 __global__ void f32_to_kernel(const float* __restrict__ src, T* __restrict__ dst, int64_t n) {
+    ACCO_PDL_PROLOGUE();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
         dst[i] = from_f<T>(src[i]);
 }
 
 __global__ void scale_kernel(float* x, float a, int64_t n) {
+    ACCO_PDL_PROLOGUE();
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) x[i] *= a;
 }
 
 __global__ void norm_sq_partial(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+    ACCO_PDL_PROLOGUE();
     __shared__ double red[256];
     double s = 0.0;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -624,6 +717,7 @@ __global__ void norm_sq_partial(const float* __restrict__ x, int64_t n, double* 
 }
 
 __global__ void norm_sq_final(const double* __restrict__ part, int nb, double* out) {
+    ACCO_PDL_PROLOGUE();
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         double s = 0.0;
         for (int i = 0; i < nb; ++i) s += part[i];
@@ -638,6 +732,7 @@ struct Ranges {
 
 __global__ void pack_kernel(const float* __restrict__ flat, float* __restrict__ padded, Ranges r, int n,
                             uint64_t chunk) {
+    ACCO_PDL_PROLOGUE();
     const uint64_t total = chunk * n;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -650,6 +745,7 @@ __global__ void pack_kernel(const float* __restrict__ flat, float* __restrict__ 
 template <class E>
 __global__ void unpack_kernel(const E* __restrict__ padded, E* __restrict__ flat, Ranges r, int n,
                               uint64_t chunk) {
+    ACCO_PDL_PROLOGUE();
     const uint64_t total = chunk * n;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -677,6 +773,7 @@ __global__ void spin_kernel(uint64_t ns) {
 template <class T>
 __global__ void rope_kernel(T* __restrict__ qkv, int64_t ld, const float2* __restrict__ cs, int M, int seq, int nh,
                             int hd, float dir) {
+    ACCO_PDL_PROLOGUE();
     const int h2 = hd / 2;
     const int64_t n = static_cast<int64_t>(M) * nh * h2;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -697,6 +794,7 @@ __global__ void rope_kernel(T* __restrict__ qkv, int64_t ld, const float2* __res
 // bf16, 8 pairs per thread (16 B loads of each half)
 __global__ void rope_vec_kernel(__nv_bfloat16* __restrict__ qkv, int64_t ld, const float2* __restrict__ cs, int M,
                                 int seq, int nh, int hd, float dir) {
+    ACCO_PDL_PROLOGUE();
     const int h2 = hd / 2, nv = h2 / 8;
     const int64_t n = static_cast<int64_t>(M) * nh * nv;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -727,6 +825,7 @@ __device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + expf
 // a[m, j] = silu(gu[m, j]) * gu[m, F + j]
 template <class T>
 __global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ a, int M, int F) {
+    ACCO_PDL_PROLOGUE();
     const int64_t n = static_cast<int64_t>(M) * F;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -741,6 +840,7 @@ __global__ void swiglu_fwd_kernel(const T* __restrict__ gu, T* __restrict__ a, i
 template <class T>
 __global__ void swiglu_bwd_kernel(const T* __restrict__ da, const T* __restrict__ gu, T* __restrict__ dgu, int M,
                                   int F) {
+    ACCO_PDL_PROLOGUE();
     const int64_t n = static_cast<int64_t>(M) * F;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -755,6 +855,7 @@ __global__ void swiglu_bwd_kernel(const T* __restrict__ da, const T* __restrict_
 
 // bf16, 8 columns per thread (F % 8 == 0)
 __global__ void swiglu_fwd_vec(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ a, int M, int F) {
+    ACCO_PDL_PROLOGUE();
     const int fv = F / 8;
     const int64_t n = static_cast<int64_t>(M) * fv;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -772,6 +873,7 @@ __global__ void swiglu_fwd_vec(const __nv_bfloat16* __restrict__ gu, __nv_bfloat
 
 __global__ void swiglu_bwd_vec(const __nv_bfloat16* __restrict__ da, const __nv_bfloat16* __restrict__ gu,
                                __nv_bfloat16* __restrict__ dgu, int M, int F) {
+    ACCO_PDL_PROLOGUE();
     const int fv = F / 8;
     const int64_t n = static_cast<int64_t>(M) * fv;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -805,14 +907,14 @@ int grid_for(int64_t n, int threads = 256) {
 void gather_tokens(const int32_t* data, int seq, int n_samples, uint64_t seed, int mode, int start, int B,
                    int32_t* tok_in, int32_t* tok_out, int32_t* idx_out, cudaStream_t s) {
     ProfScope prof(kProfEmbed, 8.0 * B * seq, s);
-    gather_tokens_kernel<<<B, 128, 0, s>>>(data, seq, n_samples, seed, mode, start, tok_in, tok_out, idx_out);
+    launch_pdl(gather_tokens_kernel, B, 128, 0, s, data, seq, n_samples, seed, mode, start, tok_in, tok_out, idx_out);
     ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
 void embed_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int M, int seq, int d, cudaStream_t s) {
     ProfScope prof(kProfEmbed, 3.0 * M * d * sizeof(T), s);
-    embed_fwd_kernel<T><<<M, 128, 0, s>>>(tok, wte, wpe, x, seq, d);
+    launch_pdl(embed_fwd_kernel<T>, M, 128, 0, s, tok, wte, wpe, x, seq, d);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -825,16 +927,16 @@ static void layernorm_fwd_impl(const T* x, const T* g, const T* b, T* y, float* 
         if (a16(x) && a16(g) && a16(b) && a16(y) && d % 256 == 0) {
             const int grid = ceil_div(M, 8);
             switch (d / 256) {
-                case 1: ln_fwd_vec<1, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 2: ln_fwd_vec<2, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 3: ln_fwd_vec<3, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 4: ln_fwd_vec<4, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
-                case 8: ln_fwd_vec<8, RMS><<<grid, 256, 0, s>>>(x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 1: launch_pdl(ln_fwd_vec<1, RMS>, grid, 256, 0, s, x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 2: launch_pdl(ln_fwd_vec<2, RMS>, grid, 256, 0, s, x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 3: launch_pdl(ln_fwd_vec<3, RMS>, grid, 256, 0, s, x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 4: launch_pdl(ln_fwd_vec<4, RMS>, grid, 256, 0, s, x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
+                case 8: launch_pdl(ln_fwd_vec<8, RMS>, grid, 256, 0, s, x, g, b, y, mean, rstd, M); ACCO_CHECK_LAUNCH(); return;
                 default: break;
             }
         }
     }
-    ln_fwd_kernel<T, RMS><<<ceil_div(M, 8), 256, 0, s>>>(x, g, b, y, mean, rstd, M, d);
+    launch_pdl(ln_fwd_kernel<T, RMS>, ceil_div(M, 8), 256, 0, s, x, g, b, y, mean, rstd, M, d);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -855,11 +957,11 @@ static bool ln_bwd_dx_vec(const T* dy, const T* x, const T* g, const float* mean
         if (a16(dy) && a16(x) && a16(g) && a16(dx) && d % 256 == 0) {
             const int grid = ceil_div(M, 8), acc = accumulate_dx ? 1 : 0;
             switch (d / 256) {
-                case 1: ln_bwd_vec<1, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 2: ln_bwd_vec<2, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 3: ln_bwd_vec<3, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 4: ln_bwd_vec<4, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
-                case 8: ln_bwd_vec<8, RMS><<<grid, 256, 0, s>>>(dy, x, g, mean, rstd, dx, acc, M); break;
+                case 1: launch_pdl(ln_bwd_vec<1, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;
+                case 2: launch_pdl(ln_bwd_vec<2, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;
+                case 3: launch_pdl(ln_bwd_vec<3, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;
+                case 4: launch_pdl(ln_bwd_vec<4, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;
+                case 8: launch_pdl(ln_bwd_vec<8, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;
                 default: return false;
             }
             ACCO_CHECK_LAUNCH();
@@ -893,7 +995,7 @@ static void colsum_vec(const T* y, int64_t ld, const T* x, const float* mean, co
     int nchunk = std::max(1, std::min(ceil_div(8 * num_sms(), slabs), ceil_div(M, kVecRows)));
     const int rpc = ceil_div(ceil_div(M, nchunk), kVecRows) * kVecRows;
     nchunk = ceil_div(M, rpc);
-    colsum_vec_kernel<T, KIND><<<dim3(slabs, nchunk), 256, 0, s>>>(y, ld, x, mean, rstd, M, N, rpc, scratch,
+    launch_pdl(colsum_vec_kernel<T, KIND>, dim3(slabs, nchunk), 256, 0, s, y, ld, x, mean, rstd, M, N, rpc, scratch,
                                                                     tickets(), out, out1, acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
@@ -914,14 +1016,14 @@ void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const floa
     float* p0 = scratch;
     float* p1 = scratch + static_cast<int64_t>(nchunk) * d;
     if (bdst)
-        colreduce_partial<T, 1><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd,
+        launch_pdl(colreduce_partial<T, 1>, dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s, dy, d, x, mean, rstd,
                                                                                              M, d, p0, p1);
     else
-        colreduce_partial<T, 2><<<dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s>>>(dy, d, x, mean, rstd,
+        launch_pdl(colreduce_partial<T, 2>, dim3(ceil_div(d, 32), nchunk), dim3(32, kColRows), 0, s, dy, d, x, mean, rstd,
                                                                                              M, d, p0, p1);
     ACCO_CHECK_LAUNCH();
-    colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p0, nchunk, d, gdst, acc ? 1 : 0);
-    if (bdst) colreduce_final<<<ceil_div(d, 256), 256, 0, s>>>(p1, nchunk, d, bdst, acc ? 1 : 0);
+    launch_pdl(colreduce_final, ceil_div(d, 256), 256, 0, s, p0, nchunk, d, gdst, acc ? 1 : 0);
+    if (bdst) launch_pdl(colreduce_final, ceil_div(d, 256), 256, 0, s, p1, nchunk, d, bdst, acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -932,10 +1034,10 @@ void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, co
     const bool v = vec_ok<T>(dy, d, d) && vec_ok<T>(x, d, d);
     if (rms) {
         if (v && ln_bwd_dx_vec<true>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) return;
-        ln_bwd_kernel<T, true><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+        launch_pdl(ln_bwd_kernel<T, true>, ceil_div(M, 8), 256, 0, s, dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
     } else {
         if (v && ln_bwd_dx_vec<false>(dy, x, g, mean, rstd, dx, accumulate_dx, M, d, s)) return;
-        ln_bwd_kernel<T, false><<<ceil_div(M, 8), 256, 0, s>>>(dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
+        launch_pdl(ln_bwd_kernel<T, false>, ceil_div(M, 8), 256, 0, s, dy, x, g, mean, rstd, dx, accumulate_dx ? 1 : 0, M, d);
     }
     ACCO_CHECK_LAUNCH();
 }
@@ -948,10 +1050,10 @@ void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch
         return;
     }
     const int nchunk = ceil_div(M, kColChunk);
-    colreduce_partial<T, 0><<<dim3(ceil_div(N, 32), nchunk), dim3(32, kColRows), 0, s>>>(
+    launch_pdl(colreduce_partial<T, 0>, dim3(ceil_div(N, 32), nchunk), dim3(32, kColRows), 0, s, 
         y, ld, nullptr, nullptr, nullptr, M, N, scratch, nullptr);
     ACCO_CHECK_LAUNCH();
-    colreduce_final<<<ceil_div(N, 256), 256, 0, s>>>(scratch, nchunk, N, out, acc ? 1 : 0);
+    launch_pdl(colreduce_final, ceil_div(N, 256), 256, 0, s, scratch, nchunk, N, out, acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -962,25 +1064,23 @@ void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, i
     if constexpr (sizeof(T) == 2) {
         const bool aligned = (reinterpret_cast<uintptr_t>(logits) & 15) == 0 && ld % 8 == 0;
         if (aligned) {
-            ce_vec_kernel<<<M, 256, 0, s>>>(reinterpret_cast<__nv_bfloat16*>(logits), ld, target, V, 1.0f / seq,
+            launch_pdl(ce_vec_kernel, M, 256, 0, s, reinterpret_cast<__nv_bfloat16*>(logits), ld, target, V, 1.0f / seq,
                                             row_loss);
             ACCO_CHECK_LAUNCH();
             return;
         }
     }
-    ce_kernel<T><<<M, 512, 0, s>>>(logits, ld, target, V, 1.0f / seq, row_loss);
+    launch_pdl(ce_kernel<T>, M, 512, 0, s, logits, ld, target, V, 1.0f / seq, row_loss);
     ACCO_CHECK_LAUNCH();
 }
 
 void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s) {
-    loss_reduce_kernel<<<1, 256, 0, s>>>(row_loss, M, seq, out);
+    launch_pdl(loss_reduce_kernel, 1, 256, 0, s, row_loss, M, seq, out);
     ACCO_CHECK_LAUNCH();
 }
 
-template <class T>
-void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
-               uint32_t* sort_scratch, bool acc_wpe, cudaStream_t s, bool zero_wte) {
-    ProfScope prof(kProfEmbed, 1.0 * M * d * sizeof(T), s);
+void embed_sort(const int32_t* tok, int M, int V, uint32_t* sort_scratch, cudaStream_t s) {
+    ProfScope prof(kProfEmbed, 8.0 * M, s);
     ACCO_REQUIRE(static_cast<uint64_t>(V) * static_cast<uint64_t>(M) < 0xffffffffull,
                  "embed_bwd: vocab * tokens exceeds the 32-bit sort key");
     int P = 1;
@@ -991,15 +1091,25 @@ void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, fl
         ACCO_CUDA(cudaFuncSetAttribute(sort_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         configured = true;
     }
-    sort_keys_kernel<<<1, 1024, P * 4, s>>>(tok, M, P, sort_scratch);
+    launch_pdl(sort_keys_kernel, 1, 1024, P * 4, s, tok, M, P, sort_scratch);
     ACCO_CHECK_LAUNCH();
+}
+
+template <class T>
+void embed_bwd(const uint32_t* sorted, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
+               float* run_sum, bool acc_wpe, cudaStream_t s, bool zero_wte) {
+    ProfScope prof(kProfEmbed, 1.0 * M * d * sizeof(T), s);
+    ACCO_REQUIRE(d % 8 == 0, "embed_bwd: d_model must be a multiple of 8");
     // untied embedding (Llama) on the stage's first micro-batch: no earlier
     // kernel wrote grad_wte, so the rows no token touches must be zeroed
     if (zero_wte) ACCO_CUDA(cudaMemsetAsync(grad_wte, 0, static_cast<size_t>(V) * d * sizeof(float), s));
-    embed_bwd_wte_kernel<T><<<M, 128, 0, s>>>(sort_scratch, M, dx, d, grad_wte);
+    const int threads = std::min(256, std::max(32, d / 8));
+    launch_pdl(embed_runs_kernel<T>, ceil_div(M, kEmbChunk), threads, 0, s, sorted, M, dx, d, run_sum);
+    ACCO_CHECK_LAUNCH();
+    launch_pdl(embed_fold_kernel, M, threads, 0, s, sorted, M, run_sum, d, grad_wte);
     ACCO_CHECK_LAUNCH();
     if (grad_wpe) {
-        embed_bwd_wpe_kernel<T><<<seq, 128, 0, s>>>(dx, M / seq, seq, d, grad_wpe, acc_wpe ? 1 : 0);
+        launch_pdl(embed_bwd_wpe_kernel<T>, seq, 128, 0, s, dx, M / seq, seq, d, grad_wpe, acc_wpe ? 1 : 0);
         ACCO_CHECK_LAUNCH();
     }
 }
@@ -1012,12 +1122,12 @@ void rope_apply(T* qkv, int64_t ld, const float2* cs, int M, int seq, int nh, in
     if constexpr (sizeof(T) == 2) {
         if ((hd / 2) % 8 == 0 && ld % 8 == 0 && a16(qkv)) {
             const int64_t n = static_cast<int64_t>(M) * nh * (hd / 16);
-            rope_vec_kernel<<<grid_for(n), 256, 0, s>>>(qkv, ld, cs, M, seq, nh, hd, dir);
+            launch_pdl(rope_vec_kernel, grid_for(n), 256, 0, s, qkv, ld, cs, M, seq, nh, hd, dir);
             ACCO_CHECK_LAUNCH();
             return;
         }
     }
-    rope_kernel<T><<<grid_for(static_cast<int64_t>(M) * nh * (hd / 2)), 256, 0, s>>>(qkv, ld, cs, M, seq, nh, hd, dir);
+    launch_pdl(rope_kernel<T>, grid_for(static_cast<int64_t>(M) * nh * (hd / 2)), 256, 0, s, qkv, ld, cs, M, seq, nh, hd, dir);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1026,12 +1136,12 @@ void swiglu_fwd(const T* gu, T* a, int M, int F, cudaStream_t s) {
     ProfScope prof(kProfOther, 3.0 * M * F * sizeof(T), s);
     if constexpr (sizeof(T) == 2) {
         if (F % 8 == 0 && a16(gu) && a16(a)) {
-            swiglu_fwd_vec<<<grid_for(static_cast<int64_t>(M) * F / 8), 256, 0, s>>>(gu, a, M, F);
+            launch_pdl(swiglu_fwd_vec, grid_for(static_cast<int64_t>(M) * F / 8), 256, 0, s, gu, a, M, F);
             ACCO_CHECK_LAUNCH();
             return;
         }
     }
-    swiglu_fwd_kernel<T><<<grid_for(static_cast<int64_t>(M) * F), 256, 0, s>>>(gu, a, M, F);
+    launch_pdl(swiglu_fwd_kernel<T>, grid_for(static_cast<int64_t>(M) * F), 256, 0, s, gu, a, M, F);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1040,22 +1150,22 @@ void swiglu_bwd(const T* da, const T* gu, T* dgu, int M, int F, cudaStream_t s) 
     ProfScope prof(kProfOther, 5.0 * M * F * sizeof(T), s);
     if constexpr (sizeof(T) == 2) {
         if (F % 8 == 0 && a16(gu) && a16(da) && a16(dgu)) {
-            swiglu_bwd_vec<<<grid_for(static_cast<int64_t>(M) * F / 8), 256, 0, s>>>(da, gu, dgu, M, F);
+            launch_pdl(swiglu_bwd_vec, grid_for(static_cast<int64_t>(M) * F / 8), 256, 0, s, da, gu, dgu, M, F);
             ACCO_CHECK_LAUNCH();
             return;
         }
     }
-    swiglu_bwd_kernel<T><<<grid_for(static_cast<int64_t>(M) * F), 256, 0, s>>>(da, gu, dgu, M, F);
+    launch_pdl(swiglu_bwd_kernel<T>, grid_for(static_cast<int64_t>(M) * F), 256, 0, s, da, gu, dgu, M, F);
     ACCO_CHECK_LAUNCH();
 }
 
 void fill_i64(int64_t* p, int64_t v, cudaStream_t s) {
-    fill_i64_kernel<<<1, 1, 0, s>>>(p, v);
+    launch_pdl(fill_i64_kernel, 1, 1, 0, s, p, v);
     ACCO_CHECK_LAUNCH();
 }
 
 void add_i64(int64_t* dst, const int64_t* a, const int64_t* b, cudaStream_t s) {
-    add_i64_kernel<<<1, 1, 0, s>>>(dst, a, b);
+    launch_pdl(add_i64_kernel, 1, 1, 0, s, dst, a, b);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1063,27 +1173,27 @@ void sum_ordered(const float* const* in, int nin, float* out, int64_t n, cudaStr
     ACCO_REQUIRE(nin >= 1 && nin <= 16, "sum_ordered: 1..16 inputs");
     PtrList l{};
     for (int i = 0; i < nin; ++i) l.p[i] = in[i];
-    sum_ordered_kernel<<<grid_for(n), 256, 0, s>>>(l, nin, out, n);
+    launch_pdl(sum_ordered_kernel, grid_for(n), 256, 0, s, l, nin, out, n);
     ACCO_CHECK_LAUNCH();
 }
 
 void f32_to(const float* src, void* dst, int dtype, int64_t n, cudaStream_t s) {
     if (dtype == 1)
-        f32_to_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, s>>>(src, static_cast<__nv_bfloat16*>(dst), n);
+        launch_pdl(f32_to_kernel<__nv_bfloat16>, grid_for(n), 256, 0, s, src, static_cast<__nv_bfloat16*>(dst), n);
     else
-        f32_to_kernel<float><<<grid_for(n), 256, 0, s>>>(src, static_cast<float*>(dst), n);
+        launch_pdl(f32_to_kernel<float>, grid_for(n), 256, 0, s, src, static_cast<float*>(dst), n);
     ACCO_CHECK_LAUNCH();
 }
 
 void scale_f32(float* x, double alpha, int64_t n, cudaStream_t s) {
-    scale_kernel<<<grid_for(n), 256, 0, s>>>(x, static_cast<float>(alpha), n);
+    launch_pdl(scale_kernel, grid_for(n), 256, 0, s, x, static_cast<float>(alpha), n);
     ACCO_CHECK_LAUNCH();
 }
 
 void norm_sq(const float* x, int64_t n, double* out, double* scratch, cudaStream_t s) {
     const int nb = 256;
-    norm_sq_partial<<<nb, 256, 0, s>>>(x, n, scratch);
-    norm_sq_final<<<1, 32, 0, s>>>(scratch, nb, out);
+    launch_pdl(norm_sq_partial, nb, 256, 0, s, x, n, scratch);
+    launch_pdl(norm_sq_final, 1, 32, 0, s, scratch, nb, out);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1099,7 +1209,7 @@ static Ranges make_ranges(const uint64_t* lo, const uint64_t* sz, int n) {
 
 void pack_padded(const float* flat, float* padded, const uint64_t* lo, const uint64_t* sz, int n, uint64_t chunk,
                  cudaStream_t s) {
-    pack_kernel<<<grid_for(static_cast<int64_t>(chunk * n)), 256, 0, s>>>(flat, padded, make_ranges(lo, sz, n), n,
+    launch_pdl(pack_kernel, grid_for(static_cast<int64_t>(chunk * n)), 256, 0, s, flat, padded, make_ranges(lo, sz, n), n,
                                                                           chunk);
     ACCO_CHECK_LAUNCH();
 }
@@ -1109,9 +1219,9 @@ void unpack_padded(const void* padded, void* flat, int elem_bytes, const uint64_
     Ranges r = make_ranges(lo, sz, n);
     const int g = grid_for(static_cast<int64_t>(chunk * n));
     if (elem_bytes == 4)
-        unpack_kernel<float><<<g, 256, 0, s>>>(static_cast<const float*>(padded), static_cast<float*>(flat), r, n, chunk);
+        launch_pdl(unpack_kernel<float>, g, 256, 0, s, static_cast<const float*>(padded), static_cast<float*>(flat), r, n, chunk);
     else
-        unpack_kernel<__nv_bfloat16><<<g, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(padded),
+        launch_pdl(unpack_kernel<__nv_bfloat16>, g, 256, 0, s, static_cast<const __nv_bfloat16*>(padded),
                                                         static_cast<__nv_bfloat16*>(flat), r, n, chunk);
     ACCO_CHECK_LAUNCH();
 }
@@ -1132,7 +1242,7 @@ void spin_ns(uint64_t ns, cudaStream_t s) {
                                       int, cudaStream_t, bool);                                               \
     template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);             \
     template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
-    template void embed_bwd<T>(const int32_t*, const T*, int, int, int, int, float*, float*, uint32_t*,      \
+    template void embed_bwd<T>(const uint32_t*, const T*, int, int, int, int, float*, float*, float*,        \
                                bool, cudaStream_t, bool);                                                     \
     template void rope_apply<T>(T*, int64_t, const float2*, int, int, int, int, bool, cudaStream_t);          \
     template void swiglu_fwd<T>(const T*, T*, int, int, cudaStream_t);                                        \

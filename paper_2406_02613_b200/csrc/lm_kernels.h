@@ -49,13 +49,16 @@ void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, i
 // out[slot] = sum over rows of row_loss / seq (fixed order) = sum of sample losses.
 void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s);
 
-// Embedding backward: grad_wte[tok[m]] += dx[m] (sorted segments, ascending m),
-// grad_wpe[t] += sum_b dx[b*seq + t] (skipped when grad_wpe == nullptr);
-// zero_wte: grad_wte is zeroed first (untied embedding, first micro-batch).
+// Embedding backward, step 1 (token-only, so it runs early on a side
+// stream): sorted[i] = keys tok[m] * M + m in ascending order.
+void embed_sort(const int32_t* tok, int M, int V, uint32_t* sorted, cudaStream_t s);
+// Step 2: grad_wte[tok] += sum of dx rows of the token's segment (fixed
+// chunk/run order, run_sum = [M, d] fp32 scratch), grad_wpe[t] += sum_b
+// dx[b*seq + t] (skipped when grad_wpe == nullptr); zero_wte: grad_wte is
+// zeroed first (untied embedding, first micro-batch).
 template <class T>
-void embed_bwd(const int32_t* tok, const T* dx, int M, int seq, int d, int V, float* grad_wte,
-               float* grad_wpe, uint32_t* sort_scratch, bool accumulate_wpe, cudaStream_t s,
-               bool zero_wte = false);
+void embed_bwd(const uint32_t* sorted, const T* dx, int M, int seq, int d, int V, float* grad_wte,
+               float* grad_wpe, float* run_sum, bool accumulate_wpe, cudaStream_t s, bool zero_wte = false);
 
 // Rotary embedding in place on the first nh heads (q then k) of qkv [M, ld]:
 // pairs (i, i + hd/2), cs[t][i] = (cos, sin); inverse = the transpose (bwd).

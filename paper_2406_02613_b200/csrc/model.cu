@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace acco {
@@ -176,6 +177,7 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_CUDA(cudaMalloc(&tok_out_, M * sizeof(int32_t)));
     ACCO_CUDA(cudaMalloc(&idx_, c.max_batch * sizeof(int32_t)));
     ACCO_CUDA(cudaMalloc(&sort_, M * sizeof(uint32_t)));
+    ACCO_CUDA(cudaMalloc(&run_sum_, static_cast<size_t>(M) * d * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&row_loss_, M * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&stats_, (4 * L + 2) * M * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&lse_, L * H * M * sizeof(float)));
@@ -200,6 +202,7 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    ACCO_CUDA(cudaEventCreateWithFlags(&ev_sort_, cudaEventDisableTiming));
 }
 
 GPTModel::~GPTModel() {
@@ -209,6 +212,7 @@ GPTModel::~GPTModel() {
     cudaFree(tok_out_);
     cudaFree(idx_);
     cudaFree(sort_);
+    cudaFree(run_sum_);
     cudaFree(row_loss_);
     cudaFree(stats_);
     cudaFree(lse_);
@@ -218,6 +222,7 @@ GPTModel::~GPTModel() {
         cudaStreamDestroy(aux_);
         cudaEventDestroy(ev_fork_);
         cudaEventDestroy(ev_join_);
+        cudaEventDestroy(ev_sort_);
     }
     cudaFree(scratch_);
     if (rope_) cudaFree(rope_);
@@ -295,6 +300,21 @@ Epilogue ep_acc(float* c, int64_t ldc, int beta) {
 
 }  // namespace
 
+// The embedding-gradient sort needs only the tokens: it runs on the side
+// stream under the forward pass; embed_bwd waits on ev_sort_.
+void GPTModel::sort_tokens(int M, cudaStream_t s) {
+    static const bool serial = std::getenv("ACCO_SERIAL_REDUCE") != nullptr;
+    if (serial) {
+        embed_sort(tok_in_, M, c_.vocab, sort_, s);
+        ACCO_CUDA(cudaEventRecord(ev_sort_, s));
+        return;
+    }
+    ACCO_CUDA(cudaEventRecord(ev_fork_, s));
+    ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    embed_sort(tok_in_, M, c_.vocab, sort_, aux_);
+    ACCO_CUDA(cudaEventRecord(ev_sort_, aux_));
+}
+
 void GPTModel::stage_input(uint64_t seed, int mode, int start, int B, cudaStream_t s) {
     const int Tq = c_.seq_len;
     if (host_data() && mode == 0)
@@ -331,6 +351,7 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
                                                             //    6 ln2w 7 ln2b 8 Wfc 9 bfc 10 Wfc2 11 bfc2
 
     stage_input(seed, mode, start, B, s);
+    if (backward) sort_tokens(M, s);
     embed_fwd<T>(tok_in_, W(kWte), W(kWpe), X(0), M, Tq, d, s);
     for (int l = 0; l < L; ++l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
@@ -360,11 +381,16 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     // an outstanding reduction still reads (DX, DA, DT, DQKV). They share one
     // scratch area, so they are serialised on aux_ (FIFO) — same kernels and
     // summation order as inline, so results are bitwise unchanged.
+    // ACCO_SERIAL_REDUCE=1 (diagnostic A/B): the reductions run inline on s
+    static const bool serial = std::getenv("ACCO_SERIAL_REDUCE") != nullptr;
+    cudaStream_t aux_ = serial ? s : this->aux_;
     auto fork = [&] {
+        if (serial) return;
         ACCO_CUDA(cudaEventRecord(ev_fork_, s));
         ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
     };
     auto join = [&] {
+        if (serial) return;
         ACCO_CUDA(cudaEventRecord(ev_join_, aux_));
         ACCO_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     };
@@ -408,7 +434,8 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
         layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s);
     }
     // wte rows: the head wgrad above stored/added every row; the embedding adds
-    embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), sort_, acc, s);
+    ACCO_CUDA(cudaStreamWaitEvent(s, ev_sort_, 0));
+    embed_bwd<T>(sort_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), run_sum_, acc, s);
     join();  // the accumulator is complete when the compute stream passes this point
 }
 
@@ -444,6 +471,7 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
     auto lse_l = [&](int l) { return lse_ + static_cast<int64_t>(l) * H * Mmax; };
 
     stage_input(seed, mode, start, B, s);
+    if (backward) sort_tokens(M, s);
     embed_fwd<T>(tok_in_, W(kWte), nullptr, X(0), M, Tq, d, s);
     for (int l = 0; l < L; ++l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
@@ -466,11 +494,16 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
 
     const bool acc = accumulate_;
     const int beta = acc ? 1 : 0;
+    // ACCO_SERIAL_REDUCE=1 (diagnostic A/B): the reductions run inline on s
+    static const bool serial = std::getenv("ACCO_SERIAL_REDUCE") != nullptr;
+    cudaStream_t aux_ = serial ? s : this->aux_;
     auto fork = [&] {
+        if (serial) return;
         ACCO_CUDA(cudaEventRecord(ev_fork_, s));
         ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
     };
     auto join = [&] {
+        if (serial) return;
         ACCO_CUDA(cudaEventRecord(ev_join_, aux_));
         ACCO_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     };
@@ -507,7 +540,8 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
                                 aux_);
         layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s, true);
     }
-    embed_bwd<T>(tok_in_, DX, M, Tq, d, V, Gp(kWte), nullptr, sort_, acc, s, !acc);
+    ACCO_CUDA(cudaStreamWaitEvent(s, ev_sort_, 0));
+    embed_bwd<T>(sort_, DX, M, Tq, d, V, Gp(kWte), nullptr, run_sum_, acc, s, !acc);
     join();
 }
 

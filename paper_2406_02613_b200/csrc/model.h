@@ -84,6 +84,7 @@ private:
     void run_llama(const T* P, uint64_t seed, int mode, int start, int B, float* G, double* loss, bool backward,
                    cudaStream_t s);
     void stage_input(uint64_t seed, int mode, int start, int B, cudaStream_t s);
+    void sort_tokens(int M, cudaStream_t s);
 
     LMConfig c_;
     std::vector<ParamSpec> layout_;
@@ -93,6 +94,7 @@ private:
     int32_t* data_ = nullptr;
     int32_t *tok_in_ = nullptr, *tok_out_ = nullptr, *idx_ = nullptr;
     uint32_t* sort_ = nullptr;
+    float* run_sum_ = nullptr;  // embedding-gradient run sums [M, d]
     void* arena_ = nullptr;
     size_t arena_bytes_ = 0;
     float* row_loss_ = nullptr;
@@ -104,7 +106,7 @@ private:
     // side stream for the bias / LN-parameter column reductions: they only feed
     // the gradient accumulator, so they run beside the GEMMs (fork/join events)
     cudaStream_t aux_ = nullptr;
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_sort_ = nullptr;
     std::vector<char*> act_;    // activation slots (see model.cu)
     // host-data path
     int32_t* pinned_data_ = nullptr;

@@ -95,6 +95,7 @@ __device__ __forceinline__ float scale_grad(float g, float r, float inv, bool ha
 
 template <int KIND, bool COMMIT, bool HAS_RET, class OutT, bool VEC>
 __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
+    ACCO_PDL_PROLOGUE();
     int64_t tot = *a.total;
     if (HAS_RET && a.rtotal) tot += *a.rtotal;
     const float inv = static_cast<float>(1.0 / static_cast<double>(tot));
@@ -173,9 +174,9 @@ void launch_vec(const KArgs& a, bool vec, cudaStream_t s) {
     int blocks = static_cast<int>(std::min<int64_t>((work + threads - 1) / threads, cap));
     if (blocks < 1) blocks = 1;
     if (vec)
-        opt_kernel<KIND, COMMIT, HAS_RET, OutT, true><<<blocks, threads, 0, s>>>(a);
+        launch_pdl(opt_kernel<KIND, COMMIT, HAS_RET, OutT, true>, blocks, threads, 0, s, a);
     else
-        opt_kernel<KIND, COMMIT, HAS_RET, OutT, false><<<blocks, threads, 0, s>>>(a);
+        launch_pdl(opt_kernel<KIND, COMMIT, HAS_RET, OutT, false>, blocks, threads, 0, s, a);
     ACCO_CHECK_LAUNCH();
 }
 
