@@ -17,6 +17,7 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -796,57 +797,73 @@ constexpr int BW_SOFTMAX = 512;
 constexpr int BW_TILE = BW_T * HD * 2;             // 16 KB [128][64] bf16
 constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P / dS operand)
 // dKV smem: K, V (once) + 2 stages x (Q, dO) + lse/D (2 stages) + P^T + dS^T
-constexpr int DKV_ST = 3;  // Q/dO ring depth (hides the L2 latency of the next query tile's loads)
-constexpr int DKV_SMEM = 1024 + 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 2 * BW_SQ + 256;
+constexpr int DKV_ST = 2;  // Q/dO ring depth
+// K/V double-buffered (the next item's K/V loads under the current item)
+constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 2 * BW_SQ + 256 + 64;
 
-// dK/dV: one CTA per (batch*head, 128-key tile); loops over the query tiles
-// at and after the diagonal. Per query tile:
+// dK/dV, persistent: grid = #SMs; work item = (128-key tile kt, batch * KV
+// head), heaviest key tiles first (kt = 0 sees every query tile), dealt
+// round-robin. Per item the CTA loops over the query tiles at and after the
+// diagonal of each of the G = H / Hkv query heads of the group (GQA; G = 1 for
+// MHA). Per query tile:
 //   S^T = K Q^T, dP^T = V dO^T          (TMEM, 128 x 128 each)
 //   softmax-bwd warps (thread = key row): P^T = 2^(S^T sl - lse2[q]),
 //   dS^T = P^T (dP^T - D[q])  -> bf16 smem operands
 //   dV += P^T dO, dK += dS^T Q          (TMEM, 128 x 64 each; Q/dO MN-major B)
+// Barrier phases run over the CTA's global tile sequence, so the next item's
+// K/V load and first S^T/dP^T overlap the current item's last tile and the
+// dK/dV epilogue; a CTA launch + TMEM alloc + pipeline fill is paid once per SM
+// instead of once per item (it was ~7 us of a ~100 us kernel per wave).
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                   const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                  int T, int H, int Hkv, float scale) {
+                  int B, int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem;
-    uint8_t* sV = sK + BW_TILE;
-    uint8_t* sQ = sV + BW_TILE;            // [DKV_ST stages]
+    uint8_t* sK = smem;                    // [2 items]
+    uint8_t* sV = sK + 2 * BW_TILE;        // [2 items]
+    uint8_t* sQ = sV + 2 * BW_TILE;        // [DKV_ST stages]
     uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
     uint8_t* sPT = sO + DKV_ST * BW_TILE;  // P^T operand
     uint8_t* sDS = sPT + BW_SQ;            // dS^T operand
     float* sL = reinterpret_cast<float*>(sDS + BW_SQ);  // [2][128] lse (log2 domain)
     float* sD = sL + 2 * BW_T;                           // [2][128] D
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BW_T);
-    uint64_t* kv_full = bars;
-    uint64_t* q_full = bars + 1;            // [DKV_ST]
-    uint64_t* q_empty = q_full + DKV_ST;    // [DKV_ST]
-    uint64_t* s_full = q_empty + DKV_ST;    // S^T and dP^T ready
-    uint64_t* s_free = s_full + 1;     // softmax has them in registers
-    uint64_t* p_full = s_free + 1;     // P^T, dS^T in smem
-    uint64_t* g_done = p_full + 1;     // dV/dK MMAs of this tile done (operands free)
+    uint64_t* kv_full = bars;                 // [2]
+    uint64_t* kv_empty = bars + 2;            // [2]: every S^T/dP^T MMA of the item issued and done
+    uint64_t* q_full = bars + 4;              // [DKV_ST]
+    uint64_t* q_empty = q_full + DKV_ST;      // [DKV_ST]
+    uint64_t* s_full = q_empty + DKV_ST;      // S^T and dP^T ready
+    uint64_t* s_free = s_full + 1;            // softmax has them in registers
+    uint64_t* p_full = s_free + 1;            // P^T, dS^T in smem
+    uint64_t* g_done = p_full + 1;            // dV/dK MMAs of this tile done (operands free)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 1);
 
     const int nt = (T + BW_T - 1) / BW_T;
-    const int kt = blockIdx.x;
-    // one CTA per (batch * KV head, key tile): the G = H / Hkv query heads of
-    // the group are folded in ascending order (GQA; G = 1 for MHA), iteration
-    // it = g * nq + (query tile - kt)
-    const int bk = blockIdx.y, b = bk / Hkv, hk = bk % Hkv;
+    const int nbk = B * Hkv;
+    const int n_items = nt * nbk;
     const int G = H / Hkv;
     const int d = H * HD;
     const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
-    const int kc = d + hk * HD, vc = kc + Hkv * HD;
-    const int k0 = kt * BW_T;
-    const int row_base = b * T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nq = nt - kt;  // query tiles kt .. nt-1 per query head
-    const int niter = G * nq;
+    struct Item {
+        int kt, b, hk, nq;
+    };
+    auto item_of = [&](int u) {  // u < n_items: kt ascending = heaviest first
+        Item w;
+        w.kt = u / nbk;
+        const int bk = u % nbk;
+        w.b = bk / Hkv;
+        w.hk = bk % Hkv;
+        w.nq = nt - w.kt;  // query tiles kt .. nt-1 per query head
+        return w;
+    };
 
     if (threadIdx.x == 0) {
-        mbar_init(kv_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&kv_full[s], 1);
+            mbar_init(&kv_empty[s], 1);
+        }
         for (int s = 0; s < DKV_ST; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
@@ -873,30 +890,38 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(kv_full, 2 * BW_TILE);
-            tma_load_2d(sK, &tmQKV, kv_full, kc, row_base + k0);
-            tma_load_2d(sV, &tmQKV, kv_full, vc, row_base + k0);
-            for (int i = 0; i < niter; ++i) {
-                const int s = i % DKV_ST;
-                const int h = hk * G + i / nq;
-                const int q0 = (kt + i % nq) * BW_T;
-                mbar_wait(&q_empty[s], ((i / DKV_ST) & 1) ^ 1);
-                mbar_expect_tx(&q_full[s], 2 * BW_TILE);
-                tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
-                tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
+            int it = 0, ni = 0;
+            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+                const Item w = item_of(u);
+                const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
+                const int row_base = w.b * T;
+                const int kb = ni & 1;
+                mbar_wait(&kv_empty[kb], ((ni >> 1) & 1) ^ 1);  // item ni-2's S^T/dP^T MMAs are done with it
+                mbar_expect_tx(&kv_full[kb], 2 * BW_TILE);
+                tma_load_2d(sK + kb * BW_TILE, &tmQKV, &kv_full[kb], kc, row_base + w.kt * BW_T);
+                tma_load_2d(sV + kb * BW_TILE, &tmQKV, &kv_full[kb], vc, row_base + w.kt * BW_T);
+                const int niter = G * w.nq;
+                for (int i = 0; i < niter; ++i, ++it) {
+                    const int s = it % DKV_ST;
+                    const int h = w.hk * G + i / w.nq;
+                    const int q0 = (w.kt + i % w.nq) * BW_T;
+                    mbar_wait(&q_empty[s], ((it / DKV_ST) & 1) ^ 1);
+                    mbar_expect_tx(&q_full[s], 2 * BW_TILE);
+                    tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
+                    tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);  // K Q^T / V dO^T
             constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);    // P^T dO / dS^T Q (B MN-major)
-            const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
             const uint32_t pt_base = smem_u32(sPT), ds_base = smem_u32(sDS);
-            mbar_wait(kv_full, 0);
-            auto issue_s = [&](int i) {  // S^T = K Q_i^T, dP^T = V dO_i^T
-                const int s = i % DKV_ST;
-                mbar_wait(&q_full[s], (i / DKV_ST) & 1);
+            auto issue_s = [&](int g, int kb) {  // S^T = K Q_g^T, dP^T = V dO_g^T (global tile g, K/V slot kb)
+                const int s = g % DKV_ST;
+                mbar_wait(&q_full[s], (g / DKV_ST) & 1);
                 tc_after();
+                const uint32_t k_base = smem_u32(sK + kb * BW_TILE), v_base = smem_u32(sV + kb * BW_TILE);
                 const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
@@ -905,99 +930,142 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 }
                 umma_commit(s_full);
             };
-            issue_s(0);
-            for (int i = 0; i < niter; ++i) {
-                const int s = i % DKV_ST;
-                const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
-                if (i + 1 < niter) {  // next tile's S^T/dP^T overlap this tile's softmax
-                    mbar_wait(s_free, i & 1);
-                    issue_s(i + 1);
-                }
-                mbar_wait(p_full, i & 1);  // P^T / dS^T written
-                tc_after();
+            int it = 0, ni = 0;
+            if (static_cast<int>(blockIdx.x) < n_items) {
+                mbar_wait(&kv_full[0], 0);
+                issue_s(0, 0);
+            }
+            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+                const Item w = item_of(u);
+                const int niter = G * w.nq;
+                const int kb = ni & 1;
+                const bool more = u + static_cast<int>(gridDim.x) < n_items;
+                for (int i = 0; i < niter; ++i) {
+                    const int g = it + i;
+                    const int s = g % DKV_ST;
+                    const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
+                    // the next tile's S^T/dP^T (possibly the next item's first, whose
+                    // K/V is already in the other slot) overlap this tile's softmax
+                    if (i + 1 < niter) {
+                        mbar_wait(s_free, g & 1);
+                        tc_after();
+                        issue_s(g + 1, kb);
+                    } else {
+                        umma_commit(&kv_empty[kb]);  // every S^T/dP^T of this item issued
+                        if (more) {
+                            mbar_wait(&kv_full[kb ^ 1], ((ni + 1) >> 1) & 1);
+                            mbar_wait(s_free, g & 1);
+                            tc_after();
+                            issue_s(g + 1, kb ^ 1);
+                        }
+                    }
+                    mbar_wait(p_full, g & 1);  // P^T / dS^T written
+                    tc_after();
 #pragma unroll
-                for (int kk = 0; kk < BW_T / 16; ++kk) {
-                    umma(tDV, a128_desc(pt_base, kk), sdesc(o_base + kk * 2048, 64 * 128, 1024), id_g,
-                         (i > 0 || kk > 0) ? 1u : 0u);
-                    umma(tDK, a128_desc(ds_base, kk), sdesc(q_base + kk * 2048, 64 * 128, 1024), id_g,
-                         (i > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < BW_T / 16; ++kk) {
+                        umma(tDV, a128_desc(pt_base, kk), sdesc(o_base + kk * 2048, 64 * 128, 1024), id_g,
+                             (i > 0 || kk > 0) ? 1u : 0u);
+                        umma(tDK, a128_desc(ds_base, kk), sdesc(q_base + kk * 2048, 64 * 128, 1024), id_g,
+                             (i > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&q_empty[s]);
+                    umma_commit(g_done);
                 }
-                umma_commit(&q_empty[s]);
-                umma_commit(g_done);
+                it += niter;
             }
         }
     } else if (warp >= 4) {
         // 16 warps: quadrant wq (key rows = TMEM lanes) x quarter qq (32 of 128 queries)
         const int wq = warp & 3, qq = (warp - 4) >> 2;
-        const int r = wq * 32 + lane;  // key row = TMEM lane
-        const int key = k0 + r;
+        const int r = wq * 32 + lane;  // key row = TMEM lane (and, for the lse/D fetch, query column)
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
-        // lse (log2) and D of query tile i, loaded one tile ahead (registers)
+        // lse (log2) and D of the next tile, loaded one tile ahead (registers)
         // by the quarter-0 threads and published through a double-buffered smem row
-        auto fetch = [&](int i, float& lv, float& dv) {
-            const int q = (kt + i % nq) * BW_T + r;
-            const bool ok = i < niter && q < T;
-            const int64_t bh = static_cast<int64_t>(b) * H + hk * G + i / nq;
-            lv = ok ? __ldg(lse + bh * T + q) * kLog2e : 0.f;
-            dv = ok ? __ldg(dsum + bh * T + q) : 0.f;
+        auto fetch = [&](int u, int i, float& lv, float& dv) {
+            lv = dv = 0.f;
+            if (u >= n_items) return;
+            const Item w = item_of(u);
+            const int q = (w.kt + i % w.nq) * BW_T + r;
+            if (q >= T) return;
+            const int64_t bh = static_cast<int64_t>(w.b) * H + w.hk * G + i / w.nq;
+            lv = __ldg(lse + bh * T + q) * kLog2e;
+            dv = __ldg(dsum + bh * T + q);
         };
         float nl = 0.f, nd = 0.f;
-        if (qq == 0) fetch(0, nl, nd);
-        for (int i = 0; i < niter; ++i) {
-            const int s = i & 1;
-            const int qi = i % nq;
-            const int q0 = (kt + qi) * BW_T;
-            if (qq == 0) {
-                sL[s * BW_T + r] = nl;
-                sD[s * BW_T + r] = nd;
-            }
-            asm volatile("bar.sync 1, 512;" ::: "memory");  // softmax warps only
-            if (qq == 0) fetch(i + 1, nl, nd);  // latency hidden behind this tile
-            mbar_wait(s_full, i & 1);
-            tc_after();
-            // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
-            // rows past T belong to the next sequence)
-            const bool edge = qi == 0 || q0 + BW_T > T;
-            const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + qq * 32);
-            const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + qq * 32);
-            {
-                // S^T and dP^T (this warp's 32 columns each) go to registers first
-                // and their TMEM is released at once, so the MMA warp computes the
-                // next tile's S^T / dP^T under this tile's exp / dS math
-                uint32_t st[32], dp[32];
-                tmem_ld32(tS + lane_off + qq * 32, st);
-                tmem_ld32(tP + lane_off + qq * 32, dp);
-                tmem_wait_ld();
-                tc_before();
-                mbar_arrive(s_free);
-                float* p = reinterpret_cast<float*>(st);  // in place
-                // valid query columns c of this quarter: q0 + qq*32 + c in [key, T)
-                const int lo = key - (q0 + qq * 32), hi = T - (q0 + qq * 32);
-                if (edge)
-                    exp_cols32<true>(st, L4, sl, 0, lo, hi, p);
-                else
-                    exp_cols32<false>(st, L4, sl, 0, lo, hi, p);
-                float* ds = reinterpret_cast<float*>(dp);  // dS^T = P^T (dP^T - D), in place
-                ds_pairs(p, dp, reinterpret_cast<const float*>(D4), 32, ds);
-                if (i > 0) {  // the previous dV/dK MMAs have read the smem operands
-                    mbar_wait(g_done, (i - 1) & 1);
-                    tc_after();
+        if (qq == 0) fetch(blockIdx.x, 0, nl, nd);
+        int it = 0;
+        for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
+            const Item w = item_of(u);
+            const int niter = G * w.nq;
+            const int k0 = w.kt * BW_T;
+            const int key = k0 + r;
+            for (int i = 0; i < niter; ++i) {
+                const int g = it + i;
+                const int s = g & 1;
+                const int qi = i % w.nq;
+                const int q0 = (w.kt + qi) * BW_T;
+                if (qq == 0) {
+                    sL[s * BW_T + r] = nl;
+                    sD[s * BW_T + r] = nd;
                 }
-                st_row32_part(sPT, qq >> 1, r, qq & 1, p);
-                st_row32_part(sDS, qq >> 1, r, qq & 1, ds);
+                asm volatile("bar.sync 1, 512;" ::: "memory");  // softmax warps only
+                if (qq == 0) {  // latency hidden behind this tile
+                    if (i + 1 < niter)
+                        fetch(u, i + 1, nl, nd);
+                    else
+                        fetch(u + gridDim.x, 0, nl, nd);
+                }
+                mbar_wait(s_full, g & 1);
+                tc_after();
+                // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
+                // rows past T belong to the next sequence)
+                const bool edge = qi == 0 || q0 + BW_T > T;
+                const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + qq * 32);
+                const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + qq * 32);
+                {
+                    // S^T and dP^T (this warp's 32 columns each) go to registers first
+                    // and their TMEM is released at once, so the MMA warp computes the
+                    // next tile's S^T / dP^T under this tile's exp / dS math
+                    uint32_t st[32], dp[32];
+                    tmem_ld32(tS + lane_off + qq * 32, st);
+                    tmem_ld32(tP + lane_off + qq * 32, dp);
+                    tmem_wait_ld();
+                    tc_before();
+                    mbar_arrive(s_free);
+                    float* p = reinterpret_cast<float*>(st);  // in place
+                    // valid query columns c of this quarter: q0 + qq*32 + c in [key, T)
+                    const int lo = key - (q0 + qq * 32), hi = T - (q0 + qq * 32);
+                    if (edge)
+                        exp_cols32<true>(st, L4, sl, 0, lo, hi, p);
+                    else
+                        exp_cols32<false>(st, L4, sl, 0, lo, hi, p);
+                    float* ds = reinterpret_cast<float*>(dp);  // dS^T = P^T (dP^T - D), in place
+                    ds_pairs(p, dp, reinterpret_cast<const float*>(D4), 32, ds);
+                    if (i > 0) {  // the previous dV/dK MMAs have read the smem operands
+                        mbar_wait(g_done, (g - 1) & 1);
+                        tc_after();
+                    }
+                    st_row32_part(sPT, qq >> 1, r, qq & 1, p);
+                    st_row32_part(sDS, qq >> 1, r, qq & 1, ds);
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tc_before();
+                mbar_arrive(p_full);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            it += niter;
+            // item epilogue: every dV/dK MMA done (this also frees the smem operands
+            // and the accumulators for the next item's first tile)
+            mbar_wait(g_done, (it - 1) & 1);
+            tc_after();
+            uint32_t o[32];  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
+            const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
+            __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(w.b) * T + key) * ldq + (qq & 1) * 32;
+            tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
+            tmem_wait_ld();
             tc_before();
-            mbar_arrive(p_full);
+            if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
         }
-        mbar_wait(g_done, (niter - 1) & 1);
-        tc_after();
-        uint32_t o[32];  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
-        __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(b) * T + key) * ldq + (qq & 1) * 32;
-        tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
-        tmem_wait_ld();
-        if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
     }
     tc_before();
     __syncthreads();
@@ -1007,28 +1075,31 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     }
 }
 
-// dQ: one CTA per (batch*head, 128-query tile), loops over key tiles up to the
-// diagonal: S = Q K^T, dP = dO V^T (TMEM); thread = query row: P, dS -> smem;
-// dQ += dS K (K as MN-major B). Heavy tiles first.
-// K/V ring depth: a K/V tile is released only when dQ of the previous use has
-// been issued, so 2 stages exposed the L2 latency of every load
-constexpr int DQ_ST = 4;
-constexpr int DQ_SMEM = 1024 + 2 * BW_TILE + DQ_ST * 2 * BW_TILE + BW_SQ + 256;
+// dQ, persistent: grid = #SMs; work item = (128-query tile qt, batch*head),
+// heaviest (last) query tiles first, dealt round-robin. Per item: loop over
+// the key tiles up to the diagonal: S = Q K^T, dP = dO V^T (TMEM); thread =
+// query row: P, dS -> smem; dQ += dS K (K as MN-major B). Q/dO are
+// double-buffered across items and the next item's first S/dP is issued
+// under the current item's last tile (barrier phases follow the CTA's global
+// tile sequence), so CTA launch / TMEM alloc / pipeline fill are paid once.
+constexpr int DQ_ST = 3;  // K/V ring depth
+constexpr int DQ_SMEM = 1024 + 2 * 2 * BW_TILE + DQ_ST * 2 * BW_TILE + BW_SQ + 256 + 64;
 
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                 int T, int H, int Hkv, float scale) {
+                 int B, int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sO = sQ + BW_TILE;           // dO
-    uint8_t* sK = sO + BW_TILE;           // [DQ_ST stages]
+    uint8_t* sQ = smem;                   // [2 items]
+    uint8_t* sO = sQ + 2 * BW_TILE;       // dO [2 items]
+    uint8_t* sK = sO + 2 * BW_TILE;       // [DQ_ST stages]
     uint8_t* sV = sK + DQ_ST * BW_TILE;   // [DQ_ST stages]
     uint8_t* sDS = sV + DQ_ST * BW_TILE;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + BW_SQ);
-    uint64_t* q_full = bars;
-    uint64_t* kv_full = bars + 1;          // [DQ_ST]
+    uint64_t* q_full = bars;               // [2]
+    uint64_t* q_empty = bars + 2;          // [2]
+    uint64_t* kv_full = bars + 4;          // [DQ_ST]
     uint64_t* kv_empty = kv_full + DQ_ST;  // [DQ_ST]
     uint64_t* s_full = kv_empty + DQ_ST;
     uint64_t* s_free = s_full + 1;
@@ -1037,18 +1108,31 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 1);
 
     const int nt = (T + BW_T - 1) / BW_T;
-    const int qt = nt - 1 - blockIdx.x;
-    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    const int nbh = B * H;
+    const int n_items = nt * nbh;
     const int d = H * HD;
     const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
-    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;  // this head's K / V columns
-    const int q0 = qt * BW_T;
-    const int row_base = b * T;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nk = qt + 1;
+    struct Item {
+        int qt, b, h, nk, kc, vc;
+    };
+    auto item_of = [&](int u) {  // heaviest (last) query tiles first
+        Item w;
+        w.qt = nt - 1 - u / nbh;
+        const int bh = u % nbh;
+        w.b = bh / H;
+        w.h = bh % H;
+        w.nk = w.qt + 1;  // key tiles 0 .. qt
+        w.kc = d + (w.h / (H / Hkv)) * HD;  // this head's K / V columns
+        w.vc = w.kc + Hkv * HD;
+        return w;
+    };
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+        }
         for (int s = 0; s < DQ_ST; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
@@ -1075,27 +1159,34 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(q_full, 2 * BW_TILE);
-            tma_load_2d(sQ, &tmQKV, q_full, h * HD, row_base + q0);
-            tma_load_2d(sO, &tmDO, q_full, h * HD, row_base + q0);
-            for (int j = 0; j < nk; ++j) {
-                const int s = j % DQ_ST;
-                mbar_wait(&kv_empty[s], ((j / DQ_ST) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
-                tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], kc, row_base + j * BW_T);
-                tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], vc, row_base + j * BW_T);
+            int it = 0, ni = 0;
+            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+                const Item w = item_of(u);
+                const int row_base = w.b * T;
+                const int qb = ni & 1;
+                mbar_wait(&q_empty[qb], ((ni >> 1) & 1) ^ 1);  // item ni-2 is done with this Q/dO slot
+                mbar_expect_tx(&q_full[qb], 2 * BW_TILE);
+                tma_load_2d(sQ + qb * BW_TILE, &tmQKV, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
+                tma_load_2d(sO + qb * BW_TILE, &tmDO, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
+                for (int j = 0; j < w.nk; ++j, ++it) {
+                    const int s = it % DQ_ST;
+                    mbar_wait(&kv_empty[s], ((it / DQ_ST) & 1) ^ 1);
+                    mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
+                    tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], w.kc, row_base + j * BW_T);
+                    tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], w.vc, row_base + j * BW_T);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);
             constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);
-            const uint32_t q_base = smem_u32(sQ), o_base = smem_u32(sO), ds_base = smem_u32(sDS);
-            mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {  // S = Q K_j^T, dP = dO V_j^T
-                const int s = j % DQ_ST;
-                mbar_wait(&kv_full[s], (j / DQ_ST) & 1);
+            const uint32_t ds_base = smem_u32(sDS);
+            auto issue_s = [&](int g, int qb) {  // S = Q K_g^T, dP = dO V_g^T (global tile g, Q/dO slot qb)
+                const int s = g % DQ_ST;
+                mbar_wait(&kv_full[s], (g / DQ_ST) & 1);
                 tc_after();
+                const uint32_t q_base = smem_u32(sQ + qb * BW_TILE), o_base = smem_u32(sO + qb * BW_TILE);
                 const uint32_t k_base = smem_u32(sK + s * BW_TILE), v_base = smem_u32(sV + s * BW_TILE);
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {
@@ -1104,76 +1195,106 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 }
                 umma_commit(s_full);
             };
-            issue_s(0);
-            for (int j = 0; j < nk; ++j) {
-                const int s = j % DQ_ST;
-                const uint32_t k_base = smem_u32(sK + s * BW_TILE);
-                if (j + 1 < nk) {
-                    mbar_wait(s_free, j & 1);
-                    issue_s(j + 1);
-                }
-                mbar_wait(p_full, j & 1);
-                tc_after();
+            int it = 0, ni = 0;
+            if (static_cast<int>(blockIdx.x) < n_items) {
+                mbar_wait(&q_full[0], 0);
+                issue_s(0, 0);
+            }
+            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+                const Item w = item_of(u);
+                const int qb = ni & 1;
+                const bool more = u + static_cast<int>(gridDim.x) < n_items;
+                for (int j = 0; j < w.nk; ++j) {
+                    const int g = it + j;
+                    const int s = g % DQ_ST;
+                    const uint32_t k_base = smem_u32(sK + s * BW_TILE);
+                    if (j + 1 < w.nk) {
+                        mbar_wait(s_free, g & 1);
+                        tc_after();
+                        issue_s(g + 1, qb);
+                    } else {
+                        umma_commit(&q_empty[qb]);  // every S/dP of this item issued
+                        if (more) {  // the next item's first S/dP under this tile's softmax
+                            mbar_wait(&q_full[qb ^ 1], ((ni + 1) >> 1) & 1);
+                            mbar_wait(s_free, g & 1);
+                            tc_after();
+                            issue_s(g + 1, qb ^ 1);
+                        }
+                    }
+                    mbar_wait(p_full, g & 1);
+                    tc_after();
 #pragma unroll
-                for (int kk = 0; kk < BW_T / 16; ++kk)
-                    umma(tDQ, a128_desc(ds_base, kk), sdesc(k_base + kk * 2048, 64 * 128, 1024), id_g,
-                         (j > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&kv_empty[s]);
-                umma_commit(g_done);
+                    for (int kk = 0; kk < BW_T / 16; ++kk)
+                        umma(tDQ, a128_desc(ds_base, kk), sdesc(k_base + kk * 2048, 64 * 128, 1024), id_g,
+                             (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit(&kv_empty[s]);
+                    umma_commit(g_done);
+                }
+                it += w.nk;
             }
         }
     } else if (warp >= 4) {
         // 16 warps: quadrant wq (query rows = TMEM lanes) x quarter qq (32 of 128 keys)
         const int wq = warp & 3, qq = (warp - 4) >> 2;
         const int r = wq * 32 + lane;
-        const int q = q0 + r;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
-        const float L = q < T ? lse[static_cast<int64_t>(bh) * T + q] * kLog2e : 0.f;
-        const float Dq = q < T ? dsum[static_cast<int64_t>(bh) * T + q] : 0.f;
-        for (int j = 0; j < nk; ++j) {
-            mbar_wait(s_full, j & 1);
-            tc_after();
-            const bool diag = j == nk - 1;
-            {
-                // S and dP to registers first, TMEM released at once: the next
-                // tile's S / dP MMAs run under this tile's exp / dS math
-                uint32_t st[32], dp[32];
-                tmem_ld32(tS + lane_off + qq * 32, st);
-                tmem_ld32(tP + lane_off + qq * 32, dp);
-                tmem_wait_ld();
-                tc_before();
-                mbar_arrive(s_free);
-                float* p = reinterpret_cast<float*>(st);  // in place
-                // valid key columns c: j*128 + qq*32 + c <= q and < T
-                const int lim = min(q + 1, T) - (j * BW_T + qq * 32);
-                if (diag)
-                    exp_row64<true, 32>(st, sl, L, lim, p);
-                else
-                    exp_row64<false, 32>(st, sl, L, lim, p);
+        int it = 0;
+        for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
+            const Item w = item_of(u);
+            const int q = w.qt * BW_T + r;
+            const int64_t bh = static_cast<int64_t>(w.b) * H + w.h;
+            const float L = q < T ? __ldg(lse + bh * T + q) * kLog2e : 0.f;
+            const float Dq = q < T ? __ldg(dsum + bh * T + q) : 0.f;
+            for (int j = 0; j < w.nk; ++j) {
+                const int g = it + j;
+                mbar_wait(s_full, g & 1);
+                tc_after();
+                const bool diag = j == w.nk - 1;
                 {
-                    float dv[32];
+                    // S and dP to registers first, TMEM released at once: the next
+                    // tile's S / dP MMAs run under this tile's exp / dS math
+                    uint32_t st[32], dp[32];
+                    tmem_ld32(tS + lane_off + qq * 32, st);
+                    tmem_ld32(tP + lane_off + qq * 32, dp);
+                    tmem_wait_ld();
+                    tc_before();
+                    mbar_arrive(s_free);
+                    float* p = reinterpret_cast<float*>(st);  // in place
+                    // valid key columns c: j*128 + qq*32 + c <= q and < T
+                    const int lim = min(q + 1, T) - (j * BW_T + qq * 32);
+                    if (diag)
+                        exp_row64<true, 32>(st, sl, L, lim, p);
+                    else
+                        exp_row64<false, 32>(st, sl, L, lim, p);
+                    {
+                        float dv[32];
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) dv[c] = Dq;
-                    ds_pairs(p, dp, dv, 32, p);
+                        for (int c = 0; c < 32; ++c) dv[c] = Dq;
+                        ds_pairs(p, dp, dv, 32, p);
+                    }
+                    if (j > 0) {  // the previous dQ MMA has read dS
+                        mbar_wait(g_done, (g - 1) & 1);
+                        tc_after();
+                    }
+                    st_row32_part(sDS, qq >> 1, r, qq & 1, p);
                 }
-                if (j > 0) {  // the previous dQ MMA has read dS
-                    mbar_wait(g_done, (j - 1) & 1);
-                    tc_after();
-                }
-                st_row32_part(sDS, qq >> 1, r, qq & 1, p);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                tc_before();
+                mbar_arrive(p_full);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            it += w.nk;
+            // item epilogue: the last dQ MMA done (also frees dS and the accumulator)
+            mbar_wait(g_done, (it - 1) & 1);
+            tc_after();
+            if (qq < 2) {
+                uint32_t o[32];
+                tmem_ld32(tDQ + lane_off + qq * 32, o);
+                tmem_wait_ld();
+                if (q < T)
+                    st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * HD + qq * 32, o, scale);
+            }
             tc_before();
-            mbar_arrive(p_full);
-        }
-        mbar_wait(g_done, (nk - 1) & 1);
-        tc_after();
-        if (qq < 2) {
-            uint32_t o[32];
-            tmem_ld32(tDQ + lane_off + qq * 32, o);
-            tmem_wait_ld();
-            if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(b) * T + q) * ldq + h * HD + qq * 32, o, scale);
         }
     }
     tc_before();
@@ -1272,9 +1393,11 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nt = (T + BW_T - 1) / BW_T;
-    launch_pdl(fa_bwd_dkv_tc, dim3(nt, B * Hkv), BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
+    launch_pdl(fa_bwd_dkv_tc, std::min(nt * B * Hkv, num_sms()), BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, B, T,
+               H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
-    launch_pdl(fa_bwd_dq_tc, dim3(nt, B * H), BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, T, H, Hkv, scale);
+    launch_pdl(fa_bwd_dq_tc, std::min(nt * B * H, num_sms()), BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, B, T,
+               H, Hkv, scale);
     ACCO_CHECK_LAUNCH();
     return true;
 }
