@@ -797,9 +797,9 @@ constexpr int BW_SOFTMAX = 512;
 constexpr int BW_TILE = BW_T * HD * 2;             // 16 KB [128][64] bf16
 constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P / dS operand)
 // dKV smem: K, V (once) + 2 stages x (Q, dO) + lse/D (2 stages) + P^T + dS^T
-constexpr int DKV_ST = 2;  // Q/dO ring depth
+constexpr int DKV_ST = 4;  // Q/dO ring depth
 // K/V double-buffered (the next item's K/V loads under the current item)
-constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 2 * BW_SQ + 256 + 64;
+constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 256 + 64;
 
 // dK/dV, persistent: grid = #SMs; work item = (128-key tile kt, batch * KV
 // head), heaviest key tiles first (kt = 0 sees every query tile), dealt
@@ -824,9 +824,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint8_t* sV = sK + 2 * BW_TILE;        // [2 items]
     uint8_t* sQ = sV + 2 * BW_TILE;        // [DKV_ST stages]
     uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
-    uint8_t* sPT = sO + DKV_ST * BW_TILE;  // P^T operand
-    uint8_t* sDS = sPT + BW_SQ;            // dS^T operand
-    float* sL = reinterpret_cast<float*>(sDS + BW_SQ);  // [2][128] lse (log2 domain)
+    float* sL = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [2][128] lse (log2 domain)
     float* sD = sL + 2 * BW_T;                           // [2][128] D
     uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BW_T);
     uint64_t* kv_full = bars;                 // [2]
@@ -835,7 +833,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint64_t* q_empty = q_full + DKV_ST;      // [DKV_ST]
     uint64_t* s_full = q_empty + DKV_ST;      // S^T and dP^T ready
     uint64_t* s_free = s_full + 1;            // softmax has them in registers
-    uint64_t* p_full = s_free + 1;            // P^T, dS^T in smem
+    uint64_t* p_full = s_free + 1;            // P^T, dS^T (bf16) in TMEM
     uint64_t* g_done = p_full + 1;            // dV/dK MMAs of this tile done (operands free)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 1);
 
@@ -886,7 +884,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t tmem = *tslot;
     pdl_trigger();
     pdl_wait();
-    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320;
+    // TMEM: S^T | dP^T (fp32, 128 cols each) | dV | dK (64 each) | P^T | dS^T
+    // (bf16 pairs, 64 cols each): the dV/dK MMAs take A straight from TMEM, so
+    // P^T/dS^T never touch shared memory, and S^T/dP^T of the next tile can
+    // land while dV/dK of this one still read P^T/dS^T
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tPT = tmem + 384,
+                   tDST = tmem + 448;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -916,7 +919,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);  // K Q^T / V dO^T
             constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);    // P^T dO / dS^T Q (B MN-major)
-            const uint32_t pt_base = smem_u32(sPT), ds_base = smem_u32(sDS);
             auto issue_s = [&](int g, int kb) {  // S^T = K Q_g^T, dP^T = V dO_g^T (global tile g, K/V slot kb)
                 const int s = g % DKV_ST;
                 mbar_wait(&q_full[s], (g / DKV_ST) & 1);
@@ -962,11 +964,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     mbar_wait(p_full, g & 1);  // P^T / dS^T written
                     tc_after();
 #pragma unroll
-                    for (int kk = 0; kk < BW_T / 16; ++kk) {
-                        umma(tDV, a128_desc(pt_base, kk), sdesc(o_base + kk * 2048, 64 * 128, 1024), id_g,
-                             (i > 0 || kk > 0) ? 1u : 0u);
-                        umma(tDK, a128_desc(ds_base, kk), sdesc(q_base + kk * 2048, 64 * 128, 1024), id_g,
-                             (i > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < BW_T / 16; ++kk) {  // 16 queries = 8 packed TMEM columns per step
+                        umma_ts(tDV, tPT + kk * 8, sdesc(o_base + kk * 2048, 64 * 128, 1024), id_g,
+                                (i > 0 || kk > 0) ? 1u : 0u);
+                        umma_ts(tDK, tDST + kk * 8, sdesc(q_base + kk * 2048, 64 * 128, 1024), id_g,
+                                (i > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&q_empty[s]);
                     umma_commit(g_done);
@@ -1042,14 +1044,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                         exp_cols32<false>(st, L4, sl, 0, lo, hi, p);
                     float* ds = reinterpret_cast<float*>(dp);  // dS^T = P^T (dP^T - D), in place
                     ds_pairs(p, dp, reinterpret_cast<const float*>(D4), 32, ds);
-                    if (i > 0) {  // the previous dV/dK MMAs have read the smem operands
+                    uint32_t pk[16], dk[16];  // bf16 pairs: query 2c (low) and 2c+1 (high)
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        __nv_bfloat162 a = __floats2bfloat162_rn(p[2 * c], p[2 * c + 1]);
+                        __nv_bfloat162 e = __floats2bfloat162_rn(ds[2 * c], ds[2 * c + 1]);
+                        pk[c] = *reinterpret_cast<uint32_t*>(&a);
+                        dk[c] = *reinterpret_cast<uint32_t*>(&e);
+                    }
+                    if (i > 0) {  // the previous dV/dK MMAs have read P^T / dS^T
                         mbar_wait(g_done, (g - 1) & 1);
                         tc_after();
                     }
-                    st_row32_part(sPT, qq >> 1, r, qq & 1, p);
-                    st_row32_part(sDS, qq >> 1, r, qq & 1, ds);
+                    tmem_st16(tPT + lane_off + qq * 16, pk);
+                    tmem_st16(tDST + lane_off + qq * 16, dk);
+                    tmem_wait_st();
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_before();
                 mbar_arrive(p_full);
             }
