@@ -996,6 +996,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         };
         float nl = 0.f, nd = 0.f;
         if (qq == 0) fetch(blockIdx.x, 0, nl, nd);
+        // dK/dV of item `prev` leave TMEM -> global: deferred into the next
+        // item's first tile (after its exp/dS math, which overlaps the item's
+        // last dV/dK MMAs), or after the loop for the CTA's last item
+        int prev = -1;
+        auto epilogue = [&](int pu) {
+            const Item w = item_of(pu);
+            const int key = w.kt * BW_T + r;
+            uint32_t o[32];  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
+            const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
+            __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(w.b) * T + key) * ldq + (qq & 1) * 32;
+            tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
+            tmem_wait_ld();
+            if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
+        };
         int it = 0;
         for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
             const Item w = item_of(u);
@@ -1052,9 +1066,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                         pk[c] = *reinterpret_cast<uint32_t*>(&a);
                         dk[c] = *reinterpret_cast<uint32_t*>(&e);
                     }
-                    if (i > 0) {  // the previous dV/dK MMAs have read P^T / dS^T
+                    if (g > 0) {  // the previous dV/dK MMAs have read P^T / dS^T
                         mbar_wait(g_done, (g - 1) & 1);
                         tc_after();
+                    }
+                    if (i == 0 && prev >= 0) {  // previous item's accumulators are final
+                        epilogue(prev);
+                        prev = -1;
                     }
                     tmem_st16(tPT + lane_off + qq * 16, pk);
                     tmem_st16(tDST + lane_off + qq * 16, dk);
@@ -1064,17 +1082,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 mbar_arrive(p_full);
             }
             it += niter;
-            // item epilogue: every dV/dK MMA done (this also frees the smem operands
-            // and the accumulators for the next item's first tile)
+            prev = u;
+        }
+        if (prev >= 0) {
             mbar_wait(g_done, (it - 1) & 1);
             tc_after();
-            uint32_t o[32];  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
-            const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
-            __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(w.b) * T + key) * ldq + (qq & 1) * 32;
-            tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
-            tmem_wait_ld();
-            tc_before();
-            if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
+            epilogue(prev);
         }
     }
     tc_before();
@@ -1092,8 +1105,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 // double-buffered across items and the next item's first S/dP is issued
 // under the current item's last tile (barrier phases follow the CTA's global
 // tile sequence), so CTA launch / TMEM alloc / pipeline fill are paid once.
-constexpr int DQ_ST = 3;  // K/V ring depth
-constexpr int DQ_SMEM = 1024 + 2 * 2 * BW_TILE + DQ_ST * 2 * BW_TILE + BW_SQ + 256 + 64;
+constexpr int DQ_ST = 4;  // K/V ring depth
+constexpr int DQ_SMEM = 1024 + 2 * 2 * BW_TILE + DQ_ST * 2 * BW_TILE + 256 + 64;
 
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
@@ -1105,8 +1118,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint8_t* sO = sQ + 2 * BW_TILE;       // dO [2 items]
     uint8_t* sK = sO + 2 * BW_TILE;       // [DQ_ST stages]
     uint8_t* sV = sK + DQ_ST * BW_TILE;   // [DQ_ST stages]
-    uint8_t* sDS = sV + DQ_ST * BW_TILE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + BW_SQ);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + DQ_ST * BW_TILE);
     uint64_t* q_full = bars;               // [2]
     uint64_t* q_empty = bars + 2;          // [2]
     uint64_t* kv_full = bars + 4;          // [DQ_ST]
@@ -1165,7 +1177,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t tmem = *tslot;
     pdl_trigger();
     pdl_wait();
-    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256;
+    // TMEM: S | dP (fp32, 128 cols each) | dQ (64) | dS (bf16 pairs, 64): the dQ
+    // MMA takes A = dS straight from TMEM
+    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256, tDS = tmem + 320;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -1191,7 +1205,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);
             constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);
-            const uint32_t ds_base = smem_u32(sDS);
             auto issue_s = [&](int g, int qb) {  // S = Q K_g^T, dP = dO V_g^T (global tile g, Q/dO slot qb)
                 const int s = g % DQ_ST;
                 mbar_wait(&kv_full[s], (g / DQ_ST) & 1);
@@ -1234,9 +1247,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     mbar_wait(p_full, g & 1);
                     tc_after();
 #pragma unroll
-                    for (int kk = 0; kk < BW_T / 16; ++kk)
-                        umma(tDQ, a128_desc(ds_base, kk), sdesc(k_base + kk * 2048, 64 * 128, 1024), id_g,
-                             (j > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < BW_T / 16; ++kk)  // 16 keys = 8 packed TMEM columns per step
+                        umma_ts(tDQ, tDS + kk * 8, sdesc(k_base + kk * 2048, 64 * 128, 1024), id_g,
+                                (j > 0 || kk > 0) ? 1u : 0u);
                     umma_commit(&kv_empty[s]);
                     umma_commit(g_done);
                 }
@@ -1249,6 +1262,18 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int r = wq * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
+        // dQ of item `prev` leaves TMEM -> global inside the next item's first
+        // tile (after its math, overlapping the last dQ MMA), or after the loop
+        int prev = -1;
+        auto epilogue = [&](int pu) {
+            if (qq >= 2) return;
+            const Item w = item_of(pu);
+            const int q = w.qt * BW_T + r;
+            uint32_t o[32];
+            tmem_ld32(tDQ + lane_off + qq * 32, o);
+            tmem_wait_ld();
+            if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * HD + qq * 32, o, scale);
+        };
         int it = 0;
         for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
             const Item w = item_of(u);
@@ -1283,28 +1308,33 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                         for (int c = 0; c < 32; ++c) dv[c] = Dq;
                         ds_pairs(p, dp, dv, 32, p);
                     }
-                    if (j > 0) {  // the previous dQ MMA has read dS
+                    uint32_t pk[16];  // bf16 pairs: key 2c (low), 2c+1 (high)
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        __nv_bfloat162 e = __floats2bfloat162_rn(p[2 * c], p[2 * c + 1]);
+                        pk[c] = *reinterpret_cast<uint32_t*>(&e);
+                    }
+                    if (g > 0) {  // the previous dQ MMA has read dS
                         mbar_wait(g_done, (g - 1) & 1);
                         tc_after();
                     }
-                    st_row32_part(sDS, qq >> 1, r, qq & 1, p);
+                    if (j == 0 && prev >= 0) {  // previous item's dQ is final
+                        epilogue(prev);
+                        prev = -1;
+                    }
+                    tmem_st16(tDS + lane_off + qq * 16, pk);
+                    tmem_wait_st();
                 }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_before();
                 mbar_arrive(p_full);
             }
             it += w.nk;
-            // item epilogue: the last dQ MMA done (also frees dS and the accumulator)
+            prev = u;
+        }
+        if (prev >= 0) {
             mbar_wait(g_done, (it - 1) & 1);
             tc_after();
-            if (qq < 2) {
-                uint32_t o[32];
-                tmem_ld32(tDQ + lane_off + qq * 32, o);
-                tmem_wait_ld();
-                if (q < T)
-                    st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * HD + qq * 32, o, scale);
-            }
-            tc_before();
+            epilogue(prev);
         }
     }
     tc_before();
