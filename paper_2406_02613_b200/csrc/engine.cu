@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <string>
 #include <numeric>
 
 namespace acco {
@@ -103,8 +104,15 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
     }
     int lo_prio = 0, hi_prio = 0;
     ACCO_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    ACCO_CUDA(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, lo_prio));
-    ACCO_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, hi_prio));
+    // ACCO_COMM_PRIO: "low" puts the comm stream at the compute stream's priority,
+    // "inverted" below it (A/B knob; default: comm high, compute low)
+    int comm_prio = hi_prio, comp_prio = lo_prio;
+    if (const char* e = std::getenv("ACCO_COMM_PRIO")) {
+        if (std::string(e) == "low") comm_prio = lo_prio;
+        if (std::string(e) == "inverted") std::swap(comm_prio, comp_prio);
+    }
+    ACCO_CUDA(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, comp_prio));
+    ACCO_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, comm_prio));
     alloc();
     if (peer_) {  // exported to the peers: accumulators, then the two replicas
         rep_[0] = theta_act_;

@@ -38,8 +38,14 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one SW128 row
 constexpr int kThreads = 256;
 constexpr int kGroupM = 8;
-constexpr int kEpiWarpBytes = 8192;  // per epilogue warp: 2 x (out + in/aux) bf16 chunks, or 2 x fp32 chunks
-constexpr int kEpiBytes = 4 * kEpiWarpBytes;
+// Per epilogue warp: 2 bf16 output chunks (or 2 fp32 chunks spanning the
+// first 8 KB) + a ring of IN_BUF 2 KB input chunks (residual / GELU aux, TMA
+// prefetched IN_BUF chunks ahead: one chunk ahead left the HBM latency of
+// every chunk exposed). BN = 192 tiles have the smem for a 4-deep ring.
+template <int BN>
+constexpr int in_bufs() { return BN == 192 ? 4 : 2; }
+template <int BN>
+constexpr int epi_warp_bytes() { return 4096 + in_bufs<BN>() * 2048 > 8192 ? 4096 + in_bufs<BN>() * 2048 : 8192; }
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -171,7 +177,8 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + kEpiBytes + (2 * STAGES + 4 + 8) * 8 + 16;
+    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + 4 * epi_warp_bytes<BN>() +
+           (2 * STAGES + 4 + 4 * in_bufs<BN>()) * 8 + 16;
 }
 
 struct Sched {
@@ -265,12 +272,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint8_t* sEpi = sB + STAGES * B_BYTES;  // 1024-aligned
-    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + kEpiBytes);
+    constexpr int kInBuf = in_bufs<BN>();
+    constexpr int kEpiWarpBytes = epi_warp_bytes<BN>();
+    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 4 * kEpiWarpBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
-    uint64_t* inbar = tempty + 2;      // [4 warps][2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 8);
+    uint64_t* inbar = tempty + 2;      // [4 warps][kInBuf]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 4 * kInBuf);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -285,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
         }
-        for (int i = 0; i < 8; ++i) mbar_init(&inbar[i], 1);
+        for (int i = 0; i < 4 * kInBuf; ++i) mbar_init(&inbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -375,12 +384,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         const int wq = warp - 4;
         uint8_t* wbuf = sEpi + wq * kEpiWarpBytes;
-        uint64_t* ib = inbar + 2 * wq;
+        uint64_t* ib = inbar + kInBuf * wq;
         const bool f32 = ep.mode == kEpiAccF32;
         const bool has_in = !f32 && (ep.mode == kEpiDGelu || ep.residual != nullptr);
         const CUtensorMap* in_map = ep.mode == kEpiDGelu ? &em.aux : &em.res;
         const __nv_bfloat16* bias = static_cast<const __nv_bfloat16*>(ep.bias);
-        uint32_t in_phase = 0;  // bit b: parity of the next wait on input buffer b
+        uint32_t in_phase = 0;  // bit k: parity of the next wait on input buffer k
         constexpr int kChunks = BN / 32;
         int lt = 0;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
@@ -389,9 +398,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = lt & 1;
             const int row0 = mb * kBM + wq * 32;
             const int n0 = nb * BN;
-            if (has_in && lane == 0) {  // input chunk 0 of this tile
-                mbar_expect_tx(&ib[0], 2048);
-                tma_load_2d(wbuf + 4096, in_map, &ib[0], n0, row0);
+            if (has_in && lane == 0) {  // input chunks 0 .. kInBuf-1 of this tile
+#pragma unroll
+                for (int c = 0; c < kInBuf; ++c)
+                    if (c < kChunks) {
+                        mbar_expect_tx(&ib[c], 2048);
+                        tma_load_2d(wbuf + 4096 + c * 2048, in_map, &ib[c], n0 + c * 32, row0);
+                    }
+            }
+            // bias of chunk 0 (each chunk then prefetches the next chunk's bias)
+            uint4 bpre[4];
+            if (bias && n0 + 32 <= N) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + n0 + 8 * q));
             }
             // ordered split-K: this quadrant's rows are added in split order
             int* sem = split_sem ? split_sem + ((mb * sc.tiles_n + nb) * 4 + wq) * 32 : nullptr;  // own 128B line
@@ -406,10 +425,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int c = 0; c < kChunks; ++c) {
                 const int b = c & 1;
+                const int ibuf = c % kInBuf;
                 const int col0 = n0 + c * 32;
-                if (has_in && lane == 0 && c + 1 < kChunks) {  // next input chunk, one ahead
-                    mbar_expect_tx(&ib[b ^ 1], 2048);
-                    tma_load_2d(wbuf + 4096 + (b ^ 1) * 2048, in_map, &ib[b ^ 1], col0 + 32, row0);
+                uint4 bcur[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bcur[q] = bpre[q];
+                if (bias && c + 1 < kChunks && col0 + 64 <= N) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + col0 + 32 + 8 * q));
                 }
                 uint32_t raw[32];
                 tmem_ld32(tbase + c * 32, raw);
@@ -425,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (col0 + 32 <= N) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const uint4 u4 = *reinterpret_cast<const uint4*>(bias + col0 + 8 * q);
+                            const uint4 u4 = bcur[q];
                             const uint32_t w[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
@@ -441,16 +464,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (has_in) {
-                    mbar_wait(&ib[b], (in_phase >> b) & 1);
-                    in_phase ^= 1u << b;
+                    mbar_wait(&ib[ibuf], (in_phase >> ibuf) & 1);
+                    in_phase ^= 1u << ibuf;
                     float iv[32];
-                    ld_row_bf16(wbuf + 4096 + b * 2048, lane, iv);
+                    ld_row_bf16(wbuf + 4096 + ibuf * 2048, lane, iv);
                     if (ep.mode == kEpiDGelu) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(iv[i]);
                     } else {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] += iv[i];
+                    }
+                    __syncwarp();  // every lane has consumed the input buffer: refill it kInBuf chunks ahead
+                    if (lane == 0 && c + kInBuf < kChunks) {
+                        mbar_expect_tx(&ib[ibuf], 2048);
+                        tma_load_2d(wbuf + 4096 + ibuf * 2048, in_map, &ib[ibuf], col0 + kInBuf * 32, row0);
                     }
                 }
                 // the TMA store that last used these staging buffers (chunk c-2)

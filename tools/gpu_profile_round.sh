@@ -1,7 +1,9 @@
+#!/bin/bash
+# Round profile evidence: bench line, launch list of a bench step, full ncu captures of the top kernels.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 300 python tools/gemm_bench.py 768 > gpurun_out/gemm_bench_768.log 2>&1
-timeout 300 python tools/gemm_bench.py 1024 > gpurun_out/gemm_bench_1024.log 2>&1
-timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r01c.log 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_r01c.csv python bench.py --steps 2 --warmup 1 --profile --no-baselines --no-cpu-baseline > gpurun_out/bench_under_ncu2.log 2>&1
-tail -3 gpurun_out/bench_r01c.log
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full.log 2>&1
+tail -1 gpurun_out/bench_full.log | cut -c1-400
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --profile --no-baselines --no-cpu-baseline > gpurun_out/bench_under_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_tc_kernel|fa_|opt_kernel|ce_vec|ln_bwd_vec|colsum_vec" -s 40 -c 14 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 1 --profile --no-baselines --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+tail -2 gpurun_out/ncu_full.log
