@@ -228,7 +228,7 @@ int Trainer::stage_len(int p, int w, bool boot) const {
     if (sim_.schedule == kReplay) {
         const long long t = update_ + p / 2;
         const int half = p % 2;  // half 0: estimate, 1: main
-        const int gw = comm_ ? rank_ : w;
+        const int gw = (comm_ || peer_) ? rank_ : w;
         const size_t i = (static_cast<size_t>(t) * 2 + half) * sim_.n_workers + gw;
         ACCO_REQUIRE(i < sim_.replay.size(), "replay schedule shorter than the run");
         const int k = sim_.replay[i];
@@ -240,7 +240,7 @@ int Trainer::stage_len(int p, int w, bool boot) const {
 
 void Trainer::micro(int w, const void* params, uint64_t round, uint64_t tag, int ordinal, float* acc,
                     double* loss_slot) {
-    const uint64_t gw = comm_ ? static_cast<uint64_t>(rank_) : static_cast<uint64_t>(w);
+    const uint64_t gw = (comm_ || peer_) ? static_cast<uint64_t>(rank_) : static_cast<uint64_t>(w);
     const uint64_t seed = rng_derive(sim_.master_seed, gw, round, tag, static_cast<uint64_t>(ordinal));
     // the stage's first micro-batch overwrites the accumulator (Bundle::reset + add)
     model_->micro_batch(params, seed, 0, 0, sim_.batch_size, acc, loss_slot, cs_, ordinal > 0);
@@ -369,11 +369,13 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
         FoldIO io = fold_sources(acc_q, est ? g_ret_ : g_main_);
         ACCO_CUDA(cudaEventRecord(ev.rs_done[p], ms_));
         if (est) {  // estimate on a transient copy of the shard state (protocols.cpp:652-658)
-            if (!comm_ && n_local_ > 1) io.ret_out = g_ret_;  // retain the folded shard for the commit
+            // retain the folded shard for the commit (NCCL: the reduce-scatter already wrote it there)
+            if (peer_ || (!comm_ && n_local_ > 1)) io.ret_out = g_ret_;
             opt_gather(false, io, nullptr, totp, nullptr, est_act_, ag_est_, ev.opt_done[p]);
         } else {    // commit with the retained estimate shard (protocols.cpp:661-670)
             const int nacc = static_cast<int>(acc_.size()) / n_local_;
-            const float* ret = (comm_ || n_local_ > 1) ? g_ret_ : acc_[static_cast<size_t>((acc_q + nacc - 1) % nacc)];
+            const float* ret =
+                (comm_ || peer_ || n_local_ > 1) ? g_ret_ : acc_[static_cast<size_t>((acc_q + nacc - 1) % nacc)];
             opt_gather(true, io, ret, totp, totp - 1, theta_act_, ag_theta_, ev.opt_done[p]);
             ++step_;
         }
@@ -493,7 +495,7 @@ void Trainer::build_timeline(int n_phases, const PhaseEvents& ev, cudaEvent_t ba
     timeline_.clear();
     const int nl = n_local_;
     const size_t n_slots = slot_used.size();  // stage_k: [slot][local worker]
-    auto wid = [&](int w) { return comm_ ? rank_ : w; };
+    auto wid = [&](int w) { return (comm_ || peer_) ? rank_ : w; };
     for (size_t q = 0; q < n_slots; ++q) {
         if (!slot_used[q]) continue;
         for (int w = 0; w < nl; ++w) {

@@ -1,0 +1,83 @@
+"""Peer fabric at world size 2 on the one GPU gpurun provides: two processes
+(ranks 0 and 1, both on device 0) exchange CUDA-IPC handles over gloo and run
+the ACCO / ZeRO-1 comm phases through the fused fold + AdamW + replica-store
+kernel, with the cross-process device-flag counts and barriers — the
+multi-rank path of the N-GPU NVLink deployment, minus NVLink. Every rank's
+parameter history must match the fp64 oracle's 2-worker run (rel <= 1e-5 per
+update) and the two ranks' replicas must agree bitwise."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MINI = dict(vocab=64, d_model=32, n_layer=2, n_head=2, seq_len=16, n_samples=32, data_seed=3)
+
+WORKER = r'''
+import os, sys
+import numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+rank, world, port, method, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4], sys.argv[5]
+import torch
+import torch.distributed as dist
+torch.cuda.set_device(0)
+dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+from paper_2406_02613_b200 import api
+MINI = dict(vocab=64, d_model=32, n_layer=2, n_head=2, seq_len=16, n_samples=32, data_seed=3)
+peer = api.PeerComm(rank=rank, world=world, device=0)
+opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95, scheduler="cosine")
+sim = api.SimConfig(n_workers=world, batch_size=4, n_grad_accumulation=2, master_seed=7, eval_every=1)
+tr = api.run_protocol(method, api.LMConfig(**MINI, precision="fp32", max_batch=4), opt, sim, 3, comm=peer)
+np.save(os.path.join(out, f"th{rank}.npy"), np.array(tr.theta_history))
+np.save(os.path.join(out, f"est{rank}.npy"), np.array(tr.estimate_history))
+np.save(os.path.join(out, f"samples{rank}.npy"), np.array([r.samples_cum for r in tr.records]))
+dist.destroy_process_group()
+print("rank", rank, "ok", flush=True)
+'''
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("method", ["acco", "zero1", "dpu", "wp"])
+def test_peer_fabric_two_ranks_one_gpu(cuda, tmp_path, method):
+    from oracle import accosim_oracle as O
+    from oracle import gpt_oracle as G
+
+    port = str(_free_port())
+    env = dict(os.environ, ROOT=ROOT)
+    procs = [subprocess.Popen([sys.executable, "-c", WORKER, str(r), "2", port, method, str(tmp_path)], env=env,
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = []
+    try:
+        for p in procs:
+            outs.append(p.communicate(timeout=240)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o[-3000:]
+    th = [np.load(tmp_path / f"th{r}.npy") for r in range(2)]
+    assert np.array_equal(th[0], th[1])  # every rank holds the same replica
+    gc = G.GPTConfig(**MINI)
+    prob = G.LMProblem(gc)
+    th0 = G.default_theta0(gc, 7).astype(np.float32).astype(np.float64)
+    ocfg = O.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
+                             scheduler="cosine")
+    ref = O.run_method(method, (lambda t, s: prob.stochastic_grad(t, s, 4)), th0, ocfg, O.SimConfig(2, 4, 2, False, 7),
+                       3, eval_fn=prob.value_and_grad)
+    for t in range(3):
+        a, b = th[0][t + 1], ref.theta_history[t + 1]
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5, t
+    assert list(np.load(tmp_path / "samples0.npy")) == [r.samples_cum for r in ref.records]
