@@ -81,3 +81,20 @@ def test_parse_config_schema_and_validation():
     with pytest.raises(api.InvalidArgument):
         api.parse_config({k: v for k, v in j.items() if k != "t_updates"})
     assert len(api.config_hash(j)) == 16
+
+
+def test_parse_config_llama_problem():
+    """problem.kind "llama" (BASELINE.json config C4) maps onto the Llama block."""
+    j = {"problem": {"kind": "llama", "vocab": 32000, "d_model": 2048, "n_layer": 22, "n_head": 32, "n_kv_head": 4,
+                     "d_ff": 5632, "seq_len": 2048, "rope_base": 10000.0, "precision": "bf16"},
+         "method_name": "acco", "optimizer": {"kind": "adamw", "learning_rate": 3e-4},
+         "n_workers": 8, "batch_size": 4, "t_updates": 10,
+         "heterogeneity": {"worker_multipliers": [4, 1, 1, 1, 1, 1, 1, 1]}}
+    cfg = api.parse_config(j)
+    p = cfg.problem
+    assert (p.arch, p.n_kv_head, p.d_ff, p.rope_base) == ("llama", 4, 5632, 10000.0)
+    c = p.to_c()
+    assert (c.arch, c.n_kv_head, c.d_ff) == (1, 4, 5632)
+    assert cfg.sim.worker_multipliers == [4, 1, 1, 1, 1, 1, 1, 1]
+    with pytest.raises(api.InvalidArgument):
+        api.LMConfig(arch="mamba").to_c()
