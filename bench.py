@@ -166,6 +166,9 @@ def main():
     ap.add_argument("--schedule", default="adaptive", choices=["adaptive", "floor"])
     ap.add_argument("--fabric", default="nccl", choices=["nccl", "peer"],
                     help="comm phase: NCCL RS/AG around the fused optimizer, or the fused peer-memory fold kernel")
+    ap.add_argument("--straggler", type=float, default=1.0,
+                    help="C4 heterogeneous scenario: rank 0's micro-batches take this many times longer "
+                         "(HeterogeneityProfile multiplier, emulated by a measured spin after each micro-batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--profile", action="store_true", help="ncu-friendly: short run, no baselines")
@@ -202,6 +205,7 @@ def main():
     opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
                               scheduler="cosine", total_steps=1000)
     hbm, tf_sus, tf_burst, peak_kind = peaks()
+    mult = [args.straggler] + [1.0] * (world - 1) if args.straggler != 1.0 else None
 
     def barrier():
         torch.cuda.synchronize()
@@ -218,7 +222,7 @@ def main():
 
     def timed(method, k, schedule, profile=False, clocks=False):
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=k, master_seed=1,
-                            schedule=schedule, eval_every=0)
+                            schedule=schedule, eval_every=0, worker_multipliers=mult)
         tr = api.Trainer(method, model, opt, sim, make_comm(method))
         tr.set_theta(model.default_theta0(1))
         tr.run(args.warmup)
@@ -264,7 +268,7 @@ def main():
         lm_h = api.LMConfig(**cfgd, n_samples=n_samples, data_seed=1, precision="bf16", max_batch=B, host_data=True)
         model_h = api.Model(lm_h)
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=1, master_seed=1,
-                            schedule=args.schedule, eval_every=0)
+                            schedule=args.schedule, eval_every=0, worker_multipliers=mult)
         tr = api.Trainer("acco", model_h, opt, sim, make_comm("acco"))
         tr.set_theta(model_h.default_theta0(1))
         tr.run(args.warmup)
@@ -335,7 +339,9 @@ def main():
                    "parallelism": f"dp{world} ACCO (ZeRO-1-sharded fp32 AdamW states, " +
                                   ("NCCL RS/AG)" if args.fabric == "nccl" else
                                    "fused peer-memory fold+AdamW+replica-store kernel over NVLink)"),
-                   "l2": "inputs larger than L2 (bf16 params 249 MB + activations per step)"},
+                   "l2": "inputs larger than L2 (bf16 params 249 MB + activations per step)",
+                   **({"straggler": f"rank 0 x{args.straggler} (HeterogeneityProfile multiplier)"}
+                      if args.straggler != 1.0 else {})},
         "exposed_comm_pct": 100.0 * st["comm_exposed_ms"] / st["comm_busy_ms"] if st["comm_busy_ms"] else 0.0,
         "comm_busy_ms_per_step": st["comm_busy_ms"] / args.steps,
         "compute_busy_ms_per_step": st["compute_busy_ms"] / args.steps,

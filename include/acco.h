@@ -201,6 +201,12 @@ int acco_model_stochastic_grad(acco_model* m, const void* params, uint64_t strea
 int acco_model_value_and_grad(acco_model* m, const void* params, double* loss_out, float* grad_out,
                               void* stream);
 
+/* Device time of one micro-batch (fwd + bwd + accumulate) of `batch` samples,
+ * mean of `reps` (ns). Used to turn the reference's HeterogeneityProfile
+ * multipliers (protocols.hpp:19-27) into per-worker throttles: a worker with
+ * multiplier m spins (m - 1) x this after each micro-batch. */
+int acco_model_time_micro_batch(acco_model* m, int batch, int reps, double* ns_out);
+
 /* --------------------------------------------------------------- trainer
  * run_protocol (proj/include/accosim/protocols.hpp:89-90) on B200: one
  * process per GPU (comm != NULL, NCCL) or all workers as virtual workers on

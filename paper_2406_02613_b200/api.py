@@ -81,6 +81,7 @@ _lib.register({
     "acco_model_dataset": (C.c_int, [_P, _P]),
     "acco_model_stochastic_grad": (C.c_int, [_P, _P, C.c_uint64, C.c_int, _P, _P, _P]),
     "acco_model_value_and_grad": (C.c_int, [_P, _P, C.POINTER(C.c_double), _P, _P]),
+    "acco_model_time_micro_batch": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "acco_trainer_create": (C.c_int, [_P, C.POINTER(_lib.OptCfg), C.POINTER(SimCfgC), C.c_int, _P,
                                       C.POINTER(C.c_void_p)]),
     "acco_trainer_create_peer": (C.c_int, [_P, C.POINTER(_lib.OptCfg), C.POINTER(SimCfgC), C.c_int, _P,
@@ -217,6 +218,12 @@ class Model:
     @property
     def handle(self):
         return self._h
+
+    def time_micro_batch(self, batch: int, reps: int = 3) -> float:
+        """Device time (ns) of one micro-batch of `batch` samples."""
+        out = C.c_double()
+        _lib.call("acco_model_time_micro_batch", self._h, batch, reps, C.byref(out))
+        return out.value
 
     def default_theta0(self, master_seed: int) -> np.ndarray:
         out = np.empty(self.dim, dtype=np.float32)
@@ -369,8 +376,16 @@ class Trainer:
             self._replay = (C.c_int32 * len(flat))(*flat)
             rp, rl = self._replay, len(flat)
         self._thr = None
-        if sim.throttle_ns is not None:
-            self._thr = (C.c_double * sim.n_workers)(*sim.throttle_ns)
+        thr = sim.throttle_ns
+        if thr is None and sim.worker_multipliers is not None and any(m != 1.0 for m in sim.worker_multipliers):
+            # HeterogeneityProfile (protocols.hpp:19-27): worker w's micro-batch lasts
+            # m_w x the base time; on the GPU the slow worker spins (m_w - 1) x the
+            # measured micro-batch time after each micro-batch (m_w < 1: no speed-up)
+            t = model.time_micro_batch(sim.batch_size)
+            thr = [max(0.0, m - 1.0) * t for m in sim.worker_multipliers]
+        if thr is not None:
+            self._thr = (C.c_double * sim.n_workers)(*thr)
+        self.throttle_ns = thr
         s = SimCfgC(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, sim.warmup_rounds, sim.master_seed,
                     SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr)
         o = opt.to_c()
