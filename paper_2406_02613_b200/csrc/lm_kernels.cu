@@ -463,7 +463,29 @@ __global__ void __launch_bounds__(256) ce_vec_kernel(__nv_bfloat16* __restrict__
     const int nvec = (V + 7) / 8;
     const int nfull = V / 8;  // vectors with 8 valid elements
     float m = -INFINITY, s = 0.f;
-    for (int i = threadIdx.x; i < nvec; i += 256) {
+    // 4 independent 16 B loads in flight per thread (the loop was load-latency bound)
+    constexpr int U = 4;
+    int i0 = threadIdx.x;
+    for (; i0 + (U - 1) * 256 < nfull; i0 += U * 256) {
+        uint4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u] = L[i0 + u * 256];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float v[8];
+            unpack8(raw[u], v);
+            float lm = v[0];
+#pragma unroll
+            for (int k = 1; k < 8; ++k) lm = fmaxf(lm, v[k]);
+            if (lm > m) {
+                s *= __expf(m - lm);
+                m = lm;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += __expf(v[k] - m);
+        }
+    }
+    for (int i = i0; i < nvec; i += 256) {
         float v[8];
         unpack8(L[i], v);
         if (i >= nfull)
@@ -495,7 +517,39 @@ __global__ void __launch_bounds__(256) ce_vec_kernel(__nv_bfloat16* __restrict__
     for (int i = 0; i < 8; ++i) tot += red_m[i] == -INFINITY ? 0.f : red_s[i] * __expf(red_m[i] - gm);
     const float lse = gm + __logf(tot);
     const int tgt = target[row];
-    for (int i = threadIdx.x; i < nvec; i += 256) {
+    // pass 2 (L2 re-read), same 4-deep batching of the loads
+    int j0 = threadIdx.x;
+    for (; j0 + (U - 1) * 256 < nvec; j0 += U * 256) {
+        uint4 raw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) raw[u] = L[j0 + u * 256];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = j0 + u * 256;
+            float v[8];
+            unpack8(raw[u], v);
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float p0 = __expf(v[2 * k] - lse), p1 = __expf(v[2 * k + 1] - lse);
+                const int e0 = i * 8 + 2 * k;
+                if (e0 >= V) p0 = 0.f;
+                if (e0 + 1 >= V) p1 = 0.f;
+                if (e0 == tgt) {
+                    row_loss[row] = lse - v[2 * k];
+                    p0 -= 1.f;
+                }
+                if (e0 + 1 == tgt) {
+                    row_loss[row] = lse - v[2 * k + 1];
+                    p1 -= 1.f;
+                }
+                __nv_bfloat162 h = __floats2bfloat162_rn(p0 * inv_seq, p1 * inv_seq);
+                w[k] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            L[i] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+    for (int i = j0; i < nvec; i += 256) {
         float v[8];
         unpack8(L[i], v);
         uint32_t w[4];

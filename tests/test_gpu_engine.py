@@ -163,3 +163,26 @@ def test_run_continues_across_calls(cuda, method):
         assert _rel(hist[i, 0], ref.theta_history[i + 1]) <= 1e-5, i
         assert _rel(hist[i, 1], ref.estimate_history[i + 1]) <= 1e-5, i
     assert [r.samples_cum for r in r1 + r2] == [o.samples_cum for o in ref.records]
+
+
+def test_heterogeneity_multipliers_throttle_one_worker(cuda):
+    """HeterogeneityProfile (protocols.hpp:19-27): worker_multipliers become a
+    measured per-worker throttle; the math is unchanged (floor schedule) and
+    the slow worker's micro-batch intervals are ~m x longer on the timeline."""
+    cfg = dict(vocab=64, d_model=64, n_layer=2, n_head=2, seq_len=32, n_samples=32, data_seed=3)
+    opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
+                              scheduler="cosine")
+    base = api.SimConfig(n_workers=2, batch_size=4, n_grad_accumulation=2, master_seed=7)
+    slow = api.SimConfig(n_workers=2, batch_size=4, n_grad_accumulation=2, master_seed=7, worker_multipliers=[4.0, 1.0])
+    lm = api.LMConfig(**cfg, precision="fp32", max_batch=4)
+    ta = api.run_protocol("acco", lm, opt, base, 3)
+    tb = api.run_protocol("acco", lm, opt, slow, 3)
+    for t in range(3):
+        assert np.array_equal(ta.theta_history[t + 1], tb.theta_history[t + 1])
+
+    def mb_time(tr, w):
+        iv = [i for i in tr.timeline if i.stream == "compute" and i.worker == w and i.kind == "microbatch"]
+        return sum(i.t_end - i.t_start for i in iv) / max(1, sum(i.micro_batches for i in iv))
+
+    r = mb_time(tb, 0) / mb_time(tb, 1)
+    assert 2.5 < r < 6.0, r
