@@ -391,7 +391,7 @@ __device__ __forceinline__ void st_row32_global_fwd(__nv_bfloat16* dst, const ui
 }
 
 constexpr int F2_STAGES = 3;
-constexpr int F2_SMEM = 1024 + 2 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + 256;
+constexpr int F2_SMEM = 1024 + 4 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + 256;
 
 __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -473,17 +473,26 @@ __device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m
     }
 }
 
+// Persistent two-tile forward: grid = #SMs; work item = (pair of 128-query
+// tiles, batch*head), heaviest pairs first, dealt round-robin. Within an item
+// the two tiles share every K/V load and ping-pong on the tensor core (the
+// MMAs of one tile run under the other's softmax). Q is double-buffered
+// across items and the K/V ring, S/P, O barriers run over the CTA's whole
+// tile sequence, so CTA launch / TMEM alloc / pipeline fill are paid once per
+// SM. TMEM: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320),
+// O tile 1 [320,384).
 __global__ void __launch_bounds__(kThreads, 1)
     fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
-               int T, int H, int Hkv, float scale) {
+               int B, int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                         // [2 tiles]
-    uint8_t* sK = sQ + 2 * Q_BYTES;             // [stage]
+    uint8_t* sQ = smem;                         // [2 items][2 tiles]
+    uint8_t* sK = sQ + 4 * Q_BYTES;             // [stage]
     uint8_t* sV = sK + F2_STAGES * KV_BYTES;    // [stage]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + F2_STAGES * KV_BYTES);
-    uint64_t* q_full = bars;
-    uint64_t* kv_full = q_full + 1;              // [F2_STAGES]
+    uint64_t* q_full = bars;                     // [2 item slots]
+    uint64_t* q_empty = bars + 2;                // [2 item slots]
+    uint64_t* kv_full = bars + 4;                // [F2_STAGES]
     uint64_t* kv_empty = kv_full + F2_STAGES;    // [F2_STAGES]
     uint64_t* s_full = kv_empty + F2_STAGES;     // [2 tiles]
     uint64_t* p_full = s_full + 2;               // [2 tiles]
@@ -492,18 +501,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int nqt = (T + BQ - 1) / BQ;
     const int npair = (nqt + 1) / 2;
-    const int pr = npair - 1 - blockIdx.x;     // heavy pairs first
-    const int bh = blockIdx.y, b = bh / H, h = bh % H;
+    const int nbh = B * H;
+    const int n_items = npair * nbh;
     const int d = H * HD;
-    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
-    const int kc = d + (h / (H / Hkv)) * HD, vc = kc + Hkv * HD;  // this head's K / V columns
-    const int row_base = b * T;
-    const int nt[2] = {2 * pr + 1, 2 * pr + 2 <= nqt ? 2 * pr + 2 : 0};  // kv tiles per query tile (0: absent)
-    const int nkv = nt[1] ? nt[1] : nt[0];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    struct Item {
+        int pr, b, h, kc, vc, nt0, nt1, nkv;
+    };
+    auto item_of = [&](int u) {
+        Item w;
+        w.pr = npair - 1 - u / nbh;  // heavy pairs first
+        const int bh = u % nbh;
+        w.b = bh / H;
+        w.h = bh % H;
+        w.kc = d + (w.h / (H / Hkv)) * HD;  // this head's K / V columns
+        w.vc = w.kc + Hkv * HD;
+        w.nt0 = 2 * w.pr + 1;                               // kv tiles of query tile 0
+        w.nt1 = 2 * w.pr + 2 <= nqt ? 2 * w.pr + 2 : 0;     // of query tile 1 (0: absent)
+        w.nkv = w.nt1 ? w.nt1 : w.nt0;
+        return w;
+    };
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], 1);
+        }
         for (int s = 0; s < F2_STAGES; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
@@ -527,76 +550,98 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tslot;
     pdl_trigger();
     pdl_wait();
-    // columns: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320), O tile 1 [320,384)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(q_full, (nt[1] ? 2 : 1) * Q_BYTES);
-            tma_load_2d(sQ, &tmQKV, q_full, h * HD, row_base + 2 * pr * BQ);
-            if (nt[1]) tma_load_2d(sQ + Q_BYTES, &tmQKV, q_full, h * HD, row_base + (2 * pr + 1) * BQ);
-            for (int j = 0; j < nkv; ++j) {
-                const int s = j % F2_STAGES;
-                mbar_wait(&kv_empty[s], ((j / F2_STAGES) & 1) ^ 1);
-                mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
-                tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], kc, row_base + j * BKV);
-                tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], vc, row_base + j * BKV);
+            int kvit = 0, ni = 0;
+            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+                const Item w = item_of(u);
+                const int row_base = w.b * T;
+                const int qs = ni & 1;
+                mbar_wait(&q_empty[qs], ((ni >> 1) & 1) ^ 1);  // item ni-2's S MMAs are done with this slot
+                mbar_expect_tx(&q_full[qs], (w.nt1 ? 2 : 1) * Q_BYTES);
+                uint8_t* q_dst = sQ + qs * 2 * Q_BYTES;
+                tma_load_2d(q_dst, &tmQKV, &q_full[qs], w.h * HD, row_base + 2 * w.pr * BQ);
+                if (w.nt1) tma_load_2d(q_dst + Q_BYTES, &tmQKV, &q_full[qs], w.h * HD, row_base + (2 * w.pr + 1) * BQ);
+                for (int j = 0; j < w.nkv; ++j, ++kvit) {
+                    const int s = kvit % F2_STAGES;
+                    mbar_wait(&kv_empty[s], ((kvit / F2_STAGES) & 1) ^ 1);
+                    mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
+                    tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], w.kc, row_base + j * BKV);
+                    tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], w.vc, row_base + j * BKV);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
             constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
-            mbar_wait(q_full, 0);
-            auto issue_s = [&](int x, int j) {
-                const int s = j % F2_STAGES;
-                if (x == 0 || !nt[0] || j >= nt[0]) {  // first user of K_j waits for it
-                    mbar_wait(&kv_full[s], (j / F2_STAGES) & 1);
+            int kvit = 0, ni = 0;
+            int cnt[2] = {0, 0};  // tiles issued so far per slot (s_full / p_full phases)
+            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+                const Item w = item_of(u);
+                const int nt[2] = {w.nt0, w.nt1};
+                const int qs = ni & 1;
+                mbar_wait(&q_full[qs], (ni >> 1) & 1);
+                const uint32_t q_item = smem_u32(sQ + qs * 2 * Q_BYTES);
+                auto issue_s = [&](int x, int j) {
+                    const int s = (kvit + j) % F2_STAGES;
+                    if (x == 0 || !nt[0] || j >= nt[0]) {  // first user of K_j waits for it
+                        mbar_wait(&kv_full[s], ((kvit + j) / F2_STAGES) & 1);
+                        tc_after();
+                    }
+                    const uint32_t q_base = q_item + x * Q_BYTES, k_base = smem_u32(sK + s * KV_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < HD / 16; ++kk)
+                        umma(tmem + x * 128, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024),
+                             id_s, kk > 0);
+                    umma_commit(&s_full[x]);
+                };
+                auto issue_pv = [&](int x, int j) {
+                    const int s = (kvit + j) % F2_STAGES;
+                    mbar_wait(&p_full[x], (cnt[x] + j) & 1);
                     tc_after();
-                }
-                const uint32_t q_base = smem_u32(sQ + x * Q_BYTES), k_base = smem_u32(sK + s * KV_BYTES);
+                    const uint32_t v_base = smem_u32(sV + s * KV_BYTES);
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk)
-                    umma(tmem + x * 128, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024), id_s,
-                         kk > 0);
-                umma_commit(&s_full[x]);
-            };
-            auto issue_pv = [&](int x, int j) {
-                const int s = j % F2_STAGES;
-                mbar_wait(&p_full[x], j & 1);
-                tc_after();
-                const uint32_t v_base = smem_u32(sV + s * KV_BYTES);
-#pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {
-                    umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8, sdesc(v_base + kk * 2048, 64 * 128, 1024),
-                            id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < BKV / 16; ++kk) {
+                        umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8,
+                                sdesc(v_base + kk * 2048, 64 * 128, 1024), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                };
+                issue_s(0, 0);
+                if (nt[1]) issue_s(1, 0);
+                for (int j = 0; j < w.nkv; ++j) {
+                    for (int x = 0; x < 2; ++x) {
+                        if (j >= nt[x]) continue;
+                        issue_pv(x, j);
+                        if (j + 1 < nt[x]) issue_s(x, j + 1);
+                        else umma_commit(&o_done[x]);
+                    }
+                    if (j + 1 == w.nkv) umma_commit(&q_empty[qs]);  // every S of the item issued
+                    umma_commit(&kv_empty[(kvit + j) % F2_STAGES]);  // both tiles' PV_j issued
                 }
-            };
-            issue_s(0, 0);
-            if (nt[1]) issue_s(1, 0);
-            for (int j = 0; j < nkv; ++j) {
-                for (int x = 0; x < 2; ++x) {
-                    if (j >= nt[x]) continue;
-                    issue_pv(x, j);
-                    if (j + 1 < nt[x]) issue_s(x, j + 1);
-                    else umma_commit(&o_done[x]);
-                }
-                umma_commit(&kv_empty[j % F2_STAGES]);  // both tiles' PV_j issued: stage free on completion
+                kvit += w.nkv;
+                cnt[0] += nt[0];
+                cnt[1] += nt[1];
             }
         }
     } else if (warp >= 4) {
-        const int x = (warp - 4) >> 2;  // tile of this softmax group
+        const int x = (warp - 4) >> 2;  // tile slot of this softmax group
         const int wq = warp & 3;
-        const int n = nt[x];
-        if (n > 0) {
-            const int r = wq * 32 + lane;
-            const int q = (2 * pr + x) * BQ + r;
-            const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
-            const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
-            const float sl = scale * kLog2e;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
+        const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
+        const float sl = scale * kLog2e;
+        int cnt = 0, nitem = 0;  // tiles / items this slot has processed (barrier phases)
+        for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
+            const Item w = item_of(u);
+            const int n = x == 0 ? w.nt0 : w.nt1;
+            if (n == 0) continue;  // absent tile (odd tile count): no phases consumed
+            const int q = (2 * w.pr + x) * BQ + r;
             float m = -INFINITY;
             float2 l2 = make_float2(0.f, 0.f);  // fp32 row sum (even / odd keys), packed adds
             for (int j = 0; j < n; ++j) {
-                mbar_wait(&s_full[x], j & 1);
+                mbar_wait(&s_full[x], (cnt + j) & 1);
                 tc_after();
                 const bool diag = j == n - 1;  // the causal edge (and any ragged tail) sits in the last tile
                 const int kbase = j * BKV;
@@ -656,11 +701,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_before();
                 mbar_arrive(&p_full[x]);
             }
-            mbar_wait(&o_done[x], 0);
+            cnt += n;
+            mbar_wait(&o_done[x], nitem & 1);
+            ++nitem;
             tc_after();
             const float l = l2.x + l2.y;  // fp32 sum: lse stays consistent with the fp32 P of the backward
             const float inv = 1.f / l;
-            __nv_bfloat16* yr = y + (static_cast<int64_t>(b) * T + q) * d + h * HD;
+            __nv_bfloat16* yr = y + (static_cast<int64_t>(w.b) * T + q) * d + w.h * HD;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 uint32_t o[32];
@@ -668,7 +715,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_wait_ld();
                 if (q < T) st_row32_global_fwd(yr + c * 32, o, inv);
             }
-            if (q < T) lse[static_cast<int64_t>(bh) * T + q] = (m + log2f(l)) / kLog2e;
+            tc_before();
+            if (q < T) lse[(static_cast<int64_t>(w.b) * H + w.h) * T + q] = (m + log2f(l)) / kLog2e;
         }
     }
     tc_before();
@@ -1461,7 +1509,8 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
     if (std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
         launch_pdl(fa_fwd_tc, dim3(nqt, B * H), kThreads, SMEM, s, m, y, lse, T, H, Hkv, scale);
     } else {
-        launch_pdl(fa_fwd_tc2, dim3((nqt + 1) / 2, B * H), kThreads, F2_SMEM, s, m, y, lse, T, H, Hkv, scale);
+        launch_pdl(fa_fwd_tc2, std::min((nqt + 1) / 2 * B * H, num_sms()), kThreads, F2_SMEM, s, m, y, lse, B, T,
+                   H, Hkv, scale);
     }
     ACCO_CHECK_LAUNCH();
     return true;
