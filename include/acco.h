@@ -235,6 +235,11 @@ typedef struct acco_sim_cfg {
     int eval_every;             /* full-dataset loss/grad every k updates; 0 = never */
     int eval_batch;             /* samples per evaluation chunk; 0 = model max_batch */
     const double* throttle_ns;  /* [n_workers] straggler delay per micro-batch, or NULL */
+    /* Single-GPU emulation of an N-GPU interconnect: every comm phase spins this
+     * many ns on the comm stream after the counts all-reduce (the NVLink time of
+     * that phase's reduce-scatter + all-gather), so the overlap of ACCO vs the
+     * synchronous baselines can be measured on one GPU. 0 = off. */
+    double comm_delay_ns;
 } acco_sim_cfg;
 
 /* RoundRecord (protocols.hpp:41-53); NaN where not evaluated. */

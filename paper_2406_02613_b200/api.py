@@ -42,7 +42,7 @@ class SimCfgC(C.Structure):
     _fields_ = [("n_workers", C.c_int), ("batch_size", C.c_int), ("n_grad_accumulation", C.c_int),
                 ("warmup_rounds", C.c_int), ("master_seed", C.c_uint64), ("schedule", C.c_int),
                 ("replay", C.POINTER(C.c_int32)), ("replay_len", C.c_int), ("eval_every", C.c_int),
-                ("eval_batch", C.c_int), ("throttle_ns", C.POINTER(C.c_double))]
+                ("eval_batch", C.c_int), ("throttle_ns", C.POINTER(C.c_double)), ("comm_delay_ns", C.c_double)]
 
 
 class RecordC(C.Structure):
@@ -322,6 +322,7 @@ class SimConfig:
     eval_every: int = 1
     eval_batch: int = 0
     throttle_ns: Optional[Sequence[float]] = None
+    comm_delay_ns: float = 0.0  # emulated interconnect time per comm phase (single-GPU overlap study)
 
 
 @dataclass
@@ -387,7 +388,8 @@ class Trainer:
             self._thr = (C.c_double * sim.n_workers)(*thr)
         self.throttle_ns = thr
         s = SimCfgC(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, sim.warmup_rounds, sim.master_seed,
-                    SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr)
+                    SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr,
+                    float(sim.comm_delay_ns))
         o = opt.to_c()
         self._h = C.c_void_p()
         if isinstance(comm, PeerComm):

@@ -55,6 +55,8 @@ SimCfg to_sim(const acco_sim_cfg* sim) {
     s.eval_every = sim->eval_every;
     s.eval_batch = sim->eval_batch;
     if (sim->throttle_ns) s.throttle_ns.assign(sim->throttle_ns, sim->throttle_ns + sim->n_workers);
+    ACCO_REQUIRE(sim->comm_delay_ns >= 0.0, "sim: comm_delay_ns >= 0");
+    s.comm_delay_ns = sim->comm_delay_ns;
     return s;
 }
 }  // namespace

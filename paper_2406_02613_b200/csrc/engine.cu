@@ -364,6 +364,7 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
         fill_i64(totp, local, ms_);
     }
     ACCO_CUDA(cudaEventRecord(ev.cnt_done[p], ms_));
+    if (sim_.comm_delay_ns > 0) spin_ns(static_cast<uint64_t>(sim_.comm_delay_ns), ms_);  // emulated interconnect
     if (method_ == kACCO) {
         const bool est = p % 2 == 0;
         FoldIO io = fold_sources(acc_q, est ? g_ret_ : g_main_);

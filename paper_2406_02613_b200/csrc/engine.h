@@ -27,6 +27,7 @@ struct SimCfg {
     int eval_every = 0;              // 0: no full-dataset evaluation
     std::vector<double> throttle_ns; // per worker, extra ns after every micro-batch
     int eval_batch = 0;              // samples per evaluation chunk (0 = model max)
+    double comm_delay_ns = 0;        // emulated interconnect time per comm phase (0 = off)
 };
 
 struct UpdateRecord {
