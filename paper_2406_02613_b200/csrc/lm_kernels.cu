@@ -5,6 +5,7 @@
 #include "lm_kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace acco {
@@ -1046,7 +1047,8 @@ static void colsum_vec(const T* y, int64_t ld, const T* x, const float* mean, co
     const int slabs = ceil_div(N, 64);
     // ~8 blocks per SM: enough 16B loads in flight to stream the (L2-resident)
     // operand at bandwidth; partials are reduced by each slab's last block
-    int nchunk = std::max(1, std::min(ceil_div(8 * num_sms(), slabs), ceil_div(M, kVecRows)));
+    static const int per_sm = std::getenv("ACCO_COLSUM_PER_SM") ? std::atoi(std::getenv("ACCO_COLSUM_PER_SM")) : 4;
+    int nchunk = std::max(1, std::min(ceil_div(per_sm * num_sms(), slabs), ceil_div(M, kVecRows)));
     const int rpc = ceil_div(ceil_div(M, nchunk), kVecRows) * kVecRows;
     nchunk = ceil_div(M, rpc);
     launch_pdl(colsum_vec_kernel<T, KIND>, dim3(slabs, nchunk), 256, 0, s, y, ld, x, mean, rstd, M, N, rpc, scratch,
