@@ -21,6 +21,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
+#include <vector>
+#include <queue>
+#include <numeric>
+#include <map>
+#include <array>
 
 namespace acco {
 namespace {
@@ -31,6 +37,15 @@ constexpr int BKV = 128; // keys per tile (UMMA N of QK^T, K of PV)
 constexpr int kStages = 2;
 constexpr int kThreads = 384;  // warps 0-3: TMA, MMA, TMEM alloc, idle; 4-11: softmax (2 per TMEM quadrant)
 constexpr float kLog2e = 1.4426950408889634f;
+
+// Persistent kernels read their work items from a host-built LPT schedule:
+// sched[cta * k_max + k] = k-th item of this CTA (-1 past the end). Items are
+// assigned largest-first to the least-loaded CTA (cost = tiles of the item), so
+// the heavy diagonal-far items do not pile up on the CTAs that round-robin
+// dealing would give them to (GQA dK/dV: 1.56x -> ~1.1x of the mean load).
+__device__ __forceinline__ int item_at(const int* __restrict__ sched, int k_max, int k) {
+    return k < k_max ? __ldg(sched + static_cast<int64_t>(blockIdx.x) * k_max + k) : -1;
+}
 constexpr float kRescaleThresh = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 
 constexpr int Q_BYTES = BQ * HD * 2;          // 16 KB
@@ -483,7 +498,7 @@ __device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m
 // O tile 1 [320,384).
 __global__ void __launch_bounds__(kThreads, 1)
     fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
-               int B, int T, int H, int Hkv, float scale) {
+               int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                         // [2 items][2 tiles]
@@ -554,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             int kvit = 0, ni = 0;
-            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
                 const int qs = ni & 1;
@@ -578,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
             int kvit = 0, ni = 0;
             int cnt[2] = {0, 0};  // tiles issued so far per slot (s_full / p_full phases)
-            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int nt[2] = {w.nt0, w.nt1};
                 const int qs = ni & 1;
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
         const float sl = scale * kLog2e;
         int cnt = 0, nitem = 0;  // tiles / items this slot has processed (barrier phases)
-        for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
+        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
             const Item w = item_of(u);
             const int n = x == 0 ? w.nt0 : w.nt1;
             if (n == 0) continue;  // absent tile (odd tile count): no phases consumed
@@ -865,7 +880,7 @@ constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 *
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                   const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                  int B, int T, int H, int Hkv, float scale) {
+                  int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;                    // [2 items]
@@ -942,7 +957,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             int it = 0, ni = 0;
-            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
                 const int row_base = w.b * T;
@@ -981,15 +996,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 umma_commit(s_full);
             };
             int it = 0, ni = 0;
-            if (static_cast<int>(blockIdx.x) < n_items) {
+            if (item_at(sched, sk, 0) >= 0) {
                 mbar_wait(&kv_full[0], 0);
                 issue_s(0, 0);
             }
-            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int niter = G * w.nq;
                 const int kb = ni & 1;
-                const bool more = u + static_cast<int>(gridDim.x) < n_items;
+                const bool more = item_at(sched, sk, k + 1) >= 0;
                 for (int i = 0; i < niter; ++i) {
                     const int g = it + i;
                     const int s = g % DKV_ST;
@@ -1034,7 +1049,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         // by the quarter-0 threads and published through a double-buffered smem row
         auto fetch = [&](int u, int i, float& lv, float& dv) {
             lv = dv = 0.f;
-            if (u >= n_items) return;
+            if (u < 0 || u >= n_items) return;
             const Item w = item_of(u);
             const int q = (w.kt + i % w.nq) * BW_T + r;
             if (q >= T) return;
@@ -1043,7 +1058,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             dv = __ldg(dsum + bh * T + q);
         };
         float nl = 0.f, nd = 0.f;
-        if (qq == 0) fetch(blockIdx.x, 0, nl, nd);
+        if (qq == 0) fetch(item_at(sched, sk, 0), 0, nl, nd);
         // dK/dV of item `prev` leave TMEM -> global: deferred into the next
         // item's first tile (after its exp/dS math, which overlaps the item's
         // last dV/dK MMAs), or after the loop for the CTA's last item
@@ -1059,7 +1074,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
         };
         int it = 0;
-        for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
+        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
             const Item w = item_of(u);
             const int niter = G * w.nq;
             const int k0 = w.kt * BW_T;
@@ -1078,7 +1093,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     if (i + 1 < niter)
                         fetch(u, i + 1, nl, nd);
                     else
-                        fetch(u + gridDim.x, 0, nl, nd);
+                        fetch(item_at(sched, sk, k + 1), 0, nl, nd);
                 }
                 mbar_wait(s_full, g & 1);
                 tc_after();
@@ -1159,7 +1174,7 @@ constexpr int DQ_SMEM = 1024 + 2 * 2 * BW_TILE + DQ_ST * 2 * BW_TILE + 256 + 64;
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                 int B, int T, int H, int Hkv, float scale) {
+                 int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                   // [2 items]
@@ -1232,7 +1247,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             int it = 0, ni = 0;
-            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
                 const int qb = ni & 1;
@@ -1267,14 +1282,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 umma_commit(s_full);
             };
             int it = 0, ni = 0;
-            if (static_cast<int>(blockIdx.x) < n_items) {
+            if (item_at(sched, sk, 0) >= 0) {
                 mbar_wait(&q_full[0], 0);
                 issue_s(0, 0);
             }
-            for (int u = blockIdx.x; u < n_items; u += gridDim.x, ++ni) {
+            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int qb = ni & 1;
-                const bool more = u + static_cast<int>(gridDim.x) < n_items;
+                const bool more = item_at(sched, sk, k + 1) >= 0;
                 for (int j = 0; j < w.nk; ++j) {
                     const int g = it + j;
                     const int s = g % DQ_ST;
@@ -1323,7 +1338,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * HD + qq * 32, o, scale);
         };
         int it = 0;
-        for (int u = blockIdx.x; u < n_items; u += gridDim.x) {
+        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
             const Item w = item_of(u);
             const int q = w.qt * BW_T + r;
             const int64_t bh = static_cast<int64_t>(w.b) * H + w.h;
@@ -1455,6 +1470,77 @@ __global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_b
     }
 }
 
+// LPT schedule of `costs.size()` items over min(items, SMs) CTAs, cached per
+// (kernel kind, shape): device table [grid][k_max] (-1 padded).
+struct Schedule {
+    const int* table = nullptr;
+    int grid = 0, k_max = 0;
+};
+
+Schedule lpt_schedule(int kind, int nt, int nbh, int G) {
+    static std::mutex mu;
+    static std::map<std::array<int, 4>, Schedule> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const std::array<int, 4> key{kind, nt, nbh, G};
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    // item u -> cost (tiles processed + a fixed per-item overhead)
+    static const int ovh = std::getenv("ACCO_ATTN_OVH") ? std::atoi(std::getenv("ACCO_ATTN_OVH")) : 2;
+    std::vector<int> cost;
+    if (kind == 0) {  // forward: pair pr = npair - 1 - u / nbh; both tiles share K/V
+        const int npair = (nt + 1) / 2;
+        for (int u = 0; u < npair * nbh; ++u) {
+            const int pr = npair - 1 - u / nbh;
+            const int n0 = 2 * pr + 1, n1 = 2 * pr + 2 <= nt ? 2 * pr + 2 : 0;
+            cost.push_back(n0 + n1 + ovh);
+        }
+    } else if (kind == 1) {  // dK/dV: kt = u / nbh, G query heads x (nt - kt) tiles
+        for (int u = 0; u < nt * nbh; ++u) cost.push_back(G * (nt - u / nbh) + ovh);
+    } else {  // dQ: qt = nt - 1 - u / nbh, qt + 1 key tiles
+        for (int u = 0; u < nt * nbh; ++u) cost.push_back(nt - u / nbh + ovh);
+    }
+    const int n = static_cast<int>(cost.size());
+    const int grid = std::min(n, num_sms());
+    if (const char* e = std::getenv("ACCO_ATTN_SCHED")) {  // A/B knob: "rr" = round-robin heavy-first
+        if (std::string(e) == "rr") {
+            const int k_max = (n + grid - 1) / grid;
+            std::vector<int> host(static_cast<size_t>(grid) * k_max, -1);
+            for (int u = 0; u < n; ++u) host[static_cast<size_t>(u % grid) * k_max + u / grid] = u;
+            int* dev = nullptr;
+            ACCO_CUDA(cudaMalloc(&dev, host.size() * sizeof(int)));
+            ACCO_CUDA(cudaMemcpy(dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice));
+            Schedule sc{dev, grid, k_max};
+            cache[key] = sc;
+            return sc;
+        }
+    }
+    std::vector<int> order(static_cast<size_t>(n));
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    std::vector<std::vector<int>> lists(static_cast<size_t>(grid));
+    using Load = std::pair<long long, int>;  // (load, cta): least-loaded first, ties by CTA index
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> pq;
+    for (int c = 0; c < grid; ++c) pq.push({0, c});
+    for (int u : order) {
+        Load l = pq.top();
+        pq.pop();
+        lists[static_cast<size_t>(l.second)].push_back(u);
+        pq.push({l.first + cost[u], l.second});
+    }
+    int k_max = 0;
+    for (auto& v : lists) k_max = std::max(k_max, static_cast<int>(v.size()));
+    std::vector<int> host(static_cast<size_t>(grid) * k_max, -1);
+    for (int c = 0; c < grid; ++c)
+        for (size_t k = 0; k < lists[static_cast<size_t>(c)].size(); ++k)
+            host[static_cast<size_t>(c) * k_max + k] = lists[static_cast<size_t>(c)][k];
+    int* dev = nullptr;
+    ACCO_CUDA(cudaMalloc(&dev, host.size() * sizeof(int)));
+    ACCO_CUDA(cudaMemcpy(dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice));
+    Schedule sc{dev, grid, k_max};
+    cache[key] = sc;
+    return sc;
+}
+
 bool tc_applicable(const void* a, const void* b, int hd) {
     return hd == HD && !(reinterpret_cast<uintptr_t>(a) & 15) && !(reinterpret_cast<uintptr_t>(b) & 15) &&
            !std::getenv("ACCO_ATTN_LEGACY");
@@ -1481,11 +1567,13 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nt = (T + BW_T - 1) / BW_T;
-    launch_pdl(fa_bwd_dkv_tc, std::min(nt * B * Hkv, num_sms()), BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, B, T,
-               H, Hkv, scale);
+    const Schedule skv = lpt_schedule(1, nt, B * Hkv, H / Hkv);
+    launch_pdl(fa_bwd_dkv_tc, skv.grid, BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
+               skv.table, skv.k_max);
     ACCO_CHECK_LAUNCH();
-    launch_pdl(fa_bwd_dq_tc, std::min(nt * B * H, num_sms()), BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, B, T,
-               H, Hkv, scale);
+    const Schedule sq = lpt_schedule(2, nt, B * H, 1);
+    launch_pdl(fa_bwd_dq_tc, sq.grid, BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale, sq.table,
+               sq.k_max);
     ACCO_CHECK_LAUNCH();
     return true;
 }
@@ -1509,8 +1597,8 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
     if (std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
         launch_pdl(fa_fwd_tc, dim3(nqt, B * H), kThreads, SMEM, s, m, y, lse, T, H, Hkv, scale);
     } else {
-        launch_pdl(fa_fwd_tc2, std::min((nqt + 1) / 2 * B * H, num_sms()), kThreads, F2_SMEM, s, m, y, lse, B, T,
-                   H, Hkv, scale);
+        const Schedule sf = lpt_schedule(0, nqt, B * H, 1);
+        launch_pdl(fa_fwd_tc2, sf.grid, kThreads, F2_SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table, sf.k_max);
     }
     ACCO_CHECK_LAUNCH();
     return true;
