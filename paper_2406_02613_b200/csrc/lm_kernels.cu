@@ -226,6 +226,59 @@ __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bflo
     }
 }
 
+// Wide rows (d >= 1024): one block of d/8 threads per row, 8 elements (16 B)
+// per thread, block reductions through smem — instead of one warp holding 64
+// elements per lane (register-bound, latency-exposed at d = 2048).
+template <int NT, bool RMS>
+__global__ void __launch_bounds__(NT) ln_bwd_wide(const __nv_bfloat16* __restrict__ dy,
+                                                  const __nv_bfloat16* __restrict__ x,
+                                                  const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
+                                                  const float* __restrict__ rstd, __nv_bfloat16* __restrict__ dx,
+                                                  int accumulate) {
+    ACCO_PDL_PROLOGUE();
+    constexpr int d = NT * 8, NW = NT / 32;
+    __shared__ float red[2][NW];
+    const int row = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t o = static_cast<int64_t>(row) * d;
+    const float mu = mean[row], rs = rstd[row];
+    float xh[8], dxh[8], gv[8], dv[8];
+    unpack8b(reinterpret_cast<const uint4*>(x + o)[t], xh);
+    unpack8b(reinterpret_cast<const uint4*>(dy + o)[t], dv);
+    unpack8b(reinterpret_cast<const uint4*>(g)[t], gv);
+    float prev[8];
+    if (accumulate) unpack8b(reinterpret_cast<const uint4*>(dx + o)[t], prev);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        xh[k] = (xh[k] - mu) * rs;
+        dxh[k] = dv[k] * gv[k];
+        s1 += dxh[k];
+        s2 += dxh[k] * xh[k];
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+        red[0][w] = s1;
+        red[1][w] = s2;
+    }
+    __syncthreads();
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {  // fixed order: deterministic
+        t1 += red[0][i];
+        t2 += red[1][i];
+    }
+    t1 = RMS ? 0.f : t1 / d;
+    t2 /= d;
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        r[k] = rs * (dxh[k] - t1 - xh[k] * t2);
+        if (accumulate) r[k] += prev[k];
+    }
+    reinterpret_cast<uint4*>(dx + o)[t] = pack8b(r);
+}
+
 // ------------------------------------------------ deterministic column reduce
 // partial[chunk][col] = sum over rows of the chunk (fixed order), then
 // out[col] += sum_chunk partial[chunk][col] (fixed order).
@@ -1011,6 +1064,14 @@ static bool ln_bwd_dx_vec(const T* dy, const T* x, const T* g, const float* mean
     if constexpr (sizeof(T) == 2) {
         if (a16(dy) && a16(x) && a16(g) && a16(dx) && d % 256 == 0) {
             const int grid = ceil_div(M, 8), acc = accumulate_dx ? 1 : 0;
+            if (d >= 1024 && !std::getenv("ACCO_LN_NARROW")) {
+                switch (d) {
+                    case 1024: launch_pdl(ln_bwd_wide<128, RMS>, M, 128, 0, s, dy, x, g, mean, rstd, dx, acc); ACCO_CHECK_LAUNCH(); return true;
+                    case 2048: launch_pdl(ln_bwd_wide<256, RMS>, M, 256, 0, s, dy, x, g, mean, rstd, dx, acc); ACCO_CHECK_LAUNCH(); return true;
+                    case 4096: launch_pdl(ln_bwd_wide<512, RMS>, M, 512, 0, s, dy, x, g, mean, rstd, dx, acc); ACCO_CHECK_LAUNCH(); return true;
+                    default: break;
+                }
+            }
             switch (d / 256) {
                 case 1: launch_pdl(ln_bwd_vec<1, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;
                 case 2: launch_pdl(ln_bwd_vec<2, RMS>, grid, 256, 0, s, dy, x, g, mean, rstd, dx, acc, M); break;

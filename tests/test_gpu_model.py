@@ -162,3 +162,25 @@ def test_micro_batch_bounds(cuda):
         _grad(m, pt, 1, 3, cuda)
     with pytest.raises(_lib.InvalidArgument):
         api.Model(api.LMConfig(vocab=64, d_model=30, n_layer=1, n_head=3, seq_len=8, n_samples=4))
+
+
+@pytest.mark.parametrize("arch,d", [("gpt2", 1024), ("llama", 2048)])
+def test_wide_row_norm_backward_matches_warp_per_row(cuda, arch, d, monkeypatch):
+    """d >= 1024 routes the LayerNorm/RMSNorm backward to the block-per-row
+    kernel; it must agree with the warp-per-row kernel (ACCO_LN_NARROW) and
+    with the fp64 oracle at bf16 rounding."""
+    c = dict(vocab=96, d_model=d, n_layer=1, n_head=d // 64, seq_len=64, n_samples=8, data_seed=2)
+    if arch == "llama":
+        c.update(arch="llama", n_kv_head=d // 128, d_ff=2 * d)
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=2))
+    gc = G.GPTConfig(**c)
+    rng = np.random.default_rng(3)
+    th = torch.tensor(G.default_theta0(gc, 1) + 0.02 * rng.standard_normal(m.dim)).to(torch.bfloat16)
+    seed = O.derive(2, 0, 0, 2, 0)
+    g_wide, l_wide = _grad(m, th.to(cuda), seed, 2, cuda)
+    monkeypatch.setenv("ACCO_LN_NARROW", "1")
+    g_nar, l_nar = _grad(m, th.to(cuda), seed, 2, cuda)
+    assert abs(l_wide - l_nar) <= 1e-6 * abs(l_nar)  # forward is shared
+    assert _rel(g_wide, g_nar) <= 1e-2
+    og, _, ol = G.LMProblem(gc).stochastic_grad(th.float().double().numpy(), seed, 2)
+    assert _rel(g_wide, og * 2) <= 5e-2
