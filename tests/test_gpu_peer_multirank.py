@@ -1,5 +1,5 @@
-"""Peer fabric at world size 2 on the one GPU gpurun provides: two processes
-(ranks 0 and 1, both on device 0) exchange CUDA-IPC handles over gloo and run
+"""Peer fabric at world size 2 and 3 on the one GPU gpurun provides: one
+process per rank (all on device 0) exchange CUDA-IPC handles over gloo and run
 the ACCO / ZeRO-1 comm phases through the fused fold + AdamW + replica-store
 kernel, with the cross-process device-flag counts and barriers — the
 multi-rank path of the N-GPU NVLink deployment, minus NVLink. Every rank's
@@ -22,13 +22,14 @@ WORKER = r'''
 import os, sys
 import numpy as np
 sys.path.insert(0, os.environ["ROOT"])
-rank, world, port, method, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4], sys.argv[5]
+rank, world, port, method, out, vocab = (int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4], sys.argv[5],
+                                         int(sys.argv[6]))
 import torch
 import torch.distributed as dist
 torch.cuda.set_device(0)
 dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
 from paper_2406_02613_b200 import api
-MINI = dict(vocab=64, d_model=32, n_layer=2, n_head=2, seq_len=16, n_samples=32, data_seed=3)
+MINI = dict(vocab=vocab, d_model=32, n_layer=2, n_head=2, seq_len=16, n_samples=32, data_seed=3)
 peer = api.PeerComm(rank=rank, world=world, device=0)
 opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95, scheduler="cosine")
 sim = api.SimConfig(n_workers=world, batch_size=4, n_grad_accumulation=2, master_seed=7, eval_every=1)
@@ -49,15 +50,16 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("method", ["acco", "zero1", "dpu", "wp"])
-def test_peer_fabric_two_ranks_one_gpu(cuda, tmp_path, method):
+@pytest.mark.parametrize("method,world,vocab", [("acco", 2, 64), ("zero1", 2, 64), ("dpu", 2, 64), ("wp", 2, 64),
+                                                ("acco", 3, 63)])  # world 3, Psi = 28000: ragged shards
+def test_peer_fabric_multi_rank_one_gpu(cuda, tmp_path, method, world, vocab):
     from oracle import accosim_oracle as O
     from oracle import gpt_oracle as G
 
     port = str(_free_port())
     env = dict(os.environ, ROOT=ROOT)
-    procs = [subprocess.Popen([sys.executable, "-c", WORKER, str(r), "2", port, method, str(tmp_path)], env=env,
-                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    procs = [subprocess.Popen([sys.executable, "-c", WORKER, str(r), str(world), port, method, str(tmp_path), str(vocab)],
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
     outs = []
     try:
         for p in procs:
@@ -68,14 +70,15 @@ def test_peer_fabric_two_ranks_one_gpu(cuda, tmp_path, method):
                 p.kill()
     for p, o in zip(procs, outs):
         assert p.returncode == 0, o[-3000:]
-    th = [np.load(tmp_path / f"th{r}.npy") for r in range(2)]
-    assert np.array_equal(th[0], th[1])  # every rank holds the same replica
-    gc = G.GPTConfig(**MINI)
+    th = [np.load(tmp_path / f"th{r}.npy") for r in range(world)]
+    for r in range(1, world):
+        assert np.array_equal(th[0], th[r])  # every rank holds the same replica
+    gc = G.GPTConfig(**{**MINI, "vocab": vocab})
     prob = G.LMProblem(gc)
     th0 = G.default_theta0(gc, 7).astype(np.float32).astype(np.float64)
     ocfg = O.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95,
                              scheduler="cosine")
-    ref = O.run_method(method, (lambda t, s: prob.stochastic_grad(t, s, 4)), th0, ocfg, O.SimConfig(2, 4, 2, False, 7),
+    ref = O.run_method(method, (lambda t, s: prob.stochastic_grad(t, s, 4)), th0, ocfg, O.SimConfig(world, 4, 2, False, 7),
                        3, eval_fn=prob.value_and_grad)
     for t in range(3):
         a, b = th[0][t + 1], ref.theta_history[t + 1]
