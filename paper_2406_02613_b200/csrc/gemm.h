@@ -27,6 +27,11 @@ enum EpiMode : int {
     kEpiGelu = 1,    // aux = acc + bias; C = gelu(aux)       (activation dtype)
     kEpiDGelu = 2,   // C = (acc) * gelu'(aux)                (activation dtype)
     kEpiAccF32 = 3,  // C_f32 = beta*C_f32 + acc              (fp32 gradient accumulator)
+    // SwiGLU (Llama MLP): N = 2F output features stored [gate (F) | up (F)];
+    // the tile's B rows come half from each half, so the epilogue sees gate and
+    // up of the same features: aux[M, 2F] = pre-activations, C[M, F] =
+    // silu(gate) * up (bf16 tcgen05 path, K-major B, F % 128 == 0)
+    kEpiSwiGLU = 4,
 };
 
 struct Epilogue {

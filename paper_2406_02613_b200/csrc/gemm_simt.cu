@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
 
 void gemm_f32(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
               cudaStream_t stream) {
+    ACCO_REQUIRE(ep.mode <= kEpiAccF32, "gemm_f32: epilogue mode not supported by the SIMT path");
     ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_f32: empty problem");
     ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
     dim3 grid(ceil_div(N, kT), ceil_div(M, kT));

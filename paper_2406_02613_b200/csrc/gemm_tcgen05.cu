@@ -44,8 +44,13 @@ constexpr int kGroupM = 8;
 // every chunk exposed). BN = 192 tiles have the smem for a 4-deep ring.
 template <int BN>
 constexpr int in_bufs() { return BN == 192 ? 4 : 2; }
-template <int BN>
-constexpr int epi_warp_bytes() { return 4096 + in_bufs<BN>() * 2048 > 8192 ? 4096 + in_bufs<BN>() * 2048 : 8192; }
+// (the 3-stage BN = 256 variant, used by the SwiGLU epilogue, spends the freed
+// stage on 12 KB per warp: its 3 outputs per chunk pair double-buffered)
+template <int BN, int STAGES>
+constexpr int epi_warp_bytes() {
+    return (BN == 256 && STAGES == 3) ? 12288
+                                      : (4096 + in_bufs<BN>() * 2048 > 8192 ? 4096 + in_bufs<BN>() * 2048 : 8192);
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -177,7 +182,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + 4 * epi_warp_bytes<BN>() +
+    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + 4 * epi_warp_bytes<BN, STAGES>() +
            (2 * STAGES + 4 + 4 * in_bufs<BN>()) * 8 + 16;
 }
 
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint8_t* sEpi = sB + STAGES * B_BYTES;  // 1024-aligned
     constexpr int kInBuf = in_bufs<BN>();
-    constexpr int kEpiWarpBytes = epi_warp_bytes<BN>();
+    constexpr int kEpiWarpBytes = epi_warp_bytes<BN, STAGES>();
     uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 4 * kEpiWarpBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
@@ -340,6 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
                             tma_load_2d(b_dst + j * 64 * kBK * 2, &tmB, &full[s], n0 + j * 64, kb * kBK);
+                    } else if (ep.mode == kEpiSwiGLU) {  // gate rows, then the matching up rows
+                        tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0 / 2);
+                        tma_load_2d(b_dst + (BN / 2) * kBK * 2, &tmB, &full[s], kb * kBK, N / 2 + n0 / 2);
                     } else {
                         tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0);
                     }
@@ -422,6 +430,55 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+            if (ep.mode == kEpiSwiGLU) {
+                // accumulator columns [0, BN/2) = gate, [BN/2, BN) = up of the same
+                // BN/2 features (n0/2 ...): store both pre-activations (for the
+                // backward) and silu(gate) * up, computed from the bf16-rounded
+                // pre-activations exactly as the unfused kernel would
+                const int F = N / 2;
+#pragma unroll 1
+                for (int c = 0; c < kChunks / 2; ++c) {
+                    uint32_t rg[32], ru[32];
+                    tmem_ld32(tbase + c * 32, rg);
+                    tmem_ld32(tbase + (c + kChunks / 2) * 32, ru);
+                    if (c == kChunks / 2 - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    float g[32], uu[32], a[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        g[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(rg[i])));
+                        uu[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ru[i])));
+                        a[i] = __fdividef(g[i], 1.0f + __expf(-g[i])) * uu[i];
+                    }
+                    // double-buffered staging when the warp has 12 KB (3-stage tiles)
+                    constexpr bool kDbl = kEpiWarpBytes >= 12288;
+                    uint8_t* sb = wbuf + (kDbl ? (c & 1) * 6144 : 0);
+                    if (lane == 0) {
+                        if (kDbl)
+                            bulk_wait_read<1>();  // the pair two back (same buffer) was read
+                        else
+                            bulk_wait_read<0>();
+                    }
+                    __syncwarp();
+                    st_row_bf16(sb, lane, g);
+                    st_row_bf16(sb + 2048, lane, uu);
+                    st_row_bf16(sb + 4096, lane, a);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int cg = n0 / 2 + c * 32;
+                        tma_store_2d(&em.aux, sb, cg, row0);
+                        tma_store_2d(&em.aux, sb + 2048, F + cg, row0);
+                        tma_store_2d(&em.out, sb + 4096, cg, row0);
+                        bulk_commit();
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
 #pragma unroll 1
             for (int c = 0; c < kChunks; ++c) {
                 const int b = c & 1;
@@ -625,12 +682,12 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
             sem = split_semaphores();
         }
     } else {
-        em.out = make_map(ep.C, N, M, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        em.out = make_map(ep.C, ep.mode == kEpiSwiGLU ? N / 2 : N, M, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (ep.aux) em.aux = make_map(ep.aux, N, M, ep.ld_aux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
         if (ep.residual) em.res = make_map(ep.residual, N, M, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     }
     CUtensorMap ta = operand_map(A, M, K, kBM);
-    CUtensorMap tb = operand_map(B, N, K, BN);
+    CUtensorMap tb = operand_map(B, N, K, ep.mode == kEpiSwiGLU ? BN / 2 : BN);
     const int grid = std::min(sc.units(), num_sms());
     launch_pdl(kern, grid, kThreads, smem, stream, ta, tb, em, M, N, sc, ep, sem);
     ACCO_CHECK_LAUNCH();
@@ -683,6 +740,12 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
                 best_sp = sp;
             }
         }
+    }
+    if (ep.mode == kEpiSwiGLU) {
+        ACCO_REQUIRE(N % 256 == 0 && !B.mn_major && !ep.residual && !ep.bias && ep.aux,
+                     "gemm_bf16: SwiGLU epilogue needs N = 2F with F % 128 == 0, K-major B, aux, no bias/residual");
+        dispatch_major<256, 3>(A, B, M, N, K, ep, 1, stream);
+        return;
     }
     if (const char* f = std::getenv("ACCO_GEMM_FORCE")) {  // tuning knob: "<bn>,<splits>"
         int fb = 0, fs = 0;

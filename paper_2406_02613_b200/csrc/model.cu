@@ -470,6 +470,9 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
     auto li = [&](int l, int j) { return 1 + 6 * l + j; };
     auto lse_l = [&](int l) { return lse_ + static_cast<int64_t>(l) * H * Mmax; };
 
+    // SwiGLU fused into the gate|up GEMM epilogue on the bf16 tcgen05 path
+    const bool no_fuse = std::getenv("ACCO_NO_SWIGLU_FUSION") != nullptr;  // A/B knob, read per call
+    const bool swiglu_fused = sizeof(T) == 2 && F % 128 == 0 && !no_fuse;
     stage_input(seed, mode, start, B, s);
     if (backward) sort_tokens(M, s);
     embed_fwd<T>(tok_in_, W(kWte), nullptr, X(0), M, Tq, d, s);
@@ -482,8 +485,16 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
         attention_fwd<T>(QKV, Y, lse_l(l), B, Tq, H, Hk, hd, s);
         mm<T>(Y, d, false, W(li(l, 2)), d, false, M, d, d, ep_store(XM, d, nullptr, X(l), d), s);
         layernorm_fwd<T>(XM, W(li(l, 3)), nullptr, H2, stat(4 * l + 2), stat(4 * l + 3), M, d, s, true);
-        mm<T>(H2, d, false, W(li(l, 4)), d, false, M, 2 * F, d, ep_store(GU, 2 * F), s);
-        swiglu_fwd<T>(GU, A, M, F, s);
+        if (swiglu_fused) {  // gate|up GEMM with silu(gate) * up in its epilogue
+            Epilogue e = ep_store(A, F);
+            e.mode = kEpiSwiGLU;
+            e.aux = GU;
+            e.ld_aux = 2 * F;
+            mm<T>(H2, d, false, W(li(l, 4)), d, false, M, 2 * F, d, e, s);
+        } else {
+            mm<T>(H2, d, false, W(li(l, 4)), d, false, M, 2 * F, d, ep_store(GU, 2 * F), s);
+            swiglu_fwd<T>(GU, A, M, F, s);
+        }
         mm<T>(A, F, false, W(li(l, 5)), F, false, M, d, F, ep_store(X(l + 1), d, nullptr, XM, d), s);
     }
     layernorm_fwd<T>(X(L), W(kNorm), nullptr, HF, stat(4 * L), stat(4 * L + 1), M, d, s, true);

@@ -151,3 +151,22 @@ def test_llama_config_validation(cuda):
     with pytest.raises(_lib.InvalidArgument):  # d_ff must keep TMA 16-byte strides
         api.Model(api.LMConfig(vocab=64, d_model=32, n_layer=1, n_head=4, d_ff=30, seq_len=8, n_samples=4,
                                arch="llama"))
+
+
+def test_swiglu_fused_epilogue_matches_unfused(cuda, monkeypatch):
+    """d_ff % 128 == 0 routes the gate|up GEMM to the fused SwiGLU epilogue
+    (tcgen05 path); it must reproduce the separate GEMM + SwiGLU kernel."""
+    c = dict(vocab=128, d_model=256, n_layer=2, n_head=4, n_kv_head=2, d_ff=384, seq_len=128, n_samples=8,
+             data_seed=6, arch="llama")
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=2))
+    gc = G.GPTConfig(**c)
+    rng = np.random.default_rng(7)
+    th = torch.tensor(G.default_theta0(gc, 3) + 0.05 * rng.standard_normal(m.dim)).to(torch.bfloat16).to(cuda)
+    seed = O.derive(6, 0, 0, 2, 0)
+    g_f, l_f = _grad(m, th, seed, 2, cuda)
+    monkeypatch.setenv("ACCO_NO_SWIGLU_FUSION", "1")
+    g_u, l_u = _grad(m, th, seed, 2, cuda)
+    og, _, ol = G.LMProblem(gc).stochastic_grad(th.float().cpu().double().numpy(), seed, 2)
+    assert abs(l_f - ol * 2) <= 1e-2 * abs(ol * 2)
+    assert _rel(g_f, og * 2) <= 5e-2
+    assert _rel(g_f, g_u) <= 2e-2
