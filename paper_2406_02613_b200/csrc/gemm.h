@@ -32,6 +32,9 @@ enum EpiMode : int {
     // up of the same features: aux[M, 2F] = pre-activations, C[M, F] =
     // silu(gate) * up (bf16 tcgen05 path, K-major B, F % 128 == 0)
     kEpiSwiGLU = 4,
+    // SwiGLU backward (dgrad of the down projection, N = F): acc = dA;
+    // aux = GU [M, 2F] pre-activations; C = dGU [M, 2F] (gate | up halves)
+    kEpiDSwiGLU = 5,
 };
 
 struct Epilogue {

@@ -427,6 +427,65 @@ __global__ void __launch_bounds__(kThreads, 1)
                 fence_async_global();
             }
             __syncwarp();
+            if (ep.mode == kEpiDSwiGLU) {
+                // acc = dA for features [n0, n0+BN); inputs gate / up pre-activations
+                // (aux columns f and F + f, one 4 KB slot per chunk, prefetched
+                // kSlots chunks ahead); outputs d(gate) / d(up) into C = dGU
+                constexpr int kSlots = (kEpiWarpBytes - 4096) / 4096;
+                static_assert(kSlots >= 1 && kSlots <= kInBuf, "DSwiGLU input slots");
+                const int F = N;
+                uint8_t* in0 = wbuf + 4096;
+                auto load_in = [&](int c) {
+                    const int sl = c % kSlots;
+                    mbar_expect_tx(&ib[sl], 4096);
+                    tma_load_2d(in0 + sl * 4096, &em.aux, &ib[sl], n0 + c * 32, row0);
+                    tma_load_2d(in0 + sl * 4096 + 2048, &em.aux, &ib[sl], F + n0 + c * 32, row0);
+                };
+                if (lane == 0)
+                    for (int c = 0; c < kSlots && c < kChunks; ++c) load_in(c);
+                mbar_wait(&tfull[acc], (lt >> 1) & 1);
+                tc_fence_after();
+                const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+#pragma unroll 1
+                for (int c = 0; c < kChunks; ++c) {
+                    const int sl = c % kSlots;
+                    uint32_t raw[32];
+                    tmem_ld32(tb + c * 32, raw);
+                    if (c == kChunks - 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                    }
+                    mbar_wait(&ib[sl], (in_phase >> sl) & 1);
+                    in_phase ^= 1u << sl;
+                    float g[32], u[32], dg[32], du[32];
+                    ld_row_bf16(in0 + sl * 4096, lane, g);
+                    ld_row_bf16(in0 + sl * 4096 + 2048, lane, u);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float dd = __bfloat162float(__float2bfloat16_rn(__uint_as_float(raw[i])));
+                        const float sg = 1.0f / (1.0f + __expf(-g[i]));
+                        dg[i] = dd * u[i] * sg * (1.0f + g[i] * (1.0f - sg));
+                        du[i] = dd * g[i] * sg;
+                    }
+                    __syncwarp();  // the slot has been consumed: refill it kSlots chunks ahead
+                    if (lane == 0 && c + kSlots < kChunks) load_in(c + kSlots);
+                    if (n0 + c * 32 >= F) continue;  // past the last feature (F % 32 == 0): no store
+                    if (lane == 0) bulk_wait_read<0>();  // the previous chunk's staging was read
+                    __syncwarp();
+                    st_row_bf16(wbuf, lane, dg);
+                    st_row_bf16(wbuf + 2048, lane, du);
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&em.out, wbuf, n0 + c * 32, row0);
+                        tma_store_2d(&em.out, wbuf + 2048, F + n0 + c * 32, row0);
+                        bulk_commit();
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
@@ -682,8 +741,11 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
             sem = split_semaphores();
         }
     } else {
-        em.out = make_map(ep.C, ep.mode == kEpiSwiGLU ? N / 2 : N, M, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
-        if (ep.aux) em.aux = make_map(ep.aux, N, M, ep.ld_aux, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+        em.out = make_map(ep.C, ep.mode == kEpiSwiGLU ? N / 2 : (ep.mode == kEpiDSwiGLU ? 2 * N : N), M, ep.ldc, 32, 32,
+                          CU_TENSOR_MAP_SWIZZLE_64B);
+        if (ep.aux)
+            em.aux = make_map(ep.aux, ep.mode == kEpiDSwiGLU ? 2 * N : N, M, ep.ld_aux, 32, 32,
+                              CU_TENSOR_MAP_SWIZZLE_64B);
         if (ep.residual) em.res = make_map(ep.residual, N, M, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     }
     CUtensorMap ta = operand_map(A, M, K, kBM);
@@ -740,6 +802,12 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
                 best_sp = sp;
             }
         }
+    }
+    if (ep.mode == kEpiDSwiGLU) {
+        ACCO_REQUIRE(ep.aux && !ep.residual && !ep.bias && N % 32 == 0,
+                     "gemm_bf16: DSwiGLU epilogue needs aux, F % 32 == 0, no bias/residual");
+        dispatch_major<192, 4>(A, B, M, N, K, ep, 1, stream);  // 192-wide tiles: 12 KB per epilogue warp
+        return;
     }
     if (ep.mode == kEpiSwiGLU) {
         ACCO_REQUIRE(N % 256 == 0 && !B.mn_major && !ep.residual && !ep.bias && ep.aux,

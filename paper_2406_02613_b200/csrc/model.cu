@@ -529,8 +529,16 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
           *GU = slot(l, sA), *A = slot(l, sU);
         // MLP
         mm<T>(DX, d, true, A, F, true, d, F, M, ep_acc(Gp(li(l, 5)), F, beta), s);
-        mm<T>(DX, d, false, W(li(l, 5)), F, true, M, F, d, ep_store(DU, F), s);
-        swiglu_bwd<T>(DU, GU, DGU, M, F, s);
+        if (swiglu_fused) {  // SwiGLU backward in the down-projection dgrad epilogue
+            Epilogue e = ep_store(DGU, 2 * F);
+            e.mode = kEpiDSwiGLU;
+            e.aux = GU;
+            e.ld_aux = 2 * F;
+            mm<T>(DX, d, false, W(li(l, 5)), F, true, M, F, d, e, s);
+        } else {
+            mm<T>(DX, d, false, W(li(l, 5)), F, true, M, F, d, ep_store(DU, F), s);
+            swiglu_bwd<T>(DU, GU, DGU, M, F, s);
+        }
         mm<T>(DGU, 2 * F, true, H2, d, true, 2 * F, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
         join();  // DT (read by the previous norm-weight reduction) is overwritten next
         mm<T>(DGU, 2 * F, false, W(li(l, 4)), d, true, M, d, 2 * F, ep_store(DT, d), s);
