@@ -36,21 +36,25 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one SW128 row
-constexpr int kThreads = 256;
+// warps 0-3: TMA producer, MMA issuer, TMEM alloc, idle; then the epilogue
+// warps: 8 (two per TMEM lane quadrant) where the smem allows it next to a
+// deep operand ring, else 4 (the 128x256 tiles keep 4 stages: a 3-stage ring
+// costs them more than a faster epilogue gains)
+template <int BN, int STAGES>
+constexpr int epi_warps() { return (BN == 256 && STAGES == 4) ? 4 : 8; }
+template <int BN, int STAGES>
+constexpr int gemm_threads() { return 128 + 32 * epi_warps<BN, STAGES>(); }
 constexpr int kGroupM = 8;
 // Per epilogue warp: 2 bf16 output chunks (or 2 fp32 chunks spanning the
 // first 8 KB) + a ring of IN_BUF 2 KB input chunks (residual / GELU aux, TMA
 // prefetched IN_BUF chunks ahead: one chunk ahead left the HBM latency of
 // every chunk exposed). BN = 192 tiles have the smem for a 4-deep ring.
 template <int BN>
-constexpr int in_bufs() { return BN == 192 ? 4 : 2; }
+constexpr int in_bufs() { return 2; }
 // (the 3-stage BN = 256 variant, used by the SwiGLU epilogue, spends the freed
 // stage on 12 KB per warp: its 3 outputs per chunk pair double-buffered)
 template <int BN, int STAGES>
-constexpr int epi_warp_bytes() {
-    return (BN == 256 && STAGES == 3) ? 12288
-                                      : (4096 + in_bufs<BN>() * 2048 > 8192 ? 4096 + in_bufs<BN>() * 2048 : 8192);
-}
+constexpr int epi_warp_bytes() { return 8192; }  // 2 bf16 output chunks (or 2 fp32 ones) + 2 input chunks
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -182,8 +186,8 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
 
 template <int BN, int STAGES>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + 4 * epi_warp_bytes<BN, STAGES>() +
-           (2 * STAGES + 4 + 4 * in_bufs<BN>()) * 8 + 16;
+    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + epi_warps<BN, STAGES>() * epi_warp_bytes<BN, STAGES>() +
+           (2 * STAGES + 4 + epi_warps<BN, STAGES>() * in_bufs<BN>()) * 8 + 16;
 }
 
 struct Sched {
@@ -266,7 +270,7 @@ struct EpiMaps {
 
 // --------------------------------------------------------------------- kernel
 template <int BN, int STAGES, int A_MN, int B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem) {
     extern __shared__ uint8_t smem_raw[];
@@ -279,12 +283,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sEpi = sB + STAGES * B_BYTES;  // 1024-aligned
     constexpr int kInBuf = in_bufs<BN>();
     constexpr int kEpiWarpBytes = epi_warp_bytes<BN, STAGES>();
-    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 4 * kEpiWarpBytes);
+    constexpr int kEpiWarps = epi_warps<BN, STAGES>();
+    constexpr int kCS = kEpiWarps / 4;  // chunk stride: epilogue warps per TMEM lane quadrant
+    uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + kEpiWarps * kEpiWarpBytes);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
-    uint64_t* inbar = tempty + 2;      // [4 warps][kInBuf]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + 4 * kInBuf);
+    uint64_t* inbar = tempty + 2;      // [8 epilogue warps][kInBuf]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + kEpiWarps * kInBuf);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -297,9 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
         }
-        for (int i = 0; i < 4 * kInBuf; ++i) mbar_init(&inbar[i], 1);
+        for (int i = 0; i < kEpiWarps * kInBuf; ++i) mbar_init(&inbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -390,9 +396,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int wq = warp - 4;
-        uint8_t* wbuf = sEpi + wq * kEpiWarpBytes;
-        uint64_t* ib = inbar + kInBuf * wq;
+        // 8 epilogue warps: warp ew handles TMEM lane quadrant wq (32 rows) and the
+        // chunks c = hf, hf+2, ... (every other 32-column chunk) of each tile, so
+        // two warps drain a quadrant in parallel (GELU/dGELU/SwiGLU epilogues were
+        // the bottleneck of their GEMMs with one warp per quadrant)
+        const int ew = warp - 4, wq = ew & 3, hf = ew >> 2;  // hf < kCS
+        uint8_t* wbuf = sEpi + ew * kEpiWarpBytes;
+        uint64_t* ib = inbar + kInBuf * ew;
         const bool f32 = ep.mode == kEpiAccF32;
         const bool has_in = !f32 && (ep.mode == kEpiDGelu || ep.residual != nullptr);
         const CUtensorMap* in_map = ep.mode == kEpiDGelu ? &em.aux : &em.res;
@@ -406,22 +416,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int acc = lt & 1;
             const int row0 = mb * kBM + wq * 32;
             const int n0 = nb * BN;
-            if (has_in && lane == 0) {  // input chunks 0 .. kInBuf-1 of this tile
+            if (has_in && lane == 0) {  // this warp's first kInBuf input chunks of the tile
 #pragma unroll
-                for (int c = 0; c < kInBuf; ++c)
-                    if (c < kChunks) {
-                        mbar_expect_tx(&ib[c], 2048);
-                        tma_load_2d(wbuf + 4096 + c * 2048, in_map, &ib[c], n0 + c * 32, row0);
+                for (int j = 0; j < kInBuf; ++j)
+                    if (hf + kCS * j < kChunks) {
+                        mbar_expect_tx(&ib[j], 2048);
+                        tma_load_2d(wbuf + 4096 + j * 2048, in_map, &ib[j], n0 + (hf + kCS * j) * 32, row0);
                     }
             }
-            // bias of chunk 0 (each chunk then prefetches the next chunk's bias)
+            // bias of this warp's first chunk (each chunk then prefetches the next one's)
             uint4 bpre[4];
-            if (bias && n0 + 32 <= N) {
+            if (bias && n0 + hf * 32 + 32 <= N) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + n0 + 8 * q));
+                for (int q = 0; q < 4; ++q)
+                    bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + n0 + hf * 32 + 8 * q));
             }
-            // ordered split-K: this quadrant's rows are added in split order
-            int* sem = split_sem ? split_sem + ((mb * sc.tiles_n + nb) * 4 + wq) * 32 : nullptr;  // own 128B line
+            // ordered split-K: this warp's (quadrant, column half) slice is added in split order
+            int* sem = split_sem ? split_sem + ((mb * sc.tiles_n + nb) * 8 + ew) * 32 : nullptr;  // own 128B line (<= 8 per tile)
             if (sem && lane == 0) {
                 while (ld_acquire(sem) != sp) __nanosleep(64);
                 fence_async_global();
@@ -429,47 +440,47 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (ep.mode == kEpiDSwiGLU) {
                 // acc = dA for features [n0, n0+BN); inputs gate / up pre-activations
-                // (aux columns f and F + f, one 4 KB slot per chunk, prefetched
-                // kSlots chunks ahead); outputs d(gate) / d(up) into C = dGU
+                // (aux columns f and F + f, one 4 KB slot per chunk); outputs
+                // d(gate) / d(up) into C = dGU
                 constexpr int kSlots = (kEpiWarpBytes - 4096) / 4096;
                 static_assert(kSlots >= 1 && kSlots <= kInBuf, "DSwiGLU input slots");
                 const int F = N;
                 uint8_t* in0 = wbuf + 4096;
-                auto load_in = [&](int c) {
-                    const int sl = c % kSlots;
+                auto load_in = [&](int j) {  // this warp's j-th chunk
+                    const int sl = j % kSlots, c = hf + kCS * j;
                     mbar_expect_tx(&ib[sl], 4096);
                     tma_load_2d(in0 + sl * 4096, &em.aux, &ib[sl], n0 + c * 32, row0);
                     tma_load_2d(in0 + sl * 4096 + 2048, &em.aux, &ib[sl], F + n0 + c * 32, row0);
                 };
                 if (lane == 0)
-                    for (int c = 0; c < kSlots && c < kChunks; ++c) load_in(c);
+                    for (int j = 0; j < kSlots && hf + kCS * j < kChunks; ++j) load_in(j);
                 mbar_wait(&tfull[acc], (lt >> 1) & 1);
                 tc_fence_after();
                 const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
 #pragma unroll 1
-                for (int c = 0; c < kChunks; ++c) {
-                    const int sl = c % kSlots;
+                for (int j = 0, c = hf; c < kChunks; ++j, c += kCS) {
+                    const int sl = j % kSlots;
                     uint32_t raw[32];
                     tmem_ld32(tb + c * 32, raw);
-                    if (c == kChunks - 1) {
+                    if (c + kCS >= kChunks) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[acc]);
                     }
                     mbar_wait(&ib[sl], (in_phase >> sl) & 1);
                     in_phase ^= 1u << sl;
-                    float g[32], u[32], dg[32], du[32];
+                    float g[32], uu[32], dg[32], du[32];
                     ld_row_bf16(in0 + sl * 4096, lane, g);
-                    ld_row_bf16(in0 + sl * 4096 + 2048, lane, u);
+                    ld_row_bf16(in0 + sl * 4096 + 2048, lane, uu);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const float dd = __bfloat162float(__float2bfloat16_rn(__uint_as_float(raw[i])));
                         const float sg = 1.0f / (1.0f + __expf(-g[i]));
-                        dg[i] = dd * u[i] * sg * (1.0f + g[i] * (1.0f - sg));
+                        dg[i] = dd * uu[i] * sg * (1.0f + g[i] * (1.0f - sg));
                         du[i] = dd * g[i] * sg;
                     }
                     __syncwarp();  // the slot has been consumed: refill it kSlots chunks ahead
-                    if (lane == 0 && c + kSlots < kChunks) load_in(c + kSlots);
+                    if (lane == 0 && hf + kCS * (j + kSlots) < kChunks) load_in(j + kSlots);
                     if (n0 + c * 32 >= F) continue;  // past the last feature (F % 32 == 0): no store
                     if (lane == 0) bulk_wait_read<0>();  // the previous chunk's staging was read
                     __syncwarp();
@@ -496,11 +507,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // pre-activations exactly as the unfused kernel would
                 const int F = N / 2;
 #pragma unroll 1
-                for (int c = 0; c < kChunks / 2; ++c) {
+                for (int c = hf; c < kChunks / 2; c += kCS) {
                     uint32_t rg[32], ru[32];
                     tmem_ld32(tbase + c * 32, rg);
                     tmem_ld32(tbase + (c + kChunks / 2) * 32, ru);
-                    if (c == kChunks / 2 - 1) {
+                    if (c + kCS >= kChunks / 2) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -512,26 +523,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uu[i] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(ru[i])));
                         a[i] = __fdividef(g[i], 1.0f + __expf(-g[i])) * uu[i];
                     }
-                    // double-buffered staging when the warp has 12 KB (3-stage tiles)
-                    constexpr bool kDbl = kEpiWarpBytes >= 12288;
-                    uint8_t* sb = wbuf + (kDbl ? (c & 1) * 6144 : 0);
-                    if (lane == 0) {
-                        if (kDbl)
-                            bulk_wait_read<1>();  // the pair two back (same buffer) was read
-                        else
-                            bulk_wait_read<0>();
-                    }
+                    if (lane == 0) bulk_wait_read<0>();  // the previous pair's staging was read
                     __syncwarp();
-                    st_row_bf16(sb, lane, g);
-                    st_row_bf16(sb + 2048, lane, uu);
-                    st_row_bf16(sb + 4096, lane, a);
+                    st_row_bf16(wbuf, lane, g);
+                    st_row_bf16(wbuf + 2048, lane, uu);
+                    st_row_bf16(wbuf + 4096, lane, a);
                     fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
                         const int cg = n0 / 2 + c * 32;
-                        tma_store_2d(&em.aux, sb, cg, row0);
-                        tma_store_2d(&em.aux, sb + 2048, F + cg, row0);
-                        tma_store_2d(&em.out, sb + 4096, cg, row0);
+                        tma_store_2d(&em.aux, wbuf, cg, row0);
+                        tma_store_2d(&em.aux, wbuf + 2048, F + cg, row0);
+                        tma_store_2d(&em.out, wbuf + 4096, cg, row0);
                         bulk_commit();
                     }
                 }
@@ -539,20 +542,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 continue;
             }
 #pragma unroll 1
-            for (int c = 0; c < kChunks; ++c) {
-                const int b = c & 1;
-                const int ibuf = c % kInBuf;
+            for (int j = 0, c = hf; c < kChunks; ++j, c += kCS) {
+                const int b = j & 1;
+                const int ibuf = j % kInBuf;
                 const int col0 = n0 + c * 32;
                 uint4 bcur[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) bcur[q] = bpre[q];
-                if (bias && c + 1 < kChunks && col0 + 64 <= N) {
+                if (bias && c + kCS < kChunks && col0 + 32 * kCS + 32 <= N) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + col0 + 32 + 8 * q));
+                    for (int q = 0; q < 4; ++q)
+                        bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + col0 + 32 * kCS + 8 * q));
                 }
                 uint32_t raw[32];
                 tmem_ld32(tbase + c * 32, raw);
-                if (c == kChunks - 1) {  // accumulator fully read: hand TMEM back to the MMA warp
+                if (c + kCS >= kChunks) {  // this warp's share of the accumulator read: hand TMEM back
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -592,13 +596,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int i = 0; i < 32; ++i) v[i] += iv[i];
                     }
                     __syncwarp();  // every lane has consumed the input buffer: refill it kInBuf chunks ahead
-                    if (lane == 0 && c + kInBuf < kChunks) {
+                    if (lane == 0 && c + kCS * kInBuf < kChunks) {
                         mbar_expect_tx(&ib[ibuf], 2048);
-                        tma_load_2d(wbuf + 4096 + ibuf * 2048, in_map, &ib[ibuf], col0 + kInBuf * 32, row0);
+                        tma_load_2d(wbuf + 4096 + ibuf * 2048, in_map, &ib[ibuf], col0 + kCS * kInBuf * 32, row0);
                     }
                 }
-                // the TMA store that last used these staging buffers (chunk c-2)
-                // must have finished reading them
+                // the TMA store that last used these staging buffers (two chunks
+                // back in this warp's sequence) must have finished reading them
                 if (lane == 0) bulk_wait_read<1>();
                 __syncwarp();
                 if (f32) {
@@ -737,7 +741,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     if (ep.mode == kEpiAccF32) {
         em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
         if (sc.splits > 1) {
-            ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 4 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
+            ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 8 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
             sem = split_semaphores();
         }
     } else {
@@ -751,7 +755,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     CUtensorMap ta = operand_map(A, M, K, kBM);
     CUtensorMap tb = operand_map(B, N, K, ep.mode == kEpiSwiGLU ? BN / 2 : BN);
     const int grid = std::min(sc.units(), num_sms());
-    launch_pdl(kern, grid, kThreads, smem, stream, ta, tb, em, M, N, sc, ep, sem);
+    launch_pdl(kern, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -793,7 +797,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     for (int bn : {256, 192, 128}) {
         for (int sp : {1, 2, 3, 4, 6, 8}) {
             if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp ||
-                           ceil_div(M, kBM) * ceil_div(N, bn) * 4 * 32 > kSemSlots))
+                           ceil_div(M, kBM) * ceil_div(N, bn) * 8 * 32 > kSemSlots))
                 continue;
             const double c = plan_cost(M, N, K, bn, sp, sms);
             if (c < best * 0.97) {
@@ -806,7 +810,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     if (ep.mode == kEpiDSwiGLU) {
         ACCO_REQUIRE(ep.aux && !ep.residual && !ep.bias && N % 32 == 0,
                      "gemm_bf16: DSwiGLU epilogue needs aux, F % 32 == 0, no bias/residual");
-        dispatch_major<192, 4>(A, B, M, N, K, ep, 1, stream);  // 192-wide tiles: 12 KB per epilogue warp
+        dispatch_major<192, 4>(A, B, M, N, K, ep, 1, stream);
         return;
     }
     if (ep.mode == kEpiSwiGLU) {
@@ -827,7 +831,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     else if (best_bn == 192)
         dispatch_major<192, 4>(A, B, M, N, K, ep, best_sp, stream);
     else
-        dispatch_major<128, 6>(A, B, M, N, K, ep, best_sp, stream);
+        dispatch_major<128, 5>(A, B, M, N, K, ep, best_sp, stream);
 }
 
 }  // namespace acco

@@ -28,6 +28,9 @@ SHAPES = [
     ("qkv_wgrad", 3 * d, d, M, True, True, "acc_f32"),
     ("qkv_dgrad", M, d, 3 * d, False, True, "store"),
     ("proj_wgrad", d, d, M, True, True, "acc_f32"),
+    # epilogue-cost probes: the same shapes with the plain store epilogue
+    ("fc_fwd_store", M, 4 * d, d, False, False, "store"),
+    ("fc2_dgrad_store", M, 4 * d, d, False, True, "store"),
 ]
 
 
