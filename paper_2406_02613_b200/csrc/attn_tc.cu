@@ -46,6 +46,17 @@ constexpr float kLog2e = 1.4426950408889634f;
 __device__ __forceinline__ int item_at(const int* __restrict__ sched, int k_max, int k) {
     return k < k_max ? __ldg(sched + static_cast<int64_t>(blockIdx.x) * k_max + k) : -1;
 }
+#ifdef ACCO_FWD_PROBE  // timeline probe of fa_fwd_tc2 (tools/diag/fwd_probe.cu only)
+__device__ unsigned long long g_probe[148][10][128];
+#define FWD_PROBE(kind, idx)                                                                     \
+    do {                                                                                         \
+        unsigned long long _t;                                                                   \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                   \
+        if ((idx) < 128 && blockIdx.x < 148) g_probe[blockIdx.x][kind][idx] = _t;                \
+    } while (0)
+#else
+#define FWD_PROBE(kind, idx)
+#endif
 constexpr float kRescaleThresh = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 
 constexpr int Q_BYTES = BQ * HD * 2;          // 16 KB
@@ -406,7 +417,10 @@ __device__ __forceinline__ void st_row32_global_fwd(__nv_bfloat16* dst, const ui
 }
 
 constexpr int F2_STAGES = 3;
-constexpr int F2_SMEM = 1024 + 4 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + 256;
+// + per tile slot: row-max exchange [2 parity][2 half][128] and row sums [2 half][128]
+constexpr int F2_SMEM = 1024 + 4 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + 256 + 2 * 6 * 128 * 4;
+// two softmax groups of 8 warps (one per tile slot): quadrant x half of the 128 keys
+constexpr int F2_THREADS = 640;
 
 __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -424,31 +438,6 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
         : "memory");
 }
 
-__device__ __forceinline__ float2 fma_f32x2(float2 a, float2 b, float2 c) {
-    uint64_t r;
-    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
-        "mov.b64 ra, {%1, %2};\n\t"
-        "mov.b64 rb, {%3, %4};\n\t"
-        "mov.b64 rc, {%5, %6};\n\t"
-        "fma.rn.f32x2 %0, ra, rb, rc;\n\t}\n"
-        : "=l"(r)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    float2 o;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
-    return o;
-}
-__device__ __forceinline__ float2 add_f32x2(float2 a, float2 b) {
-    uint64_t r;
-    asm("{\n\t.reg .b64 ra, rb;\n\t"
-        "mov.b64 ra, {%1, %2};\n\t"
-        "mov.b64 rb, {%3, %4};\n\t"
-        "add.rn.f32x2 %0, ra, rb;\n\t}\n"
-        : "=l"(r)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-    float2 o;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(o.x), "=f"(o.y) : "l"(r));
-    return o;
-}
 __device__ __forceinline__ float max3(float a, float b, float c) {
     float r;
     asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));  // FMNMX3
@@ -496,7 +485,7 @@ __device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m
 // tile sequence, so CTA launch / TMEM alloc / pipeline fill are paid once per
 // SM. TMEM: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320),
 // O tile 1 [320,384).
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(F2_THREADS, 1)
     fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
                int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
     extern __shared__ uint8_t smem_raw[];
@@ -548,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int x = 0; x < 2; ++x) {
             mbar_init(&s_full[x], 1);
-            mbar_init(&p_full[x], 128);
+            mbar_init(&p_full[x], 256);
             mbar_init(&o_done[x], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -593,6 +582,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
             int kvit = 0, ni = 0;
             int cnt[2] = {0, 0};  // tiles issued so far per slot (s_full / p_full phases)
+            int pc_s = 0, pc_pv = 0;
+            (void)pc_s;
+            (void)pc_pv;
             for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int nt[2] = {w.nt0, w.nt1};
@@ -605,6 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_wait(&kv_full[s], ((kvit + j) / F2_STAGES) & 1);
                         tc_after();
                     }
+                    FWD_PROBE(0, pc_s);
+                    ++pc_s;
                     const uint32_t q_base = q_item + x * Q_BYTES, k_base = smem_u32(sK + s * KV_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < HD / 16; ++kk)
@@ -616,6 +610,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = (kvit + j) % F2_STAGES;
                     mbar_wait(&p_full[x], (cnt[x] + j) & 1);
                     tc_after();
+                    FWD_PROBE(1, pc_pv);
+                    ++pc_pv;
                     const uint32_t v_base = smem_u32(sV + s * KV_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk) {
@@ -641,12 +637,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int x = (warp - 4) >> 2;  // tile slot of this softmax group
-        const int wq = warp & 3;
+        // two groups of 8 softmax warps, one per tile slot x; in a group, warp
+        // (quadrant wq, half) owns TMEM lanes wq*32.. and keys half*64..+63 of
+        // each S tile (and O columns half*32..+31): the row max is exchanged with
+        // the partner warp through smem, and P (bf16 pairs) lands on packed
+        // columns half*32.. after both halves have read their S
+        const int x = (warp - 4) >> 3;
+        const int wq = warp & 3, half = ((warp - 4) >> 2) & 1;
         const int r = wq * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
         const float sl = scale * kLog2e;
+        float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tslot) + 16) + x * 6 * 128;  // [2][2][128] max
+        float* lsum = red + 4 * 128;                                                                  // [2][128] sums
+        const int bar_id = 2 + x * 4 + wq;  // the quadrant's two warps
         int cnt = 0, nitem = 0;  // tiles / items this slot has processed (barrier phases)
         for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
             const Item w = item_of(u);
@@ -654,84 +658,84 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n == 0) continue;  // absent tile (odd tile count): no phases consumed
             const int q = (2 * w.pr + x) * BQ + r;
             float m = -INFINITY;
-            float2 l2 = make_float2(0.f, 0.f);  // fp32 row sum (even / odd keys), packed adds
+            float2 l2 = make_float2(0.f, 0.f);  // fp32 partial row sum over this half's keys
             for (int j = 0; j < n; ++j) {
                 mbar_wait(&s_full[x], (cnt + j) & 1);
                 tc_after();
+                if (lane == 0 && wq == 0 && half == 0) FWD_PROBE(2 + 2 * x, cnt + j);
                 const bool diag = j == n - 1;  // the causal edge (and any ragged tail) sits in the last tile
                 const int kbase = j * BKV;
-                // pass 1: row max, S streamed from TMEM 64 columns (two loads) per wait.
-                // Valid keys of this row in the diagonal tile: [kbase, min(q + 1, T)).
-                const int lim = min(q + 1, T) - kbase;
-                float mx = -INFINITY;
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    uint32_t sv[64];
-                    tmem_ld32(tS + h2 * 64, sv);
-                    tmem_ld32(tS + h2 * 64 + 32, sv + 32);
-                    tmem_wait_ld();
-                    mx = diag ? row_max64<true>(sv, h2 * 64, lim, mx) : row_max64<false>(sv, h2 * 64, lim, mx);
-                }
-                mx *= sl;
+                const int lim = min(q + 1, T) - kbase;  // valid keys of this row: [kbase, kbase + lim)
+                uint32_t sv[64];
+                tmem_ld32(tS + half * 64, sv);
+                tmem_ld32(tS + half * 64 + 32, sv + 32);
+                tmem_wait_ld();
+                if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(6, cnt + j);
+                float mx = diag ? row_max64<true>(sv, half * 64, lim, -INFINITY)
+                                : row_max64<false>(sv, half * 64, lim, -INFINITY);
+                float* rb = red + (j & 1) * 256;
+                rb[half * 128 + r] = mx;
+                asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both halves have read S
+                if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(7, cnt + j);
+                mx = fmaxf(mx, rb[(1 - half) * 128 + r]) * sl;
                 // lazy rescale: move the reference max only when it grows by > 2^8;
                 // O is stable here (s_full(j) is committed after PV(j-1))
+                bool need = false;
+                float alpha = 1.f;
                 if (j == 0) {
                     m = mx;
                 } else {
-                    const bool need = mx > m + kRescaleThresh;
-                    const float alpha = need ? ex2(m - mx) : 1.f;
+                    need = mx > m + kRescaleThresh;
+                    alpha = need ? ex2(m - mx) : 1.f;
                     if (need) m = mx;
                     l2.x *= alpha;
                     l2.y *= alpha;
-                    if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
-                        uint32_t o[32];
-#pragma unroll
-                        for (int c = 0; c < 2; ++c) {
-                            tmem_ld32(tO + c * 32, o);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                            tmem_st32(tO + c * 32, o);
-                        }
-                        tmem_wait_st();
-                    }
                 }
-                // pass 2: P = 2^(s - m) -> bf16 pairs over the consumed S columns; S
-                // re-read 64 columns per wait (P chunk h2 lands on columns already read)
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    uint32_t sv[64];
-                    tmem_ld32(tS + h2 * 64, sv);
-                    tmem_ld32(tS + h2 * 64 + 32, sv + 32);
-                    tmem_wait_ld();
+                // P = 2^(s - m) -> bf16 pairs on packed columns half*32.. (over S columns
+                // both halves have already read: the barrier above)
+                {
                     uint32_t pk[32];
                     if (diag)
-                        exp_pack64<true>(sv, sl, m, h2 * 64, lim, l2, pk);
+                        exp_pack64<true>(sv, sl, m, half * 64, lim, l2, pk);
                     else
-                        exp_pack64<false>(sv, sl, m, h2 * 64, lim, l2, pk);
-                    tmem_st16(tS + h2 * 32, pk);
-                    tmem_st16(tS + h2 * 32 + 16, pk + 16);
+                        exp_pack64<false>(sv, sl, m, half * 64, lim, l2, pk);
+                    if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(8, cnt + j);
+                    tmem_st16(tS + half * 32, pk);
+                    tmem_st16(tS + half * 32 + 16, pk + 16);
+                }
+                // O *= alpha where the max moved (before this tile's PV, which waits p_full)
+                if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
+                    uint32_t o[32];
+                    tmem_ld32(tO + half * 32, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                    tmem_st32(tO + half * 32, o);
                 }
                 tmem_wait_st();
+                if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(9, cnt + j);
                 tc_before();
                 mbar_arrive(&p_full[x]);
+                if (lane == 0 && wq == 0 && half == 0) FWD_PROBE(3 + 2 * x, cnt + j);
             }
             cnt += n;
+            // epilogue: O / l, l = both halves' partial sums (fp32: lse stays consistent
+            // with the fp32 P of the backward)
+            lsum[half * 128 + r] = l2.x + l2.y;
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+            const float l = lsum[0 * 128 + r] + lsum[1 * 128 + r];
             mbar_wait(&o_done[x], nitem & 1);
             ++nitem;
             tc_after();
-            const float l = l2.x + l2.y;  // fp32 sum: lse stays consistent with the fp32 P of the backward
             const float inv = 1.f / l;
-            __nv_bfloat16* yr = y + (static_cast<int64_t>(w.b) * T + q) * d + w.h * HD;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t o[32];
-                tmem_ld32(tO + c * 32, o);  // warp-collective: every lane loads
-                tmem_wait_ld();
-                if (q < T) st_row32_global_fwd(yr + c * 32, o, inv);
-            }
+            __nv_bfloat16* yr = y + (static_cast<int64_t>(w.b) * T + q) * d + w.h * HD + half * 32;
+            uint32_t o[32];
+            tmem_ld32(tO + half * 32, o);  // warp-collective: every lane loads
+            tmem_wait_ld();
+            if (q < T) st_row32_global_fwd(yr, o, inv);
             tc_before();
-            if (q < T) lse[(static_cast<int64_t>(w.b) * H + w.h) * T + q] = (m + log2f(l)) / kLog2e;
+            if (q < T && half == 0) lse[(static_cast<int64_t>(w.b) * H + w.h) * T + q] = (m + log2f(l)) / kLog2e;
+            asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // lsum reusable
         }
     }
     tc_before();
@@ -1598,7 +1602,7 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
         launch_pdl(fa_fwd_tc, dim3(nqt, B * H), kThreads, SMEM, s, m, y, lse, T, H, Hkv, scale);
     } else {
         const Schedule sf = lpt_schedule(0, nqt, B * H, 1);
-        launch_pdl(fa_fwd_tc2, sf.grid, kThreads, F2_SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table, sf.k_max);
+        launch_pdl(fa_fwd_tc2, sf.grid, F2_THREADS, F2_SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table, sf.k_max);
     }
     ACCO_CHECK_LAUNCH();
     return true;

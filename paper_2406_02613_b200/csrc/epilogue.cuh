@@ -60,14 +60,14 @@ __device__ __forceinline__ void epilogue_row(const Epilogue& ep, int row, int co
 #pragma unroll
         for (int i = 0; i < NV; ++i)
             if (i < n) {
-                aux[i] = from_f<T>(x[i]);
+                aux[i] = from_f<T>(dgelu_f(x[i]));  // the slope, consumed by kEpiDGelu
                 x[i] = gelu_f(x[i]);
             }
     } else if (ep.mode == kEpiDGelu) {
         const T* aux = static_cast<const T*>(ep.aux) + (int64_t)row * ep.ld_aux + col;
 #pragma unroll
         for (int i = 0; i < NV; ++i)
-            if (i < n) x[i] *= dgelu_f(to_f(aux[i]));
+            if (i < n) x[i] *= to_f(aux[i]);
     }
     if (ep.residual) {
         const T* r = static_cast<const T*>(ep.residual) + (int64_t)row * ep.ldr + col;

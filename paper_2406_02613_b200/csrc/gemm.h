@@ -24,8 +24,8 @@ struct GemmOperand {
 
 enum EpiMode : int {
     kEpiStore = 0,   // C = acc + bias + residual            (activation dtype)
-    kEpiGelu = 1,    // aux = acc + bias; C = gelu(aux)       (activation dtype)
-    kEpiDGelu = 2,   // C = (acc) * gelu'(aux)                (activation dtype)
+    kEpiGelu = 1,    // x = acc + bias; C = gelu(x); aux = gelu'(x)  (activation dtype)
+    kEpiDGelu = 2,   // C = acc * aux (aux = the slope kEpiGelu stored)
     kEpiAccF32 = 3,  // C_f32 = beta*C_f32 + acc              (fp32 gradient accumulator)
     // SwiGLU (Llama MLP): N = 2F output features stored [gate (F) | up (F)];
     // the tile's B rows come half from each half, so the epilogue sees gate and

@@ -215,14 +215,31 @@ __device__ __forceinline__ float tanh_fast(float x) {
     return y;
 }
 // bf16-path GELU (tanh form) on the MUFU tanh; error << bf16 rounding
-__device__ __forceinline__ float gelu_fast(float x) {
+#ifdef ACCO_GEMM_PROBE
+__device__ unsigned long long g_gprobe[148][6][16];
+#define GEMM_PROBE(kind, idx)                                                        \
+    do {                                                                             \
+        unsigned long long _t;                                                       \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                       \
+        if ((idx) < 16 && blockIdx.x < 148) g_gprobe[blockIdx.x][kind][idx] = _t;    \
+    } while (0)
+#else
+#define GEMM_PROBE(kind, idx)
+#endif
+// GELU and its slope gelu'(x) from one MUFU tanh: the forward epilogue stores
+// the slope as aux, so the backward (dGELU) epilogue is a single multiply
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+// (on a pair, with packed fp32 math: half the issue slots — the epilogue warps
+// share the SM sub-partitions with the TMA and MMA issuers)
+__device__ __forceinline__ float2 gelu_slope_fast2(float2 x, float2& slope) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    return 0.5f * x * (1.0f + tanh_fast(k0 * (x + k1 * x * x * x)));
-}
-__device__ __forceinline__ float dgelu_fast(float x) {
-    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    const float t = tanh_fast(k0 * (x + k1 * x * x * x));
-    return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x * x);
+    const float2 x2 = mul_f32x2(x, x);
+    const float2 u = mul_f32x2(x, fma_f32x2(f2(k0 * k1), x2, f2(k0)));
+    const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+    const float2 h = mul_f32x2(f2(0.5f), x);
+    const float2 hq = mul_f32x2(h, fma_f32x2(make_float2(-t.x, -t.y), t, f2(1.0f)));
+    slope = fma_f32x2(hq, fma_f32x2(f2(3.0f * k0 * k1), x2, f2(k0)), fma_f32x2(f2(0.5f), t, f2(0.5f)));
+    return fma_f32x2(h, t, h);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -372,6 +389,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                 const int acc = lt & 1;
                 mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
                 tc_fence_after();
+                GEMM_PROBE(0, lt);
                 const uint32_t tmem_d = tmem_base + acc * BN;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
@@ -393,6 +411,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
+                GEMM_PROBE(1, lt);
             }
         }
     } else if (warp >= 4) {
@@ -499,6 +518,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
             }
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
+            if (lane == 0 && (ew == 0 || ew == kEpiWarps - 1)) GEMM_PROBE(ew == 0 ? 2 : 4, lt);
             const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
             if (ep.mode == kEpiSwiGLU) {
                 // accumulator columns [0, BN/2) = gate, [BN/2, BN) = up of the same
@@ -572,9 +592,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                             const uint32_t w[4] = {u4.x, u4.y, u4.z, u4.w};
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
-                                const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[k]);
-                                v[8 * q + 2 * k] += __bfloat162float(h.x);
-                                v[8 * q + 2 * k + 1] += __bfloat162float(h.y);
+                                const float2 bf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+                                const float2 r2 = add_f32x2(make_float2(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]), bf);
+                                v[8 * q + 2 * k] = r2.x;
+                                v[8 * q + 2 * k + 1] = r2.y;
                             }
                         }
                     } else {
@@ -588,9 +609,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                     in_phase ^= 1u << ibuf;
                     float iv[32];
                     ld_row_bf16(wbuf + 4096 + ibuf * 2048, lane, iv);
-                    if (ep.mode == kEpiDGelu) {
+                    if (ep.mode == kEpiDGelu) {  // aux = gelu'(pre-activation), stored by the forward
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] *= dgelu_fast(iv[i]);
+                        for (int i = 0; i < 32; ++i) v[i] *= iv[i];
                     } else {
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] += iv[i];
@@ -620,9 +641,17 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                 } else {
                     uint8_t* ob = wbuf + b * 2048;
                     if (ep.mode == kEpiGelu) {
-                        st_row_bf16(wbuf + 4096 + b * 2048, lane, v);  // pre-activation (aux)
+                        float sl[32];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = gelu_fast(v[i]);
+                        for (int i = 0; i < 32; i += 2) {
+                            float2 s2;
+                            const float2 g2 = gelu_slope_fast2(make_float2(v[i], v[i + 1]), s2);
+                            v[i] = g2.x;
+                            v[i + 1] = g2.y;
+                            sl[i] = s2.x;
+                            sl[i + 1] = s2.y;
+                        }
+                        st_row_bf16(wbuf + 4096 + b * 2048, lane, sl);  // gelu' (aux, for the backward)
                     }
                     st_row_bf16(ob, lane, v);
                     fence_async_smem();
@@ -634,6 +663,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                     }
                 }
             }
+            if (lane == 0 && (ew == 0 || ew == kEpiWarps - 1)) GEMM_PROBE(ew == 0 ? 3 : 5, lt);
             if (sem && lane == 0) {  // this split's adds are complete: hand over to split sp+1
                 bulk_wait_all();
                 fence_async_global();

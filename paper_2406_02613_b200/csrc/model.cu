@@ -134,7 +134,7 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     auto sz = [&](int slot) -> int64_t {
         switch (slot) {
             case sQKV: return nqkv;
-            case sA: return llama ? 2 * F : 4 * d;  // llama: gate|up pre-activation
+            case sA: return llama ? 2 * F : 4 * d;  // llama: gate|up pre-activation; gpt2: gelu slope
             case sU: return llama ? F : 4 * d;      // MLP activation (gelu / swiglu output)
             default: return d;
         }

@@ -80,15 +80,15 @@ def test_epilogues(cuda, dtype):
     gemm(a, False, b, False, m, n, k, c, mode=1, bias=bias, aux=aux)
     torch.cuda.synchronize()
     pre = acc + bias.float()
-    assert _rel(aux, pre) < tol
     assert _rel(c, torch.nn.functional.gelu(pre, approximate="tanh")) < tol
-    # dgelu
+    # aux = gelu'(pre) (the slope the backward multiplies by)
+    x = pre.clone().requires_grad_(True)
+    (slope,) = torch.autograd.grad(torch.nn.functional.gelu(x, approximate="tanh"), x, torch.ones_like(pre))
+    assert _rel(aux, slope) < tol
+    # dgelu: C = acc * aux
     gemm(a, False, b, False, m, n, k, c, mode=2, aux=aux)
     torch.cuda.synchronize()
-    x = aux.float().requires_grad_(True)
-    y = torch.nn.functional.gelu(x, approximate="tanh")
-    (gx,) = torch.autograd.grad(y, x, acc)
-    assert _rel(c, gx) < tol
+    assert _rel(c, acc * aux.float()) < tol
 
 
 @pytest.mark.parametrize("a_mn,b_mn", list(itertools.product([False, True], repeat=2)))
