@@ -75,6 +75,13 @@ int main(int argc, char** argv) {
             }
     printf("per tile: MMA issue span %.0f ns, epilogue warp0 %.0f ns, warp last %.0f ns; gap MMA(i-1) end -> MMA(i) start %.0f ns (n=%d)\n",
            mma / n, epi0 / n, epi7 / n, stall / std::max(ns, 1), n);
+    {
+        unsigned long long t1 = 0;
+        for (int cta = 0; cta < 148; ++cta)
+            for (int k = 0; k < 6; ++k)
+                for (int i = 0; i < 16; ++i) t1 = std::max(t1, pr[cta][k][i]);
+        printf("kernel span (first MMA -> last epilogue): %.2f us\n", (t1 - t0) / 1000.0);
+    }
     for (int cta : {0, 1, 100}) {
         printf("cta %d:\n", cta);
         for (int k = 0; k < 6; ++k) {
