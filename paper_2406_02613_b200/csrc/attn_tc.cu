@@ -119,6 +119,17 @@ __device__ __forceinline__ void umma(uint32_t d, uint64_t a, uint64_t b, uint32_
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// one lane of a converged warp (the MMA issuers walk their schedule warp-wide so
+// descriptors stay in uniform registers; only the elected lane issues)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -577,64 +588,76 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
-            constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
-            int kvit = 0, ni = 0;
-            int cnt[2] = {0, 0};  // tiles issued so far per slot (s_full / p_full phases)
-            int pc_s = 0, pc_pv = 0;
-            (void)pc_s;
-            (void)pc_pv;
-            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
-                const Item w = item_of(u);
-                const int nt[2] = {w.nt0, w.nt1};
-                const int qs = ni & 1;
-                mbar_wait(&q_full[qs], (ni >> 1) & 1);
-                const uint32_t q_item = smem_u32(sQ + qs * 2 * Q_BYTES);
-                auto issue_s = [&](int x, int j) {
-                    const int s = (kvit + j) % F2_STAGES;
-                    if (x == 0 || !nt[0] || j >= nt[0]) {  // first user of K_j waits for it
-                        mbar_wait(&kv_full[s], ((kvit + j) / F2_STAGES) & 1);
-                        tc_after();
-                    }
-                    FWD_PROBE(0, pc_s);
-                    ++pc_s;
-                    const uint32_t q_base = q_item + x * Q_BYTES, k_base = smem_u32(sK + s * KV_BYTES);
-#pragma unroll
-                    for (int kk = 0; kk < HD / 16; ++kk)
-                        umma(tmem + x * 128, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024),
-                             id_s, kk > 0);
-                    umma_commit(&s_full[x]);
-                };
-                auto issue_pv = [&](int x, int j) {
-                    const int s = (kvit + j) % F2_STAGES;
-                    mbar_wait(&p_full[x], (cnt[x] + j) & 1);
+        // warp-wide walk and waits, one elected lane issues (it shares its SM
+        // sub-partition with four softmax warps: keep its instruction count low)
+        constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
+        constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
+        int kvit = 0, ni = 0;
+        int cnt[2] = {0, 0};  // tiles issued so far per slot (s_full / p_full phases)
+        int pc_s = 0, pc_pv = 0;
+        (void)pc_s;
+        (void)pc_pv;
+        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+            const Item w = item_of(u);
+            const int nt[2] = {w.nt0, w.nt1};
+            const int qs = ni & 1;
+            mbar_wait(&q_full[qs], (ni >> 1) & 1);
+            const uint32_t q_item = smem_u32(sQ + qs * 2 * Q_BYTES);
+            auto issue_s = [&](int x, int j) {
+                const int s = (kvit + j) % F2_STAGES;
+                if (x == 0 || !nt[0] || j >= nt[0]) {  // first user of K_j waits for it
+                    mbar_wait(&kv_full[s], ((kvit + j) / F2_STAGES) & 1);
                     tc_after();
-                    FWD_PROBE(1, pc_pv);
-                    ++pc_pv;
-                    const uint32_t v_base = smem_u32(sV + s * KV_BYTES);
+                }
+                if (lane == 0) FWD_PROBE(0, pc_s);
+                ++pc_s;
+                // K-major: the 16-deep k slices are 32 B apart inside the 128B swizzle row
+                const uint64_t qd = sdesc(q_item + x * Q_BYTES, 16, 1024), kd = sdesc(smem_u32(sK + s * KV_BYTES), 16, 1024);
+                if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < BKV / 16; ++kk) {
-                        umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8,
-                                sdesc(v_base + kk * 2048, 64 * 128, 1024), id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < HD / 16; ++kk) umma(tmem + x * 128, qd + 2 * kk, kd + 2 * kk, id_s, kk > 0);
+                    umma_commit(&s_full[x]);
+                }
+                __syncwarp();
+            };
+            auto issue_pv = [&](int x, int j) {
+                const int s = (kvit + j) % F2_STAGES;
+                mbar_wait(&p_full[x], (cnt[x] + j) & 1);
+                tc_after();
+                if (lane == 0) FWD_PROBE(1, pc_pv);
+                ++pc_pv;
+                // V MN-major: 16-key slices are two 8-row atoms (2048 B) apart
+                const uint64_t vd = sdesc(smem_u32(sV + s * KV_BYTES), 64 * 128, 1024);
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < BKV / 16; ++kk)
+                        umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8, vd + 128 * kk, id_o,
+                                (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                __syncwarp();
+            };
+            issue_s(0, 0);
+            if (nt[1]) issue_s(1, 0);
+            for (int j = 0; j < w.nkv; ++j) {
+                for (int x = 0; x < 2; ++x) {
+                    if (j >= nt[x]) continue;
+                    issue_pv(x, j);
+                    if (j + 1 < nt[x]) {
+                        issue_s(x, j + 1);
+                    } else {
+                        if (elect_one()) umma_commit(&o_done[x]);
+                        __syncwarp();
                     }
-                };
-                issue_s(0, 0);
-                if (nt[1]) issue_s(1, 0);
-                for (int j = 0; j < w.nkv; ++j) {
-                    for (int x = 0; x < 2; ++x) {
-                        if (j >= nt[x]) continue;
-                        issue_pv(x, j);
-                        if (j + 1 < nt[x]) issue_s(x, j + 1);
-                        else umma_commit(&o_done[x]);
-                    }
+                }
+                if (elect_one()) {
                     if (j + 1 == w.nkv) umma_commit(&q_empty[qs]);  // every S of the item issued
                     umma_commit(&kv_empty[(kvit + j) % F2_STAGES]);  // both tiles' PV_j issued
                 }
-                kvit += w.nkv;
-                cnt[0] += nt[0];
-                cnt[1] += nt[1];
+                __syncwarp();
             }
+            kvit += w.nkv;
+            cnt[0] += nt[0];
+            cnt[1] += nt[1];
         }
     } else if (warp >= 4) {
         // two groups of 8 softmax warps, one per tile slot x; in a group, warp
@@ -983,65 +1006,72 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);  // K Q^T / V dO^T
-            constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);    // P^T dO / dS^T Q (B MN-major)
-            auto issue_s = [&](int g, int kb) {  // S^T = K Q_g^T, dP^T = V dO_g^T (global tile g, K/V slot kb)
-                const int s = g % DKV_ST;
-                mbar_wait(&q_full[s], (g / DKV_ST) & 1);
-                tc_after();
-                const uint32_t k_base = smem_u32(sK + kb * BW_TILE), v_base = smem_u32(sV + kb * BW_TILE);
-                const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
+        // warp-wide walk and waits, one elected lane issues (see fa_fwd_tc2);
+        // descriptors are built once per operand tile and stepped per 16-deep slice
+        constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);  // K Q^T / V dO^T
+        constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);    // P^T dO / dS^T Q (B MN-major)
+        auto issue_s = [&](int g, int kb) {  // S^T = K Q_g^T, dP^T = V dO_g^T (global tile g, K/V slot kb)
+            const int s = g % DKV_ST;
+            mbar_wait(&q_full[s], (g / DKV_ST) & 1);
+            tc_after();
+            const uint64_t kd = sdesc(smem_u32(sK + kb * BW_TILE), 16, 1024), vd = sdesc(smem_u32(sV + kb * BW_TILE), 16, 1024);
+            const uint64_t qd = sdesc(smem_u32(sQ + s * BW_TILE), 16, 1024), od = sdesc(smem_u32(sO + s * BW_TILE), 16, 1024);
+            if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    umma(tS, sdesc(k_base + kk * 32, 16, 1024), sdesc(q_base + kk * 32, 16, 1024), id_s, kk > 0);
-                    umma(tP, sdesc(v_base + kk * 32, 16, 1024), sdesc(o_base + kk * 32, 16, 1024), id_s, kk > 0);
+                for (int kk = 0; kk < HD / 16; ++kk) {  // K-major: 32 B per slice
+                    umma(tS, kd + 2 * kk, qd + 2 * kk, id_s, kk > 0);
+                    umma(tP, vd + 2 * kk, od + 2 * kk, id_s, kk > 0);
                 }
                 umma_commit(s_full);
-            };
-            int it = 0, ni = 0;
-            if (item_at(sched, sk, 0) >= 0) {
-                mbar_wait(&kv_full[0], 0);
-                issue_s(0, 0);
             }
-            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
-                const Item w = item_of(u);
-                const int niter = G * w.nq;
-                const int kb = ni & 1;
-                const bool more = item_at(sched, sk, k + 1) >= 0;
-                for (int i = 0; i < niter; ++i) {
-                    const int g = it + i;
-                    const int s = g % DKV_ST;
-                    const uint32_t q_base = smem_u32(sQ + s * BW_TILE), o_base = smem_u32(sO + s * BW_TILE);
-                    // the next tile's S^T/dP^T (possibly the next item's first, whose
-                    // K/V is already in the other slot) overlap this tile's softmax
-                    if (i + 1 < niter) {
+            __syncwarp();
+        };
+        int it = 0, ni = 0;
+        if (item_at(sched, sk, 0) >= 0) {
+            mbar_wait(&kv_full[0], 0);
+            issue_s(0, 0);
+        }
+        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+            const Item w = item_of(u);
+            const int niter = G * w.nq;
+            const int kb = ni & 1;
+            const bool more = item_at(sched, sk, k + 1) >= 0;
+            for (int i = 0; i < niter; ++i) {
+                const int g = it + i;
+                const int s = g % DKV_ST;
+                // MN-major B: 16-query slices are two 8-row atoms (2048 B) apart
+                const uint64_t qd = sdesc(smem_u32(sQ + s * BW_TILE), 64 * 128, 1024);
+                const uint64_t od = sdesc(smem_u32(sO + s * BW_TILE), 64 * 128, 1024);
+                // the next tile's S^T/dP^T (possibly the next item's first, whose
+                // K/V is already in the other slot) overlap this tile's softmax
+                if (i + 1 < niter) {
+                    mbar_wait(s_free, g & 1);
+                    tc_after();
+                    issue_s(g + 1, kb);
+                } else {
+                    if (elect_one()) umma_commit(&kv_empty[kb]);  // every S^T/dP^T of this item issued
+                    __syncwarp();
+                    if (more) {
+                        mbar_wait(&kv_full[kb ^ 1], ((ni + 1) >> 1) & 1);
                         mbar_wait(s_free, g & 1);
                         tc_after();
-                        issue_s(g + 1, kb);
-                    } else {
-                        umma_commit(&kv_empty[kb]);  // every S^T/dP^T of this item issued
-                        if (more) {
-                            mbar_wait(&kv_full[kb ^ 1], ((ni + 1) >> 1) & 1);
-                            mbar_wait(s_free, g & 1);
-                            tc_after();
-                            issue_s(g + 1, kb ^ 1);
-                        }
+                        issue_s(g + 1, kb ^ 1);
                     }
-                    mbar_wait(p_full, g & 1);  // P^T / dS^T written
-                    tc_after();
+                }
+                mbar_wait(p_full, g & 1);  // P^T / dS^T written
+                tc_after();
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < BW_T / 16; ++kk) {  // 16 queries = 8 packed TMEM columns per step
-                        umma_ts(tDV, tPT + kk * 8, sdesc(o_base + kk * 2048, 64 * 128, 1024), id_g,
-                                (i > 0 || kk > 0) ? 1u : 0u);
-                        umma_ts(tDK, tDST + kk * 8, sdesc(q_base + kk * 2048, 64 * 128, 1024), id_g,
-                                (i > 0 || kk > 0) ? 1u : 0u);
+                        umma_ts(tDV, tPT + kk * 8, od + 128 * kk, id_g, (i > 0 || kk > 0) ? 1u : 0u);
+                        umma_ts(tDK, tDST + kk * 8, qd + 128 * kk, id_g, (i > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&q_empty[s]);
                     umma_commit(g_done);
                 }
-                it += niter;
+                __syncwarp();
             }
+            it += niter;
         }
     } else if (warp >= 4) {
         // 16 warps: quadrant wq (key rows = TMEM lanes) x quarter qq (32 of 128 queries)
@@ -1269,59 +1299,64 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);
-            constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);
-            auto issue_s = [&](int g, int qb) {  // S = Q K_g^T, dP = dO V_g^T (global tile g, Q/dO slot qb)
-                const int s = g % DQ_ST;
-                mbar_wait(&kv_full[s], (g / DQ_ST) & 1);
-                tc_after();
-                const uint32_t q_base = smem_u32(sQ + qb * BW_TILE), o_base = smem_u32(sO + qb * BW_TILE);
-                const uint32_t k_base = smem_u32(sK + s * BW_TILE), v_base = smem_u32(sV + s * BW_TILE);
+        // warp-wide walk and waits, one elected lane issues (see fa_fwd_tc2)
+        constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);
+        constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);
+        auto issue_s = [&](int g, int qb) {  // S = Q K_g^T, dP = dO V_g^T (global tile g, Q/dO slot qb)
+            const int s = g % DQ_ST;
+            mbar_wait(&kv_full[s], (g / DQ_ST) & 1);
+            tc_after();
+            const uint64_t qd = sdesc(smem_u32(sQ + qb * BW_TILE), 16, 1024), od = sdesc(smem_u32(sO + qb * BW_TILE), 16, 1024);
+            const uint64_t kd = sdesc(smem_u32(sK + s * BW_TILE), 16, 1024), vd = sdesc(smem_u32(sV + s * BW_TILE), 16, 1024);
+            if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    umma(tS, sdesc(q_base + kk * 32, 16, 1024), sdesc(k_base + kk * 32, 16, 1024), id_s, kk > 0);
-                    umma(tP, sdesc(o_base + kk * 32, 16, 1024), sdesc(v_base + kk * 32, 16, 1024), id_s, kk > 0);
+                for (int kk = 0; kk < HD / 16; ++kk) {  // K-major: 32 B per slice
+                    umma(tS, qd + 2 * kk, kd + 2 * kk, id_s, kk > 0);
+                    umma(tP, od + 2 * kk, vd + 2 * kk, id_s, kk > 0);
                 }
                 umma_commit(s_full);
-            };
-            int it = 0, ni = 0;
-            if (item_at(sched, sk, 0) >= 0) {
-                mbar_wait(&q_full[0], 0);
-                issue_s(0, 0);
             }
-            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
-                const Item w = item_of(u);
-                const int qb = ni & 1;
-                const bool more = item_at(sched, sk, k + 1) >= 0;
-                for (int j = 0; j < w.nk; ++j) {
-                    const int g = it + j;
-                    const int s = g % DQ_ST;
-                    const uint32_t k_base = smem_u32(sK + s * BW_TILE);
-                    if (j + 1 < w.nk) {
+            __syncwarp();
+        };
+        int it = 0, ni = 0;
+        if (item_at(sched, sk, 0) >= 0) {
+            mbar_wait(&q_full[0], 0);
+            issue_s(0, 0);
+        }
+        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+            const Item w = item_of(u);
+            const int qb = ni & 1;
+            const bool more = item_at(sched, sk, k + 1) >= 0;
+            for (int j = 0; j < w.nk; ++j) {
+                const int g = it + j;
+                const int s = g % DQ_ST;
+                const uint64_t kd = sdesc(smem_u32(sK + s * BW_TILE), 64 * 128, 1024);  // MN-major B
+                if (j + 1 < w.nk) {
+                    mbar_wait(s_free, g & 1);
+                    tc_after();
+                    issue_s(g + 1, qb);
+                } else {
+                    if (elect_one()) umma_commit(&q_empty[qb]);  // every S/dP of this item issued
+                    __syncwarp();
+                    if (more) {  // the next item's first S/dP under this tile's softmax
+                        mbar_wait(&q_full[qb ^ 1], ((ni + 1) >> 1) & 1);
                         mbar_wait(s_free, g & 1);
                         tc_after();
-                        issue_s(g + 1, qb);
-                    } else {
-                        umma_commit(&q_empty[qb]);  // every S/dP of this item issued
-                        if (more) {  // the next item's first S/dP under this tile's softmax
-                            mbar_wait(&q_full[qb ^ 1], ((ni + 1) >> 1) & 1);
-                            mbar_wait(s_free, g & 1);
-                            tc_after();
-                            issue_s(g + 1, qb ^ 1);
-                        }
+                        issue_s(g + 1, qb ^ 1);
                     }
-                    mbar_wait(p_full, g & 1);
-                    tc_after();
+                }
+                mbar_wait(p_full, g & 1);
+                tc_after();
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < BW_T / 16; ++kk)  // 16 keys = 8 packed TMEM columns per step
-                        umma_ts(tDQ, tDS + kk * 8, sdesc(k_base + kk * 2048, 64 * 128, 1024), id_g,
-                                (j > 0 || kk > 0) ? 1u : 0u);
+                        umma_ts(tDQ, tDS + kk * 8, kd + 128 * kk, id_g, (j > 0 || kk > 0) ? 1u : 0u);
                     umma_commit(&kv_empty[s]);
                     umma_commit(g_done);
                 }
-                it += w.nk;
+                __syncwarp();
             }
+            it += w.nk;
         }
     } else if (warp >= 4) {
         // 16 warps: quadrant wq (query rows = TMEM lanes) x quarter qq (32 of 128 keys)

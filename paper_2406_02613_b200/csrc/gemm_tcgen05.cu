@@ -89,6 +89,15 @@ __device__ __forceinline__ void watchdog(uint64_t& t0) {
     if (t0 == 0) t0 = now;
     else if (now - t0 > 4000000000ull) __trap();
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
     uint32_t spins = 0;
@@ -342,7 +351,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
     pdl_wait();
 
     if (warp == 0) {
-        if (lane == 0) {
+        // like the MMA issuer: warp-uniform walk and waits, one elected lane issues
+        {
             int it = 0;
             for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
                 int mb, nb, sp;
@@ -354,65 +364,73 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                    uint8_t* a_dst = sA + s * A_BYTES;
-                    uint8_t* b_dst = sB + s * B_BYTES;
-                    if (A_MN) {
+                    if (elect_one()) {
+                        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                        uint8_t* a_dst = sA + s * A_BYTES;
+                        uint8_t* b_dst = sB + s * B_BYTES;
+                        if (A_MN) {
 #pragma unroll
-                        for (int j = 0; j < kBM / 64; ++j)
-                            tma_load_2d(a_dst + j * 64 * kBK * 2, &tmA, &full[s], m0 + j * 64, kb * kBK);
-                    } else {
-                        tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m0);
-                    }
-                    if (B_MN) {
+                            for (int j = 0; j < kBM / 64; ++j)
+                                tma_load_2d(a_dst + j * 64 * kBK * 2, &tmA, &full[s], m0 + j * 64, kb * kBK);
+                        } else {
+                            tma_load_2d(a_dst, &tmA, &full[s], kb * kBK, m0);
+                        }
+                        if (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            tma_load_2d(b_dst + j * 64 * kBK * 2, &tmB, &full[s], n0 + j * 64, kb * kBK);
-                    } else if (ep.mode == kEpiSwiGLU) {  // gate rows, then the matching up rows
-                        tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0 / 2);
-                        tma_load_2d(b_dst + (BN / 2) * kBK * 2, &tmB, &full[s], kb * kBK, N / 2 + n0 / 2);
-                    } else {
-                        tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0);
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_2d(b_dst + j * 64 * kBK * 2, &tmB, &full[s], n0 + j * 64, kb * kBK);
+                        } else if (ep.mode == kEpiSwiGLU) {  // gate rows, then the matching up rows
+                            tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0 / 2);
+                            tma_load_2d(b_dst + (BN / 2) * kBK * 2, &tmB, &full[s], kb * kBK, N / 2 + n0 / 2);
+                        } else {
+                            tma_load_2d(b_dst, &tmB, &full[s], kb * kBK, n0);
+                        }
                     }
+                    __syncwarp();
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(kBM, BN, A_MN, B_MN);
-            int it = 0, lt = 0;
-            for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
-                int mb, nb, sp;
-                decode(sc, u, mb, nb, sp);
-                const int kb0 = sp * sc.kb_per_split;
-                const int kb1 = min(sc.kb_total, kb0 + sc.kb_per_split);
-                const int acc = lt & 1;
-                mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+        // The whole warp walks the schedule and waits (warp-uniform control, so the
+        // descriptors live in uniform registers); one elected lane issues the MMAs
+        // and commits. This keeps the issuer's instruction count per k-block low:
+        // it shares its SM sub-partition with two epilogue warps.
+        constexpr uint32_t idesc = idesc_bf16(kBM, BN, A_MN, B_MN);
+        // descriptor start-address step per 16-deep k slice (address >> 4):
+        // K-major 32 B inside the 128B swizzle row, MN-major two 8-row atoms (2048 B)
+        constexpr uint64_t a_step = A_MN ? 2048 >> 4 : 32 >> 4;
+        constexpr uint64_t b_step = B_MN ? 2048 >> 4 : 32 >> 4;
+        int it = 0, lt = 0;
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
+            int mb, nb, sp;
+            decode(sc, u, mb, nb, sp);
+            const int kb0 = sp * sc.kb_per_split;
+            const int kb1 = min(sc.kb_total, kb0 + sc.kb_per_split);
+            const int acc = lt & 1;
+            mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            tc_fence_after();
+            if (lane == 0) GEMM_PROBE(0, lt);
+            const uint32_t tmem_d = tmem_base + acc * BN;
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                const int s = it % STAGES;
+                const uint32_t ph = (it / STAGES) & 1;
+                mbar_wait(&full[s], ph);
                 tc_fence_after();
-                GEMM_PROBE(0, lt);
-                const uint32_t tmem_d = tmem_base + acc * BN;
-                for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(&full[s], ph);
-                    tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-                    const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+                const uint64_t ad = A_MN ? sdesc(smem_u32(sA + s * A_BYTES), 64 * kBK * 2, 1024)
+                                         : sdesc(smem_u32(sA + s * A_BYTES), 16, 1024);
+                const uint64_t bd = B_MN ? sdesc(smem_u32(sB + s * B_BYTES), 64 * kBK * 2, 1024)
+                                         : sdesc(smem_u32(sB + s * B_BYTES), 16, 1024);
+                if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        // K-major: advance 16 elements (32 B) inside the 128B swizzle row.
-                        // MN-major: advance 16 K-rows = two 8-row atoms (2048 B).
-                        const uint64_t ad = A_MN ? sdesc(a_base + kk * 2048, 64 * kBK * 2, 1024)
-                                                 : sdesc(a_base + kk * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? sdesc(b_base + kk * 2048, 64 * kBK * 2, 1024)
-                                                 : sdesc(b_base + kk * 32, 16, 1024);
-                        umma_bf16(tmem_d, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-                    }
+                    for (int kk = 0; kk < kBK / 16; ++kk)
+                        umma_bf16(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
                     umma_commit(&empty[s]);
                 }
-                umma_commit(&tfull[acc]);
-                GEMM_PROBE(1, lt);
+                __syncwarp();
             }
+            if (elect_one()) umma_commit(&tfull[acc]);
+            __syncwarp();
+            if (lane == 0) GEMM_PROBE(1, lt);
         }
     } else if (warp >= 4) {
         // 8 epilogue warps: warp ew handles TMEM lane quadrant wq (32 rows) and the
