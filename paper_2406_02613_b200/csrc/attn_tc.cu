@@ -567,23 +567,30 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     pdl_wait();
 
     if (warp == 0) {
-        if (lane == 0) {
+        {  // warp-wide walk and waits, one elected lane issues
             int kvit = 0, ni = 0;
             for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
                 const int qs = ni & 1;
                 mbar_wait(&q_empty[qs], ((ni >> 1) & 1) ^ 1);  // item ni-2's S MMAs are done with this slot
-                mbar_expect_tx(&q_full[qs], (w.nt1 ? 2 : 1) * Q_BYTES);
-                uint8_t* q_dst = sQ + qs * 2 * Q_BYTES;
-                tma_load_2d(q_dst, &tmQKV, &q_full[qs], w.h * HD, row_base + 2 * w.pr * BQ);
-                if (w.nt1) tma_load_2d(q_dst + Q_BYTES, &tmQKV, &q_full[qs], w.h * HD, row_base + (2 * w.pr + 1) * BQ);
+                if (elect_one()) {
+                    mbar_expect_tx(&q_full[qs], (w.nt1 ? 2 : 1) * Q_BYTES);
+                    uint8_t* q_dst = sQ + qs * 2 * Q_BYTES;
+                    tma_load_2d(q_dst, &tmQKV, &q_full[qs], w.h * HD, row_base + 2 * w.pr * BQ);
+                    if (w.nt1)
+                        tma_load_2d(q_dst + Q_BYTES, &tmQKV, &q_full[qs], w.h * HD, row_base + (2 * w.pr + 1) * BQ);
+                }
+                __syncwarp();
                 for (int j = 0; j < w.nkv; ++j, ++kvit) {
                     const int s = kvit % F2_STAGES;
                     mbar_wait(&kv_empty[s], ((kvit / F2_STAGES) & 1) ^ 1);
-                    mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
-                    tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], w.kc, row_base + j * BKV);
-                    tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], w.vc, row_base + j * BKV);
+                    if (elect_one()) {
+                        mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
+                        tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], w.kc, row_base + j * BKV);
+                        tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], w.vc, row_base + j * BKV);
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -982,7 +989,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                    tDST = tmem + 448;
 
     if (warp == 0) {
-        if (lane == 0) {
+        {  // warp-wide walk and waits, one elected lane issues
             int it = 0, ni = 0;
             for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
@@ -990,18 +997,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int row_base = w.b * T;
                 const int kb = ni & 1;
                 mbar_wait(&kv_empty[kb], ((ni >> 1) & 1) ^ 1);  // item ni-2's S^T/dP^T MMAs are done with it
-                mbar_expect_tx(&kv_full[kb], 2 * BW_TILE);
-                tma_load_2d(sK + kb * BW_TILE, &tmQKV, &kv_full[kb], kc, row_base + w.kt * BW_T);
-                tma_load_2d(sV + kb * BW_TILE, &tmQKV, &kv_full[kb], vc, row_base + w.kt * BW_T);
+                if (elect_one()) {
+                    mbar_expect_tx(&kv_full[kb], 2 * BW_TILE);
+                    tma_load_2d(sK + kb * BW_TILE, &tmQKV, &kv_full[kb], kc, row_base + w.kt * BW_T);
+                    tma_load_2d(sV + kb * BW_TILE, &tmQKV, &kv_full[kb], vc, row_base + w.kt * BW_T);
+                }
+                __syncwarp();
                 const int niter = G * w.nq;
                 for (int i = 0; i < niter; ++i, ++it) {
                     const int s = it % DKV_ST;
                     const int h = w.hk * G + i / w.nq;
                     const int q0 = (w.kt + i % w.nq) * BW_T;
                     mbar_wait(&q_empty[s], ((it / DKV_ST) & 1) ^ 1);
-                    mbar_expect_tx(&q_full[s], 2 * BW_TILE);
-                    tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
-                    tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
+                    if (elect_one()) {
+                        mbar_expect_tx(&q_full[s], 2 * BW_TILE);
+                        tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
+                        tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
+                    }
+                    __syncwarp();
                 }
             }
         }
@@ -1279,22 +1292,28 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256, tDS = tmem + 320;
 
     if (warp == 0) {
-        if (lane == 0) {
+        {  // warp-wide walk and waits, one elected lane issues
             int it = 0, ni = 0;
             for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
                 const int qb = ni & 1;
                 mbar_wait(&q_empty[qb], ((ni >> 1) & 1) ^ 1);  // item ni-2 is done with this Q/dO slot
-                mbar_expect_tx(&q_full[qb], 2 * BW_TILE);
-                tma_load_2d(sQ + qb * BW_TILE, &tmQKV, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
-                tma_load_2d(sO + qb * BW_TILE, &tmDO, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
+                if (elect_one()) {
+                    mbar_expect_tx(&q_full[qb], 2 * BW_TILE);
+                    tma_load_2d(sQ + qb * BW_TILE, &tmQKV, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
+                    tma_load_2d(sO + qb * BW_TILE, &tmDO, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
+                }
+                __syncwarp();
                 for (int j = 0; j < w.nk; ++j, ++it) {
                     const int s = it % DQ_ST;
                     mbar_wait(&kv_empty[s], ((it / DQ_ST) & 1) ^ 1);
-                    mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
-                    tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], w.kc, row_base + j * BW_T);
-                    tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], w.vc, row_base + j * BW_T);
+                    if (elect_one()) {
+                        mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
+                        tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], w.kc, row_base + j * BW_T);
+                        tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], w.vc, row_base + j * BW_T);
+                    }
+                    __syncwarp();
                 }
             }
         }
