@@ -57,6 +57,17 @@ __device__ unsigned long long g_probe[148][10][128];
 #else
 #define FWD_PROBE(kind, idx)
 #endif
+#ifdef ACCO_BWD_PROBE  // timeline probe of fa_bwd_dkv_tc (tools/diag/bwd_probe.cu only)
+__device__ unsigned long long g_bprobe[148][8][64];
+#define BWD_PROBE(kind, idx)                                                                     \
+    do {                                                                                         \
+        unsigned long long _t;                                                                   \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                   \
+        if ((idx) < 64 && blockIdx.x < 148) g_bprobe[blockIdx.x][kind][idx] = _t;                \
+    } while (0)
+#else
+#define BWD_PROBE(kind, idx)
+#endif
 constexpr float kRescaleThresh = 8.0f;  // log2 domain: rescale O only if the max grows by > 2^8
 
 constexpr int Q_BYTES = BQ * HD * 2;          // 16 KB
@@ -1029,6 +1040,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             tc_after();
             const uint64_t kd = sdesc(smem_u32(sK + kb * BW_TILE), 16, 1024), vd = sdesc(smem_u32(sV + kb * BW_TILE), 16, 1024);
             const uint64_t qd = sdesc(smem_u32(sQ + s * BW_TILE), 16, 1024), od = sdesc(smem_u32(sO + s * BW_TILE), 16, 1024);
+            if (lane == 0) BWD_PROBE(0, g);
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < HD / 16; ++kk) {  // K-major: 32 B per slice
@@ -1073,6 +1085,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 }
                 mbar_wait(p_full, g & 1);  // P^T / dS^T written
                 tc_after();
+                if (lane == 0) BWD_PROBE(1, g);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < BW_T / 16; ++kk) {  // 16 queries = 8 packed TMEM columns per step
@@ -1136,6 +1149,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     sD[s * BW_T + r] = nd;
                 }
                 asm volatile("bar.sync 1, 512;" ::: "memory");  // softmax warps only
+                if (warp == 4 && lane == 0) BWD_PROBE(2, g);
                 if (qq == 0) {  // latency hidden behind this tile
                     if (i + 1 < niter)
                         fetch(u, i + 1, nl, nd);
@@ -1144,6 +1158,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 }
                 mbar_wait(s_full, g & 1);
                 tc_after();
+                if (warp == 4 && lane == 0) BWD_PROBE(3, g);
                 // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
                 // rows past T belong to the next sequence)
                 const bool edge = qi == 0 || q0 + BW_T > T;
@@ -1176,10 +1191,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                         pk[c] = *reinterpret_cast<uint32_t*>(&a);
                         dk[c] = *reinterpret_cast<uint32_t*>(&e);
                     }
+                    if (warp == 4 && lane == 0) BWD_PROBE(4, g);
                     if (g > 0) {  // the previous dV/dK MMAs have read P^T / dS^T
                         mbar_wait(g_done, (g - 1) & 1);
                         tc_after();
                     }
+                    if (warp == 4 && lane == 0) BWD_PROBE(5, g);
                     if (i == 0 && prev >= 0) {  // previous item's accumulators are final
                         epilogue(prev);
                         prev = -1;
@@ -1190,6 +1207,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 }
                 tc_before();
                 mbar_arrive(p_full);
+                if (warp == 4 && lane == 0) BWD_PROBE(6, g);
             }
             it += niter;
             prev = u;
