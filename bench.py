@@ -16,6 +16,7 @@ baselines run on the same kernels with k=2 (equal samples per update).
 from __future__ import annotations
 
 import argparse
+import csv
 import json
 import os
 import statistics
@@ -309,17 +310,32 @@ def main():
 
     # ---- roofline of the dominant kernel class (GEMMs, tensor bound)
     p = acco["prof"]
+    # DRAM traffic per launch from the committed `ncu --set full` capture of a
+    # bench step (tools/gpu_final.sh -> profiles/prof_step_r01d_raw.csv)
+    def ncu_traffic(prefix):
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "prof_step_r01d_raw.csv")
+        try:
+            with open(path) as f:
+                rows = [r for r in csv.DictReader(f) if prefix in r["kernel"]]
+        except (OSError, KeyError):
+            return None
+        if not rows:
+            return None
+        return sum(float(r["dram_read_bytes"]) + float(r["dram_write_bytes"]) for r in rows) / len(rows)
     g = p["gemm"]
     gemm_tf = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
     roof = {"kernel": "tcgen05 bf16 GEMM (fwd/dgrad/wgrad, all launches of the timed steps)", "bound": "tensor",
             "achieved": gemm_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": gemm_tf / tf_sus,
-            "traffic": None, "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
+            "traffic": ncu_traffic("gemm_tc_kernel"),
+            "traffic_note": "mean DRAM read+write bytes per GEMM launch, ncu --set full capture of 12 step GEMMs "
+                            "(profiles/prof_step_r01d_raw.csv); operands are re-read from L2, not DRAM",
+            "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
             "launches": g["launches"], "avg_launch_ms": g["ms"] / max(g["launches"], 1),
             "share_of_step": g["ms"] / p["wall_ms"]}
     o = p["optimizer"]
     opt_gbs = o["work"] / (o["ms"] / 1e3) / 1e9 if o["ms"] > 0 else 0.0
     roof_opt = {"kernel": "fused sharded AdamW estimate (K6) / commit (K7)", "bound": "hbm", "achieved": opt_gbs,
-                "peak": hbm, "unit": "GB/s", "frac": opt_gbs / hbm, "traffic": None,
+                "peak": hbm, "unit": "GB/s", "frac": opt_gbs / hbm, "traffic": ncu_traffic("opt_kernel"),
                 "launches": o["launches"], "avg_launch_ms": o["ms"] / max(o["launches"], 1),
                 "bytes_per_elem": "18 (estimate) + 34 (commit) = 52 B per shard element per update"}
     a = p["attention"]
