@@ -149,9 +149,18 @@ __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloa
     const int lane = threadIdx.x & 31;
     if (row >= M) return;
     const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(row) * d);
+    // every load of the row (x, gamma, beta) is issued before the reductions,
+    // so their latencies overlap instead of adding up
+    uint4 xv[CH], gw[CH], bw[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+        xv[i] = xr[lane + 32 * i];
+        gw[i] = reinterpret_cast<const uint4*>(g)[lane + 32 * i];
+        if (!RMS) bw[i] = reinterpret_cast<const uint4*>(b)[lane + 32 * i];
+    }
     float v[CH * 8];
 #pragma unroll
-    for (int i = 0; i < CH; ++i) unpack8b(xr[lane + 32 * i], v + 8 * i);
+    for (int i = 0; i < CH; ++i) unpack8b(xv[i], v + 8 * i);
     float s = 0.f;
     if (!RMS) {
 #pragma unroll
@@ -166,8 +175,8 @@ __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloa
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
         float gv[8], bv[8] = {0, 0, 0, 0, 0, 0, 0, 0}, o[8];
-        unpack8b(reinterpret_cast<const uint4*>(g)[lane + 32 * i], gv);
-        if (!RMS) unpack8b(reinterpret_cast<const uint4*>(b)[lane + 32 * i], bv);
+        unpack8b(gw[i], gv);
+        if (!RMS) unpack8b(bw[i], bv);
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = (v[8 * i + k] - mu) * rs * gv[k] + bv[k];
         yr[lane + 32 * i] = pack8b(o);
@@ -191,6 +200,13 @@ __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bflo
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + o);
     const uint4* xr = reinterpret_cast<const uint4*>(x + o);
     const float mu = mean[row], rs = rstd[row];
+    uint4* dxr = reinterpret_cast<uint4*>(dx + o);
+    // the accumulated dx is loaded with the inputs (not after the reductions)
+    uint4 pv[CH];
+    if (accumulate) {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) pv[i] = dxr[lane + 32 * i];
+    }
     float xh[CH * 8], dxh[CH * 8];
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
@@ -212,11 +228,10 @@ __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bflo
     }
     s1 = RMS ? 0.f : warp_sum(s1) / d;
     s2 = warp_sum(s2) / d;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + o);
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
         float r[8], prev[8];
-        if (accumulate) unpack8b(dxr[lane + 32 * i], prev);
+        if (accumulate) unpack8b(pv[i], prev);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             r[k] = rs * (dxh[8 * i + k] - s1 - xh[8 * i + k] * s2);
