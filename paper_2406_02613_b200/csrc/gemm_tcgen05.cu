@@ -830,6 +830,37 @@ double plan_cost(int M, int N, int K, int bn, int splits, int sms) {
     return c;
 }
 
+// fp32 -> bf16 copy of the split-K workspace into C (pure-store GEMMs)
+__global__ void f32_to_bf16_rows(const float* __restrict__ ws, int64_t ldw, __nv_bfloat16* __restrict__ c,
+                                 int64_t ldc, int M, int N) {
+    ACCO_PDL_PROLOGUE();
+    const int n8 = N / 8;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(M) * n8) return;
+    const int r = static_cast<int>(i / n8), c8 = static_cast<int>(i % n8);
+    const float4* src = reinterpret_cast<const float4*>(ws + r * ldw + c8 * 8);
+    const float4 a = __ldcs(src), b = __ldcs(src + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    *reinterpret_cast<uint4*>(c + r * ldc + c8 * 8) = make_uint4(
+        pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
+}
+
+// Workspace for split-K of pure-store GEMMs (grown on demand; GEMMs are
+// stream-ordered on the compute stream, like the split-K semaphores).
+float* splitk_workspace(size_t elems, cudaStream_t s) {
+    static float* ws = nullptr;
+    static size_t cap = 0;
+    if (elems > cap) {
+        if (ws) {
+            ACCO_CUDA(cudaStreamSynchronize(s));
+            ACCO_CUDA(cudaFree(ws));
+        }
+        ACCO_CUDA(cudaMalloc(&ws, elems * sizeof(float)));
+        cap = elems;
+    }
+    return ws;
+}
+
 }  // namespace
 
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
@@ -865,6 +896,47 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
         ACCO_REQUIRE(N % 256 == 0 && !B.mn_major && !ep.residual && !ep.bias && ep.aux,
                      "gemm_bf16: SwiGLU epilogue needs N = 2F with F % 128 == 0, K-major B, aux, no bias/residual");
         dispatch_major<256, 3>(A, B, M, N, K, ep, 1, stream);
+        return;
+    }
+    // A pure-store GEMM whose tiles cannot fill the SMs and whose K is long
+    // (the LM-head dgrad: 192 tiles x 786 k-blocks) runs as an ordered split-K
+    // into an fp32 workspace (first split stores, the rest TMA-reduce-add in
+    // split order: deterministic) plus one fp32 -> bf16 pass into C.
+    const bool pure_store = ep.mode == kEpiStore && !ep.bias && !ep.residual && N % 8 == 0 && ep.ldc % 8 == 0 &&
+                            (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && !std::getenv("ACCO_GEMM_NO_WS_SPLIT");
+    int ws_bn = 0, ws_sp = 1;
+    if (pure_store) {
+        // the conversion pass, in cost units (one unit ~ 1.3 ns: a 256-wide k-block ~ 0.33 us)
+        const double conv = 6.0 * M * N / 6.5e3 / 1.3;
+        for (int bn : {256, 192, 128})
+            for (int sp : {2, 3, 4, 6, 8}) {
+                if (ceil_div(K, kBK) < 16 * sp || ceil_div(M, kBM) * ceil_div(N, bn) * 8 * 32 > kSemSlots) continue;
+                const double c = plan_cost(M, N, K, bn, sp, sms) + conv;
+                if (c < best * 0.9) {
+                    best = c;
+                    ws_bn = bn;
+                    ws_sp = sp;
+                }
+            }
+    }
+    if (ws_bn && !std::getenv("ACCO_GEMM_FORCE")) {
+        const int64_t ldw = (N + 3) / 4 * 4;
+        float* ws = splitk_workspace(static_cast<size_t>(M) * ldw, stream);
+        Epilogue e = ep;
+        e.mode = kEpiAccF32;
+        e.C = ws;
+        e.ldc = ldw;
+        e.beta = 0;
+        if (ws_bn == 256)
+            dispatch_major<256, 4>(A, B, M, N, K, e, ws_sp, stream);
+        else if (ws_bn == 192)
+            dispatch_major<192, 4>(A, B, M, N, K, e, ws_sp, stream);
+        else
+            dispatch_major<128, 5>(A, B, M, N, K, e, ws_sp, stream);
+        const int64_t n = static_cast<int64_t>(M) * (N / 8);
+        launch_pdl(f32_to_bf16_rows, static_cast<int>((n + 255) / 256), 256, 0, stream, ws, ldw,
+                   static_cast<__nv_bfloat16*>(ep.C), ep.ldc, M, N);
+        ACCO_CHECK_LAUNCH();
         return;
     }
     if (const char* f = std::getenv("ACCO_GEMM_FORCE")) {  // tuning knob: "<bn>,<splits>"

@@ -133,3 +133,26 @@ def test_every_tile_config(cuda, monkeypatch, force, a_mn, b_mn):
     assert _rel(c, ref) < 6e-3
     assert _rel(c32, c0 + ref) < 2e-6
     assert _rel(cg, torch.nn.functional.gelu(ref, approximate="tanh")) < 8e-3
+
+
+def test_pure_store_split_k_workspace(cuda, monkeypatch):
+    """A pure-store GEMM with few tiles and a long K (the LM-head dgrad shape
+    class) runs as ordered split-K into an fp32 workspace + one bf16 pass:
+    same result as the single-split kernel within bf16 rounding, bitwise
+    deterministic across runs."""
+    m, n, k = 1024, 256, 16384
+    g = torch.Generator().manual_seed(23)
+    a = torch.randn(m, k, generator=g).to(torch.bfloat16).to(cuda)
+    b = torch.randn(k, n, generator=g).to(torch.bfloat16).to(cuda)  # MN-major B, as in the head dgrad
+    ref = a.float() @ b.float()
+    c1 = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    c2 = torch.empty_like(c1)
+    gemm(a, False, b, True, m, n, k, c1)
+    gemm(a, False, b, True, m, n, k, c2)
+    monkeypatch.setenv("ACCO_GEMM_NO_WS_SPLIT", "1")
+    c0 = torch.empty_like(c1)
+    gemm(a, False, b, True, m, n, k, c0)
+    torch.cuda.synchronize()
+    assert _rel(c1, ref) < 6e-3
+    assert torch.equal(c1, c2)
+    assert _rel(c1, c0.float()) < 6e-3
