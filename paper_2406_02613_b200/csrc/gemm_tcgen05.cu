@@ -201,6 +201,7 @@ constexpr int smem_bytes() {
 
 struct Sched {
     int tiles_m, tiles_n, splits, kb_total, kb_per_split;
+    int group_m;  // m-blocks per raster group (see decode)
     __host__ __device__ int units() const { return tiles_m * tiles_n * splits; }
 };
 
@@ -209,10 +210,10 @@ __device__ __forceinline__ void decode(const Sched& s, int u, int& mb, int& nb, 
     const int tiles = s.tiles_m * s.tiles_n;
     sp = u / tiles;
     const int t = u % tiles;
-    const int per_group = kGroupM * s.tiles_n;
+    const int per_group = s.group_m * s.tiles_n;
     const int g = t / per_group;
-    const int first_m = g * kGroupM;
-    const int gsize = min(s.tiles_m - first_m, kGroupM);
+    const int first_m = g * s.group_m;
+    const int gsize = min(s.tiles_m - first_m, s.group_m);
     const int r = t % per_group;
     mb = first_m + r % gsize;
     nb = r / gsize;
@@ -780,6 +781,15 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     sc.tiles_m = ceil_div(M, kBM);
     sc.tiles_n = ceil_div(N, BN);
     sc.kb_total = ceil_div(K, kBK);
+    // raster: groups of kGroupM m-blocks sweep all n-blocks (A rows reused from
+    // L2, B streamed once per group). When B is too big to stay in L2 between
+    // groups but all of A is small, the group spans every m-block so each B
+    // n-block is read from HBM once: the LM head (B = 77 MB of embeddings, 824
+    // MB of logits streaming through L2) re-read B per group, 529 -> 492 us
+    sc.group_m = static_cast<double>(M) * K * 2 <= 32e6 && static_cast<double>(N) * K * 2 > 32e6 &&
+                         !std::getenv("ACCO_GEMM_GROUP8")
+                     ? sc.tiles_m
+                     : kGroupM;
     sc.splits = splits;
     sc.kb_per_split = ceil_div(sc.kb_total, splits);
     sc.splits = ceil_div(sc.kb_total, sc.kb_per_split);  // no empty splits
