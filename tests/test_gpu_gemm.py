@@ -156,3 +156,21 @@ def test_pure_store_split_k_workspace(cuda, monkeypatch):
     assert _rel(c1, ref) < 6e-3
     assert torch.equal(c1, c2)
     assert _rel(c1, c0.float()) < 6e-3
+
+
+def test_large_b_raster_matches_grouped_raster(cuda, monkeypatch):
+    """A GEMM whose B exceeds L2 residency (> 32 MB) with a small A takes the
+    whole-M raster (the LM-head forward); the raster only reorders tiles, so
+    the result is bitwise the 8-m-block-group raster's."""
+    m, n, k = 1024, 20480, 1024  # B = 42 MB, A = 2 MB
+    g = torch.Generator().manual_seed(29)
+    a = torch.randn(m, k, generator=g).to(torch.bfloat16).to(cuda)
+    b = torch.randn(n, k, generator=g).to(torch.bfloat16).to(cuda)
+    c1 = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+    gemm(a, False, b, False, m, n, k, c1)
+    monkeypatch.setenv("ACCO_GEMM_GROUP8", "1")
+    c2 = torch.empty_like(c1)
+    gemm(a, False, b, False, m, n, k, c2)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+    assert _rel(c1, a.float() @ b.float().t()) < 6e-3
