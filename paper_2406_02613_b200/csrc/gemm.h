@@ -7,8 +7,8 @@
 //   MN-major: A(m,k) = A.ptr[k*ld + m]      (a transposed view, e.g. dY^T in wgrad)
 //
 // The bf16 path is the tcgen05/TMA/TMEM kernel (gemm_tcgen05.cu); the fp32
-// path is a SIMT kernel used only for the fp32-accurate parity mode
-// (SURVEY.md §7 "fp64 oracle vs fp32/bf16 GPU").
+// path (the fp32-accurate parity mode, SURVEY.md §7 "fp64 oracle vs
+// fp32/bf16 GPU") is the same kernel on kind::tf32 with the 3xTF32 split.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -51,6 +51,13 @@ struct Epilogue {
 
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
                const Epilogue& ep, cudaStream_t stream);
+// fp32 operands: the 3xTF32 tcgen05 kernel (gemm_tcgen05.cu) ...
+void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
+                 const Epilogue& ep, cudaStream_t stream);
+// ... or the SIMT kernel (gemm_simt.cu; ACCO_GEMM_SIMT=1 A/B knob). gemm_f32
+// dispatches between them.
+void gemm_f32_simt(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
+                   const Epilogue& ep, cudaStream_t stream);
 void gemm_f32(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
               const Epilogue& ep, cudaStream_t stream);
 

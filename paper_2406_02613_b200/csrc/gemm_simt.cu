@@ -1,11 +1,12 @@
-// fp32 SIMT GEMM: the fp32-accurate contraction used by the parity mode
-// (precision "fp32": bf16 UMMA is ~1e-3 relative per GEMM, which
-// cannot meet the rel <= 1e-5 parity bar against the fp64 oracle). Throughput
-// runs use gemm_bf16 (tcgen05). Sequential-k accumulation, no atomics, so the
-// result is bitwise deterministic.
+// fp32 SIMT GEMM: the A/B twin of the fp32-accurate parity contraction
+// (precision "fp32" runs the 3xTF32 tcgen05 kernel, gemm_f32_tc; this kernel
+// is selected only by ACCO_GEMM_SIMT=1). Sequential-k accumulation, no
+// atomics, so the result is bitwise deterministic.
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "gemm.h"
+
+#include <cstdlib>
 
 namespace acco {
 namespace {
@@ -66,6 +67,15 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const float* __restrict_
 
 void gemm_f32(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
               cudaStream_t stream) {
+    const bool simt = std::getenv("ACCO_GEMM_SIMT") != nullptr;  // A/B knob (read per call): the SIMT kernel
+    if (simt)
+        gemm_f32_simt(A, B, M, N, K, ep, stream);
+    else
+        gemm_f32_tc(A, B, M, N, K, ep, stream);
+}
+
+void gemm_f32_simt(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
+                   cudaStream_t stream) {
     ACCO_REQUIRE(ep.mode <= kEpiAccF32, "gemm_f32: epilogue mode not supported by the SIMT path");
     ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_f32: empty problem");
     ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);

@@ -22,6 +22,15 @@
 // MN-major) and wgrad (both MN-major, fp32 accumulate epilogue into the
 // gradient-accumulation buffer: the reference's Bundle::add,
 // /root/reference/proj/src/protocols.cpp:61-66, fused into the GEMM).
+//
+// fp32-accurate variant (X3 = 1, the parity mode, precision "fp32"): the same
+// pipeline on kind::tf32 with the 3xTF32 split. A pre-pass writes every fp32
+// operand as two K-major tf32 planes, hi = rna_tf32(x) and lo = rna_tf32(x - hi)
+// (hi + lo carries 22 significand bits), and each k-slice issues
+// lo*hi + hi*lo + hi*hi into the fp32 TMEM accumulator; the dropped lo*lo term
+// and the rounding of lo are ~2^-22 relative. That keeps the fp32 contraction
+// within the rel <= 1e-5 parity bar against the fp64 oracle,
+// which one bf16 or tf32 pass (2^-8 / 2^-11) cannot meet.
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "gemm.h"
@@ -40,10 +49,12 @@ constexpr int kBK = 64;  // 64 bf16 = 128 bytes: one SW128 row
 // warps: 8 (two per TMEM lane quadrant) where the smem allows it next to a
 // deep operand ring, else 4 (the 128x256 tiles keep 4 stages: a 3-stage ring
 // costs them more than a faster epilogue gains)
-template <int BN, int STAGES>
-constexpr int epi_warps() { return (BN == 256 && STAGES == 4) ? 4 : 8; }
-template <int BN, int STAGES>
-constexpr int gemm_threads() { return 128 + 32 * epi_warps<BN, STAGES>(); }
+// (the 3xTF32 variant stages two planes per operand: 4 epilogue warps leave
+// room for a 3-deep ring of 128x128 tiles)
+template <int BN, int STAGES, int X3 = 0>
+constexpr int epi_warps() { return ((BN == 256 && STAGES == 4) || X3) ? 4 : 8; }
+template <int BN, int STAGES, int X3 = 0>
+constexpr int gemm_threads() { return 128 + 32 * epi_warps<BN, STAGES, X3>(); }
 constexpr int kGroupM = 8;
 // Per epilogue warp: 2 bf16 output chunks (or 2 fp32 chunks spanning the
 // first 8 KB) + a ring of IN_BUF 2 KB input chunks (residual / GELU aux, TMA
@@ -111,6 +122,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -192,11 +211,27 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_
            (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
            (static_cast<uint32_t>(m >> 4) << 24);
 }
+// kind::tf32: a/b format 2 (TF32), fp32 accumulator, both operands K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
 
-template <int BN, int STAGES>
+// One operand tile is 128 B per row in every variant: 64 bf16 or 32 fp32 (tf32)
+// elements of K. The 3xTF32 variant stages a hi and a lo plane per operand.
+template <int BN, int STAGES, int X3 = 0>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN) * kBK * 2 + epi_warps<BN, STAGES>() * epi_warp_bytes<BN, STAGES>() +
-           (2 * STAGES + 4 + epi_warps<BN, STAGES>() * in_bufs<BN>()) * 8 + 16;
+    return 1024 /*align slack*/ + STAGES * (kBM + BN) * 128 * (X3 ? 2 : 1) +
+           epi_warps<BN, STAGES, X3>() * epi_warp_bytes<BN, STAGES>() +
+           (2 * STAGES + 4 + epi_warps<BN, STAGES, X3>() * in_bufs<BN>()) * 8 + 16;
 }
 
 struct Sched {
@@ -296,21 +331,24 @@ struct EpiMaps {
 };
 
 // --------------------------------------------------------------------- kernel
-template <int BN, int STAGES, int A_MN, int B_MN>
-__global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
+template <int BN, int STAGES, int A_MN, int B_MN, int X3 = 0>
+__global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem) {
+    static_assert(!X3 || (!A_MN && !B_MN), "3xTF32: the split pre-pass writes K-major planes");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    constexpr int A_BYTES = kBM * kBK * 2;
-    constexpr int B_BYTES = BN * kBK * 2;
+    constexpr int A_TILE = kBM * 128;  // one plane: 128 rows x 128 B
+    constexpr int B_TILE = BN * 128;
+    constexpr int A_BYTES = A_TILE * (X3 ? 2 : 1);  // per stage (hi | lo planes for X3)
+    constexpr int B_BYTES = B_TILE * (X3 ? 2 : 1);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint8_t* sEpi = sB + STAGES * B_BYTES;  // 1024-aligned
     constexpr int kInBuf = in_bufs<BN>();
     constexpr int kEpiWarpBytes = epi_warp_bytes<BN, STAGES>();
-    constexpr int kEpiWarps = epi_warps<BN, STAGES>();
+    constexpr int kEpiWarps = epi_warps<BN, STAGES, X3>();
     constexpr int kCS = kEpiWarps / 4;  // chunk stride: epilogue warps per TMEM lane quadrant
     uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + kEpiWarps * kEpiWarpBytes);
     uint64_t* empty = full + STAGES;
@@ -365,7 +403,17 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
-                    if (elect_one()) {
+                    if (X3) {
+                        if (elect_one()) {  // hi and lo planes of both operands (3-D maps {K, rows, plane})
+                            mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                            uint8_t* a_dst = sA + s * A_BYTES;
+                            uint8_t* b_dst = sB + s * B_BYTES;
+                            tma_load_3d(a_dst, &tmA, &full[s], kb * 32, m0, 0);
+                            tma_load_3d(a_dst + A_TILE, &tmA, &full[s], kb * 32, m0, 1);
+                            tma_load_3d(b_dst, &tmB, &full[s], kb * 32, n0, 0);
+                            tma_load_3d(b_dst + B_TILE, &tmB, &full[s], kb * 32, n0, 1);
+                        }
+                    } else if (elect_one()) {
                         mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
                         uint8_t* a_dst = sA + s * A_BYTES;
                         uint8_t* b_dst = sB + s * B_BYTES;
@@ -421,7 +469,21 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES>(), 1)
                                          : sdesc(smem_u32(sA + s * A_BYTES), 16, 1024);
                 const uint64_t bd = B_MN ? sdesc(smem_u32(sB + s * B_BYTES), 64 * kBK * 2, 1024)
                                          : sdesc(smem_u32(sB + s * B_BYTES), 16, 1024);
-                if (elect_one()) {
+                if (X3) {
+                    // 4 slices of K = 8 per 128 B row; per slice lo*hi + hi*lo + hi*hi
+                    constexpr uint32_t idesc3 = idesc_tf32(kBM, BN);
+                    constexpr uint64_t a_lo = A_TILE >> 4, b_lo = B_TILE >> 4;
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t ah = ad + kk * 2, bh = bd + kk * 2;
+                            umma_tf32(tmem_d, ah + a_lo, bh, idesc3, (kb > kb0 || kk > 0) ? 1u : 0u);
+                            umma_tf32(tmem_d, ah, bh + b_lo, idesc3, 1u);
+                            umma_tf32(tmem_d, ah, bh, idesc3, 1u);
+                        }
+                        umma_commit(&empty[s]);
+                    }
+                } else if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
                         umma_bf16(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
@@ -755,7 +817,7 @@ CUtensorMap operand_map(const GemmOperand& op, int rows, int K, int tile_rows) {
     return make_map(op.ptr, K, rows, op.ld, kBK, tile_rows);             // stored [rows][K]
 }
 
-constexpr int kSemSlots = 1 << 18;  // (tile, quadrant) semaphores for ordered split-K
+constexpr int kSemSlots = 1 << 21;  // (tile, quadrant) semaphores for ordered split-K (8 MB)
 
 int* split_semaphores() {
     static int* sem = nullptr;
@@ -872,7 +934,174 @@ float* splitk_workspace(size_t elems, cudaStream_t s) {
     return ws;
 }
 
+// ------------------------------------------------------------ 3xTF32 (fp32)
+__device__ __forceinline__ float rna_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// src (K-major [rows][ld] or MN-major [K][ld]) -> planes dst[0] = hi, dst[1] =
+// lo, each K-major [rows][kp]. 32 x 32 tiles through smem so both the reads and
+// the writes are coalesced for either source major-ness.
+__global__ void tf32_split_kernel(const float* __restrict__ src, int64_t ld, int mn_major, int rows, int K,
+                                  int64_t kp, float* __restrict__ dst) {
+    ACCO_PDL_PROLOGUE();
+    __shared__ float t[32][33];
+    const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    const int64_t plane = static_cast<int64_t>(rows) * kp;
+    for (int j = ty; j < 32; j += 8) {
+        float x = 0.f;
+        if (mn_major) {  // src[k * ld + r]: lanes walk r
+            const int k = k0 + j, r = r0 + tx;
+            if (k < K && r < rows) x = src[static_cast<int64_t>(k) * ld + r];
+            t[tx][j] = x;  // t[r][k]
+        } else {  // src[r * ld + k]: lanes walk k
+            const int r = r0 + j, k = k0 + tx;
+            if (k < K && r < rows) x = src[static_cast<int64_t>(r) * ld + k];
+            t[j][tx] = x;
+        }
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int r = r0 + j, k = k0 + tx;
+        if (r < rows && k < K) {
+            const float x = t[j][tx];
+            const float hi = rna_tf32(x);
+            const int64_t o = static_cast<int64_t>(r) * kp + k;
+            dst[o] = hi;
+            dst[plane + o] = rna_tf32(x - hi);
+        }
+    }
+}
+
+// The non-accumulating epilogues of the fp32 path after the tensor-core
+// contraction: acc[M][ldw] (fp32) -> bias / GELU / dGELU / residual -> C, the
+// same per-element math as the SIMT kernel's epilogue_row<float>.
+__global__ void f32_epilogue_kernel(const float* __restrict__ acc, int64_t ldw, int M, int N, Epilogue ep) {
+    ACCO_PDL_PROLOGUE();
+    const int n4 = (N + 3) / 4;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<int64_t>(M) * n4) return;
+    const int r = static_cast<int>(i / n4), c = static_cast<int>(i % n4) * 4;
+    float x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = c + j < N ? acc[r * ldw + c + j] : 0.f;
+    epilogue_row<float, 4>(ep, r, c, min(4, N - c), x);
+}
+
+// Stream-ordered scratch from the device's default memory pool: each call
+// allocates on the launching stream and frees after its last use on that
+// stream, so concurrent GEMMs on different streams or devices never share it.
+void* pool_alloc(size_t bytes, cudaStream_t s) {
+    static std::once_flag once[64];
+    int dev = 0;
+    ACCO_CUDA(cudaGetDevice(&dev));
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        ACCO_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = ~0ull;  // keep freed blocks cached: the same sizes recur every micro-batch
+        ACCO_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    });
+    void* p = nullptr;
+    ACCO_CUDA(cudaMallocAsync(&p, bytes, s));
+    return p;
+}
+
+void launch_x3(const float* a_planes, const float* b_planes, int64_t kp, int M, int N, int K, const Epilogue& ep,
+               int splits, cudaStream_t stream) {
+    constexpr int BN = 128, STAGES = 3;
+    auto kern = gemm_tc_kernel<BN, STAGES, 0, 0, 1>;
+    constexpr int smem = smem_bytes<BN, STAGES, 1>();
+    static_assert(smem <= 232448, "shared memory budget");
+    static bool configured = false;
+    if (!configured) {
+        ACCO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        configured = true;
+    }
+    Sched sc;
+    sc.tiles_m = ceil_div(M, kBM);
+    sc.tiles_n = ceil_div(N, BN);
+    sc.kb_total = ceil_div(K, 32);
+    sc.group_m = kGroupM;
+    sc.kb_per_split = ceil_div(sc.kb_total, splits);
+    sc.splits = ceil_div(sc.kb_total, sc.kb_per_split);
+    auto planes = [&](const float* p, int rows, uint32_t box_rows) {
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), 2};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(kp) * 4, static_cast<cuuint64_t>(kp) * 4 * rows};
+        cuuint32_t box[3] = {32, box_rows, 1};
+        return encode(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    };
+    EpiMaps em;
+    std::memset(&em, 0, sizeof(em));
+    em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
+    int* sem = nullptr;
+    if (sc.splits > 1) {
+        ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 8 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
+        sem = split_semaphores();
+    }
+    const CUtensorMap ta = planes(a_planes, M, kBM), tb = planes(b_planes, N, BN);
+    const int grid = std::min(sc.units(), num_sms());
+    launch_pdl(kern, grid, gemm_threads<BN, STAGES, 1>(), smem, stream, ta, tb, em, M, N, sc, ep, sem);
+    ACCO_CHECK_LAUNCH();
+}
+
 }  // namespace
+
+// fp32-accurate GEMM on the tensor cores (precision "fp32"): split pre-pass,
+// 3xTF32 tcgen05 contraction into fp32, then the epilogue. kEpiAccF32 goes
+// straight into C (TMA store / reduce-add, ordered split-K); the other
+// epilogues contract into a scratch accumulator first (C may alias the
+// residual) and finish in f32_epilogue_kernel.
+void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
+                 cudaStream_t stream) {
+    ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_f32: empty problem");
+    ACCO_REQUIRE(ep.mode <= kEpiAccF32, "gemm_f32: epilogue mode not supported by the fp32 path");
+    ACCO_REQUIRE(ep.mode == kEpiStore || ep.mode == kEpiAccF32 || ep.aux, "gemm_f32: GELU epilogues need aux");
+    ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
+    const int64_t kp = (K + 3) / 4 * 4;  // 16 B row stride for TMA
+    float* pa = static_cast<float*>(pool_alloc(sizeof(float) * 2 * kp * (M + N), stream));
+    float* pb = pa + 2 * kp * M;
+    launch_pdl(tf32_split_kernel, dim3(ceil_div(K, 32), ceil_div(M, 32)), 256, 0, stream,
+               static_cast<const float*>(A.ptr), A.ld, static_cast<int>(A.mn_major), M, K, kp, pa);
+    ACCO_CHECK_LAUNCH();
+    launch_pdl(tf32_split_kernel, dim3(ceil_div(K, 32), ceil_div(N, 32)), 256, 0, stream,
+               static_cast<const float*>(B.ptr), B.ld, static_cast<int>(B.mn_major), N, K, kp, pb);
+    ACCO_CHECK_LAUNCH();
+    // Ordered split-K bounds the accumulation chain in TMEM. The tensor core's
+    // fp32 accumulation error grows linearly with the number of MMAs chained
+    // into one accumulator (measured, tools/diag/tf32_accuracy.py: ~2.2e-7
+    // relative per 32-deep k-block, so 7e-6 at K = 8192 unsplit), while the
+    // split partials are summed by round-to-nearest fp32 TMA reduce-adds in
+    // split order. A chain of 4 k-blocks (K = 128) holds every contraction at
+    // ~1e-6 whatever K is, SIMT-fp32 level. ACCO_TF32_CHAIN=<k-blocks> overrides.
+    const int tiles = ceil_div(M, kBM) * ceil_div(N, 128), kbt = ceil_div(K, 32);
+    int chain = 4;
+    if (const char* c = std::getenv("ACCO_TF32_CHAIN")) chain = std::max(1, std::atoi(c));
+    int splits = ceil_div(kbt, chain);
+    if (const char* f = std::getenv("ACCO_TF32_SPLITS")) splits = std::max(1, std::atoi(f));
+    if (tiles * 8 * 32 > kSemSlots) splits = 1;
+    const bool direct = ep.mode == kEpiAccF32 && ep.ldc % 4 == 0 && (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0;
+    if (direct) {
+        launch_x3(pa, pb, kp, M, N, K, ep, splits, stream);
+    } else {
+        const int64_t ldw = (N + 3) / 4 * 4;
+        float* ws = static_cast<float*>(pool_alloc(sizeof(float) * ldw * M, stream));
+        Epilogue e;
+        e.mode = kEpiAccF32;
+        e.C = ws;
+        e.ldc = ldw;
+        e.beta = 0;
+        launch_x3(pa, pb, kp, M, N, K, e, splits, stream);
+        const int64_t n = static_cast<int64_t>(M) * ((N + 3) / 4);
+        launch_pdl(f32_epilogue_kernel, static_cast<int>((n + 255) / 256), 256, 0, stream,
+                   static_cast<const float*>(ws), ldw, M, N, ep);
+        ACCO_CHECK_LAUNCH();
+        ACCO_CUDA(cudaFreeAsync(ws, stream));
+    }
+    ACCO_CUDA(cudaFreeAsync(pa, stream));
+}
 
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
                cudaStream_t stream) {
