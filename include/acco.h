@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define ACCO_ABI_VERSION 1
+#define ACCO_ABI_VERSION 2
 
 #define ACCO_OK 0
 #define ACCO_VERIFY_FAIL 1  /* accosim exit 1 */
@@ -99,8 +99,9 @@ typedef struct acco_shard_state {
  * shard state: theta_est = Opt(theta, gsum / total); m, v and step are NOT
  * written. `total` is read from device memory (the counts all-reduce output).
  * Output dtype is ACCO_DTYPE_F32 or ACCO_DTYPE_BF16 (the all-gather payload).
- * `nonfinite_flag` (device int, nullable) is set to 1 if any input is
- * non-finite — opt_step's std::invalid_argument (optim.cpp:56-57). */
+ * `nonfinite_flag` (device int, nullable) gets bit 0 (value 1) if any input is
+ * non-finite — opt_step's std::invalid_argument (optim.cpp:56-57) — and bit 1
+ * (value 2) if a new parameter is non-finite. */
 int acco_opt_estimate(const acco_opt_cfg* cfg, const acco_shard_state* st, const float* gsum,
                       const int64_t* total_dev, void* theta_out, int out_dtype,
                       int* nonfinite_flag, void* stream);
@@ -267,6 +268,8 @@ typedef struct acco_run_stats {
     int diverged;
     long long h2d_bytes; /* host-data path: token rows shipped host->device */
     long long d2h_bytes; /* host-data path: per-micro-batch losses read back */
+    int n_records;       /* valid rows of recs / mb_counts / theta_history: t_updates, or fewer
+                            when the run diverged (the reference's partial RunTrace) */
 } acco_run_stats;
 
 typedef struct acco_trainer acco_trainer;
@@ -278,6 +281,13 @@ int acco_trainer_set_theta(acco_trainer* t, const float* host_theta);
 /* which: 0 committed theta replica, 1 estimate replica, 2 this rank's fp32 master shard. */
 int acco_trainer_get_theta(acco_trainer* t, int which, float* host_out);
 /* Runs t_updates committed updates (continuing). recs: [t_updates];
+ * Divergence, as the reference (protocols.cpp:113-119,164-167,298-306;
+ * optim.cpp:56-57): a non-finite parameter state or evaluated loss at a commit
+ * ends the run with that record (loss +inf for the state) and returns
+ * ACCO_DIVERGED; a synchronous round whose reduced mean is non-finite ends it
+ * before its record (ACCO_DIVERGED); in ACCO a non-finite input to either
+ * optimizer step is the reference's opt_step invalid_argument: ACCO_INVALID,
+ * no records. stats->n_records counts the valid rows.
  * mb_counts (nullable): [t_updates][2][n_local] (mb_estimate, mb_main);
  * theta_history (nullable, host fp32): [t_updates][2][psi] = theta^(t+1) and
  * theta-tilde^(t+1) after each commit (RunTrace.theta/estimate_history,

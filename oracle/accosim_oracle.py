@@ -461,24 +461,29 @@ class _Commit:
         nan = float("nan")
         loss = gsq = gsq_e = nan
         lyap = None
-        if self.eval_fn is not None and self.eval_every > 0 and (update + 1) % self.eval_every == 0:
-            if np.all(np.isfinite(theta)) and np.all(np.isfinite(estimate)):
-                loss, g = self.eval_fn(theta)
-                le, ge = self.eval_fn(estimate)
-                gsq = _dot_seq(g, g)
-                gsq_e = _dot_seq(ge, ge)
-                if self.fstar is not None:
-                    d = theta - estimate
-                    lyap = (loss - self.fstar) + self.eta * self.l * (le - self.fstar) + self.l * _dot_seq(d, d)
-            else:
-                loss = gsq = gsq_e = float("inf")
+        evaluated = False
+        if not (np.all(np.isfinite(theta)) and np.all(np.isfinite(estimate))):
+            # finite_state check (protocols.cpp:113-119): +inf whatever the cadence
+            loss = gsq = gsq_e = float("inf")
+            evaluated = True
+        elif self.eval_fn is not None and self.eval_every > 0 and (update + 1) % self.eval_every == 0:
+            evaluated = True
+            loss, g = self.eval_fn(theta)
+            le, ge = self.eval_fn(estimate)
+            gsq = _dot_seq(g, g)
+            gsq_e = _dot_seq(ge, ge)
+            if self.fstar is not None:
+                d = theta - estimate
+                lyap = (loss - self.fstar) + self.eta * self.l * (le - self.fstar) + self.l * _dot_seq(d, d)
         self.samples_cum += consumed
         trace.records.append(Record(update, loss, gsq, gsq_e, lyap, self.samples_cum, list(mb_main),
                                     list(mb_est), train_loss))
         trace.theta_history.append(theta.copy())
         trace.estimate_history.append(estimate.copy())
         trace.consumed_mean_grad.append(mean)
-        if not math.isfinite(loss) and not math.isnan(loss):
+        # NaN marks "not evaluated" under an eval cadence; an evaluated
+        # non-finite loss (inf or NaN) is divergence (protocols.cpp:164-167)
+        if evaluated and not math.isfinite(loss):
             trace.diverged = True
             return False
         return True
@@ -670,8 +675,25 @@ def run_wp(grad_fn, theta0, cfg, sim, t_updates, **kw) -> Trace:
     return _run_delayed("wp", grad_fn, theta0, cfg, sim, t_updates, **kw)
 
 
+class ProtocolLogicError(RuntimeError):
+    """std::logic_error of the reference (protocol invariants)."""
+
+
+def check_theta0(method: str, theta0: np.ndarray, n_workers: int) -> None:
+    """A non-finite theta0 fails where the reference first touches it: the
+    synchronous rounds start with check_replicas (protocols.cpp:208-212,
+    321-322; NaN != NaN across >= 2 replicas: logic_error), otherwise the first
+    stochastic_grad's check_theta throws invalid_argument (problems.cpp:37-42)."""
+    if np.all(np.isfinite(theta0)):
+        return
+    if method != "acco" and n_workers >= 2:
+        raise ProtocolLogicError("protocol: parameter divergence across workers")
+    raise ValueError("theta has non-finite entries")
+
+
 def run_method(method: str, grad_fn, theta0, cfg, sim, t_updates, schedule=None, **kw) -> Trace:
     """run_protocol's dispatch (protocols.cpp:734-741)."""
+    check_theta0(method, np.asarray(theta0), sim.n_workers)
     if method == "acco":
         return run_acco(grad_fn, theta0, cfg, sim, t_updates, schedule=schedule, **kw)
     if method in ("ddp", "zero1"):

@@ -10,6 +10,9 @@
 //   io/            write_run_outputs of one run + the trace it was written from
 //                  (proj/src/csvio.cpp:12-102, config.cpp:147-157)
 //   memory.json    memory_model_bytes / memory_reported_gb (proj/src/convergence.cpp:182-205)
+//   divergence.json partial traces / exceptions of diverging runs
+//                  (protocols.cpp:113-119,164-167,298-306; optim.cpp:56-57;
+//                  the case of proj/tests/test_protocols.cpp:328-336)
 #include <cmath>
 #include <cstdio>
 #include <limits>
@@ -228,9 +231,10 @@ static json problem_json(const Problem& p) {
 }
 
 static json run_case(const std::string& name, Method m, const Problem& p, OptimizerConfig cfg,
-                     const SimConfig& sim, int t) {
+                     const SimConfig& sim, int t, std::vector<double> theta0 = {}) {
     RunOptions opts;
     opts.record_details = true;
+    opts.theta0 = std::move(theta0);
     RunTrace tr = run_protocol(m, p, cfg, sim, t, opts);
     if (cfg.total_steps == 0) cfg.total_steps = t;
     json j;
@@ -417,6 +421,45 @@ static json protocols_fixture() {
     return cases;
 }
 
+// Diverging runs. json has no inf / NaN: non-finite losses and parameters are
+// written as null (nlohmann's encoding).
+static json divergence_fixture() {
+    json cases = json::array();
+    auto sgd = [](double lr) {
+        OptimizerConfig c;
+        c.kind = OptKind::sgd;
+        c.learning_rate = lr;
+        return c;
+    };
+    // proj/tests/test_protocols.cpp:328-336, for every method
+    auto guarded_case = [&](const std::string& name, Method m, const Problem& p, OptimizerConfig cfg,
+                            const SimConfig& sim, int t, std::vector<double> theta0) {
+        try {
+            cases.push_back(run_case(name, m, p, cfg, sim, t, std::move(theta0)));
+        } catch (const std::invalid_argument& e) {
+            cases.push_back({{"name", name}, {"method", to_string(m)}, {"throws", "invalid_argument"}, {"what", e.what()}});
+        } catch (const std::logic_error& e) {
+            cases.push_back({{"name", name}, {"method", to_string(m)}, {"throws", "logic_error"}, {"what", e.what()}});
+        }
+    };
+    for (Method m : {Method::ddp, Method::dpu, Method::wp, Method::acco}) {
+        SimConfig sim;
+        guarded_case(std::string(to_string(m)) + "_identity_sgd1e8", m, make_identity_quadratic(1), sgd(1e8), sim,
+                     200, {1.0});
+    }
+    // a non-finite theta0: the synchronous rounds see a non-finite mean (diverged,
+    // no record); ACCO's optimizer step throws invalid_argument
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    for (Method m : {Method::ddp, Method::acco}) {
+        SimConfig sim;
+        sim.n_workers = 2;
+        sim.batch_size = 2;
+        guarded_case(std::string(to_string(m)) + "_nan_theta0", m, make_quadratic(3, 3, 0.2, 1.0, 0.1), sgd(0.1),
+                     sim, 5, {1.0, nan, 0.5});
+    }
+    return cases;
+}
+
 static json io_fixture(const std::string& dir) {
     // the config of proj/tests/test_io.cpp:17-37
     json cfgj = {
@@ -491,5 +534,6 @@ int main(int argc, char** argv) {
     write(dir, "protocols.json", protocols_fixture());
     write(dir, "io_trace.json", io_fixture(dir));
     write(dir, "memory.json", memory_fixture());
+    write(dir, "divergence.json", divergence_fixture());
     return 0;
 }

@@ -56,7 +56,7 @@ class StatsC(C.Structure):
                 ("discarded_micro_batches", C.c_longlong), ("wall_ms", C.c_double),
                 ("compute_busy_ms", C.c_double), ("comm_busy_ms", C.c_double), ("comm_exposed_ms", C.c_double),
                 ("opt_ms", C.c_double), ("opt_launches", C.c_int), ("diverged", C.c_int),
-                ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong)]
+                ("h2d_bytes", C.c_longlong), ("d2h_bytes", C.c_longlong), ("n_records", C.c_int)]
 
 
 class IntervalC(C.Structure):
@@ -430,8 +430,13 @@ class Trainer:
         diverged = rc == _lib.DIVERGED
         if rc not in (_lib.OK, _lib.DIVERGED):
             _lib.check(rc)
+        # a diverged run keeps the records up to the divergence (the
+        # reference's partial RunTrace, protocols.cpp:164-167)
+        n_rec = st.n_records
+        if hist is not None:
+            hist = hist[:n_rec]
         out = []
-        for i in range(t_updates):
+        for i in range(n_rec):
             r = recs[i]
             out.append(RoundRecord(r.update, r.time_s, r.loss, r.grad_sq, r.grad_sq_estimate, r.lyapunov,
                                    r.samples_cum, counts[i, 1].tolist(), counts[i, 0].tolist(), r.train_loss))

@@ -265,7 +265,6 @@ int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t*
                     mb_counts[(i * 2 + 0) * nl + w] = r[i].mb_estimate[static_cast<size_t>(w)];
                     mb_counts[(i * 2 + 1) * nl + w] = r[i].mb_main[static_cast<size_t>(w)];
                 }
-            if (std::isinf(r[i].loss)) diverged = 1;
         }
         if (stats) {
             stats->issued_micro_batches = st.issued;
@@ -277,14 +276,15 @@ int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t*
             stats->comm_exposed_ms = st.comm_exposed_ms;
             stats->opt_ms = st.opt_ms;
             stats->opt_launches = st.opt_launches;
-            stats->diverged = st.diverged || diverged;
+            stats->diverged = st.diverged;
             stats->h2d_bytes = st.h2d_bytes;
             stats->d2h_bytes = st.d2h_bytes;
+            stats->n_records = st.n_records;
         }
         if (st.diverged) diverged = 1;
     });
     if (rc == kOk && diverged) {
-        set_last_error("run diverged: non-finite optimizer input or loss");
+        set_last_error("run diverged: non-finite parameters or evaluated loss");
         return kDiverged;
     }
     return rc;

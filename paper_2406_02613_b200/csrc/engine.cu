@@ -20,6 +20,7 @@
 #include "lm_kernels.h"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <numeric>
@@ -127,7 +128,7 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
 Trainer::~Trainer() {
     cudaStreamSynchronize(cs_);
     cudaStreamSynchronize(ms_);
-    void* bufs[] = {theta_act_, est_act_, master_, m_, v_, pad_send_, g_ret_, g_main_, cnt_send_, flag_,
+    void* bufs[] = {theta_act_, est_act_, master_, m_, v_, pad_send_, g_ret_, g_main_, cnt_send_,
                     loss_ring_, eval_grad_, eval_scratch_};
     for (void* b : bufs) cudaFree(b);
     if (ag_theta_ != theta_act_) cudaFree(ag_theta_);
@@ -170,8 +171,6 @@ void Trainer::alloc() {
     if (comm_ || peer_ || n_local_ > 1) ACCO_CUDA(cudaMalloc(&g_ret_, own_cap * 4));  // retained estimate shard
     if (comm_) ACCO_CUDA(cudaMalloc(&g_main_, own_cap * 4));                  // reduce-scatter target
     ACCO_CUDA(cudaMalloc(&cnt_send_, 8));
-    ACCO_CUDA(cudaMalloc(&flag_, sizeof(int)));
-    ACCO_CUDA(cudaMemset(flag_, 0, sizeof(int)));
     loss_cap_ = 1 << 16;
     ACCO_CUDA(cudaMalloc(&loss_ring_, loss_cap_ * sizeof(double)));
     if (model_->host_data()) ACCO_CUDA(cudaHostAlloc(&loss_host_, loss_cap_ * sizeof(double), cudaHostAllocDefault));
@@ -183,6 +182,12 @@ void Trainer::alloc() {
 
 void Trainer::set_theta(const float* host) {
     const size_t P = static_cast<size_t>(psi_);
+    theta0_nonfinite_ = false;
+    for (size_t i = 0; i < P; ++i)
+        if (!std::isfinite(host[i])) {
+            theta0_nonfinite_ = true;
+            break;
+        }
     float* tmp = nullptr;
     ACCO_CUDA(cudaMalloc(&tmp, P * 4));
     ACCO_CUDA(cudaMemcpy(tmp, host, P * 4, cudaMemcpyHostToDevice));
@@ -320,7 +325,7 @@ void Trainer::opt_gather(bool commit, FoldIO io, const float* ret, const int64_t
             io.dst[r] = static_cast<char*>(peer_->peer_buffer(r, static_cast<int>(acc_.size()) + ri)) +
                         static_cast<size_t>(own_lo_) * e;
         io.ndst = world_;
-        opt_fold(cfg_, step_, commit, io, ret, tot, ret_tot, master_, m_, v_, own_n_, act, flag_, ms_);
+        opt_fold(cfg_, step_, commit, io, ret, tot, ret_tot, master_, m_, v_, own_n_, act, cur_flag_, ms_);
         if (after_opt) ACCO_CUDA(cudaEventRecord(after_opt, ms_));
         return;
     }
@@ -328,7 +333,7 @@ void Trainer::opt_gather(bool commit, FoldIO io, const float* ret, const int64_t
     void* out = sharded ? static_cast<char*>(ag_dst) + static_cast<size_t>(rank_) * chunk_ * e : act_dst;
     io.dst[0] = out;
     io.ndst = 1;
-    opt_fold(cfg_, step_, commit, io, ret, tot, ret_tot, master_, m_, v_, own_n_, act, flag_, ms_);
+    opt_fold(cfg_, step_, commit, io, ret, tot, ret_tot, master_, m_, v_, own_n_, act, cur_flag_, ms_);
     if (after_opt) ACCO_CUDA(cudaEventRecord(after_opt, ms_));
     if (!sharded) return;
     comm_->all_gather(out, ag_dst, static_cast<size_t>(chunk_), act, ms_);
@@ -352,6 +357,9 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
     long long local = 0;
     for (int w = 0; w < n_local_; ++w) local += ev.counts[static_cast<size_t>(p) * n_local_ + w];
     int64_t* totp = tot + p;
+    // non-finite bits: one slot per ACCO phase; the synchronous family uses
+    // slot 2r for the round's step and 2r+1 for WP's prediction step
+    cur_flag_ = phase_flags_ + (method_ == kACCO ? p : 2 * p);
     // 1. Fabric::all_reduce_counts (collectives.cpp:48-53)
     const unsigned long long seq = ++phase_seq_;
     if (peer_) {  // post + wait for every rank's post; counts folded in rank order
@@ -394,7 +402,10 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
             opt_gather(true, io, nullptr, totp, nullptr, theta_act_, ag_theta_, ev.opt_done[p]);
             ++step_;
             // WP: prediction step from the updated state on a throwaway copy (protocols.cpp:398-403)
-            if (method_ == kWP) opt_gather(false, io, nullptr, totp, nullptr, est_act_, ag_est_, nullptr);
+            if (method_ == kWP) {
+                cur_flag_ = phase_flags_ + 2 * p + 1;
+                opt_gather(false, io, nullptr, totp, nullptr, est_act_, ag_est_, nullptr);
+            }
         }
     }
     if (peer_) peer_->signal_done(seq, ms_);  // this rank's shard is in every replica
@@ -406,9 +417,19 @@ void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* t
     ACCO_REQUIRE(!peer_ || peer_->connected(), "peer fabric: connect the ranks before run()");
     if (peer_ && phase_seq_ > 0) peer_->wait_done(phase_seq_, cs_);  // peers finished writing our replicas
     if (cfg_.total_steps == 0) cfg_.total_steps = T;  // run_protocol, protocols.cpp:729
+    if (theta0_nonfinite_ && update_ == 0) {
+        // where the reference first touches theta0: the synchronous rounds'
+        // check_replicas (NaN != NaN across >= 2 replicas, protocols.cpp:208-212),
+        // else the first stochastic_grad's check_theta (problems.cpp:37-42)
+        if (method_ != kACCO && sim_.n_workers >= 2)
+            throw Error(kLogicError, "protocol: parameter divergence across workers");
+        throw Error(kInvalidArg, "theta has non-finite entries");
+    }
     recs.clear();
     st = RunStats{};
     if (theta_hist) ACCO_CUDA(cudaMalloc(&hist_dev_, static_cast<size_t>(T) * 2 * psi_ * model_->act_bytes()));
+    ACCO_CUDA(cudaMalloc(&phase_flags_, static_cast<size_t>(2 * T) * sizeof(int)));
+    ACCO_CUDA(cudaMemsetAsync(phase_flags_, 0, static_cast<size_t>(2 * T) * sizeof(int), cs_));
     const long long h2d0 = model_->h2d_bytes(), d2h0 = d2h_bytes_;
     try {
         if (method_ == kACCO)
@@ -425,10 +446,14 @@ void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* t
     } catch (...) {
         if (hist_dev_) cudaFree(hist_dev_);
         hist_dev_ = nullptr;
+        cudaFree(phase_flags_);
+        phase_flags_ = cur_flag_ = nullptr;
         throw;
     }
     if (hist_dev_) cudaFree(hist_dev_);
     hist_dev_ = nullptr;
+    cudaFree(phase_flags_);
+    phase_flags_ = cur_flag_ = nullptr;
 }
 
 // after the commit of update t (comm stream): copy theta^(t+1), theta-tilde^(t+1)
@@ -639,11 +664,25 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
         evh.resize(static_cast<size_t>(T) * 2 * (n_eval_chunks + 1));
         ACCO_CUDA(cudaMemcpy(evh.data(), eval_buf, evh.size() * sizeof(double), cudaMemcpyDeviceToHost));
     }
-    int flag = 0;
-    ACCO_CUDA(cudaMemcpy(&flag, flag_, sizeof(int), cudaMemcpyDeviceToHost));
-    st.diverged = flag;
+    std::vector<int> pf(static_cast<size_t>(NP));
+    ACCO_CUDA(cudaMemcpy(pf.data(), phase_flags_, NP * sizeof(int), cudaMemcpyDeviceToHost));
+    // the reference's order of events: phase 2t (estimate), phase 2t+1
+    // (commit), then TraceBuilder::commit of update t. A non-finite input to
+    // either optimizer step throws invalid_argument out of run_protocol
+    // (optim.cpp:56-57: no trace, CLI exit 2); a non-finite state or
+    // evaluated loss at the commit ends the run with that record (loss = +inf
+    // for a non-finite state, protocols.cpp:113-119,164-167: exit 3).
+    int first_bad_input = -1;
+    for (int p = 0; p < NP && first_bad_input < 0; ++p)
+        if (pf[static_cast<size_t>(p)] & 1) first_bad_input = p;
     const int n = model_->cfg().n_samples;
+    std::string invalid;  // thrown after this run's resources are released
     for (int t = 0; t < T; ++t) {
+        if (first_bad_input >= 0 && first_bad_input <= 2 * t + 1) {
+            invalid = "opt_step: non-finite input (update " + std::to_string(update_ + t) +
+                      (first_bad_input % 2 == 0 ? ", estimate phase)" : ", commit phase)");
+            break;
+        }
         UpdateRecord r;
         r.update = static_cast<int>(update_) + t;
         r.time_s = elapsed(base, ev.done[2 * t + 1]) * 1e-3;
@@ -668,9 +707,17 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             r.grad_sq = e0[n_eval_chunks];
             r.grad_sq_estimate = e0[2 * n_eval_chunks + 1];
         }
+        const bool evaluated = do_eval && (update_ + t + 1) % sim_.eval_every == 0;
+        const bool bad_state = ((pf[static_cast<size_t>(2 * t)] | pf[static_cast<size_t>(2 * t + 1)]) & 2) != 0;
+        if (bad_state) r.loss = r.grad_sq = r.grad_sq_estimate = INFINITY;
         st.consumed += comb / B;
         recs.push_back(r);
+        if (bad_state || (evaluated && !std::isfinite(r.loss))) {
+            st.diverged = 1;
+            break;
+        }
     }
+    st.n_records = static_cast<int>(recs.size());
     st.issued = nmb;
     // timeline: comm phases vs compute stages
     std::vector<std::pair<double, double>> comm_iv, comp_iv;
@@ -693,6 +740,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     cudaEventDestroy(base);
     cudaFree(tot);
     if (eval_buf) cudaFree(eval_buf);
+    if (!invalid.empty()) throw Error(kInvalidArg, invalid);
 }
 
 // Synchronous family (SyncEngine, protocols.cpp:218-425). DDP / ZeRO-1: the
@@ -836,11 +884,24 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
         evh.resize(static_cast<size_t>(T) * 2 * (n_eval_chunks + 1));
         ACCO_CUDA(cudaMemcpy(evh.data(), eval_buf, evh.size() * sizeof(double), cudaMemcpyDeviceToHost));
     }
-    int flag = 0;
-    ACCO_CUDA(cudaMemcpy(&flag, flag_, sizeof(int), cudaMemcpyDeviceToHost));
-    st.diverged = flag;
+    std::vector<int> pf(static_cast<size_t>(2 * T));
+    ACCO_CUDA(cudaMemcpy(pf.data(), phase_flags_, 2 * T * sizeof(int), cudaMemcpyDeviceToHost));
     const int n = model_->cfg().n_samples;
+    std::string invalid;  // thrown after this run's resources are released
     for (int r = 0; r < T; ++r) {
+        // apply_and_commit (protocols.cpp:298-318): a non-finite mean ends the
+        // run before the round's record; a non-finite new state or evaluated
+        // loss ends it with the record (loss = +inf for the state). WP's
+        // prediction opt_step on a non-finite theta throws invalid_argument
+        // (protocols.cpp:398-403, optim.cpp:56-57).
+        if (pf[static_cast<size_t>(2 * r)] & 1) {
+            st.diverged = 1;
+            break;
+        }
+        if (pf[static_cast<size_t>(2 * r + 1)] & 1) {
+            invalid = "opt_step: non-finite input (update " + std::to_string(update_ + r) + ", prediction step)";
+            break;
+        }
         UpdateRecord rec;
         rec.update = static_cast<int>(update_) + r;
         rec.time_s = elapsed(base, ev.done[r]) * 1e-3;
@@ -860,9 +921,17 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             rec.grad_sq = e0[n_eval_chunks];
             rec.grad_sq_estimate = est_is_theta[static_cast<size_t>(r)] ? rec.grad_sq : e0[2 * n_eval_chunks + 1];
         }
+        const bool evaluated = do_eval && (update_ + r + 1) % sim_.eval_every == 0;
+        const bool bad_state = ((pf[static_cast<size_t>(2 * r)] | pf[static_cast<size_t>(2 * r + 1)]) & 2) != 0;
+        if (bad_state) rec.loss = rec.grad_sq = rec.grad_sq_estimate = INFINITY;
         st.consumed += tot_h[r] / B;
         recs.push_back(rec);
+        if (bad_state || (evaluated && !std::isfinite(rec.loss))) {
+            st.diverged = 1;
+            break;
+        }
     }
+    st.n_records = static_cast<int>(recs.size());
     st.issued = nmb;
     if (delayed_method && pending_valid_) {
         pending_k_ = slot_k[static_cast<size_t>(T)];
@@ -893,6 +962,7 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     cudaEventDestroy(base);
     cudaFree(tot);
     if (eval_buf) cudaFree(eval_buf);
+    if (!invalid.empty()) throw Error(kInvalidArg, invalid);
 }
 
 }  // namespace acco

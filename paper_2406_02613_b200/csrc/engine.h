@@ -46,6 +46,7 @@ struct RunStats {
     int opt_launches = 0;
     int diverged = 0;
     long long h2d_bytes = 0, d2h_bytes = 0;  // host-data path traffic during the run
+    int n_records = 0;  // committed records (< t_updates when the run diverged)
 };
 
 // One timeline.csv row (simclock.hpp Interval; csvio.cpp:48-66), from CUDA
@@ -125,7 +126,8 @@ private:
     float* pad_send_ = nullptr;
     float *g_ret_ = nullptr, *g_main_ = nullptr, *full_red_ = nullptr;
     int64_t* cnt_send_ = nullptr;
-    int* flag_ = nullptr;
+    int* phase_flags_ = nullptr;  // this run's per-phase optimizer non-finite bits (see optim.cu)
+    int* cur_flag_ = nullptr;     // the phase being launched
     double* loss_ring_ = nullptr;
     double* loss_host_ = nullptr;  // pinned mirror of loss_ring_ (host-data path)
     long long d2h_bytes_ = 0;
@@ -138,6 +140,7 @@ private:
     long long mb_counter_ = 0;
     // DPU / WP: the bundle computed in the last round awaits its optimizer
     // step (SyncEngine::pending_, protocols.cpp:268); it survives run() calls
+    bool theta0_nonfinite_ = false;  // set_theta saw a non-finite theta0 (raised by run())
     bool pending_valid_ = false;
     int pending_slot_ = 0;       // accumulator parity holding it
     int pending_k_ = 0;          // its micro-batches per worker

@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;  // power of two >= 2 accumulators
+    // two accumulator buffers (tile ping-pong); the 3xTF32 variant keeps a main
+    // (hi*hi) and a correction (lo*hi + hi*lo) accumulator per buffer
+    constexpr int kAccCols = X3 ? 2 * BN : BN;
+    constexpr uint32_t kTmemCols = 2 * kAccCols <= 256 ? 256 : 512;  // power of two >= 2 accumulators
     if (warp == 2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(kTmemCols));
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
             tc_fence_after();
             if (lane == 0) GEMM_PROBE(0, lt);
-            const uint32_t tmem_d = tmem_base + acc * BN;
+            const uint32_t tmem_d = tmem_base + acc * kAccCols;
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
@@ -470,16 +473,22 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 const uint64_t bd = B_MN ? sdesc(smem_u32(sB + s * B_BYTES), 64 * kBK * 2, 1024)
                                          : sdesc(smem_u32(sB + s * B_BYTES), 16, 1024);
                 if (X3) {
-                    // 4 slices of K = 8 per 128 B row; per slice lo*hi + hi*lo + hi*hi
+                    // 4 slices of K = 8 per 128 B row; per slice hi*hi into the main
+                    // accumulator and lo*hi + hi*lo into the correction accumulator.
+                    // The tensor core truncates at every accumulate; chaining the
+                    // 2^-11-sized correction terms into the main sum would cost an
+                    // ulp of the main sum each, in their own they cost 2^-11 of it
+                    // (the epilogue adds the two in round-to-nearest fp32).
                     constexpr uint32_t idesc3 = idesc_tf32(kBM, BN);
                     constexpr uint64_t a_lo = A_TILE >> 4, b_lo = B_TILE >> 4;
                     if (elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t ah = ad + kk * 2, bh = bd + kk * 2;
-                            umma_tf32(tmem_d, ah + a_lo, bh, idesc3, (kb > kb0 || kk > 0) ? 1u : 0u);
-                            umma_tf32(tmem_d, ah, bh + b_lo, idesc3, 1u);
-                            umma_tf32(tmem_d, ah, bh, idesc3, 1u);
+                            const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
+                            umma_tf32(tmem_d + BN, ah + a_lo, bh, idesc3, first);
+                            umma_tf32(tmem_d + BN, ah, bh + b_lo, idesc3, 1u);
+                            umma_tf32(tmem_d, ah, bh, idesc3, first);
                         }
                         umma_commit(&empty[s]);
                     }
@@ -556,7 +565,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                     for (int j = 0; j < kSlots && hf + kCS * j < kChunks; ++j) load_in(j);
                 mbar_wait(&tfull[acc], (lt >> 1) & 1);
                 tc_fence_after();
-                const uint32_t tb = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+                const uint32_t tb = tmem_base + acc * kAccCols + (static_cast<uint32_t>(wq * 32) << 16);
 #pragma unroll 1
                 for (int j = 0, c = hf; c < kChunks; ++j, c += kCS) {
                     const int sl = j % kSlots;
@@ -600,7 +609,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             mbar_wait(&tfull[acc], (lt >> 1) & 1);
             tc_fence_after();
             if (lane == 0 && (ew == 0 || ew == kEpiWarps - 1)) GEMM_PROBE(ew == 0 ? 2 : 4, lt);
-            const uint32_t tbase = tmem_base + acc * BN + (static_cast<uint32_t>(wq * 32) << 16);
+            const uint32_t tbase = tmem_base + acc * kAccCols + (static_cast<uint32_t>(wq * 32) << 16);
             if (ep.mode == kEpiSwiGLU) {
                 // accumulator columns [0, BN/2) = gate, [BN/2, BN) = up of the same
                 // BN/2 features (n0/2 ...): store both pre-activations (for the
@@ -657,6 +666,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 }
                 uint32_t raw[32];
                 tmem_ld32(tbase + c * 32, raw);
+                if (X3) {  // main + correction accumulator
+                    uint32_t cr[32];
+                    tmem_ld32(tbase + BN + c * 32, cr);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) raw[i] = __float_as_uint(__uint_as_float(raw[i]) + __uint_as_float(cr[i]));
+                }
                 if (c + kCS >= kChunks) {  // this warp's share of the accumulator read: hand TMEM back
                     tc_fence_before();
                     __syncwarp();

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
     int64_t tot = *a.total;
     if (HAS_RET && a.rtotal) tot += *a.rtotal;
     const float inv = static_cast<float>(1.0 / static_cast<double>(tot));
-    bool bad = false;
+    bool bad = false, bad_out = false;  // non-finite input (opt_step's invalid_argument) / new parameters
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t n4 = VEC ? a.n / 4 : 0;
@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
                     reinterpret_cast<float4*>(a.v)[q] = v;
                 }
             }
+            bad_out |= !(isfinite(nt.x) && isfinite(nt.y) && isfinite(nt.z) && isfinite(nt.w));
             for (int k = 0; k < a.ndst; ++k) store4<OutT>(a.dst[k], q, nt);
         }
     }
@@ -155,13 +156,18 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
         float m = KIND != 0 ? a.m[i] : 0.f, v = KIND != 0 ? a.v[i] : 0.f;
         bad |= !(isfinite(g) && isfinite(th));
         float nt = step_elem<KIND>(a, g, th, m, v);
+        bad_out |= !isfinite(nt);
         if (COMMIT) {
             a.theta[i] = nt;
             if (KIND != 0) { a.m[i] = m; a.v[i] = v; }
         }
         for (int k = 0; k < a.ndst; ++k) store_out<OutT>(a.dst[k], i, nt);
     }
-    if (bad && a.flag) atomicOr(a.flag, 1);
+    // bit 0: a non-finite gradient or parameter entered the step (the
+    // reference's opt_step throws invalid_argument, optim.cpp:56-57); bit 1:
+    // the step produced a non-finite parameter (the next commit's finite-state
+    // check makes the loss +inf: diverged, protocols.cpp:113-119,164-167)
+    if ((bad || bad_out) && a.flag) atomicOr(a.flag, (bad ? 1 : 0) | (bad_out ? 2 : 0));
 }
 
 template <int KIND, bool COMMIT, bool HAS_RET, class OutT>

@@ -114,7 +114,15 @@ def test_nonfinite_flag_and_empty_shard(cuda):
     _lib.call("acco_opt_commit", C.byref(cfg), C.byref(st), _p(g), None, _p(tot), None, None, _lib.DTYPE_F32,
               _p(flag), _stream())
     torch.cuda.synchronize()
-    assert flag.item() == 1
+    # bit 0: non-finite input (opt_step's invalid_argument); bit 1: non-finite new parameter
+    assert flag.item() & 1
+    flag.zero_()
+    g.zero_()
+    st2, th2, m2, v2 = _state(np.ones(n), n, cuda)  # (the commit above wrote non-finite theta into st)
+    _lib.call("acco_opt_commit", C.byref(cfg), C.byref(st2), _p(g), None, _p(tot), None, None, _lib.DTYPE_F32,
+              _p(flag), _stream())
+    torch.cuda.synchronize()
+    assert flag.item() == 0
     # empty trailing shard is a no-op (proj/tests/test_optim.cpp:168-181)
     st0 = _lib.ShardState(0, 0, 0, 0, 5, 5)
     _lib.call("acco_opt_commit", C.byref(cfg), C.byref(st0), None, None, _p(tot), None, None, _lib.DTYPE_F32,

@@ -147,3 +147,51 @@ def test_heterogeneous_steady_state_counts():
     for r in c["records"][3:]:
         assert r["mb_main"] == [4, 4, 4, 1]
         assert r["mb_estimate"] == [4, 4, 4, 1]
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in load("divergence.json")])
+def test_divergence_semantics_match_reference(name):
+    """Diverging runs (divergence.json, written by the reference): the partial
+    trace, the diverged flag and the non-finite last loss of
+    test_protocols.cpp:328-336 for every method; a non-finite theta0 raises
+    the reference's exception type (invalid_argument -> ValueError,
+    logic_error -> ProtocolLogicError)."""
+    c = next(c for c in load("divergence.json") if c["name"] == name)
+    if "throws" in c:
+        exc = ValueError if c["throws"] == "invalid_argument" else O.ProtocolLogicError
+        nan_case = {"ddp": ("ddp", 2), "acco": ("acco", 2)}[c["method"]]
+        with pytest.raises(exc, match=c["what"]):
+            O.check_theta0(nan_case[0], np.array([1.0, np.nan, 0.5]), nan_case[1])
+        return
+    tr = _run_golden_case(c)
+    assert tr.diverged == c["diverged"] is True
+    assert len(tr.records) == len(c["records"]) < c["t_updates"]
+    for r, g in zip(tr.records, c["records"]):
+        if g["loss"] is None:  # json null = the reference's non-finite loss
+            assert not np.isfinite(r.loss)
+        else:
+            assert r.loss == g["loss"]
+    assert not np.isfinite(tr.records[-1].loss)
+    for a, b in zip(tr.theta_history, c["theta_history"]):
+        assert [x if np.isfinite(x) else None for x in a.tolist()] == b
+
+
+def test_nan_loss_under_eval_is_divergence():
+    """An evaluated NaN loss ends the run (protocols.cpp:164-167: !isfinite);
+    NaN only means "not evaluated" when the cadence skipped the update."""
+    p = O.AnalyticProblem(next(c for c in load("divergence.json") if c["name"] == "ddp_identity_sgd1e8")["problem"])
+    cfg = O.OptimizerConfig(kind="sgd", learning_rate=0.1)
+    sim = O.SimConfig(1, 1, 1, False, 1)
+    calls = []
+
+    def eval_fn(theta):
+        calls.append(1)
+        return (float("nan") if len(calls) > 2 else 1.0), np.zeros_like(theta)
+
+    tr = O.run_ddp(lambda th, s: p.stochastic_grad(th, s, 1, False), np.array([1.0]), cfg, sim, 10, eval_fn=eval_fn)
+    assert tr.diverged and len(tr.records) == 2
+    calls.clear()  # cadence 3: updates 2 (finite) and 5 (NaN) are evaluated, the rest carry NaN
+    tr = O.run_ddp(lambda th, s: p.stochastic_grad(th, s, 1, False), np.array([1.0]), cfg, sim, 10, eval_fn=eval_fn,
+                   eval_every=3)
+    assert tr.diverged and len(tr.records) == 6
+    assert np.isnan(tr.records[0].loss) and tr.records[2].loss == 1.0
