@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 30
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert lib.acco_version() == 1
+    assert lib.acco_version() == 2  # ABI 2: acco_run_stats.n_records (partial traces)
 
 
 def test_shard_partition_bitexact():
