@@ -241,6 +241,11 @@ typedef struct acco_sim_cfg {
      * that phase's reduce-scatter + all-gather), so the overlap of ACCO vs the
      * synchronous baselines can be measured on one GPU. 0 = off. */
     double comm_delay_ns;
+    /* Debug (the reference's check_replicas, protocols.cpp:208-212): after every
+     * comm phase the ranks hash their theta / theta-tilde replicas, exchange
+     * the hashes and compare; a mismatch fails the run with ACCO_LOGIC_ERROR.
+     * One extra barrier per phase. 0 = off. */
+    int check_replicas;
 } acco_sim_cfg;
 
 /* RoundRecord (protocols.hpp:41-53); NaN where not evaluated. */

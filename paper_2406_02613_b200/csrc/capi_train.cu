@@ -57,6 +57,7 @@ SimCfg to_sim(const acco_sim_cfg* sim) {
     if (sim->throttle_ns) s.throttle_ns.assign(sim->throttle_ns, sim->throttle_ns + sim->n_workers);
     ACCO_REQUIRE(sim->comm_delay_ns >= 0.0, "sim: comm_delay_ns >= 0");
     s.comm_delay_ns = sim->comm_delay_ns;
+    s.check_replicas = sim->check_replicas;
     return s;
 }
 }  // namespace

@@ -7,7 +7,10 @@
 #include "host_util.h"
 #include "lm_kernels.h"
 
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 namespace acco {
@@ -26,7 +29,43 @@ Comm::Comm(int nranks, int rank, const ncclUniqueId& id, int device) : nranks_(n
 }
 
 Comm::~Comm() {
-    if (comm_) ncclCommDestroy(comm_);
+    if (comm_ && !aborted_) ncclCommDestroy(comm_);
+}
+
+double Comm::timeout_s() {
+    const char* e = std::getenv("ACCO_NCCL_TIMEOUT_S");  // read per wait: tests shorten it
+    const double v = e ? std::atof(e) : 600.0;
+    return v > 0 ? v : 600.0;
+}
+
+void Comm::abort_and_throw(const std::string& why) {
+    if (!aborted_) {
+        ncclCommAbort(comm_);  // NCCL's kernels observe the abort flag and exit
+        aborted_ = true;
+    }
+    throw Error(kCudaError, "nccl rank " + std::to_string(rank_) + "/" + std::to_string(nranks_) + ": " + why);
+}
+
+void Comm::wait(cudaEvent_t ev) {
+    ACCO_REQUIRE(!aborted_, "comm: communicator was aborted after an earlier failure");
+    const auto t0 = std::chrono::steady_clock::now();
+    const double limit = timeout_s();
+    int spins = 0;
+    while (true) {
+        const cudaError_t q = cudaEventQuery(ev);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) ACCO_CUDA(q);
+        ncclResult_t async = ncclSuccess;
+        ACCO_NCCL(ncclCommGetAsyncError(comm_, &async));
+        if (async != ncclSuccess && async != ncclInProgress)
+            abort_and_throw(std::string("asynchronous NCCL error: ") + ncclGetErrorString(async));
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > limit)
+            abort_and_throw("no progress for " + std::to_string(static_cast<int>(limit)) +
+                            " s (a rank died or stopped issuing collectives); communicator aborted");
+        // poll tightly at first (the common case is a short wait), then back off
+        if (++spins > 1000) std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
 }
 
 void Comm::all_reduce_f32(const float* send, float* recv, size_t n, cudaStream_t s) {
@@ -40,6 +79,9 @@ void Comm::reduce_scatter_f32(const float* send, float* recv, size_t n, cudaStre
 }
 void Comm::all_gather(const void* send, void* recv, size_t n, int dtype, cudaStream_t s) {
     ACCO_NCCL(ncclAllGather(send, recv, n, dtype == ACCO_DTYPE_BF16 ? ncclBfloat16 : ncclFloat32, comm_, s));
+}
+void Comm::all_gather_u64(const uint64_t* send, uint64_t* recv, size_t n, cudaStream_t s) {
+    ACCO_NCCL(ncclAllGather(send, recv, n, ncclUint64, comm_, s));
 }
 
 }  // namespace acco

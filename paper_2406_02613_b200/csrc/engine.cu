@@ -21,6 +21,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <numeric>
@@ -114,6 +116,7 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
     }
     ACCO_CUDA(cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking, comp_prio));
     ACCO_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, comm_prio));
+    for (auto& e : sync_ev_) ACCO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     alloc();
     if (peer_) {  // exported to the peers: accumulators, then the two replicas
         rep_[0] = theta_act_;
@@ -134,9 +137,26 @@ Trainer::~Trainer() {
     if (ag_theta_ != theta_act_) cudaFree(ag_theta_);
     if (ag_est_ != est_act_) cudaFree(ag_est_);
     for (float* a : acc_) cudaFree(a);
+    if (hash_buf_) cudaFree(hash_buf_);
     if (loss_host_) cudaFreeHost(loss_host_);
+    for (auto& e : sync_ev_)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(cs_);
     cudaStreamDestroy(ms_);
+}
+
+void Trainer::wait_event(cudaEvent_t e) {
+    if (comm_)
+        comm_->wait(e);
+    else
+        ACCO_CUDA(cudaEventSynchronize(e));
+}
+
+void Trainer::sync_streams() {
+    ACCO_CUDA(cudaEventRecord(sync_ev_[0], ms_));
+    ACCO_CUDA(cudaEventRecord(sync_ev_[1], cs_));
+    wait_event(sync_ev_[0]);
+    wait_event(sync_ev_[1]);
 }
 
 void Trainer::alloc() {
@@ -171,6 +191,7 @@ void Trainer::alloc() {
     if (comm_ || peer_ || n_local_ > 1) ACCO_CUDA(cudaMalloc(&g_ret_, own_cap * 4));  // retained estimate shard
     if (comm_) ACCO_CUDA(cudaMalloc(&g_main_, own_cap * 4));                  // reduce-scatter target
     ACCO_CUDA(cudaMalloc(&cnt_send_, 8));
+    if (sim_.check_replicas) ACCO_CUDA(cudaMalloc(&hash_buf_, (2 + 2 * 64) * sizeof(uint64_t)));
     loss_cap_ = 1 << 16;
     ACCO_CUDA(cudaMalloc(&loss_ring_, loss_cap_ * sizeof(double)));
     if (model_->host_data()) ACCO_CUDA(cudaHostAlloc(&loss_host_, loss_cap_ * sizeof(double), cudaHostAllocDefault));
@@ -207,8 +228,7 @@ void Trainer::set_theta(const float* host) {
 }
 
 void Trainer::get_theta(int which, float* host) {
-    ACCO_CUDA(cudaStreamSynchronize(ms_));
-    ACCO_CUDA(cudaStreamSynchronize(cs_));
+    sync_streams();
     if (which == 2) {
         ACCO_CUDA(cudaMemcpy(host, master_, static_cast<size_t>(own_n_) * 4, cudaMemcpyDeviceToHost));
         return;
@@ -409,7 +429,35 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
         }
     }
     if (peer_) peer_->signal_done(seq, ms_);  // this rank's shard is in every replica
+    if (sim_.check_replicas && (comm_ || peer_)) check_replicas(p, seq);
     ACCO_CUDA(cudaEventRecord(ev.done[p], ms_));
+}
+
+// check_replicas (protocols.cpp:208-212) across the ranks: after the phase's
+// all-gather every rank's theta and theta-tilde replicas must be bitwise equal.
+// Each rank hashes both, the hashes are exchanged (NCCL all-gather of 16 B, or
+// the peer flag blocks) and compared on the device; a mismatch sets bit 2
+// (value 4) of the phase's flag and run() throws logic_error. Debug mode
+// (SimConfig.check_replicas): one extra barrier per phase.
+void Trainer::check_replicas(int p, unsigned long long seq) {
+    int* flag = phase_flags_ + (method_ == kACCO ? p : 2 * p);
+    const size_t bytes = static_cast<size_t>(psi_) * model_->act_bytes();
+    if (peer_) peer_->wait_done(seq, ms_);  // every rank's shard has landed in our replicas
+    // fault injection for the tests: ACCO_DEBUG_CORRUPT=<rank>,<phase> perturbs
+    // one parameter of that rank's replica before the check
+    if (const char* c = std::getenv("ACCO_DEBUG_CORRUPT")) {
+        int cr = -1, cp = -1;
+        if (std::sscanf(c, "%d,%d", &cr, &cp) == 2 && cr == rank_ && cp == p)
+            ACCO_CUDA(cudaMemsetAsync(theta_act_, 0x3f, 2, ms_));
+    }
+    replica_hash(theta_act_, static_cast<int64_t>(bytes), hash_buf_, ms_);
+    replica_hash(est_act_, static_cast<int64_t>(bytes), hash_buf_ + 1, ms_);
+    if (peer_) {
+        peer_->check_hashes(seq, hash_buf_, flag, 4, ms_);
+    } else {
+        comm_->all_gather_u64(hash_buf_, hash_buf_ + 2, 2, ms_);
+        hash_compare(hash_buf_ + 2, world_, 2, flag, 4, ms_);
+    }
 }
 
 void Trainer::run(int T, std::vector<UpdateRecord>& recs, RunStats& st, float* theta_hist) {
@@ -616,7 +664,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
                     // floor met: the decision is taken when micro-batch k-1
                     // completes, as in on_mb_done (protocols.cpp:566-573) — hand
                     // off iff phase p-1 has completed, else accumulate another.
-                    ACCO_CUDA(cudaEventSynchronize(ev.mb[(k - 1) % 4]));
+                    wait_event(ev.mb[(k - 1) % 4]);
                     if (cudaEventQuery(ev.done[p - 1]) == cudaSuccess) break;
                 }
                 const int slot = static_cast<int>(mb_counter_ % loss_cap_);
@@ -643,8 +691,7 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             }
         }
     }
-    ACCO_CUDA(cudaStreamSynchronize(ms_));
-    ACCO_CUDA(cudaStreamSynchronize(cs_));
+    sync_streams();
 
     // ---- gather results
     std::vector<int64_t> tot_h(NP);
@@ -672,6 +719,10 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     // (optim.cpp:56-57: no trace, CLI exit 2); a non-finite state or
     // evaluated loss at the commit ends the run with that record (loss = +inf
     // for a non-finite state, protocols.cpp:113-119,164-167: exit 3).
+    for (int p = 0; p < NP; ++p)
+        if (pf[static_cast<size_t>(p)] & 4)
+            throw Error(kLogicError, "protocol: parameter divergence across workers (comm phase " +
+                                         std::to_string(p) + " of this run)");
     int first_bad_input = -1;
     for (int p = 0; p < NP && first_bad_input < 0; ++p)
         if (pf[static_cast<size_t>(p)] & 1) first_bad_input = p;
@@ -864,8 +915,7 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             ACCO_CUDA(cudaStreamWaitEvent(ms_, eval_done, 0));
         }
     }
-    ACCO_CUDA(cudaStreamSynchronize(ms_));
-    ACCO_CUDA(cudaStreamSynchronize(cs_));
+    sync_streams();
     std::vector<int64_t> tot_h(T);
     ACCO_CUDA(cudaMemcpy(tot_h.data(), tot, T * sizeof(int64_t), cudaMemcpyDeviceToHost));
     const long long nmb = mb_counter_ - mb0;
@@ -886,6 +936,10 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
     }
     std::vector<int> pf(static_cast<size_t>(2 * T));
     ACCO_CUDA(cudaMemcpy(pf.data(), phase_flags_, 2 * T * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int r = 0; r < T; ++r)
+        if (pf[static_cast<size_t>(2 * r)] & 4)
+            throw Error(kLogicError, "protocol: parameter divergence across workers (round " + std::to_string(r) +
+                                         " of this run)");
     const int n = model_->cfg().n_samples;
     std::string invalid;  // thrown after this run's resources are released
     for (int r = 0; r < T; ++r) {

@@ -28,6 +28,7 @@ struct SimCfg {
     std::vector<double> throttle_ns; // per worker, extra ns after every micro-batch
     int eval_batch = 0;              // samples per evaluation chunk (0 = model max)
     double comm_delay_ns = 0;        // emulated interconnect time per comm phase (0 = off)
+    int check_replicas = 0;          // debug: cross-rank replica checksum after every comm phase
 };
 
 struct UpdateRecord {
@@ -101,6 +102,13 @@ private:
     void micro(int w, const void* params, uint64_t round, uint64_t tag, int ordinal, float* acc, double* loss_slot);
     void eval(const void* params, double* loss_slots, double* gsq_slot);
     void* theta_params() const { return theta_act_; }
+    void check_replicas(int p, unsigned long long seq);
+    uint64_t* hash_buf_ = nullptr;  // [2 local][kMaxPeers * 2 gathered]
+    // Blocking waits that cannot hang on a dead rank: in NCCL mode they poll the
+    // communicator's async error state with a timeout (Comm::wait).
+    void wait_event(cudaEvent_t e);
+    void sync_streams();
+    cudaEvent_t sync_ev_[2] = {nullptr, nullptr};
     void* est_params() const { return est_act_; }
 
     GPTModel* model_;

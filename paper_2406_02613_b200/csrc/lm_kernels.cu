@@ -878,6 +878,25 @@ __global__ void unpack_kernel(const E* __restrict__ padded, E* __restrict__ flat
     }
 }
 
+__global__ void replica_hash_kernel(const uint32_t* __restrict__ w, int64_t n, unsigned long long* out) {
+    ACCO_PDL_PROLOGUE();
+    unsigned long long h = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        h += splitmix_finalize(static_cast<uint64_t>(i) * kGolden ^ (static_cast<uint64_t>(__ldg(w + i)) << 17));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, h);  // wrapping u64 sum: order-independent
+}
+
+__global__ void hash_compare_kernel(const unsigned long long* all, int n, int k, int* flag, int bit) {
+    ACCO_PDL_PROLOGUE();
+    bool bad = false;
+    for (int r = 1; r < n; ++r)
+        for (int j = 0; j < k; ++j) bad |= all[r * k + j] != all[j];
+    if (bad) atomicOr(flag, bit);
+}
+
 __global__ void spin_kernel(uint64_t ns) {
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -1288,6 +1307,21 @@ void swiglu_bwd(const T* da, const T* gu, T* dgu, int M, int F, cudaStream_t s) 
         }
     }
     launch_pdl(swiglu_bwd_kernel<T>, grid_for(static_cast<int64_t>(M) * F), 256, 0, s, da, gu, dgu, M, F);
+    ACCO_CHECK_LAUNCH();
+}
+
+void replica_hash(const void* p, int64_t bytes, uint64_t* out, cudaStream_t s) {
+    ACCO_REQUIRE(bytes % 4 == 0, "replica_hash: whole 32-bit words");
+    ACCO_CUDA(cudaMemsetAsync(out, 0, sizeof(uint64_t), s));
+    const int64_t n = bytes / 4;
+    const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * num_sms()));
+    launch_pdl(replica_hash_kernel, std::max(blocks, 1), 256, 0, s, static_cast<const uint32_t*>(p), n,
+               reinterpret_cast<unsigned long long*>(out));
+    ACCO_CHECK_LAUNCH();
+}
+
+void hash_compare(const uint64_t* all, int n, int k, int* flag, int bit, cudaStream_t s) {
+    launch_pdl(hash_compare_kernel, 1, 1, 0, s, reinterpret_cast<const unsigned long long*>(all), n, k, flag, bit);
     ACCO_CHECK_LAUNCH();
 }
 

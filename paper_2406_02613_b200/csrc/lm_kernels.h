@@ -94,6 +94,12 @@ void pack_padded(const float* flat, float* padded, const uint64_t* lo, const uin
                  uint64_t chunk, cudaStream_t s);
 void unpack_padded(const void* padded, void* flat, int elem_bytes, const uint64_t* lo,
                    const uint64_t* sz, int n, uint64_t chunk, cudaStream_t s);
+// Replica consistency (the reference's check_replicas, protocols.cpp:208-212,
+// as a debug cross-rank checksum): out = order-independent 64-bit hash of the
+// buffer (wrapping sum of mixed (word index, word) pairs: deterministic for any
+// launch shape); compare sets `bit` in *flag when all[r*k + j] != all[j].
+void replica_hash(const void* p, int64_t bytes, uint64_t* out, cudaStream_t s);
+void hash_compare(const uint64_t* all, int n, int k, int* flag, int bit, cudaStream_t s);
 // straggler throttle (HeterogeneityProfile, protocols.hpp:19-27): spin ns on the stream
 void spin_ns(uint64_t ns, cudaStream_t s);
 

@@ -53,6 +53,32 @@ __global__ void peer_wait_kernel(PeerFlags* local, int world, unsigned long long
     __threadfence_system();
 }
 
+__global__ void peer_hash_kernel(PeerFlagPtrs fp, PeerFlags* local, int world, int rank, unsigned long long seq,
+                                 const unsigned long long* h2, int* flag, int bit) {
+    const unsigned long long a = h2[0], b = h2[1];
+    for (int r = 0; r < world; ++r) {
+        PeerFlags* f = fp.p[r];
+        f->csum[rank][0] = a;
+        f->csum[rank][1] = b;
+        __threadfence_system();
+        st_release_sys(&f->csum_seq[rank], seq);
+    }
+    bool bad = false;
+    for (int r = 0; r < world; ++r) {
+        uint64_t t0 = 0;
+        while (ld_acquire_sys(&local->csum_seq[r]) < seq) {
+            __nanosleep(200);
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (!t0) t0 = now;
+            else if (now - t0 > 60000000000ull) __trap();
+        }
+        bad |= *(volatile unsigned long long*)&local->csum[r][0] != a ||
+               *(volatile unsigned long long*)&local->csum[r][1] != b;
+    }
+    if (bad) atomicOr(flag, bit);
+}
+
 }  // namespace
 
 PeerFabric::PeerFabric(int world, int rank, int device) : world_(world), rank_(rank), device_(device) {
@@ -137,6 +163,12 @@ void PeerFabric::signal_done(unsigned long long seq, cudaStream_t s) {
 
 void PeerFabric::wait_done(unsigned long long seq, cudaStream_t s) {
     peer_wait_kernel<<<1, 1, 0, s>>>(flags_, world_, seq, 0, 0, nullptr);
+    ACCO_CHECK_LAUNCH();
+}
+
+void PeerFabric::check_hashes(unsigned long long seq, const uint64_t* local_hash2, int* flag, int bit, cudaStream_t s) {
+    peer_hash_kernel<<<1, 1, 0, s>>>(flag_ptrs_, flags_, world_, rank_, seq,
+                                     reinterpret_cast<const unsigned long long*>(local_hash2), flag, bit);
     ACCO_CHECK_LAUNCH();
 }
 

@@ -31,6 +31,8 @@ struct PeerFlags {  // device memory, one block per rank, written by the peers
     unsigned long long post[kMaxPeers];
     unsigned long long done[kMaxPeers];
     long long counts[2][kMaxPeers];  // [phase parity][rank]
+    unsigned long long csum_seq[kMaxPeers];  // replica checksums (debug check_replicas)
+    unsigned long long csum[kMaxPeers][2];
 };
 
 struct PeerFlagPtrs {
@@ -61,6 +63,9 @@ public:
     void wait_posts(unsigned long long seq, int parity, int64_t* total_out, cudaStream_t s);
     void signal_done(unsigned long long seq, cudaStream_t s);
     void wait_done(unsigned long long seq, cudaStream_t s);
+    // Debug replica check: publish this rank's 2 replica hashes for phase seq
+    // into every rank's block, wait for every rank's, compare (flag |= bit).
+    void check_hashes(unsigned long long seq, const uint64_t* local_hash2, int* flag, int bit, cudaStream_t s);
 
 private:
     int world_, rank_, device_;

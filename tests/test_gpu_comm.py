@@ -127,3 +127,39 @@ def test_peer_fabric_rejects_ddp(cuda):
         api.Trainer("ddp", api.Model(api.LMConfig(**MINI, precision="fp32", max_batch=4)),
                     api.OptimizerConfig(kind="sgd", learning_rate=0.1), api.SimConfig(n_workers=1, batch_size=4),
                     peer)
+
+
+def test_engine_nccl_replica_check(cuda, nccl_comm):
+    """Debug replica check on the NCCL path: both replicas hashed after every
+    comm phase, hashes all-gathered over NCCL (8 B each) and compared."""
+    opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4, weight_decay=0.1, adam_beta2=0.95)
+    sim = api.SimConfig(n_workers=1, batch_size=4, master_seed=7, check_replicas=True)
+    tr = api.run_protocol("acco", api.LMConfig(**MINI, precision="bf16", max_batch=4), opt, sim, 3, comm=nccl_comm)
+    assert len(tr.records) == 3 and not tr.diverged
+
+
+def test_nccl_stuck_phase_fails_instead_of_hanging(cuda, nccl_comm, monkeypatch):
+    """Failure detection on the NCCL path (the reference's deadlock detection,
+    protocols.cpp:476-482): a comm phase that makes no progress — here a 3 s
+    spin on the comm stream standing in for a dead peer — trips the
+    ACCO_NCCL_TIMEOUT_S watchdog, which aborts the communicator and raises
+    (code 4) instead of blocking forever. A fresh communicator is used: an
+    aborted one is unusable."""
+    uid = (C.c_ubyte * 128)()
+    _lib.call("acco_comm_unique_id", uid)
+    h = C.c_void_p()
+    _lib.call("acco_comm_init_rank", 1, 0, uid, 0, C.byref(h))
+
+    class _C:
+        handle, rank, world = h, 0, 1
+
+    monkeypatch.setenv("ACCO_NCCL_TIMEOUT_S", "1")
+    opt = api.OptimizerConfig(kind="adamw", learning_rate=6e-4)
+    sim = api.SimConfig(n_workers=1, batch_size=2, master_seed=7, eval_every=0, comm_delay_ns=3e9)
+    import time
+    t0 = time.time()
+    with pytest.raises(_lib.AccoError, match="no progress") as e:
+        api.run_protocol("acco", api.LMConfig(**MINI, precision="bf16", max_batch=2), opt, sim, 1, comm=_C())
+    assert e.value.code == 4 and time.time() - t0 < 30
+    torch.cuda.synchronize()
+    _lib.lib().acco_comm_destroy(h)

@@ -4,7 +4,11 @@ the ACCO / ZeRO-1 comm phases through the fused fold + AdamW + replica-store
 kernel, with the cross-process device-flag counts and barriers — the
 multi-rank path of the N-GPU NVLink deployment, minus NVLink. Every rank's
 parameter history must match the fp64 oracle's 2-worker run (rel <= 1e-5 per
-update) and the two ranks' replicas must agree bitwise."""
+update) and the two ranks' replicas must agree bitwise. The runs enable the
+debug replica check (check_replicas: hashes of both replicas exchanged and
+compared after every comm phase, the reference's check_replicas,
+protocols.cpp:208-212); a corrupted replica must fail every rank with the
+reference's logic_error."""
 import os
 import socket
 import subprocess
@@ -37,8 +41,13 @@ if hetero:  # rank 0 is 4x slower; the adaptive schedule lets the fast rank accu
     sim = api.SimConfig(n_workers=world, batch_size=4, n_grad_accumulation=1, master_seed=7, eval_every=1,
                         schedule="adaptive", worker_multipliers=[4.0] + [1.0] * (world - 1))
 else:
-    sim = api.SimConfig(n_workers=world, batch_size=4, n_grad_accumulation=2, master_seed=7, eval_every=1)
-tr = api.run_protocol(method, api.LMConfig(**MINI, precision="fp32", max_batch=4), opt, sim, 3, comm=peer)
+    sim = api.SimConfig(n_workers=world, batch_size=4, n_grad_accumulation=2, master_seed=7, eval_every=1,
+                        check_replicas=True)
+try:
+    tr = api.run_protocol(method, api.LMConfig(**MINI, precision="fp32", max_batch=4), opt, sim, 3, comm=peer)
+except api.LogicError as e:
+    print("LOGIC_ERROR", e, flush=True)
+    sys.exit(5)
 np.save(os.path.join(out, f"th{rank}.npy"), np.array(tr.theta_history))
 np.save(os.path.join(out, f"est{rank}.npy"), np.array(tr.estimate_history))
 np.save(os.path.join(out, f"samples{rank}.npy"), np.array([r.samples_cum for r in tr.records]))
@@ -133,3 +142,25 @@ def test_peer_fabric_heterogeneous_adaptive_two_ranks(cuda, tmp_path):
     for t in range(T):
         a, b = th[0][t + 1], ref.theta_history[t + 1]
         assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-5, (t, sched)
+
+
+def test_replica_check_catches_a_corrupted_rank(cuda, tmp_path):
+    """ACCO_DEBUG_CORRUPT=1,1: rank 1 perturbs its theta replica after comm
+    phase 1; the replica hashes disagree and BOTH ranks fail with
+    "protocol: parameter divergence across workers" (no hang)."""
+    world = 2
+    port = str(_free_port())
+    env = dict(os.environ, ROOT=ROOT, ACCO_DEBUG_CORRUPT="1,1")
+    procs = [subprocess.Popen([sys.executable, "-c", WORKER, str(r), str(world), port, "acco", str(tmp_path), "64"],
+                              env=env, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(world)]
+    outs = []
+    try:
+        for p in procs:
+            outs.append(p.communicate(timeout=240)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for p, o in zip(procs, outs):
+        assert p.returncode == 5, o[-3000:]
+        assert "parameter divergence across workers" in o
