@@ -142,7 +142,9 @@ def reference_arm(args, cfgd):
     dt = time.perf_counter() - t0
     tokens = args.steps * cfg.seq_len
     v = tokens / dt
-    cores = os.cpu_count()
+    from oracle.cpu_bench import blas_threads
+
+    cores = blas_threads()
     line = {"impl": "reference", "metric": "tokens/s", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -184,6 +186,11 @@ def main():
         return reference_arm(args, cfgd)
 
     world, rank, local = dist_setup(args.gpus)
+    if world > 1:
+        # NCCL's INIT lines (nranks, transports, NVLS) on stderr, keeping stdout to the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import torch
 
     torch.cuda.set_device(local)
@@ -267,10 +274,18 @@ def main():
             prof = api.prof_read()
             prof["wall_ms"] = pstats["wall_ms"]
             api.prof_enable(False)
+        # collectives of the timed pass from its CUDA-event timeline (this rank)
+        tl = [iv for iv in tr.timeline() if iv.stream == "comm"]
         del tr
+        coll = {}
+        for kind in ("reduce_scatter", "all_gather", "optimizer", "all_reduce"):
+            ivs = [iv for iv in tl if iv.kind == kind]
+            if ivs:
+                coll[kind] = {"ms_per_phase": max_over_ranks(sum(iv.t_end - iv.t_start for iv in ivs) / len(ivs) * 1e3),
+                              "phases": len(ivs), "bytes_per_phase": ivs[0].bytes}
         return {"tokens_per_s": tokens / (ms / 1e3), "ms": ms, "ms_per_step": ms / args.steps, "tokens": tokens,
                 "stats": stats, "prof": prof, "launches": launches, "clocks": ck.summary() if ck else None,
-                "mb": [(r.mb_estimate, r.mb_main) for r in recs[:4]]}
+                "mb": [(r.mb_estimate, r.mb_main) for r in recs[:4]], "coll": coll}
 
     acco = timed("acco", 1, args.schedule, profile=True, clocks=True)
     base = {}
@@ -360,6 +375,23 @@ def main():
                "sample": r["sample"]}
 
     st = acco["stats"]
+
+    def bus(c, n):  # NCCL bus bandwidth of a collective moving `bytes` per rank: bytes x (N-1)/N / t
+        if n <= 1 or not c or c["ms_per_phase"] <= 0:
+            return None
+        return c["bytes_per_phase"] * (n - 1) / n / (c["ms_per_phase"] / 1e3) / 1e9
+    collectives = {
+        "n_ranks": world, "fabric": args.fabric,
+        "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if world > 1 and args.fabric == "nccl" else None,
+        "per_phase_ms": {k: v["ms_per_phase"] for k, v in acco["coll"].items()},
+        "reduce_scatter_busbw_GBps": bus(acco["coll"].get("reduce_scatter"), world),
+        "all_gather_busbw_GBps": bus(acco["coll"].get("all_gather"), world),
+        "link_GBps": 900.0,
+        "cost_model_ms_per_phase": {  # reference collective_time (collectives.cpp:16-25) at NVLink 5, alpha = 0
+            k: (acco["coll"][k]["bytes_per_phase"] * (world - 1) / world / 900e9 * 1e3 if world > 1 else 0.0)
+            for k in ("reduce_scatter", "all_gather") if k in acco["coll"]},
+        "note": "from the timed ACCO pass's CUDA-event timeline on the comm stream (in-situ, overlapping compute); "
+                "max over ranks"}
     line = {
         "metric": "tokens/s", "value": acco["tokens_per_s"], "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": acco["ms_per_step"], "higher_is_better": True,
@@ -386,6 +418,8 @@ def main():
                           "exposed_comm_pct": 100.0 * v["stats"]["comm_exposed_ms"] / v["stats"]["comm_busy_ms"]
                           if v["stats"]["comm_busy_ms"] else 0.0} for k, v in base.items()},
         "acco_vs_zero1_speedup": acco["tokens_per_s"] / base["zero1"]["tokens_per_s"] if "zero1" in base else None,
+        "acco_vs_ddp_speedup": acco["tokens_per_s"] / base["ddp"]["tokens_per_s"] if "ddp" in base else None,
+        "collectives": collectives,
         "roofline": roof, "roofline_optimizer": roof_opt, "attention": attn, "breakdown": breakdown,
         "cpu_baseline": cpu, "e2e": e2e, "clocks": acco["clocks"], "gpu_launches": acco["launches"],
         "stage_counts_first_updates": acco["mb"],
