@@ -301,6 +301,27 @@ int acco_trainer_run(acco_trainer* t, int t_updates, acco_record* recs, int32_t*
                      float* theta_history, acco_run_stats* stats);
 int acco_trainer_n_local(const acco_trainer* t);
 
+/* ------------------------------------------------------- config-level run
+ * The reference's CLI `run` path as one call: load_config / parse_config
+ * (proj/src/config.cpp:80-145; `config` is a JSON file path, or the JSON text
+ * itself when it starts with '{') -> run_protocol (protocols.hpp:89-90) on this
+ * device (n_workers virtual workers) -> write_run_outputs (csvio.cpp:79-102:
+ * metrics.csv, timeline.csv, manifest.json; the manifest and config hash are
+ * the reference's byte for byte). out_dir NULL/"" -> the config's output_dir,
+ * else $ACCOSIM_OUT/run_<config_hash> (accosim_main.cpp:35-40,57-58).
+ * Returns the CLI exit code (accosim_main.cpp:30-33): ACCO_OK, ACCO_DIVERGED
+ * (outputs written), ACCO_INVALID (bad config), plus ACCO_CUDA_ERROR /
+ * ACCO_LOGIC_ERROR. problem.kind: "gpt" or "llama" (B200 LM problems). */
+typedef struct acco_run_summary {
+    int updates;       /* records written to metrics.csv */
+    int diverged;
+    double final_loss; /* the last record's loss (NaN when not evaluated) */
+    long long samples; /* samples_cum of the last record */
+    double wall_ms;    /* device time of the run */
+    char out_dir[1024];
+} acco_run_summary;
+int acco_run(const char* config, const char* out_dir, acco_run_summary* summary);
+
 /* ------------------------------------------------------------- peer fabric
  * B200-native alternative to NCCL for the comm phase: ONE fused kernel per
  * phase reads every rank's accumulator shard over NVLink peer memory (CUDA

@@ -615,6 +615,29 @@ def config_hash(j: dict) -> str:
     return f"{h:016x}"
 
 
+# ------------------------------------------------------- config-level entry
+class RunSummaryC(C.Structure):
+    _fields_ = [("updates", C.c_int), ("diverged", C.c_int), ("final_loss", C.c_double),
+                ("samples", C.c_longlong), ("wall_ms", C.c_double), ("out_dir", C.c_char * 1024)]
+
+
+_lib.register({"acco_run": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(RunSummaryC)])})
+
+
+def run_config(config: str, out_dir: str = "") -> tuple:
+    """acco_run (include/acco.h): the reference CLI's `run` as one library call
+    (load_config -> run_protocol -> write_run_outputs, proj/src/config.cpp:135-145,
+    csvio.cpp:79-102). `config`: a JSON file path or JSON text. Returns
+    (exit code, summary dict); 0 ok, 3 diverged (outputs written); invalid
+    configs raise InvalidArgument (exit 2)."""
+    s = RunSummaryC()
+    rc = _lib.lib().acco_run(config.encode(), out_dir.encode(), C.byref(s))
+    if rc not in (_lib.OK, _lib.DIVERGED):
+        _lib.check(rc)
+    return rc, {"updates": s.updates, "diverged": bool(s.diverged), "final_loss": s.final_loss,
+                "samples": s.samples, "wall_ms": s.wall_ms, "out_dir": s.out_dir.decode()}
+
+
 # ---------------------------------------------------------------- memory model
 MEMORY_METHODS = ("ddp", "zero1", "zero2", "zero3", "slowmo", "diloco", "co2", "dpu", "wp", "acco")
 

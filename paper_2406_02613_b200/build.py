@@ -1,6 +1,7 @@
 """In-tree build of the CUDA library ``_acco_b200.so`` (sm_100a only).
 
-Compiles every ``csrc/*.cu`` (device kernels and host C++ alike) with nvcc
+Compiles every ``csrc/*.cu`` (device kernels and host C++ alike) and
+``csrc/*.cpp`` (host-only C++) with nvcc
 (``-gencode arch=compute_100a,code=sm_100a -lineinfo``) and links one shared
 library next to this file, so it travels to the GPU box with the repo snapshot.
 NCCL comes from the system (``/usr/include/nccl.h``, soname ``libnccl.so.2``);
@@ -23,6 +24,10 @@ LIB = os.path.join(HERE, "_acco_b200.so")
 REPO = os.path.dirname(HERE)
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# nlohmann/json (the JSON library the reference parses and dumps with), for
+# the config-level entry csrc/run_api.cpp; a header-only library in the image
+JSON_INC = os.environ.get(
+    "ACCO_JSON_INC", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [
     "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
@@ -44,6 +49,8 @@ def _compile(src: str, verbose: bool) -> str:
         if t >= os.path.getmtime(src) and t >= _newest_header():
             return obj
     cmd = [NVCC, *ARCH, *COMMON, "-c", src, "-o", obj]
+    if src.endswith(".cpp"):  # host-only translation unit
+        cmd[1:1] = ["-x", "c++", f"-I{JSON_INC}", "-Xcompiler", "-std=c++17"]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,7 +63,7 @@ def _compile(src: str, verbose: bool) -> str:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     newest = max(os.path.getmtime(o) for o in objs)

@@ -62,6 +62,49 @@ SimCfg to_sim(const acco_sim_cfg* sim) {
 }
 }  // namespace
 
+namespace acco {
+// Device time of one micro-batch (fwd + bwd + accumulate), mean of `reps` (ns).
+double time_micro_batch(GPTModel& g, int batch, int reps) {
+    const int64_t n = g.num_params();
+    const size_t eb = g.act_bytes();
+    std::vector<float> th(static_cast<size_t>(n));
+    lm_default_theta0(g.cfg(), 1, th.data());
+    void* params = nullptr;
+    float* grad = nullptr;
+    double* slot = nullptr;
+    ACCO_CUDA(cudaMalloc(&params, n * eb));
+    ACCO_CUDA(cudaMalloc(&grad, n * sizeof(float)));
+    ACCO_CUDA(cudaMalloc(&slot, sizeof(double)));
+    cudaStream_t s = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ACCO_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ACCO_CUDA(cudaEventCreate(&e0));
+    ACCO_CUDA(cudaEventCreate(&e1));
+    {
+        float* tmp = nullptr;
+        ACCO_CUDA(cudaMalloc(&tmp, n * sizeof(float)));
+        ACCO_CUDA(cudaMemcpy(tmp, th.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+        f32_to(tmp, params, g.act_dtype(), n, s);
+        ACCO_CUDA(cudaStreamSynchronize(s));
+        cudaFree(tmp);
+    }
+    g.micro_batch(params, 1, 0, 0, batch, grad, slot, s, false);  // warm-up
+    ACCO_CUDA(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) g.micro_batch(params, 2 + r, 0, 0, batch, grad, slot, s, r > 0);
+    ACCO_CUDA(cudaEventRecord(e1, s));
+    ACCO_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    ACCO_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(s);
+    cudaFree(params);
+    cudaFree(grad);
+    cudaFree(slot);
+    return 1e6 * ms / reps;
+}
+}  // namespace acco
+
 extern "C" {
 
 int acco_model_create(const acco_lm_cfg* cfg, acco_model** out) {
@@ -125,44 +168,7 @@ int acco_model_value_and_grad(acco_model* m, const void* params, double* loss_ou
 int acco_model_time_micro_batch(acco_model* m, int batch, int reps, double* ns_out) {
     return guarded([&] {
         ACCO_REQUIRE(m && ns_out && reps >= 1, "acco_model_time_micro_batch: bad argument");
-        GPTModel& g = *m->impl;
-        const int64_t n = g.num_params();
-        const size_t eb = g.act_bytes();
-        std::vector<float> th(static_cast<size_t>(n));
-        lm_default_theta0(g.cfg(), 1, th.data());
-        void* params = nullptr;
-        float* grad = nullptr;
-        double* slot = nullptr;
-        ACCO_CUDA(cudaMalloc(&params, n * eb));
-        ACCO_CUDA(cudaMalloc(&grad, n * sizeof(float)));
-        ACCO_CUDA(cudaMalloc(&slot, sizeof(double)));
-        cudaStream_t s = nullptr;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        ACCO_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        ACCO_CUDA(cudaEventCreate(&e0));
-        ACCO_CUDA(cudaEventCreate(&e1));
-        {
-            float* tmp = nullptr;
-            ACCO_CUDA(cudaMalloc(&tmp, n * sizeof(float)));
-            ACCO_CUDA(cudaMemcpy(tmp, th.data(), n * sizeof(float), cudaMemcpyHostToDevice));
-            f32_to(tmp, params, g.act_dtype(), n, s);
-            ACCO_CUDA(cudaStreamSynchronize(s));
-            cudaFree(tmp);
-        }
-        g.micro_batch(params, 1, 0, 0, batch, grad, slot, s, false);  // warm-up
-        ACCO_CUDA(cudaEventRecord(e0, s));
-        for (int r = 0; r < reps; ++r) g.micro_batch(params, 2 + r, 0, 0, batch, grad, slot, s, r > 0);
-        ACCO_CUDA(cudaEventRecord(e1, s));
-        ACCO_CUDA(cudaEventSynchronize(e1));
-        float ms = 0.f;
-        ACCO_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-        *ns_out = 1e6 * ms / reps;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaStreamDestroy(s);
-        cudaFree(params);
-        cudaFree(grad);
-        cudaFree(slot);
+        *ns_out = time_micro_batch(*m->impl, batch, reps);
     });
 }
 

@@ -119,4 +119,8 @@ private:
     const int32_t* stage_tokens(uint64_t seed, int B, cudaStream_t s);
 };
 
+// Device time of one micro-batch of `batch` samples (fwd + bwd + accumulate),
+// mean of `reps`, ns (the HeterogeneityProfile throttle base, protocols.hpp:19-27).
+double time_micro_batch(GPTModel& g, int batch, int reps);
+
 }  // namespace acco
