@@ -246,6 +246,11 @@ typedef struct acco_sim_cfg {
      * the hashes and compare; a mismatch fails the run with ACCO_LOGIC_ERROR.
      * One extra barrier per phase. 0 = off. */
     int check_replicas;
+    /* Straggler emulation mode for throttle_ns: 0 = a spin kernel on the
+     * worker's compute stream after each micro-batch (device time); 1 = the
+     * paper's method (time.sleep): the host waits for the
+     * micro-batch to complete, then sleeps, leaving the GPU idle. */
+    int throttle_host;
 } acco_sim_cfg;
 
 /* RoundRecord (protocols.hpp:41-53); NaN where not evaluated. */

@@ -43,7 +43,7 @@ class SimCfgC(C.Structure):
                 ("warmup_rounds", C.c_int), ("master_seed", C.c_uint64), ("schedule", C.c_int),
                 ("replay", C.POINTER(C.c_int32)), ("replay_len", C.c_int), ("eval_every", C.c_int),
                 ("eval_batch", C.c_int), ("throttle_ns", C.POINTER(C.c_double)), ("comm_delay_ns", C.c_double),
-                ("check_replicas", C.c_int)]
+                ("check_replicas", C.c_int), ("throttle_host", C.c_int)]
 
 
 class RecordC(C.Structure):
@@ -325,6 +325,7 @@ class SimConfig:
     throttle_ns: Optional[Sequence[float]] = None
     comm_delay_ns: float = 0.0  # emulated interconnect time per comm phase (single-GPU overlap study)
     check_replicas: bool = False  # debug: cross-rank replica checksum after every comm phase
+    throttle_host: bool = False   # straggler by host sleep after each micro-batch (the paper's time.sleep)
 
 
 @dataclass
@@ -391,7 +392,7 @@ class Trainer:
         self.throttle_ns = thr
         s = SimCfgC(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, sim.warmup_rounds, sim.master_seed,
                     SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr,
-                    float(sim.comm_delay_ns), int(sim.check_replicas))
+                    float(sim.comm_delay_ns), int(sim.check_replicas), int(sim.throttle_host))
         o = opt.to_c()
         self._h = C.c_void_p()
         if isinstance(comm, PeerComm):
@@ -580,7 +581,8 @@ def parse_config(j: dict) -> ExperimentConfig:
                     n_grad_accumulation=_get(j, "n_grad_accumulation", 1), warmup_rounds=_get(j, "warmup_rounds", 0),
                     full_batch_gradients=_get(j, "full_batch_gradients", False), master_seed=_get(j, "master_seed", 1),
                     schedule=_get(j, "schedule", "floor"), eval_every=_get(j, "eval_every", 1),
-                    check_replicas=bool(_get(j, "check_replicas", False)))
+                    check_replicas=bool(_get(j, "check_replicas", False)),
+                    throttle_host=bool(_get(j, "throttle_host", False)))
     if "heterogeneity" in j:
         sim.worker_multipliers = _get(j["heterogeneity"], "worker_multipliers", None)
     t = _req(j, "t_updates")

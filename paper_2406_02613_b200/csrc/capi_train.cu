@@ -58,6 +58,7 @@ SimCfg to_sim(const acco_sim_cfg* sim) {
     ACCO_REQUIRE(sim->comm_delay_ns >= 0.0, "sim: comm_delay_ns >= 0");
     s.comm_delay_ns = sim->comm_delay_ns;
     s.check_replicas = sim->check_replicas;
+    s.throttle_host = sim->throttle_host;
     return s;
 }
 }  // namespace

@@ -20,7 +20,9 @@
 #include "lm_kernels.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -274,7 +276,18 @@ void Trainer::micro(int w, const void* params, uint64_t round, uint64_t tag, int
         ACCO_CUDA(cudaMemcpyAsync(loss_host_ + slot, loss_slot, sizeof(double), cudaMemcpyDeviceToHost, cs_));
         d2h_bytes_ += sizeof(double);
     }
-    if (!sim_.throttle_ns.empty()) spin_ns(static_cast<uint64_t>(sim_.throttle_ns[static_cast<size_t>(gw)]), cs_);
+    if (!sim_.throttle_ns.empty()) {
+        const double ns = sim_.throttle_ns[static_cast<size_t>(gw)];
+        if (sim_.throttle_host) {  // the paper's time.sleep: GPU idle while the worker sleeps
+            if (ns > 0) {
+                ACCO_CUDA(cudaEventRecord(sync_ev_[2], cs_));
+                wait_event(sync_ev_[2]);
+                std::this_thread::sleep_for(std::chrono::nanoseconds(static_cast<long long>(ns)));
+            }
+        } else {
+            spin_ns(static_cast<uint64_t>(ns), cs_);
+        }
+    }
 }
 
 void Trainer::eval(const void* params, double* loss_slots, double* gsq_slot) {

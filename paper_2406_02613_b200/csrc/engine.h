@@ -29,6 +29,7 @@ struct SimCfg {
     int eval_batch = 0;              // samples per evaluation chunk (0 = model max)
     double comm_delay_ns = 0;        // emulated interconnect time per comm phase (0 = off)
     int check_replicas = 0;          // debug: cross-rank replica checksum after every comm phase
+    int throttle_host = 0;           // 1: throttle by a host sleep after the micro-batch completes
 };
 
 struct UpdateRecord {
@@ -108,7 +109,7 @@ private:
     // communicator's async error state with a timeout (Comm::wait).
     void wait_event(cudaEvent_t e);
     void sync_streams();
-    cudaEvent_t sync_ev_[2] = {nullptr, nullptr};
+    cudaEvent_t sync_ev_[3] = {nullptr, nullptr, nullptr};  // [2]: host-throttle micro-batch completion
     void* est_params() const { return est_act_; }
 
     GPTModel* model_;

@@ -124,6 +124,7 @@ RunConfig parse(const json& j) {
     else throw std::invalid_argument("config: schedule must be floor or adaptive");
     c.sim.eval_every = get_or<int>(j, "eval_every", 1);
     c.sim.check_replicas = get_or<bool>(j, "check_replicas", false) ? 1 : 0;
+    c.sim.throttle_host = get_or<bool>(j, "throttle_host", false) ? 1 : 0;
     if (j.contains("heterogeneity"))
         c.multipliers = get_or<std::vector<double>>(j.at("heterogeneity"), "worker_multipliers", {});
     c.t_updates = require<int>(j, "t_updates");

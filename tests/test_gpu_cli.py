@@ -68,11 +68,12 @@ def test_sweep_aggregates_in_seed_order(cuda, tmp_path):
     assert m["seeds"] == [1, 2, 3] and m["outputs"] == ["sweep.csv"]
 
 
-@pytest.mark.parametrize("suite", ["shard-equivalence", "collectives", "acco-gd-equivalence"])
+@pytest.mark.parametrize("suite", ["shard-equivalence", "collectives", "acco-gd-equivalence", "heterogeneous"])
 def test_gpu_verify_suites_pass(cuda, tmp_path, suite):
     out = tmp_path / "rep.json"
     assert main(["verify", "--suite", suite, "--out", str(out)]) == 0
     rep = json.loads(out.read_text())
+    print(json.dumps(rep))
     assert rep["pass"] and rep["suite"] == suite
 
 
