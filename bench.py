@@ -173,9 +173,12 @@ def main():
                     help="C4 heterogeneous scenario: rank 0's micro-batches take this many times longer "
                          "(HeterogeneityProfile multiplier, emulated by a measured spin after each micro-batch)")
     ap.add_argument("--emulate-comm-gpus", type=int, default=0,
-                    help="single-GPU study of the overlap: every comm phase spins for the NVLink time "
-                         "(measured 770 GB/s per direction) of an N-GPU reduce-scatter + all-gather "
-                         "(all-reduce for DDP); 0 = off")
+                    help="single-GPU study of the overlap: every comm phase holds the comm stream for the NVLink "
+                         "time (770 GB/s per direction) of an N-GPU reduce-scatter + all-gather (all-reduce for "
+                         "DDP); 0 = off")
+    ap.add_argument("--emulate-ctas", type=int, default=16,
+                    help="with --emulate-comm-gpus: the stand-in collective is a paced HBM copy of the phase's bytes "
+                         "on this many CTAs (NCCL's channel count), holding SMs like NCCL; 0 = a one-thread spin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--profile", action="store_true", help="ncu-friendly: short run, no baselines")
@@ -219,15 +222,21 @@ def main():
     hbm, tf_sus, tf_burst, peak_kind = peaks()
     mult = [args.straggler] + [1.0] * (world - 1) if args.straggler != 1.0 else None
 
-    def comm_delay_ns(method):
+    def comm_bytes(method):
         n = args.emulate_comm_gpus
         if n <= 1:
             return 0.0
-        psi = model.dim
         frac = (n - 1) / n
         # bytes each GPU sends per comm phase: RS fp32 + AG bf16 (ACCO, ZeRO-1), ring AR fp32 (DDP)
-        nbytes = frac * psi * 8.0 if method == "ddp" else frac * psi * (4.0 + 2.0)
-        return nbytes / 770e9 * 1e9
+        return frac * model.dim * 8.0 if method == "ddp" else frac * model.dim * (4.0 + 2.0)
+
+    def comm_delay_ns(method):
+        return comm_bytes(method) / 770e9 * 1e9
+
+    def standin(method):
+        if args.emulate_comm_gpus <= 1 or args.emulate_ctas <= 0:
+            return {}
+        return {"comm_standin_ctas": args.emulate_ctas, "comm_standin_bytes": comm_bytes(method)}
 
     def barrier():
         torch.cuda.synchronize()
@@ -245,7 +254,7 @@ def main():
     def timed(method, k, schedule, profile=False, clocks=False):
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=k, master_seed=1,
                             schedule=schedule, eval_every=0, worker_multipliers=mult,
-                            comm_delay_ns=comm_delay_ns(method))
+                            comm_delay_ns=comm_delay_ns(method), **standin(method))
         tr = api.Trainer(method, model, opt, sim, make_comm(method))
         tr.set_theta(model.default_theta0(1))
         tr.run(args.warmup)
@@ -300,7 +309,7 @@ def main():
         model_h = api.Model(lm_h)
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=1, master_seed=1,
                             schedule=args.schedule, eval_every=0, worker_multipliers=mult,
-                            comm_delay_ns=comm_delay_ns("acco"))
+                            comm_delay_ns=comm_delay_ns("acco"), **standin("acco"))
         tr = api.Trainer("acco", model_h, opt, sim, make_comm("acco"))
         tr.set_theta(model_h.default_theta0(1))
         tr.run(args.warmup)
@@ -409,7 +418,9 @@ def main():
                    **({"emulated_interconnect": {
                        "gpus": args.emulate_comm_gpus, "link_GBps": 770,
                        "phase_ms": {m: comm_delay_ns(m) / 1e6 for m in ("acco", "zero1", "ddp")},
-                       "note": "single GPU; each comm phase spins for the NVLink time of the N-GPU collectives"}}
+                       "standin_ctas": args.emulate_ctas,
+                       "note": "single GPU; each comm phase holds the comm stream for the NVLink time of the N-GPU "
+                               "collectives, as a paced HBM copy of their bytes on standin_ctas CTAs (0: a spin)"}}
                       if args.emulate_comm_gpus > 1 else {})},
         "exposed_comm_pct": 100.0 * st["comm_exposed_ms"] / st["comm_busy_ms"] if st["comm_busy_ms"] else 0.0,
         "comm_busy_ms_per_step": st["comm_busy_ms"] / args.steps,

@@ -251,6 +251,11 @@ typedef struct acco_sim_cfg {
      * paper's method (time.sleep): the host waits for the
      * micro-batch to complete, then sleeps, leaving the GPU idle. */
     int throttle_host;
+    /* With comm_delay_ns > 0: 0 = the phase's emulated interconnect time is a
+     * one-thread spin; > 0 = a paced HBM copy of comm_standin_bytes on this
+     * many CTAs (NCCL's channel count), holding SMs like the real collectives. */
+    int comm_standin_ctas;
+    double comm_standin_bytes;
 } acco_sim_cfg;
 
 /* RoundRecord (protocols.hpp:41-53); NaN where not evaluated. */

@@ -43,7 +43,8 @@ class SimCfgC(C.Structure):
                 ("warmup_rounds", C.c_int), ("master_seed", C.c_uint64), ("schedule", C.c_int),
                 ("replay", C.POINTER(C.c_int32)), ("replay_len", C.c_int), ("eval_every", C.c_int),
                 ("eval_batch", C.c_int), ("throttle_ns", C.POINTER(C.c_double)), ("comm_delay_ns", C.c_double),
-                ("check_replicas", C.c_int), ("throttle_host", C.c_int)]
+                ("check_replicas", C.c_int), ("throttle_host", C.c_int), ("comm_standin_ctas", C.c_int),
+                ("comm_standin_bytes", C.c_double)]
 
 
 class RecordC(C.Structure):
@@ -326,6 +327,8 @@ class SimConfig:
     comm_delay_ns: float = 0.0  # emulated interconnect time per comm phase (single-GPU overlap study)
     check_replicas: bool = False  # debug: cross-rank replica checksum after every comm phase
     throttle_host: bool = False   # straggler by host sleep after each micro-batch (the paper's time.sleep)
+    comm_standin_ctas: int = 0    # emulated interconnect: paced HBM copy on this many CTAs (0 = 1-thread spin)
+    comm_standin_bytes: float = 0.0
 
 
 @dataclass
@@ -392,7 +395,8 @@ class Trainer:
         self.throttle_ns = thr
         s = SimCfgC(sim.n_workers, sim.batch_size, sim.n_grad_accumulation, sim.warmup_rounds, sim.master_seed,
                     SCHEDULES[sim.schedule], rp, rl, sim.eval_every, sim.eval_batch, self._thr,
-                    float(sim.comm_delay_ns), int(sim.check_replicas), int(sim.throttle_host))
+                    float(sim.comm_delay_ns), int(sim.check_replicas), int(sim.throttle_host),
+                    int(sim.comm_standin_ctas), float(sim.comm_standin_bytes))
         o = opt.to_c()
         self._h = C.c_void_p()
         if isinstance(comm, PeerComm):

@@ -59,6 +59,9 @@ SimCfg to_sim(const acco_sim_cfg* sim) {
     s.comm_delay_ns = sim->comm_delay_ns;
     s.check_replicas = sim->check_replicas;
     s.throttle_host = sim->throttle_host;
+    ACCO_REQUIRE(sim->comm_standin_ctas >= 0 && sim->comm_standin_bytes >= 0, "sim: comm stand-in sizes >= 0");
+    s.comm_standin_ctas = sim->comm_standin_ctas;
+    s.comm_standin_bytes = sim->comm_standin_bytes;
     return s;
 }
 }  // namespace

@@ -140,6 +140,7 @@ Trainer::~Trainer() {
     if (ag_est_ != est_act_) cudaFree(ag_est_);
     for (float* a : acc_) cudaFree(a);
     if (hash_buf_) cudaFree(hash_buf_);
+    if (standin_buf_) cudaFree(standin_buf_);
     if (loss_host_) cudaFreeHost(loss_host_);
     for (auto& e : sync_ev_)
         if (e) cudaEventDestroy(e);
@@ -194,6 +195,8 @@ void Trainer::alloc() {
     if (comm_) ACCO_CUDA(cudaMalloc(&g_main_, own_cap * 4));                  // reduce-scatter target
     ACCO_CUDA(cudaMalloc(&cnt_send_, 8));
     if (sim_.check_replicas) ACCO_CUDA(cudaMalloc(&hash_buf_, (2 + 2 * 64) * sizeof(uint64_t)));
+    if (sim_.comm_standin_ctas > 0 && sim_.comm_standin_bytes > 0)
+        ACCO_CUDA(cudaMalloc(&standin_buf_, 2 * (static_cast<size_t>(sim_.comm_standin_bytes) / 16 + 1) * 16));
     loss_cap_ = 1 << 16;
     ACCO_CUDA(cudaMalloc(&loss_ring_, loss_cap_ * sizeof(double)));
     if (model_->host_data()) ACCO_CUDA(cudaHostAlloc(&loss_host_, loss_cap_ * sizeof(double), cudaHostAllocDefault));
@@ -405,7 +408,7 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
         fill_i64(totp, local, ms_);
     }
     ACCO_CUDA(cudaEventRecord(ev.cnt_done[p], ms_));
-    if (sim_.comm_delay_ns > 0) spin_ns(static_cast<uint64_t>(sim_.comm_delay_ns), ms_);  // emulated interconnect
+    emulate_comm(2.0 / 3.0);  // emulated interconnect: the reduce-scatter share
     if (method_ == kACCO) {
         const bool est = p % 2 == 0;
         FoldIO io = fold_sources(acc_q, est ? g_ret_ : g_main_);
@@ -441,9 +444,27 @@ void Trainer::launch_phase(int p, int acc_q, int64_t* tot, PhaseEvents& ev, bool
             }
         }
     }
+    emulate_comm(1.0 / 3.0);  // emulated interconnect: the all-gather share
     if (peer_) peer_->signal_done(seq, ms_);  // this rank's shard is in every replica
     if (sim_.check_replicas && (comm_ || peer_)) check_replicas(p, seq);
     ACCO_CUDA(cudaEventRecord(ev.done[p], ms_));
+}
+
+// Single-GPU study of the overlap (bench.py --emulate-comm-gpus): the phase's
+// NVLink time comm_delay_ns, split 2:1 between the reduce-scatter (fp32) and
+// the all-gather (bf16) byte volumes; a one-thread spin, or with
+// comm_standin_ctas > 0 a paced copy that holds that many SMs and moves the
+// bytes through HBM like NCCL's kernels.
+void Trainer::emulate_comm(double frac) {
+    if (!(sim_.comm_delay_ns > 0)) return;
+    const uint64_t ns = static_cast<uint64_t>(sim_.comm_delay_ns * frac);
+    if (sim_.comm_standin_ctas > 0 && standin_buf_) {
+        const int64_t bytes = static_cast<int64_t>(sim_.comm_standin_bytes * frac) / 16 * 16;
+        const size_t half = (static_cast<size_t>(sim_.comm_standin_bytes) / 16 + 1) * 16;
+        comm_standin(standin_buf_, static_cast<char*>(standin_buf_) + half, bytes, sim_.comm_standin_ctas, ns, ms_);
+    } else {
+        spin_ns(ns, ms_);
+    }
 }
 
 // check_replicas (protocols.cpp:208-212) across the ranks: after the phase's

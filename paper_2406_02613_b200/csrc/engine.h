@@ -30,6 +30,12 @@ struct SimCfg {
     double comm_delay_ns = 0;        // emulated interconnect time per comm phase (0 = off)
     int check_replicas = 0;          // debug: cross-rank replica checksum after every comm phase
     int throttle_host = 0;           // 1: throttle by a host sleep after the micro-batch completes
+    // emulated interconnect: with comm_standin_ctas > 0 the comm_delay_ns of
+    // a phase is spent by a paced HBM copy of comm_standin_bytes on that many
+    // CTAs (2/3 before the optimizer: reduce-scatter, 1/3 after: all-gather)
+    // instead of a one-thread spin
+    int comm_standin_ctas = 0;
+    double comm_standin_bytes = 0;
 };
 
 struct UpdateRecord {
@@ -105,6 +111,8 @@ private:
     void* theta_params() const { return theta_act_; }
     void check_replicas(int p, unsigned long long seq);
     uint64_t* hash_buf_ = nullptr;  // [2 local][kMaxPeers * 2 gathered]
+    void* standin_buf_ = nullptr;   // comm stand-in source / destination (2 x bytes)
+    void emulate_comm(double frac);
     // Blocking waits that cannot hang on a dead rank: in NCCL mode they poll the
     // communicator's async error state with a timeout (Comm::wait).
     void wait_event(cudaEvent_t e);

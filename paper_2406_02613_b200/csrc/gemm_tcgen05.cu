@@ -150,6 +150,28 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, const 
                  "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
+// Cluster launch control (sm_100): steal the work of a CTA of this grid that
+// has not launched yet. The 16-byte response lands in smem and completes the
+// mbarrier's transaction count; it decodes to that CTA's id, or "none left".
+__device__ __forceinline__ void clc_try_cancel(void* resp, uint64_t* bar) {
+    asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+                     smem_u32(resp)),
+                 "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ int clc_decode(const void* resp) {
+    uint32_t x = 0, ok = 0;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b128 r;\n\t"
+        "ld.shared.b128 r, [%2];\n\t"
+        "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n\t"
+        "selp.u32 %1, 1, 0, p;\n\t"
+        "@p clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%0, _, _, _}, r;\n\t}\n"
+        : "=r"(x), "=r"(ok)
+        : "r"(smem_u32(resp))
+        : "memory");
+    return ok ? static_cast<int>(x) : -1;
+}
 __device__ __forceinline__ int ld_acquire(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -231,7 +253,8 @@ template <int BN, int STAGES, int X3 = 0>
 constexpr int smem_bytes() {
     return 1024 /*align slack*/ + STAGES * (kBM + BN) * 128 * (X3 ? 2 : 1) +
            epi_warps<BN, STAGES, X3>() * epi_warp_bytes<BN, STAGES>() +
-           (2 * STAGES + 4 + epi_warps<BN, STAGES, X3>() * in_bufs<BN>()) * 8 + 16;
+           (2 * STAGES + 4 + epi_warps<BN, STAGES, X3>() * in_bufs<BN>()) * 8 + 16 +
+           48 /* CLC: full / empty mbarriers, 16 B response, alignment */;
 }
 
 struct Sched {
@@ -334,7 +357,8 @@ struct EpiMaps {
 template <int BN, int STAGES, int A_MN, int B_MN, int X3 = 0>
 __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem) {
+                   const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem,
+                   int use_clc) {
     static_assert(!X3 || (!A_MN && !B_MN), "3xTF32: the split pre-pass writes K-major planes");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -355,7 +379,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
     uint64_t* inbar = tempty + 2;      // [8 epilogue warps][kInBuf]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + kEpiWarps * kInBuf);
+    uint64_t* clc_full = inbar + kEpiWarps * kInBuf;  // CLC response ready (1 arrive + 16 B tx)
+    uint64_t* clc_empty = clc_full + 1;                // every role warp has read it
+    uint8_t* clc_resp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(clc_empty + 1) + 15) & ~uintptr_t(15));
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(clc_resp + 16);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -371,6 +398,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
         }
         for (int i = 0; i < kEpiWarps * kInBuf; ++i) mbar_init(&inbar[i], 1);
+        mbar_init(clc_full, 1);
+        mbar_init(clc_empty, 2 + kEpiWarps);  // producer, MMA issuer, epilogue warps
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -392,11 +421,41 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     pdl_trigger();
     pdl_wait();
 
-    if (warp == 0) {
+    // Work units. Static: u, u + grid, ... (grid = min(units, SMs)). With
+    // cluster launch control (use_clc, grid = units): after its own unit a CTA
+    // takes over the units of CTAs that have not launched — SMs held by
+    // another stream's kernels (the comm stream's collectives and optimizer)
+    // just launch fewer CTAs, and the running ones absorb the work instead of
+    // a static tile list waiting for its SM. Warp 3 claims one unit ahead; the
+    // role warps read each claim from smem and release it.
+    int clc_i = 0;
+    auto next_unit = [&](int u) -> int {
+        if (!use_clc) return u + static_cast<int>(gridDim.x) < nunits ? u + static_cast<int>(gridDim.x) : -1;
+        mbar_wait(clc_full, clc_i & 1);
+        const int nu = clc_decode(clc_resp);
+        fence_async_smem();  // the async proxy rewrites the response next
+        __syncwarp();
+        if (lane == 0) mbar_arrive(clc_empty);
+        ++clc_i;
+        return nu;
+    };
+
+    if (warp == 3 && use_clc) {
+        for (int i = 0;; ++i) {
+            if (i > 0) mbar_wait(clc_empty, (i - 1) & 1);  // every role warp has read claim i-1
+            if (elect_one()) {
+                mbar_expect_tx(clc_full, 16);
+                clc_try_cancel(clc_resp, clc_full);
+            }
+            __syncwarp();
+            mbar_wait(clc_full, i & 1);
+            if (clc_decode(clc_resp) < 0) break;  // no unlaunched CTA left
+        }
+    } else if (warp == 0) {
         // like the MMA issuer: warp-uniform walk and waits, one elected lane issues
         {
             int it = 0;
-            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            for (int u = blockIdx.x; u >= 0; u = next_unit(u)) {
                 int mb, nb, sp;
                 decode(sc, u, mb, nb, sp);
                 const int m0 = mb * kBM, n0 = nb * BN;
@@ -453,7 +512,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         constexpr uint64_t a_step = A_MN ? 2048 >> 4 : 32 >> 4;
         constexpr uint64_t b_step = B_MN ? 2048 >> 4 : 32 >> 4;
         int it = 0, lt = 0;
-        for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
+        for (int u = blockIdx.x; u >= 0; u = next_unit(u), ++lt) {
             int mb, nb, sp;
             decode(sc, u, mb, nb, sp);
             const int kb0 = sp * sc.kb_per_split;
@@ -519,7 +578,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         uint32_t in_phase = 0;  // bit k: parity of the next wait on input buffer k
         constexpr int kChunks = BN / 32;
         int lt = 0;
-        for (int u = blockIdx.x; u < nunits; u += gridDim.x, ++lt) {
+        for (int u = blockIdx.x; u >= 0; u = next_unit(u), ++lt) {
             int mb, nb, sp;
             decode(sc, u, mb, nb, sp);
             const int acc = lt & 1;
@@ -834,6 +893,10 @@ CUtensorMap operand_map(const GemmOperand& op, int rows, int K, int tile_rows) {
 
 constexpr int kSemSlots = 1 << 21;  // (tile, quadrant) semaphores for ordered split-K (8 MB)
 
+// CLC scheduling for every non-split GEMM (ACCO_GEMM_NO_CLC=1: static persistent
+// schedule, the A/B knob; read per launch)
+bool use_clc(const Sched& sc) { return sc.splits == 1 && std::getenv("ACCO_GEMM_NO_CLC") == nullptr; }
+
 int* split_semaphores() {
     static int* sem = nullptr;
     if (!sem) {
@@ -890,8 +953,11 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     }
     CUtensorMap ta = operand_map(A, M, K, kBM);
     CUtensorMap tb = operand_map(B, N, K, ep.mode == kEpiSwiGLU ? BN / 2 : BN);
-    const int grid = std::min(sc.units(), num_sms());
-    launch_pdl(kern, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem);
+    // cluster-launch-control work stealing unless split-K: the ordered split
+    // hand-off assumes the static unit order
+    const int clc = use_clc(sc) ? 1 : 0;
+    const int grid = clc ? sc.units() : std::min(sc.units(), num_sms());
+    launch_pdl(kern, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, clc);
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1057,8 +1123,9 @@ void launch_x3(const float* a_planes, const float* b_planes, int64_t kp, int M, 
         sem = split_semaphores();
     }
     const CUtensorMap ta = planes(a_planes, M, kBM), tb = planes(b_planes, N, BN);
-    const int grid = std::min(sc.units(), num_sms());
-    launch_pdl(kern, grid, gemm_threads<BN, STAGES, 1>(), smem, stream, ta, tb, em, M, N, sc, ep, sem);
+    const int clc = use_clc(sc) ? 1 : 0;
+    const int grid = clc ? sc.units() : std::min(sc.units(), num_sms());
+    launch_pdl(kern, grid, gemm_threads<BN, STAGES, 1>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, clc);
     ACCO_CHECK_LAUNCH();
 }
 

@@ -907,6 +907,39 @@ __global__ void spin_kernel(uint64_t ns) {
     }
 }
 
+// paced multi-CTA copy (see lm_kernels.h comm_standin)
+__global__ void __launch_bounds__(512) comm_standin_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                           int64_t n16, uint64_t ns) {
+    ACCO_PDL_PROLOGUE();
+    __shared__ uint64_t t0s;
+    if (threadIdx.x == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        t0s = t;
+    }
+    __syncthreads();
+    const uint64_t t0 = t0s;
+    const int64_t per = (n16 + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = static_cast<int64_t>(blockIdx.x) * per, hi = min(n16, lo + per);
+    constexpr int kChunk = 512 * 8;  // 64 KB per CTA step
+    const int64_t steps = (hi - lo + kChunk - 1) / kChunk;
+    for (int64_t s = 0; s < steps; ++s) {
+        const int64_t b = lo + s * kChunk;
+#pragma unroll 8
+        for (int k = 0; k < 8; ++k) {
+            const int64_t i = b + k * 512 + threadIdx.x;
+            if (i < hi) dst[i] = __ldcs(src + i);
+        }
+        // pace: the link delivers (s + 1) / steps of this CTA's share by t0 + that fraction of ns
+        const uint64_t due = t0 + static_cast<uint64_t>(static_cast<double>(ns) * (s + 1) / steps);
+        uint64_t t;
+        do {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t < due) __nanosleep(500);
+        } while (t < due);
+    }
+}
+
 // ------------------------------------------------------ rotary / SwiGLU (Llama)
 // In place on the q|k columns of qkv [M, ld]: nh = n_head + n_kv_head heads
 // of hd columns from column 0. Pair (i, i + hd/2), angle table cs[t][i] =
@@ -1395,6 +1428,13 @@ void unpack_padded(const void* padded, void* flat, int elem_bytes, const uint64_
 void spin_ns(uint64_t ns, cudaStream_t s) {
     if (ns == 0) return;
     spin_kernel<<<1, 1, 0, s>>>(ns);
+    ACCO_CHECK_LAUNCH();
+}
+
+void comm_standin(const void* src, void* dst, int64_t bytes, int ctas, uint64_t ns, cudaStream_t s) {
+    if (bytes <= 0 || ctas <= 0) return;
+    launch_pdl(comm_standin_kernel, ctas, 512, 0, s, static_cast<const uint4*>(src), static_cast<uint4*>(dst),
+               bytes / 16, ns);
     ACCO_CHECK_LAUNCH();
 }
 

@@ -102,5 +102,10 @@ void replica_hash(const void* p, int64_t bytes, uint64_t* out, cudaStream_t s);
 void hash_compare(const uint64_t* all, int n, int k, int* flag, int bit, cudaStream_t s);
 // straggler throttle (HeterogeneityProfile, protocols.hpp:19-27): spin ns on the stream
 void spin_ns(uint64_t ns, cudaStream_t s);
+// Single-GPU stand-in for an NVLink collective: `ctas` CTAs (NCCL's channel
+// count) copy `bytes` through HBM from src to dst (both >= bytes), paced so the
+// copy lasts `ns` — occupying SMs and HBM bandwidth the way the real
+// reduce-scatter / all-gather kernels would, for as long as they would.
+void comm_standin(const void* src, void* dst, int64_t bytes, int ctas, uint64_t ns, cudaStream_t s);
 
 }  // namespace acco

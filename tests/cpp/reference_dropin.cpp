@@ -231,7 +231,7 @@ int main() {
         acco_lm_cfg lm{64, 32, 2, 2, 16, 32, 3, ACCO_DTYPE_F32, 3, 0, 0, 0, 0, 0.0};
         acco_model* model = nullptr;
         acco_model_create(&lm, &model);
-        acco_sim_cfg s{2, 3, 2, 0, 9, ACCO_SCHED_FLOOR, nullptr, 0, 0, 0, nullptr, 0.0, 0, 0};
+        acco_sim_cfg s{2, 3, 2, 0, 9, ACCO_SCHED_FLOOR, nullptr, 0, 0, 0, nullptr, 0.0, 0, 0, 0, 0.0};
         oc.total_steps = T;
         const acco_opt_cfg cc = to_c(oc);
         acco_trainer* trn = nullptr;
