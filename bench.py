@@ -172,6 +172,9 @@ def main():
     ap.add_argument("--straggler", type=float, default=1.0,
                     help="C4 heterogeneous scenario: rank 0's micro-batches take this many times longer "
                          "(HeterogeneityProfile multiplier, emulated by a measured spin after each micro-batch)")
+    ap.add_argument("--straggler-mode", default="device", choices=["device", "host"],
+                    help="device: a spin kernel on the slow rank's compute stream after each micro-batch; host: the "
+                         "paper's time.sleep (PAPER.md:394) after each completed micro-batch, GPU idle")
     ap.add_argument("--emulate-comm-gpus", type=int, default=0,
                     help="single-GPU study of the overlap: every comm phase holds the comm stream for the NVLink "
                          "time (770 GB/s per direction) of an N-GPU reduce-scatter + all-gather (all-reduce for "
@@ -254,6 +257,7 @@ def main():
     def timed(method, k, schedule, profile=False, clocks=False):
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=k, master_seed=1,
                             schedule=schedule, eval_every=0, worker_multipliers=mult,
+                            throttle_host=args.straggler_mode == "host",
                             comm_delay_ns=comm_delay_ns(method), **standin(method))
         tr = api.Trainer(method, model, opt, sim, make_comm(method))
         tr.set_theta(model.default_theta0(1))
@@ -309,6 +313,7 @@ def main():
         model_h = api.Model(lm_h)
         sim = api.SimConfig(n_workers=world, batch_size=B, n_grad_accumulation=1, master_seed=1,
                             schedule=args.schedule, eval_every=0, worker_multipliers=mult,
+                            throttle_host=args.straggler_mode == "host",
                             comm_delay_ns=comm_delay_ns("acco"), **standin("acco"))
         tr = api.Trainer("acco", model_h, opt, sim, make_comm("acco"))
         tr.set_theta(model_h.default_theta0(1))
@@ -335,9 +340,13 @@ def main():
     # ---- roofline of the dominant kernel class (GEMMs, tensor bound)
     p = acco["prof"]
     # DRAM traffic per launch from the committed `ncu --set full` capture of a
-    # bench step (tools/gpu_final.sh -> profiles/prof_step_r01d_raw.csv)
+    # bench step (tools/gpu_r2_profile.sh -> profiles/prof_step_r02_raw.csv; the
+    # capture's commit is in profiles/prof_step_r02_meta.json): static evidence
+    # taken once per round, not measured in this run
+    prof_dir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+
     def ncu_traffic(prefix):
-        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "prof_step_r01d_raw.csv")
+        path = os.path.join(prof_dir, "prof_step_r02_raw.csv")
         try:
             with open(path) as f:
                 rows = [r for r in csv.DictReader(f) if prefix in r["kernel"]]
@@ -346,13 +355,20 @@ def main():
         if not rows:
             return None
         return sum(float(r["dram_read_bytes"]) + float(r["dram_write_bytes"]) for r in rows) / len(rows)
+
+    try:
+        with open(os.path.join(prof_dir, "prof_step_r02_meta.json")) as f:
+            traffic_source = {"file": "profiles/prof_step_r02_raw.csv", **json.load(f)}
+    except (OSError, ValueError):
+        traffic_source = None
     g = p["gemm"]
     gemm_tf = g["work"] / (g["ms"] / 1e3) / 1e12 if g["ms"] > 0 else 0.0
     roof = {"kernel": "tcgen05 bf16 GEMM (fwd/dgrad/wgrad, all launches of the timed steps)", "bound": "tensor",
             "achieved": gemm_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": gemm_tf / tf_sus,
             "traffic": ncu_traffic("gemm_tc_kernel"),
             "traffic_note": "mean DRAM read+write bytes per GEMM launch, ncu --set full capture of 12 step GEMMs "
-                            "(profiles/prof_step_r01d_raw.csv); operands are re-read from L2, not DRAM",
+                            "(static evidence, see traffic_source); operands are re-read from L2, not DRAM",
+            "traffic_source": traffic_source,
             "peak_kind": f"{peak_kind} sustained bf16 (kernel timed inside a long step)",
             "launches": g["launches"], "avg_launch_ms": g["ms"] / max(g["launches"], 1),
             "share_of_step": g["ms"] / p["wall_ms"]}
@@ -413,7 +429,11 @@ def main():
                                   ("NCCL RS/AG)" if args.fabric == "nccl" else
                                    "fused peer-memory fold+AdamW+replica-store kernel over NVLink)"),
                    "l2": "inputs larger than L2 (bf16 params 249 MB + activations per step)",
-                   **({"straggler": f"rank 0 x{args.straggler} (HeterogeneityProfile multiplier)"}
+                   "eval": "no full-dataset evaluation inside the timed region: the reference's TraceBuilder::commit "
+                           "evaluates f(theta), f(theta~) every update (protocols.cpp:113-134); here the cadence "
+                           "eval_every = 0 (SURVEY.md a19); parity runs use eval_every = 1",
+                   **({"straggler": f"rank 0 x{args.straggler} (HeterogeneityProfile multiplier, "
+                                    f"{args.straggler_mode} throttle)"}
                       if args.straggler != 1.0 else {}),
                    **({"emulated_interconnect": {
                        "gpus": args.emulate_comm_gpus, "link_GBps": 770,

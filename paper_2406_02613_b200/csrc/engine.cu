@@ -701,6 +701,10 @@ void Trainer::run_acco(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
                     wait_event(ev.mb[(k - 1) % 4]);
                     if (cudaEventQuery(ev.done[p - 1]) == cudaSuccess) break;
                 }
+                // the loss ring holds every micro-batch loss of this run() until it ends:
+                // fail before overwriting one (an adaptive schedule can run long stages)
+                ACCO_REQUIRE(mb_counter_ - mb0 < loss_cap_,
+                             "loss ring overflow: more than 65536 micro-batches in one run() call");
                 const int slot = static_cast<int>(mb_counter_ % loss_cap_);
                 micro(w, params, round, tag, k, acc, loss_ring_ + slot);
                 ACCO_CUDA(cudaEventRecord(ev.mb[k % 4], cs_));
@@ -890,6 +894,8 @@ void Trainer::run_sync(int T, std::vector<UpdateRecord>& recs, RunStats& st) {
             ACCO_CUDA(cudaEventRecord(ev.stage_start[static_cast<size_t>(slot) * nl + w], cs_));
             float* acc = acc_[static_cast<size_t>(w) * nacc + q % nacc];
             for (int j = 0; j < n; ++j) {
+                ACCO_REQUIRE(mb_counter_ - mb0 < loss_cap_,
+                             "loss ring overflow: more than 65536 micro-batches in one run() call");
                 const int ls = static_cast<int>(mb_counter_ % loss_cap_);
                 micro(w, params, round, tag, j, acc, loss_ring_ + ls);
                 mb_slot.push_back(slot);

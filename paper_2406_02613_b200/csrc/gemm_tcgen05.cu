@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 
 namespace acco {
@@ -897,8 +898,24 @@ constexpr int kSemSlots = 1 << 21;  // (tile, quadrant) semaphores for ordered s
 // schedule, the A/B knob; read per launch)
 bool use_clc(const Sched& sc) { return sc.splits == 1 && std::getenv("ACCO_GEMM_NO_CLC") == nullptr; }
 
-int* split_semaphores() {
-    static int* sem = nullptr;
+// Split-K semaphores and the pure-store split workspace are per (device,
+// stream): the hand-off protocol and the workspace contents are
+// stream-ordered, so GEMMs that run concurrently on different streams (the
+// model's weight-gradient side stream, torch's stream in the tests) or devices
+// must not share them.
+struct StreamKey {
+    int dev;
+    cudaStream_t s;
+    bool operator<(const StreamKey& o) const { return dev != o.dev ? dev < o.dev : s < o.s; }
+};
+std::mutex g_scratch_mu;
+
+int* split_semaphores(cudaStream_t stream) {
+    static std::map<StreamKey, int*> sems;
+    int dev = 0;
+    ACCO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    int*& sem = sems[StreamKey{dev, stream}];
     if (!sem) {
         ACCO_CUDA(cudaMalloc(&sem, kSemSlots * sizeof(int)));
         ACCO_CUDA(cudaMemset(sem, 0, kSemSlots * sizeof(int)));
@@ -941,7 +958,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
         em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
         if (sc.splits > 1) {
             ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 8 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
-            sem = split_semaphores();
+            sem = split_semaphores(stream);
         }
     } else {
         em.out = make_map(ep.C, ep.mode == kEpiSwiGLU ? N / 2 : (ep.mode == kEpiDSwiGLU ? 2 * N : N), M, ep.ldc, 32, 32,
@@ -999,20 +1016,27 @@ __global__ void f32_to_bf16_rows(const float* __restrict__ ws, int64_t ldw, __nv
         pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]), pack_bf16(v[6], v[7]));
 }
 
-// Workspace for split-K of pure-store GEMMs (grown on demand; GEMMs are
-// stream-ordered on the compute stream, like the split-K semaphores).
+// Workspace for split-K of pure-store GEMMs, per (device, stream) like the
+// semaphores (grown on demand; uses on one stream are ordered by the stream).
 float* splitk_workspace(size_t elems, cudaStream_t s) {
-    static float* ws = nullptr;
-    static size_t cap = 0;
-    if (elems > cap) {
-        if (ws) {
+    struct Ws {
+        float* p = nullptr;
+        size_t cap = 0;
+    };
+    static std::map<StreamKey, Ws> wss;
+    int dev = 0;
+    ACCO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    Ws& w = wss[StreamKey{dev, s}];
+    if (elems > w.cap) {
+        if (w.p) {
             ACCO_CUDA(cudaStreamSynchronize(s));
-            ACCO_CUDA(cudaFree(ws));
+            ACCO_CUDA(cudaFree(w.p));
         }
-        ACCO_CUDA(cudaMalloc(&ws, elems * sizeof(float)));
-        cap = elems;
+        ACCO_CUDA(cudaMalloc(&w.p, elems * sizeof(float)));
+        w.cap = elems;
     }
-    return ws;
+    return w.p;
 }
 
 // ------------------------------------------------------------ 3xTF32 (fp32)
@@ -1120,7 +1144,7 @@ void launch_x3(const float* a_planes, const float* b_planes, int64_t kp, int M, 
     int* sem = nullptr;
     if (sc.splits > 1) {
         ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 8 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
-        sem = split_semaphores();
+        sem = split_semaphores(stream);
     }
     const CUtensorMap ta = planes(a_planes, M, kBM), tb = planes(b_planes, N, BN);
     const int clc = use_clc(sc) ? 1 : 0;

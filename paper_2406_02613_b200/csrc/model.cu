@@ -203,6 +203,7 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     ACCO_CUDA(cudaEventCreateWithFlags(&ev_sort_, cudaEventDisableTiming));
+    for (auto& e : ev_rd_) ACCO_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 GPTModel::~GPTModel() {
@@ -223,6 +224,7 @@ GPTModel::~GPTModel() {
         cudaEventDestroy(ev_fork_);
         cudaEventDestroy(ev_join_);
         cudaEventDestroy(ev_sort_);
+        for (auto& e : ev_rd_) cudaEventDestroy(e);
     }
     cudaFree(scratch_);
     if (rope_) cudaFree(rope_);
@@ -375,19 +377,30 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     // per-stage memset of the accumulator is unnecessary.
     const bool acc = accumulate_;
     const int beta = acc ? 1 : 0;
-    // Column reductions (bias and LN-parameter gradients) go to the side
-    // stream aux_ right after their input is produced and overlap the next
-    // GEMMs; `join` is placed before the next kernel that overwrites a buffer
-    // an outstanding reduction still reads (DX, DA, DT, DQKV). They share one
-    // scratch area, so they are serialised on aux_ (FIFO) — same kernels and
-    // summation order as inline, so results are bitwise unchanged.
-    // ACCO_SERIAL_REDUCE=1 (diagnostic A/B): the reductions run inline on s
+    // The column reductions (bias and LN-parameter gradients) depend on
+    // nothing the input-gradient chain produces next, so they run on the side
+    // stream aux_, concurrently with the chain on s: each is forked right
+    // after its input exists, and s waits for a buffer's last side-stream
+    // reader (ev_rd_) only right before it overwrites that buffer. Same
+    // kernels and summation orders as inline, so results are bitwise unchanged.
+    // ACCO_WGRAD_SIDE=1 also moves the weight-gradient GEMMs there (measured:
+    // neutral, 810-813k vs 815-828k tok/s inline, profiles/r02_summary.md);
+    // ACCO_SERIAL_REDUCE=1: everything inline on s (A/B).
     static const bool serial = std::getenv("ACCO_SERIAL_REDUCE") != nullptr;
+    const bool wg_side = !serial && std::getenv("ACCO_WGRAD_SIDE") != nullptr;
     cudaStream_t aux_ = serial ? s : this->aux_;
+    cudaStream_t ws = wg_side ? aux_ : s;  // weight-gradient stream
+    enum { kRdDX, kRdDA, kRdDT, kRdDQKV };
     auto fork = [&] {
         if (serial) return;
         ACCO_CUDA(cudaEventRecord(ev_fork_, s));
         ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+    };
+    auto mark = [&](int b) {  // the side-stream work issued so far is buffer b's last reader
+        if (!serial) ACCO_CUDA(cudaEventRecord(ev_rd_[b], aux_));
+    };
+    auto guard = [&](int b) {  // s is about to overwrite buffer b
+        if (!serial) ACCO_CUDA(cudaStreamWaitEvent(s, ev_rd_[b], 0));
     };
     auto join = [&] {
         if (serial) return;
@@ -395,10 +408,12 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
         ACCO_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     };
     // LM head (tied to wte): dwte (+)= dlogits^T hf ; dhf = dlogits wte
-    mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d, beta), s);
+    if (wg_side) fork();
+    mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d, beta), ws);
     mm<T>(LOG, vpad_, false, W(kWte), d, true, M, d, V, ep_store(DT, d), s);
     fork();
     layernorm_bwd_params<T>(DT, X(L), stat(4 * L), stat(4 * L + 1), Gp(kLnf), Gp(kLnf + 1), scratch_, M, d, acc, aux_);
+    mark(kRdDT);
     layernorm_bwd_dx<T>(DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), DX, false, M, d, s);
     for (int l = L - 1; l >= 0; --l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
@@ -406,34 +421,45 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
         // MLP
         fork();
         colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, acc, aux_);
-        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d, beta), s);
-        join();  // DA (and DT, DX) free of outstanding readers
+        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d, beta), ws);
+        mark(kRdDX);
+        guard(kRdDA);
         mm<T>(DX, d, false, W(li(l, 10)), 4 * d, true, M, 4 * d, d, ep_dgelu(DA, 4 * d, A), s);
         fork();
         colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, acc, aux_);
-        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d, beta), s);
+        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d, beta), ws);
+        mark(kRdDA);
+        guard(kRdDT);
         mm<T>(DA, 4 * d, false, W(li(l, 8)), d, true, M, d, 4 * d, ep_store(DT, d), s);
         fork();
         layernorm_bwd_params<T>(DT, XM, stat(4 * l + 2), stat(4 * l + 3), Gp(li(l, 6)), Gp(li(l, 7)), scratch_, M, d,
                                 acc, aux_);
+        mark(kRdDT);
+        guard(kRdDX);
         layernorm_bwd_dx<T>(DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), DX, true, M, d, s);
         // attention
         fork();
         colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, acc, aux_);
-        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
-        join();  // DT (read by the LN2 parameter reduction) is overwritten next
+        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d, beta), ws);
+        mark(kRdDX);
+        guard(kRdDT);
         mm<T>(DX, d, false, W(li(l, 4)), d, true, M, d, d, ep_store(DT, d), s);
+        guard(kRdDQKV);
         attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, H, hd, s);
         fork();
         colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, aux_);
-        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d, beta), s);
+        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d, beta), ws);
+        mark(kRdDQKV);
         mm<T>(DQKV, 3 * d, false, W(li(l, 2)), d, true, M, d, 3 * d, ep_store(DT, d), s);
         fork();
         layernorm_bwd_params<T>(DT, X(l), stat(4 * l), stat(4 * l + 1), Gp(li(l, 0)), Gp(li(l, 1)), scratch_, M, d,
                                 acc, aux_);
+        mark(kRdDT);
+        guard(kRdDX);
         layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s);
     }
-    // wte rows: the head wgrad above stored/added every row; the embedding adds
+    // wte rows: the head wgrad stored/added every row; the embedding adds (after it)
+    join();
     ACCO_CUDA(cudaStreamWaitEvent(s, ev_sort_, 0));
     embed_bwd<T>(sort_, DX, M, Tq, d, V, Gp(kWte), Gp(kWpe), run_sum_, acc, s);
     join();  // the accumulator is complete when the compute stream passes this point

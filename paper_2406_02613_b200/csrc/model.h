@@ -107,6 +107,9 @@ private:
     // the gradient accumulator, so they run beside the GEMMs (fork/join events)
     cudaStream_t aux_ = nullptr;
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr, ev_sort_ = nullptr;
+    // last side-stream reader of each backward scratch buffer (DX, DA, DT, DQKV):
+    // the compute stream waits on it only right before overwriting that buffer
+    cudaEvent_t ev_rd_[4] = {nullptr, nullptr, nullptr, nullptr};
     std::vector<char*> act_;    // activation slots (see model.cu)
     // host-data path
     int32_t* pinned_data_ = nullptr;

@@ -1,5 +1,5 @@
 """The committed profile evidence that bench.py reads at run time
-(profiles/prof_step_r01d_raw.csv -> the roofline `traffic` fields) parses and
+(profiles/prof_step_r02_raw.csv -> the roofline `traffic` fields) parses and
 covers the kernel classes bench.py reports."""
 import csv
 import os
@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_ncu_summary_has_traffic_for_reported_kernels():
-    path = os.path.join(ROOT, "profiles", "prof_step_r01d_raw.csv")
+    path = os.path.join(ROOT, "profiles", "prof_step_r02_raw.csv")
     with open(path) as f:
         rows = list(csv.DictReader(f))
     assert {"kernel", "time_us", "dram_read_bytes", "dram_write_bytes"} <= set(rows[0])
@@ -21,7 +21,15 @@ def test_ncu_summary_has_traffic_for_reported_kernels():
 
 
 def test_launch_list_present():
-    path = os.path.join(ROOT, "profiles", "r01_launches_bench_step.csv")
+    path = os.path.join(ROOT, "profiles", "r02_launches_bench_step.csv")
     with open(path) as f:
         text = f.read()
     assert "gemm_tc_kernel" in text and "gpu__time_duration.sum" in text
+
+
+def test_capture_commit_recorded():
+    import json
+
+    with open(os.path.join(ROOT, "profiles", "prof_step_r02_meta.json")) as f:
+        meta = json.load(f)
+    assert len(meta["capture_commit"]) >= 7 and "ncu --set full" in meta["command"]
