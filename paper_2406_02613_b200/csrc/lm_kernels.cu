@@ -658,47 +658,87 @@ __global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int M, in
 }
 
 // --------------------------------------------------------- embedding backward
-// single-CTA bitonic sort of keys (tok * M + m): stable grouping by token with
-// ascending positions inside each group.
-__global__ void sort_keys_kernel(const int32_t* __restrict__ tok, int M, int P, uint32_t* out) {
-    ACCO_PDL_PROLOGUE();
-    extern __shared__ uint32_t keys[];
-    for (int i = threadIdx.x; i < P; i += blockDim.x)
-        keys[i] = i < M ? static_cast<uint32_t>(tok[i]) * static_cast<uint32_t>(M) + i : 0xffffffffu;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
-                int ixj = i ^ j;
-                if (ixj > i) {
-                    uint32_t a = keys[i], b = keys[ixj];
-                    bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        keys[i] = b;
-                        keys[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (int i = threadIdx.x; i < M; i += blockDim.x) out[i] = keys[i];
+// Keys (token << 32 | position) sorted by a stable LSD radix sort on the token
+// bits (8-bit digits): positions come in ascending order, so every token's
+// positions stay ascending, and the keys are unique, so the order is unique —
+// deterministic, any micro-batch size, any vocabulary (< 2^31). Per pass:
+// per-tile digit histograms [digit][tile], one exclusive scan, then each tile
+// scatters its keys in index order (one warp per tile, match_any ranking).
+constexpr int kSortTile = 1024;
+
+__device__ __forceinline__ uint64_t sort_key_in(const uint64_t* keys, const int32_t* tok, int i) {
+    return keys ? keys[i] : (static_cast<uint64_t>(static_cast<uint32_t>(tok[i])) << 32) | static_cast<uint32_t>(i);
 }
 
-template <class T>
-__global__ void embed_bwd_wte_kernel(const uint32_t* __restrict__ sorted, int M, const T* __restrict__ dx,
-                                     int d, float* __restrict__ grad_wte) {
+__global__ void radix_hist_kernel(const uint64_t* __restrict__ keys, const int32_t* __restrict__ tok, int M, int shift,
+                                  unsigned* __restrict__ hist) {
     ACCO_PDL_PROLOGUE();
-    const int i = blockIdx.x;
-    const uint32_t tok = sorted[i] / static_cast<uint32_t>(M);
-    if (i > 0 && sorted[i - 1] / static_cast<uint32_t>(M) == tok) return;  // not a segment start
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        float acc = 0.f;
-        for (int j = i; j < M && sorted[j] / static_cast<uint32_t>(M) == tok; ++j) {
-            const int m = static_cast<int>(sorted[j] % static_cast<uint32_t>(M));
-            acc += to_f(dx[static_cast<int64_t>(m) * d + c]);
+    __shared__ unsigned cnt[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int t0 = blockIdx.x * kSortTile, t1 = min(M, t0 + kSortTile);
+    for (int i = t0 + threadIdx.x; i < t1; i += blockDim.x)
+        atomicAdd(&cnt[(sort_key_in(keys, tok, i) >> (32 + shift)) & 255u], 1u);  // integer: order-free
+    __syncthreads();
+    for (int dgt = threadIdx.x; dgt < 256; dgt += blockDim.x) hist[dgt * gridDim.x + blockIdx.x] = cnt[dgt];
+}
+
+// in-place exclusive scan of n counters, one block of 1024 threads
+__global__ void radix_scan_kernel(unsigned* __restrict__ h, int n) {
+    ACCO_PDL_PROLOGUE();
+    __shared__ unsigned part[32];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int a = threadIdx.x * per, b = min(n, a + per);
+    unsigned s = 0;
+    for (int i = a; i < b; ++i) s += h[i];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned x = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) part[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned p = lane < static_cast<int>(blockDim.x >> 5) ? part[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, p, o);
+            if (lane >= o) p += y;
         }
-        grad_wte[static_cast<int64_t>(tok) * d + c] += acc;
+        part[lane] = p;
+    }
+    __syncthreads();
+    unsigned run = x - s + (w > 0 ? part[w - 1] : 0u);  // exclusive prefix of this thread's segment
+    for (int i = a; i < b; ++i) {
+        const unsigned v = h[i];
+        h[i] = run;
+        run += v;
+    }
+}
+
+// one warp per tile: stable scatter in index order
+__global__ void radix_scatter_kernel(const uint64_t* __restrict__ keys, const int32_t* __restrict__ tok, int M,
+                                     int shift, const unsigned* __restrict__ offs, uint64_t* __restrict__ out) {
+    ACCO_PDL_PROLOGUE();
+    __shared__ unsigned run[256];
+    const int lane = threadIdx.x;
+    for (int dgt = lane; dgt < 256; dgt += 32) run[dgt] = offs[dgt * gridDim.x + blockIdx.x];
+    __syncwarp();
+    const int t0 = blockIdx.x * kSortTile, t1 = min(M, t0 + kSortTile);
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = t0; base < t1; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < t1;
+        const uint64_t key = valid ? sort_key_in(keys, tok, i) : 0;
+        const unsigned dgt = valid ? static_cast<unsigned>(key >> (32 + shift)) & 255u : 256u + lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, dgt);
+        const unsigned rank = __popc(peers & lt);
+        if (valid) out[run[dgt] + rank] = key;
+        __syncwarp();
+        if (valid && rank == 0) run[dgt] += __popc(peers);
+        __syncwarp();
     }
 }
 
@@ -712,18 +752,17 @@ __global__ void embed_bwd_wte_kernel(const uint32_t* __restrict__ sorted, int M,
 constexpr int kEmbChunk = 32;
 
 template <class T>
-__global__ void embed_runs_kernel(const uint32_t* __restrict__ sorted, int M, const T* __restrict__ dx, int d,
+__global__ void embed_runs_kernel(const uint64_t* __restrict__ sorted, int M, const T* __restrict__ dx, int d,
                                   float* __restrict__ run_sum) {
     ACCO_PDL_PROLOGUE();
     const int p0 = blockIdx.x * kEmbChunk, p1 = min(M, p0 + kEmbChunk);
-    const uint32_t uM = static_cast<uint32_t>(M);
     for (int cg = threadIdx.x; cg < d / 8; cg += blockDim.x) {
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint32_t prev = sorted[p0] / uM;
+        uint32_t prev = static_cast<uint32_t>(sorted[p0] >> 32);
         int r = 0;
         for (int p = p0; p < p1; ++p) {
-            const uint32_t key = sorted[p];
-            const uint32_t tok = key / uM;
+            const uint64_t key = sorted[p];
+            const uint32_t tok = static_cast<uint32_t>(key >> 32);
             if (tok != prev) {
                 float4* o = reinterpret_cast<float4*>(run_sum + static_cast<int64_t>(p0 + r) * d + cg * 8);
                 o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -734,7 +773,7 @@ __global__ void embed_runs_kernel(const uint32_t* __restrict__ sorted, int M, co
                 prev = tok;
             }
             float v[8];
-            load8<T>(dx + static_cast<int64_t>(key % uM) * d + cg * 8, v);
+            load8<T>(dx + static_cast<int64_t>(static_cast<uint32_t>(key)) * d + cg * 8, v);
 #pragma unroll
             for (int k = 0; k < 8; ++k) acc[k] += v[k];
         }
@@ -744,21 +783,21 @@ __global__ void embed_runs_kernel(const uint32_t* __restrict__ sorted, int M, co
     }
 }
 
-__global__ void embed_fold_kernel(const uint32_t* __restrict__ sorted, int M, const float* __restrict__ run_sum,
+__global__ void embed_fold_kernel(const uint64_t* __restrict__ sorted, int M, const float* __restrict__ run_sum,
                                   int d, float* __restrict__ grad_wte) {
     ACCO_PDL_PROLOGUE();
     const int i = blockIdx.x;
-    const uint32_t uM = static_cast<uint32_t>(M);
-    const uint32_t tok = sorted[i] / uM;
-    if (i > 0 && sorted[i - 1] / uM == tok) return;  // not a segment start
+    auto tok_at = [&](int p) { return static_cast<uint32_t>(sorted[p] >> 32); };
+    const uint32_t tok = tok_at(i);
+    if (i > 0 && tok_at(i - 1) == tok) return;  // not a segment start
     const int c = i / kEmbChunk;
     int r0 = 0;  // run index of this segment inside its first chunk
-    for (int p = c * kEmbChunk + 1; p <= i; ++p) r0 += (sorted[p] / uM != sorted[p - 1] / uM) ? 1 : 0;
+    for (int p = c * kEmbChunk + 1; p <= i; ++p) r0 += tok_at(p) != tok_at(p - 1) ? 1 : 0;
     for (int cg = threadIdx.x; cg < d / 8; cg += blockDim.x) {
         const float4* a = reinterpret_cast<const float4*>(run_sum + static_cast<int64_t>(c * kEmbChunk + r0) * d +
                                                           cg * 8);
         float4 s0 = a[0], s1 = a[1];
-        for (int cc = c + 1; cc * kEmbChunk < M && sorted[cc * kEmbChunk] / uM == tok; ++cc) {
+        for (int cc = c + 1; cc * kEmbChunk < M && tok_at(cc * kEmbChunk) == tok; ++cc) {
             const float4* b = reinterpret_cast<const float4*>(run_sum + static_cast<int64_t>(cc) * kEmbChunk * d +
                                                               cg * 8);
             const float4 t0 = b[0], t1 = b[1];
@@ -1263,24 +1302,30 @@ void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_
     ACCO_CHECK_LAUNCH();
 }
 
-void embed_sort(const int32_t* tok, int M, int V, uint32_t* sort_scratch, cudaStream_t s) {
+void embed_sort(const int32_t* tok, int M, int V, uint64_t* sorted, uint64_t* tmp, unsigned* hist, cudaStream_t s) {
     ProfScope prof(kProfEmbed, 8.0 * M, s);
-    ACCO_REQUIRE(static_cast<uint64_t>(V) * static_cast<uint64_t>(M) < 0xffffffffull,
-                 "embed_bwd: vocab * tokens exceeds the 32-bit sort key");
-    int P = 1;
-    while (P < M) P <<= 1;
-    ACCO_REQUIRE(P * 4 <= 200 * 1024, "embed_bwd: micro-batch too large for the single-CTA sort");
-    static bool configured = false;
-    if (!configured) {
-        ACCO_CUDA(cudaFuncSetAttribute(sort_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        configured = true;
+    ACCO_REQUIRE(V >= 1 && M >= 1, "embed_sort: empty input");
+    int bits = 0;
+    while ((1ll << bits) < V) ++bits;
+    const int passes = std::max(1, (bits + 7) / 8);
+    const int tiles = ceil_div(M, kSortTile);
+    // ping-pong so the last pass lands in `sorted`
+    uint64_t* bufs[2] = {passes % 2 ? sorted : tmp, passes % 2 ? tmp : sorted};
+    const uint64_t* in = nullptr;  // pass 0 reads the tokens (keys built on the fly)
+    for (int p = 0; p < passes; ++p) {
+        uint64_t* out = bufs[p & 1];
+        launch_pdl(radix_hist_kernel, tiles, 256, 0, s, in, tok, M, 8 * p, hist);
+        ACCO_CHECK_LAUNCH();
+        launch_pdl(radix_scan_kernel, 1, 1024, 0, s, hist, 256 * tiles);
+        ACCO_CHECK_LAUNCH();
+        launch_pdl(radix_scatter_kernel, tiles, 32, 0, s, in, tok, M, 8 * p, static_cast<const unsigned*>(hist), out);
+        ACCO_CHECK_LAUNCH();
+        in = out;
     }
-    launch_pdl(sort_keys_kernel, 1, 1024, P * 4, s, tok, M, P, sort_scratch);
-    ACCO_CHECK_LAUNCH();
 }
 
 template <class T>
-void embed_bwd(const uint32_t* sorted, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
+void embed_bwd(const uint64_t* sorted, const T* dx, int M, int seq, int d, int V, float* grad_wte, float* grad_wpe,
                float* run_sum, bool acc_wpe, cudaStream_t s, bool zero_wte) {
     ProfScope prof(kProfEmbed, 1.0 * M * d * sizeof(T), s);
     ACCO_REQUIRE(d % 8 == 0, "embed_bwd: d_model must be a multiple of 8");
@@ -1448,7 +1493,7 @@ void comm_standin(const void* src, void* dst, int64_t bytes, int ctas, uint64_t 
                                       int, cudaStream_t, bool);                                               \
     template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);             \
     template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
-    template void embed_bwd<T>(const uint32_t*, const T*, int, int, int, int, float*, float*, float*,        \
+    template void embed_bwd<T>(const uint64_t*, const T*, int, int, int, int, float*, float*, float*,        \
                                bool, cudaStream_t, bool);                                                     \
     template void rope_apply<T>(T*, int64_t, const float2*, int, int, int, int, bool, cudaStream_t);          \
     template void swiglu_fwd<T>(const T*, T*, int, int, cudaStream_t);                                        \

@@ -50,14 +50,15 @@ void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, i
 void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s);
 
 // Embedding backward, step 1 (token-only, so it runs early on a side
-// stream): sorted[i] = keys tok[m] * M + m in ascending order.
-void embed_sort(const int32_t* tok, int M, int V, uint32_t* sorted, cudaStream_t s);
+// stream): sorted[i] = keys (tok[m] << 32 | m) in ascending order (stable LSD
+// radix sort on the token bits; tmp: M keys, hist: 256 x ceil(M / 1024)).
+void embed_sort(const int32_t* tok, int M, int V, uint64_t* sorted, uint64_t* tmp, unsigned* hist, cudaStream_t s);
 // Step 2: grad_wte[tok] += sum of dx rows of the token's segment (fixed
 // chunk/run order, run_sum = [M, d] fp32 scratch), grad_wpe[t] += sum_b
 // dx[b*seq + t] (skipped when grad_wpe == nullptr); zero_wte: grad_wte is
 // zeroed first (untied embedding, first micro-batch).
 template <class T>
-void embed_bwd(const uint32_t* sorted, const T* dx, int M, int seq, int d, int V, float* grad_wte,
+void embed_bwd(const uint64_t* sorted, const T* dx, int M, int seq, int d, int V, float* grad_wte,
                float* grad_wpe, float* run_sum, bool accumulate_wpe, cudaStream_t s, bool zero_wte = false);
 
 // Rotary embedding in place on the first nh heads (q then k) of qkv [M, ld]:

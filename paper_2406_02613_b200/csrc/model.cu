@@ -176,7 +176,9 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     ACCO_CUDA(cudaMalloc(&tok_in_, M * sizeof(int32_t)));
     ACCO_CUDA(cudaMalloc(&tok_out_, M * sizeof(int32_t)));
     ACCO_CUDA(cudaMalloc(&idx_, c.max_batch * sizeof(int32_t)));
-    ACCO_CUDA(cudaMalloc(&sort_, M * sizeof(uint32_t)));
+    ACCO_CUDA(cudaMalloc(&sort_, M * sizeof(uint64_t)));
+    ACCO_CUDA(cudaMalloc(&sort_tmp_, M * sizeof(uint64_t)));
+    ACCO_CUDA(cudaMalloc(&sort_hist_, 256 * ((M + 1023) / 1024) * sizeof(unsigned)));
     ACCO_CUDA(cudaMalloc(&run_sum_, static_cast<size_t>(M) * d * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&row_loss_, M * sizeof(float)));
     ACCO_CUDA(cudaMalloc(&stats_, (4 * L + 2) * M * sizeof(float)));
@@ -213,6 +215,8 @@ GPTModel::~GPTModel() {
     cudaFree(tok_out_);
     cudaFree(idx_);
     cudaFree(sort_);
+    cudaFree(sort_tmp_);
+    cudaFree(sort_hist_);
     cudaFree(run_sum_);
     cudaFree(row_loss_);
     cudaFree(stats_);
@@ -307,13 +311,13 @@ Epilogue ep_acc(float* c, int64_t ldc, int beta) {
 void GPTModel::sort_tokens(int M, cudaStream_t s) {
     static const bool serial = std::getenv("ACCO_SERIAL_REDUCE") != nullptr;
     if (serial) {
-        embed_sort(tok_in_, M, c_.vocab, sort_, s);
+        embed_sort(tok_in_, M, c_.vocab, sort_, sort_tmp_, sort_hist_, s);
         ACCO_CUDA(cudaEventRecord(ev_sort_, s));
         return;
     }
     ACCO_CUDA(cudaEventRecord(ev_fork_, s));
     ACCO_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
-    embed_sort(tok_in_, M, c_.vocab, sort_, aux_);
+    embed_sort(tok_in_, M, c_.vocab, sort_, sort_tmp_, sort_hist_, aux_);
     ACCO_CUDA(cudaEventRecord(ev_sort_, aux_));
 }
 

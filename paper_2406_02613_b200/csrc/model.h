@@ -93,7 +93,9 @@ private:
     // device buffers
     int32_t* data_ = nullptr;
     int32_t *tok_in_ = nullptr, *tok_out_ = nullptr, *idx_ = nullptr;
-    uint32_t* sort_ = nullptr;
+    uint64_t* sort_ = nullptr;      // sorted (token, position) keys of the embedding backward
+    uint64_t* sort_tmp_ = nullptr;
+    unsigned* sort_hist_ = nullptr;
     float* run_sum_ = nullptr;  // embedding-gradient run sums [M, d]
     void* arena_ = nullptr;
     size_t arena_bytes_ = 0;

@@ -184,3 +184,31 @@ def test_wide_row_norm_backward_matches_warp_per_row(cuda, arch, d, monkeypatch)
     assert _rel(g_wide, g_nar) <= 1e-2
     og, _, ol = G.LMProblem(gc).stochastic_grad(th.float().double().numpy(), seed, 2)
     assert _rel(g_wide, og * 2) <= 5e-2
+
+
+def test_embedding_backward_past_the_old_sort_limits(cuda):
+    """The embedding-gradient sort is a multi-CTA stable radix sort on 64-bit
+    (token, position) keys: one micro-batch of 40 x 1024 = 40960 tokens (> the
+    old single-CTA sort's 32768) over a 150000-token vocabulary (V * M > 2^32,
+    the old 32-bit key limit) gives the same full-dataset gradient as two
+    micro-batches of 20 sequences (which the old sort handled)."""
+    c = dict(vocab=150000, d_model=32, n_layer=1, n_head=1, seq_len=1024, n_samples=40, data_seed=5)
+    grads = []
+    for mb in (40, 20):
+        m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=mb))
+        th = torch.tensor(m.default_theta0(3)).to(torch.bfloat16).to(cuda)
+        g = torch.zeros(m.dim, device=cuda)
+        loss = C.c_double()
+        _lib.call("acco_model_value_and_grad", m.handle, C.c_void_p(th.data_ptr()), C.byref(loss),
+                  C.c_void_p(g.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        grads.append((g.double().cpu().numpy(), loss.value))
+        del m
+        torch.cuda.empty_cache()
+    (g1, l1), (g2, l2) = grads
+    # (fp32 accumulation orders differ: K = 40960 vs 2 x 20480 in the weight
+    # gradients; a mis-sorted or dropped token would be an O(1) error)
+    assert abs(l1 - l2) <= 1e-6 * abs(l2)
+    assert _rel(g1, g2) <= 1e-4
+    V, d = c["vocab"], c["d_model"]
+    assert _rel(g1[:V * d], g2[:V * d]) <= 1e-4  # the token-embedding rows themselves
