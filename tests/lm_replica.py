@@ -178,3 +178,158 @@ def loss_and_grad(cfg, theta, tokens, bf16=False, dtype=torch.float64):
     G["wpe"] = dx.view(B, T, d).sum(0)
     grad = torch.cat([G[n].reshape(-1) for n, _, _ in param_layout(cfg)])
     return loss_sum, grad
+
+
+# ----------------------------------------------------------------- Llama family
+def llama_param_layout(cfg):
+    """oracle/gpt_oracle.py param_layout, arch="llama": (name, shape, offset)."""
+    d, V, H = cfg["d_model"], cfg["vocab"], cfg["n_head"]
+    Hk = cfg.get("n_kv_head") or H
+    hd = d // H
+    F = cfg.get("d_ff") or 4 * d
+    specs = [("wte", (V, d))]
+    for l in range(cfg["n_layer"]):
+        p = f"layers.{l}."
+        specs += [(p + "attention_norm.weight", (d,)), (p + "attention.wqkv", ((H + 2 * Hk) * hd, d)),
+                  (p + "attention.wo", (d, H * hd)), (p + "ffn_norm.weight", (d,)),
+                  (p + "feed_forward.w_gate_up", (2 * F, d)), (p + "feed_forward.w_down", (d, F))]
+    specs += [("norm.weight", (d,)), ("output.weight", (V, d))]
+    out, off = [], 0
+    for n, s in specs:
+        out.append((n, s, off))
+        off += math.prod(s)
+    return out
+
+
+def llama_loss_and_grad(cfg, theta, tokens, bf16=False, dtype=torch.float64):
+    """The Llama block of oracle/gpt_oracle.py (_llama_loss_and_grad) — RMSNorm,
+    fused q|k|v with grouped-query attention, rotary embeddings (rotate-half),
+    SwiGLU with a fused gate|up projection, untied head — with the bf16
+    rounding points of model.cu run_llama in bf16 mode (the fused SwiGLU
+    epilogues: gate / up pre-activations and silu(gate) * up stored in bf16;
+    the down projection's dgrad rounded to bf16 before the dSwiGLU math;
+    RoPE applied to the bf16 q / k with the fp32 (cos, sin) table)."""
+    if bf16:
+        assert dtype == torch.float32
+
+        def R(x):
+            return x.to(torch.bfloat16).to(torch.float32)
+    else:
+        def R(x):
+            return x
+
+    dev = theta.device
+    V, d, L, H, T = cfg["vocab"], cfg["d_model"], cfg["n_layer"], cfg["n_head"], cfg["seq_len"]
+    Hk = cfg.get("n_kv_head") or H
+    F = cfg.get("d_ff") or 4 * d
+    base = cfg.get("rope_base") or 10000.0
+    hd = d // H
+    G_ = H // Hk
+    B = tokens.shape[0]
+    M = B * T
+    th = R(theta.to(dtype))
+    P = {n: th[o:o + math.prod(s)].view(s) for n, s, o in llama_param_layout(cfg)}
+    xi = tokens[:, :T].reshape(-1)
+    yt = tokens[:, 1:T + 1].reshape(-1)
+    scale = 1.0 / math.sqrt(hd)
+    mask = torch.triu(torch.ones(T, T, dtype=torch.bool, device=dev), 1)
+    i = torch.arange(hd // 2, dtype=torch.float64, device=dev)
+    ang = torch.arange(T, dtype=torch.float64, device=dev)[:, None] * (base ** (-2.0 * i / hd))[None, :]
+    cos, sin = torch.cos(ang), torch.sin(ang)
+    if bf16:  # the kernels read the fp64 angles' cos / sin rounded to fp32
+        cos, sin = cos.float(), sin.float()
+    cos, sin = cos.to(dtype), sin.to(dtype)
+
+    def rms(x, g):
+        rs = torch.rsqrt((x * x).mean(-1, keepdim=True) + LN_EPS)
+        xh = x * rs
+        return R(xh * g), (xh, rs)
+
+    def rms_bwd(dy, g, cache, prev=None):
+        xh, rs = cache
+        dxh = dy * g
+        dx = rs * (dxh - xh * (dxh * xh).mean(-1, keepdim=True))
+        if prev is not None:
+            dx = dx + prev
+        return R(dx), (dy * xh).sum(0)
+
+    def rope(t, inverse=False):  # t [B, nh, T, hd]
+        h2 = hd // 2
+        a, b = t[..., :h2], t[..., h2:]
+        if inverse:
+            return R(torch.cat([a * cos + b * sin, b * cos - a * sin], -1))
+        return R(torch.cat([a * cos - b * sin, b * cos + a * sin], -1))
+
+    def heads(t, n):  # [M, n*hd] -> [B, n, T, hd]
+        return t.view(B, T, n, hd).permute(0, 2, 1, 3)
+
+    def unheads(t):
+        return t.permute(0, 2, 1, 3).reshape(M, -1)
+
+    x = P["wte"][xi].clone()
+    caches = []
+    for l in range(L):
+        p = f"layers.{l}."
+        h1, c1 = rms(x, P[p + "attention_norm.weight"])
+        qkv = R(h1 @ P[p + "attention.wqkv"].t())
+        q = rope(heads(qkv[:, :H * hd], H))
+        k = rope(heads(qkv[:, H * hd:(H + Hk) * hd], Hk))
+        v = heads(qkv[:, (H + Hk) * hd:], Hk)
+        kr, vr = k.repeat_interleave(G_, dim=1), v.repeat_interleave(G_, dim=1)
+        s = (q @ kr.transpose(-1, -2)) * scale
+        s = s.masked_fill(mask, float("-inf"))
+        mx = s.amax(-1, keepdim=True)
+        e = torch.exp(s - mx)
+        lsum = e.sum(-1, keepdim=True)
+        y = R(unheads((R(e) @ vr) / lsum))
+        lse = mx + torch.log(lsum)
+        xm = R(y @ P[p + "attention.wo"].t() + x)
+        h2, c2 = rms(xm, P[p + "ffn_norm.weight"])
+        gu = R(h2 @ P[p + "feed_forward.w_gate_up"].t())
+        g, u = gu[:, :F], gu[:, F:]
+        sg = torch.sigmoid(g)
+        a = R(g * sg * u)
+        x_next = R(a @ P[p + "feed_forward.w_down"].t() + xm)
+        caches.append((h1, c1, q, kr, vr, s, lse, y, xm, h2, c2, g, u, sg, a))
+        x = x_next
+    hf, cf = rms(x, P["norm.weight"])
+    logits = R(hf @ P["output.weight"].t())
+    lse_v = torch.logsumexp(logits, -1)
+    loss_sum = (lse_v - logits.gather(1, yt[:, None])[:, 0]).sum() / T
+    dlog = torch.exp(logits - lse_v[:, None])
+    dlog[torch.arange(M, device=dev), yt] -= 1.0
+    dlog = R(dlog / T)
+
+    Gd = {}
+    Gd["output.weight"] = dlog.t() @ hf
+    dt = R(dlog @ P["output.weight"])
+    dx, Gd["norm.weight"] = rms_bwd(dt, P["norm.weight"], cf)
+    for l in reversed(range(L)):
+        p = f"layers.{l}."
+        h1, c1, q, kr, vr, s, lse, y, xm, h2, c2, g, u, sg, a = caches[l]
+        Gd[p + "feed_forward.w_down"] = dx.t() @ a
+        dd = R(dx @ P[p + "feed_forward.w_down"])
+        dgu = torch.cat([R(dd * u * sg * (1.0 + g * (1.0 - sg))), R(dd * g * sg)], -1)
+        Gd[p + "feed_forward.w_gate_up"] = dgu.t() @ h2
+        dt = R(dgu @ P[p + "feed_forward.w_gate_up"])
+        dx, Gd[p + "ffn_norm.weight"] = rms_bwd(dt, P[p + "ffn_norm.weight"], c2, prev=dx)
+        Gd[p + "attention.wo"] = dx.t() @ y
+        dy = R(dx @ P[p + "attention.wo"])
+        dyh = heads(dy, H)
+        Dsum = (dyh * heads(y, H)).sum(-1, keepdim=True)
+        pr = torch.exp(s - lse)
+        dp = dyh @ vr.transpose(-1, -2)
+        ds = pr * (dp - Dsum)
+        dvr = R(pr).transpose(-1, -2) @ dyh
+        dkr = scale * (R(ds).transpose(-1, -2) @ q)
+        dq = R(scale * (R(ds) @ kr))
+        dk = R(dkr.view(B, Hk, G_, T, hd).sum(2))  # the group's query heads fold into their KV head
+        dv = R(dvr.view(B, Hk, G_, T, hd).sum(2))
+        dq, dk = rope(dq, inverse=True), rope(dk, inverse=True)
+        dqkv = torch.cat([unheads(dq), unheads(dk), unheads(dv)], -1)
+        Gd[p + "attention.wqkv"] = dqkv.t() @ h1
+        dt = R(dqkv @ P[p + "attention.wqkv"])
+        dx, Gd[p + "attention_norm.weight"] = rms_bwd(dt, P[p + "attention_norm.weight"], c1, prev=dx)
+    Gd["wte"] = torch.zeros_like(P["wte"]).index_add(0, xi, dx)
+    grad = torch.cat([Gd[n].reshape(-1) for n, _, _ in llama_param_layout(cfg)])
+    return loss_sum, grad

@@ -18,6 +18,10 @@ pinned to the numpy oracle (oracle/gpt_oracle.py) at these exact shapes with
 one sequence (test_replica_is_oracle_at_bench_shape) and at small shapes on
 CPU (tests/test_lm_replica.py).
 
+test_llama_bench_shapes_bf16_and_fp32 does the same at config 4's shapes
+(Llama-1B: d = 2048, GQA 32 / 4 heads, SwiGLU 5632, V = 32000, T = 2048,
+B = 4; L = 2) against the Llama replica (lm_replica.llama_loss_and_grad).
+
 test_reduced_width_loss_curve is BASELINE.json config 2's "loss-curve parity
 vs CPU oracle at reduced width": d = 64, L = 12, V = 50257, T = 1024, 20 ACCO
 updates on the GPU engine vs oracle.run_acco (the protocol restatement pinned
@@ -196,3 +200,68 @@ def test_reduced_width_loss_curve(cuda, precision):
             assert abs(r.loss - o.loss) <= 1e-2 * abs(o.loss), (t, r.loss, o.loss)
     print(precision, "loss curve", [round(r.loss, 5) for r in tr.records])
     assert tr.records[-1].loss < tr.records[0].loss
+
+
+# BASELINE.json config 4 (bench.py --model llama-1b): d = 2048, 32 query / 4 KV
+# heads of 64, SwiGLU 5632, V = 32000, T = 2048, B = 4 — at L = 2
+LLAMA1B = dict(vocab=32000, d_model=2048, n_layer=2, n_head=32, seq_len=2048, n_samples=16, data_seed=1,
+               arch="llama", n_kv_head=4, d_ff=5632)
+LB = 4
+
+
+def _llama_case(cuda):
+    gc = G.GPTConfig(**LLAMA1B)
+    rng = np.random.default_rng(11)
+    th = (G.default_theta0(gc, 1) + 0.02 * rng.standard_normal(G.param_count(gc))).astype(np.float32)
+    seed = O.derive(1, 0, 0, 2, 0)
+    idx = O.sample_indices(seed, LB, gc.n_samples)
+    tok = torch.tensor(G.dataset(gc)[idx], device=cuda)
+    return th, seed, tok
+
+
+def _per_tensor_llama(g, ref):
+    return {name: _rel(g[off:off + int(np.prod(shape))], ref[off:off + int(np.prod(shape))])
+            for name, shape, off in lm_replica.llama_param_layout(LLAMA1B)}
+
+
+def test_llama_bench_shapes_bf16_and_fp32(cuda):
+    """Config 4's compute path at its shapes: the bf16 tcgen05 path (fused
+    SwiGLU / dSwiGLU epilogues, GQA attention, RoPE, wide-row RMSNorm backward)
+    against the bf16-matched replica and fp64; the fp32 path against fp64."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    th, seed, tok = _llama_case(cuda)
+    m = api.Model(api.LMConfig(**LLAMA1B, precision="bf16", max_batch=LB))
+    th_bf = torch.tensor(th).to(torch.bfloat16).to(cuda)
+    g, loss_sum, names = _kernel_grad(m, th_bf, seed, LB, cuda)
+    for k in ("fa_fwd_tc2", "fa_bwd_dkv_tc", "fa_bwd_dq_tc", "rope_vec_kernel", "ln_bwd_wide",
+              "gemm_tc_kernel<256, 3, 0, 0, 0>"):
+        assert any(k in n for n in names), (k, sorted(names))
+    del m
+    l16, g16 = lm_replica.llama_loss_and_grad(LLAMA1B, th_bf.float(), tok, bf16=True, dtype=torch.float32)
+    l64, g64 = lm_replica.llama_loss_and_grad(LLAMA1B, th_bf.double(), tok)
+    per16, per64, rep64 = _per_tensor_llama(g, g16), _per_tensor_llama(g, g64), _per_tensor_llama(g16, g64)
+    for name in per16:
+        print(f"{name:34s} kernel vs bf16 replica {per16[name]:.2e}   kernel vs fp64 {per64[name]:.2e}   "
+              f"replica vs fp64 {rep64[name]:.2e}")
+    print("loss", loss_sum, l16.item(), l64.item())
+    assert abs(loss_sum - l16.item()) <= 2e-3 * abs(l16.item())
+    # d = 2048 and T = 2048 chains carry more bf16 rounding than GPT-2 small:
+    # the replica itself sits 1.6-2.9e-2 from fp64 per tensor (measured), so
+    # the kernel-vs-replica bound is 3e-2 here; the decisive check is the
+    # next one — the kernel's fp64 error is the bf16-storage error (measured
+    # ratio 1.00-1.02), nothing on top
+    assert not {k: v for k, v in per16.items() if not v <= 3e-2}
+    assert not {k: (per64[k], rep64[k]) for k in per64 if not per64[k] <= 1.5 * rep64[k] + 1e-3}
+    del g16, g64
+    torch.cuda.empty_cache()
+    # fp32 parity path (3xTF32 GEMMs) at the same shapes
+    m = api.Model(api.LMConfig(**LLAMA1B, precision="fp32", max_batch=LB))
+    pt = torch.tensor(th, device=cuda)
+    g, loss_sum, _ = _kernel_grad(m, pt, seed, LB, cuda)
+    del m
+    l64, g64 = lm_replica.llama_loss_and_grad(LLAMA1B, pt.double(), tok)
+    per = _per_tensor_llama(g, g64)
+    print("fp32 overall", _rel(g, g64), "worst", max(per.values()), "loss", loss_sum, l64.item())
+    assert abs(loss_sum - l64.item()) <= 1e-6 * abs(l64.item())
+    assert _rel(g, g64) <= 1e-5
+    assert not {k: v for k, v in per.items() if not v <= 1e-5}

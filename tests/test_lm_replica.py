@@ -49,3 +49,29 @@ def test_replica_bf16_mode_near_fp64():
     l16, g16 = lm_replica.loss_and_grad(c, th_bf.float(), tok, bf16=True, dtype=torch.float32)
     assert abs(l16.item() - l64.item()) <= 1e-2 * abs(l64.item())
     assert _rel(g16.double().numpy(), g64.numpy()) <= 5e-2
+
+
+LLAMA = dict(vocab=96, d_model=64, n_layer=2, n_head=4, seq_len=24, n_samples=16, data_seed=2, arch="llama",
+             n_kv_head=2, d_ff=96)
+
+
+def test_llama_replica_fp64_is_the_oracle():
+    gc = G.GPTConfig(**LLAMA)
+    rng = np.random.default_rng(5)
+    th = G.default_theta0(gc, 4) + 0.03 * rng.standard_normal(G.param_count(gc))
+    tok = G.dataset(gc)[:3]
+    ol, og = G.loss_and_grad(gc, th, tok)
+    rl, rg = lm_replica.llama_loss_and_grad(LLAMA, torch.tensor(th), torch.tensor(tok))
+    assert abs(rl.item() / 3 - ol) <= 1e-12 * abs(ol)
+    assert _rel(rg.numpy() / 3, og) <= 1e-10
+    assert [(n, s, o) for n, s, _, o in G.param_layout(gc)] == lm_replica.llama_param_layout(LLAMA)
+
+
+def test_llama_replica_bf16_mode_near_fp64():
+    gc = G.GPTConfig(**LLAMA)
+    th_bf = torch.tensor(G.default_theta0(gc, 1)).to(torch.bfloat16).double()
+    tok = torch.tensor(G.dataset(gc)[:4])
+    l64, g64 = lm_replica.llama_loss_and_grad(LLAMA, th_bf, tok)
+    l16, g16 = lm_replica.llama_loss_and_grad(LLAMA, th_bf.float(), tok, bf16=True, dtype=torch.float32)
+    assert abs(l16.item() - l64.item()) <= 1e-2 * abs(l64.item())
+    assert _rel(g16.double().numpy(), g64.numpy()) <= 5e-2
