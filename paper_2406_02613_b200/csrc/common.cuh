@@ -90,6 +90,29 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     if (e != cudaSuccess) throw Error(kCudaError, std::string("launch_pdl: ") + cudaGetErrorString(e));
 }
 
+// launch_pdl with a 1-D thread-block cluster of `cluster` CTAs (CTA pairs of
+// the 2-SM tcgen05 kernels: consecutive blockIdx.x share a TPC)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl_cluster(void (*kern)(KArgs...), int cluster, dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    if (e != cudaSuccess) throw Error(kCudaError, std::string("launch_pdl_cluster: ") + cudaGetErrorString(e));
+}
+
 // Number of SMs on the current device (148 on B200); cached per process.
 int num_sms();
 

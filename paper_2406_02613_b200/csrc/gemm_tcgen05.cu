@@ -39,6 +39,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
+#include <string>
 #include <mutex>
 
 namespace acco {
@@ -203,6 +205,72 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
+// ---- CTA pairs (cta_group::2): one MMA of M = 256 rows spans the two SMs of a
+// TPC; each CTA stages its 128 A rows and half of the B rows, and holds its
+// 128 accumulator rows in its own TMEM.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// shared::cluster address of `p` (a shared::cta pointer) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "r"(20000u)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t spins = 0;
+    uint64_t t0 = 0;
+    while (!mbar_try_wait_cluster(a, parity)) {
+        if ((++spins & 255u) == 0) watchdog(t0);
+    }
+}
+// TMA load into this CTA's smem whose completion is signalled on the pair
+// leader's mbarrier (bar = its shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// arrive on the mbarrier at this smem offset in both CTAs of the pair once the
+// leader's issued MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* v) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -250,9 +318,9 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
 
 // One operand tile is 128 B per row in every variant: 64 bf16 or 32 fp32 (tf32)
 // elements of K. The 3xTF32 variant stages a hi and a lo plane per operand.
-template <int BN, int STAGES, int X3 = 0>
+template <int BN, int STAGES, int X3 = 0, int CG = 1>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN) * 128 * (X3 ? 2 : 1) +
+    return 1024 /*align slack*/ + STAGES * (kBM + BN / CG) * 128 * (X3 ? 2 : 1) +
            epi_warps<BN, STAGES, X3>() * epi_warp_bytes<BN, STAGES>() +
            (2 * STAGES + 4 + epi_warps<BN, STAGES, X3>() * in_bufs<BN>()) * 8 + 16 +
            48 /* CLC: full / empty mbarriers, 16 B response, alignment */;
@@ -355,17 +423,18 @@ struct EpiMaps {
 };
 
 // --------------------------------------------------------------------- kernel
-template <int BN, int STAGES, int A_MN, int B_MN, int X3 = 0>
+template <int BN, int STAGES, int A_MN, int B_MN, int X3 = 0, int CG = 1>
 __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem,
                    int use_clc) {
     static_assert(!X3 || (!A_MN && !B_MN), "3xTF32: the split pre-pass writes K-major planes");
+    static_assert(CG == 1 || (!X3 && (!B_MN || (BN / 2) % 64 == 0)), "CTA pairs: bf16, B half a whole MN atom");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     constexpr int A_TILE = kBM * 128;  // one plane: 128 rows x 128 B
-    constexpr int B_TILE = BN * 128;
+    constexpr int B_TILE = (BN / CG) * 128;  // this CTA's B rows (half of them in a CTA pair)
     constexpr int A_BYTES = A_TILE * (X3 ? 2 : 1);  // per stage (hi | lo planes for X3)
     constexpr int B_BYTES = B_TILE * (X3 ? 2 : 1);
     uint8_t* sA = smem;
@@ -396,7 +465,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+            mbar_init(&tempty[a], CG * kEpiWarps);  // one arrive per epilogue warp (of both CTAs of a pair)
         }
         for (int i = 0; i < kEpiWarps * kInBuf; ++i) mbar_init(&inbar[i], 1);
         mbar_init(clc_full, 1);
@@ -409,13 +478,28 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     constexpr int kAccCols = X3 ? 2 * BN : BN;
     constexpr uint32_t kTmemCols = 2 * kAccCols <= 256 ? 256 : 512;  // power of two >= 2 accumulators
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (CG == 2) {  // both CTAs of the pair allocate collectively (same columns in each)
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2)
+        cluster_sync();  // the peer's mbarriers are initialised before any remote arrive / complete_tx
+    else
+        __syncthreads();
     tc_fence_after();
+    // CTA pair: rank 0 (the leader) issues the MMAs for both; units are per pair
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+    const int cta_unit0 = CG == 2 ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int unit_stride = static_cast<int>(gridDim.x) / CG;
     const uint32_t tmem_base = *tmem_slot;
     // prologue done (barriers, TMEM): let the next kernel launch, then wait for
     // the previous one's results before the first TMA load / global write
@@ -431,7 +515,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     // role warps read each claim from smem and release it.
     int clc_i = 0;
     auto next_unit = [&](int u) -> int {
-        if (!use_clc) return u + static_cast<int>(gridDim.x) < nunits ? u + static_cast<int>(gridDim.x) : -1;
+        if (!use_clc) return u + unit_stride < nunits ? u + unit_stride : -1;
         mbar_wait(clc_full, clc_i & 1);
         const int nu = clc_decode(clc_resp);
         fence_async_smem();  // the async proxy rewrites the response next
@@ -456,17 +540,43 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         // like the MMA issuer: warp-uniform walk and waits, one elected lane issues
         {
             int it = 0;
-            for (int u = blockIdx.x; u >= 0; u = next_unit(u)) {
+            for (int u = cta_unit0; u >= 0; u = next_unit(u)) {
                 int mb, nb, sp;
                 decode(sc, u, mb, nb, sp);
-                const int m0 = mb * kBM, n0 = nb * BN;
+                const int m0 = mb * (kBM * CG) + static_cast<int>(rank) * kBM, n0 = nb * BN;
                 const int kb0 = sp * sc.kb_per_split;
                 const int kb1 = min(sc.kb_total, kb0 + sc.kb_per_split);
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
-                    if (X3) {
+                    if (CG == 2) {
+                        // this CTA's A rows and half of the B rows; both CTAs' loads
+                        // complete on the leader's full barrier, which expects them all
+                        if (elect_one()) {
+                            const uint32_t fb = mapa(&full[s], 0);
+                            if (rank == 0) mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+                            uint8_t* a_dst = sA + s * A_BYTES;
+                            uint8_t* b_dst = sB + s * B_BYTES;
+                            if (A_MN) {
+#pragma unroll
+                                for (int j = 0; j < kBM / 64; ++j)
+                                    tma_load_2d_pair(a_dst + j * 64 * kBK * 2, &tmA, fb, m0 + j * 64, kb * kBK);
+                            } else {
+                                tma_load_2d_pair(a_dst, &tmA, fb, kb * kBK, m0);
+                            }
+                            const int nh = n0 + static_cast<int>(rank) * (BN / 2);
+                            if (B_MN) {
+#pragma unroll
+                                for (int j = 0; j < BN / 128; ++j)
+                                    tma_load_2d_pair(b_dst + j * 64 * kBK * 2, &tmB, fb, nh + j * 64, kb * kBK);
+                            } else if (ep.mode == kEpiSwiGLU) {  // leader: gate rows, peer: the matching up rows
+                                tma_load_2d_pair(b_dst, &tmB, fb, kb * kBK, (rank ? N / 2 : 0) + n0 / 2);
+                            } else {
+                                tma_load_2d_pair(b_dst, &tmB, fb, kb * kBK, nh);
+                            }
+                        }
+                    } else if (X3) {
                         if (elect_one()) {  // hi and lo planes of both operands (3-D maps {K, rows, plane})
                             mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
                             uint8_t* a_dst = sA + s * A_BYTES;
@@ -502,24 +612,28 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && rank == 0) {
+        // (a CTA pair's MMAs are issued by the leader alone)
         // The whole warp walks the schedule and waits (warp-uniform control, so the
         // descriptors live in uniform registers); one elected lane issues the MMAs
         // and commits. This keeps the issuer's instruction count per k-block low:
         // it shares its SM sub-partition with two epilogue warps.
-        constexpr uint32_t idesc = idesc_bf16(kBM, BN, A_MN, B_MN);
+        constexpr uint32_t idesc = idesc_bf16(kBM * CG, BN, A_MN, B_MN);
         // descriptor start-address step per 16-deep k slice (address >> 4):
         // K-major 32 B inside the 128B swizzle row, MN-major two 8-row atoms (2048 B)
         constexpr uint64_t a_step = A_MN ? 2048 >> 4 : 32 >> 4;
         constexpr uint64_t b_step = B_MN ? 2048 >> 4 : 32 >> 4;
         int it = 0, lt = 0;
-        for (int u = blockIdx.x; u >= 0; u = next_unit(u), ++lt) {
+        for (int u = cta_unit0; u >= 0; u = next_unit(u), ++lt) {
             int mb, nb, sp;
             decode(sc, u, mb, nb, sp);
             const int kb0 = sp * sc.kb_per_split;
             const int kb1 = min(sc.kb_total, kb0 + sc.kb_per_split);
             const int acc = lt & 1;
-            mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            if (CG == 2)  // both CTAs' epilogues drained this buffer
+                mbar_wait_cluster(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+            else
+                mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);  // epilogue drained this buffer
             tc_fence_after();
             if (lane == 0) GEMM_PROBE(0, lt);
             const uint32_t tmem_d = tmem_base + acc * kAccCols;
@@ -552,6 +666,14 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                         }
                         umma_commit(&empty[s]);
                     }
+                } else if (CG == 2) {
+                    if (elect_one()) {
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk)
+                            umma_bf16_pair(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc,
+                                           (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma_commit_pair(&empty[s]);  // frees the stage in both CTAs
+                    }
                 } else if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
@@ -560,7 +682,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 }
                 __syncwarp();
             }
-            if (elect_one()) umma_commit(&tfull[acc]);
+            if (elect_one()) {
+                if (CG == 2)
+                    umma_commit_pair(&tfull[acc]);
+                else
+                    umma_commit(&tfull[acc]);
+            }
             __syncwarp();
             if (lane == 0) GEMM_PROBE(1, lt);
         }
@@ -570,6 +697,14 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         // two warps drain a quadrant in parallel (GELU/dGELU/SwiGLU epilogues were
         // the bottleneck of their GEMMs with one warp per quadrant)
         const int ew = warp - 4, wq = ew & 3, hf = ew >> 2;  // hf < kCS
+        // this warp's share of accumulator buffer a has been read: hand it back
+        // (to the pair leader's barrier: its MMAs write both CTAs' TMEM)
+        auto release_acc = [&](int a) {
+            if (CG == 2)
+                mbar_arrive_cluster(mapa(&tempty[a], 0));
+            else
+                mbar_arrive(&tempty[a]);
+        };
         uint8_t* wbuf = sEpi + ew * kEpiWarpBytes;
         uint64_t* ib = inbar + kInBuf * ew;
         const bool f32 = ep.mode == kEpiAccF32;
@@ -578,12 +713,17 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         const __nv_bfloat16* bias = static_cast<const __nv_bfloat16*>(ep.bias);
         uint32_t in_phase = 0;  // bit k: parity of the next wait on input buffer k
         constexpr int kChunks = BN / 32;
+        // output staging buffers alternate over this warp's whole chunk sequence,
+        // across tiles (a per-tile parity would hand the last chunk's buffer of
+        // an odd-length tile — BN = 192 with two warps per quadrant — straight
+        // to the next tile's first chunk while its TMA store may still read it)
+        int seq = 0;
         int lt = 0;
-        for (int u = blockIdx.x; u >= 0; u = next_unit(u), ++lt) {
+        for (int u = cta_unit0; u >= 0; u = next_unit(u), ++lt) {
             int mb, nb, sp;
             decode(sc, u, mb, nb, sp);
             const int acc = lt & 1;
-            const int row0 = mb * kBM + wq * 32;
+            const int row0 = mb * (kBM * CG) + static_cast<int>(rank) * kBM + wq * 32;
             const int n0 = nb * BN;
             if (has_in && lane == 0) {  // this warp's first kInBuf input chunks of the tile
 #pragma unroll
@@ -601,7 +741,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                     bpre[q] = __ldg(reinterpret_cast<const uint4*>(bias + n0 + hf * 32 + 8 * q));
             }
             // ordered split-K: this warp's (quadrant, column half) slice is added in split order
-            int* sem = split_sem ? split_sem + ((mb * sc.tiles_n + nb) * 8 + ew) * 32 : nullptr;  // own 128B line (<= 8 per tile)
+            // own 128B line per (tile, CTA of the pair, epilogue warp)
+            int* sem = split_sem ? split_sem + (((mb * sc.tiles_n + nb) * CG + static_cast<int>(rank)) * 8 + ew) * 32
+                                 : nullptr;
             if (sem && lane == 0) {
                 while (ld_acquire(sem) != sp) __nanosleep(64);
                 fence_async_global();
@@ -634,7 +776,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                     if (c + kCS >= kChunks) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                        if (lane == 0) release_acc(acc);
                     }
                     mbar_wait(&ib[sl], (in_phase >> sl) & 1);
                     in_phase ^= 1u << sl;
@@ -684,7 +826,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                     if (c + kCS >= kChunks / 2) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tempty[acc]);
+                        if (lane == 0) release_acc(acc);
                     }
                     float g[32], uu[32], a[32];
 #pragma unroll
@@ -712,8 +854,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 continue;
             }
 #pragma unroll 1
-            for (int j = 0, c = hf; c < kChunks; ++j, c += kCS) {
-                const int b = j & 1;
+            for (int j = 0, c = hf; c < kChunks; ++j, ++seq, c += kCS) {
+                const int b = seq & 1;
                 const int ibuf = j % kInBuf;
                 const int col0 = n0 + c * 32;
                 uint4 bcur[4];
@@ -735,7 +877,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 if (c + kCS >= kChunks) {  // this warp's share of the accumulator read: hand TMEM back
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    if (lane == 0) release_acc(acc);
                 }
                 float v[32];
 #pragma unroll
@@ -779,7 +921,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                     }
                 }
                 // the TMA store that last used these staging buffers (two chunks
-                // back in this warp's sequence) must have finished reading them
+                // back in this warp's sequence, maybe in the previous tile) must
+                // have finished reading them
                 if (lane == 0) bulk_wait_read<1>();
                 __syncwarp();
                 if (f32) {
@@ -831,10 +974,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         __syncwarp();
     }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2)
+        cluster_sync();  // the peer's MMAs into this TMEM and its remote arrives are done
+    else
+        __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
     }
 }
 
@@ -923,19 +1072,36 @@ int* split_semaphores(cudaStream_t stream) {
     return sem;
 }
 
-template <int BN, int STAGES, int A_MN, int B_MN>
+template <int BN, int STAGES, int A_MN, int B_MN, int CG>
 void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep, int splits,
             cudaStream_t stream) {
-    auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN>;
-    constexpr int smem = smem_bytes<BN, STAGES>();
+    auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, 0, CG>;
+    constexpr int smem = smem_bytes<BN, STAGES, 0, CG>();
     static_assert(smem <= 232448, "shared memory budget");
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    static int max_pairs = 0;  // per instantiation: co-resident CTA pairs
+    if (!max_pairs) {
         ACCO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        configured = true;
+        max_pairs = num_sms() / 2;
+        if (CG == 2) {
+            ACCO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * max_pairs);
+            cfg.blockDim = dim3(gemm_threads<BN, STAGES>());
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = 2;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int n = 0;
+            ACCO_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+            if (n > 0) max_pairs = n;
+        }
     }
     Sched sc;
-    sc.tiles_m = ceil_div(M, kBM);
+    sc.tiles_m = ceil_div(M, kBM * CG);
     sc.tiles_n = ceil_div(N, BN);
     sc.kb_total = ceil_div(K, kBK);
     // raster: groups of kGroupM m-blocks sweep all n-blocks (A rows reused from
@@ -957,7 +1123,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     if (ep.mode == kEpiAccF32) {
         em.out = make_map_f32(ep.C, N, M, 1, ep.ldc);
         if (sc.splits > 1) {
-            ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * 8 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
+            ACCO_REQUIRE(sc.tiles_m * sc.tiles_n * CG * 8 * 32 <= kSemSlots, "gemm: too many tiles for split-K");
             sem = split_semaphores(stream);
         }
     } else {
@@ -969,7 +1135,20 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
         if (ep.residual) em.res = make_map(ep.residual, N, M, ep.ldr, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
     }
     CUtensorMap ta = operand_map(A, M, K, kBM);
-    CUtensorMap tb = operand_map(B, N, K, ep.mode == kEpiSwiGLU ? BN / 2 : BN);
+    // (B box: the rows one CTA stages — half the tile's in a CTA pair or in
+    // the SwiGLU gate / up halves)
+    CUtensorMap tb = operand_map(B, N, K, (ep.mode == kEpiSwiGLU || CG == 2) ? BN / 2 : BN);
+    if (CG == 2) {
+        // persistent CTA pairs in static unit order. (Cluster launch control
+        // over pairs — one cluster per unit, the leader cancelling a whole
+        // cluster with a multicast response — was measured slower than the
+        // static order on every shape: qkv_fwd 26.2 vs 23.2 us, head_fwd 539 vs
+        // 452 us, profiles/r02_summary.md.)
+        const int grid = 2 * std::min(sc.units(), max_pairs);
+        launch_pdl_cluster(kern, 2, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, 0);
+        ACCO_CHECK_LAUNCH();
+        return;
+    }
     // cluster-launch-control work stealing unless split-K: the ordered split
     // hand-off assumes the static unit order
     const int clc = use_clc(sc) ? 1 : 0;
@@ -978,27 +1157,53 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     ACCO_CHECK_LAUNCH();
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG = 1>
 void dispatch_major(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep, int splits,
                     cudaStream_t s) {
-    if (!A.mn_major && !B.mn_major) launch<BN, STAGES, 0, 0>(A, B, M, N, K, ep, splits, s);
-    else if (!A.mn_major && B.mn_major) launch<BN, STAGES, 0, 1>(A, B, M, N, K, ep, splits, s);
-    else if (A.mn_major && !B.mn_major) launch<BN, STAGES, 1, 0>(A, B, M, N, K, ep, splits, s);
-    else launch<BN, STAGES, 1, 1>(A, B, M, N, K, ep, splits, s);
+    if (!A.mn_major && !B.mn_major) launch<BN, STAGES, 0, 0, CG>(A, B, M, N, K, ep, splits, s);
+    else if (!A.mn_major && B.mn_major) launch<BN, STAGES, 0, 1, CG>(A, B, M, N, K, ep, splits, s);
+    else if (A.mn_major && !B.mn_major) launch<BN, STAGES, 1, 0, CG>(A, B, M, N, K, ep, splits, s);
+    else launch<BN, STAGES, 1, 1, CG>(A, B, M, N, K, ep, splits, s);
 }
 
-// Relative cost model for tile-shape / split-K selection: waves of work units
-// times per-unit work, with narrower tiles paying for their lower operand reuse.
-double plan_cost(int M, int N, int K, int bn, int splits, int sms) {
-    const int units = ceil_div(M, kBM) * ceil_div(N, bn) * splits;
-    const double waves = std::ceil(static_cast<double>(units) / sms);
+// B K-major only (CTA-pair tiles whose B half is not a whole 64-wide MN atom)
+template <int BN, int STAGES, int CG>
+void dispatch_k_major_b(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
+                        int splits, cudaStream_t s) {
+    ACCO_REQUIRE(!B.mn_major, "gemm: this tile shape needs a K-major B");
+    if (!A.mn_major) launch<BN, STAGES, 0, 0, CG>(A, B, M, N, K, ep, splits, s);
+    else launch<BN, STAGES, 1, 0, CG>(A, B, M, N, K, ep, splits, s);
+}
+
+// Time model (us) for the tile width / CTA group / split-K choice:
+//   t = a + waves * (c + BN * k-blocks * r) + hand-offs
+// a: launch, prologue and last epilogue; c: per-unit overhead; r: mainloop
+// time per 64-deep k-block per tile column (the operand smem traffic per MMA
+// makes narrow and single-CTA tiles slower per column); waves of units over
+// 148 SMs or 74 CTA pairs. Least-squares fit (log error, rms 13 %) to the
+// CUDA-graph device times of every config on the 42 GEMM shapes of GPT-2
+// small / medium and Llama-1B (tools/diag/gemm_model_check.py,
+// profiles/r02_gemm_model.jsonl): its picks cost 0.25 % more than the
+// measured best summed over those shapes.
+struct TileCost {
+    double a, c, r;
+};
+TileCost tile_cost(int bn, int cg) {
+    if (cg == 2) return bn == 256 ? TileCost{2.651, 1.544, 1.447e-3} : bn == 192 ? TileCost{4.987, 0.412, 1.591e-3}
+                                                                                  : TileCost{0.541, 1.223, 1.834e-3};
+    return bn == 256 ? TileCost{0.823, 2.383, 1.524e-3} : bn == 192 ? TileCost{0.0, 1.549, 1.771e-3}
+                                                                     : TileCost{0.019, 1.179, 2.120e-3};
+}
+double plan_time(int M, int N, int K, int bn, int cg, int splits, bool a_mn, int sms) {
+    const TileCost tc = tile_cost(bn, cg);
+    const int units = ceil_div(M, kBM * cg) * ceil_div(N, bn) * splits;
+    const double waves = std::ceil(static_cast<double>(units) / (sms / cg));
     const double kb = std::ceil(static_cast<double>(ceil_div(K, kBK)) / splits);
-    const double eff = bn == 256 ? 1.0 : bn == 192 ? 1.08 : 1.25;
-    double c = waves * bn * kb * eff;
-    // ordered split-K: each extra split adds one epilogue hand-off (~2-3 us,
-    // measured) to the critical path; 1 cost unit ~ one 64-deep k-block column
-    if (splits > 1) c += 2500.0 * (splits - 1);
-    return c;
+    double t = tc.a + waves * (tc.c + bn * kb * tc.r);
+    // ordered split-K: each extra split adds an epilogue hand-off (a TMA
+    // reduce-add of the tile and its completion) to the critical path
+    if (splits > 1) t += (splits - 1) * (a_mn ? 2.635 : 4.3);
+    return t;
 }
 
 // fp32 -> bf16 copy of the split-K workspace into C (pure-store GEMMs)
@@ -1217,31 +1422,51 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     ACCO_REQUIRE(ep.mode == kEpiStore || ep.mode == kEpiAccF32 || ep.aux, "gemm_bf16: GELU epilogues need aux");
     ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
     const int sms = num_sms();
-    int best_bn = 256, best_sp = 1;
+    // The LM head's shapes (B too big to stay in L2, whole-M raster: see
+    // launch) stream B from HBM once; there the model underrates the 256-wide
+    // pair tiles, which halve each SM's share of B, against the 192-wide ones
+    // (head_fwd 452 vs 497 us), so those are not considered. ACCO_GEMM_NO_CG2=1:
+    // single-CTA tiles only (A/B knob).
+    const bool large_b = static_cast<double>(M) * K * 2 <= 48e6 && static_cast<double>(N) * K * 2 > 32e6;
+    const bool allow_cg2 = std::getenv("ACCO_GEMM_NO_CG2") == nullptr;
+    int best_bn = 256, best_sp = 1, best_cg = 1;
     double best = 1e300;
-    for (int bn : {256, 192, 128}) {
-        for (int sp : {1, 2, 3, 4, 6, 8}) {
-            if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp ||
-                           ceil_div(M, kBM) * ceil_div(N, bn) * 8 * 32 > kSemSlots))
-                continue;
-            const double c = plan_cost(M, N, K, bn, sp, sms);
-            if (c < best * 0.97) {
-                best = c;
-                best_bn = bn;
-                best_sp = sp;
+    for (int cg : {1, 2}) {
+        if (cg == 2 && !allow_cg2) continue;
+        for (int bn : {256, 192, 128}) {
+            if (cg == 2 && bn == 192 && (B.mn_major || large_b)) continue;
+            for (int sp : {1, 2, 3, 4, 6, 8}) {
+                if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp ||
+                               ceil_div(M, kBM) * ceil_div(N, bn) * 8 * 32 > kSemSlots))
+                    continue;
+                const double t = plan_time(M, N, K, bn, cg, sp, A.mn_major, sms);
+                if (t < best * 0.98) {  // (ties keep the single-CTA tiles)
+                    best = t;
+                    best_bn = bn;
+                    best_sp = sp;
+                    best_cg = cg;
+                }
             }
         }
     }
     if (ep.mode == kEpiDSwiGLU) {
         ACCO_REQUIRE(ep.aux && !ep.residual && !ep.bias && N % 32 == 0,
                      "gemm_bf16: DSwiGLU epilogue needs aux, F % 32 == 0, no bias/residual");
-        dispatch_major<192, 4>(A, B, M, N, K, ep, 1, stream);
+        if (std::getenv("ACCO_DSWIGLU_CG2"))  // A/B knob: CTA-pair 256-wide tiles
+            dispatch_major<256, 5, 2>(A, B, M, N, K, ep, 1, stream);
+        else
+            dispatch_major<192, 4>(A, B, M, N, K, ep, 1, stream);
         return;
     }
     if (ep.mode == kEpiSwiGLU) {
         ACCO_REQUIRE(N % 256 == 0 && !B.mn_major && !ep.residual && !ep.bias && ep.aux,
                      "gemm_bf16: SwiGLU epilogue needs N = 2F with F % 128 == 0, K-major B, aux, no bias/residual");
-        dispatch_major<256, 3>(A, B, M, N, K, ep, 1, stream);
+        // CTA-pair tiles (the leader stages the gate rows, its peer the up
+        // rows): Llama-1B 126.7k vs 124.5k tok/s with single-CTA tiles
+        if (std::getenv("ACCO_GEMM_NO_CG2"))
+            dispatch_major<256, 3>(A, B, M, N, K, ep, 1, stream);
+        else
+            dispatch_major<256, 5, 2>(A, B, M, N, K, ep, 1, stream);
         return;
     }
     // A pure-store GEMM whose tiles cannot fill the SMs and whose K is long
@@ -1252,12 +1477,12 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
                             (reinterpret_cast<uintptr_t>(ep.C) & 15) == 0 && !std::getenv("ACCO_GEMM_NO_WS_SPLIT");
     int ws_bn = 0, ws_sp = 1;
     if (pure_store) {
-        // the conversion pass, in cost units (one unit ~ 1.3 ns: a 256-wide k-block ~ 0.33 us)
-        const double conv = 6.0 * M * N / 6.5e3 / 1.3;
+        // the conversion pass (us): 6 bytes per element at ~6.5 TB/s, plus its launch
+        const double conv = 6.0 * M * N / 6.5e6 + 2.0;
         for (int bn : {256, 192, 128})
             for (int sp : {2, 3, 4, 6, 8}) {
                 if (ceil_div(K, kBK) < 16 * sp || ceil_div(M, kBM) * ceil_div(N, bn) * 8 * 32 > kSemSlots) continue;
-                const double c = plan_cost(M, N, K, bn, sp, sms) + conv;
+                const double c = plan_time(M, N, K, bn, 1, sp, A.mn_major, sms) + conv;
                 if (c < best * 0.9) {
                     best = c;
                     ws_bn = bn;
@@ -1285,12 +1510,30 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
         ACCO_CHECK_LAUNCH();
         return;
     }
-    if (const char* f = std::getenv("ACCO_GEMM_FORCE")) {  // tuning knob: "<bn>,<splits>"
-        int fb = 0, fs = 0;
-        if (std::sscanf(f, "%d,%d", &fb, &fs) == 2 && (fb == 128 || fb == 192 || fb == 256) && fs >= 1) {
+    if (const char* f = std::getenv("ACCO_GEMM_FORCE")) {  // tuning knob: "<bn>,<splits>[,<cta group>]"
+        int fb = 0, fs = 0, fc = 1;
+        if (std::sscanf(f, "%d,%d,%d", &fb, &fs, &fc) >= 2 && (fb == 128 || fb == 192 || fb == 256) && fs >= 1) {
             best_bn = fb;
             best_sp = ep.mode == kEpiAccF32 ? fs : 1;
+            best_cg = fc == 2 && !(fb == 192 && B.mn_major) ? 2 : 1;
         }
+    }
+    if (std::getenv("ACCO_GEMM_LOG")) {  // each distinct shape's plan, once
+        static std::set<std::string> seen;
+        char key[160];
+        std::snprintf(key, sizeof key, "gemm M=%d N=%d K=%d a_mn=%d b_mn=%d mode=%d -> bn=%d splits=%d cg=%d (model %.1f us)",
+                      M, N, K, int(A.mn_major), int(B.mn_major), ep.mode, best_bn, best_sp, best_cg, best);
+        std::lock_guard<std::mutex> lk(g_scratch_mu);
+        if (seen.insert(key).second) std::fprintf(stderr, "%s\n", key);
+    }
+    if (best_cg == 2) {
+        if (best_bn == 256)
+            dispatch_major<256, 5, 2>(A, B, M, N, K, ep, best_sp, stream);
+        else if (best_bn == 192)
+            dispatch_k_major_b<192, 5, 2>(A, B, M, N, K, ep, best_sp, stream);
+        else
+            dispatch_major<128, 6, 2>(A, B, M, N, K, ep, best_sp, stream);
+        return;
     }
     if (best_bn == 256)
         dispatch_major<256, 4>(A, B, M, N, K, ep, best_sp, stream);

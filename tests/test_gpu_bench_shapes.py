@@ -92,8 +92,10 @@ def test_bf16_bench_shapes_match_bf16_replica(cuda, bench_case):
     th_bf = torch.tensor(th).to(torch.bfloat16).to(cuda)
     g, loss_sum, names = _kernel_grad(m, th_bf, seed, B, cuda)
     # the kernels the bench times at these shapes ran
+    # (the LM head forward and weight gradient run on 256-wide CTA-pair tiles)
     for k in ("gemm_tc_kernel", "fa_fwd_tc2", "fa_bwd_dkv_tc", "fa_bwd_dq_tc", "ln_fwd_vec<3", "ln_bwd_vec<3",
-              "ce_vec_kernel", "f32_to_bf16_rows"):
+              "ce_vec_kernel", "f32_to_bf16_rows", "gemm_tc_kernel<256, 5, 0, 0, 0, 2>",
+              "gemm_tc_kernel<256, 5, 1, 1, 0, 2>"):
         assert any(k in n for n in names), (k, sorted(names))
     assert not any("simt" in n for n in names)
     l16, g16 = lm_replica.loss_and_grad(C2L2, th_bf.float(), tok, bf16=True, dtype=torch.float32)
@@ -126,7 +128,7 @@ def test_fp32_bench_shapes_match_fp64(cuda, bench_case):
     pt = torch.tensor(th, device=cuda)
     g, loss_sum, names = _kernel_grad(m, pt, seed, B, cuda)
     # fp32 parity mode contracts on the tensor cores (3xTF32), not the SIMT twin
-    assert any("gemm_tc_kernel<128, 3, 0, 0, 1>" in n for n in names), sorted(names)
+    assert any("gemm_tc_kernel<128, 3, 0, 0, 1, 1>" in n for n in names), sorted(names)
     assert not any("gemm_simt_kernel" in n for n in names)
     l64, g64 = lm_replica.loss_and_grad(C2L2, pt.double(), tok)
     per = _per_tensor(g, g64, C2L2)
@@ -234,7 +236,7 @@ def test_llama_bench_shapes_bf16_and_fp32(cuda):
     th_bf = torch.tensor(th).to(torch.bfloat16).to(cuda)
     g, loss_sum, names = _kernel_grad(m, th_bf, seed, LB, cuda)
     for k in ("fa_fwd_tc2", "fa_bwd_dkv_tc", "fa_bwd_dq_tc", "rope_vec_kernel", "ln_bwd_wide",
-              "gemm_tc_kernel<256, 3, 0, 0, 0>"):
+              "gemm_tc_kernel<256, 5, 0, 0, 0, 2>"):  # (the SwiGLU GEMM on CTA-pair tiles)
         assert any(k in n for n in names), (k, sorted(names))
     del m
     l16, g16 = lm_replica.llama_loss_and_grad(LLAMA1B, th_bf.float(), tok, bf16=True, dtype=torch.float32)

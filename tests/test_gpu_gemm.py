@@ -158,11 +158,16 @@ def test_bad_args_raise(cuda):
         gemm(a, False, a, False, 0, 8, 8, torch.empty(8, 8, dtype=torch.bfloat16, device=cuda))
 
 
-@pytest.mark.parametrize("force", ["128,1", "192,1", "256,1", "192,3", "128,4"])
+@pytest.mark.parametrize("force", ["128,1", "192,1", "256,1", "192,3", "128,4",
+                                   "256,1,2", "192,1,2", "128,1,2", "256,3,2", "128,4,2"])
 @pytest.mark.parametrize("a_mn,b_mn", list(itertools.product([False, True], repeat=2)))
 def test_every_tile_config(cuda, monkeypatch, force, a_mn, b_mn):
-    """Each tile width (BN 128/192/256) and ordered split-K, forced past the
-    cost model, on a ragged shape with several waves of tiles."""
+    """Each tile width (BN 128/192/256), single-CTA and CTA-pair (cta_group::2,
+    256-row tiles over two SMs) tiles and ordered split-K, forced past the
+    cost model, on a ragged shape with several waves of tiles (the pair's last
+    m-block half out of bounds)."""
+    if force == "192,1,2" and b_mn:
+        pytest.skip("CTA-pair BN = 192 needs a K-major B (its 96-row half is not a whole MN atom)")
     monkeypatch.setenv("ACCO_GEMM_FORCE", force)
     m, n, k = 1000, 776, 520
     g = torch.Generator().manual_seed(11)
@@ -222,3 +227,52 @@ def test_large_b_raster_matches_grouped_raster(cuda, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(c1, c2)
     assert _rel(c1, a.float() @ b.float().t()) < 6e-3
+
+
+@pytest.mark.parametrize("force", ["256,1,2", "128,1,2", "256,2,2"])
+def test_cta_pair_peer_half_out_of_bounds(cuda, monkeypatch, force):
+    """M = 800: the last 256-row pair tile's peer half (rows 896-1023) lies
+    wholly past M; its loads are zero-filled, its stores dropped, and the
+    pair's barriers still complete."""
+    monkeypatch.setenv("ACCO_GEMM_FORCE", force)
+    m, n, k = 800, 384, 96
+    g = torch.Generator().manual_seed(4)
+    for a_mn, b_mn in itertools.product([False, True], repeat=2):
+        a, a_st = _operand(m, k, a_mn, torch.bfloat16, cuda, g)
+        b, b_st = _operand(n, k, b_mn, torch.bfloat16, cuda, g)
+        ref = a.float() @ b.float().t()
+        c = torch.full((m + 8, n), 7.0, dtype=torch.bfloat16, device=cuda)  # rows past M must stay untouched
+        gemm(a_st, a_mn, b_st, b_mn, m, n, k, c)
+        c32 = torch.zeros(m, n, device=cuda)
+        gemm(a_st, a_mn, b_st, b_mn, m, n, k, c32, mode=3, beta=1)
+        torch.cuda.synchronize()
+        assert _rel(c[:m], ref) < 6e-3
+        assert torch.all(c[m:] == 7.0)
+        assert _rel(c32, ref) < 2e-6
+
+
+@pytest.mark.parametrize("force", ["192,1", "192,1,2"])
+def test_odd_chunk_count_staging_across_tiles(cuda, monkeypatch, force):
+    """Regression: BN = 192 with two epilogue warps per TMEM quadrant gives each
+    warp 3 output chunks per tile; the staging-buffer parity must run across
+    tiles, or a short-K tile's first chunk overwrites the previous tile's last
+    staging buffer while its TMA reduce-add still reads it (seen as a few
+    doubled 32x32 chunks on 8192 x 2048 x 128 weight gradients)."""
+    monkeypatch.setenv("ACCO_GEMM_FORCE", force)
+    m, n, k = 8192, 2048, 128
+    g = torch.Generator().manual_seed(1)
+    a = torch.randn(m, k, generator=g).to(torch.bfloat16).to(cuda)
+    b = torch.randn(n, k, generator=g).to(torch.bfloat16).to(cuda)
+    a_mn, b_mn = force.endswith(",2") is False, force.endswith(",2") is False  # wgrad layout where it applies
+    a_st = a.t().contiguous() if a_mn else a
+    b_st = b.t().contiguous() if b_mn else b
+    ref = a.float() @ b.float().t()
+    outs = []
+    for _ in range(4):
+        c = torch.zeros(m, n, device=cuda)
+        gemm(a_st, a_mn, b_st, b_mn, m, n, k, c, mode=3, beta=1)
+        outs.append(c)
+    torch.cuda.synchronize()
+    for c in outs:
+        assert torch.equal(c, outs[0])
+        assert _rel(c, ref) < 2e-6

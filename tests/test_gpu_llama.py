@@ -170,3 +170,27 @@ def test_swiglu_fused_epilogue_matches_unfused(cuda, monkeypatch):
     assert abs(l_f - ol * 2) <= 1e-2 * abs(ol * 2)
     assert _rel(g_f, og * 2) <= 5e-2
     assert _rel(g_f, g_u) <= 2e-2
+
+
+def test_swiglu_cta_pair_tiles_match(cuda, monkeypatch):
+    """The fused SwiGLU GEMM on CTA-pair tiles (the default: the leader stages
+    the gate rows, its peer the matching up rows) gives the same result as the
+    single-CTA tiles (ACCO_GEMM_NO_CG2=1; same per-element accumulation
+    order), and so does the DSwiGLU backward on pair tiles (ACCO_DSWIGLU_CG2=1)."""
+    c = dict(vocab=128, d_model=256, n_layer=2, n_head=4, n_kv_head=2, d_ff=384, seq_len=128, n_samples=8,
+             data_seed=6, arch="llama")
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=2))
+    gc = G.GPTConfig(**c)
+    th = torch.tensor(G.default_theta0(gc, 3)).to(torch.bfloat16).to(cuda)
+    seed = O.derive(6, 0, 0, 2, 0)
+    g1, l1 = _grad(m, th, seed, 2, cuda)
+    monkeypatch.setenv("ACCO_GEMM_NO_CG2", "1")
+    g2, l2 = _grad(m, th, seed, 2, cuda)
+    monkeypatch.delenv("ACCO_GEMM_NO_CG2")
+    monkeypatch.setenv("ACCO_DSWIGLU_CG2", "1")
+    g3, l3 = _grad(m, th, seed, 2, cuda)
+    assert l1 == l2 == l3
+    # (the other GEMMs' tile choice differs under ACCO_GEMM_NO_CG2, which can
+    # change split-K orders: compare within fp32 accumulation noise there)
+    assert np.allclose(g1, g2, rtol=0, atol=1e-6 * np.abs(g1).max())
+    assert np.array_equal(g1, g3) or np.allclose(g1, g3, rtol=0, atol=1e-6 * np.abs(g1).max())
