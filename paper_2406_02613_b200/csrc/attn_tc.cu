@@ -907,7 +907,7 @@ constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P /
 // dKV smem: K, V (once) + 2 stages x (Q, dO) + lse/D (2 stages) + P^T + dS^T
 constexpr int DKV_ST = 4;  // Q/dO ring depth
 // K/V double-buffered (the next item's K/V loads under the current item)
-constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + 2 * 2 * BW_T * 4 + 256 + 64;
+constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + (BW_SOFTMAX / 32) * 64 * 4 + 256 + 64;
 
 // dK/dV, persistent: grid = #SMs; work item = (128-key tile kt, batch * KV
 // head), heaviest key tiles first (kt = 0 sees every query tile), dealt
@@ -932,9 +932,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint8_t* sV = sK + 2 * BW_TILE;        // [2 items]
     uint8_t* sQ = sV + 2 * BW_TILE;        // [DKV_ST stages]
     uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
-    float* sL = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [2][128] lse (log2 domain)
-    float* sD = sL + 2 * BW_T;                           // [2][128] D
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sD + 2 * BW_T);
+    // per softmax warp: its 32 query columns' lse (log2 domain) | D, for float4 broadcasts
+    float* sLD = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [16 warps][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + (BW_SOFTMAX / 32) * 64);
     uint64_t* kv_full = bars;                 // [2]
     uint64_t* kv_empty = bars + 2;            // [2]: every S^T/dP^T MMA of the item issued and done
     uint64_t* q_full = bars + 4;              // [DKV_ST]
@@ -1102,23 +1102,25 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     } else if (warp >= 4) {
         // 16 warps: quadrant wq (key rows = TMEM lanes) x quarter qq (32 of 128 queries)
         const int wq = warp & 3, qq = (warp - 4) >> 2;
-        const int r = wq * 32 + lane;  // key row = TMEM lane (and, for the lse/D fetch, query column)
+        const int r = wq * 32 + lane;  // key row = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
-        // lse (log2) and D of the next tile, loaded one tile ahead (registers)
-        // by the quarter-0 threads and published through a double-buffered smem row
+        // lse (log2) and D of this warp's 32 query columns of the next tile,
+        // loaded one tile ahead into registers (lane = column) and published
+        // through the warp's own smem row: no barrier across the softmax warps
+        float* myLD = sLD + (warp - 4) * 64;
         auto fetch = [&](int u, int i, float& lv, float& dv) {
             lv = dv = 0.f;
             if (u < 0 || u >= n_items) return;
             const Item w = item_of(u);
-            const int q = (w.kt + i % w.nq) * BW_T + r;
+            const int q = (w.kt + i % w.nq) * BW_T + qq * 32 + lane;
             if (q >= T) return;
             const int64_t bh = static_cast<int64_t>(w.b) * H + w.hk * G + i / w.nq;
             lv = __ldg(lse + bh * T + q) * kLog2e;
             dv = __ldg(dsum + bh * T + q);
         };
         float nl = 0.f, nd = 0.f;
-        if (qq == 0) fetch(item_at(sched, sk, 0), 0, nl, nd);
+        fetch(item_at(sched, sk, 0), 0, nl, nd);
         // dK/dV of item `prev` leave TMEM -> global: deferred into the next
         // item's first tile (after its exp/dS math, which overlaps the item's
         // last dV/dK MMAs), or after the loop for the CTA's last item
@@ -1141,29 +1143,26 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const int key = k0 + r;
             for (int i = 0; i < niter; ++i) {
                 const int g = it + i;
-                const int s = g & 1;
                 const int qi = i % w.nq;
                 const int q0 = (w.kt + qi) * BW_T;
-                if (qq == 0) {
-                    sL[s * BW_T + r] = nl;
-                    sD[s * BW_T + r] = nd;
-                }
-                asm volatile("bar.sync 1, 512;" ::: "memory");  // softmax warps only
+                __syncwarp();  // the previous tile's broadcasts are read
+                myLD[lane] = nl;
+                myLD[32 + lane] = nd;
+                __syncwarp();
                 if (warp == 4 && lane == 0) BWD_PROBE(2, g);
-                if (qq == 0) {  // latency hidden behind this tile
-                    if (i + 1 < niter)
-                        fetch(u, i + 1, nl, nd);
-                    else
-                        fetch(item_at(sched, sk, k + 1), 0, nl, nd);
-                }
+                // the next tile's values: latency hidden behind this tile
+                if (i + 1 < niter)
+                    fetch(u, i + 1, nl, nd);
+                else
+                    fetch(item_at(sched, sk, k + 1), 0, nl, nd);
                 mbar_wait(s_full, g & 1);
                 tc_after();
                 if (warp == 4 && lane == 0) BWD_PROBE(3, g);
                 // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
                 // rows past T belong to the next sequence)
                 const bool edge = qi == 0 || q0 + BW_T > T;
-                const float4* L4 = reinterpret_cast<const float4*>(sL + s * BW_T + qq * 32);
-                const float4* D4 = reinterpret_cast<const float4*>(sD + s * BW_T + qq * 32);
+                const float4* L4 = reinterpret_cast<const float4*>(myLD);
+                const float4* D4 = reinterpret_cast<const float4*>(myLD + 32);
                 {
                     // S^T and dP^T (this warp's 32 columns each) go to registers first
                     // and their TMEM is released at once, so the MMA warp computes the
@@ -1413,13 +1412,26 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             tmem_wait_ld();
             if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * HD + qq * 32, o, scale);
         };
+        // this row's lse (log2) and D, loaded one item ahead
+        auto fetch = [&](int u, float& L, float& Dq) {
+            L = Dq = 0.f;
+            if (u < 0) return;
+            const Item w = item_of(u);
+            const int q = w.qt * BW_T + r;
+            const int64_t bh = static_cast<int64_t>(w.b) * H + w.h;
+            if (q < T) {
+                L = __ldg(lse + bh * T + q) * kLog2e;
+                Dq = __ldg(dsum + bh * T + q);
+            }
+        };
+        float nL, nD;
+        fetch(item_at(sched, sk, 0), nL, nD);
         int it = 0;
         for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
             const Item w = item_of(u);
             const int q = w.qt * BW_T + r;
-            const int64_t bh = static_cast<int64_t>(w.b) * H + w.h;
-            const float L = q < T ? __ldg(lse + bh * T + q) * kLog2e : 0.f;
-            const float Dq = q < T ? __ldg(dsum + bh * T + q) : 0.f;
+            const float L = nL, Dq = nD;
+            fetch(item_at(sched, sk, k + 1), nL, nD);
             for (int j = 0; j < w.nk; ++j) {
                 const int g = it + j;
                 mbar_wait(s_full, g & 1);

@@ -1,0 +1,202 @@
+// tcgen05.mma issue-rate microbenchmark (B200, sm_100a): one CTA (or CTA pair)
+// per SM issues back-to-back bf16 MMAs of one shape (K = 16 each) from smem
+// (SS) or with A from TMEM (TS), into 1 or 2 alternating accumulators, and
+// times the chain with %globaltimer. Prints ns per instruction and the
+// per-SM rate against the dense 8192 FLOP/clk/SM. Diagnostic only.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/diag/mma_rate.cu -o tools/diag/mma_rate.bin
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int b_mn = 0) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(b_mn) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0,1,0,p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+template <int M, int N, int CG, int TS, int NACC, int BMN = 0, int LDW = 0>
+__global__ void __launch_bounds__(128 + 32 * LDW, 1) mma_rate(int iters, unsigned long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = sm;                    // 128 rows x 128 B
+    uint8_t* sB = sm + 128 * 128;        // N/CG rows x 128 B (MN-major: 64-wide atoms of 64 K rows, 8 KB apart)
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    uint32_t rank = 0;
+    if (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    for (int i = threadIdx.x; i < (128 * 128 + (N / CG) * 128) / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(sm)[i] = make_uint4(0x3c003c00u, 0x3c003c00u, 0x3c003c00u, 0x3c003c00u);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 2) {
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    if (CG == 2)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tslot;
+    if (warp == 1 && rank == 0 && (threadIdx.x & 31) == 0) {
+        constexpr uint32_t id = idesc_bf16(M, N, BMN);
+        const uint64_t ad = sdesc(smem_u32(sA), 16, 1024);
+        const uint64_t bd = BMN ? sdesc(smem_u32(sB), 64 * 128, 1024) : sdesc(smem_u32(sB), 16, 1024);
+        constexpr uint64_t bstep = BMN ? 128 : 2;  // MN-major: 16 K rows = two 8-row atoms (2048 B)
+        const uint32_t ta = tmem + 448;  // TS: A (M x 16 bf16 = 8 packed columns) from TMEM
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (int i = 0; i < iters; ++i) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t d = tmem + ((i * 4 + kk) % NACC) * (N <= 128 ? 128 : 256) * 0 + ((i * 4 + kk) % NACC) * N;
+                const uint32_t acc = i > 0 ? 1u : 0u;
+                if (CG == 2) {
+                    if (TS)
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                                     "r"(ta), "l"(bd + bstep * kk), "r"(id), "r"(acc));
+                    else
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                                     "l"(ad + 2 * kk), "l"(bd + bstep * kk), "r"(id), "r"(acc));
+                } else {
+                    if (TS)
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                                     "r"(ta), "l"(bd + bstep * kk), "r"(id), "r"(acc));
+                    else
+                        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                                     "l"(ad + 2 * kk), "l"(bd + bstep * kk), "r"(id), "r"(acc));
+                }
+            }
+        }
+        if (CG == 2)
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                         ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+        else
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
+                         : "memory");
+        mbar_wait(&bar, 0);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        out[blockIdx.x] = t1 - t0;
+    }
+    if (LDW && warp >= 4) {  // TMEM readers (like softmax warps): 32x32b.x32 loads from columns 384.. of their quadrant
+        const uint32_t ta = tmem + 384 + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        uint32_t acc = 0;
+        for (int i = 0; i < iters / 2; ++i) {
+            uint32_t v[32];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                           "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+                           "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                           "=r"(v[30]), "=r"(v[31])
+                         : "r"(ta));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            acc += v[0] ^ v[31];
+        }
+        if (acc == 0x12345678u) out[0] = 1;
+    }
+    if (CG == 2 && rank == 1 && threadIdx.x == 0) mbar_wait(&bar, 0);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    if (CG == 2)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else
+        __syncthreads();
+    if (warp == 2) {
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <int M, int N, int CG, int TS, int NACC, int BMN = 0, int LDW = 0>
+void run(const char* name) {
+    const int iters = 2000, nsm = 148;
+    unsigned long long* d;
+    cudaMalloc(&d, nsm * 8);
+    cudaMemset(d, 0, nsm * 8);
+    auto k = mma_rate<M, N, CG, TS, NACC, BMN, LDW>;
+    const int smem = 1024 + 128 * 128 + (BMN ? 64 * 128 * ((N / CG + 63) / 64) : (N / CG) * 128);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nsm);
+    cfg.blockDim = dim3(128 + 32 * LDW);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k, iters, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<unsigned long long> h(nsm);
+    cudaMemcpy(h.data(), d, nsm * 8, cudaMemcpyDeviceToHost);
+    double mx = 0, sum = 0;
+    int n = 0;
+    for (auto v : h)
+        if (v) { mx = v > mx ? v : mx; sum += v; ++n; }
+    const double ns = sum / n / (iters * 4.0);
+    const double flop_per_sm = 2.0 * M * N * 16 / CG;  // per SM
+    printf("{\"mma\": \"%s\", \"B_mn\": %d, \"ld_warps\": %d, \"M\": %d, \"N\": %d, \"cta_group\": %d, \"A_tmem\": %d, \"accumulators\": %d, "
+           "\"ns_per_instr\": %.1f, \"tflops_per_sm\": %.2f, \"chip_tflops\": %.0f, \"err\": \"%s\"}\n",
+           name, BMN, LDW, M, N, CG, TS, NACC, ns, flop_per_sm / ns * 1e-3, flop_per_sm / ns * 1e-3 * 148, cudaGetErrorString(e));
+    cudaFree(d);
+}
+
+int main() {
+    run<128, 64, 1, 1, 2, 1, 0>("TS MN-B");
+    run<128, 64, 1, 1, 2, 1, 16>("TS MN-B + 16 ld warps");
+    run<128, 64, 1, 1, 2, 0, 16>("TS + 16 ld warps");
+    run<128, 128, 1, 0, 2, 0, 16>("SS + 16 ld warps");
+    run<128, 128, 1, 0, 2, 1, 0>("SS MN-B");
+    run<128, 256, 1, 0, 1, 1, 0>("SS MN-B");
+    run<128, 64, 1, 0, 1>("SS");
+    run<128, 64, 1, 0, 2>("SS");
+    run<128, 64, 1, 1, 2>("TS");
+    run<128, 128, 1, 0, 1>("SS");
+    run<128, 128, 1, 0, 2>("SS");
+    run<128, 128, 1, 1, 2>("TS");
+    run<128, 192, 1, 0, 2>("SS");
+    run<128, 256, 1, 0, 1>("SS");
+    run<128, 256, 1, 1, 1>("TS");
+    run<256, 64, 2, 0, 2>("SS");
+    run<256, 64, 2, 1, 2>("TS");
+    run<256, 128, 2, 0, 2>("SS");
+    run<256, 128, 2, 1, 2>("TS");
+    run<256, 256, 2, 0, 1>("SS");
+    run<256, 256, 2, 1, 1>("TS");
+    return 0;
+}
