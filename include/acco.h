@@ -155,6 +155,15 @@ int acco_gemm(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t
               int b_mn_major, int m, int n, int k, int dtype, int epi_mode, void* c, int64_t ldc,
               const void* bias, const void* residual, int64_t ldr, void* aux, int64_t ld_aux,
               int beta, void* stream);
+/* Weight-gradient GEMM with its bias gradient (bf16 operands, fp32 outputs):
+ * C[m,n] (+)= sum_k A(m,k) B(n,k) and bias_grad[m] (+)= sum_k A(m,k) (the
+ * column sums of dY for A = dY^T), '+' when beta = 1. The row sums come off
+ * the tensor core (a ones-operand MMA in the first n-block's tiles), fused
+ * into the same launch — the reference's Bundle::add of the bias entries
+ * (/root/reference/proj/src/protocols.cpp:61-66) without a separate pass. */
+int acco_gemm_bias_grad(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t ldb,
+                        int b_mn_major, int m, int n, int k, float* c, int64_t ldc, float* bias_grad,
+                        int beta, void* stream);
 
 /* ------------------------------------------------------ model plugin (LM)
  * The B200 gradient oracle for the GPT-style LM defined in

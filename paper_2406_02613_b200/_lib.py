@@ -77,6 +77,8 @@ _PROTOS = {
     "acco_gemm": (C.c_int, [_P, C.c_int64, C.c_int, _P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
                             C.c_int, C.c_int, _P, C.c_int64, _P, _P, C.c_int64, _P, C.c_int64,
                             C.c_int, _P]),
+    "acco_gemm_bias_grad": (C.c_int, [_P, C.c_int64, C.c_int, _P, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      _P, C.c_int64, _P, C.c_int, _P]),
 }
 
 

@@ -133,4 +133,21 @@ int acco_gemm(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t
     });
 }
 
+int acco_gemm_bias_grad(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t ldb,
+                        int b_mn_major, int m, int n, int k, float* c, int64_t ldc, float* bias_grad,
+                        int beta, void* stream) {
+    return guarded([&] {
+        ACCO_REQUIRE(bias_grad != nullptr, "acco_gemm_bias_grad: bias_grad is null");
+        GemmOperand A{a, lda, a_mn_major != 0};
+        GemmOperand B{b, ldb, b_mn_major != 0};
+        Epilogue ep;
+        ep.mode = kEpiAccF32;
+        ep.C = c;
+        ep.ldc = ldc;
+        ep.beta = beta;
+        ep.bias_grad = bias_grad;
+        gemm_bf16(A, B, m, n, k, ep, static_cast<cudaStream_t>(stream));
+    });
+}
+
 }  // extern "C"

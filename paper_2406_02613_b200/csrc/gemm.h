@@ -47,10 +47,20 @@ struct Epilogue {
     void* aux = nullptr;             // [M, ld_aux] pre-activation (gelu modes)
     int64_t ld_aux = 0;
     int beta = 0;                    // kEpiAccF32: accumulate into C when 1
+    // kEpiAccF32 (weight gradients dW = dY^T X, A = dY^T): also the bias
+    // gradient db[m] (+)= sum_k A(m, k) = the column sums of dY, fp32 [M],
+    // accumulated like C (beta). Computed on the tensor core by the tiles of
+    // the first n-block: one extra 16-wide MMA per k-slice against a ones tile.
+    float* bias_grad = nullptr;
 };
 
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
                const Epilogue& ep, cudaStream_t stream);
+// Whether a bf16 fp32-accumulate GEMM of this shape should take
+// Epilogue::bias_grad: the bias MMA needs a tile width <= 192 (TMEM), so it is
+// fused only when the best plan overall already has such a width (else the
+// caller reduces the columns separately).
+bool gemm_bias_grad_free(const GemmOperand& A, const GemmOperand& B, int M, int N, int K);
 // fp32 operands: the 3xTF32 tcgen05 kernel (gemm_tcgen05.cu) ...
 void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
                  const Epilogue& ep, cudaStream_t stream);

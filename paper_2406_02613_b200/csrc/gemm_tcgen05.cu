@@ -296,6 +296,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
     return d;
 }
 
+// UMMA shared-memory descriptor without swizzle (K-major: 8-row x 16 B core
+// matrices; lbo = byte stride between core matrices along K, sbo along M/N)
+__device__ __forceinline__ uint64_t sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // version = 1 (tcgen05); layout 0 = SWIZZLE_NONE
+    return d;
+}
+
 // Instruction descriptor for kind::f16: bf16 x bf16 -> fp32.
 __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n, int a_mn, int b_mn) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(a_mn) << 15) |
@@ -318,9 +329,16 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
 
 // One operand tile is 128 B per row in every variant: 64 bf16 or 32 fp32 (tf32)
 // elements of K. The 3xTF32 variant stages a hi and a lo plane per operand.
+// Bias-gradient MMAs (Epilogue::bias_grad) need 2 x 16 spare TMEM columns next
+// to the two accumulators (BN <= 192) and a ones B operand: a 16 x 16 bf16
+// K-major tile without swizzle (four 8 x 8 core matrices, 512 B).
+template <int BN, int X3 = 0>
+constexpr bool has_bias_mma() { return !X3 && BN <= 192; }
+constexpr int kOnesBytes = 512;
 template <int BN, int STAGES, int X3 = 0, int CG = 1>
 constexpr int smem_bytes() {
-    return 1024 /*align slack*/ + STAGES * (kBM + BN / CG) * 128 * (X3 ? 2 : 1) +
+    return 1024 /*align slack*/ + (has_bias_mma<BN, X3>() ? kOnesBytes + 128 : 0) +
+           STAGES * (kBM + BN / CG) * 128 * (X3 ? 2 : 1) +
            epi_warps<BN, STAGES, X3>() * epi_warp_bytes<BN, STAGES>() +
            (2 * STAGES + 4 + epi_warps<BN, STAGES, X3>() * in_bufs<BN>()) * 8 + 16 +
            48 /* CLC: full / empty mbarriers, 16 B response, alignment */;
@@ -453,10 +471,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     uint64_t* clc_empty = clc_full + 1;                // every role warp has read it
     uint8_t* clc_resp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(clc_empty + 1) + 15) & ~uintptr_t(15));
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(clc_resp + 16);
+    uint8_t* sOnes = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 127) & ~uintptr_t(127));
+    constexpr bool kBiasMma = has_bias_mma<BN, X3>();
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nunits = sc.units();
+    if (kBiasMma && ep.bias_grad && warp == 3) {  // the ones tile (bf16 1.0), for the async proxy
+        reinterpret_cast<uint4*>(sOnes)[lane] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+        fence_async_smem();
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -476,7 +500,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     // two accumulator buffers (tile ping-pong); the 3xTF32 variant keeps a main
     // (hi*hi) and a correction (lo*hi + hi*lo) accumulator per buffer
     constexpr int kAccCols = X3 ? 2 * BN : BN;
-    constexpr uint32_t kTmemCols = 2 * kAccCols <= 256 ? 256 : 512;  // power of two >= 2 accumulators
+    // power of two >= 2 accumulators (+ 2 x 16 bias-gradient columns)
+    constexpr uint32_t kTmemCols = 2 * kAccCols + (kBiasMma ? 32 : 0) <= 256 ? 256 : 512;
+    constexpr uint32_t kBiasCol = 2 * kAccCols;  // bias-gradient accumulators [2][16]
     if (warp == 2) {
         if (CG == 2) {  // both CTAs of the pair allocate collectively (same columns in each)
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -619,6 +645,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         // and commits. This keeps the issuer's instruction count per k-block low:
         // it shares its SM sub-partition with two epilogue warps.
         constexpr uint32_t idesc = idesc_bf16(kBM * CG, BN, A_MN, B_MN);
+        constexpr uint32_t idesc_b = idesc_bf16(kBM * CG, 16, A_MN, 0);
+        // no-swizzle K-major ones tile: 8 x 16 B core matrices, 128 B apart along
+        // K (LBO), 256 B apart along N (SBO); every k-slice reads the same tile
+        const uint64_t ones_d = sdesc_noswz(smem_u32(sOnes), 128, 256);
         // descriptor start-address step per 16-deep k slice (address >> 4):
         // K-major 32 B inside the 128B swizzle row, MN-major two 8-row atoms (2048 B)
         constexpr uint64_t a_step = A_MN ? 2048 >> 4 : 32 >> 4;
@@ -637,6 +667,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             tc_fence_after();
             if (lane == 0) GEMM_PROBE(0, lt);
             const uint32_t tmem_d = tmem_base + acc * kAccCols;
+            // the first n-block's tiles also accumulate the bias gradient (16
+            // columns, each the row sum of A) against the ones tile
+            const bool bias_unit = kBiasMma && ep.bias_grad != nullptr && nb == 0;
+            const uint32_t tmem_b = tmem_base + kBiasCol + acc * 16;
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
@@ -672,12 +706,22 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                         for (int kk = 0; kk < kBK / 16; ++kk)
                             umma_bf16_pair(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc,
                                            (kb > kb0 || kk > 0) ? 1u : 0u);
+                        if (kBiasMma && bias_unit) {
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 16; ++kk)
+                                umma_bf16_pair(tmem_b, ad + kk * a_step, ones_d, idesc_b, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        }
                         umma_commit_pair(&empty[s]);  // frees the stage in both CTAs
                     }
                 } else if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
                         umma_bf16(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    if (kBiasMma && bias_unit) {  // bias gradient: row sums of A (x ones)
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 16; ++kk)
+                            umma_bf16(tmem_b, ad + kk * a_step, ones_d, idesc_b, (kb > kb0 || kk > 0) ? 1u : 0u);
+                    }
                     umma_commit(&empty[s]);
                 }
                 __syncwarp();
@@ -812,6 +856,21 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             tc_fence_after();
             if (lane == 0 && (ew == 0 || ew == kEpiWarps - 1)) GEMM_PROBE(ew == 0 ? 2 : 4, lt);
             const uint32_t tbase = tmem_base + acc * kAccCols + (static_cast<uint32_t>(wq * 32) << 16);
+            if (kBiasMma && ep.bias_grad && nb == 0 && hf == 0) {
+                // bias gradient of this quadrant's rows (column 0 of the 16 equal
+                // ones-MMA columns), added in split order like the tile itself
+                uint32_t bv;
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                             : "=r"(bv)
+                             : "r"(tmem_base + kBiasCol + acc * 16 + (static_cast<uint32_t>(wq * 32) << 16)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int row = row0 + lane;
+                if (row < M) {
+                    float* bg = ep.bias_grad + row;
+                    *bg = (sp > 0 || ep.beta) ? *bg + __uint_as_float(bv) : __uint_as_float(bv);
+                    __threadfence();  // visible before this warp's split hand-off (lane 0's release)
+                }
+            }
             if (ep.mode == kEpiSwiGLU) {
                 // accumulator columns [0, BN/2) = gate, [BN/2, BN) = up of the same
                 // BN/2 features (n0/2 ...): store both pre-activations (for the
@@ -1369,6 +1428,7 @@ void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K
                  cudaStream_t stream) {
     ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_f32: empty problem");
     ACCO_REQUIRE(ep.mode <= kEpiAccF32, "gemm_f32: epilogue mode not supported by the fp32 path");
+    ACCO_REQUIRE(!ep.bias_grad, "gemm_f32: bias_grad is a bf16-path epilogue (the fp32 path reduces columns separately)");
     ACCO_REQUIRE(ep.mode == kEpiStore || ep.mode == kEpiAccF32 || ep.aux, "gemm_f32: GELU epilogues need aux");
     ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
     const int64_t kp = (K + 3) / 4 * 4;  // 16 B row stride for TMA
@@ -1414,13 +1474,10 @@ void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K
     ACCO_CUDA(cudaFreeAsync(pa, stream));
 }
 
-void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
-               cudaStream_t stream) {
-    ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_bf16: empty problem");
-    ACCO_REQUIRE(!(ep.residual && (ep.mode == kEpiGelu || ep.mode == kEpiDGelu)),
-                 "gemm_bf16: residual add is not combined with the GELU epilogues");
-    ACCO_REQUIRE(ep.mode == kEpiStore || ep.mode == kEpiAccF32 || ep.aux, "gemm_bf16: GELU epilogues need aux");
-    ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
+namespace {
+// The planner: tile width, split-K and CTA group with the least modelled time.
+double plan_gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, bool acc_f32, bool bias_grad,
+                 int& best_bn, int& best_sp, int& best_cg) {
     const int sms = num_sms();
     // The LM head's shapes (B too big to stay in L2, whole-M raster: see
     // launch) stream B from HBM once; there the model underrates the 256-wide
@@ -1429,14 +1486,17 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     // single-CTA tiles only (A/B knob).
     const bool large_b = static_cast<double>(M) * K * 2 <= 48e6 && static_cast<double>(N) * K * 2 > 32e6;
     const bool allow_cg2 = std::getenv("ACCO_GEMM_NO_CG2") == nullptr;
-    int best_bn = 256, best_sp = 1, best_cg = 1;
+    best_bn = 256;
+    best_sp = 1;
+    best_cg = 1;
     double best = 1e300;
     for (int cg : {1, 2}) {
         if (cg == 2 && !allow_cg2) continue;
         for (int bn : {256, 192, 128}) {
             if (cg == 2 && bn == 192 && (B.mn_major || large_b)) continue;
+            if (bias_grad && !has_bias_mma<256>() && bn == 256) continue;  // no TMEM for the bias columns
             for (int sp : {1, 2, 3, 4, 6, 8}) {
-                if (sp > 1 && (ep.mode != kEpiAccF32 || ceil_div(K, kBK) < 4 * sp ||
+                if (sp > 1 && (!acc_f32 || ceil_div(K, kBK) < 4 * sp ||
                                ceil_div(M, kBM) * ceil_div(N, bn) * 8 * 32 > kSemSlots))
                     continue;
                 const double t = plan_time(M, N, K, bn, cg, sp, A.mn_major, sms);
@@ -1449,6 +1509,32 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
             }
         }
     }
+    return best;
+}
+}  // namespace
+
+bool gemm_bias_grad_free(const GemmOperand& A, const GemmOperand& B, int M, int N, int K) {
+    if (std::getenv("ACCO_GEMM_FORCE")) return true;
+    int bn = 256, sp = 1, cg = 1;
+    const double t_free = plan_gemm(A, B, M, N, K, true, false, bn, sp, cg);
+    const double t_bias = plan_gemm(A, B, M, N, K, true, true, bn, sp, cg);
+    // only where the restriction costs nothing: the 192-wide alternatives to a
+    // 256-wide best plan measured slower than the model says (GPT-2 medium
+    // fc / fc2 weight gradients, +0.7 ms per step with a 3 us allowance)
+    return t_bias <= t_free * 1.0001;
+}
+
+void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,
+               cudaStream_t stream) {
+    ACCO_REQUIRE(M > 0 && N > 0 && K > 0, "gemm_bf16: empty problem");
+    ACCO_REQUIRE(!(ep.residual && (ep.mode == kEpiGelu || ep.mode == kEpiDGelu)),
+                 "gemm_bf16: residual add is not combined with the GELU epilogues");
+    ACCO_REQUIRE(ep.mode == kEpiStore || ep.mode == kEpiAccF32 || ep.aux, "gemm_bf16: GELU epilogues need aux");
+    ACCO_REQUIRE(!ep.bias_grad || ep.mode == kEpiAccF32, "gemm_bf16: bias_grad needs the fp32 accumulate epilogue");
+    ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
+    const int sms = num_sms();
+    int best_bn = 256, best_sp = 1, best_cg = 1;
+    double best = plan_gemm(A, B, M, N, K, ep.mode == kEpiAccF32, ep.bias_grad != nullptr, best_bn, best_sp, best_cg);
     if (ep.mode == kEpiDSwiGLU) {
         ACCO_REQUIRE(ep.aux && !ep.residual && !ep.bias && N % 32 == 0,
                      "gemm_bf16: DSwiGLU epilogue needs aux, F % 32 == 0, no bias/residual");
@@ -1516,6 +1602,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
             best_bn = fb;
             best_sp = ep.mode == kEpiAccF32 ? fs : 1;
             best_cg = fc == 2 && !(fb == 192 && B.mn_major) ? 2 : 1;
+            if (ep.bias_grad && best_bn == 256) best_bn = 192;
         }
     }
     if (std::getenv("ACCO_GEMM_LOG")) {  // each distinct shape's plan, once

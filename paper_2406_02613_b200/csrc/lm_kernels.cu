@@ -187,6 +187,15 @@ __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloa
     }
 }
 
+// Per-element norm-backward math with explicit roundings (no FMA contraction
+// left to the compiler), shared by ln_bwd_vec and ln_bwd_vec_p so their dx are
+// bitwise equal: xhat = (x - mu) rs, dxh = dy g; s1 += dxh, s2 += dxh xhat;
+// dx = rs (dxh - s1 - xhat s2).
+__device__ __forceinline__ float ln_xhat(float x, float mu, float rs) { return __fmul_rn(__fsub_rn(x, mu), rs); }
+__device__ __forceinline__ float ln_dx(float dxh, float xh, float s1, float s2, float rs) {
+    return __fmul_rn(rs, __fsub_rn(__fsub_rn(dxh, s1), __fmul_rn(xh, s2)));
+}
+
 template <int CH, bool RMS>
 __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                            const __nv_bfloat16* __restrict__ g, const float* __restrict__ mean,
@@ -216,15 +225,15 @@ __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bflo
         unpack8b(reinterpret_cast<const uint4*>(g)[lane + 32 * i], gv);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            xh[8 * i + k] = (xh[8 * i + k] - mu) * rs;
-            dxh[8 * i + k] = dv[k] * gv[k];
+            xh[8 * i + k] = ln_xhat(xh[8 * i + k], mu, rs);
+            dxh[8 * i + k] = __fmul_rn(dv[k], gv[k]);
         }
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < CH * 8; ++i) {
-        s1 += dxh[i];
-        s2 += dxh[i] * xh[i];
+        s1 = __fadd_rn(s1, dxh[i]);
+        s2 = __fadd_rn(s2, __fmul_rn(dxh[i], xh[i]));
     }
     s1 = RMS ? 0.f : warp_sum(s1) / d;
     s2 = warp_sum(s2) / d;
@@ -234,8 +243,8 @@ __global__ void ln_bwd_vec(const __nv_bfloat16* __restrict__ dy, const __nv_bflo
         if (accumulate) unpack8b(pv[i], prev);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            r[k] = rs * (dxh[8 * i + k] - s1 - xh[8 * i + k] * s2);
-            if (accumulate) r[k] += prev[k];
+            r[k] = ln_dx(dxh[8 * i + k], xh[8 * i + k], s1, s2, rs);
+            if (accumulate) r[k] = __fadd_rn(r[k], prev[k]);
         }
         dxr[lane + 32 * i] = pack8b(r);
     }
@@ -292,6 +301,126 @@ __global__ void __launch_bounds__(NT) ln_bwd_wide(const __nv_bfloat16* __restric
         if (accumulate) r[k] += prev[k];
     }
     reinterpret_cast<uint4*>(dx + o)[t] = pack8b(r);
+}
+
+// ------------------------- norm backward with fused parameter-gradient partials
+// Persistent forms of ln_bwd_vec / ln_bwd_wide (the same per-row arithmetic,
+// so dx is bitwise unchanged): block b takes rows b, b + G, ... (fixed) and
+// also accumulates, per column, dgamma = sum dy * xhat and dbeta = sum dy over
+// its rows in registers; at the end the block's partial sums go to
+// part[b][q][d] (q = 0 dgamma, 1 dbeta). One ln_param_fold per micro-batch
+// then sums every norm's G partials in block order into the gradient
+// accumulator: the parameter reductions no longer re-read dy and x on a side
+// stream (two launches and 2 x M x d x 2 bytes per norm before).
+template <int CH, bool RMS>
+__global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __restrict__ dy,
+                                                       const __nv_bfloat16* __restrict__ x,
+                                                       const __nv_bfloat16* __restrict__ g,
+                                                       const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                       __nv_bfloat16* __restrict__ dx, int accumulate, int M,
+                                                       float* __restrict__ part) {
+    ACCO_PDL_PROLOGUE();
+    constexpr int d = 256 * CH;
+    extern __shared__ float red[];  // [8 warps][d]
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // (registers: the per-lane parameter sums stay resident, the row's values
+    // are unpacked per 8-column chunk in each of the two passes, so two blocks
+    // of 8 warps fit an SM)
+    float ag[CH * 8], ab[CH * 8];
+#pragma unroll
+    for (int i = 0; i < CH * 8; ++i) ag[i] = ab[i] = 0.f;
+    const uint4* gq = reinterpret_cast<const uint4*>(g);
+    for (int row = blockIdx.x * 8 + w; row < M; row += gridDim.x * 8) {
+        const int64_t o = static_cast<int64_t>(row) * d;
+        const uint4* dyr = reinterpret_cast<const uint4*>(dy + o);
+        const uint4* xr = reinterpret_cast<const uint4*>(x + o);
+        uint4* dxr = reinterpret_cast<uint4*>(dx + o);
+        const float mu = mean[row], rs = rstd[row];
+        uint4 xv[CH], dvv[CH], pv[CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            xv[i] = xr[lane + 32 * i];
+            dvv[i] = dyr[lane + 32 * i];
+            if (accumulate) pv[i] = dxr[lane + 32 * i];
+        }
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            float xh[8], dv[8], gv[8];
+            unpack8b(xv[i], xh);
+            unpack8b(dvv[i], dv);
+            unpack8b(gq[lane + 32 * i], gv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                xh[k] = ln_xhat(xh[k], mu, rs);
+                const float dxh = __fmul_rn(dv[k], gv[k]);
+                s1 = __fadd_rn(s1, dxh);
+                s2 = __fadd_rn(s2, __fmul_rn(dxh, xh[k]));
+                ag[8 * i + k] += dv[k] * xh[k];
+                if (!RMS) ab[8 * i + k] += dv[k];
+            }
+        }
+        s1 = RMS ? 0.f : warp_sum(s1) / d;
+        s2 = warp_sum(s2) / d;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            float xh[8], dv[8], gv[8], r[8], prev[8];
+            unpack8b(xv[i], xh);
+            unpack8b(dvv[i], dv);
+            unpack8b(gq[lane + 32 * i], gv);
+            if (accumulate) unpack8b(pv[i], prev);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                r[k] = ln_dx(__fmul_rn(dv[k], gv[k]), ln_xhat(xh[k], mu, rs), s1, s2, rs);
+                if (accumulate) r[k] = __fadd_rn(r[k], prev[k]);
+            }
+            dxr[lane + 32 * i] = pack8b(r);
+        }
+    }
+    // block partials: the 8 warps' column sums in warp order
+#pragma unroll
+    for (int q = 0; q < (RMS ? 1 : 2); ++q) {
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) red[w * d + 8 * (lane + 32 * i) + k] = q ? ab[8 * i + k] : ag[8 * i + k];
+        __syncthreads();
+        for (int c = threadIdx.x; c < d; c += 256) {
+            float t = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t += red[j * d + c];
+            part[(static_cast<int64_t>(blockIdx.x) * 2 + q) * d + c] = t;
+        }
+        __syncthreads();
+    }
+}
+
+// Every norm of the micro-batch: grad[g_off + c] (+)= sum_b part[b][0][c] and
+// grad[b_off + c] (+)= sum_b part[b][1][c] (b_off < 0: RMSNorm), blocks summed
+// in four fixed interleaved sub-sums then in a fixed order — deterministic.
+__global__ void __launch_bounds__(256) ln_param_fold_kernel(const LnFold* __restrict__ table, const float* __restrict__ parts,
+                                                            float* __restrict__ grad, int G, int acc) {
+    ACCO_PDL_PROLOGUE();
+    __shared__ float sub_sum[4][64];
+    const LnFold e = table[blockIdx.y];
+    const int nq = e.b_off >= 0 ? 2 : 1;
+    const int cc = threadIdx.x & 63, sub = threadIdx.x >> 6;
+    const int col = blockIdx.x * 64 + cc;
+    const bool live = col < nq * e.d;
+    const int q = live ? col / e.d : 0, c = live ? col % e.d : 0;
+    float t = 0.f;
+    if (live) {
+        const float* p = parts + e.part_off + static_cast<int64_t>(q) * e.d + c;
+#pragma unroll 4
+        for (int b = sub; b < G; b += 4) t += __ldcs(p + static_cast<int64_t>(b) * 2 * e.d);
+    }
+    sub_sum[sub][cc] = t;
+    __syncthreads();
+    if (sub == 0 && live) {
+        const float r = ((sub_sum[0][cc] + sub_sum[1][cc]) + sub_sum[2][cc]) + sub_sum[3][cc];
+        float* o = grad + (q ? e.b_off : e.g_off) + c;
+        *o = (acc ? *o : 0.f) + r;
+    }
 }
 
 // ------------------------------------------------ deterministic column reduce
@@ -1265,6 +1394,66 @@ void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, co
     ACCO_CHECK_LAUNCH();
 }
 
+int ln_part_blocks() {
+    static const int per_sm = std::getenv("ACCO_LN_PART_PER_SM") ? std::atoi(std::getenv("ACCO_LN_PART_PER_SM")) : 2;
+    return std::max(1, per_sm) * num_sms();
+}
+
+// The warp-per-row form keeps 2 x 8 CH parameter sums per lane: CH <= 3
+// without spills. Wider rows keep the block-per-row dx kernel and the separate
+// side-stream parameter reduction: a persistent block-per-row form with the
+// sums in registers (d = 1024: 4 warps per block) measured slower end to end
+// (GPT-2 medium 319.8k vs 335.2k tok/s, profiles/r02_summary.md).
+bool ln_fused_supported(int d) {
+    if (d % 256 != 0 || d > 768 || std::getenv("ACCO_LN_PARAMS_SEPARATE")) return false;
+    const int ch = d / 256;
+    return ch == 1 || ch == 2 || ch == 3;
+}
+
+template <class T>
+void layernorm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
+                         bool accumulate_dx, int M, int d, float* part, cudaStream_t s, bool rms) {
+    if constexpr (sizeof(T) != 2) {
+        throw Error(kInvalidArg, "layernorm_bwd_fused: bf16 only");
+    } else {
+        ACCO_REQUIRE(ln_fused_supported(d) && a16(dy) && a16(x) && a16(g) && a16(dx),
+                     "layernorm_bwd_fused: unsupported width or alignment");
+        ProfScope prof(kProfNorm, 3.0 * M * d * sizeof(T) + 8.0 * M, s);
+        const int G = ln_part_blocks(), acc = accumulate_dx ? 1 : 0;
+#define ACCO_LNP(KERN, BLOCK, SMEM)                                                                    \
+    do {                                                                                               \
+        static bool cfg = false;                                                                       \
+        if (!cfg && (SMEM) > 48 * 1024) {                                                              \
+            ACCO_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (SMEM))); \
+        }                                                                                              \
+        cfg = true;                                                                                    \
+        launch_pdl(KERN, G, BLOCK, SMEM, s, dy, x, g, mean, rstd, dx, acc, M, part);                   \
+    } while (0)
+        {
+            const int smem = 8 * d * 4;  // block reduction of the 8 warps' sums
+            switch ((d / 256) * 2 + (rms ? 1 : 0)) {
+                case 2: ACCO_LNP((ln_bwd_vec_p<1, false>), 256, smem); break;
+                case 3: ACCO_LNP((ln_bwd_vec_p<1, true>), 256, smem); break;
+                case 4: ACCO_LNP((ln_bwd_vec_p<2, false>), 256, smem); break;
+                case 5: ACCO_LNP((ln_bwd_vec_p<2, true>), 256, smem); break;
+                case 6: ACCO_LNP((ln_bwd_vec_p<3, false>), 256, smem); break;
+                case 7: ACCO_LNP((ln_bwd_vec_p<3, true>), 256, smem); break;
+                default: throw Error(kInvalidArg, "layernorm_bwd_fused: unsupported width");
+            }
+        }
+#undef ACCO_LNP
+        ACCO_CHECK_LAUNCH();
+    }
+}
+
+void ln_param_fold(const LnFold* table, int n, int d_max, const float* parts, float* grad, bool acc, cudaStream_t s) {
+    if (n == 0) return;
+    ProfScope prof(kProfReduce, 1.0 * n * ln_part_blocks() * 2 * d_max * 4, s);
+    launch_pdl(ln_param_fold_kernel, dim3(ceil_div(2 * d_max, 64), n), 256, 0, s, table, parts, grad, ln_part_blocks(),
+               acc ? 1 : 0);
+    ACCO_CHECK_LAUNCH();
+}
+
 template <class T>
 void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, bool acc, cudaStream_t s) {
     ProfScope prof(kProfReduce, 1.0 * M * N * sizeof(T), s);
@@ -1491,7 +1680,9 @@ void comm_standin(const void* src, void* dst, int64_t bytes, int ctas, uint64_t 
                                           float*, int, int, bool, cudaStream_t);                              \
     template void layernorm_bwd_dx<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, int, \
                                       int, cudaStream_t, bool);                                               \
-    template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);             \
+    template void colsum_add<T>(const T*, int64_t, int, int, float*, float*, bool, cudaStream_t);\
+    template void layernorm_bwd_fused<T>(const T*, const T*, const T*, const float*, const float*, T*, bool, int, \
+                                         int, float*, cudaStream_t, bool);             \
     template void cross_entropy<T>(T*, int64_t, const int32_t*, int, int, int, float*, cudaStream_t);         \
     template void embed_bwd<T>(const uint64_t*, const T*, int, int, int, int, float*, float*, float*,        \
                                bool, cudaStream_t, bool);                                                     \

@@ -35,6 +35,29 @@ template <class T>
 void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
                       bool accumulate_dx, int M, int d, cudaStream_t s, bool rms = false);
 
+// bf16 norm backward with the parameter gradients fused: dx as
+// layernorm_bwd_dx, plus per-block column partials part[G][2][d] (dgamma =
+// sum dy * xhat, dbeta = sum dy; G = ln_part_blocks()) for ln_param_fold.
+// ln_fused_supported(d): d % 256 == 0 and a width the vec / wide kernels take.
+int ln_part_blocks();
+bool ln_fused_supported(int d);
+template <class T>
+void layernorm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, T* dx,
+                         bool accumulate_dx, int M, int d, float* part, cudaStream_t s, bool rms = false);
+// One norm's partials -> its gradient entries (offsets into the gradient
+// buffer; b_off < 0: RMSNorm, weight only). part_off indexes `parts`.
+struct LnFold {
+    int64_t part_off;
+    int64_t g_off;
+    int64_t b_off;
+    int d;
+    int pad;
+};
+// every norm of a micro-batch in one launch: grad[g_off..] (+)= sum_b part[b][0],
+// grad[b_off..] (+)= sum_b part[b][1]; `table` in device memory
+void ln_param_fold(const LnFold* table, int n, int d_max, const float* parts, float* grad, bool accumulate,
+                   cudaStream_t s);
+
 // out[c] += sum_r y[r*ld + c] (deterministic two-level), fp32 out.
 template <class T>
 void colsum_add(const T* y, int64_t ld, int M, int N, float* out, float* scratch, bool accumulate,

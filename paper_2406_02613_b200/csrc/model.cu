@@ -188,6 +188,36 @@ GPTModel::GPTModel(const LMConfig& c) : c_(c) {
     // 8 x SMs) (see colsum_vec / colreduce in lm_kernels.cu)
     const int64_t nchunk = std::max<int64_t>((M + 255) / 256, 8 * num_sms());
     ACCO_CUDA(cudaMalloc(&scratch_, nchunk * 4 * d * 2 * sizeof(float)));
+    // fused norm-parameter gradients (bf16): norm i = 0 the final norm, 1 + 2l
+    // the first norm of layer l, 2 + 2l its second; LnFold entries in that order
+    fuse_ln_ = c.precision == 1 && ln_fused_supported(d);  // (precision 1: bf16, see micro_batch)
+    if (fuse_ln_) {
+        n_ln_ = 2 * L + 1;
+        ACCO_CUDA(cudaMalloc(&ln_part_, static_cast<size_t>(n_ln_) * ln_part_blocks() * 2 * d * sizeof(float)));
+        std::vector<LnFold> tab(static_cast<size_t>(n_ln_));
+        auto off = [&](int i) { return static_cast<int64_t>(layout_[static_cast<size_t>(i)].off); };
+        for (int i = 0; i < n_ln_; ++i) {
+            LnFold& e = tab[static_cast<size_t>(i)];
+            e.part_off = static_cast<int64_t>(i) * ln_part_blocks() * 2 * d;
+            e.d = d;
+            e.pad = 0;
+            // parameter indices (layout_ order, see run / run_llama)
+            int gi, bi;
+            if (llama) {
+                const int l = (i - 1) / 2;
+                gi = i == 0 ? 1 + 6 * L : 1 + 6 * l + (i % 2 == 1 ? 0 : 3);
+                bi = -1;
+            } else {
+                const int l = (i - 1) / 2;
+                gi = i == 0 ? 2 + 12 * L : 2 + 12 * l + (i % 2 == 1 ? 0 : 6);
+                bi = gi + 1;
+            }
+            e.g_off = off(gi);
+            e.b_off = bi >= 0 ? off(bi) : -1;
+        }
+        ACCO_CUDA(cudaMalloc(&ln_fold_, tab.size() * sizeof(LnFold)));
+        ACCO_CUDA(cudaMemcpy(ln_fold_, tab.data(), tab.size() * sizeof(LnFold), cudaMemcpyHostToDevice));
+    }
     if (llama) {  // rotary table, fp64 angles rounded to fp32 (oracle rope_table)
         const int hd = c.d_model / c.n_head, h2 = hd / 2;
         std::vector<float2> tab(static_cast<size_t>(c.seq_len) * h2);
@@ -231,6 +261,8 @@ GPTModel::~GPTModel() {
         for (auto& e : ev_rd_) cudaEventDestroy(e);
     }
     cudaFree(scratch_);
+    if (ln_part_) cudaFree(ln_part_);
+    if (ln_fold_) cudaFree(ln_fold_);
     if (rope_) cudaFree(rope_);
     if (pinned_data_) cudaFreeHost(pinned_data_);
     if (stage_host_) cudaFreeHost(stage_host_);
@@ -395,6 +427,23 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     cudaStream_t aux_ = serial ? s : this->aux_;
     cudaStream_t ws = wg_side ? aux_ : s;  // weight-gradient stream
     enum { kRdDX, kRdDA, kRdDT, kRdDQKV };
+    // bf16: every bias gradient (the column sums of the dY that is the A
+    // operand of its weight-gradient GEMM) comes off the tensor core in that
+    // GEMM (Epilogue::bias_grad) instead of a separate column reduction that
+    // re-reads dY; ACCO_BIAS_COLSUM=1: the separate reductions (A/B)
+    // (per weight gradient: only where its best tile plan leaves TMEM for the
+    // bias columns, gemm_bias_grad_free; GPT-2 small: all four)
+    const bool colsum_env = std::getenv("ACCO_BIAS_COLSUM") != nullptr;
+    auto bias_free = [&](int m, int n) {
+        return sizeof(T) == 2 && !colsum_env && gemm_bias_grad_free({nullptr, 0, true}, {nullptr, 0, true}, m, n, M);
+    };
+    const bool fb_fc2 = bias_free(d, 4 * d), fb_fc = bias_free(4 * d, d), fb_proj = bias_free(d, d),
+               fb_qkv = bias_free(3 * d, d);
+    auto ep_wg = [&](float* c, int64_t ldc, float* bias_grad, bool fuse) {
+        Epilogue e = ep_acc(c, ldc, beta);
+        if (fuse) e.bias_grad = bias_grad;
+        return e;
+    };
     auto fork = [&] {
         if (serial) return;
         ACCO_CUDA(cudaEventRecord(ev_fork_, s));
@@ -415,53 +464,58 @@ void GPTModel::run(const T* P, uint64_t seed, int mode, int start, int B, float*
     if (wg_side) fork();
     mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kWte), d, beta), ws);
     mm<T>(LOG, vpad_, false, W(kWte), d, true, M, d, V, ep_store(DT, d), s);
-    fork();
-    layernorm_bwd_params<T>(DT, X(L), stat(4 * L), stat(4 * L + 1), Gp(kLnf), Gp(kLnf + 1), scratch_, M, d, acc, aux_);
-    mark(kRdDT);
-    layernorm_bwd_dx<T>(DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), DX, false, M, d, s);
+    // norm backward: with fuse_ln_ the parameter gradients leave as per-block
+    // partials of the dx kernel (one fold per micro-batch at the end), else a
+    // separate reduction on the side stream reads dy and x again
+    auto norm_bwd = [&](int ni, const T* dy, const T* x, const T* gam, const float* mu, const float* rs, int gi,
+                        bool acc_dx) {
+        if (fuse_ln_) {
+            layernorm_bwd_fused<T>(dy, x, gam, mu, rs, DX, acc_dx, M, d, ln_part(ni), s);
+            return;
+        }
+        fork();
+        layernorm_bwd_params<T>(dy, x, mu, rs, Gp(gi), Gp(gi + 1), scratch_, M, d, acc, aux_);
+        mark(kRdDT);
+        guard(kRdDX);
+        layernorm_bwd_dx<T>(dy, x, gam, mu, rs, DX, acc_dx, M, d, s);
+    };
+    norm_bwd(0, DT, X(L), W(kLnf), stat(4 * L), stat(4 * L + 1), kLnf, false);
     for (int l = L - 1; l >= 0; --l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
           *A = slot(l, sA), *U = slot(l, sU);
         // MLP
         fork();
-        colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, acc, aux_);
-        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_acc(Gp(li(l, 10)), 4 * d, beta), ws);
+        if (!fb_fc2) colsum_add<T>(DX, d, M, d, Gp(li(l, 11)), scratch_, acc, aux_);
+        mm<T>(DX, d, true, U, 4 * d, true, d, 4 * d, M, ep_wg(Gp(li(l, 10)), 4 * d, Gp(li(l, 11)), fb_fc2), ws);
         mark(kRdDX);
         guard(kRdDA);
         mm<T>(DX, d, false, W(li(l, 10)), 4 * d, true, M, 4 * d, d, ep_dgelu(DA, 4 * d, A), s);
         fork();
-        colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, acc, aux_);
-        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_acc(Gp(li(l, 8)), d, beta), ws);
+        if (!fb_fc) colsum_add<T>(DA, 4 * d, M, 4 * d, Gp(li(l, 9)), scratch_, acc, aux_);
+        mm<T>(DA, 4 * d, true, H2, d, true, 4 * d, d, M, ep_wg(Gp(li(l, 8)), d, Gp(li(l, 9)), fb_fc), ws);
         mark(kRdDA);
         guard(kRdDT);
         mm<T>(DA, 4 * d, false, W(li(l, 8)), d, true, M, d, 4 * d, ep_store(DT, d), s);
-        fork();
-        layernorm_bwd_params<T>(DT, XM, stat(4 * l + 2), stat(4 * l + 3), Gp(li(l, 6)), Gp(li(l, 7)), scratch_, M, d,
-                                acc, aux_);
-        mark(kRdDT);
         guard(kRdDX);
-        layernorm_bwd_dx<T>(DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), DX, true, M, d, s);
+        norm_bwd(2 + 2 * l, DT, XM, W(li(l, 6)), stat(4 * l + 2), stat(4 * l + 3), li(l, 6), true);
         // attention
         fork();
-        colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, acc, aux_);
-        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 4)), d, beta), ws);
+        if (!fb_proj) colsum_add<T>(DX, d, M, d, Gp(li(l, 5)), scratch_, acc, aux_);
+        mm<T>(DX, d, true, Y, d, true, d, d, M, ep_wg(Gp(li(l, 4)), d, Gp(li(l, 5)), fb_proj), ws);
         mark(kRdDX);
         guard(kRdDT);
         mm<T>(DX, d, false, W(li(l, 4)), d, true, M, d, d, ep_store(DT, d), s);
         guard(kRdDQKV);
         attention_bwd<T>(QKV, Y, lse_ + static_cast<int64_t>(l) * H * Mmax, DT, DQKV, dsum_, B, Tq, H, H, hd, s);
         fork();
-        colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, aux_);
-        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_acc(Gp(li(l, 2)), d, beta), ws);
+        if (!fb_qkv) colsum_add<T>(DQKV, 3 * d, M, 3 * d, Gp(li(l, 3)), scratch_, acc, aux_);
+        mm<T>(DQKV, 3 * d, true, H1, d, true, 3 * d, d, M, ep_wg(Gp(li(l, 2)), d, Gp(li(l, 3)), fb_qkv), ws);
         mark(kRdDQKV);
         mm<T>(DQKV, 3 * d, false, W(li(l, 2)), d, true, M, d, 3 * d, ep_store(DT, d), s);
-        fork();
-        layernorm_bwd_params<T>(DT, X(l), stat(4 * l), stat(4 * l + 1), Gp(li(l, 0)), Gp(li(l, 1)), scratch_, M, d,
-                                acc, aux_);
-        mark(kRdDT);
         guard(kRdDX);
-        layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s);
+        norm_bwd(1 + 2 * l, DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), li(l, 0), true);
     }
+    if (fuse_ln_) ln_param_fold(ln_fold_, n_ln_, d, ln_part_, G, acc, s);
     // wte rows: the head wgrad stored/added every row; the embedding adds (after it)
     join();
     ACCO_CUDA(cudaStreamWaitEvent(s, ev_sort_, 0));
@@ -551,9 +605,17 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
     // LM head (untied): doutput (+)= dlogits^T hf ; dhf = dlogits output
     mm<T>(LOG, vpad_, true, HF, d, true, V, d, M, ep_acc(Gp(kOut), d, beta), s);
     mm<T>(LOG, vpad_, false, W(kOut), d, true, M, d, V, ep_store(DT, d), s);
-    fork();
-    layernorm_bwd_params<T>(DT, X(L), stat(4 * L), stat(4 * L + 1), Gp(kNorm), nullptr, scratch_, M, d, acc, aux_);
-    layernorm_bwd_dx<T>(DT, X(L), W(kNorm), stat(4 * L), stat(4 * L + 1), DX, false, M, d, s, true);
+    // RMSNorm backward (see run: fused parameter partials, or a side-stream reduction)
+    auto norm_bwd = [&](int ni, const T* x, const T* gam, const float* mu, const float* rs, int gi, bool acc_dx) {
+        if (fuse_ln_) {
+            layernorm_bwd_fused<T>(DT, x, gam, mu, rs, DX, acc_dx, M, d, ln_part(ni), s, true);
+            return;
+        }
+        fork();
+        layernorm_bwd_params<T>(DT, x, mu, rs, Gp(gi), nullptr, scratch_, M, d, acc, aux_);
+        layernorm_bwd_dx<T>(DT, x, gam, mu, rs, DX, acc_dx, M, d, s, true);
+    };
+    norm_bwd(0, X(L), W(kNorm), stat(4 * L), stat(4 * L + 1), kNorm, false);
     for (int l = L - 1; l >= 0; --l) {
         T *H1 = slot(l, sH1), *QKV = slot(l, sQKV), *Y = slot(l, sY), *XM = slot(l, sXM), *H2 = slot(l, sH2),
           *GU = slot(l, sA), *A = slot(l, sU);
@@ -572,10 +634,7 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
         mm<T>(DGU, 2 * F, true, H2, d, true, 2 * F, d, M, ep_acc(Gp(li(l, 4)), d, beta), s);
         join();  // DT (read by the previous norm-weight reduction) is overwritten next
         mm<T>(DGU, 2 * F, false, W(li(l, 4)), d, true, M, d, 2 * F, ep_store(DT, d), s);
-        fork();
-        layernorm_bwd_params<T>(DT, XM, stat(4 * l + 2), stat(4 * l + 3), Gp(li(l, 3)), nullptr, scratch_, M, d, acc,
-                                aux_);
-        layernorm_bwd_dx<T>(DT, XM, W(li(l, 3)), stat(4 * l + 2), stat(4 * l + 3), DX, true, M, d, s, true);
+        norm_bwd(2 + 2 * l, XM, W(li(l, 3)), stat(4 * l + 2), stat(4 * l + 3), li(l, 3), true);
         // attention
         mm<T>(DX, d, true, Y, d, true, d, d, M, ep_acc(Gp(li(l, 2)), d, beta), s);
         join();
@@ -584,11 +643,9 @@ void GPTModel::run_llama(const T* P, uint64_t seed, int mode, int start, int B, 
         rope_apply<T>(DQKV, nqkv, rope_, M, Tq, H + Hk, hd, true, s);
         mm<T>(DQKV, nqkv, true, H1, d, true, nqkv, d, M, ep_acc(Gp(li(l, 1)), d, beta), s);
         mm<T>(DQKV, nqkv, false, W(li(l, 1)), d, true, M, d, nqkv, ep_store(DT, d), s);
-        fork();
-        layernorm_bwd_params<T>(DT, X(l), stat(4 * l), stat(4 * l + 1), Gp(li(l, 0)), nullptr, scratch_, M, d, acc,
-                                aux_);
-        layernorm_bwd_dx<T>(DT, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), DX, true, M, d, s, true);
+        norm_bwd(1 + 2 * l, X(l), W(li(l, 0)), stat(4 * l), stat(4 * l + 1), li(l, 0), true);
     }
+    if (fuse_ln_) ln_param_fold(ln_fold_, n_ln_, d, ln_part_, G, acc, s);
     ACCO_CUDA(cudaStreamWaitEvent(s, ev_sort_, 0));
     embed_bwd<T>(sort_, DX, M, Tq, d, V, Gp(kWte), nullptr, run_sum_, acc, s, !acc);
     join();

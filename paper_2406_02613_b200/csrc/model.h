@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "lm_kernels.h"
 
 namespace acco {
 
@@ -104,6 +105,14 @@ private:
     float* lse_ = nullptr;      // per-layer attention lse
     float* dsum_ = nullptr;
     float* scratch_ = nullptr;  // column-reduce partials
+    // bf16: the norms' parameter gradients as per-block partials of the fused
+    // norm backward (ln_part_ [n_ln][G][2][d]), folded once per micro-batch
+    // through ln_fold_ (device table, entry = norm index, see ln_index)
+    bool fuse_ln_ = false;
+    float* ln_part_ = nullptr;
+    LnFold* ln_fold_ = nullptr;
+    int n_ln_ = 0;
+    float* ln_part(int i) const { return ln_part_ + static_cast<int64_t>(i) * ln_part_blocks() * 2 * c_.d_model; }
     float2* rope_ = nullptr;    // llama: (cos, sin) [seq][hd/2]
     // side stream for the bias / LN-parameter column reductions: they only feed
     // the gradient accumulator, so they run beside the GEMMs (fork/join events)

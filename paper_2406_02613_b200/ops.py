@@ -40,3 +40,10 @@ def gemm(a, a_mn: bool, b, b_mn: bool, m: int, n: int, k: int, c, *, mode=0, bia
               m, n, k, _dtype_code(a), int(_EPI.get(mode, mode)), _ptr(c), c.stride(0),
               _ptr(bias), _ptr(residual), residual.stride(0) if residual is not None else 0,
               _ptr(aux), aux.stride(0) if aux is not None else 0, int(beta), _stream(stream))
+
+
+def gemm_bias_grad(a, a_mn: bool, b, b_mn: bool, m: int, n: int, k: int, c, bias_grad, *, beta=0, stream=None):
+    """C[m,n] (+)= A B^T and bias_grad[m] (+)= row sums of A, bf16 operands;
+    see include/acco.h acco_gemm_bias_grad."""
+    _lib.call("acco_gemm_bias_grad", _ptr(a), a.stride(0), int(a_mn), _ptr(b), b.stride(0), int(b_mn),
+              m, n, k, _ptr(c), c.stride(0), _ptr(bias_grad), int(beta), _stream(stream))

@@ -93,7 +93,7 @@ def test_bf16_bench_shapes_match_bf16_replica(cuda, bench_case):
     g, loss_sum, names = _kernel_grad(m, th_bf, seed, B, cuda)
     # the kernels the bench times at these shapes ran
     # (the LM head forward and weight gradient run on 256-wide CTA-pair tiles)
-    for k in ("gemm_tc_kernel", "fa_fwd_tc2", "fa_bwd_dkv_tc", "fa_bwd_dq_tc", "ln_fwd_vec<3", "ln_bwd_vec<3",
+    for k in ("gemm_tc_kernel", "fa_fwd_tc2", "fa_bwd_dkv_tc", "fa_bwd_dq_tc", "ln_fwd_vec<3", "ln_bwd_vec_p<3", "ln_param_fold",
               "ce_vec_kernel", "f32_to_bf16_rows", "gemm_tc_kernel<256, 5, 0, 0, 0, 2>",
               "gemm_tc_kernel<256, 5, 1, 1, 0, 2>"):
         assert any(k in n for n in names), (k, sorted(names))

@@ -276,3 +276,33 @@ def test_odd_chunk_count_staging_across_tiles(cuda, monkeypatch, force):
     for c in outs:
         assert torch.equal(c, outs[0])
         assert _rel(c, ref) < 2e-6
+
+
+@pytest.mark.parametrize("force", [None, "192,1", "128,1", "192,3", "128,4", "192,1,2", "128,1,2", "128,3,2"])
+@pytest.mark.parametrize("a_mn,b_mn", [(True, True), (False, False), (True, False)])
+def test_bias_grad_fused(cuda, monkeypatch, force, a_mn, b_mn):
+    """Weight gradient with its bias gradient in one launch: the first
+    n-block's tiles add a ones-operand MMA (row sums of A = column sums of dY)
+    into spare TMEM columns; fp32 accumulate (beta) and split-K order as the
+    tile itself. Ragged m / n / k, CTA-pair tiles included."""
+    from paper_2406_02613_b200.ops import gemm_bias_grad
+
+    if force:
+        monkeypatch.setenv("ACCO_GEMM_FORCE", force)
+    m, n, k = 904, 776, 1048  # (m: a pair tile's peer half partly past M)
+    g = torch.Generator().manual_seed(31)
+    a, a_st = _operand(m, k, a_mn, torch.bfloat16, cuda, g)
+    b, b_st = _operand(n, k, b_mn, torch.bfloat16, cuda, g)
+    ref = a.float() @ b.float().t()
+    rs = a.double().sum(dim=1)
+    c = torch.randn(m, n, generator=g).to(cuda)
+    bg = torch.randn(m, generator=g).to(cuda)
+    c0, bg0 = c.clone(), bg.clone()
+    gemm_bias_grad(a_st, a_mn, b_st, b_mn, m, n, k, c, bg, beta=1)
+    torch.cuda.synchronize()
+    assert _rel(c, c0 + ref) < 2e-6
+    assert _rel(bg.double(), bg0.double() + rs) < 2e-6
+    gemm_bias_grad(a_st, a_mn, b_st, b_mn, m, n, k, c, bg, beta=0)
+    torch.cuda.synchronize()
+    assert _rel(c, ref) < 2e-6
+    assert _rel(bg.double(), rs) < 2e-6

@@ -214,3 +214,35 @@ def test_embedding_backward_past_the_old_sort_limits(cuda):
     assert _rel(g1, g2) <= 2e-3
     V, d = c["vocab"], c["d_model"]
     assert _rel(g1[:V * d], g2[:V * d]) <= 2e-3  # the token-embedding rows themselves
+
+
+@pytest.mark.parametrize("arch,d", [("gpt2", 768), ("gpt2", 1024), ("gpt2", 256), ("llama", 2048), ("llama", 512)])
+def test_fused_bias_and_norm_param_grads_match_separate(cuda, arch, d, monkeypatch):
+    """bf16 path: the bias gradients come off the weight-gradient GEMMs
+    (ones-operand MMA) and the norm weights' / biases' gradients from per-block
+    partials of the norm backward folded once per micro-batch; the separate
+    column reductions (ACCO_BIAS_COLSUM=1, ACCO_LN_PARAMS_SEPARATE=1) sum the
+    same bf16 values in another fp32 order: the two agree to fp32 rounding.
+    The fused norm kernel's dx is bitwise the unfused one's, so the weight
+    gradients differ only where the bias restriction (tile width <= 192)
+    changes a weight-gradient GEMM's split-K order."""
+    c = dict(vocab=96, d_model=d, n_layer=2, n_head=max(1, d // 64), seq_len=128, n_samples=8, data_seed=4)
+    if arch == "llama":
+        c.update(arch="llama", n_kv_head=max(1, d // 128), d_ff=2 * d)
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=3))
+    gc = G.GPTConfig(**c)
+    rng = np.random.default_rng(5)
+    th = torch.tensor(G.default_theta0(gc, 2) + 0.02 * rng.standard_normal(m.dim)).to(torch.bfloat16).to(cuda)
+    seed = O.derive(4, 0, 0, 3, 0)
+    g_f, l_f = _grad(m, th, seed, 3, cuda)
+    monkeypatch.setenv("ACCO_BIAS_COLSUM", "1")
+    monkeypatch.setenv("ACCO_LN_PARAMS_SEPARATE", "1")
+    m2 = api.Model(api.LMConfig(**c, precision="bf16", max_batch=3))  # (the norm path is chosen per model)
+    g_s, l_s = _grad(m2, th, seed, 3, cuda)
+    assert l_f == l_s
+    small = np.zeros(m.dim, dtype=bool)  # the column-reduced entries: biases and norm parameters
+    for name, shape, _kind, off in G.param_layout(gc):
+        if len(shape) == 1:
+            small[off:off + shape[0]] = True
+    assert _rel(g_f[~small], g_s[~small]) <= 1e-6
+    assert _rel(g_f[small], g_s[small]) <= 2e-6
