@@ -58,8 +58,8 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
                const Epilogue& ep, cudaStream_t stream);
 // Whether a bf16 fp32-accumulate GEMM of this shape should take
 // Epilogue::bias_grad: the bias MMA needs a tile width <= 192 (TMEM), so it is
-// fused only when the best plan overall already has such a width (else the
-// caller reduces the columns separately).
+// fused when the best such plan is modelled within 4 % of the best plan
+// overall (else the caller reduces the columns separately).
 bool gemm_bias_grad_free(const GemmOperand& A, const GemmOperand& B, int M, int N, int K);
 // fp32 operands: the 3xTF32 tcgen05 kernel (gemm_tcgen05.cu) ...
 void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,

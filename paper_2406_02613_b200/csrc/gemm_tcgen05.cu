@@ -1518,10 +1518,11 @@ bool gemm_bias_grad_free(const GemmOperand& A, const GemmOperand& B, int M, int 
     int bn = 256, sp = 1, cg = 1;
     const double t_free = plan_gemm(A, B, M, N, K, true, false, bn, sp, cg);
     const double t_bias = plan_gemm(A, B, M, N, K, true, true, bn, sp, cg);
-    // only where the restriction costs nothing: the 192-wide alternatives to a
-    // 256-wide best plan measured slower than the model says (GPT-2 medium
-    // fc / fc2 weight gradients, +0.7 ms per step with a 3 us allowance)
-    return t_bias <= t_free * 1.0001;
+    // within 4 % (model): GPT-2 small's fc / fc2 weight gradients (3.3 %; the
+    // restricted 128-wide pair tiles measure faster, 32.1 vs 33.4 us) fuse,
+    // GPT-2 medium's (22 %) and its qkv (5 %) do not — a 3 us allowance fused
+    // those and cost 0.7 ms per step
+    return t_bias <= t_free * 1.04;
 }
 
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep,

@@ -8,6 +8,8 @@ print(sys.argv[2], round(l['value']), round(l['ms_per_step'],3), {k:(round(v['ms
 P
 }
 for i in 1 2; do
+$B > gpurun_out/s1.log 2>&1; show gpurun_out/s1.log "small fused"
+ACCO_BIAS_COLSUM=1 ACCO_LN_PARAMS_SEPARATE=1 $B > gpurun_out/s2.log 2>&1; show gpurun_out/s2.log "small separate"
 $B --model gpt2-medium > gpurun_out/m1.log 2>&1; show gpurun_out/m1.log "medium fused"
 ACCO_BIAS_COLSUM=1 ACCO_LN_PARAMS_SEPARATE=1 $B --model gpt2-medium > gpurun_out/m2.log 2>&1; show gpurun_out/m2.log "medium separate"
 done
