@@ -866,9 +866,10 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 const int row = row0 + lane;
                 if (row < M) {
+                    // (ordered before the next split's reads by this warp's
+                    // __syncwarp()s and lane 0's st.release of the hand-off)
                     float* bg = ep.bias_grad + row;
                     *bg = (sp > 0 || ep.beta) ? *bg + __uint_as_float(bv) : __uint_as_float(bv);
-                    __threadfence();  // visible before this warp's split hand-off (lane 0's release)
                 }
             }
             if (ep.mode == kEpiSwiGLU) {
@@ -1477,7 +1478,7 @@ void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K
 namespace {
 // The planner: tile width, split-K and CTA group with the least modelled time.
 double plan_gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, bool acc_f32, bool bias_grad,
-                 int& best_bn, int& best_sp, int& best_cg) {
+                 int& best_bn, int& best_sp, int& best_cg, bool no_pairs = false) {
     const int sms = num_sms();
     // The LM head's shapes (B too big to stay in L2, whole-M raster: see
     // launch) stream B from HBM once; there the model underrates the 256-wide
@@ -1491,7 +1492,7 @@ double plan_gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K
     best_cg = 1;
     double best = 1e300;
     for (int cg : {1, 2}) {
-        if (cg == 2 && !allow_cg2) continue;
+        if (cg == 2 && (!allow_cg2 || no_pairs)) continue;
         for (int bn : {256, 192, 128}) {
             if (cg == 2 && bn == 192 && (B.mn_major || large_b)) continue;
             if (bias_grad && !has_bias_mma<256>() && bn == 256) continue;  // no TMEM for the bias columns
@@ -1535,7 +1536,10 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
     ProfScope prof(kProfGemm, 2.0 * M * N * K, stream);
     const int sms = num_sms();
     int best_bn = 256, best_sp = 1, best_cg = 1;
-    double best = plan_gemm(A, B, M, N, K, ep.mode == kEpiAccF32, ep.bias_grad != nullptr, best_bn, best_sp, best_cg);
+    // (the dGELU epilogue, which streams the stored GELU slope in, is slower on
+    // pair tiles than the model's store-epilogue fit: fc2 dgrad 41.6 vs 40.4 us)
+    double best = plan_gemm(A, B, M, N, K, ep.mode == kEpiAccF32, ep.bias_grad != nullptr, best_bn, best_sp, best_cg,
+                            ep.mode == kEpiDGelu);
     if (ep.mode == kEpiDSwiGLU) {
         ACCO_REQUIRE(ep.aux && !ep.residual && !ep.bias && N % 32 == 0,
                      "gemm_bf16: DSwiGLU epilogue needs aux, F % 32 == 0, no bias/residual");
