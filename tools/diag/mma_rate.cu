@@ -30,8 +30,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
                      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-template <int M, int N, int CG, int TS, int NACC, int BMN = 0, int LDW = 0>
-__global__ void __launch_bounds__(128 + 32 * LDW, 1) mma_rate(int iters, unsigned long long* out) {
+template <int M, int N, int CG, int TS, int NACC, int BMN = 0, int LDW = 0, int STW = 0, int MW = 0>
+__global__ void __launch_bounds__(128 + 32 * (MW ? MW : (LDW > STW ? LDW : STW)), 1) mma_rate(int iters, unsigned long long* out) {
     extern __shared__ uint8_t raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = sm;                    // 128 rows x 128 B
@@ -108,6 +108,28 @@ __global__ void __launch_bounds__(128 + 32 * LDW, 1) mma_rate(int iters, unsigne
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         out[blockIdx.x] = t1 - t0;
     }
+    if (MW && warp >= 4) {  // softmax-like math warps: ex2 (MUFU) + packed FMA chains
+        float a = threadIdx.x * 1e-3f, b = 0.f;
+        for (int i = 0; i < iters * 8; ++i) {
+            float e;
+            asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(a));
+            b = fmaf(e, 0.999f, b);
+            a = fmaf(a, 0.9999f, -1e-7f);
+        }
+        if (b == 12345.f) out[0] = 1;
+    }
+    if (STW && warp >= 4) {  // TMEM writers (like the backward's P^T / dS^T stores): 32x32b.x16 to columns 384..
+        const uint32_t ta = tmem + 384 + (static_cast<uint32_t>((warp & 3) * 32) << 16) + ((warp >> 2) & 3) * 16;
+        uint32_t v[16];
+        for (int i = 0; i < 16; ++i) v[i] = threadIdx.x * 16 + i;
+        for (int i = 0; i < iters / 2; ++i) {
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                         ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                         "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            v[0] += 1;
+        }
+    }
     if (LDW && warp >= 4) {  // TMEM readers (like softmax warps): 32x32b.x32 loads from columns 384.. of their quadrant
         const uint32_t ta = tmem + 384 + (static_cast<uint32_t>((warp & 3) * 32) << 16);
         uint32_t acc = 0;
@@ -140,18 +162,18 @@ __global__ void __launch_bounds__(128 + 32 * LDW, 1) mma_rate(int iters, unsigne
     }
 }
 
-template <int M, int N, int CG, int TS, int NACC, int BMN = 0, int LDW = 0>
+template <int M, int N, int CG, int TS, int NACC, int BMN = 0, int LDW = 0, int STW = 0, int MW = 0>
 void run(const char* name) {
     const int iters = 2000, nsm = 148;
     unsigned long long* d;
     cudaMalloc(&d, nsm * 8);
     cudaMemset(d, 0, nsm * 8);
-    auto k = mma_rate<M, N, CG, TS, NACC, BMN, LDW>;
+    auto k = mma_rate<M, N, CG, TS, NACC, BMN, LDW, STW, MW>;
     const int smem = 1024 + 128 * 128 + (BMN ? 64 * 128 * ((N / CG + 63) / 64) : (N / CG) * 128);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nsm);
-    cfg.blockDim = dim3(128 + 32 * LDW);
+    cfg.blockDim = dim3(128 + 32 * (MW ? MW : (LDW > STW ? LDW : STW)));
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -176,7 +198,92 @@ void run(const char* name) {
     cudaFree(d);
 }
 
+
+// The dK/dV kernel's per-tile MMA pattern back to back, no softmax in between:
+// 4 k-slices x (S^T = K Q^T, dP^T = V dO^T) SS MMAs (N = 128) into two
+// accumulators, commit; then 8 x (dV += P^T dO, dK += dS^T Q) TS MMAs (N = 64,
+// A from TMEM, MN-major B), commit; Q/dO cycling over a 4-stage ring.
+__global__ void __launch_bounds__(128, 1) dkv_pattern(int tiles, unsigned long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    // K, V (16 KB each) + 4 stages x (Q, dO) (16 KB each)
+    __shared__ uint64_t bar[2];
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 10 * 16384 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(sm)[i] = make_uint4(0x3c003c00u, 0x3c003c00u, 0x3c003c00u, 0x3c003c00u);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tslot;
+    if (warp == 1 && (threadIdx.x & 31) == 0) {
+        constexpr uint32_t id_s = idesc_bf16(128, 128, 0);
+        constexpr uint32_t id_g = idesc_bf16(128, 64, 1);
+        const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tPT = tmem + 384, tDST = tmem + 448;
+        unsigned long long t0, t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (int g = 0; g < tiles; ++g) {
+            const int st = g & 3;
+            const uint64_t kd = sdesc(smem_u32(sm), 16, 1024), vd = sdesc(smem_u32(sm + 16384), 16, 1024);
+            const uint64_t qd = sdesc(smem_u32(sm + 32768 + st * 32768), 16, 1024);
+            const uint64_t od = sdesc(smem_u32(sm + 32768 + st * 32768 + 16384), 16, 1024);
+            for (int kk = 0; kk < 4; ++kk) {
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                             ::"r"(tS), "l"(kd + 2 * kk), "l"(qd + 2 * kk), "r"(id_s), "r"(kk > 0 ? 1u : 0u));
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                             ::"r"(tP), "l"(vd + 2 * kk), "l"(od + 2 * kk), "r"(id_s), "r"(kk > 0 ? 1u : 0u));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar[0])) : "memory");
+            const uint64_t qm = sdesc(smem_u32(sm + 32768 + st * 32768), 64 * 128, 1024);
+            const uint64_t om = sdesc(smem_u32(sm + 32768 + st * 32768 + 16384), 64 * 128, 1024);
+            for (int kk = 0; kk < 8; ++kk) {
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+                             ::"r"(tDV), "r"(tPT + kk * 8), "l"(om + 128 * kk), "r"(id_g), "r"(1u));
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+                             ::"r"(tDK), "r"(tDST + kk * 8), "l"(qm + 128 * kk), "r"(id_g), "r"(1u));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar[1])) : "memory");
+        }
+        mbar_wait(&bar[1], (tiles - 1) & 1);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        out[blockIdx.x] = (t1 - t0) / tiles;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+void run_dkv_pattern() {
+    unsigned long long* d;
+    cudaMalloc(&d, 148 * 8);
+    const int smem = 1024 + 10 * 16384;
+    cudaFuncSetAttribute(dkv_pattern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    dkv_pattern<<<148, 128, smem>>>(400, d);
+    dkv_pattern<<<148, 128, smem>>>(400, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    unsigned long long h[148];
+    cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    double s = 0;
+    for (auto v : h) s += v;
+    printf("{\"pattern\": \"dK/dV tile: 8 SS N=128 + commit, 16 TS N=64 + commit\", \"ns_per_tile\": %.0f, "
+           "\"isolated_rate_estimate_ns\": %.0f, \"err\": \"%s\"}\n", s / 148, 8 * 35.5 + 16 * 25.3, cudaGetErrorString(e));
+}
+
 int main() {
+    run_dkv_pattern();
+    run<128, 128, 1, 0, 2, 0, 0, 0, 16>("SS + 16 ex2/FMA warps");
+    run<128, 64, 1, 1, 2, 1, 0, 0, 16>("TS MN-B + 16 ex2/FMA warps");
+    run<128, 64, 1, 1, 2, 1, 0, 16>("TS MN-B + 16 st warps");
+    run<128, 128, 1, 0, 2, 0, 0, 16>("SS + 16 st warps");
     run<128, 64, 1, 1, 2, 1, 0>("TS MN-B");
     run<128, 64, 1, 1, 2, 1, 16>("TS MN-B + 16 ld warps");
     run<128, 64, 1, 1, 2, 0, 16>("TS + 16 ld warps");
