@@ -17,6 +17,7 @@
 // stream waits on the event before starting the next stage), which makes
 // micro-batch counts bit-exact and replayable by the oracle.
 #include "engine.h"
+#include "gemm.h"
 #include "lm_kernels.h"
 
 #include <algorithm>
@@ -93,6 +94,9 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
         ACCO_REQUIRE(sim.schedule != kAdaptive || n_local_ == 1,
                      "adaptive schedule needs one worker per device (NCCL mode)");
     }
+    // collectives beside compute (real ranks or an emulated interconnect):
+    // CTA-pair GEMMs take their tiles from a work queue (gemm_set_pair_queue)
+    gemm_set_pair_queue(world_ > 1 || sim.comm_delay_ns > 0 || sim.comm_standin_ctas > 0);
     psi_ = model->num_params();
     layout_ = shard_partition(static_cast<uint64_t>(psi_), sim.n_workers);
     const bool sharded = (comm_ || peer_) && method_ != kDDP;

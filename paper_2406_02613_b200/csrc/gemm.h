@@ -61,6 +61,9 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
 // fused when the best such plan is modelled within 4 % of the best plan
 // overall (else the caller reduces the columns separately).
 bool gemm_bias_grad_free(const GemmOperand& A, const GemmOperand& B, int M, int N, int K);
+// CTA-pair tiles: take units from a work queue instead of the static
+// persistent order (set by the trainer when collectives run beside compute).
+void gemm_set_pair_queue(bool on);
 // fp32 operands: the 3xTF32 tcgen05 kernel (gemm_tcgen05.cu) ...
 void gemm_f32_tc(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
                  const Epilogue& ep, cudaStream_t stream);

@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <set>
 #include <string>
@@ -334,6 +335,12 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
 // K-major tile without swizzle (four 8 x 8 core matrices, 512 B).
 template <int BN, int X3 = 0>
 constexpr bool has_bias_mma() { return !X3 && BN <= 192; }
+// CTA-pair work queue: slots between the leader's producer, which claims each
+// next unit one unit ahead of loading it, and the slowest reader (the epilogue warps
+// read a unit's successor after that unit's epilogue; the producer is at most
+// ~2 units ahead of them)
+constexpr int kQueue = 3;
+constexpr int kRespBytes = 4 * kQueue > 16 ? (4 * kQueue + 15) / 16 * 16 : 16;  // CLC response / queue slots
 constexpr int kOnesBytes = 512;
 template <int BN, int STAGES, int X3 = 0, int CG = 1>
 constexpr int smem_bytes() {
@@ -341,7 +348,8 @@ constexpr int smem_bytes() {
            STAGES * (kBM + BN / CG) * 128 * (X3 ? 2 : 1) +
            epi_warps<BN, STAGES, X3>() * epi_warp_bytes<BN, STAGES>() +
            (2 * STAGES + 4 + epi_warps<BN, STAGES, X3>() * in_bufs<BN>()) * 8 + 16 +
-           48 /* CLC: full / empty mbarriers, 16 B response, alignment */;
+           48 /* CLC: full / empty mbarriers, 16 B response, alignment */ +
+           2 * (kQueue - 1) * 8 + (kRespBytes - 16) /* the CTA-pair work queue's further slots */;
 }
 
 struct Sched {
@@ -445,7 +453,7 @@ template <int BN, int STAGES, int A_MN, int B_MN, int X3 = 0, int CG = 1>
 __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ EpiMaps em, int M, int N, Sched sc, Epilogue ep, int* split_sem,
-                   int use_clc) {
+                   int use_clc, int* __restrict__ work_ctr) {
     static_assert(!X3 || (!A_MN && !B_MN), "3xTF32: the split pre-pass writes K-major planes");
     static_assert(CG == 1 || (!X3 && (!B_MN || (BN / 2) % 64 == 0)), "CTA pairs: bf16, B half a whole MN atom");
     extern __shared__ uint8_t smem_raw[];
@@ -467,10 +475,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     uint64_t* tfull = empty + STAGES;  // [2]
     uint64_t* tempty = tfull + 2;      // [2]
     uint64_t* inbar = tempty + 2;      // [8 epilogue warps][kInBuf]
-    uint64_t* clc_full = inbar + kEpiWarps * kInBuf;  // CLC response ready (1 arrive + 16 B tx)
-    uint64_t* clc_empty = clc_full + 1;                // every role warp has read it
-    uint8_t* clc_resp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(clc_empty + 1) + 15) & ~uintptr_t(15));
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(clc_resp + 16);
+    // CLC response ready (1 arrive + 16 B tx) / every role warp has read it;
+    // the CTA-pair work queue uses kQueue slots of each (response ints in clc_resp)
+    uint64_t* clc_full = inbar + kEpiWarps * kInBuf;
+    uint64_t* clc_empty = clc_full + kQueue;
+    uint8_t* clc_resp = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(clc_empty + kQueue) + 15) & ~uintptr_t(15));
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(clc_resp + kRespBytes);
     uint8_t* sOnes = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 127) & ~uintptr_t(127));
     constexpr bool kBiasMma = has_bias_mma<BN, X3>();
 
@@ -492,8 +502,12 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             mbar_init(&tempty[a], CG * kEpiWarps);  // one arrive per epilogue warp (of both CTAs of a pair)
         }
         for (int i = 0; i < kEpiWarps * kInBuf; ++i) mbar_init(&inbar[i], 1);
-        mbar_init(clc_full, 1);
-        mbar_init(clc_empty, 2 + kEpiWarps);  // producer, MMA issuer, epilogue warps
+        for (int q = 0; q < kQueue; ++q) mbar_init(&clc_full[q], 1);
+        // producer, MMA issuer, epilogue warps (a CTA pair's work queue: both
+        // producers and all epilogue warps arrive on the leader's)
+        // (a CTA pair's queue: the peer's producer, the MMA issuer and every
+        // epilogue warp of both CTAs read a claim; the leader's producer writes it)
+        for (int q = 0; q < kQueue; ++q) mbar_init(&clc_empty[q], CG == 2 ? 2 * kEpiWarps + 2 : 2 + kEpiWarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -539,27 +553,69 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     // just launch fewer CTAs, and the running ones absorb the work instead of
     // a static tile list waiting for its SM. Warp 3 claims one unit ahead; the
     // role warps read each claim from smem and release it.
+    // CTA pairs (use_clc with CG == 2): cluster launch control over clusters
+    // measured slow, so the pairs are persistent and, after their first unit,
+    // take units from a per-stream counter in unit order (work_ctr[0]): the
+    // leader's producer claims the next unit while it loads the current one (a
+    // pair holds at most one unstarted claim) and posts the claim into
+    // both CTAs' smem for the other role warps. Pairs that start late (SMs held
+    // by the comm stream) just claim fewer units. The last pair to retire
+    // resets the counter for the next launch on the stream.
     int clc_i = 0;
+    // the leader producer's claim for the unit after the current one, issued
+    // when the current one starts (its latency hides under that unit's loads)
+    int pending = 0;
+    if (CG == 2 && use_clc && warp == 0 && rank == 0 && lane == 0) pending = atomicAdd(work_ctr, 1);
+    auto claim_next = [&]() -> int {  // the leader's producer (CG == 2 queue)
+        const int q = clc_i % kQueue;
+        if (clc_i >= kQueue) mbar_wait_cluster(&clc_empty[q], (clc_i / kQueue - 1) & 1);  // slot read by all
+        int nu = -1;
+        if (lane == 0) {
+            const int c = pending;
+            nu = c + unit_stride < nunits ? c + unit_stride : -1;
+            if (nu >= 0) pending = atomicAdd(work_ctr, 1);
+            reinterpret_cast<volatile int*>(clc_resp)[q] = nu;
+            asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(mapa(clc_resp + 4 * q, 1)), "r"(nu) : "memory");
+            mbar_arrive_cluster(mapa(&clc_full[q], 0));
+            mbar_arrive_cluster(mapa(&clc_full[q], 1));  // (release: the peer's response store before it)
+            if (nu < 0 && atomicAdd(work_ctr + 1, 1) == unit_stride - 1) {  // every pair has stopped claiming
+                atomicExch(work_ctr, 0);
+                atomicExch(work_ctr + 1, 0);
+            }
+        }
+        ++clc_i;
+        return __shfl_sync(0xffffffffu, nu, 0);
+    };
     auto next_unit = [&](int u) -> int {
         if (!use_clc) return u + unit_stride < nunits ? u + unit_stride : -1;
-        mbar_wait(clc_full, clc_i & 1);
+        if (CG == 2) {
+            if (warp == 0 && rank == 0) return claim_next();
+            const int q = clc_i % kQueue;
+            mbar_wait_cluster(&clc_full[q], (clc_i / kQueue) & 1);
+            const int nu = reinterpret_cast<volatile int*>(clc_resp)[q];
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa(&clc_empty[q], 0));
+            ++clc_i;
+            return nu;
+        }
+        mbar_wait(&clc_full[0], clc_i & 1);
         const int nu = clc_decode(clc_resp);
         fence_async_smem();  // the async proxy rewrites the response next
         __syncwarp();
-        if (lane == 0) mbar_arrive(clc_empty);
+        if (lane == 0) mbar_arrive(&clc_empty[0]);
         ++clc_i;
         return nu;
     };
 
-    if (warp == 3 && use_clc) {
+    if (warp == 3 && use_clc && CG == 1) {
         for (int i = 0;; ++i) {
-            if (i > 0) mbar_wait(clc_empty, (i - 1) & 1);  // every role warp has read claim i-1
+            if (i > 0) mbar_wait(&clc_empty[0], (i - 1) & 1);  // every role warp has read claim i-1
             if (elect_one()) {
-                mbar_expect_tx(clc_full, 16);
-                clc_try_cancel(clc_resp, clc_full);
+                mbar_expect_tx(&clc_full[0], 16);
+                clc_try_cancel(clc_resp, &clc_full[0]);
             }
             __syncwarp();
-            mbar_wait(clc_full, i & 1);
+            mbar_wait(&clc_full[0], i & 1);
             if (clc_decode(clc_resp) < 0) break;  // no unlaunched CTA left
         }
     } else if (warp == 0) {
@@ -1132,6 +1188,34 @@ int* split_semaphores(cudaStream_t stream) {
     return sem;
 }
 
+// CTA-pair scheduling: static persistent order (fastest with the GPU to
+// itself: qkv_fwd 23.4 vs 27.4 us) or the work queue (robust when another
+// stream's kernels hold SMs: under the emulated 8-GPU interconnect ACCO 742.9k
+// vs 719.1k tok/s, 1.021x vs 0.973x ZeRO-1). The trainer turns the queue on
+// when collectives run beside compute (world > 1 or an emulated interconnect);
+// ACCO_PAIR_STATIC / ACCO_PAIR_DYNAMIC override.
+std::atomic<int> g_pair_queue{0};
+bool pair_queue_on() {
+    const bool st = std::getenv("ACCO_PAIR_STATIC") != nullptr, dy = std::getenv("ACCO_PAIR_DYNAMIC") != nullptr;
+    return dy || (!st && g_pair_queue.load(std::memory_order_relaxed) != 0);
+}
+
+// CTA-pair work-queue counters ([claimed, retired]) per (device, stream),
+// like the split-K semaphores: launches on one stream are ordered, the last
+// pair of each launch resets them
+int* work_counters(cudaStream_t stream) {
+    static std::map<StreamKey, int*> ctrs;
+    int dev = 0;
+    ACCO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    int*& c = ctrs[StreamKey{dev, stream}];
+    if (!c) {
+        ACCO_CUDA(cudaMalloc(&c, 32 * sizeof(int)));
+        ACCO_CUDA(cudaMemset(c, 0, 32 * sizeof(int)));
+    }
+    return c;
+}
+
 template <int BN, int STAGES, int A_MN, int B_MN, int CG>
 void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const Epilogue& ep, int splits,
             cudaStream_t stream) {
@@ -1199,13 +1283,17 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     // the SwiGLU gate / up halves)
     CUtensorMap tb = operand_map(B, N, K, (ep.mode == kEpiSwiGLU || CG == 2) ? BN / 2 : BN);
     if (CG == 2) {
-        // persistent CTA pairs in static unit order. (Cluster launch control
-        // over pairs — one cluster per unit, the leader cancelling a whole
-        // cluster with a multicast response — was measured slower than the
-        // static order on every shape: qkv_fwd 26.2 vs 23.2 us, head_fwd 539 vs
-        // 452 us, profiles/r02_summary.md.)
+        // persistent CTA pairs; unless split-K (whose ordered hand-off needs the
+        // static order) the units after each pair's first come from a per-stream
+        // counter (see the kernel). (Cluster launch control over pairs — one
+        // cluster per unit, the leader cancelling a whole cluster with a
+        // multicast response — was measured slower than the static order on
+        // every shape: qkv_fwd 26.2 vs 23.2 us, head_fwd 539 vs 452 us,
+        // profiles/r02_summary.md.)
+        const int q = use_clc(sc) && pair_queue_on() ? 1 : 0;
         const int grid = 2 * std::min(sc.units(), max_pairs);
-        launch_pdl_cluster(kern, 2, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, 0);
+        launch_pdl_cluster(kern, 2, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, q,
+                           q ? work_counters(stream) : static_cast<int*>(nullptr));
         ACCO_CHECK_LAUNCH();
         return;
     }
@@ -1213,7 +1301,8 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
     // hand-off assumes the static unit order
     const int clc = use_clc(sc) ? 1 : 0;
     const int grid = clc ? sc.units() : std::min(sc.units(), num_sms());
-    launch_pdl(kern, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, clc);
+    launch_pdl(kern, grid, gemm_threads<BN, STAGES>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, clc,
+               static_cast<int*>(nullptr));
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1414,7 +1503,8 @@ void launch_x3(const float* a_planes, const float* b_planes, int64_t kp, int M, 
     const CUtensorMap ta = planes(a_planes, M, kBM), tb = planes(b_planes, N, BN);
     const int clc = use_clc(sc) ? 1 : 0;
     const int grid = clc ? sc.units() : std::min(sc.units(), num_sms());
-    launch_pdl(kern, grid, gemm_threads<BN, STAGES, 1>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, clc);
+    launch_pdl(kern, grid, gemm_threads<BN, STAGES, 1>(), smem, stream, ta, tb, em, M, N, sc, ep, sem, clc,
+               static_cast<int*>(nullptr));
     ACCO_CHECK_LAUNCH();
 }
 
@@ -1513,6 +1603,8 @@ double plan_gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K
     return best;
 }
 }  // namespace
+
+void gemm_set_pair_queue(bool on) { g_pair_queue.store(on ? 1 : 0, std::memory_order_relaxed); }
 
 bool gemm_bias_grad_free(const GemmOperand& A, const GemmOperand& B, int M, int N, int K) {
     if (std::getenv("ACCO_GEMM_FORCE")) return true;

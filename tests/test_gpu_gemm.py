@@ -306,3 +306,36 @@ def test_bias_grad_fused(cuda, monkeypatch, force, a_mn, b_mn):
     torch.cuda.synchronize()
     assert _rel(c, ref) < 2e-6
     assert _rel(bg.double(), rs) < 2e-6
+
+
+@pytest.mark.parametrize("force", ["256,1,2", "128,1,2", "192,1,2"])
+def test_cta_pair_work_queue(cuda, monkeypatch, force):
+    """CTA-pair tiles taking their units from the per-stream work queue (the
+    mode the trainer selects when collectives run beside compute): the same
+    result as the static order, bitwise, over repeated launches (the queue
+    resets itself at the end of each launch), every epilogue kind."""
+    monkeypatch.setenv("ACCO_GEMM_FORCE", force)
+    m, n, k = 2000, 1000, 320
+    g = torch.Generator().manual_seed(41)
+    a = torch.randn(m, k, generator=g).to(torch.bfloat16).to(cuda)
+    b = torch.randn(n, k, generator=g).to(torch.bfloat16).to(cuda)
+    ref = a.float() @ b.float().t()
+    outs = {}
+    for mode in ("ACCO_PAIR_STATIC", "ACCO_PAIR_DYNAMIC", "ACCO_PAIR_DYNAMIC"):
+        monkeypatch.delenv("ACCO_PAIR_STATIC", raising=False)
+        monkeypatch.delenv("ACCO_PAIR_DYNAMIC", raising=False)
+        monkeypatch.setenv(mode, "1")
+        c = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+        gemm(a, False, b, False, m, n, k, c)
+        aux = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+        cg = torch.empty(m, n, dtype=torch.bfloat16, device=cuda)
+        gemm(a, False, b, False, m, n, k, cg, mode=1, aux=aux)
+        c32 = torch.zeros(m, n, device=cuda)
+        gemm(a, False, b, False, m, n, k, c32, mode=3, beta=1)
+        torch.cuda.synchronize()
+        assert _rel(c, ref) < 6e-3 and _rel(c32, ref) < 2e-6
+        outs.setdefault(mode, []).append((c, cg, aux, c32))
+    (s,) = outs["ACCO_PAIR_STATIC"]
+    for d in outs["ACCO_PAIR_DYNAMIC"]:
+        for x, y in zip(s, d):
+            assert torch.equal(x, y)
