@@ -223,6 +223,11 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// relaxed: the arriving warp only reports that it has read a slot (its value is
+// already in registers), nothing it wrote must become visible
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -335,10 +340,11 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
 // K-major tile without swizzle (four 8 x 8 core matrices, 512 B).
 template <int BN, int X3 = 0>
 constexpr bool has_bias_mma() { return !X3 && BN <= 192; }
-// CTA-pair work queue: slots between the leader's producer, which claims each
-// next unit one unit ahead of loading it, and the slowest reader (the epilogue warps
-// read a unit's successor after that unit's epilogue; the producer is at most
-// ~2 units ahead of them)
+// CTA-pair work queue: slots between the leader's producer, which posts each
+// unit's successor when it starts the unit (claimed by an atomic issued one
+// unit earlier), and the slowest reader (the epilogue warps read a unit's
+// successor after that unit's epilogue; the producer is at most ~2 units
+// ahead of them)
 constexpr int kQueue = 3;
 constexpr int kRespBytes = 4 * kQueue > 16 ? (4 * kQueue + 15) / 16 * 16 : 16;  // CLC response / queue slots
 constexpr int kOnesBytes = 512;
@@ -556,8 +562,8 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     // CTA pairs (use_clc with CG == 2): cluster launch control over clusters
     // measured slow, so the pairs are persistent and, after their first unit,
     // take units from a per-stream counter in unit order (work_ctr[0]): the
-    // leader's producer claims the next unit while it loads the current one (a
-    // pair holds at most one unstarted claim) and posts the claim into
+    // leader's producer posts the successor of each unit as it starts loading
+    // it (a pair holds at most two unstarted claims) into
     // both CTAs' smem for the other role warps. Pairs that start late (SMs held
     // by the comm stream) just claim fewer units. The last pair to retire
     // resets the counter for the next launch on the stream.
@@ -586,15 +592,16 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         ++clc_i;
         return __shfl_sync(0xffffffffu, nu, 0);
     };
+    int lead_next = -1;  // the leader producer: the successor it posted when starting the current unit
     auto next_unit = [&](int u) -> int {
         if (!use_clc) return u + unit_stride < nunits ? u + unit_stride : -1;
         if (CG == 2) {
-            if (warp == 0 && rank == 0) return claim_next();
+            if (warp == 0 && rank == 0) return lead_next;
             const int q = clc_i % kQueue;
             mbar_wait_cluster(&clc_full[q], (clc_i / kQueue) & 1);
             const int nu = reinterpret_cast<volatile int*>(clc_resp)[q];
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(mapa(&clc_empty[q], 0));
+            if (lane == 0) mbar_arrive_cluster_relaxed(mapa(&clc_empty[q], 0));
             ++clc_i;
             return nu;
         }
@@ -623,6 +630,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
         {
             int it = 0;
             for (int u = cta_unit0; u >= 0; u = next_unit(u)) {
+                // (pair queue: the leader posts this unit's successor as it starts the
+                // unit, so the peer's producer never waits on it)
+                if (CG == 2 && use_clc && rank == 0) lead_next = claim_next();
                 int mb, nb, sp;
                 decode(sc, u, mb, nb, sp);
                 const int m0 = mb * (kBM * CG) + static_cast<int>(rank) * kBM, n0 = nb * BN;
