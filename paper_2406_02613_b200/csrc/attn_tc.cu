@@ -16,6 +16,7 @@
 // S of tile j+1 is issued while the softmax of tile j runs.
 #include "common.cuh"
 
+#include <atomic>
 #include <cmath>
 #include <algorithm>
 #include <cstdlib>
@@ -45,6 +46,22 @@ constexpr float kLog2e = 1.4426950408889634f;
 // dealing would give them to (GQA dK/dV: 1.56x -> ~1.1x of the mean load).
 __device__ __forceinline__ int item_at(const int* __restrict__ sched, int k_max, int k) {
     return k < k_max ? __ldg(sched + static_cast<int64_t>(blockIdx.x) * k_max + k) : -1;
+}
+// Dynamic alternative (when collectives run beside compute and hold SMs, a
+// static table waits for its late CTAs): items in the same heaviest-first
+// order, each CTA's producer warp claiming the next one from a per-stream
+// counter (list scheduling) and publishing it into the CTA's smem list, one
+// item ahead of its own loads (a CTA holds at most two unstarted claims).
+// ctr == nullptr: the static table. The last CTA to retire resets ctr.
+struct ItemQueue {
+    const int* order;  // items, heaviest first
+    int n;
+    int* ctr;          // [claimed, retired] or nullptr
+};
+constexpr int kItemQ = 64;  // smem list entries per CTA (the last is always -1)
+__device__ __forceinline__ int iq_claim(const ItemQueue& q) {
+    const int c = atomicAdd(q.ctr, 1);
+    return c < q.n ? __ldg(q.order + c) : -1;
 }
 #ifdef ACCO_FWD_PROBE  // timeline probe of fa_fwd_tc2 (tools/diag/fwd_probe.cu only)
 __device__ unsigned long long g_probe[148][10][128];
@@ -509,7 +526,9 @@ __device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m
 // O tile 1 [320,384).
 __global__ void __launch_bounds__(F2_THREADS, 1)
     fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
-               int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
+               int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk, ItemQueue iq) {
+    __shared__ uint64_t q_ready[kItemQ];
+    __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                         // [2 items][2 tiles]
@@ -549,6 +568,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     };
 
     if (threadIdx.x == 0) {
+        for (int q = 0; q < kItemQ; ++q) mbar_init(&q_ready[q], 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
@@ -576,11 +596,52 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     const uint32_t tmem = *tslot;
     pdl_trigger();
     pdl_wait();
+    // the item sequence of this CTA: the static LPT table, or the dynamic queue
+    // (q_list filled by the producer warp, q_ready[k] completes when entry k is in)
+    auto citem = [&](int k) -> int {
+        if (!iq.ctr) return item_at(sched, sk, k);
+        if (k >= kItemQ) return -1;
+        mbar_wait(&q_ready[k], 0);
+        return *reinterpret_cast<volatile int*>(&q_list[k]);
+    };
+    // producer warp: publish entry k + 1 as item k starts (claimed during item
+    // k - 1), claim for entry k + 2; entry kItemQ - 1 is always the end marker
+    int q_pend = -1;
+    auto q_publish = [&](int k, int u) {
+        q_list[k] = u;
+        mbar_arrive(&q_ready[k]);
+    };
+    auto q_retire = [&]() {  // after the end marker: no claim of this CTA is left; the last CTA resets
+        if (atomicAdd(iq.ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+            atomicExch(iq.ctr, 0);
+            atomicExch(iq.ctr + 1, 0);
+        }
+    };
+    auto q_start = [&]() {  // producer lane 0, before the first item
+        const int c0 = iq_claim(iq);
+        q_publish(0, c0);
+        q_pend = c0 >= 0 ? iq_claim(iq) : -1;
+        if (c0 < 0) q_retire();
+    };
+    auto q_next = [&](int k) {  // producer lane 0, as item k starts
+        const int nx = k + 1 <= kItemQ - 2 ? q_pend : -1;
+        q_publish(k + 1, nx);
+        q_pend = nx >= 0 && k + 2 <= kItemQ - 2 ? iq_claim(iq) : -1;
+        if (nx < 0) q_retire();
+    };
 
     if (warp == 0) {
         {  // warp-wide walk and waits, one elected lane issues
             int kvit = 0, ni = 0;
-            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+            if (iq.ctr) {  // dynamic queue: entry 0 (and the claim for entry 1)
+                if (lane == 0) q_start();
+                __syncwarp();
+            }
+            for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
+                if (iq.ctr) {  // publish entry k + 1 as item k starts
+                    if (lane == 0) q_next(k);
+                    __syncwarp();
+                }
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
                 const int qs = ni & 1;
@@ -615,7 +676,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         int pc_s = 0, pc_pv = 0;
         (void)pc_s;
         (void)pc_pv;
-        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+        for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
             const Item w = item_of(u);
             const int nt[2] = {w.nt0, w.nt1};
             const int qs = ni & 1;
@@ -693,7 +754,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         float* lsum = red + 4 * 128;                                                                  // [2][128] sums
         const int bar_id = 2 + x * 4 + wq;  // the quadrant's two warps
         int cnt = 0, nitem = 0;  // tiles / items this slot has processed (barrier phases)
-        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
+        for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
             const Item w = item_of(u);
             const int n = x == 0 ? w.nt0 : w.nt1;
             if (n == 0) continue;  // absent tile (odd tile count): no phases consumed
@@ -925,7 +986,9 @@ constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + (BW_SOF
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                   const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                  int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
+                  int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk, ItemQueue iq) {
+    __shared__ uint64_t q_ready[kItemQ];
+    __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sK = smem;                    // [2 items]
@@ -966,6 +1029,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     };
 
     if (threadIdx.x == 0) {
+        for (int q = 0; q < kItemQ; ++q) mbar_init(&q_ready[q], 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&kv_full[s], 1);
             mbar_init(&kv_empty[s], 1);
@@ -992,6 +1056,39 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t tmem = *tslot;
     pdl_trigger();
     pdl_wait();
+    // the item sequence of this CTA: the static LPT table, or the dynamic queue
+    // (q_list filled by the producer warp, q_ready[k] completes when entry k is in)
+    auto citem = [&](int k) -> int {
+        if (!iq.ctr) return item_at(sched, sk, k);
+        if (k >= kItemQ) return -1;
+        mbar_wait(&q_ready[k], 0);
+        return *reinterpret_cast<volatile int*>(&q_list[k]);
+    };
+    // producer warp: publish entry k + 1 as item k starts (claimed during item
+    // k - 1), claim for entry k + 2; entry kItemQ - 1 is always the end marker
+    int q_pend = -1;
+    auto q_publish = [&](int k, int u) {
+        q_list[k] = u;
+        mbar_arrive(&q_ready[k]);
+    };
+    auto q_retire = [&]() {  // after the end marker: no claim of this CTA is left; the last CTA resets
+        if (atomicAdd(iq.ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+            atomicExch(iq.ctr, 0);
+            atomicExch(iq.ctr + 1, 0);
+        }
+    };
+    auto q_start = [&]() {  // producer lane 0, before the first item
+        const int c0 = iq_claim(iq);
+        q_publish(0, c0);
+        q_pend = c0 >= 0 ? iq_claim(iq) : -1;
+        if (c0 < 0) q_retire();
+    };
+    auto q_next = [&](int k) {  // producer lane 0, as item k starts
+        const int nx = k + 1 <= kItemQ - 2 ? q_pend : -1;
+        q_publish(k + 1, nx);
+        q_pend = nx >= 0 && k + 2 <= kItemQ - 2 ? iq_claim(iq) : -1;
+        if (nx < 0) q_retire();
+    };
     // TMEM: S^T | dP^T (fp32, 128 cols each) | dV | dK (64 each) | P^T | dS^T
     // (bf16 pairs, 64 cols each): the dV/dK MMAs take A straight from TMEM, so
     // P^T/dS^T never touch shared memory, and S^T/dP^T of the next tile can
@@ -1002,7 +1099,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     if (warp == 0) {
         {  // warp-wide walk and waits, one elected lane issues
             int it = 0, ni = 0;
-            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+            if (iq.ctr) {  // dynamic queue: entry 0 (and the claim for entry 1)
+                if (lane == 0) q_start();
+                __syncwarp();
+            }
+            for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
+                if (iq.ctr) {  // publish entry k + 1 as item k starts
+                    if (lane == 0) q_next(k);
+                    __syncwarp();
+                }
                 const Item w = item_of(u);
                 const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
                 const int row_base = w.b * T;
@@ -1052,15 +1157,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             __syncwarp();
         };
         int it = 0, ni = 0;
-        if (item_at(sched, sk, 0) >= 0) {
+        if (citem(0) >= 0) {
             mbar_wait(&kv_full[0], 0);
             issue_s(0, 0);
         }
-        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+        for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
             const Item w = item_of(u);
             const int niter = G * w.nq;
             const int kb = ni & 1;
-            const bool more = item_at(sched, sk, k + 1) >= 0;
+            const bool more = citem(k + 1) >= 0;
             for (int i = 0; i < niter; ++i) {
                 const int g = it + i;
                 const int s = g % DKV_ST;
@@ -1120,7 +1225,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             dv = __ldg(dsum + bh * T + q);
         };
         float nl = 0.f, nd = 0.f;
-        fetch(item_at(sched, sk, 0), 0, nl, nd);
+        fetch(citem(0), 0, nl, nd);
         // dK/dV of item `prev` leave TMEM -> global: deferred into the next
         // item's first tile (after its exp/dS math, which overlaps the item's
         // last dV/dK MMAs), or after the loop for the CTA's last item
@@ -1136,7 +1241,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
         };
         int it = 0;
-        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
+        for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
             const Item w = item_of(u);
             const int niter = G * w.nq;
             const int k0 = w.kt * BW_T;
@@ -1154,7 +1259,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 if (i + 1 < niter)
                     fetch(u, i + 1, nl, nd);
                 else
-                    fetch(item_at(sched, sk, k + 1), 0, nl, nd);
+                    fetch(citem(k + 1), 0, nl, nd);
                 mbar_wait(s_full, g & 1);
                 tc_after();
                 if (warp == 4 && lane == 0) BWD_PROBE(3, g);
@@ -1238,7 +1343,9 @@ constexpr int DQ_SMEM = 1024 + 2 * 2 * BW_TILE + DQ_ST * 2 * BW_TILE + 256 + 64;
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                 int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk) {
+                 int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk, ItemQueue iq) {
+    __shared__ uint64_t q_ready[kItemQ];
+    __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                   // [2 items]
@@ -1278,6 +1385,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     };
 
     if (threadIdx.x == 0) {
+        for (int q = 0; q < kItemQ; ++q) mbar_init(&q_ready[q], 1);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], 1);
@@ -1304,6 +1412,39 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const uint32_t tmem = *tslot;
     pdl_trigger();
     pdl_wait();
+    // the item sequence of this CTA: the static LPT table, or the dynamic queue
+    // (q_list filled by the producer warp, q_ready[k] completes when entry k is in)
+    auto citem = [&](int k) -> int {
+        if (!iq.ctr) return item_at(sched, sk, k);
+        if (k >= kItemQ) return -1;
+        mbar_wait(&q_ready[k], 0);
+        return *reinterpret_cast<volatile int*>(&q_list[k]);
+    };
+    // producer warp: publish entry k + 1 as item k starts (claimed during item
+    // k - 1), claim for entry k + 2; entry kItemQ - 1 is always the end marker
+    int q_pend = -1;
+    auto q_publish = [&](int k, int u) {
+        q_list[k] = u;
+        mbar_arrive(&q_ready[k]);
+    };
+    auto q_retire = [&]() {  // after the end marker: no claim of this CTA is left; the last CTA resets
+        if (atomicAdd(iq.ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+            atomicExch(iq.ctr, 0);
+            atomicExch(iq.ctr + 1, 0);
+        }
+    };
+    auto q_start = [&]() {  // producer lane 0, before the first item
+        const int c0 = iq_claim(iq);
+        q_publish(0, c0);
+        q_pend = c0 >= 0 ? iq_claim(iq) : -1;
+        if (c0 < 0) q_retire();
+    };
+    auto q_next = [&](int k) {  // producer lane 0, as item k starts
+        const int nx = k + 1 <= kItemQ - 2 ? q_pend : -1;
+        q_publish(k + 1, nx);
+        q_pend = nx >= 0 && k + 2 <= kItemQ - 2 ? iq_claim(iq) : -1;
+        if (nx < 0) q_retire();
+    };
     // TMEM: S | dP (fp32, 128 cols each) | dQ (64) | dS (bf16 pairs, 64): the dQ
     // MMA takes A = dS straight from TMEM
     const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256, tDS = tmem + 320;
@@ -1311,7 +1452,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     if (warp == 0) {
         {  // warp-wide walk and waits, one elected lane issues
             int it = 0, ni = 0;
-            for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+            if (iq.ctr) {  // dynamic queue: entry 0 (and the claim for entry 1)
+                if (lane == 0) q_start();
+                __syncwarp();
+            }
+            for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
+                if (iq.ctr) {  // publish entry k + 1 as item k starts
+                    if (lane == 0) q_next(k);
+                    __syncwarp();
+                }
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
                 const int qb = ni & 1;
@@ -1355,14 +1504,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             __syncwarp();
         };
         int it = 0, ni = 0;
-        if (item_at(sched, sk, 0) >= 0) {
+        if (citem(0) >= 0) {
             mbar_wait(&q_full[0], 0);
             issue_s(0, 0);
         }
-        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; ++ni, u = item_at(sched, sk, ++k)) {
+        for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
             const Item w = item_of(u);
             const int qb = ni & 1;
-            const bool more = item_at(sched, sk, k + 1) >= 0;
+            const bool more = citem(k + 1) >= 0;
             for (int j = 0; j < w.nk; ++j) {
                 const int g = it + j;
                 const int s = g % DQ_ST;
@@ -1425,13 +1574,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             }
         };
         float nL, nD;
-        fetch(item_at(sched, sk, 0), nL, nD);
+        fetch(citem(0), nL, nD);
         int it = 0;
-        for (int k = 0, u = item_at(sched, sk, 0); u >= 0; u = item_at(sched, sk, ++k)) {
+        for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
             const Item w = item_of(u);
             const int q = w.qt * BW_T + r;
             const float L = nL, Dq = nD;
-            fetch(item_at(sched, sk, k + 1), nL, nD);
+            fetch(citem(k + 1), nL, nD);
             for (int j = 0; j < w.nk; ++j) {
                 const int g = it + j;
                 mbar_wait(s_full, g & 1);
@@ -1563,7 +1712,36 @@ __global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_b
 struct Schedule {
     const int* table = nullptr;
     int grid = 0, k_max = 0;
+    const int* order = nullptr;  // every item, heaviest first (the dynamic queue's order)
+    int n = 0;
 };
+
+// Dynamic attention schedules (see ItemQueue): set by the trainer together
+// with the CTA-pair GEMM queue when collectives run beside compute;
+// ACCO_ATTN_STATIC / ACCO_ATTN_DYNAMIC override.
+std::atomic<int> g_attn_dynamic{0};
+struct StreamKeyA {
+    int dev;
+    cudaStream_t s;
+    bool operator<(const StreamKeyA& o) const { return dev != o.dev ? dev < o.dev : s < o.s; }
+};
+ItemQueue item_queue(const Schedule& sc, cudaStream_t stream) {
+    ItemQueue q{sc.order, sc.n, nullptr};
+    const bool st = std::getenv("ACCO_ATTN_STATIC") != nullptr, dy = std::getenv("ACCO_ATTN_DYNAMIC") != nullptr;
+    if (!(dy || (!st && g_attn_dynamic.load(std::memory_order_relaxed)))) return q;
+    static std::mutex mu;
+    static std::map<StreamKeyA, int*> ctrs;  // [claimed, retired] per (device, stream): launches are stream-ordered
+    int dev = 0;
+    ACCO_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    int*& c = ctrs[StreamKeyA{dev, stream}];
+    if (!c) {
+        ACCO_CUDA(cudaMalloc(&c, 32 * sizeof(int)));
+        ACCO_CUDA(cudaMemset(c, 0, 32 * sizeof(int)));
+    }
+    q.ctr = c;
+    return q;
+}
 
 Schedule lpt_schedule(int kind, int nt, int nbh, int G) {
     static std::mutex mu;
@@ -1597,7 +1775,12 @@ Schedule lpt_schedule(int kind, int nt, int nbh, int G) {
             int* dev = nullptr;
             ACCO_CUDA(cudaMalloc(&dev, host.size() * sizeof(int)));
             ACCO_CUDA(cudaMemcpy(dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice));
-            Schedule sc{dev, grid, k_max};
+            std::vector<int> ord(static_cast<size_t>(n));
+            std::iota(ord.begin(), ord.end(), 0);
+            int* dord = nullptr;
+            ACCO_CUDA(cudaMalloc(&dord, ord.size() * sizeof(int)));
+            ACCO_CUDA(cudaMemcpy(dord, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice));
+            Schedule sc{dev, grid, k_max, dord, n};
             cache[key] = sc;
             return sc;
         }
@@ -1624,7 +1807,10 @@ Schedule lpt_schedule(int kind, int nt, int nbh, int G) {
     int* dev = nullptr;
     ACCO_CUDA(cudaMalloc(&dev, host.size() * sizeof(int)));
     ACCO_CUDA(cudaMemcpy(dev, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice));
-    Schedule sc{dev, grid, k_max};
+    int* dord = nullptr;
+    ACCO_CUDA(cudaMalloc(&dord, order.size() * sizeof(int)));
+    ACCO_CUDA(cudaMemcpy(dord, order.data(), order.size() * sizeof(int), cudaMemcpyHostToDevice));
+    Schedule sc{dev, grid, k_max, dord, n};
     cache[key] = sc;
     return sc;
 }
@@ -1635,6 +1821,8 @@ bool tc_applicable(const void* a, const void* b, int hd) {
 }
 
 }  // namespace
+
+void attention_set_dynamic(bool on) { g_attn_dynamic.store(on ? 1 : 0, std::memory_order_relaxed); }
 
 bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse, const __nv_bfloat16* dy,
                       __nv_bfloat16* dqkv, float* dsum, int B, int T, int H, int Hkv, int hd, cudaStream_t s) {
@@ -1657,11 +1845,11 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     const int nt = (T + BW_T - 1) / BW_T;
     const Schedule skv = lpt_schedule(1, nt, B * Hkv, H / Hkv);
     launch_pdl(fa_bwd_dkv_tc, skv.grid, BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
-               skv.table, skv.k_max);
+               skv.table, skv.k_max, item_queue(skv, s));
     ACCO_CHECK_LAUNCH();
     const Schedule sq = lpt_schedule(2, nt, B * H, 1);
     launch_pdl(fa_bwd_dq_tc, sq.grid, BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale, sq.table,
-               sq.k_max);
+               sq.k_max, item_queue(sq, s));
     ACCO_CHECK_LAUNCH();
     return true;
 }
@@ -1686,7 +1874,8 @@ bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, in
         launch_pdl(fa_fwd_tc, dim3(nqt, B * H), kThreads, SMEM, s, m, y, lse, T, H, Hkv, scale);
     } else {
         const Schedule sf = lpt_schedule(0, nqt, B * H, 1);
-        launch_pdl(fa_fwd_tc2, sf.grid, F2_THREADS, F2_SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table, sf.k_max);
+        launch_pdl(fa_fwd_tc2, sf.grid, F2_THREADS, F2_SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table, sf.k_max,
+                   item_queue(sf, s));
     }
     ACCO_CHECK_LAUNCH();
     return true;

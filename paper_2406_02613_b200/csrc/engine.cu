@@ -95,8 +95,13 @@ Trainer::Trainer(GPTModel* model, const OptConfig& cfg, const SimCfg& sim, int m
                      "adaptive schedule needs one worker per device (NCCL mode)");
     }
     // collectives beside compute (real ranks or an emulated interconnect):
-    // CTA-pair GEMMs take their tiles from a work queue (gemm_set_pair_queue)
-    gemm_set_pair_queue(world_ > 1 || sim.comm_delay_ns > 0 || sim.comm_standin_ctas > 0);
+    // CTA-pair GEMMs and the attention kernels take their work from queues
+    // (the overlapping protocols only: DDP / ZeRO-1 run their collectives after
+    // the backward, where the static schedules are faster)
+    const bool beside = (world_ > 1 || sim.comm_delay_ns > 0 || sim.comm_standin_ctas > 0) &&
+                        (method == kACCO || method == kDPU || method == kWP);
+    gemm_set_pair_queue(beside);
+    attention_set_dynamic(beside);  // the attention kernels' work items from a queue as well
     psi_ = model->num_params();
     layout_ = shard_partition(static_cast<uint64_t>(psi_), sim.n_workers);
     const bool sharded = (comm_ || peer_) && method_ != kDDP;

@@ -100,6 +100,10 @@ void swiglu_bwd(const T* da, const T* gu, T* dgu, int M, int F, cudaStream_t s);
 // dy [B*seq, H*hd]; dqkv has qkv's layout. Hkv == H: plain MHA (GPT-2).
 template <class T>
 void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int Hkv, int hd, cudaStream_t s);
+// tcgen05 attention kernels: take their work items from a per-stream queue
+// (list scheduling) instead of the static LPT tables (set by the trainer
+// when collectives run beside compute)
+void attention_set_dynamic(bool on);
 template <class T>
 void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* dqkv, float* dsum,
                    int B, int seq, int H, int Hkv, int hd, cudaStream_t s);

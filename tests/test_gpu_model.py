@@ -246,3 +246,26 @@ def test_fused_bias_and_norm_param_grads_match_separate(cuda, arch, d, monkeypat
             small[off:off + shape[0]] = True
     assert _rel(g_f[~small], g_s[~small]) <= 1e-6
     assert _rel(g_f[small], g_s[small]) <= 2e-6
+
+
+@pytest.mark.parametrize("arch", ["gpt2", "llama"])
+def test_attention_dynamic_queue_matches_static(cuda, arch, monkeypatch):
+    """The tcgen05 attention kernels taking their work items from the
+    per-stream queue (the mode with collectives beside compute) compute every
+    item exactly as the static LPT tables do: bitwise equal gradients and loss,
+    over repeated launches (the queue resets itself after each kernel)."""
+    c = dict(vocab=96, d_model=256, n_layer=2, n_head=4, seq_len=512, n_samples=8, data_seed=4)
+    if arch == "llama":
+        c.update(arch="llama", n_kv_head=2, d_ff=512)
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=3))
+    gc = G.GPTConfig(**c)
+    th = torch.tensor(G.default_theta0(gc, 2)).to(torch.bfloat16).to(cuda)
+    seed = O.derive(4, 0, 0, 3, 0)
+    monkeypatch.setenv("ACCO_ATTN_STATIC", "1")
+    g_s, l_s = _grad(m, th, seed, 3, cuda)
+    monkeypatch.delenv("ACCO_ATTN_STATIC")
+    monkeypatch.setenv("ACCO_ATTN_DYNAMIC", "1")
+    for _ in range(2):
+        g_d, l_d = _grad(m, th, seed, 3, cuda)
+        assert l_d == l_s
+        assert np.array_equal(g_d, g_s)
