@@ -296,9 +296,10 @@ void attention_fwd(const T* qkv, T* y, float* lse, int B, int seq, int H, int Hk
     }
     if (hd == 32) fwd_impl<T, 32>(qkv, y, lse, B, seq, H, Hkv, s);
     else if (hd == 64) fwd_impl<T, 64>(qkv, y, lse, B, seq, H, Hkv, s);
+    else if (hd == 128) fwd_impl<T, 128>(qkv, y, lse, B, seq, H, Hkv, s);
     else if (hd == 16) fwd_impl<T, 16>(qkv, y, lse, B, seq, H, Hkv, s);
     else if (hd == 8) fwd_impl<T, 8>(qkv, y, lse, B, seq, H, Hkv, s);
-    else throw Error(kInvalidArg, "attention: head size must be 8, 16, 32 or 64");
+    else throw Error(kInvalidArg, "attention: head size must be 8, 16, 32, 64 or 128");
 }
 
 template <class T>
@@ -312,9 +313,10 @@ void attention_bwd(const T* qkv, const T* y, const float* lse, const T* dy, T* d
     }
     if (hd == 32) bwd_impl<T, 32>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
     else if (hd == 64) bwd_impl<T, 64>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
+    else if (hd == 128) bwd_impl<T, 128>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
     else if (hd == 16) bwd_impl<T, 16>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
     else if (hd == 8) bwd_impl<T, 8>(qkv, y, lse, dy, dqkv, dsum, B, seq, H, Hkv, s);
-    else throw Error(kInvalidArg, "attention: head size must be 8, 16, 32 or 64");
+    else throw Error(kInvalidArg, "attention: head size must be 8, 16, 32, 64 or 128");
 }
 
 template void attention_fwd<float>(const float*, float*, float*, int, int, int, int, int, cudaStream_t);

@@ -455,11 +455,26 @@ __device__ __forceinline__ void st_row32_global_fwd(__nv_bfloat16* dst, const ui
     }
 }
 
-constexpr int F2_STAGES = 3;
-// + per tile slot: row-max exchange [2 parity][2 half][128] and row sums [2 half][128]
-constexpr int F2_SMEM = 1024 + 4 * Q_BYTES + F2_STAGES * 2 * KV_BYTES + 256 + 2 * 6 * 128 * 4;
+// Head size D = 64 or 128. Tiles of D > 64 columns are D / 64 TMA boxes of
+// 64 columns (SW128 sub-tiles 16 KB apart); D = 128 keeps one item slot of Q
+// and a 2-stage K/V ring to fit shared memory.
+template <int D>
+struct Fwd2 {
+    static constexpr int QB = BQ * D * 2, KVB = BKV * D * 2;
+    static constexpr int STAGES = D == 64 ? 3 : 2, QSLOTS = D == 64 ? 2 : 1;
+    // + per tile slot: row-max exchange [2 parity][2 half][128] and row sums [2 half][128]
+    static constexpr int SMEM = 1024 + QSLOTS * 2 * QB + STAGES * 2 * KVB + 256 + 2 * 6 * 128 * 4;
+};
 // two softmax groups of 8 warps (one per tile slot): quadrant x half of the 128 keys
 constexpr int F2_THREADS = 640;
+// a [128 rows][D] bf16 tile as D / 64 boxes of 64 columns, 16 KB apart
+template <int D>
+__device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* map, uint64_t* bar, int col, int row) {
+#pragma unroll
+    for (int sub = 0; sub < D / 64; ++sub) tma_load_2d(static_cast<uint8_t*>(dst) + sub * 16384, map, bar, col + 64 * sub, row);
+}
+// K-major descriptor of 16-deep k-slice kk of such a tile
+__device__ __forceinline__ uint64_t kslice(uint64_t desc, int kk) { return desc + (kk >> 2) * (16384 >> 4) + (kk & 3) * 2; }
 
 __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -524,6 +539,7 @@ __device__ __forceinline__ void exp_pack64(const uint32_t* sv, float sl, float m
 // tile sequence, so CTA launch / TMEM alloc / pipeline fill are paid once per
 // SM. TMEM: S/P tile 0 [0,128), S/P tile 1 [128,256), O tile 0 [256,320),
 // O tile 1 [320,384).
+template <int D>
 __global__ void __launch_bounds__(F2_THREADS, 1)
     fa_fwd_tc2(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
                int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk, ItemQueue iq) {
@@ -531,12 +547,14 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                         // [2 items][2 tiles]
-    uint8_t* sK = sQ + 4 * Q_BYTES;             // [stage]
+    constexpr int Q_BYTES = Fwd2<D>::QB, KV_BYTES = Fwd2<D>::KVB, F2_STAGES = Fwd2<D>::STAGES,
+                  QSLOTS = Fwd2<D>::QSLOTS;
+    uint8_t* sQ = smem;                         // [QSLOTS items][2 tiles]
+    uint8_t* sK = sQ + QSLOTS * 2 * Q_BYTES;    // [stage]
     uint8_t* sV = sK + F2_STAGES * KV_BYTES;    // [stage]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + F2_STAGES * KV_BYTES);
-    uint64_t* q_full = bars;                     // [2 item slots]
-    uint64_t* q_empty = bars + 2;                // [2 item slots]
+    uint64_t* q_full = bars;                     // [item slots] (2 reserved)
+    uint64_t* q_empty = bars + 2;                // [item slots] (2 reserved)
     uint64_t* kv_full = bars + 4;                // [F2_STAGES]
     uint64_t* kv_empty = kv_full + F2_STAGES;    // [F2_STAGES]
     uint64_t* s_full = kv_empty + F2_STAGES;     // [2 tiles]
@@ -548,7 +566,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     const int npair = (nqt + 1) / 2;
     const int nbh = B * H;
     const int n_items = npair * nbh;
-    const int d = H * HD;
+    const int d = H * D;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     struct Item {
         int pr, b, h, kc, vc, nt0, nt1, nkv;
@@ -559,8 +577,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         const int bh = u % nbh;
         w.b = bh / H;
         w.h = bh % H;
-        w.kc = d + (w.h / (H / Hkv)) * HD;  // this head's K / V columns
-        w.vc = w.kc + Hkv * HD;
+        w.kc = d + (w.h / (H / Hkv)) * D;  // this head's K / V columns
+        w.vc = w.kc + Hkv * D;
         w.nt0 = 2 * w.pr + 1;                               // kv tiles of query tile 0
         w.nt1 = 2 * w.pr + 2 <= nqt ? 2 * w.pr + 2 : 0;     // of query tile 1 (0: absent)
         w.nkv = w.nt1 ? w.nt1 : w.nt0;
@@ -644,14 +662,13 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 }
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
-                const int qs = ni & 1;
-                mbar_wait(&q_empty[qs], ((ni >> 1) & 1) ^ 1);  // item ni-2's S MMAs are done with this slot
+                const int qs = ni % QSLOTS;
+                mbar_wait(&q_empty[qs], ((ni / QSLOTS) & 1) ^ 1);  // item ni-QSLOTS's S MMAs are done with this slot
                 if (elect_one()) {
                     mbar_expect_tx(&q_full[qs], (w.nt1 ? 2 : 1) * Q_BYTES);
                     uint8_t* q_dst = sQ + qs * 2 * Q_BYTES;
-                    tma_load_2d(q_dst, &tmQKV, &q_full[qs], w.h * HD, row_base + 2 * w.pr * BQ);
-                    if (w.nt1)
-                        tma_load_2d(q_dst + Q_BYTES, &tmQKV, &q_full[qs], w.h * HD, row_base + (2 * w.pr + 1) * BQ);
+                    tma_tile<D>(q_dst, &tmQKV, &q_full[qs], w.h * D, row_base + 2 * w.pr * BQ);
+                    if (w.nt1) tma_tile<D>(q_dst + Q_BYTES, &tmQKV, &q_full[qs], w.h * D, row_base + (2 * w.pr + 1) * BQ);
                 }
                 __syncwarp();
                 for (int j = 0; j < w.nkv; ++j, ++kvit) {
@@ -659,8 +676,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                     mbar_wait(&kv_empty[s], ((kvit / F2_STAGES) & 1) ^ 1);
                     if (elect_one()) {
                         mbar_expect_tx(&kv_full[s], 2 * KV_BYTES);
-                        tma_load_2d(sK + s * KV_BYTES, &tmQKV, &kv_full[s], w.kc, row_base + j * BKV);
-                        tma_load_2d(sV + s * KV_BYTES, &tmQKV, &kv_full[s], w.vc, row_base + j * BKV);
+                        tma_tile<D>(sK + s * KV_BYTES, &tmQKV, &kv_full[s], w.kc, row_base + j * BKV);
+                        tma_tile<D>(sV + s * KV_BYTES, &tmQKV, &kv_full[s], w.vc, row_base + j * BKV);
                     }
                     __syncwarp();
                 }
@@ -670,7 +687,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         // warp-wide walk and waits, one elected lane issues (it shares its SM
         // sub-partition with four softmax warps: keep its instruction count low)
         constexpr uint32_t id_s = idesc_bf16(BQ, BKV, 0, 0);  // Q K^T: both K-major
-        constexpr uint32_t id_o = idesc_bf16(BQ, HD, 0, 1);   // P V: P from TMEM (K-major), V MN-major
+        constexpr uint32_t id_o = idesc_bf16(BQ, D, 0, 1);    // P V: P from TMEM (K-major), V MN-major
         int kvit = 0, ni = 0;
         int cnt[2] = {0, 0};  // tiles issued so far per slot (s_full / p_full phases)
         int pc_s = 0, pc_pv = 0;
@@ -679,8 +696,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
             const Item w = item_of(u);
             const int nt[2] = {w.nt0, w.nt1};
-            const int qs = ni & 1;
-            mbar_wait(&q_full[qs], (ni >> 1) & 1);
+            const int qs = ni % QSLOTS;
+            mbar_wait(&q_full[qs], (ni / QSLOTS) & 1);
             const uint32_t q_item = smem_u32(sQ + qs * 2 * Q_BYTES);
             auto issue_s = [&](int x, int j) {
                 const int s = (kvit + j) % F2_STAGES;
@@ -694,7 +711,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 const uint64_t qd = sdesc(q_item + x * Q_BYTES, 16, 1024), kd = sdesc(smem_u32(sK + s * KV_BYTES), 16, 1024);
                 if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < HD / 16; ++kk) umma(tmem + x * 128, qd + 2 * kk, kd + 2 * kk, id_s, kk > 0);
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        umma(tmem + x * 128, kslice(qd, kk), kslice(kd, kk), id_s, kk > 0);
                     umma_commit(&s_full[x]);
                 }
                 __syncwarp();
@@ -706,11 +724,12 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 if (lane == 0) FWD_PROBE(1, pc_pv);
                 ++pc_pv;
                 // V MN-major: 16-key slices are two 8-row atoms (2048 B) apart
-                const uint64_t vd = sdesc(smem_u32(sV + s * KV_BYTES), 64 * 128, 1024);
+                // (N = D: 64-wide MN atoms, one 16 KB sub-tile apart)
+                const uint64_t vd = sdesc(smem_u32(sV + s * KV_BYTES), D == 64 ? 64 * 128 : 16384, 1024);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk)
-                        umma_ts(tmem + 256 + x * 64, tmem + x * 128 + kk * 8, vd + 128 * kk, id_o,
+                        umma_ts(tmem + 256 + x * D, tmem + x * 128 + kk * 8, vd + 128 * kk, id_o,
                                 (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 __syncwarp();
@@ -748,7 +767,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
         const int wq = warp & 3, half = ((warp - 4) >> 2) & 1;
         const int r = wq * 32 + lane;
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
-        const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 64 + lane_off;
+        const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * D + lane_off;
+        constexpr int OH = D / 2;  // O columns per half warp pair
         const float sl = scale * kLog2e;
         float* red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tslot) + 16) + x * 6 * 128;  // [2][2][128] max
         float* lsum = red + 4 * 128;                                                                  // [2][128] sums
@@ -807,12 +827,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 }
                 // O *= alpha where the max moved (before this tile's PV, which waits p_full)
                 if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
-                    uint32_t o[32];
-                    tmem_ld32(tO + half * 32, o);
-                    tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                    tmem_st32(tO + half * 32, o);
+                    for (int c = 0; c < OH / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(tO + half * OH + c * 32, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        tmem_st32(tO + half * OH + c * 32, o);
+                    }
                 }
                 tmem_wait_st();
                 if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(9, cnt + j);
@@ -830,11 +853,14 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             ++nitem;
             tc_after();
             const float inv = 1.f / l;
-            __nv_bfloat16* yr = y + (static_cast<int64_t>(w.b) * T + q) * d + w.h * HD + half * 32;
-            uint32_t o[32];
-            tmem_ld32(tO + half * 32, o);  // warp-collective: every lane loads
-            tmem_wait_ld();
-            if (q < T) st_row32_global_fwd(yr, o, inv);
+            __nv_bfloat16* yr = y + (static_cast<int64_t>(w.b) * T + q) * d + w.h * D + half * OH;
+#pragma unroll
+            for (int c = 0; c < OH / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(tO + half * OH + c * 32, o);  // warp-collective: every lane loads
+                tmem_wait_ld();
+                if (q < T) st_row32_global_fwd(yr + c * 32, o, inv);
+            }
             tc_before();
             if (q < T && half == 0) lse[(static_cast<int64_t>(w.b) * H + w.h) * T + q] = (m + log2f(l)) / kLog2e;
             asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // lsum reusable
@@ -963,12 +989,19 @@ constexpr int BW_T = 128;                          // tile rows (keys or queries
 // scheduler, so 4 per scheduler keep the issue slots busy
 constexpr int BW_THREADS = 640;
 constexpr int BW_SOFTMAX = 512;
-constexpr int BW_TILE = BW_T * HD * 2;             // 16 KB [128][64] bf16
 constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P / dS operand)
-// dKV smem: K, V (once) + 2 stages x (Q, dO) + lse/D (2 stages) + P^T + dS^T
-constexpr int DKV_ST = 4;  // Q/dO ring depth
-// K/V double-buffered (the next item's K/V loads under the current item)
-constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + (BW_SOFTMAX / 32) * 64 * 4 + 256 + 64;
+// dKV smem: K, V (KVS item slots) + DKV_ST stages x (Q, dO) + per-warp lse / D
+// rows. D = 64: K/V double-buffered (the next item's K/V under the current
+// item), a 4-deep Q/dO ring. D = 128: one K/V slot, a 2-deep ring, and TMEM
+// S^T | dP^T | dV | dK (128 columns each) with P^T / dS^T (bf16) written over
+// the consumed S^T / dP^T columns, so the next tile's S^T / dP^T are issued
+// after this tile's dV / dK MMAs (in-order tensor pipe).
+template <int D>
+struct Dkv {
+    static constexpr int TILE = BW_T * D * 2, ST = D == 64 ? 4 : 2, KVS = D == 64 ? 2 : 1;
+    static constexpr bool P_IN_S = D > 64;
+    static constexpr int SMEM = 1024 + KVS * 2 * TILE + ST * 2 * TILE + (BW_SOFTMAX / 32) * 64 * 4 + 256 + 64;
+};
 
 // dK/dV, persistent: grid = #SMs; work item = (128-key tile kt, batch * KV
 // head), heaviest key tiles first (kt = 0 sees every query tile), dealt
@@ -983,6 +1016,7 @@ constexpr int DKV_SMEM = 1024 + 2 * 2 * BW_TILE + DKV_ST * 2 * BW_TILE + (BW_SOF
 // K/V load and first S^T/dP^T overlap the current item's last tile and the
 // dK/dV epilogue; a CTA launch + TMEM alloc + pipeline fill is paid once per SM
 // instead of once per item (it was ~7 us of a ~100 us kernel per wave).
+template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dkv_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                   const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
@@ -991,15 +1025,17 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sK = smem;                    // [2 items]
-    uint8_t* sV = sK + 2 * BW_TILE;        // [2 items]
-    uint8_t* sQ = sV + 2 * BW_TILE;        // [DKV_ST stages]
+    constexpr int BW_TILE = Dkv<D>::TILE, DKV_ST = Dkv<D>::ST, KVS = Dkv<D>::KVS;
+    constexpr bool P_IN_S = Dkv<D>::P_IN_S;
+    uint8_t* sK = smem;                    // [KVS items]
+    uint8_t* sV = sK + KVS * BW_TILE;      // [KVS items]
+    uint8_t* sQ = sV + KVS * BW_TILE;      // [DKV_ST stages]
     uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
     // per softmax warp: its 32 query columns' lse (log2 domain) | D, for float4 broadcasts
     float* sLD = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [16 warps][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + (BW_SOFTMAX / 32) * 64);
-    uint64_t* kv_full = bars;                 // [2]
-    uint64_t* kv_empty = bars + 2;            // [2]: every S^T/dP^T MMA of the item issued and done
+    uint64_t* kv_full = bars;                 // [KVS] (2 reserved)
+    uint64_t* kv_empty = bars + 2;            // [KVS]: every S^T/dP^T MMA of the item issued and done
     uint64_t* q_full = bars + 4;              // [DKV_ST]
     uint64_t* q_empty = q_full + DKV_ST;      // [DKV_ST]
     uint64_t* s_full = q_empty + DKV_ST;      // S^T and dP^T ready
@@ -1012,8 +1048,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const int nbk = B * Hkv;
     const int n_items = nt * nbk;
     const int G = H / Hkv;
-    const int d = H * HD;
-    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    const int d = H * D;
+    const int ldq = (H + 2 * Hkv) * D;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     struct Item {
         int kt, b, hk, nq;
@@ -1093,8 +1129,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     // (bf16 pairs, 64 cols each): the dV/dK MMAs take A straight from TMEM, so
     // P^T/dS^T never touch shared memory, and S^T/dP^T of the next tile can
     // land while dV/dK of this one still read P^T/dS^T
-    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 320, tPT = tmem + 384,
-                   tDST = tmem + 448;
+    // (D = 128: dV | dK 128 columns each, P^T / dS^T over S^T / dP^T)
+    const uint32_t tS = tmem, tP = tmem + 128, tDV = tmem + 256, tDK = tmem + 256 + D,
+                   tPT = P_IN_S ? tS : tmem + 384, tDST = P_IN_S ? tP : tmem + 448;
 
     if (warp == 0) {
         {  // warp-wide walk and waits, one elected lane issues
@@ -1109,14 +1146,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     __syncwarp();
                 }
                 const Item w = item_of(u);
-                const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
+                const int kc = d + w.hk * D, vc = kc + Hkv * D;
                 const int row_base = w.b * T;
-                const int kb = ni & 1;
-                mbar_wait(&kv_empty[kb], ((ni >> 1) & 1) ^ 1);  // item ni-2's S^T/dP^T MMAs are done with it
+                const int kb = ni % KVS;
+                mbar_wait(&kv_empty[kb], ((ni / KVS) & 1) ^ 1);  // item ni-KVS's S^T/dP^T MMAs are done with it
                 if (elect_one()) {
                     mbar_expect_tx(&kv_full[kb], 2 * BW_TILE);
-                    tma_load_2d(sK + kb * BW_TILE, &tmQKV, &kv_full[kb], kc, row_base + w.kt * BW_T);
-                    tma_load_2d(sV + kb * BW_TILE, &tmQKV, &kv_full[kb], vc, row_base + w.kt * BW_T);
+                    tma_tile<D>(sK + kb * BW_TILE, &tmQKV, &kv_full[kb], kc, row_base + w.kt * BW_T);
+                    tma_tile<D>(sV + kb * BW_TILE, &tmQKV, &kv_full[kb], vc, row_base + w.kt * BW_T);
                 }
                 __syncwarp();
                 const int niter = G * w.nq;
@@ -1127,8 +1164,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     mbar_wait(&q_empty[s], ((it / DKV_ST) & 1) ^ 1);
                     if (elect_one()) {
                         mbar_expect_tx(&q_full[s], 2 * BW_TILE);
-                        tma_load_2d(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * HD, row_base + q0);
-                        tma_load_2d(sO + s * BW_TILE, &tmDO, &q_full[s], h * HD, row_base + q0);
+                        tma_tile<D>(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * D, row_base + q0);
+                        tma_tile<D>(sO + s * BW_TILE, &tmDO, &q_full[s], h * D, row_base + q0);
                     }
                     __syncwarp();
                 }
@@ -1138,7 +1175,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         // warp-wide walk and waits, one elected lane issues (see fa_fwd_tc2);
         // descriptors are built once per operand tile and stepped per 16-deep slice
         constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);  // K Q^T / V dO^T
-        constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);    // P^T dO / dS^T Q (B MN-major)
+        constexpr uint32_t id_g = idesc_bf16(BW_T, D, 0, 1);     // P^T dO / dS^T Q (B MN-major)
         auto issue_s = [&](int g, int kb) {  // S^T = K Q_g^T, dP^T = V dO_g^T (global tile g, K/V slot kb)
             const int s = g % DKV_ST;
             mbar_wait(&q_full[s], (g / DKV_ST) & 1);
@@ -1148,9 +1185,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             if (lane == 0) BWD_PROBE(0, g);
             if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {  // K-major: 32 B per slice
-                    umma(tS, kd + 2 * kk, qd + 2 * kk, id_s, kk > 0);
-                    umma(tP, vd + 2 * kk, od + 2 * kk, id_s, kk > 0);
+                for (int kk = 0; kk < D / 16; ++kk) {  // K-major: 32 B per slice (sub-tiles of 64 columns)
+                    umma(tS, kslice(kd, kk), kslice(qd, kk), id_s, kk > 0);
+                    umma(tP, kslice(vd, kk), kslice(od, kk), id_s, kk > 0);
                 }
                 umma_commit(s_full);
             }
@@ -1164,30 +1201,36 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
             const Item w = item_of(u);
             const int niter = G * w.nq;
-            const int kb = ni & 1;
+            const int kb = ni % KVS;
             const bool more = citem(k + 1) >= 0;
             for (int i = 0; i < niter; ++i) {
                 const int g = it + i;
                 const int s = g % DKV_ST;
-                // MN-major B: 16-query slices are two 8-row atoms (2048 B) apart
-                const uint64_t qd = sdesc(smem_u32(sQ + s * BW_TILE), 64 * 128, 1024);
-                const uint64_t od = sdesc(smem_u32(sO + s * BW_TILE), 64 * 128, 1024);
+                // MN-major B: 16-query slices are two 8-row atoms (2048 B) apart;
+                // N = D: 64-wide atoms one 16 KB sub-tile apart
+                const uint64_t qd = sdesc(smem_u32(sQ + s * BW_TILE), D == 64 ? 64 * 128 : 16384, 1024);
+                const uint64_t od = sdesc(smem_u32(sO + s * BW_TILE), D == 64 ? 64 * 128 : 16384, 1024);
                 // the next tile's S^T/dP^T (possibly the next item's first, whose
-                // K/V is already in the other slot) overlap this tile's softmax
-                if (i + 1 < niter) {
-                    mbar_wait(s_free, g & 1);
-                    tc_after();
-                    issue_s(g + 1, kb);
-                } else {
-                    if (elect_one()) umma_commit(&kv_empty[kb]);  // every S^T/dP^T of this item issued
-                    __syncwarp();
-                    if (more) {
-                        mbar_wait(&kv_full[kb ^ 1], ((ni + 1) >> 1) & 1);
-                        mbar_wait(s_free, g & 1);
+                // K/V is already in the other slot): D = 64 under this tile's
+                // softmax (its S^T/dP^T columns are free once read), D = 128 after
+                // this tile's dV/dK MMAs (which read P^T/dS^T from those columns)
+                auto next_s = [&](bool wait_free) {
+                    if (i + 1 < niter) {
+                        if (wait_free) mbar_wait(s_free, g & 1);
                         tc_after();
-                        issue_s(g + 1, kb ^ 1);
+                        issue_s(g + 1, kb);
+                    } else {
+                        if (elect_one()) umma_commit(&kv_empty[kb]);  // every S^T/dP^T of this item issued
+                        __syncwarp();
+                        if (more) {
+                            mbar_wait(&kv_full[(ni + 1) % KVS], ((ni + 1) / KVS) & 1);
+                            if (wait_free) mbar_wait(s_free, g & 1);
+                            tc_after();
+                            issue_s(g + 1, (ni + 1) % KVS);
+                        }
                     }
-                }
+                };
+                if (!P_IN_S) next_s(true);
                 mbar_wait(p_full, g & 1);  // P^T / dS^T written
                 tc_after();
                 if (lane == 0) BWD_PROBE(1, g);
@@ -1201,6 +1244,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     umma_commit(g_done);
                 }
                 __syncwarp();
+                if (P_IN_S) next_s(false);
             }
             it += niter;
         }
@@ -1233,12 +1277,22 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         auto epilogue = [&](int pu) {
             const Item w = item_of(pu);
             const int key = w.kt * BW_T + r;
-            uint32_t o[32];  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
-            const int kc = d + w.hk * HD, vc = kc + Hkv * HD;
-            __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(w.b) * T + key) * ldq + (qq & 1) * 32;
-            tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
-            tmem_wait_ld();
-            if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc), o, qq < 2 ? 1.f : scale);
+            const int kc = d + w.hk * D, vc = kc + Hkv * D;
+            __nv_bfloat16* dst = dqkv + (static_cast<int64_t>(w.b) * T + key) * ldq;
+            if (D == 64) {  // quarters 0/1: dV columns, 2/3: dK columns (32 each)
+                uint32_t o[32];
+                tmem_ld32((qq < 2 ? tDV : tDK) + lane_off + (qq & 1) * 32, o);
+                tmem_wait_ld();
+                if (key < T) st_row32_global(dst + (qq < 2 ? vc : kc) + (qq & 1) * 32, o, qq < 2 ? 1.f : scale);
+            } else {  // quarter qq: dV and dK columns qq*32 ..
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    uint32_t o[32];
+                    tmem_ld32((t ? tDK : tDV) + lane_off + qq * 32, o);
+                    tmem_wait_ld();
+                    if (key < T) st_row32_global(dst + (t ? kc : vc) + qq * 32, o, t ? scale : 1.f);
+                }
+            }
         };
         int it = 0;
         for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
@@ -1305,6 +1359,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                         epilogue(prev);
                         prev = -1;
                     }
+                    // (D = 128: P^T / dS^T go over S^T / dP^T columns other warps read:
+                    // every softmax thread has them in registers once s_free completes)
+                    if (P_IN_S) mbar_wait(s_free, g & 1);
                     tmem_st16(tPT + lane_off + qq * 16, pk);
                     tmem_st16(tDST + lane_off + qq * 16, dk);
                     tmem_wait_st();
@@ -1337,9 +1394,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 // double-buffered across items and the next item's first S/dP is issued
 // under the current item's last tile (barrier phases follow the CTA's global
 // tile sequence), so CTA launch / TMEM alloc / pipeline fill are paid once.
-constexpr int DQ_ST = 4;  // K/V ring depth
-constexpr int DQ_SMEM = 1024 + 2 * 2 * BW_TILE + DQ_ST * 2 * BW_TILE + 256 + 64;
+// head size D = 64 or 128: D = 128 keeps one item slot of Q / dO and a 2-deep
+// K/V ring (shared memory)
+template <int D>
+struct Dq {
+    static constexpr int TILE = BW_T * D * 2, ST = D == 64 ? 4 : 2, QS = D == 64 ? 2 : 1;
+    static constexpr int SMEM = 1024 + QS * 2 * TILE + ST * 2 * TILE + 256 + 64;
+};
 
+template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
                  const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
@@ -1348,13 +1411,14 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                   // [2 items]
-    uint8_t* sO = sQ + 2 * BW_TILE;       // dO [2 items]
-    uint8_t* sK = sO + 2 * BW_TILE;       // [DQ_ST stages]
+    constexpr int BW_TILE = Dq<D>::TILE, DQ_ST = Dq<D>::ST, QS = Dq<D>::QS;
+    uint8_t* sQ = smem;                   // [QS items]
+    uint8_t* sO = sQ + QS * BW_TILE;      // dO [QS items]
+    uint8_t* sK = sO + QS * BW_TILE;      // [DQ_ST stages]
     uint8_t* sV = sK + DQ_ST * BW_TILE;   // [DQ_ST stages]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + DQ_ST * BW_TILE);
-    uint64_t* q_full = bars;               // [2]
-    uint64_t* q_empty = bars + 2;          // [2]
+    uint64_t* q_full = bars;               // [QS] (2 reserved)
+    uint64_t* q_empty = bars + 2;          // [QS] (2 reserved)
     uint64_t* kv_full = bars + 4;          // [DQ_ST]
     uint64_t* kv_empty = kv_full + DQ_ST;  // [DQ_ST]
     uint64_t* s_full = kv_empty + DQ_ST;
@@ -1366,8 +1430,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     const int nt = (T + BW_T - 1) / BW_T;
     const int nbh = B * H;
     const int n_items = nt * nbh;
-    const int d = H * HD;
-    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    const int d = H * D;
+    const int ldq = (H + 2 * Hkv) * D;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     struct Item {
         int qt, b, h, nk, kc, vc;
@@ -1379,8 +1443,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         w.b = bh / H;
         w.h = bh % H;
         w.nk = w.qt + 1;  // key tiles 0 .. qt
-        w.kc = d + (w.h / (H / Hkv)) * HD;  // this head's K / V columns
-        w.vc = w.kc + Hkv * HD;
+        w.kc = d + (w.h / (H / Hkv)) * D;  // this head's K / V columns
+        w.vc = w.kc + Hkv * D;
         return w;
     };
 
@@ -1445,9 +1509,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         q_pend = nx >= 0 && k + 2 <= kItemQ - 2 ? iq_claim(iq) : -1;
         if (nx < 0) q_retire();
     };
-    // TMEM: S | dP (fp32, 128 cols each) | dQ (64) | dS (bf16 pairs, 64): the dQ
+    // TMEM: S | dP (fp32, 128 cols each) | dQ (D) | dS (bf16 pairs, 64): the dQ
     // MMA takes A = dS straight from TMEM
-    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256, tDS = tmem + 320;
+    const uint32_t tS = tmem, tP = tmem + 128, tDQ = tmem + 256, tDS = tmem + 256 + D;
 
     if (warp == 0) {
         {  // warp-wide walk and waits, one elected lane issues
@@ -1463,12 +1527,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 }
                 const Item w = item_of(u);
                 const int row_base = w.b * T;
-                const int qb = ni & 1;
-                mbar_wait(&q_empty[qb], ((ni >> 1) & 1) ^ 1);  // item ni-2 is done with this Q/dO slot
+                const int qb = ni % QS;
+                mbar_wait(&q_empty[qb], ((ni / QS) & 1) ^ 1);  // item ni-QS is done with this Q/dO slot
                 if (elect_one()) {
                     mbar_expect_tx(&q_full[qb], 2 * BW_TILE);
-                    tma_load_2d(sQ + qb * BW_TILE, &tmQKV, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
-                    tma_load_2d(sO + qb * BW_TILE, &tmDO, &q_full[qb], w.h * HD, row_base + w.qt * BW_T);
+                    tma_tile<D>(sQ + qb * BW_TILE, &tmQKV, &q_full[qb], w.h * D, row_base + w.qt * BW_T);
+                    tma_tile<D>(sO + qb * BW_TILE, &tmDO, &q_full[qb], w.h * D, row_base + w.qt * BW_T);
                 }
                 __syncwarp();
                 for (int j = 0; j < w.nk; ++j, ++it) {
@@ -1476,8 +1540,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     mbar_wait(&kv_empty[s], ((it / DQ_ST) & 1) ^ 1);
                     if (elect_one()) {
                         mbar_expect_tx(&kv_full[s], 2 * BW_TILE);
-                        tma_load_2d(sK + s * BW_TILE, &tmQKV, &kv_full[s], w.kc, row_base + j * BW_T);
-                        tma_load_2d(sV + s * BW_TILE, &tmQKV, &kv_full[s], w.vc, row_base + j * BW_T);
+                        tma_tile<D>(sK + s * BW_TILE, &tmQKV, &kv_full[s], w.kc, row_base + j * BW_T);
+                        tma_tile<D>(sV + s * BW_TILE, &tmQKV, &kv_full[s], w.vc, row_base + j * BW_T);
                     }
                     __syncwarp();
                 }
@@ -1486,7 +1550,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     } else if (warp == 1) {
         // warp-wide walk and waits, one elected lane issues (see fa_fwd_tc2)
         constexpr uint32_t id_s = idesc_bf16(BW_T, BW_T, 0, 0);
-        constexpr uint32_t id_g = idesc_bf16(BW_T, HD, 0, 1);
+        constexpr uint32_t id_g = idesc_bf16(BW_T, D, 0, 1);
         auto issue_s = [&](int g, int qb) {  // S = Q K_g^T, dP = dO V_g^T (global tile g, Q/dO slot qb)
             const int s = g % DQ_ST;
             mbar_wait(&kv_full[s], (g / DQ_ST) & 1);
@@ -1495,9 +1559,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const uint64_t kd = sdesc(smem_u32(sK + s * BW_TILE), 16, 1024), vd = sdesc(smem_u32(sV + s * BW_TILE), 16, 1024);
             if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {  // K-major: 32 B per slice
-                    umma(tS, qd + 2 * kk, kd + 2 * kk, id_s, kk > 0);
-                    umma(tP, od + 2 * kk, vd + 2 * kk, id_s, kk > 0);
+                for (int kk = 0; kk < D / 16; ++kk) {  // K-major: 32 B per slice (sub-tiles of 64 columns)
+                    umma(tS, kslice(qd, kk), kslice(kd, kk), id_s, kk > 0);
+                    umma(tP, kslice(od, kk), kslice(vd, kk), id_s, kk > 0);
                 }
                 umma_commit(s_full);
             }
@@ -1510,12 +1574,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         }
         for (int k = 0, u = citem(0); u >= 0; ++ni, u = citem(++k)) {
             const Item w = item_of(u);
-            const int qb = ni & 1;
+            const int qb = ni % QS;
             const bool more = citem(k + 1) >= 0;
             for (int j = 0; j < w.nk; ++j) {
                 const int g = it + j;
                 const int s = g % DQ_ST;
-                const uint64_t kd = sdesc(smem_u32(sK + s * BW_TILE), 64 * 128, 1024);  // MN-major B
+                // MN-major B (N = D: 64-wide atoms one 16 KB sub-tile apart)
+                const uint64_t kd = sdesc(smem_u32(sK + s * BW_TILE), D == 64 ? 64 * 128 : 16384, 1024);
                 if (j + 1 < w.nk) {
                     mbar_wait(s_free, g & 1);
                     tc_after();
@@ -1524,10 +1589,10 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     if (elect_one()) umma_commit(&q_empty[qb]);  // every S/dP of this item issued
                     __syncwarp();
                     if (more) {  // the next item's first S/dP under this tile's softmax
-                        mbar_wait(&q_full[qb ^ 1], ((ni + 1) >> 1) & 1);
+                        mbar_wait(&q_full[(ni + 1) % QS], ((ni + 1) / QS) & 1);
                         mbar_wait(s_free, g & 1);
                         tc_after();
-                        issue_s(g + 1, qb ^ 1);
+                        issue_s(g + 1, (ni + 1) % QS);
                     }
                 }
                 mbar_wait(p_full, g & 1);
@@ -1553,13 +1618,13 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         // tile (after its math, overlapping the last dQ MMA), or after the loop
         int prev = -1;
         auto epilogue = [&](int pu) {
-            if (qq >= 2) return;
+            if (qq >= D / 32) return;
             const Item w = item_of(pu);
             const int q = w.qt * BW_T + r;
             uint32_t o[32];
             tmem_ld32(tDQ + lane_off + qq * 32, o);
             tmem_wait_ld();
-            if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * HD + qq * 32, o, scale);
+            if (q < T) st_row32_global(dqkv + (static_cast<int64_t>(w.b) * T + q) * ldq + w.h * D + qq * 32, o, scale);
         };
         // this row's lse (log2) and D, loaded one item ahead
         auto fetch = [&](int u, float& L, float& Dq) {
@@ -1677,14 +1742,16 @@ CUtensorMap rows_map(const void* p, int64_t cols, int64_t rows, int64_t ld) {
 }
 
 // D[bh, t] = sum_c dO[t, c] O[t, c]. y / dy are read as one flat stream of
-// 64-element head rows in memory order (token-major, head-minor): 8 threads
-// per row, 16 B each, 3-step shuffle reduction.
+// D-element head rows in memory order (token-major, head-minor): D / 8
+// threads per row, 16 B each, a shuffle reduction.
+template <int D>
 __global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_bfloat16* __restrict__ dy,
                                float* __restrict__ dsum, int B, int T, int H) {
     ACCO_PDL_PROLOGUE();
+    constexpr int TPR = D / 8;  // threads per head row
     const int64_t nrow = static_cast<int64_t>(B) * T * H;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int64_t row = i >> 3;  // (b*T + t)*H + h
+    const int64_t row = i / TPR;  // (b*T + t)*H + h
     float s = 0.f;
     if (row < nrow) {
         const uint4 a = __ldg(reinterpret_cast<const uint4*>(y) + i);
@@ -1696,10 +1763,9 @@ __global__ void dsum_tc_kernel(const __nv_bfloat16* __restrict__ y, const __nv_b
             s = fmaf(__uint_as_float(wa[k] & 0xffff0000u), __uint_as_float(wg[k] & 0xffff0000u), s);
         }
     }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    if (row < nrow && (threadIdx.x & 7) == 0) {
+#pragma unroll
+    for (int o = 1; o < TPR; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (row < nrow && (threadIdx.x & (TPR - 1)) == 0) {
         const int h = static_cast<int>(row % H);
         const int64_t bt = row / H;
         const int t = static_cast<int>(bt % T), b = static_cast<int>(bt / T);
@@ -1815,9 +1881,10 @@ Schedule lpt_schedule(int kind, int nt, int nbh, int G) {
     return sc;
 }
 
-bool tc_applicable(const void* a, const void* b, int hd) {
-    return hd == HD && !(reinterpret_cast<uintptr_t>(a) & 15) && !(reinterpret_cast<uintptr_t>(b) & 15) &&
-           !std::getenv("ACCO_ATTN_LEGACY");
+// head size 64 (forward and backward) or 128 (allow128: the kernels templated on it)
+bool tc_applicable(const void* a, const void* b, int hd, bool allow128 = false) {
+    return (hd == HD || (allow128 && hd == 128)) && !(reinterpret_cast<uintptr_t>(a) & 15) &&
+           !(reinterpret_cast<uintptr_t>(b) & 15) && !std::getenv("ACCO_ATTN_LEGACY");
 }
 
 }  // namespace
@@ -1826,30 +1893,43 @@ void attention_set_dynamic(bool on) { g_attn_dynamic.store(on ? 1 : 0, std::memo
 
 bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const float* lse, const __nv_bfloat16* dy,
                       __nv_bfloat16* dqkv, float* dsum, int B, int T, int H, int Hkv, int hd, cudaStream_t s) {
-    if (!tc_applicable(qkv, dy, hd) || !tc_applicable(y, dqkv, hd)) return false;
-    const int d = H * HD;
-    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    if (!tc_applicable(qkv, dy, hd, true) || !tc_applicable(y, dqkv, hd, true)) return false;
+    const int d = H * hd;
+    const int ldq = (H + 2 * Hkv) * hd;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     const int64_t rows = static_cast<int64_t>(B) * T;
     const int64_t nrow = rows * H;
-    launch_pdl(dsum_tc_kernel, static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
+    if (hd == 128)
+        launch_pdl(dsum_tc_kernel<128>, static_cast<int>((nrow * 16 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
+    else
+        launch_pdl(dsum_tc_kernel<64>, static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
     ACCO_CHECK_LAUNCH();
     CUtensorMap mq = rows_map(qkv, ldq, rows, ldq);
     CUtensorMap mo = rows_map(dy, d, rows, d);
     static bool cfg = false;
     if (!cfg) {
-        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dkv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, DKV_SMEM));
-        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dq_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, DQ_SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dkv_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv<64>::SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dkv_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv<128>::SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dq_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq<64>::SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dq_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq<128>::SMEM));
         cfg = true;
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nt = (T + BW_T - 1) / BW_T;
     const Schedule skv = lpt_schedule(1, nt, B * Hkv, H / Hkv);
-    launch_pdl(fa_bwd_dkv_tc, skv.grid, BW_THREADS, DKV_SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
-               skv.table, skv.k_max, item_queue(skv, s));
+    if (hd == 128)
+        launch_pdl(fa_bwd_dkv_tc<128>, skv.grid, BW_THREADS, Dkv<128>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv,
+                   scale, skv.table, skv.k_max, item_queue(skv, s));
+    else
+        launch_pdl(fa_bwd_dkv_tc<64>, skv.grid, BW_THREADS, Dkv<64>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv,
+                   scale, skv.table, skv.k_max, item_queue(skv, s));
     ACCO_CHECK_LAUNCH();
     const Schedule sq = lpt_schedule(2, nt, B * H, 1);
-    launch_pdl(fa_bwd_dq_tc, sq.grid, BW_THREADS, DQ_SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale, sq.table,
-               sq.k_max, item_queue(sq, s));
+    if (hd == 128)
+        launch_pdl(fa_bwd_dq_tc<128>, sq.grid, BW_THREADS, Dq<128>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
+                   sq.table, sq.k_max, item_queue(sq, s));
+    else
+        launch_pdl(fa_bwd_dq_tc<64>, sq.grid, BW_THREADS, Dq<64>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
+                   sq.table, sq.k_max, item_queue(sq, s));
     ACCO_CHECK_LAUNCH();
     return true;
 }
@@ -1858,24 +1938,28 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
 // returns false if the tensor-core path does not apply (head size, alignment).
 bool attention_fwd_tc(const __nv_bfloat16* qkv, __nv_bfloat16* y, float* lse, int B, int T, int H, int Hkv, int hd,
                       cudaStream_t s) {
-    if (!tc_applicable(qkv, y, hd)) return false;
-    const int d = H * HD;
-    const int ldq = (H + 2 * Hkv) * HD;  // qkv row: H q heads | Hkv k heads | Hkv v heads
+    if (!tc_applicable(qkv, y, hd, true)) return false;
+    const int ldq = (H + 2 * Hkv) * hd;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     CUtensorMap m = rows_map(qkv, ldq, static_cast<int64_t>(B) * T, ldq);
     static bool cfg = false;
     if (!cfg) {
         ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-        ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, F2_SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2<64>::SMEM));
+        ACCO_CUDA(cudaFuncSetAttribute(fa_fwd_tc2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd2<128>::SMEM));
         cfg = true;
     }
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nqt = (T + BQ - 1) / BQ;
-    if (std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
+    if (hd == 64 && std::getenv("ACCO_ATTN_FWD_V1")) {  // single-tile kernel (A/B reference)
         launch_pdl(fa_fwd_tc, dim3(nqt, B * H), kThreads, SMEM, s, m, y, lse, T, H, Hkv, scale);
     } else {
         const Schedule sf = lpt_schedule(0, nqt, B * H, 1);
-        launch_pdl(fa_fwd_tc2, sf.grid, F2_THREADS, F2_SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table, sf.k_max,
-                   item_queue(sf, s));
+        if (hd == 128)
+            launch_pdl(fa_fwd_tc2<128>, sf.grid, F2_THREADS, Fwd2<128>::SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table,
+                       sf.k_max, item_queue(sf, s));
+        else
+            launch_pdl(fa_fwd_tc2<64>, sf.grid, F2_THREADS, Fwd2<64>::SMEM, s, m, y, lse, B, T, H, Hkv, scale, sf.table,
+                       sf.k_max, item_queue(sf, s));
     }
     ACCO_CHECK_LAUNCH();
     return true;

@@ -1,6 +1,7 @@
 // Standalone driver of the tcgen05 flash-attention kernels (attn_tc.cu) at the
 // GPT-2-small shape (B = 8, T = 1024, H = 12, hd = 64): event-timed forward
-// and backward, for A/B runs and ncu captures. Diagnostic only.
+// and backward, for A/B runs and ncu captures (args: B T H Hkv reps hd).
+// Diagnostic only.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo \
 //        -Ipaper_2406_02613_b200/csrc -Iinclude tools/diag/attn_bench.cu -lcuda -o tools/diag/attn_bench.bin
 #include "../../paper_2406_02613_b200/csrc/attn_tc.cu"
@@ -16,7 +17,8 @@ int num_sms() { return 148; }
 
 int main(int argc, char** argv) {
     const int B = argc > 1 ? atoi(argv[1]) : 8, T = argc > 2 ? atoi(argv[2]) : 1024, H = argc > 3 ? atoi(argv[3]) : 12;
-    const int Hkv = argc > 4 ? atoi(argv[4]) : H, reps = argc > 5 ? atoi(argv[5]) : 20, hd = 64;
+    const int Hkv = argc > 4 ? atoi(argv[4]) : H, reps = argc > 5 ? atoi(argv[5]) : 20,
+              hd = argc > 6 ? atoi(argv[6]) : 64;
     const size_t n_qkv = size_t(B) * T * (H + 2 * Hkv) * hd, n_y = size_t(B) * T * H * hd;
     std::vector<__nv_bfloat16> h(n_qkv), hy(n_y);
     uint32_t st = 12345;
@@ -66,9 +68,9 @@ int main(int argc, char** argv) {
     tb /= reps;
     // causal FLOPs: fwd 2 matmuls, bwd 5, each 2 * T^2/2 * hd per (b, h)
     const double f1 = 2.0 * B * H * (double(T) * T / 2) * hd * 2;
-    printf("{\"B\": %d, \"T\": %d, \"H\": %d, \"Hkv\": %d, \"fwd_us\": %.1f, \"bwd_us\": %.1f, \"fwd_tflops\": %.0f, "
+    printf("{\"hd\": %d, \"B\": %d, \"T\": %d, \"H\": %d, \"Hkv\": %d, \"fwd_us\": %.1f, \"bwd_us\": %.1f, \"fwd_tflops\": %.0f, "
            "\"bwd_tflops\": %.0f, \"err\": \"%s\"}\n",
-           B, T, H, Hkv, tf * 1e3, tb * 1e3, f1 / (tf * 1e-3) / 1e12, 2.5 * f1 / (tb * 1e-3) / 1e12,
+           hd, B, T, H, Hkv, tf * 1e3, tb * 1e3, f1 / (tf * 1e-3) / 1e12, 2.5 * f1 / (tb * 1e-3) / 1e12,
            cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
