@@ -42,6 +42,7 @@
 #include <map>
 #include <set>
 #include <string>
+#include <type_traits>
 #include <mutex>
 
 namespace acco {
@@ -737,6 +738,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
             // columns, each the row sum of A) against the ones tile
             const bool bias_unit = kBiasMma && ep.bias_grad != nullptr && nb == 0;
             const uint32_t tmem_b = tmem_base + kBiasCol + acc * 16;
+            // two instantiations of the k-loop: tiles without the bias gradient
+            // carry no (predicated-off) ones-MMAs, which cost the 128/192-wide
+            // single-CTA tiles up to 25 % of their mainloop rate
+            auto kloop = [&](auto with_bias) {
+            constexpr bool kB = decltype(with_bias)::value;
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % STAGES;
                 const uint32_t ph = (it / STAGES) & 1;
@@ -772,7 +778,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                         for (int kk = 0; kk < kBK / 16; ++kk)
                             umma_bf16_pair(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc,
                                            (kb > kb0 || kk > 0) ? 1u : 0u);
-                        if (kBiasMma && bias_unit) {
+                        if constexpr (kB) {
 #pragma unroll
                             for (int kk = 0; kk < kBK / 16; ++kk)
                                 umma_bf16_pair(tmem_b, ad + kk * a_step, ones_d, idesc_b, (kb > kb0 || kk > 0) ? 1u : 0u);
@@ -783,7 +789,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk)
                         umma_bf16(tmem_d, ad + kk * a_step, bd + kk * b_step, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-                    if (kBiasMma && bias_unit) {  // bias gradient: row sums of A (x ones)
+                    if constexpr (kB) {  // bias gradient: row sums of A (x ones)
 #pragma unroll
                         for (int kk = 0; kk < kBK / 16; ++kk)
                             umma_bf16(tmem_b, ad + kk * a_step, ones_d, idesc_b, (kb > kb0 || kk > 0) ? 1u : 0u);
@@ -792,6 +798,11 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
                 }
                 __syncwarp();
             }
+            };
+            if (kBiasMma && bias_unit)
+                kloop(std::integral_constant<bool, kBiasMma>{});
+            else
+                kloop(std::false_type{});
             if (elect_one()) {
                 if (CG == 2)
                     umma_commit_pair(&tfull[acc]);
