@@ -47,17 +47,49 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock sampler during the timed region (B200_PROFILING.md clocks
+    line): NVML every ~2 ms from a thread, so a timed region of a few hundred
+    ms gets hundreds of samples under load (nvidia-smi -lms 200 caught mostly
+    the idle clock around a short region). nvidia-smi is the fallback."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+            0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
         self.p = None
+        self.nv = None
+        self.samples = []
 
     def __enter__(self):
+        try:
+            import threading
+
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.nv = (pynvml, h)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.stop = False
+
+            def run():
+                while not self.stop:
+                    try:
+                        self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                             pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                                             pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.th = threading.Thread(target=run, daemon=True)
+            self.th.start()
+            return self
+        except Exception:
+            self.nv = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -68,6 +100,10 @@ class Clocks:
 
     def __exit__(self, *a):
         self.out = ""
+        if self.nv:
+            self.stop = True
+            self.th.join()
+            return
         if self.p:
             time.sleep(0.25)
             self.p.terminate()
@@ -77,6 +113,22 @@ class Clocks:
                 self.p.kill()
 
     def summary(self):
+        if self.nv:
+            if not self.samples:
+                return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "source": "nvml"}
+            clk = sorted(x[0] for x in self.samples)
+            pw = sorted(x[1] for x in self.samples)
+            reasons, capped = set(), 0
+            for _, _, r in self.samples:
+                for b, n in self.BITS.items():
+                    if r & b:
+                        reasons.add(n)
+                capped += bool(r & 0x4)
+            return {"sm_mhz": float(statistics.median(clk)), "sm_max_mhz": float(self.max_mhz),
+                    "reasons": sorted(reasons), "samples": len(clk), "source": "nvml, every ~2 ms",
+                    "sm_mhz_p10_p90": [clk[len(clk) // 10], clk[9 * len(clk) // 10]],
+                    "power_w_median": round(statistics.median(pw), 1),
+                    "sw_power_cap_fraction": round(capped / len(clk), 3)}
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (self.out or "").splitlines():
@@ -92,7 +144,7 @@ class Clocks:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "reasons": sorted(reasons), "samples": len(sms), "source": "nvidia-smi -lms 200"}
 
 
 def dist_setup(n_gpus):

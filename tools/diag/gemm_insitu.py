@@ -53,6 +53,6 @@ tag = os.environ.get("TAG", "")
 out = []
 for i, (n, d) in enumerate(seqs[0]):
     ds = sorted(sq[i][1] for sq in seqs if i < len(sq) and sq[i][0] == n)
-    out.append({"i": i, "k": n.split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")[:60],
+    out.append({"i": i, "k": n.replace("void ", "").replace("acco::(anonymous namespace)::", "")[:40],
                 "us": round(ds[len(ds) // 2], 2)})
 print(json.dumps({"tag": tag, "kernels": out}))
