@@ -41,6 +41,25 @@ __global__ void gather_tokens_kernel(const int32_t* __restrict__ data, int seq, 
     }
 }
 
+// bf16 x 8 <-> fp32 (16 B vectors)
+__device__ __forceinline__ void unpack8b(const uint4& u, float* v) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        v[2 * k] = __uint_as_float(w[k] << 16);
+        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ uint4 pack8b(const float* v) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+        w[k] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 // ----------------------------------------------------------------- embedding
 template <class T>
 __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ wte,
@@ -55,6 +74,19 @@ __global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const T* __res
         return;
     }
     const T* p = wpe + static_cast<int64_t>(t) * d;
+    if constexpr (sizeof(T) == 2) {
+        if ((d & 7) == 0) {  // 16 B per thread (the same per-element rounding)
+            for (int c = threadIdx.x; c < d / 8; c += blockDim.x) {
+                float ev[8], pv[8], r[8];
+                unpack8b(reinterpret_cast<const uint4*>(e)[c], ev);
+                unpack8b(reinterpret_cast<const uint4*>(p)[c], pv);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = ev[k] + pv[k];
+                reinterpret_cast<uint4*>(o)[c] = pack8b(r);
+            }
+            return;
+        }
+    }
     for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = from_f<T>(to_f(e[c]) + to_f(p[c]));
 }
 
@@ -120,25 +152,7 @@ __global__ void ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
 }
 
 // bf16 LayerNorm with 16B vector loads, row held in registers: lane owns
-// chunks c = lane + 32*i (8 elements each), d = 256 * CH.
-__device__ __forceinline__ void unpack8b(const uint4& u, float* v) {
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        v[2 * k] = __uint_as_float(w[k] << 16);
-        v[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
-    }
-}
-__device__ __forceinline__ uint4 pack8b(const float* v) {
-    uint32_t w[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
-        w[k] = *reinterpret_cast<uint32_t*>(&h);
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
-}
-
+// chunks c = lane + 32*i (8 elements each), d = 256 * CH (unpack8b / pack8b above).
 template <int CH, bool RMS>
 __global__ void ln_fwd_vec(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ g,
                            const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, float* __restrict__ mean,
@@ -312,6 +326,40 @@ __global__ void __launch_bounds__(NT) ln_bwd_wide(const __nv_bfloat16* __restric
 // then sums every norm's G partials in block order into the gradient
 // accumulator: the parameter reductions no longer re-read dy and x on a side
 // stream (two launches and 2 x M x d x 2 bytes per norm before).
+// Bulk async copies (TMA, non-tensor) of whole rows into shared memory,
+// completing on a per-warp mbarrier
+__device__ __forceinline__ void lnb_mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))));
+}
+__device__ __forceinline__ void lnb_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void lnb_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+        "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+        : "memory");
+}
+__device__ __forceinline__ void lnb_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0,1,0,p;\n\t}"
+                     : "=r"(ok)
+                     : "r"(a), "r"(parity)
+                     : "memory");
+}
+
+// Rows are staged through shared memory by bulk async copies, two rows ahead
+// per warp (x, dy and the accumulated dx: 3 x 2 d bytes per row and stage), so
+// the HBM latency of the next rows overlaps this row's math: each warp used
+// to wait a full memory round trip per row. The values and their order of
+// use are unchanged (dx and the partials are bitwise the same).
+constexpr int kLnStages = 2;
 template <int CH, bool RMS>
 __global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __restrict__ dy,
                                                        const __nv_bfloat16* __restrict__ x,
@@ -319,10 +367,32 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __re
                                                        const float* __restrict__ mean, const float* __restrict__ rstd,
                                                        __nv_bfloat16* __restrict__ dx, int accumulate, int M,
                                                        float* __restrict__ part) {
-    ACCO_PDL_PROLOGUE();
     constexpr int d = 256 * CH;
-    extern __shared__ float red[];  // [8 warps][d]
+    constexpr uint32_t kRow = d * 2;  // bytes per bf16 row
+    // [8 warps][kLnStages][x | dy | dx rows]; reused as [8 warps][d] fp32 for the block reduction
+    extern __shared__ __align__(128) uint8_t lnsm[];
+    __shared__ uint64_t bars[8][kLnStages];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint8_t* stage0 = lnsm + w * kLnStages * 3 * kRow;
+    if (lane == 0) {
+        for (int q = 0; q < kLnStages; ++q) lnb_mbar_init(&bars[w][q]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    ACCO_PDL_PROLOGUE();
+    const int step = gridDim.x * 8;
+    const int row0 = blockIdx.x * 8 + w;
+    auto issue = [&](int row, int q) {  // lane 0: the row's x, dy (and dx) into stage q
+        const int64_t o = static_cast<int64_t>(row) * d;
+        uint8_t* st = stage0 + q * 3 * kRow;
+        lnb_expect(&bars[w][q], (accumulate ? 3 : 2) * kRow);
+        lnb_copy(st, x + o, kRow, &bars[w][q]);
+        lnb_copy(st + kRow, dy + o, kRow, &bars[w][q]);
+        if (accumulate) lnb_copy(st + 2 * kRow, dx + o, kRow, &bars[w][q]);
+    };
+    if (lane == 0)
+        for (int q = 0; q < kLnStages; ++q)
+            if (row0 + q * step < M) issue(row0 + q * step, q);
     // (registers: the per-lane parameter sums stay resident, the row's values
     // are unpacked per 8-column chunk in each of the two passes, so two blocks
     // of 8 warps fit an SM)
@@ -330,18 +400,31 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __re
 #pragma unroll
     for (int i = 0; i < CH * 8; ++i) ag[i] = ab[i] = 0.f;
     const uint4* gq = reinterpret_cast<const uint4*>(g);
-    for (int row = blockIdx.x * 8 + w; row < M; row += gridDim.x * 8) {
+    float mu = 0.f, rs = 0.f;
+    if (row0 < M) {
+        mu = mean[row0];
+        rs = rstd[row0];
+    }
+    int k = 0;
+    for (int row = row0; row < M; row += step, ++k) {
         const int64_t o = static_cast<int64_t>(row) * d;
-        const uint4* dyr = reinterpret_cast<const uint4*>(dy + o);
-        const uint4* xr = reinterpret_cast<const uint4*>(x + o);
         uint4* dxr = reinterpret_cast<uint4*>(dx + o);
-        const float mu = mean[row], rs = rstd[row];
+        const int q = k % kLnStages;
+        lnb_wait(&bars[w][q], (k / kLnStages) & 1);
+        const uint4* st = reinterpret_cast<const uint4*>(stage0 + q * 3 * kRow);
         uint4 xv[CH], dvv[CH], pv[CH];
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
-            xv[i] = xr[lane + 32 * i];
-            dvv[i] = dyr[lane + 32 * i];
-            if (accumulate) pv[i] = dxr[lane + 32 * i];
+            xv[i] = st[lane + 32 * i];
+            dvv[i] = st[d / 8 + lane + 32 * i];
+            if (accumulate) pv[i] = st[d / 4 + lane + 32 * i];
+        }
+        __syncwarp();  // every lane has the stage in registers: refill it
+        if (lane == 0 && row + kLnStages * step < M) issue(row + kLnStages * step, q);
+        const float cmu = mu, crs = rs;
+        if (row + step < M) {  // the next row's statistics, under this row's math
+            mu = mean[row + step];
+            rs = rstd[row + step];
         }
         float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -351,13 +434,13 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __re
             unpack8b(dvv[i], dv);
             unpack8b(gq[lane + 32 * i], gv);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                xh[k] = ln_xhat(xh[k], mu, rs);
-                const float dxh = __fmul_rn(dv[k], gv[k]);
+            for (int k2 = 0; k2 < 8; ++k2) {
+                xh[k2] = ln_xhat(xh[k2], cmu, crs);
+                const float dxh = __fmul_rn(dv[k2], gv[k2]);
                 s1 = __fadd_rn(s1, dxh);
-                s2 = __fadd_rn(s2, __fmul_rn(dxh, xh[k]));
-                ag[8 * i + k] += dv[k] * xh[k];
-                if (!RMS) ab[8 * i + k] += dv[k];
+                s2 = __fadd_rn(s2, __fmul_rn(dxh, xh[k2]));
+                ag[8 * i + k2] += dv[k2] * xh[k2];
+                if (!RMS) ab[8 * i + k2] += dv[k2];
             }
         }
         s1 = RMS ? 0.f : warp_sum(s1) / d;
@@ -370,20 +453,23 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __re
             unpack8b(gq[lane + 32 * i], gv);
             if (accumulate) unpack8b(pv[i], prev);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                r[k] = ln_dx(__fmul_rn(dv[k], gv[k]), ln_xhat(xh[k], mu, rs), s1, s2, rs);
-                if (accumulate) r[k] = __fadd_rn(r[k], prev[k]);
+            for (int k2 = 0; k2 < 8; ++k2) {
+                r[k2] = ln_dx(__fmul_rn(dv[k2], gv[k2]), ln_xhat(xh[k2], cmu, crs), s1, s2, crs);
+                if (accumulate) r[k2] = __fadd_rn(r[k2], prev[k2]);
             }
             dxr[lane + 32 * i] = pack8b(r);
         }
     }
-    // block partials: the 8 warps' column sums in warp order
+    // block partials: the 8 warps' column sums in warp order (the staging
+    // buffers are free: every copy issued was waited for)
+    __syncthreads();
+    float* red = reinterpret_cast<float*>(lnsm);
 #pragma unroll
     for (int q = 0; q < (RMS ? 1 : 2); ++q) {
 #pragma unroll
         for (int i = 0; i < CH; ++i)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) red[w * d + 8 * (lane + 32 * i) + k] = q ? ab[8 * i + k] : ag[8 * i + k];
+            for (int k2 = 0; k2 < 8; ++k2) red[w * d + 8 * (lane + 32 * i) + k2] = q ? ab[8 * i + k2] : ag[8 * i + k2];
         __syncthreads();
         for (int c = threadIdx.x; c < d; c += 256) {
             float t = 0.f;
@@ -397,27 +483,32 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_vec_p(const __nv_bfloat16* __re
 
 // Every norm of the micro-batch: grad[g_off + c] (+)= sum_b part[b][0][c] and
 // grad[b_off + c] (+)= sum_b part[b][1][c] (b_off < 0: RMSNorm), blocks summed
-// in four fixed interleaved sub-sums then in a fixed order — deterministic.
+// in kFoldSub fixed interleaved sub-sums (b = sub mod kFoldSub) then a fixed
+// pairwise tree — deterministic. 32 columns x 8 sub-sums per block: each
+// thread has ~G / 8 dependent-free loads in flight (it was 64 x 4, G / 4
+// loads per thread and a latency-bound 23 us per micro-batch).
+constexpr int kFoldCols = 32, kFoldSub = 8;
 __global__ void __launch_bounds__(256) ln_param_fold_kernel(const LnFold* __restrict__ table, const float* __restrict__ parts,
                                                             float* __restrict__ grad, int G, int acc) {
     ACCO_PDL_PROLOGUE();
-    __shared__ float sub_sum[4][64];
+    __shared__ float sub_sum[kFoldSub][kFoldCols];
     const LnFold e = table[blockIdx.y];
     const int nq = e.b_off >= 0 ? 2 : 1;
-    const int cc = threadIdx.x & 63, sub = threadIdx.x >> 6;
-    const int col = blockIdx.x * 64 + cc;
+    const int cc = threadIdx.x % kFoldCols, sub = threadIdx.x / kFoldCols;
+    const int col = blockIdx.x * kFoldCols + cc;
     const bool live = col < nq * e.d;
     const int q = live ? col / e.d : 0, c = live ? col % e.d : 0;
     float t = 0.f;
     if (live) {
         const float* p = parts + e.part_off + static_cast<int64_t>(q) * e.d + c;
-#pragma unroll 4
-        for (int b = sub; b < G; b += 4) t += __ldcs(p + static_cast<int64_t>(b) * 2 * e.d);
+#pragma unroll 8
+        for (int b = sub; b < G; b += kFoldSub) t += __ldcs(p + static_cast<int64_t>(b) * 2 * e.d);
     }
     sub_sum[sub][cc] = t;
     __syncthreads();
     if (sub == 0 && live) {
-        const float r = ((sub_sum[0][cc] + sub_sum[1][cc]) + sub_sum[2][cc]) + sub_sum[3][cc];
+        const float r = ((sub_sum[0][cc] + sub_sum[1][cc]) + (sub_sum[2][cc] + sub_sum[3][cc])) +
+                        ((sub_sum[4][cc] + sub_sum[5][cc]) + (sub_sum[6][cc] + sub_sum[7][cc]));
         float* o = grad + (q ? e.b_off : e.g_off) + c;
         *o = (acc ? *o : 0.f) + r;
     }
@@ -774,9 +865,10 @@ __global__ void __launch_bounds__(256) ce_vec_kernel(__nv_bfloat16* __restrict__
 
 __global__ void loss_reduce_kernel(const float* __restrict__ row_loss, int M, int seq, double* out) {
     ACCO_PDL_PROLOGUE();
-    __shared__ double red[256];
+    __shared__ double red[1024];
     double s = 0.0;
-    for (int i = threadIdx.x; i < M; i += blockDim.x) s += row_loss[i];
+#pragma unroll 8
+    for (int i = threadIdx.x; i < M; i += blockDim.x) s += row_loss[i];  // (loads independent of the adds)
     red[threadIdx.x] = s;
     __syncthreads();
     for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -1423,14 +1515,15 @@ void layernorm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean,
 #define ACCO_LNP(KERN, BLOCK, SMEM)                                                                    \
     do {                                                                                               \
         static bool cfg = false;                                                                       \
-        if (!cfg && (SMEM) > 48 * 1024) {                                                              \
+        if (!cfg && (SMEM) > 40 * 1024) { /* (+ the static barriers) */                               \
             ACCO_CUDA(cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (SMEM))); \
         }                                                                                              \
         cfg = true;                                                                                    \
         launch_pdl(KERN, G, BLOCK, SMEM, s, dy, x, g, mean, rstd, dx, acc, M, part);                   \
     } while (0)
         {
-            const int smem = 8 * d * 4;  // block reduction of the 8 warps' sums
+            // per warp kLnStages x (x | dy | dx) staged rows; the block reduction reuses it
+            const int smem = std::max(8 * kLnStages * 3 * d * 2, 8 * d * 4);
             switch ((d / 256) * 2 + (rms ? 1 : 0)) {
                 case 2: ACCO_LNP((ln_bwd_vec_p<1, false>), 256, smem); break;
                 case 3: ACCO_LNP((ln_bwd_vec_p<1, true>), 256, smem); break;
@@ -1449,7 +1542,7 @@ void layernorm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean,
 void ln_param_fold(const LnFold* table, int n, int d_max, const float* parts, float* grad, bool acc, cudaStream_t s) {
     if (n == 0) return;
     ProfScope prof(kProfReduce, 1.0 * n * ln_part_blocks() * 2 * d_max * 4, s);
-    launch_pdl(ln_param_fold_kernel, dim3(ceil_div(2 * d_max, 64), n), 256, 0, s, table, parts, grad, ln_part_blocks(),
+    launch_pdl(ln_param_fold_kernel, dim3(ceil_div(2 * d_max, kFoldCols), n), kFoldCols * kFoldSub, 0, s, table, parts, grad, ln_part_blocks(),
                acc ? 1 : 0);
     ACCO_CHECK_LAUNCH();
 }
@@ -1487,7 +1580,7 @@ void cross_entropy(T* logits, int64_t ld, const int32_t* target, int V, int M, i
 }
 
 void loss_reduce(const float* row_loss, int M, int seq, double* out, cudaStream_t s) {
-    launch_pdl(loss_reduce_kernel, 1, 256, 0, s, row_loss, M, seq, out);
+    launch_pdl(loss_reduce_kernel, 1, 1024, 0, s, row_loss, M, seq, out);
     ACCO_CHECK_LAUNCH();
 }
 
