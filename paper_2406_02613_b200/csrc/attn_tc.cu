@@ -616,7 +616,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     pdl_wait();
     // the item sequence of this CTA: the static LPT table, or the dynamic queue
     // (q_list filled by the producer warp, q_ready[k] completes when entry k is in)
+    // static tables are copied to q_list once (a global load per item start
+    // stalled every warp on a memory round trip before its first tile)
+    const bool st_smem = !iq.ctr && sk <= kItemQ;
+    if (st_smem) {
+        for (int k = threadIdx.x; k < sk; k += blockDim.x) q_list[k] = item_at(sched, sk, k);
+        __syncthreads();
+    }
     auto citem = [&](int k) -> int {
+        if (st_smem) return k < sk ? q_list[k] : -1;
         if (!iq.ctr) return item_at(sched, sk, k);
         if (k >= kItemQ) return -1;
         mbar_wait(&q_ready[k], 0);
@@ -1094,7 +1102,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     pdl_wait();
     // the item sequence of this CTA: the static LPT table, or the dynamic queue
     // (q_list filled by the producer warp, q_ready[k] completes when entry k is in)
+    // static tables are copied to q_list once (a global load per item start
+    // stalled every warp on a memory round trip before its first tile)
+    const bool st_smem = !iq.ctr && sk <= kItemQ;
+    if (st_smem) {
+        for (int k = threadIdx.x; k < sk; k += blockDim.x) q_list[k] = item_at(sched, sk, k);
+        __syncthreads();
+    }
     auto citem = [&](int k) -> int {
+        if (st_smem) return k < sk ? q_list[k] : -1;
         if (!iq.ctr) return item_at(sched, sk, k);
         if (k >= kItemQ) return -1;
         mbar_wait(&q_ready[k], 0);
@@ -1265,7 +1281,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const int q = (w.kt + i % w.nq) * BW_T + qq * 32 + lane;
             if (q >= T) return;
             const int64_t bh = static_cast<int64_t>(w.b) * H + w.hk * G + i / w.nq;
-            lv = __ldg(lse + bh * T + q) * kLog2e;
+            lv = __ldg(lse + bh * T + q);  // (scaled to log2 where published: no stall on the load here)
             dv = __ldg(dsum + bh * T + q);
         };
         float nl = 0.f, nd = 0.f;
@@ -1305,7 +1321,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int qi = i % w.nq;
                 const int q0 = (w.kt + qi) * BW_T;
                 __syncwarp();  // the previous tile's broadcasts are read
-                myLD[lane] = nl;
+                myLD[lane] = nl * kLog2e;
                 myLD[32 + lane] = nd;
                 __syncwarp();
                 if (warp == 4 && lane == 0) BWD_PROBE(2, g);
@@ -1327,20 +1343,27 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     // and their TMEM is released at once, so the MMA warp computes the
                     // next tile's S^T / dP^T under this tile's exp / dS math
                     uint32_t st[32], dp[32];
+#ifndef ACCO_DIAG_DKV_NO_TMEM
                     tmem_ld32(tS + lane_off + qq * 32, st);
                     tmem_ld32(tP + lane_off + qq * 32, dp);
                     tmem_wait_ld();
+#else  // diagnostic builds only (tools/diag/attn_bench.cu): what bounds the tile
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) st[c] = dp[c] = 0u;
+#endif
                     tc_before();
                     mbar_arrive(s_free);
                     float* p = reinterpret_cast<float*>(st);  // in place
                     // valid query columns c of this quarter: q0 + qq*32 + c in [key, T)
                     const int lo = key - (q0 + qq * 32), hi = T - (q0 + qq * 32);
+                    float* ds = reinterpret_cast<float*>(dp);  // dS^T = P^T (dP^T - D), in place
+#ifndef ACCO_DIAG_DKV_NO_MATH
                     if (edge)
                         exp_cols32<true>(st, L4, sl, 0, lo, hi, p);
                     else
                         exp_cols32<false>(st, L4, sl, 0, lo, hi, p);
-                    float* ds = reinterpret_cast<float*>(dp);  // dS^T = P^T (dP^T - D), in place
                     ds_pairs(p, dp, reinterpret_cast<const float*>(D4), 32, ds);
+#endif
                     uint32_t pk[16], dk[16];  // bf16 pairs: query 2c (low) and 2c+1 (high)
 #pragma unroll
                     for (int c = 0; c < 16; ++c) {
@@ -1362,9 +1385,11 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     // (D = 128: P^T / dS^T go over S^T / dP^T columns other warps read:
                     // every softmax thread has them in registers once s_free completes)
                     if (P_IN_S) mbar_wait(s_free, g & 1);
+#ifndef ACCO_DIAG_DKV_NO_TMEM
                     tmem_st16(tPT + lane_off + qq * 16, pk);
                     tmem_st16(tDST + lane_off + qq * 16, dk);
                     tmem_wait_st();
+#endif
                 }
                 tc_before();
                 mbar_arrive(p_full);
@@ -1478,7 +1503,15 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     pdl_wait();
     // the item sequence of this CTA: the static LPT table, or the dynamic queue
     // (q_list filled by the producer warp, q_ready[k] completes when entry k is in)
+    // static tables are copied to q_list once (a global load per item start
+    // stalled every warp on a memory round trip before its first tile)
+    const bool st_smem = !iq.ctr && sk <= kItemQ;
+    if (st_smem) {
+        for (int k = threadIdx.x; k < sk; k += blockDim.x) q_list[k] = item_at(sched, sk, k);
+        __syncthreads();
+    }
     auto citem = [&](int k) -> int {
+        if (st_smem) return k < sk ? q_list[k] : -1;
         if (!iq.ctr) return item_at(sched, sk, k);
         if (k >= kItemQ) return -1;
         mbar_wait(&q_ready[k], 0);
@@ -1634,7 +1667,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const int q = w.qt * BW_T + r;
             const int64_t bh = static_cast<int64_t>(w.b) * H + w.h;
             if (q < T) {
-                L = __ldg(lse + bh * T + q) * kLog2e;
+                L = __ldg(lse + bh * T + q);  // (scaled to log2 at the item start: no stall here)
                 Dq = __ldg(dsum + bh * T + q);
             }
         };
@@ -1644,7 +1677,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
             const Item w = item_of(u);
             const int q = w.qt * BW_T + r;
-            const float L = nL, Dq = nD;
+            const float L = nL * kLog2e, Dq = nD;
             fetch(citem(k + 1), nL, nD);
             for (int j = 0; j < w.nk; ++j) {
                 const int g = it + j;
