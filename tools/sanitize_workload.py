@@ -4,7 +4,8 @@ pair, ordered split-K, the fp32-workspace split, the 3xTF32 fp32 path) with
 all epilogues and the fused bias gradient, and one bf16
 micro-batch (forward + backward) of a GPT-2-shaped LM at head size 64, so the
 four tcgen05 attention kernels (fa_fwd_tc2, fa_bwd_dkv_tc, fa_bwd_dq_tc,
-dsum_tc_kernel), the LN / CE / embedding kernels and the fused AdamW run.
+dsum_tc_kernel; and at head size 128), the LN / CE / embedding kernels and the
+fused AdamW run.
 
   compute-sanitizer --tool memcheck python tools/sanitize_workload.py
 """
@@ -67,4 +68,9 @@ lm = api.LMConfig(vocab=128, d_model=256, n_layer=1, n_head=4, seq_len=256, n_sa
 opt = api.OptimizerConfig(kind="adamw", learning_rate=1e-3, adam_beta2=0.95)
 tr = api.run_protocol("acco", lm, opt, api.SimConfig(n_workers=1, batch_size=2, master_seed=1), 1)
 torch.cuda.synchronize()
-print("sanitize workload done", tr.records[0].loss, flush=True)
+# head size 128 on the tcgen05 attention kernels (fa_fwd_tc2<128>, fa_bwd_dq_tc<128>, fa_bwd_dkv_tc<128>)
+lm128 = api.LMConfig(vocab=128, d_model=256, n_layer=1, n_head=2, seq_len=256, n_samples=8, precision="bf16",
+                     max_batch=2)
+tr128 = api.run_protocol("acco", lm128, opt, api.SimConfig(n_workers=1, batch_size=2, master_seed=1), 1)
+torch.cuda.synchronize()
+print("sanitize workload done", tr.records[0].loss, tr128.records[0].loss, flush=True)
