@@ -1421,17 +1421,43 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
 // tile sequence), so CTA launch / TMEM alloc / pipeline fill are paid once.
 // head size D = 64 or 128: D = 128 keeps one item slot of Q / dO and a 2-deep
 // K/V ring (shared memory)
+// With fuse_d the kernel also loads the item's O tile and computes D =
+// rowsum(dO o O) for its 128 queries itself (written to dsum for the dK/dV
+// kernel, which then runs after it): the separate D pass over O and dO
+// (25 MB at GPT-2 small, ~6 us per layer) is gone.
 template <int D>
 struct Dq {
     static constexpr int TILE = BW_T * D * 2, ST = D == 64 ? 4 : 2, QS = D == 64 ? 2 : 1;
-    static constexpr int SMEM = 1024 + QS * 2 * TILE + ST * 2 * TILE + 256 + 64;
+    static constexpr int SMEM = 1024 + QS * 3 * TILE + ST * 2 * TILE + 256 + 64;
 };
+// D of query row r from K-major SW128 tiles of dO and O ([128 rows][128 B]
+// sub-tiles of 64 columns, 16 B unit u of row r at (u ^ (r & 7)) << 4):
+// columns in order, one fp32 FMA chain
+template <int D>
+__device__ __forceinline__ float row_dot_sw128(const uint8_t* a, const uint8_t* b, int r) {
+    float acc = 0.f;
+#pragma unroll
+    for (int sub = 0; sub < D / 64; ++sub)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int off = sub * (BW_T * 128) + r * 128 + ((u ^ (r & 7)) << 4);
+            const uint4 x = *reinterpret_cast<const uint4*>(a + off), y = *reinterpret_cast<const uint4*>(b + off);
+            const uint32_t xw[4] = {x.x, x.y, x.z, x.w}, yw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                acc = fmaf(__uint_as_float(xw[k] << 16), __uint_as_float(yw[k] << 16), acc);
+                acc = fmaf(__uint_as_float(xw[k] & 0xffff0000u), __uint_as_float(yw[k] & 0xffff0000u), acc);
+            }
+        }
+    return acc;
+}
 
 template <int D>
 __global__ void __launch_bounds__(BW_THREADS, 1)
     fa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmDO,
-                 const float* __restrict__ lse, const float* __restrict__ dsum, __nv_bfloat16* __restrict__ dqkv,
-                 int B, int T, int H, int Hkv, float scale, const int* __restrict__ sched, int sk, ItemQueue iq) {
+                 const __grid_constant__ CUtensorMap tmY, const float* __restrict__ lse, float* __restrict__ dsum,
+                 __nv_bfloat16* __restrict__ dqkv, int B, int T, int H, int Hkv, float scale,
+                 const int* __restrict__ sched, int sk, ItemQueue iq, int fuse_d) {
     __shared__ uint64_t q_ready[kItemQ];
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
@@ -1439,7 +1465,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     constexpr int BW_TILE = Dq<D>::TILE, DQ_ST = Dq<D>::ST, QS = Dq<D>::QS;
     uint8_t* sQ = smem;                   // [QS items]
     uint8_t* sO = sQ + QS * BW_TILE;      // dO [QS items]
-    uint8_t* sK = sO + QS * BW_TILE;      // [DQ_ST stages]
+    uint8_t* sY = sO + QS * BW_TILE;      // O [QS items] (fuse_d)
+    uint8_t* sK = sY + QS * BW_TILE;      // [DQ_ST stages]
     uint8_t* sV = sK + DQ_ST * BW_TILE;   // [DQ_ST stages]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + DQ_ST * BW_TILE);
     uint64_t* q_full = bars;               // [QS] (2 reserved)
@@ -1450,7 +1477,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint64_t* s_free = s_full + 1;
     uint64_t* p_full = s_free + 1;
     uint64_t* g_done = p_full + 1;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 1);
+    uint64_t* d_free = g_done + 1;  // [2] (fuse_d) the softmax warps have read dO / O of the slot
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(d_free + 2);
 
     const int nt = (T + BW_T - 1) / BW_T;
     const int nbh = B * H;
@@ -1487,6 +1515,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         mbar_init(s_free, BW_SOFTMAX);
         mbar_init(p_full, BW_SOFTMAX);
         mbar_init(g_done, 1);
+        mbar_init(&d_free[0], BW_SOFTMAX);
+        mbar_init(&d_free[1], BW_SOFTMAX);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -1562,10 +1592,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int row_base = w.b * T;
                 const int qb = ni % QS;
                 mbar_wait(&q_empty[qb], ((ni / QS) & 1) ^ 1);  // item ni-QS is done with this Q/dO slot
+                if (fuse_d) mbar_wait(&d_free[qb], ((ni / QS) & 1) ^ 1);  // ... and its D is computed
                 if (elect_one()) {
-                    mbar_expect_tx(&q_full[qb], 2 * BW_TILE);
+                    mbar_expect_tx(&q_full[qb], (fuse_d ? 3 : 2) * BW_TILE);
                     tma_tile<D>(sQ + qb * BW_TILE, &tmQKV, &q_full[qb], w.h * D, row_base + w.qt * BW_T);
                     tma_tile<D>(sO + qb * BW_TILE, &tmDO, &q_full[qb], w.h * D, row_base + w.qt * BW_T);
+                    if (fuse_d) tma_tile<D>(sY + qb * BW_TILE, &tmY, &q_full[qb], w.h * D, row_base + w.qt * BW_T);
                 }
                 __syncwarp();
                 for (int j = 0; j < w.nk; ++j, ++it) {
@@ -1668,7 +1700,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             const int64_t bh = static_cast<int64_t>(w.b) * H + w.h;
             if (q < T) {
                 L = __ldg(lse + bh * T + q);  // (scaled to log2 at the item start: no stall here)
-                Dq = __ldg(dsum + bh * T + q);
+                if (!fuse_d) Dq = __ldg(dsum + bh * T + q);
             }
         };
         float nL, nD;
@@ -1677,7 +1709,16 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
             const Item w = item_of(u);
             const int q = w.qt * BW_T + r;
-            const float L = nL * kLog2e, Dq = nD;
+            float Dq = nD;
+            if (fuse_d) {  // D of this row from the item's dO and O tiles (every warp of the row alike)
+                const int qb = k % QS;
+                mbar_wait(&q_full[qb], (k / QS) & 1);
+                Dq = row_dot_sw128<D>(sO + qb * BW_TILE, sY + qb * BW_TILE, r);
+                mbar_arrive(&d_free[qb]);
+                if (qq == 0 && q < T) dsum[(static_cast<int64_t>(w.b) * H + w.h) * T + q] = Dq;
+                if (q >= T) Dq = 0.f;
+            }
+            const float L = nL * kLog2e;
             fetch(citem(k + 1), nL, nD);
             for (int j = 0; j < w.nk; ++j) {
                 const int g = it + j;
@@ -1931,13 +1972,20 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     const int ldq = (H + 2 * Hkv) * hd;  // qkv row: H q heads | Hkv k heads | Hkv v heads
     const int64_t rows = static_cast<int64_t>(B) * T;
     const int64_t nrow = rows * H;
-    if (hd == 128)
-        launch_pdl(dsum_tc_kernel<128>, static_cast<int>((nrow * 16 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
-    else
-        launch_pdl(dsum_tc_kernel<64>, static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
-    ACCO_CHECK_LAUNCH();
+    // D = rowsum(dO o O): inside the dQ kernel (which then runs first), or
+    // as its own pass (ACCO_ATTN_DSUM_PASS, A/B)
+    const bool fuse_d = std::getenv("ACCO_ATTN_DSUM_PASS") == nullptr;
+    if (!fuse_d) {
+        if (hd == 128)
+            launch_pdl(dsum_tc_kernel<128>, static_cast<int>((nrow * 16 + 255) / 256), 256, 0, s, y, dy, dsum, B, T,
+                       H);
+        else
+            launch_pdl(dsum_tc_kernel<64>, static_cast<int>((nrow * 8 + 255) / 256), 256, 0, s, y, dy, dsum, B, T, H);
+        ACCO_CHECK_LAUNCH();
+    }
     CUtensorMap mq = rows_map(qkv, ldq, rows, ldq);
     CUtensorMap mo = rows_map(dy, d, rows, d);
+    CUtensorMap my = rows_map(y, d, rows, d);
     static bool cfg = false;
     if (!cfg) {
         ACCO_CUDA(cudaFuncSetAttribute(fa_bwd_dkv_tc<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv<64>::SMEM));
@@ -1949,21 +1997,34 @@ bool attention_bwd_tc(const __nv_bfloat16* qkv, const __nv_bfloat16* y, const fl
     const float scale = 1.0f / sqrtf(static_cast<float>(hd));
     const int nt = (T + BW_T - 1) / BW_T;
     const Schedule skv = lpt_schedule(1, nt, B * Hkv, H / Hkv);
-    if (hd == 128)
-        launch_pdl(fa_bwd_dkv_tc<128>, skv.grid, BW_THREADS, Dkv<128>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv,
-                   scale, skv.table, skv.k_max, item_queue(skv, s));
-    else
-        launch_pdl(fa_bwd_dkv_tc<64>, skv.grid, BW_THREADS, Dkv<64>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv,
-                   scale, skv.table, skv.k_max, item_queue(skv, s));
-    ACCO_CHECK_LAUNCH();
+    auto dkv = [&] {
+        if (hd == 128)
+            launch_pdl(fa_bwd_dkv_tc<128>, skv.grid, BW_THREADS, Dkv<128>::SMEM, s, mq, mo, lse,
+                       static_cast<const float*>(dsum), dqkv, B, T, H, Hkv, scale, skv.table, skv.k_max,
+                       item_queue(skv, s));
+        else
+            launch_pdl(fa_bwd_dkv_tc<64>, skv.grid, BW_THREADS, Dkv<64>::SMEM, s, mq, mo, lse,
+                       static_cast<const float*>(dsum), dqkv, B, T, H, Hkv, scale, skv.table, skv.k_max,
+                       item_queue(skv, s));
+        ACCO_CHECK_LAUNCH();
+    };
     const Schedule sq = lpt_schedule(2, nt, B * H, 1);
-    if (hd == 128)
-        launch_pdl(fa_bwd_dq_tc<128>, sq.grid, BW_THREADS, Dq<128>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
-                   sq.table, sq.k_max, item_queue(sq, s));
-    else
-        launch_pdl(fa_bwd_dq_tc<64>, sq.grid, BW_THREADS, Dq<64>::SMEM, s, mq, mo, lse, dsum, dqkv, B, T, H, Hkv, scale,
-                   sq.table, sq.k_max, item_queue(sq, s));
-    ACCO_CHECK_LAUNCH();
+    auto dq = [&] {
+        if (hd == 128)
+            launch_pdl(fa_bwd_dq_tc<128>, sq.grid, BW_THREADS, Dq<128>::SMEM, s, mq, mo, my, lse, dsum, dqkv, B, T, H,
+                       Hkv, scale, sq.table, sq.k_max, item_queue(sq, s), fuse_d ? 1 : 0);
+        else
+            launch_pdl(fa_bwd_dq_tc<64>, sq.grid, BW_THREADS, Dq<64>::SMEM, s, mq, mo, my, lse, dsum, dqkv, B, T, H,
+                       Hkv, scale, sq.table, sq.k_max, item_queue(sq, s), fuse_d ? 1 : 0);
+        ACCO_CHECK_LAUNCH();
+    };
+    if (fuse_d) {  // dQ computes D, the dK/dV kernel reads it
+        dq();
+        dkv();
+    } else {
+        dkv();
+        dq();
+    }
     return true;
 }
 
