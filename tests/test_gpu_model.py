@@ -269,3 +269,22 @@ def test_attention_dynamic_queue_matches_static(cuda, arch, monkeypatch):
         g_d, l_d = _grad(m, th, seed, 3, cuda)
         assert l_d == l_s
         assert np.array_equal(g_d, g_s)
+
+
+@pytest.mark.parametrize("arch,hd", [("gpt2", 64), ("llama", 64), ("gpt2", 128)])
+def test_attention_d_in_dq_matches_separate_pass(cuda, arch, hd, monkeypatch):
+    """D = rowsum(dO o O) computed inside the dQ kernel (default) vs the
+    separate D pass (ACCO_ATTN_DSUM_PASS): the same values up to the fp32
+    summation order, so the gradients agree to fp32/bf16 rounding."""
+    c = dict(vocab=96, d_model=256, n_layer=2, n_head=256 // hd, seq_len=384, n_samples=8, data_seed=4)
+    if arch == "llama":
+        c.update(arch="llama", n_kv_head=2, d_ff=512)
+    m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=3))
+    gc = G.GPTConfig(**c)
+    th = torch.tensor(G.default_theta0(gc, 2)).to(torch.bfloat16).to(cuda)
+    seed = O.derive(4, 0, 0, 3, 0)
+    g_f, l_f = _grad(m, th, seed, 3, cuda)
+    monkeypatch.setenv("ACCO_ATTN_DSUM_PASS", "1")
+    g_p, l_p = _grad(m, th, seed, 3, cuda)
+    assert abs(l_f - l_p) <= 1e-6 * abs(l_p)
+    assert _rel(g_f, g_p) <= 1e-3
