@@ -522,8 +522,7 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     // (hi*hi) and a correction (lo*hi + hi*lo) accumulator per buffer
     constexpr int kAccCols = X3 ? 2 * BN : BN;
     // power of two >= 2 accumulators (+ 2 x 16 bias-gradient columns)
-    // (the bias columns only when this launch computes a bias gradient: a
-    // 512-column allocation slowed the 128-wide tiles)
+    // (the bias columns only when this launch computes a bias gradient)
     const uint32_t kTmemCols = 2 * kAccCols + (kBiasMma && ep.bias_grad ? 32 : 0) <= 256 ? 256 : 512;
     constexpr uint32_t kBiasCol = 2 * kAccCols;  // bias-gradient accumulators [2][16]
     if (warp == 2) {
