@@ -560,7 +560,13 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     uint64_t* s_full = kv_empty + F2_STAGES;     // [2 tiles]
     uint64_t* p_full = s_full + 2;               // [2 tiles]
     uint64_t* o_done = p_full + 2;               // [2 tiles]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(o_done + 2);
+    uint64_t* s_free = o_done + 2;               // [2 tiles] (SEPP) S in the softmax warps' registers
+    uint64_t* pv_done = s_free + 2;              // [2 tiles] (SEPP) PV done: P and O free
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(pv_done + 2);
+    // SEPP (D = 64): P in its own TMEM columns [384 + 64 x, +64) instead of over
+    // S, so S(j + 1) is issued as soon as the softmax warps hold S(j) in
+    // registers instead of after PV(j) (D = 128: O takes those columns)
+    constexpr bool SEPP = D == 64;
 
     const int nqt = (T + BQ - 1) / BQ;
     const int npair = (nqt + 1) / 2;
@@ -599,6 +605,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             mbar_init(&s_full[x], 1);
             mbar_init(&p_full[x], 256);
             mbar_init(&o_done[x], 1);
+            mbar_init(&s_free[x], 256);
+            mbar_init(&pv_done[x], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -709,6 +717,10 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             const uint32_t q_item = smem_u32(sQ + qs * 2 * Q_BYTES);
             auto issue_s = [&](int x, int j) {
                 const int s = (kvit + j) % F2_STAGES;
+                if (SEPP && cnt[x] + j > 0) {  // the softmax warps hold the slot's previous S
+                    mbar_wait(&s_free[x], (cnt[x] + j - 1) & 1);
+                    tc_after();
+                }
                 if (x == 0 || !nt[0] || j >= nt[0]) {  // first user of K_j waits for it
                     mbar_wait(&kv_full[s], ((kvit + j) / F2_STAGES) & 1);
                     tc_after();
@@ -734,11 +746,12 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 // V MN-major: 16-key slices are two 8-row atoms (2048 B) apart
                 // (N = D: 64-wide MN atoms, one 16 KB sub-tile apart)
                 const uint64_t vd = sdesc(smem_u32(sV + s * KV_BYTES), D == 64 ? 64 * 128 : 16384, 1024);
+                const uint32_t tp = SEPP ? tmem + 384 + x * 64 : tmem + x * 128;
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk)
-                        umma_ts(tmem + 256 + x * D, tmem + x * 128 + kk * 8, vd + 128 * kk, id_o,
-                                (j > 0 || kk > 0) ? 1u : 0u);
+                        umma_ts(tmem + 256 + x * D, tp + kk * 8, vd + 128 * kk, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    if (SEPP) umma_commit(&pv_done[x]);
                 }
                 __syncwarp();
             };
@@ -747,10 +760,11 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
             for (int j = 0; j < w.nkv; ++j) {
                 for (int x = 0; x < 2; ++x) {
                     if (j >= nt[x]) continue;
+                    if (SEPP && j + 1 < nt[x]) issue_s(x, j + 1);  // under this tile's softmax
                     issue_pv(x, j);
-                    if (j + 1 < nt[x]) {
+                    if (!SEPP && j + 1 < nt[x]) {
                         issue_s(x, j + 1);
-                    } else {
+                    } else if (j + 1 >= nt[x]) {
                         if (elect_one()) umma_commit(&o_done[x]);
                         __syncwarp();
                     }
@@ -800,6 +814,10 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 tmem_ld32(tS + half * 64, sv);
                 tmem_ld32(tS + half * 64 + 32, sv + 32);
                 tmem_wait_ld();
+                if (SEPP) {  // S(j + 1) may land now
+                    tc_before();
+                    mbar_arrive(&s_free[x]);
+                }
                 if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(6, cnt + j);
                 float mx = diag ? row_max64<true>(sv, half * 64, lim, -INFINITY)
                                 : row_max64<false>(sv, half * 64, lim, -INFINITY);
@@ -809,7 +827,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                 if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(7, cnt + j);
                 mx = fmaxf(mx, rb[(1 - half) * 128 + r]) * sl;
                 // lazy rescale: move the reference max only when it grows by > 2^8;
-                // O is stable here (s_full(j) is committed after PV(j-1))
+                // O is stable once PV(j-1) is done (!SEPP: s_full(j) is committed
+                // after it; SEPP: pv_done, waited below before O or P is touched)
                 bool need = false;
                 float alpha = 1.f;
                 if (j == 0) {
@@ -830,8 +849,13 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
                     else
                         exp_pack64<false>(sv, sl, m, half * 64, lim, l2, pk);
                     if (lane == 0 && wq == 0 && half == 0 && x == 0) FWD_PROBE(8, cnt + j);
-                    tmem_st16(tS + half * 32, pk);
-                    tmem_st16(tS + half * 32 + 16, pk + 16);
+                    if (SEPP && cnt + j > 0) {  // PV(j-1) has read P and updated O
+                        mbar_wait(&pv_done[x], (cnt + j - 1) & 1);
+                        tc_after();
+                    }
+                    const uint32_t tPk = SEPP ? tmem + 384 + x * 64 + lane_off : tS;
+                    tmem_st16(tPk + half * 32, pk);
+                    tmem_st16(tPk + half * 32 + 16, pk + 16);
                 }
                 // O *= alpha where the max moved (before this tile's PV, which waits p_full)
                 if (__any_sync(0xffffffffu, need)) {  // tcgen05.ld/st are warp-collective
