@@ -12,6 +12,7 @@ N="ncu --set full --clock-control none --import-source on"
 # fused bias gradient)
 timeout 900 $N -k regex:gemm_tc_kernel -s 44 -c 15 -o gpurun_out/r02_prof_gemm $P > gpurun_out/ncu_gemm.log 2>&1
 timeout 900 $N -k regex:"fa_bwd|fa_fwd" -s 24 -c 3 -o gpurun_out/r02_prof_attn $P > gpurun_out/ncu_attn.log 2>&1
+timeout 900 $N -k regex:"fa_fwd" -s 1 -c 2 -o gpurun_out/r02_prof_attnf $P > gpurun_out/ncu_attnf.log 2>&1
 timeout 900 $N -k regex:"opt_kernel" -c 2 -o gpurun_out/r02_prof_opt $P > gpurun_out/ncu_opt.log 2>&1
 timeout 900 $N -k regex:"ce_vec|ln_bwd_vec_p" -c 5 -o gpurun_out/r02_prof_ce_ln $P > gpurun_out/ncu_ce.log 2>&1
 timeout 900 $N -k regex:"ln_param_fold|ln_fwd_vec" -c 3 -o gpurun_out/r02_prof_misc $P > gpurun_out/ncu_misc.log 2>&1
