@@ -907,7 +907,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
 }
 
 // ---- backward softmax helpers (masking hoisted out of the unrolled loops)
-// p[c] = 2^(s_c * sl - lse2[c]) for 32 columns; MASK: columns outside
+// p[c] = 2^(s_c * sl - lse[c] * log2 e) for 32 columns; MASK: columns outside
 // [lo, hi) -> 0 (dK/dV: thread = key, columns = queries)
 template <bool MASK>
 __device__ __forceinline__ void exp_cols32(const uint32_t* st, const float4* L4, float sl, int base, int lo, int hi,
@@ -916,9 +916,9 @@ __device__ __forceinline__ void exp_cols32(const uint32_t* st, const float4* L4,
     for (int c4 = 0; c4 < 8; ++c4) {
         const float4 l4 = L4[c4];
         const float2 a = fma_f32x2(make_float2(__uint_as_float(st[4 * c4]), __uint_as_float(st[4 * c4 + 1])),
-                                   make_float2(sl, sl), make_float2(-l4.x, -l4.y));
+                                   make_float2(sl, sl), make_float2(-(l4.x * kLog2e), -(l4.y * kLog2e)));
         const float2 b = fma_f32x2(make_float2(__uint_as_float(st[4 * c4 + 2]), __uint_as_float(st[4 * c4 + 3])),
-                                   make_float2(sl, sl), make_float2(-l4.z, -l4.w));
+                                   make_float2(sl, sl), make_float2(-(l4.z * kLog2e), -(l4.w * kLog2e)));
         float v[4] = {ex2(a.x), ex2(a.y), ex2(b.x), ex2(b.y)};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -1032,7 +1032,7 @@ template <int D>
 struct Dkv {
     static constexpr int TILE = BW_T * D * 2, ST = D == 64 ? 4 : 2, KVS = D == 64 ? 2 : 1;
     static constexpr bool P_IN_S = D > 64;
-    static constexpr int SMEM = 1024 + KVS * 2 * TILE + ST * 2 * TILE + (BW_SOFTMAX / 32) * 64 * 4 + 256 + 64;
+    static constexpr int SMEM = 1024 + KVS * 2 * TILE + ST * 2 * TILE + (BW_SOFTMAX / 32) * 2 * 64 * 4 + 256 + 64;
 };
 
 // dK/dV, persistent: grid = #SMs; work item = (128-key tile kt, batch * KV
@@ -1063,9 +1063,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint8_t* sV = sK + KVS * BW_TILE;      // [KVS items]
     uint8_t* sQ = sV + KVS * BW_TILE;      // [DKV_ST stages]
     uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
-    // per softmax warp: its 32 query columns' lse (log2 domain) | D, for float4 broadcasts
-    float* sLD = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [16 warps][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + (BW_SOFTMAX / 32) * 64);
+    // per softmax warp, two tile slots: its 32 query columns' lse | D, for float4 broadcasts
+    float* sLD = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [16 warps][2][64]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + (BW_SOFTMAX / 32) * 2 * 64);
     uint64_t* kv_full = bars;                 // [KVS] (2 reserved)
     uint64_t* kv_empty = bars + 2;            // [KVS]: every S^T/dP^T MMA of the item issued and done
     uint64_t* q_full = bars + 4;              // [DKV_ST]
@@ -1294,22 +1294,32 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int r = wq * 32 + lane;  // key row = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
-        // lse (log2) and D of this warp's 32 query columns of the next tile,
-        // loaded one tile ahead into registers (lane = column) and published
-        // through the warp's own smem row: no barrier across the softmax warps
-        float* myLD = sLD + (warp - 4) * 64;
-        auto fetch = [&](int u, int i, float& lv, float& dv) {
-            lv = dv = 0.f;
-            if (u < 0 || u >= n_items) return;
-            const Item w = item_of(u);
-            const int q = (w.kt + i % w.nq) * BW_T + qq * 32 + lane;
-            if (q >= T) return;
-            const int64_t bh = static_cast<int64_t>(w.b) * H + w.hk * G + i / w.nq;
-            lv = __ldg(lse + bh * T + q);  // (scaled to log2 where published: no stall on the load here)
-            dv = __ldg(dsum + bh * T + q);
+        // lse and D of this warp's 32 query columns of the next tile, copied one
+        // tile ahead by cp.async (lane = column) into the warp's own smem slot:
+        // no register waits on the loads (a register load one tile ahead still
+        // left ~1 us of its latency exposed per tile) and no barrier across the
+        // softmax warps
+        float* myLD = sLD + (warp - 4) * 128;  // [2 slots][lse 32 | D 32]
+        auto fetch = [&](int u, int i, float* slot) {
+            const uint32_t dl = smem_u32(slot + lane), dd = smem_u32(slot + 32 + lane);
+            const float* pl = lse;
+            const float* pd = dsum;
+            uint32_t n = 0;  // bytes copied (0: zero fill)
+            if (u >= 0 && u < n_items) {
+                const Item w = item_of(u);
+                const int q = (w.kt + i % w.nq) * BW_T + qq * 32 + lane;
+                if (q < T) {
+                    const int64_t bh = static_cast<int64_t>(w.b) * H + w.hk * G + i / w.nq;
+                    pl = lse + bh * T + q;
+                    pd = dsum + bh * T + q;
+                    n = 4;
+                }
+            }
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dl), "l"(pl), "r"(n) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dd), "l"(pd), "r"(n) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
         };
-        float nl = 0.f, nd = 0.f;
-        fetch(citem(0), 0, nl, nd);
+        fetch(citem(0), 0, myLD);
         // dK/dV of item `prev` leave TMEM -> global: deferred into the next
         // item's first tile (after its exp/dS math, which overlaps the item's
         // last dV/dK MMAs), or after the loop for the CTA's last item
@@ -1344,24 +1354,24 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int g = it + i;
                 const int qi = i % w.nq;
                 const int q0 = (w.kt + qi) * BW_T;
-                __syncwarp();  // the previous tile's broadcasts are read
-                myLD[lane] = nl * kLog2e;
-                myLD[32 + lane] = nd;
+                // this tile's lse / D are in slot g & 1 (every lane's copy done, then
+                // visible to the warp); the other slot (read last tile) is refilled
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
                 __syncwarp();
+                float* cur = myLD + (g & 1) * 64;
                 if (warp == 4 && lane == 0) BWD_PROBE(2, g);
-                // the next tile's values: latency hidden behind this tile
                 if (i + 1 < niter)
-                    fetch(u, i + 1, nl, nd);
+                    fetch(u, i + 1, myLD + ((g + 1) & 1) * 64);
                 else
-                    fetch(citem(k + 1), 0, nl, nd);
+                    fetch(citem(k + 1), 0, myLD + ((g + 1) & 1) * 64);
                 mbar_wait(s_full, g & 1);
                 tc_after();
                 if (warp == 4 && lane == 0) BWD_PROBE(3, g);
                 // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
                 // rows past T belong to the next sequence)
                 const bool edge = qi == 0 || q0 + BW_T > T;
-                const float4* L4 = reinterpret_cast<const float4*>(myLD);
-                const float4* D4 = reinterpret_cast<const float4*>(myLD + 32);
+                const float4* L4 = reinterpret_cast<const float4*>(cur);  // lse (natural log: x kLog2e at use)
+                const float4* D4 = reinterpret_cast<const float4*>(cur + 32);
                 {
                     // S^T and dP^T (this warp's 32 columns each) go to registers first
                     // and their TMEM is released at once, so the MMA warp computes the
