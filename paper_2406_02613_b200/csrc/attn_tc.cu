@@ -1288,6 +1288,19 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             }
             it += niter;
         }
+#ifdef ACCO_BWD_PROBE
+    } else if (warp == 3) {  // observer (diagnostic builds only): when each tile's S^T/dP^T completes
+        int it = 0;
+        for (int k = 0, u = citem(0); u >= 0; u = citem(++k)) {
+            const Item w = item_of(u);
+            const int niter = G * w.nq;
+            for (int i = 0; i < niter; ++i) {
+                mbar_wait(s_full, (it + i) & 1);
+                if (lane == 0) BWD_PROBE(7, it + i);
+            }
+            it += niter;
+        }
+#endif
     } else if (warp >= 4) {
         // 16 warps: quadrant wq (key rows = TMEM lanes) x quarter qq (32 of 128 queries)
         const int wq = warp & 3, qq = (warp - 4) >> 2;

@@ -76,8 +76,21 @@ int main(int argc, char** argv) {
             ++n;
         }
     for (int k = 0; k < 7; ++k) printf("  %-28s %7.0f ns\n", nm[k], acc[k] / std::max(n, 1));
+    {  // observer (warp 3): S^T/dP^T completion vs issue and vs the softmax seeing it
+        double a = 0, b = 0;
+        int m = 0;
+        for (int c = 0; c < 148; ++c)
+            for (int g = 1; g < 63; ++g)
+                if (pr[c][7][g] && pr[c][0][g] && pr[c][3][g]) {
+                    a += double(pr[c][7][g]) - double(pr[c][0][g]);
+                    b += double(pr[c][3][g]) - double(pr[c][7][g]);
+                    ++m;
+                }
+        printf("  S issue -> S complete (observer) %7.0f ns; complete -> softmax sees it %7.0f ns (n=%d)\n",
+               a / std::max(m, 1), b / std::max(m, 1), m);
+    }
     printf("cta 0 (us): \n");
-    for (int k = 0; k < 7; ++k) {
+    for (int k = 0; k < 8; ++k) {
         printf(" k%d:", k);
         for (int i = 0; i < 12; ++i)
             if (pr[0][k][i]) printf(" %.2f", (pr[0][k][i] - t0) / 1000.0);
