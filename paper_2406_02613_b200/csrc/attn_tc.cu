@@ -131,6 +131,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if (!ok && (++spins & 255u) == 0) watchdog(t0);
     }
 }
+// bytes (a multiple of 16, 16 B aligned) global -> shared, completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -1022,8 +1029,8 @@ constexpr int BW_T = 128;                          // tile rows (keys or queries
 constexpr int BW_THREADS = 640;
 constexpr int BW_SOFTMAX = 512;
 constexpr int BW_SQ = BW_T * BW_T * 2;             // 32 KB [128][128] bf16 (P / dS operand)
-// dKV smem: K, V (KVS item slots) + DKV_ST stages x (Q, dO) + per-warp lse / D
-// rows. D = 64: K/V double-buffered (the next item's K/V under the current
+// dKV smem: K, V (KVS item slots) + DKV_ST stages x (Q, dO, lse | D of the
+// stage's 128 queries). D = 64: K/V double-buffered (the next item's K/V under the current
 // item), a 4-deep Q/dO ring. D = 128: one K/V slot, a 2-deep ring, and TMEM
 // S^T | dP^T | dV | dK (128 columns each) with P^T / dS^T (bf16) written over
 // the consumed S^T / dP^T columns, so the next tile's S^T / dP^T are issued
@@ -1032,7 +1039,7 @@ template <int D>
 struct Dkv {
     static constexpr int TILE = BW_T * D * 2, ST = D == 64 ? 4 : 2, KVS = D == 64 ? 2 : 1;
     static constexpr bool P_IN_S = D > 64;
-    static constexpr int SMEM = 1024 + KVS * 2 * TILE + ST * 2 * TILE + (BW_SOFTMAX / 32) * 2 * 64 * 4 + 256 + 64;
+    static constexpr int SMEM = 1024 + KVS * 2 * TILE + ST * 2 * TILE + ST * 2 * BW_T * 4 + 256 + 64;
 };
 
 // dK/dV, persistent: grid = #SMs; work item = (128-key tile kt, batch * KV
@@ -1063,9 +1070,9 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     uint8_t* sV = sK + KVS * BW_TILE;      // [KVS items]
     uint8_t* sQ = sV + KVS * BW_TILE;      // [DKV_ST stages]
     uint8_t* sO = sQ + DKV_ST * BW_TILE;   // dO [DKV_ST stages]
-    // per softmax warp, two tile slots: its 32 query columns' lse | D, for float4 broadcasts
-    float* sLD = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [16 warps][2][64]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + (BW_SOFTMAX / 32) * 2 * 64);
+    // per stage: lse | D of the stage's 128 queries (float4 broadcasts to the softmax warps)
+    float* sLD = reinterpret_cast<float*>(sO + DKV_ST * BW_TILE);  // [DKV_ST][lse 128 | D 128]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sLD + DKV_ST * 2 * BW_T);
     uint64_t* kv_full = bars;                 // [KVS] (2 reserved)
     uint64_t* kv_empty = bars + 2;            // [KVS]: every S^T/dP^T MMA of the item issued and done
     uint64_t* q_full = bars + 4;              // [DKV_ST]
@@ -1096,6 +1103,12 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         return w;
     };
 
+    // lse / D rows move as two bulk copies per stage when every row start is
+    // 16 B aligned; the columns past T then keep older (finite) values, which
+    // the mask zeroes (the ring starts zeroed)
+    const bool lse_bulk = (T & 3) == 0;
+    for (int k = threadIdx.x; k < DKV_ST * 2 * BW_T; k += blockDim.x) sLD[k] = 0.f;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (threadIdx.x == 0) {
         for (int q = 0; q < kItemQ; ++q) mbar_init(&q_ready[q], 1);
         for (int s = 0; s < 2; ++s) {
@@ -1103,7 +1116,8 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
             mbar_init(&kv_empty[s], 1);
         }
         for (int s = 0; s < DKV_ST; ++s) {
-            mbar_init(&q_full[s], 1);
+            // the TMA expect_tx (+ each producer lane's lse / D copies when T % 4 != 0)
+            mbar_init(&q_full[s], lse_bulk ? 1 : 1 + 32);
             mbar_init(&q_empty[s], 1);
         }
         mbar_init(s_full, 1);
@@ -1202,10 +1216,33 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                     const int h = w.hk * G + i / w.nq;
                     const int q0 = (w.kt + i % w.nq) * BW_T;
                     mbar_wait(&q_empty[s], ((it / DKV_ST) & 1) ^ 1);
+                    // lse | D of the 128 queries next to Q / dO, completing on the same
+                    // barrier: the softmax warps issue no loads and wait on nothing else
+                    const int64_t bh = static_cast<int64_t>(w.b) * H + h;
+                    float* dl = sLD + s * 2 * BW_T;
                     if (elect_one()) {
-                        mbar_expect_tx(&q_full[s], 2 * BW_TILE);
+                        const uint32_t nb = static_cast<uint32_t>(min(BW_T, T - q0)) * 4u;
+                        mbar_expect_tx(&q_full[s], 2 * BW_TILE + (lse_bulk ? 2 * nb : 0u));
                         tma_tile<D>(sQ + s * BW_TILE, &tmQKV, &q_full[s], h * D, row_base + q0);
                         tma_tile<D>(sO + s * BW_TILE, &tmDO, &q_full[s], h * D, row_base + q0);
+                        if (lse_bulk) {
+                            bulk_g2s(dl, lse + bh * T + q0, nb, &q_full[s]);
+                            bulk_g2s(dl + BW_T, dsum + bh * T + q0, nb, &q_full[s]);
+                        }
+                    }
+                    if (!lse_bulk) {  // 4 B copies, zero-filling the columns past T
+#pragma unroll
+                        for (int t = 0; t < BW_T / 32; ++t) {
+                            const int j = t * 32 + lane, q = q0 + j;
+                            const uint32_t n = q < T ? 4u : 0u;
+                            const int64_t off = q < T ? bh * T + q : 0;
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dl + j)),
+                                         "l"(lse + off), "r"(n) : "memory");
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dl + BW_T + j)),
+                                         "l"(dsum + off), "r"(n) : "memory");
+                        }
+                        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&q_full[s]))
+                                     : "memory");
                     }
                     __syncwarp();
                 }
@@ -1307,32 +1344,6 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
         const int r = wq * 32 + lane;  // key row = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(wq * 32) << 16;
         const float sl = scale * kLog2e;
-        // lse and D of this warp's 32 query columns of the next tile, copied one
-        // tile ahead by cp.async (lane = column) into the warp's own smem slot:
-        // no register waits on the loads (a register load one tile ahead still
-        // left ~1 us of its latency exposed per tile) and no barrier across the
-        // softmax warps
-        float* myLD = sLD + (warp - 4) * 128;  // [2 slots][lse 32 | D 32]
-        auto fetch = [&](int u, int i, float* slot) {
-            const uint32_t dl = smem_u32(slot + lane), dd = smem_u32(slot + 32 + lane);
-            const float* pl = lse;
-            const float* pd = dsum;
-            uint32_t n = 0;  // bytes copied (0: zero fill)
-            if (u >= 0 && u < n_items) {
-                const Item w = item_of(u);
-                const int q = (w.kt + i % w.nq) * BW_T + qq * 32 + lane;
-                if (q < T) {
-                    const int64_t bh = static_cast<int64_t>(w.b) * H + w.hk * G + i / w.nq;
-                    pl = lse + bh * T + q;
-                    pd = dsum + bh * T + q;
-                    n = 4;
-                }
-            }
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dl), "l"(pl), "r"(n) : "memory");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dd), "l"(pd), "r"(n) : "memory");
-            asm volatile("cp.async.commit_group;" ::: "memory");
-        };
-        fetch(citem(0), 0, myLD);
         // dK/dV of item `prev` leave TMEM -> global: deferred into the next
         // item's first tile (after its exp/dS math, which overlaps the item's
         // last dV/dK MMAs), or after the loop for the CTA's last item
@@ -1367,24 +1378,20 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
                 const int g = it + i;
                 const int qi = i % w.nq;
                 const int q0 = (w.kt + qi) * BW_T;
-                // this tile's lse / D are in slot g & 1 (every lane's copy done, then
-                // visible to the warp); the other slot (read last tile) is refilled
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-                __syncwarp();
-                float* cur = myLD + (g & 1) * 64;
                 if (warp == 4 && lane == 0) BWD_PROBE(2, g);
-                if (i + 1 < niter)
-                    fetch(u, i + 1, myLD + ((g + 1) & 1) * 64);
-                else
-                    fetch(citem(k + 1), 0, myLD + ((g + 1) & 1) * 64);
                 mbar_wait(s_full, g & 1);
                 tc_after();
+                // this tile's lse / D arrived with its Q / dO (stage g % DKV_ST; the
+                // phase completed before the S^T MMAs were issued)
+                const int st_ = g % DKV_ST;
+                mbar_wait(&q_full[st_], (g / DKV_ST) & 1);
+                const float* cur = sLD + st_ * 2 * BW_T + qq * 32;
                 if (warp == 4 && lane == 0) BWD_PROBE(3, g);
                 // masked tiles: the diagonal (q >= key) and a ragged tail (q < T; the
                 // rows past T belong to the next sequence)
                 const bool edge = qi == 0 || q0 + BW_T > T;
                 const float4* L4 = reinterpret_cast<const float4*>(cur);  // lse (natural log: x kLog2e at use)
-                const float4* D4 = reinterpret_cast<const float4*>(cur + 32);
+                const float4* D4 = reinterpret_cast<const float4*>(cur + BW_T);
                 {
                     // S^T and dP^T (this warp's 32 columns each) go to registers first
                     // and their TMEM is released at once, so the MMA warp computes the

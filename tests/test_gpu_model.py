@@ -115,7 +115,7 @@ def test_bf16_gradient_close_to_oracle(cuda, name):
     assert _rel(g, og * B) <= 3e-2
 
 
-@pytest.mark.parametrize("seq", [128, 100, 256])
+@pytest.mark.parametrize("seq", [128, 100, 256, 131, 141])
 def test_bf16_tensor_core_attention_per_tensor(cuda, seq):
     """head size 64 routes attention to the mma.sync flash kernels; check every
     weight tensor's gradient separately so an attention-backward error cannot
@@ -139,10 +139,13 @@ def test_bf16_tensor_core_attention_per_tensor(cuda, seq):
         assert _rel(g[off:off + n], og[off:off + n]) <= 5e-2, name
 
 
-@pytest.mark.parametrize("seq", [128, 200, 384, 1024])
+@pytest.mark.parametrize("seq", [128, 200, 384, 1024, 1023])
 def test_tcgen05_attention_matches_mma_path(cuda, seq, monkeypatch):
     """Same bf16 model gradient with the tcgen05 flash forward vs the mma.sync
-    one (ACCO_ATTN_LEGACY): both bf16, so agreement is at bf16 rounding."""
+    one (ACCO_ATTN_LEGACY): both bf16, so agreement is at bf16 rounding.
+    (T = 141: the legacy mma.sync backward disagrees by 8 % while the tcgen05
+    path matches the oracle there, test_bf16_tensor_core_attention_per_tensor;
+    the legacy comparator is not on the product path.)"""
     c = dict(vocab=128, d_model=128, n_layer=1, n_head=2, seq_len=seq, n_samples=8, data_seed=6)
     m = api.Model(api.LMConfig(**c, precision="bf16", max_batch=2))
     gc = G.GPTConfig(**c)
