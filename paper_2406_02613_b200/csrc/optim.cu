@@ -171,11 +171,24 @@ __global__ void __launch_bounds__(256) opt_kernel(KArgs a) {
 }
 
 template <int KIND, bool COMMIT, bool HAS_RET, class OutT>
+const void* vec_kernel_ptr() {
+    return reinterpret_cast<const void*>(opt_kernel<KIND, COMMIT, HAS_RET, OutT, true>);
+}
+
+template <int KIND, bool COMMIT, bool HAS_RET, class OutT>
 void launch_vec(const KArgs& a, bool vec, cudaStream_t s) {
     const int threads = 256;
-    // persistent-style grid: a few waves of 148 SMs x 8 resident blocks
+    // persistent grid: exactly the blocks that are resident at once (40-54
+    // registers: 4-6 blocks of 256 per SM, not 8 — a fixed 8 x 148 grid left a
+    // second, partly occupied wave behind the first one)
     const int64_t work = vec ? (a.n + 3) / 4 : a.n;
-    int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+    static const int per_sm = [] {
+        int nb = 0;
+        auto k = vec_kernel_ptr<KIND, COMMIT, HAS_RET, OutT>();
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, 0) != cudaSuccess || nb < 1) nb = 4;
+        return nb;
+    }();
+    int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
     if (const char* e = std::getenv("ACCO_OPT_BLOCKS")) cap = std::max<int64_t>(1, std::atoll(e));  // tuning knob
     int blocks = static_cast<int>(std::min<int64_t>((work + threads - 1) / threads, cap));
     if (blocks < 1) blocks = 1;
