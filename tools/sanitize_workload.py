@@ -73,4 +73,9 @@ lm128 = api.LMConfig(vocab=128, d_model=256, n_layer=1, n_head=2, seq_len=256, n
                      max_batch=2)
 tr128 = api.run_protocol("acco", lm128, opt, api.SimConfig(n_workers=1, batch_size=2, master_seed=1), 1)
 torch.cuda.synchronize()
-print("sanitize workload done", tr.records[0].loss, tr128.records[0].loss, flush=True)
+# ragged T (T % 4 != 0): dK/dV lse / D through per-lane cp.async on the stage barrier
+lm_r = api.LMConfig(vocab=128, d_model=256, n_layer=1, n_head=4, seq_len=141, n_samples=8, precision="bf16",
+                    max_batch=2)
+tr_r = api.run_protocol("acco", lm_r, opt, api.SimConfig(n_workers=1, batch_size=2, master_seed=1), 1)
+torch.cuda.synchronize()
+print("sanitize workload done", tr.records[0].loss, tr128.records[0].loss, tr_r.records[0].loss, flush=True)
