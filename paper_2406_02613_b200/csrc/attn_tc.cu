@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fa_fwd_tc(const __grid_constant__ CUtensorMap tmQKV, __nv_bfloat16* __restrict__ y, float* __restrict__ lse,
               int T, int H, int Hkv, float scale) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer (LDS/STS, not generic LD/ST)
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + Q_BYTES;                       // [stage] K tiles
     uint8_t* sV = sK + kStages * KV_BYTES;            // [stage] V tiles
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1)
     __shared__ uint64_t q_ready[kItemQ];
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer (LDS/STS, not generic LD/ST)
     constexpr int Q_BYTES = Fwd2<D>::QB, KV_BYTES = Fwd2<D>::KVB, F2_STAGES = Fwd2<D>::STAGES,
                   QSLOTS = Fwd2<D>::QSLOTS;
     uint8_t* sQ = smem;                         // [QSLOTS items][2 tiles]
@@ -1063,7 +1063,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     __shared__ uint64_t q_ready[kItemQ];
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer (LDS/STS, not generic LD/ST)
     constexpr int BW_TILE = Dkv<D>::TILE, DKV_ST = Dkv<D>::ST, KVS = Dkv<D>::KVS;
     constexpr bool P_IN_S = Dkv<D>::P_IN_S;
     uint8_t* sK = smem;                    // [KVS items]
@@ -1515,7 +1515,7 @@ __global__ void __launch_bounds__(BW_THREADS, 1)
     __shared__ uint64_t q_ready[kItemQ];
     __shared__ int q_list[kItemQ];
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, still a shared pointer (LDS/STS, not generic LD/ST)
     constexpr int BW_TILE = Dq<D>::TILE, DQ_ST = Dq<D>::ST, QS = Dq<D>::QS;
     uint8_t* sQ = smem;                   // [QS items]
     uint8_t* sO = sQ + QS * BW_TILE;      // dO [QS items]

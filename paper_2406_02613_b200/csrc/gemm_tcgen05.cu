@@ -464,8 +464,9 @@ __global__ void __launch_bounds__(gemm_threads<BN, STAGES, X3>(), 1)
     static_assert(!X3 || (!A_MN && !B_MN), "3xTF32: the split pre-pass writes K-major planes");
     static_assert(CG == 1 || (!X3 && (!B_MN || (BN / 2) % 64 == 0)), "CTA pairs: bf16, B half a whole MN atom");
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1 KB aligned by offsetting the shared array itself, so every pointer derived
+    // from it stays in the shared address space (LDS / STS, not generic LD / ST)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int A_TILE = kBM * 128;  // one plane: 128 rows x 128 B
     constexpr int B_TILE = (BN / CG) * 128;  // this CTA's B rows (half of them in a CTA pair)
     constexpr int A_BYTES = A_TILE * (X3 ? 2 : 1);  // per stage (hi | lo planes for X3)
