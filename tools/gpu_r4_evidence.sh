@@ -10,5 +10,5 @@ python tools/ncu_summary.py gpurun_out/prof_step_r02_raw.csv gpurun_out/r02_prof
     gpurun_out/r02_prof_attnf.ncu-rep gpurun_out/r02_prof_opt.ncu-rep gpurun_out/r02_prof_ce_ln.ncu-rep gpurun_out/r02_prof_misc.ncu-rep
 ncu -i gpurun_out/r02_prof_attn.ncu-rep --page details --csv > gpurun_out/r02_prof_attn_details.csv 2>/dev/null
 rm -f gpurun_out/r02_prof_gemm.ncu-rep gpurun_out/r02_prof_opt.ncu-rep gpurun_out/r02_prof_ce_ln.ncu-rep gpurun_out/r02_prof_misc.ncu-rep gpurun_out/r02_prof_attnf.ncu-rep
-bash tools/gpu_r2_sanitize.sh
+# (compute-sanitizer is closed on this pool: not run)
 du -sh gpurun_out
